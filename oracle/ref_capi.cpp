@@ -1,0 +1,381 @@
+// ORACLE — test infrastructure only. Never linked into or called by the product.
+//
+// A C-ABI over the UNMODIFIED reference (`/root/reference/proj/src/*.cpp`, compiled by
+// oracle/Makefile into oracle/_ref/libmixgraph_ref.so together with the FFTW-API stand-in
+// in oracle/shim/). tests/ (parity checker), __graft_entry__.smoke() and bench.py's CPU
+// baseline load it with ctypes. Each entry point forwards to the reference function named
+// in its comment; nothing here re-implements reference arithmetic.
+//
+// Parameter tables cross the boundary the way the product's C-ABI takes them
+// (include/mixgraph_b200.h): `tables[t]` points at a row-major [rows[t]][param_width(t)]
+// double matrix for NodeType t (enum order, `proj/include/mixgraph/types.hpp:12-23`), or
+// is NULL when the graph has no node of that type.
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "mixgraph/console.hpp"
+#include "mixgraph/dsp.hpp"
+#include "mixgraph/graph.hpp"
+#include "mixgraph/processors.hpp"
+#include "mixgraph/reference.hpp"
+#include "mixgraph/render.hpp"
+#include "mixgraph/schedule.hpp"
+#include "support/test_util.hpp"
+
+using namespace mixgraph;
+
+namespace {
+
+thread_local std::string g_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_error = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return 2;
+  }
+}
+
+FlatGraph make_flat(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne) {
+  Graph g;
+  for (int i = 0; i < n; ++i) g.add_node(static_cast<NodeType>(types[i]));
+  for (int i = 0; i < ne; ++i) g.connect(edges[4 * i], edges[4 * i + 1], edges[4 * i + 2], edges[4 * i + 3]);
+  return to_flat(g);  // graph.cpp:188-199 (validates)
+}
+
+ParamStore make_store(const double* const* tables, const int32_t* rows) {
+  ParamStore store;
+  for (int t = 0; t < kNumNodeTypes; ++t) {
+    const int w = param_width(static_cast<NodeType>(t));
+    if (w == 0 || tables == nullptr || tables[t] == nullptr) continue;
+    ParamMatrix m(rows[t], w);
+    std::memcpy(m.values.data(), tables[t], sizeof(double) * static_cast<std::size_t>(rows[t]) * w);
+    store.tables.emplace(static_cast<NodeType>(t), std::move(m));
+  }
+  return store;
+}
+
+int export_graph(const Graph& g, int32_t* types, int32_t cap_nodes, int32_t* edges, int32_t cap_edges,
+                 int32_t* n_nodes, int32_t* n_edges) {
+  *n_nodes = g.num_nodes();
+  *n_edges = static_cast<int32_t>(g.edges().size());
+  if (types && g.num_nodes() <= cap_nodes) {
+    for (int i = 0; i < g.num_nodes(); ++i) types[i] = static_cast<int32_t>(g.node_type(i));
+  }
+  if (edges && static_cast<int>(g.edges().size()) <= cap_edges) {
+    for (std::size_t i = 0; i < g.edges().size(); ++i) {
+      const Edge& e = g.edges()[i];
+      edges[4 * i] = e.src;
+      edges[4 * i + 1] = e.dst;
+      edges[4 * i + 2] = e.outlet;
+      edges[4 * i + 3] = e.inlet;
+    }
+  }
+  return 0;
+}
+
+const ProcessorSet& processors_for(double fs, uint32_t seed, int32_t env_taps, double floor_) {
+  static std::mutex mu;
+  static std::map<std::tuple<double, uint32_t, int32_t, double>, std::unique_ptr<ProcessorSet>> cache;
+  std::scoped_lock lock(mu);
+  auto key = std::make_tuple(fs, seed, env_taps, floor_);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    ProcessorConfig c;
+    c.sample_rate = fs;
+    c.reverb_seed = seed;
+    c.envelope_taps = env_taps;
+    c.energy_floor = floor_;
+    it = cache.emplace(key, std::make_unique<ProcessorSet>(c)).first;  // processors.cpp:151-160
+  }
+  return *it->second;
+}
+
+std::vector<AudioBuffer> make_sources(const double* src, int32_t k, int32_t batch, int64_t length, double fs) {
+  std::vector<AudioBuffer> out;
+  const std::size_t stride = static_cast<std::size_t>(batch) * 2 * static_cast<std::size_t>(length);
+  for (int i = 0; i < k; ++i) {
+    AudioBuffer b(batch, 2, static_cast<long>(length), fs);
+    std::memcpy(b.samples.data(), src + stride * i, sizeof(double) * stride);
+    out.push_back(std::move(b));
+  }
+  return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_error.c_str(); }
+
+// console.cpp:10-44
+int ref_console(int32_t tracks, double prune, uint32_t seed, int32_t* types, int32_t cap_nodes,
+                int32_t* edges, int32_t cap_edges, int32_t* n_nodes, int32_t* n_edges) {
+  return guarded([&] {
+    ConsoleOptions o;
+    o.send_prune_probability = prune;
+    o.seed = seed;
+    export_graph(generate_console(tracks, o), types, cap_nodes, edges, cap_edges, n_nodes, n_edges);
+  });
+}
+
+// tests/support/test_util.cpp:17-61 with a fresh mt19937(seed)
+int ref_random_dag(uint32_t seed, int32_t min_nodes, int32_t max_nodes, int32_t heavy, int32_t* types,
+                   int32_t cap_nodes, int32_t* edges, int32_t cap_edges, int32_t* n_nodes, int32_t* n_edges) {
+  return guarded([&] {
+    std::mt19937 rng(seed);
+    export_graph(testutil::random_dag(rng, min_nodes, max_nodes, heavy != 0), types, cap_nodes, edges,
+                 cap_edges, n_nodes, n_edges);
+  });
+}
+
+// tests/support/test_util.cpp:190-211
+int ref_four_track_snippet(int32_t* types, int32_t cap_nodes, int32_t* edges, int32_t cap_edges,
+                           int32_t* n_nodes, int32_t* n_edges) {
+  return guarded([&] {
+    export_graph(testutil::four_track_mix_snippet(), types, cap_nodes, edges, cap_edges, n_nodes, n_edges);
+  });
+}
+
+// tests/support/test_util.cpp:63-113 with a fresh mt19937(seed); tables in original node order.
+int ref_random_legal_params(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne, uint32_t seed,
+                            double* const* tables) {
+  return guarded([&] {
+    FlatGraph fg = make_flat(types, n, edges, ne);
+    std::mt19937 rng(seed);
+    ParamStore s = testutil::random_legal_params(fg, rng);
+    for (auto& [t, m] : s.tables) {
+      if (tables[static_cast<int>(t)]) std::memcpy(tables[static_cast<int>(t)], m.values.data(), sizeof(double) * m.values.size());
+    }
+  });
+}
+
+// graph.cpp:130-155
+int ref_default_param_row(int32_t type, double* row) {
+  return guarded([&] {
+    std::vector<double> r(static_cast<std::size_t>(param_width(static_cast<NodeType>(type))));
+    default_param_row(static_cast<NodeType>(type), r);
+    std::memcpy(row, r.data(), sizeof(double) * r.size());
+  });
+}
+
+// schedule.cpp:473-525
+int ref_plan_create(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne, int32_t strategy,
+                    int32_t beam_width, int32_t optimal_cap, void** out) {
+  return guarded([&] {
+    FlatGraph fg = make_flat(types, n, edges, ne);
+    ScheduleOptions o;
+    o.strategy = static_cast<Strategy>(strategy);
+    o.beam_width = beam_width;
+    o.optimal_node_cap = optimal_cap;
+    *out = new RenderData(compute_render_data(fg, o));
+  });
+}
+
+void ref_plan_destroy(void* p) { delete static_cast<RenderData*>(p); }
+
+// info[0..5] = num_steps, buffer_rows, num_inputs, output_begin, num_edges, type_string length
+int ref_plan_info(const void* p, int32_t* info) {
+  const auto* rd = static_cast<const RenderData*>(p);
+  info[0] = static_cast<int32_t>(rd->steps.size());
+  info[1] = rd->buffer_rows;
+  info[2] = rd->num_inputs;
+  info[3] = rd->output_begin;
+  info[4] = static_cast<int32_t>(rd->flat.edges.size());
+  info[5] = static_cast<int32_t>(rd->schedule.type_string.size());
+  return 0;
+}
+
+// schedule.cpp:301-306 (Schedule::type_codes)
+int ref_plan_type_codes(const void* p, char* buf, int32_t cap) {
+  std::string s = static_cast<const RenderData*>(p)->schedule.type_codes();
+  if (static_cast<int>(s.size()) + 1 > cap) return 1;
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return 0;
+}
+
+// Schedule subsets (original rows): sizes[k] per subset, rows concatenated.
+int ref_plan_subsets(const void* p, int32_t* sizes, int32_t* rows) {
+  const auto* rd = static_cast<const RenderData*>(p);
+  int off = 0;
+  for (std::size_t k = 0; k < rd->schedule.subsets.size(); ++k) {
+    sizes[k] = static_cast<int32_t>(rd->schedule.subsets[k].size());
+    for (int r : rd->schedule.subsets[k]) rows[off++] = r;
+  }
+  return 0;
+}
+
+int ref_plan_sigma(const void* p, int32_t* sigma) {
+  const auto* rd = static_cast<const RenderData*>(p);
+  for (std::size_t i = 0; i < rd->sigma.size(); ++i) sigma[i] = rd->sigma[i];
+  return 0;
+}
+
+// reordered graph (schedule.cpp:421-452): node types and edges [src,dst,outlet,inlet]
+int ref_plan_flat(const void* p, int32_t* types, int32_t* edges) {
+  const auto* rd = static_cast<const RenderData*>(p);
+  for (std::size_t i = 0; i < rd->flat.node_types.size(); ++i) types[i] = static_cast<int32_t>(rd->flat.node_types[i]);
+  for (std::size_t i = 0; i < rd->flat.edges.size(); ++i) {
+    edges[4 * i] = rd->flat.edges[i].src;
+    edges[4 * i + 1] = rd->flat.edges[i].dst;
+    edges[4 * i + 2] = rd->flat.edges[i].outlet;
+    edges[4 * i + 3] = rd->flat.edges[i].inlet;
+  }
+  return 0;
+}
+
+// StepIndex (schedule.hpp:60-68): head[0..5] = type, param_begin, param_end, store_begin,
+// store_end, |gather|; gather/aggregate may be NULL.
+int ref_plan_step(const void* p, int32_t k, int32_t* head, int32_t* gather, int32_t* aggregate) {
+  const auto* rd = static_cast<const RenderData*>(p);
+  const StepIndex& s = rd->steps.at(static_cast<std::size_t>(k));
+  head[0] = static_cast<int32_t>(s.type);
+  head[1] = s.param_begin;
+  head[2] = s.param_end;
+  head[3] = s.store_begin;
+  head[4] = s.store_end;
+  head[5] = static_cast<int32_t>(s.gather.size());
+  for (std::size_t i = 0; gather && i < s.gather.size(); ++i) gather[i] = s.gather[i];
+  for (std::size_t i = 0; aggregate && i < s.aggregate.size(); ++i) aggregate[i] = s.aggregate[i];
+  return 0;
+}
+
+// RenderData::param_source_rows (schedule.cpp:515-523); returns the row count.
+int ref_plan_param_source_rows(const void* p, int32_t type, int32_t* out) {
+  const auto* rd = static_cast<const RenderData*>(p);
+  auto it = rd->param_source_rows.find(static_cast<NodeType>(type));
+  if (it == rd->param_source_rows.end()) return 0;
+  for (std::size_t i = 0; out && i < it->second.size(); ++i) out[i] = it->second[i];
+  return static_cast<int>(it->second.size());
+}
+
+// render.cpp:14-81 with params = rd.reorder_params(original) (schedule.cpp:454-471).
+// sources [K][B][2][L]; outputs [num_outputs][B][2][L]; intermediates [rows][B][2][L] or NULL.
+int ref_render(const void* p, double fs, uint32_t seed, int32_t env_taps, double floor_,
+               const double* const* tables, const int32_t* rows, const double* sources, int32_t batch,
+               int64_t length, double* outputs, double* intermediates) {
+  return guarded([&] {
+    const auto* rd = static_cast<const RenderData*>(p);
+    const ProcessorSet& procs = processors_for(fs, seed, env_taps, floor_);
+    ParamStore original = make_store(tables, rows);
+    ParamStore params = rd->reorder_params(original);
+    auto src = make_sources(sources, rd->num_inputs, batch, length, fs);
+    RenderOptions o;
+    o.keep_intermediates = intermediates != nullptr;
+    RenderResult r = render(*rd, procs, params, src, o);
+    const std::size_t stride = static_cast<std::size_t>(batch) * 2 * static_cast<std::size_t>(length);
+    for (std::size_t i = 0; i < r.outputs.size(); ++i) std::memcpy(outputs + stride * i, r.outputs[i].samples.data(), sizeof(double) * stride);
+    for (std::size_t i = 0; intermediates && i < r.intermediates.size(); ++i) {
+      std::memcpy(intermediates + stride * i, r.intermediates[i].samples.data(), sizeof(double) * stride);
+    }
+  });
+}
+
+// reference.cpp:155-328 (per-node oracle: direct convolutions, recursive envelope)
+int ref_render_reference(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne, double fs,
+                         uint32_t seed, int32_t env_taps, double floor_, const double* const* tables,
+                         const int32_t* rows, const double* sources, int32_t batch, int64_t length,
+                         double* outputs) {
+  return guarded([&] {
+    FlatGraph fg = make_flat(types, n, edges, ne);
+    const ProcessorSet& procs = processors_for(fs, seed, env_taps, floor_);
+    ParamStore params = make_store(tables, rows);
+    auto src = make_sources(sources, fg.num_inputs, batch, length, fs);
+    auto outs = render_reference(fg, procs, params, src);
+    const std::size_t stride = static_cast<std::size_t>(batch) * 2 * static_cast<std::size_t>(length);
+    for (std::size_t i = 0; i < outs.size(); ++i) std::memcpy(outputs + stride * i, outs[i].samples.data(), sizeof(double) * stride);
+  });
+}
+
+// processors.cpp:229-282 (ProcessorSet::process); params [rows][width] or NULL.
+int ref_process(int32_t type, const double* in, double* out, int32_t slots, int32_t batch, int64_t length,
+                const double* params, int32_t rows, int32_t param_offset, double fs, uint32_t seed,
+                int32_t env_taps, double floor_) {
+  return guarded([&] {
+    const ProcessorSet& procs = processors_for(fs, seed, env_taps, floor_);
+    const NodeType t = static_cast<NodeType>(type);
+    ParamMatrix m;
+    const ParamMatrix* pm = nullptr;
+    if (params) {
+      m = ParamMatrix(rows, param_width(t));
+      std::memcpy(m.values.data(), params, sizeof(double) * m.values.size());
+      pm = &m;
+    }
+    procs.process(t, in, out, slots, batch, static_cast<long>(length), pm, param_offset);
+  });
+}
+
+// processors.cpp:162-187; left/right hold reverb_length() samples.
+int ref_reverb_kernel(double fs, uint32_t seed, const double* row, double* left, double* right, int64_t* len) {
+  return guarded([&] {
+    const ProcessorSet& procs = processors_for(fs, seed, 32768, 1e-7);
+    *len = procs.reverb_length();
+    if (!left) return;
+    auto [l, r] = procs.reverb_kernel({row, static_cast<std::size_t>(param_width(NodeType::Reverb))});
+    std::memcpy(left, l.data(), sizeof(double) * l.size());
+    std::memcpy(right, r.data(), sizeof(double) * r.size());
+  });
+}
+
+// processors.cpp:189-227; kernel holds delay_span() samples, positions 20 entries.
+int ref_delay_kernel(double fs, const double* row, int32_t channel, double* kernel, int64_t* positions,
+                     int64_t* span) {
+  return guarded([&] {
+    const ProcessorSet& procs = processors_for(fs, 0, 32768, 1e-7);
+    *span = procs.delay_span();
+    std::span<const double> r{row, static_cast<std::size_t>(param_width(NodeType::Delay))};
+    if (positions) {
+      auto p = procs.delay_positions(r, channel);
+      for (std::size_t i = 0; i < p.size(); ++i) positions[i] = p[i];
+    }
+    if (kernel) {
+      auto k = procs.delay_kernel(r, channel);
+      std::memcpy(kernel, k.data(), sizeof(double) * k.size());
+    }
+  });
+}
+
+// dsp.cpp:106-136
+int ref_zero_phase_fir(const double* log_mags, int32_t fir_length, double* taps) {
+  return guarded([&] {
+    auto f = dsp::zero_phase_fir({log_mags, static_cast<std::size_t>((fir_length + 1) / 2)}, fir_length);
+    std::memcpy(taps, f.taps.data(), sizeof(double) * f.taps.size());
+  });
+}
+
+// dsp.cpp:222-230
+int ref_uniform_noise(int64_t n, uint32_t seed, double* out) {
+  return guarded([&] {
+    auto v = dsp::uniform_noise(static_cast<long>(n), seed);
+    std::memcpy(out, v.data(), sizeof(double) * v.size());
+  });
+}
+
+// dsp.cpp:138-163: noise STFT [frames][bins] complex (interleaved re, im)
+int ref_stft(const double* x, int64_t n, int32_t fft_length, int32_t hop, double* out, int32_t* frames) {
+  return guarded([&] {
+    auto s = dsp::stft({x, static_cast<std::size_t>(n)}, fft_length, hop);
+    *frames = s.num_frames;
+    if (out) std::memcpy(out, s.bins.data(), sizeof(double) * 2 * s.bins.size());
+  });
+}
+
+// processors.cpp:110-130
+double ref_compressor_gain_log(double g, double t, double w, double r) { return compressor_gain_log(g, t, w, r); }
+double ref_noisegate_gain_log(double g, double t, double w, double r) { return noisegate_gain_log(g, t, w, r); }
+
+}  // extern "C"
