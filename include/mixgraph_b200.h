@@ -1,0 +1,134 @@
+/* mixgraph_b200 — C ABI of the B200-native batched audio-graph renderer.
+ *
+ * This is the drop-in boundary for the reference's render path. The reference exposes a
+ * C++ API (no FFI in the snapshot: its pybind11 module `mixgraph._core`,
+ * proj/CMakeLists.txt:47-74, is absent); every entry point below is what such a binding
+ * would call, and cites the reference interface it replaces. Conventions:
+ *  - every function returns MG_OK (0) or an error code; mg_last_error() gives the
+ *    message (thread-local). MG_EINVAL corresponds to the reference's
+ *    std::invalid_argument and carries the same message text (tests match substrings
+ *    such as "cycle", "channel", "homogeneity", "causality", "empty", "beam");
+ *  - node types are the reference enum values (proj/include/mixgraph/types.hpp:12-23):
+ *    0 in, 1 out, 2 mix, 3 gain, 4 eq, 5 compressor, 6 noisegate, 7 imager, 8 reverb, 9 delay;
+ *  - edges are int32 quadruples [src, dst, outlet, inlet] in insertion order;
+ *  - parameter tables are passed as `const double* const tables[10]` indexed by node type
+ *    (NULL for absent types) with `rows[10]`; each table is row-major
+ *    [rows][param_width(type)] (widths: gain 2, eq 1024, compressor/noisegate 4,
+ *    imager 1, reverb 768, delay 880, others 0);
+ *  - audio buffers are [batch][2][length] per signal, signals concatenated.
+ * No function falls back to the CPU: without a CUDA device the render/process calls
+ * return MG_ERUNTIME.
+ */
+#ifndef MIXGRAPH_B200_H
+#define MIXGRAPH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MG_OK 0
+#define MG_EINVAL 1
+#define MG_ERUNTIME 2
+
+#define MG_STRATEGY_ONE_BY_ONE 0
+#define MG_STRATEGY_GREEDY 1
+#define MG_STRATEGY_BEAM 2
+#define MG_STRATEGY_OPTIMAL 3
+
+typedef struct mg_plan mg_plan;             /* RenderData (+ its device step table) */
+typedef struct mg_processors mg_processors; /* ProcessorSet (device constants) */
+
+const char* mg_last_error(void);
+int32_t mg_abi_version(void);
+int32_t mg_param_width(int32_t node_type); /* types.cpp:14-25 */
+
+/* Graph::validate (graph.cpp:48-114) on an edge list; MG_EINVAL with "cycle"/"channel"/... */
+int32_t mg_graph_validate(const int32_t* node_types, int32_t num_nodes, const int32_t* edges, int32_t num_edges);
+
+/* to_flat (graph.cpp:188-199) + compute_render_data (schedule.cpp:473-525). */
+int32_t mg_plan_create(const int32_t* node_types, int32_t num_nodes, const int32_t* edges, int32_t num_edges,
+                       int32_t strategy, int32_t beam_width, int32_t optimal_node_cap, mg_plan** out);
+void mg_plan_destroy(mg_plan* plan);
+/* info[6] = num_steps, buffer_rows, num_inputs, output_begin, num_edges, type string length */
+int32_t mg_plan_info(const mg_plan* plan, int32_t* info);
+/* Schedule::type_codes (schedule.cpp:301-306), NUL-terminated */
+int32_t mg_plan_type_codes(const mg_plan* plan, char* buf, int32_t cap);
+/* Schedule::subsets (original rows): sizes[type string length], rows concatenated */
+int32_t mg_plan_subsets(const mg_plan* plan, int32_t* sizes, int32_t* rows);
+/* RenderData::sigma (old row -> new row) */
+int32_t mg_plan_sigma(const mg_plan* plan, int32_t* sigma);
+/* RenderData::flat (reorder_flat, schedule.cpp:421-452): node types and edges */
+int32_t mg_plan_flat(const mg_plan* plan, int32_t* node_types, int32_t* edges);
+/* StepIndex k (schedule.hpp:60-68): head[6] = type, param_begin, param_end, store_begin,
+ * store_end, |gather|; gather / aggregate may be NULL. */
+int32_t mg_plan_step(const mg_plan* plan, int32_t k, int32_t* head, int32_t* gather, int32_t* aggregate);
+/* RenderData::param_source_rows[type] (schedule.cpp:515-523); returns the count (>= 0) */
+int32_t mg_plan_param_source_rows(const mg_plan* plan, int32_t node_type, int32_t* out);
+/* RenderData::reorder_params (schedule.cpp:454-471): original-order tables -> render order */
+int32_t mg_plan_reorder_params(const mg_plan* plan, const double* const* original, const int32_t* rows,
+                               double* const* reordered);
+/* validate_schedule (schedule.cpp:351-395) */
+int32_t mg_validate_schedule(const int32_t* node_types, int32_t num_nodes, const int32_t* edges, int32_t num_edges,
+                             const int32_t* type_string, int32_t num_subsets, const int32_t* subset_sizes,
+                             const int32_t* subset_rows);
+
+/* ProcessorSet(ProcessorConfig) (processors.cpp:151-160) on CUDA device `device`. */
+int32_t mg_processors_create(double sample_rate, uint32_t reverb_seed, int32_t envelope_taps, double energy_floor,
+                             int32_t device, mg_processors** out);
+void mg_processors_destroy(mg_processors* procs);
+/* info[3] = delay_span, delay_window, reverb_length */
+int32_t mg_processors_info(const mg_processors* procs, int64_t* info);
+
+/* render(rd, procs, params, sources, {keep_intermediates}) (render.cpp:14-81): host double
+ * buffers; tables in render (reordered) row order; sources [K][B][2][L]; outputs
+ * [num_outputs][B][2][L]; intermediates [buffer_rows][B][2][L] in ORIGINAL row order or NULL. */
+int32_t mg_render(const mg_plan* plan, const mg_processors* procs, const double* const* tables, const int32_t* rows,
+                  const double* sources, int32_t num_sources, int32_t batch, int64_t length, double sample_rate,
+                  double* outputs, double* intermediates);
+
+/* Device-resident render (the hot path): d_tables are device fp64 tables in render order;
+ * d_arena holds buffer_rows x [B][2][L] fp32 with the sources in rows [0, num_inputs);
+ * outputs are rows [output_begin, buffer_rows). Asynchronous on `stream` (cudaStream_t). */
+int32_t mg_plan_workspace_bytes(const mg_plan* plan, const mg_processors* procs, int32_t batch, int64_t length,
+                                uint64_t* bytes);
+int32_t mg_plan_kernel_count(const mg_plan* plan, int32_t batch, int64_t length, int32_t* count);
+int32_t mg_render_arena(const mg_plan* plan, const mg_processors* procs, const double* const* d_tables, float* d_arena,
+                        int32_t batch, int64_t length, void* d_workspace, uint64_t workspace_bytes, void* stream);
+
+/* Same as mg_render_arena with a device event pair recorded around every step; when step_ms
+ * is non-NULL the call synchronises `stream` and writes each step's duration (ms). */
+int32_t mg_render_arena_profiled(const mg_plan* plan, const mg_processors* procs, const double* const* d_tables,
+                                 float* d_arena, int32_t batch, int64_t length, void* d_workspace,
+                                 uint64_t workspace_bytes, void* stream, float* step_ms);
+
+/* ProcessorSet::process (processors.cpp:229-282): in/out [slots][B][2][L] host double;
+ * params [param_rows][width] (NULL for in/out/mix). */
+int32_t mg_process(const mg_processors* procs, int32_t node_type, const double* in, double* out, int32_t slots,
+                   int32_t batch, int64_t length, const double* params, int32_t param_rows, int32_t param_offset);
+/* ProcessorSet::reverb_kernel (processors.cpp:162-187): left/right hold reverb_length samples */
+int32_t mg_reverb_kernel(const mg_processors* procs, const double* row, double* left, double* right);
+/* ProcessorSet::delay_kernel / delay_positions (processors.cpp:189-227) */
+int32_t mg_delay_kernel(const mg_processors* procs, const double* row, int32_t channel, double* kernel,
+                        int64_t* positions);
+/* compressor_gain_log / noisegate_gain_log (processors.cpp:110-130) */
+double mg_compressor_gain_log(double g_u, double threshold, double knee_half_width, double ratio);
+double mg_noisegate_gain_log(double g_u, double threshold, double knee_half_width, double ratio);
+/* check_param_row (processors.cpp:132-149) */
+int32_t mg_check_param_row(int32_t node_type, const double* row);
+
+/* Synthetic workload generators, bit-identical to the reference's: generate_console
+ * (console.cpp:10-44), random_legal_params (tests/support/test_util.cpp:63-113, fresh
+ * mt19937(seed), tables in original row order), dsp::uniform_noise (dsp.cpp:222-230). */
+int32_t mg_generate_console(int32_t tracks, double prune, uint32_t seed, int32_t* node_types, int32_t cap_nodes,
+                            int32_t* edges, int32_t cap_edges, int32_t* num_nodes, int32_t* num_edges);
+int32_t mg_random_legal_params(const int32_t* node_types, int32_t num_nodes, uint32_t seed, double* const* tables);
+int32_t mg_default_param_row(int32_t node_type, double* row);
+int32_t mg_uniform_noise(int64_t n, uint32_t seed, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MIXGRAPH_B200_H */

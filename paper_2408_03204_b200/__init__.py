@@ -1,0 +1,554 @@
+"""B200-native batched audio-graph renderer (GRAFX, arXiv 2408.03204) — Python host mirror.
+
+The product is ``libmgb200.so`` (host scheduler in C++ + sm_100a kernels behind the C ABI
+declared in ``include/mixgraph_b200.h``). This module binds that ABI with ctypes and mirrors
+the reference's C++ render API (``proj/include/mixgraph/{graph,schedule,processors,render}.hpp``)
+with the same names, argument meaning and error behaviour: the reference's
+``std::invalid_argument`` surfaces here as ``ValueError`` carrying the same message text.
+
+There is no CPU fallback: render/process calls go through CUDA kernels, and importing the
+module fails loudly if the shared library is missing.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmgb200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(make -C paper_2408_03204_b200/csrc). There is no CPU fallback.")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_u32 = ctypes.c_uint32
+_u64 = ctypes.c_uint64
+_dbl = ctypes.c_double
+_vp = ctypes.c_void_p
+_P = ctypes.POINTER
+
+
+def _sig(name, restype, *argtypes):
+    f = getattr(_lib, name)
+    f.restype = restype
+    f.argtypes = list(argtypes)
+    return f
+
+
+_sig("mg_last_error", ctypes.c_char_p)
+_sig("mg_abi_version", _i32)
+_sig("mg_param_width", _i32, _i32)
+_sig("mg_graph_validate", _i32, _vp, _i32, _vp, _i32)
+_sig("mg_plan_create", _i32, _vp, _i32, _vp, _i32, _i32, _i32, _i32, _P(_vp))
+_sig("mg_plan_destroy", None, _vp)
+_sig("mg_plan_info", _i32, _vp, _vp)
+_sig("mg_plan_type_codes", _i32, _vp, ctypes.c_char_p, _i32)
+_sig("mg_plan_subsets", _i32, _vp, _vp, _vp)
+_sig("mg_plan_sigma", _i32, _vp, _vp)
+_sig("mg_plan_flat", _i32, _vp, _vp, _vp)
+_sig("mg_plan_step", _i32, _vp, _i32, _vp, _vp, _vp)
+_sig("mg_plan_param_source_rows", _i32, _vp, _i32, _vp)
+_sig("mg_plan_reorder_params", _i32, _vp, _vp, _vp, _vp)
+_sig("mg_validate_schedule", _i32, _vp, _i32, _vp, _i32, _vp, _i32, _vp, _vp)
+_sig("mg_processors_create", _i32, _dbl, _u32, _i32, _dbl, _i32, _P(_vp))
+_sig("mg_processors_destroy", None, _vp)
+_sig("mg_processors_info", _i32, _vp, _vp)
+_sig("mg_render", _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i64, _dbl, _vp, _vp)
+_sig("mg_plan_workspace_bytes", _i32, _vp, _vp, _i32, _i64, _P(_u64))
+_sig("mg_plan_kernel_count", _i32, _vp, _i32, _i64, _P(_i32))
+_sig("mg_render_arena", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp)
+_sig("mg_render_arena_profiled", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp, _vp)
+_sig("mg_process", _i32, _vp, _i32, _vp, _vp, _i32, _i32, _i64, _vp, _i32, _i32)
+_sig("mg_reverb_kernel", _i32, _vp, _vp, _vp, _vp)
+_sig("mg_delay_kernel", _i32, _vp, _vp, _i32, _vp, _vp)
+_sig("mg_compressor_gain_log", _dbl, _dbl, _dbl, _dbl, _dbl)
+_sig("mg_noisegate_gain_log", _dbl, _dbl, _dbl, _dbl, _dbl)
+_sig("mg_check_param_row", _i32, _i32, _vp)
+_sig("mg_generate_console", _i32, _i32, _dbl, _u32, _vp, _i32, _vp, _i32, _P(_i32), _P(_i32))
+_sig("mg_random_legal_params", _i32, _vp, _i32, _u32, _vp)
+_sig("mg_default_param_row", _i32, _i32, _vp)
+_sig("mg_uniform_noise", _i32, _i64, _u32, _vp)
+
+
+def _check(status: int) -> None:
+    if status == 0:
+        return
+    msg = (_lib.mg_last_error() or b"").decode()
+    if status == 1:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(_vp)
+
+
+class NodeType(enum.IntEnum):
+    """`proj/include/mixgraph/types.hpp:12-23`."""
+    IN = 0
+    OUT = 1
+    MIX = 2
+    GAIN = 3
+    EQ = 4
+    COMPRESSOR = 5
+    NOISEGATE = 6
+    IMAGER = 7
+    REVERB = 8
+    DELAY = 9
+
+
+NUM_NODE_TYPES = 10
+_CODES = "iomgecnsrd"
+_NAMES = ["in", "out", "mix", "gain", "eq", "compressor", "noisegate", "imager", "reverb", "delay"]
+
+
+def type_code(t: int) -> str:
+    return _CODES[int(t)]
+
+
+def type_name(t: int) -> str:
+    return _NAMES[int(t)]
+
+
+def type_from_code(c: str) -> NodeType:
+    return NodeType(_CODES.index(c))
+
+
+def param_width(t: int) -> int:
+    return int(_lib.mg_param_width(int(t)))
+
+
+class Strategy(enum.IntEnum):
+    """`proj/include/mixgraph/schedule.hpp:12-17`."""
+    ONE_BY_ONE = 0
+    GREEDY = 1
+    BEAM = 2
+    OPTIMAL = 3
+
+
+# ---- graph -------------------------------------------------------------------------------
+
+class Graph:
+    """Builder (`graph.hpp:26-47`). Edges are (src, dst, outlet, inlet)."""
+
+    def __init__(self):
+        self._types: List[int] = []
+        self._edges: List[Tuple[int, int, int, int]] = []
+
+    def add_node(self, t: int) -> int:
+        self._types.append(int(t))
+        return len(self._types) - 1
+
+    def add_serial_chain(self, types: Sequence[int]) -> Tuple[int, int]:
+        if not types:
+            raise ValueError("add_serial_chain: empty type list")
+        first = self.add_node(types[0])
+        for t in types[1:]:
+            nid = self.add_node(t)
+            self.connect(nid - 1, nid)
+        return first, len(self._types) - 1
+
+    def connect(self, src: int, dst: int, outlet: int = 0, inlet: int = 0) -> None:
+        for nid in (src, dst):
+            if nid < 0 or nid >= len(self._types):
+                raise ValueError(f"connect: unknown node id {nid}")
+        if self._types[dst] == NodeType.IN:
+            raise ValueError("connect: in nodes take no incoming edges")
+        if self._types[src] == NodeType.OUT:
+            raise ValueError("connect: out nodes have no outgoing edges")
+        self._edges.append((int(src), int(dst), int(outlet), int(inlet)))
+
+    def validate(self) -> None:
+        t, e = self.arrays()
+        _check(_lib.mg_graph_validate(_ptr(t), len(t), _ptr(e), len(self._edges)))
+
+    def num_nodes(self) -> int:
+        return len(self._types)
+
+    def node_type(self, i: int) -> NodeType:
+        return NodeType(self._types[i])
+
+    @property
+    def node_types(self) -> List[NodeType]:
+        return [NodeType(t) for t in self._types]
+
+    @property
+    def edges(self) -> List[Tuple[int, int, int, int]]:
+        return list(self._edges)
+
+    def arrays(self) -> Tuple[np.ndarray, np.ndarray]:
+        t = np.asarray(self._types, dtype=np.int32)
+        e = np.asarray(self._edges, dtype=np.int32).reshape(-1, 4)
+        return np.ascontiguousarray(t), np.ascontiguousarray(e)
+
+    @staticmethod
+    def from_arrays(types, edges) -> "Graph":
+        g = Graph()
+        g._types = [int(x) for x in np.asarray(types).reshape(-1)]
+        g._edges = [tuple(int(v) for v in row) for row in np.asarray(edges).reshape(-1, 4)]
+        return g
+
+
+def disjoint_union(graphs: Sequence[Graph]) -> Graph:
+    """`graph.cpp:116-128`."""
+    out = Graph()
+    for g in graphs:
+        g.validate()
+        off = out.num_nodes()
+        out._types.extend(g._types)
+        out._edges.extend((s + off, d + off, o, i) for (s, d, o, i) in g._edges)
+    return out
+
+
+def default_param_row(t: int) -> np.ndarray:
+    row = np.zeros(param_width(t), dtype=np.float64)
+    if row.size:
+        _check(_lib.mg_default_param_row(int(t), _ptr(row)))
+    return row
+
+
+def default_params(node_types: Sequence[int]) -> Dict[NodeType, np.ndarray]:
+    """`graph.cpp:157-169`: one table per parameterised type present, default rows."""
+    counts: Dict[int, int] = {}
+    for t in node_types:
+        if param_width(t) > 0:
+            counts[int(t)] = counts.get(int(t), 0) + 1
+    return {NodeType(t): np.tile(default_param_row(t), (n, 1)) for t, n in sorted(counts.items())}
+
+
+def concat_params(stores: Sequence[Dict[NodeType, np.ndarray]]) -> Dict[NodeType, np.ndarray]:
+    """`graph.cpp:171-186`."""
+    out: Dict[NodeType, np.ndarray] = {}
+    for s in stores:
+        for t, m in sorted(s.items()):
+            if t in out:
+                if out[t].shape[1] != m.shape[1]:
+                    raise ValueError("concat_params: column mismatch")
+                out[t] = np.concatenate([out[t], m], axis=0)
+            else:
+                out[t] = np.array(m, dtype=np.float64)
+    return out
+
+
+@dataclass
+class FlatGraph:
+    """`graph.hpp:92-101`."""
+    node_types: List[NodeType]
+    edges: List[Tuple[int, int, int, int]]
+    params: Dict[NodeType, np.ndarray] = field(default_factory=dict)
+    num_inputs: int = 0
+    num_outputs: int = 0
+
+    def num_nodes(self) -> int:
+        return len(self.node_types)
+
+    def arrays(self) -> Tuple[np.ndarray, np.ndarray]:
+        return (np.ascontiguousarray(np.asarray([int(t) for t in self.node_types], dtype=np.int32)),
+                np.ascontiguousarray(np.asarray(self.edges, dtype=np.int32).reshape(-1, 4)))
+
+
+def to_flat(g: Graph) -> FlatGraph:
+    """`graph.cpp:188-199`: validate, freeze, default parameter rows."""
+    g.validate()
+    types = g.node_types
+    return FlatGraph(types, g.edges, default_params(types),
+                     sum(1 for t in types if t == NodeType.IN), sum(1 for t in types if t == NodeType.OUT))
+
+
+def _tables(params: Dict[int, np.ndarray]):
+    """Pointer array [10] + rows [10] for a per-type table dict (keeps arrays alive)."""
+    keep = []
+    ptrs = (_vp * NUM_NODE_TYPES)()
+    rows = np.zeros(NUM_NODE_TYPES, dtype=np.int32)
+    for t, m in params.items():
+        a = np.ascontiguousarray(m, dtype=np.float64)
+        if a.ndim != 2:
+            a = a.reshape(-1, param_width(t))
+        keep.append(a)
+        ptrs[int(t)] = a.ctypes.data
+        rows[int(t)] = a.shape[0]
+    return ptrs, rows, keep
+
+
+# ---- scheduling ------------------------------------------------------------------------------
+
+@dataclass
+class StepIndex:
+    """`schedule.hpp:60-68`."""
+    type: NodeType
+    gather: List[int]
+    aggregate: List[int]
+    param_begin: int
+    param_end: int
+    store_begin: int
+    store_end: int
+
+
+@dataclass
+class Schedule:
+    type_string: List[NodeType]
+    subsets: List[List[int]]
+
+    def num_steps(self) -> int:
+        return len(self.subsets) - 1
+
+    def type_codes(self) -> str:
+        return "".join(type_code(t) for t in self.type_string)
+
+
+class RenderData:
+    """`schedule.hpp:72-86`, computed by the C++ plan builder (owns the C handle)."""
+
+    def __init__(self, handle, fg: FlatGraph):
+        self._h = handle
+        info = np.zeros(6, dtype=np.int32)
+        _check(_lib.mg_plan_info(self._h, _ptr(info)))
+        n_steps, self.buffer_rows, self.num_inputs, self.output_begin, n_edges, n_ts = (int(x) for x in info)
+        buf = ctypes.create_string_buffer(n_ts + 1)
+        _check(_lib.mg_plan_type_codes(self._h, buf, n_ts + 1))
+        sizes = np.zeros(n_ts, dtype=np.int32)
+        rows = np.zeros(fg.num_nodes(), dtype=np.int32)
+        _check(_lib.mg_plan_subsets(self._h, _ptr(sizes), _ptr(rows)))
+        subsets, off = [], 0
+        for s in sizes:
+            subsets.append([int(r) for r in rows[off:off + s]])
+            off += int(s)
+        self.schedule = Schedule([type_from_code(c) for c in buf.value.decode()], subsets)
+        sig = np.zeros(fg.num_nodes(), dtype=np.int32)
+        _check(_lib.mg_plan_sigma(self._h, _ptr(sig)))
+        self.sigma = [int(x) for x in sig]
+        ft = np.zeros(fg.num_nodes(), dtype=np.int32)
+        fe = np.zeros((max(n_edges, 1), 4), dtype=np.int32)
+        _check(_lib.mg_plan_flat(self._h, _ptr(ft), _ptr(fe)))
+        self.flat = FlatGraph([NodeType(int(t)) for t in ft], [tuple(int(v) for v in r) for r in fe[:n_edges]],
+                              {}, fg.num_inputs, fg.num_outputs)
+        self.steps: List[StepIndex] = []
+        head = np.zeros(6, dtype=np.int32)
+        for k in range(n_steps):
+            _check(_lib.mg_plan_step(self._h, k, _ptr(head), None, None))
+            g = np.zeros(max(int(head[5]), 1), dtype=np.int32)
+            a = np.zeros(max(int(head[5]), 1), dtype=np.int32)
+            _check(_lib.mg_plan_step(self._h, k, _ptr(head), _ptr(g), _ptr(a)))
+            m = int(head[5])
+            self.steps.append(StepIndex(NodeType(int(head[0])), [int(x) for x in g[:m]], [int(x) for x in a[:m]],
+                                        int(head[1]), int(head[2]), int(head[3]), int(head[4])))
+        self.param_source_rows: Dict[NodeType, List[int]] = {}
+        for t in range(NUM_NODE_TYPES):
+            n = int(_lib.mg_plan_param_source_rows(self._h, t, None))
+            if n > 0:
+                out = np.zeros(n, dtype=np.int32)
+                _lib.mg_plan_param_source_rows(self._h, t, _ptr(out))
+                self.param_source_rows[NodeType(t)] = [int(x) for x in out]
+        if fg.params:
+            self.flat.params = self.reorder_params(fg.params)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def reorder_params(self, original: Dict[int, np.ndarray]) -> Dict[NodeType, np.ndarray]:
+        """`schedule.cpp:454-471`."""
+        ptrs, rows, keep = _tables(original)
+        out = {t: np.zeros((len(r), param_width(t)), dtype=np.float64) for t, r in self.param_source_rows.items()}
+        optrs = (_vp * NUM_NODE_TYPES)()
+        for t, m in out.items():
+            optrs[int(t)] = m.ctypes.data
+        _check(_lib.mg_plan_reorder_params(self._h, ptrs, _ptr(rows), optrs))
+        del keep
+        return out
+
+    def kernel_count(self, batch: int, length: int) -> int:
+        c = _i32()
+        _check(_lib.mg_plan_kernel_count(self._h, batch, length, ctypes.byref(c)))
+        return int(c.value)
+
+    def __del__(self, _destroy=_lib.mg_plan_destroy):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            _destroy(h)
+
+
+def compute_render_data(fg: FlatGraph, strategy: int = Strategy.GREEDY, beam_width: int = 32,
+                        optimal_node_cap: int = 256) -> RenderData:
+    """`schedule.cpp:473-525` (validates the graph like to_flat)."""
+    t, e = fg.arrays()
+    h = _vp()
+    _check(_lib.mg_plan_create(_ptr(t), len(t), _ptr(e), len(fg.edges), int(strategy), int(beam_width),
+                               int(optimal_node_cap), ctypes.byref(h)))
+    return RenderData(h, fg)
+
+
+def make_schedule(fg: FlatGraph, strategy: int = Strategy.GREEDY, beam_width: int = 32,
+                  optimal_node_cap: int = 256) -> Schedule:
+    """`schedule.cpp:325-338` (returned from the full plan build)."""
+    return compute_render_data(fg, strategy, beam_width, optimal_node_cap).schedule
+
+
+def validate_schedule(fg: FlatGraph, s: Schedule) -> None:
+    """`schedule.cpp:351-395`."""
+    t, e = fg.arrays()
+    ts = np.asarray([int(x) for x in s.type_string], dtype=np.int32)
+    sizes = np.asarray([len(x) for x in s.subsets], dtype=np.int32)
+    rows = np.asarray([r for x in s.subsets for r in x] or [0], dtype=np.int32)
+    _check(_lib.mg_validate_schedule(_ptr(t), len(t), _ptr(e), len(fg.edges), _ptr(ts), len(ts), _ptr(sizes), _ptr(rows)))
+
+
+# ---- processors and rendering -----------------------------------------------------------------
+
+class ProcessorSet:
+    """`processors.hpp:25-66` with device-resident constants on CUDA device `device`."""
+
+    def __init__(self, sample_rate: float = 44100.0, reverb_seed: int = 0, envelope_taps: int = 32768,
+                 energy_floor: float = 1e-7, device: int = 0):
+        self._h = _vp()
+        _check(_lib.mg_processors_create(float(sample_rate), int(reverb_seed), int(envelope_taps), float(energy_floor),
+                                         int(device), ctypes.byref(self._h)))
+        info = np.zeros(3, dtype=np.int64)
+        _check(_lib.mg_processors_info(self._h, _ptr(info)))
+        self.sample_rate = float(sample_rate)
+        self.device = int(device)
+        self.delay_span, self.delay_window, self.reverb_length = (int(x) for x in info)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def process(self, t: int, inp: np.ndarray, slots: int, batch: int, length: int,
+                params: Optional[np.ndarray] = None, param_offset: int = 0) -> np.ndarray:
+        """`processors.cpp:229-282`: inp [slots][batch][2][length] -> same shape."""
+        x = np.ascontiguousarray(inp, dtype=np.float64)
+        out = np.zeros_like(x)
+        p = None if params is None else np.ascontiguousarray(params, dtype=np.float64).reshape(-1, param_width(t))
+        _check(_lib.mg_process(self._h, int(t), _ptr(x), _ptr(out), slots, batch, length, _ptr(p),
+                               0 if p is None else p.shape[0], param_offset))
+        return out
+
+    def process_node(self, t: int, inp: np.ndarray, params: Sequence[float] = ()) -> np.ndarray:
+        """`processors.cpp:284-297`: inp [batch][2][length]."""
+        x = np.asarray(inp, dtype=np.float64)
+        if x.ndim != 3 or x.shape[1] != 2:
+            raise ValueError("process_node: processors are stereo (2 channels)")
+        p = np.asarray(params, dtype=np.float64).reshape(-1)
+        if p.size != param_width(t):
+            raise ValueError(f"{type_name(t)}: expected {param_width(t)} parameters")
+        return self.process(t, x[None], 1, x.shape[0], x.shape[2], p.reshape(1, -1) if p.size else None, 0)[0]
+
+    def reverb_kernel(self, row: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+        r = np.ascontiguousarray(row, dtype=np.float64)
+        left = np.zeros(self.reverb_length)
+        right = np.zeros(self.reverb_length)
+        _check(_lib.mg_reverb_kernel(self._h, _ptr(r), _ptr(left), _ptr(right)))
+        return left, right
+
+    def delay_kernel(self, row: np.ndarray, channel: int) -> np.ndarray:
+        r = np.ascontiguousarray(row, dtype=np.float64)
+        k = np.zeros(self.delay_span)
+        _check(_lib.mg_delay_kernel(self._h, _ptr(r), int(channel), _ptr(k), None))
+        return k
+
+    def delay_positions(self, row: np.ndarray, channel: int) -> List[int]:
+        r = np.ascontiguousarray(row, dtype=np.float64)
+        pos = np.zeros(20, dtype=np.int64)
+        _check(_lib.mg_delay_kernel(self._h, _ptr(r), int(channel), None, _ptr(pos)))
+        return [int(x) for x in pos]
+
+    def __del__(self, _destroy=_lib.mg_processors_destroy):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            _destroy(h)
+
+
+def compressor_gain_log(g_u, threshold, knee, ratio) -> float:
+    return float(_lib.mg_compressor_gain_log(g_u, threshold, knee, ratio))
+
+
+def noisegate_gain_log(g_u, threshold, knee, ratio) -> float:
+    return float(_lib.mg_noisegate_gain_log(g_u, threshold, knee, ratio))
+
+
+def check_param_row(t: int, row: Sequence[float]) -> None:
+    r = np.ascontiguousarray(row, dtype=np.float64)
+    _check(_lib.mg_check_param_row(int(t), _ptr(r)))
+
+
+def render(rd: RenderData, procs: ProcessorSet, params: Optional[Dict[int, np.ndarray]], sources: np.ndarray,
+           keep_intermediates: bool = False, sample_rate: Optional[float] = None, out: Optional[np.ndarray] = None):
+    """`render.cpp:14-81`. sources [K][B][2][L] (host, double); params in render order
+    (RenderData.reorder_params) or None for rd.flat.params. Returns outputs
+    [num_outputs][B][2][L] (and intermediates [rows][B][2][L], original row order)."""
+    src = np.ascontiguousarray(sources, dtype=np.float64)
+    if src.ndim != 4:
+        raise ValueError("render: sources must be [K][B][2][L]")
+    if src.shape[0] != rd.num_inputs:
+        raise ValueError(f"render: expected {rd.num_inputs} sources, got {src.shape[0]}")
+    if src.shape[2] != 2:
+        raise ValueError("render: sources must be stereo")
+    k, b, _, n = src.shape
+    ptrs, rows, keep = _tables(rd.flat.params if params is None else params)
+    shape = (rd.buffer_rows - rd.output_begin, b, 2, n)
+    if out is not None:
+        if out.shape != shape or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ValueError(f"render: out must be a contiguous float64 array of shape {shape}")
+        outs = out
+    else:
+        outs = np.zeros(shape)
+    inter = np.zeros((rd.buffer_rows, b, 2, n)) if keep_intermediates else None
+    fs = procs.sample_rate if sample_rate is None else sample_rate
+    _check(_lib.mg_render(rd.handle, procs.handle, ptrs, _ptr(rows), _ptr(src), k, b, n, fs, _ptr(outs), _ptr(inter)))
+    del keep
+    return (outs, inter) if keep_intermediates else outs
+
+
+# ---- workload generators (bit-identical to the reference's) ------------------------------------
+
+def generate_console(tracks: int, prune: float = 0.0, seed: int = 0) -> Graph:
+    """`console.cpp:10-44`."""
+    cap_n, cap_e = 8 * tracks + 16, 10 * tracks + 16
+    t = np.zeros(cap_n, dtype=np.int32)
+    e = np.zeros((cap_e, 4), dtype=np.int32)
+    nn, ne = _i32(), _i32()
+    _check(_lib.mg_generate_console(tracks, prune, seed, _ptr(t), cap_n, _ptr(e), cap_e, ctypes.byref(nn), ctypes.byref(ne)))
+    return Graph.from_arrays(t[:nn.value], e[:ne.value])
+
+
+def random_legal_params(node_types: Sequence[int], seed: int) -> Dict[NodeType, np.ndarray]:
+    """`tests/support/test_util.cpp:63-113` with a fresh mt19937(seed), original row order."""
+    counts: Dict[int, int] = {}
+    for t in node_types:
+        if param_width(t) > 0:
+            counts[int(t)] = counts.get(int(t), 0) + 1
+    out = {NodeType(t): np.zeros((n, param_width(t))) for t, n in sorted(counts.items())}
+    tt = np.ascontiguousarray(np.asarray([int(x) for x in node_types], dtype=np.int32))
+    ptrs = (_vp * NUM_NODE_TYPES)()
+    for t, m in out.items():
+        ptrs[int(t)] = m.ctypes.data
+    _check(_lib.mg_random_legal_params(_ptr(tt), len(tt), seed, ptrs))
+    return out
+
+
+def uniform_noise(n: int, seed: int) -> np.ndarray:
+    """`dsp.cpp:222-230`."""
+    out = np.zeros(n)
+    _check(_lib.mg_uniform_noise(n, seed, _ptr(out)))
+    return out
+
+
+from .device import DeviceRenderer  # noqa: E402  (torch-backed device path)
+
+__all__ = [
+    "NodeType", "Strategy", "Graph", "FlatGraph", "RenderData", "StepIndex", "Schedule", "ProcessorSet",
+    "DeviceRenderer", "to_flat", "disjoint_union", "default_params", "default_param_row", "concat_params",
+    "compute_render_data", "make_schedule", "validate_schedule", "render", "param_width", "type_code", "type_name",
+    "generate_console", "random_legal_params", "uniform_noise", "compressor_gain_log", "noisegate_gain_log",
+    "check_param_row", "LIB_PATH",
+]

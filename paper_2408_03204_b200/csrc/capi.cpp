@@ -1,0 +1,401 @@
+// C ABI (include/mixgraph_b200.h): thin extern "C" layer over the C++ API.
+// Exceptions become status codes; std::invalid_argument keeps its message (MG_EINVAL).
+#include "../../include/mixgraph_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "mixgraph_b200/render.hpp"
+
+namespace mixgraph::workload {
+Graph generate_console(int tracks, double prune, std::uint32_t seed);
+ParamStore random_legal_params(const std::vector<NodeType>& types, std::uint32_t seed);
+}  // namespace mixgraph::workload
+
+using namespace mixgraph;
+
+struct mg_plan {
+  RenderData rd;
+  std::unique_ptr<DevicePlan> dev;  // uploaded lazily on first device render
+  std::vector<cudaEvent_t> events;  // per-step timing events (profiled renders)
+  std::mutex mu;
+  ~mg_plan() {
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+  }
+};
+
+struct mg_processors {
+  std::unique_ptr<ProcessorSet> ps;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int32_t guarded(F&& f) {
+  try {
+    f();
+    return MG_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return MG_EINVAL;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return MG_EINVAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MG_ERUNTIME;
+  } catch (...) {
+    g_err = "unknown error";
+    return MG_ERUNTIME;
+  }
+}
+
+NodeType to_type(int32_t t) {
+  if (t < 0 || t >= kNumNodeTypes) throw std::invalid_argument("unknown node type " + std::to_string(t));
+  return static_cast<NodeType>(t);
+}
+
+Graph make_graph(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne) {
+  std::vector<NodeType> tv(static_cast<std::size_t>(n));
+  for (int i = 0; i < n; ++i) tv[static_cast<std::size_t>(i)] = to_type(types[i]);
+  std::vector<Edge> ev(static_cast<std::size_t>(ne));
+  for (int i = 0; i < ne; ++i) ev[static_cast<std::size_t>(i)] = Edge{edges[4 * i], edges[4 * i + 1], edges[4 * i + 2], edges[4 * i + 3]};
+  Graph g;
+  g.append_unchecked(tv, ev);
+  return g;
+}
+
+ParamStore make_store(const double* const* tables, const int32_t* rows) {
+  ParamStore s;
+  for (int t = 0; t < kNumNodeTypes; ++t) {
+    const int w = param_width(static_cast<NodeType>(t));
+    if (w == 0 || !tables || !tables[t]) continue;
+    ParamMatrix m(rows[t], w);
+    std::memcpy(m.values.data(), tables[t], sizeof(double) * m.values.size());
+    s.tables.emplace(static_cast<NodeType>(t), std::move(m));
+  }
+  return s;
+}
+
+void export_graph(const Graph& g, int32_t* types, int32_t cap_nodes, int32_t* edges, int32_t cap_edges, int32_t* nn,
+                  int32_t* ne) {
+  *nn = g.num_nodes();
+  *ne = static_cast<int32_t>(g.edges().size());
+  if (types && g.num_nodes() <= cap_nodes) {
+    for (int i = 0; i < g.num_nodes(); ++i) types[i] = static_cast<int32_t>(g.node_type(i));
+  }
+  if (edges && static_cast<int>(g.edges().size()) <= cap_edges) {
+    for (std::size_t i = 0; i < g.edges().size(); ++i) {
+      const Edge& e = g.edges()[i];
+      edges[4 * i] = e.src;
+      edges[4 * i + 1] = e.dst;
+      edges[4 * i + 2] = e.outlet;
+      edges[4 * i + 3] = e.inlet;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mg_last_error(void) { return g_err.c_str(); }
+int32_t mg_abi_version(void) { return 1; }
+int32_t mg_param_width(int32_t t) { return (t < 0 || t >= kNumNodeTypes) ? -1 : param_width(static_cast<NodeType>(t)); }
+
+int32_t mg_graph_validate(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne) {
+  return guarded([&] { make_graph(types, n, edges, ne).validate(); });
+}
+
+int32_t mg_plan_create(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne, int32_t strategy,
+                       int32_t beam_width, int32_t optimal_cap, mg_plan** out) {
+  return guarded([&] {
+    if (strategy < 0 || strategy > 3) throw std::invalid_argument("unknown strategy");
+    FlatGraph fg = to_flat(make_graph(types, n, edges, ne));
+    ScheduleOptions o;
+    o.strategy = static_cast<Strategy>(strategy);
+    o.beam_width = beam_width;
+    o.optimal_node_cap = optimal_cap;
+    auto p = std::make_unique<mg_plan>();
+    p->rd = compute_render_data(fg, o);
+    *out = p.release();
+  });
+}
+
+void mg_plan_destroy(mg_plan* p) { delete p; }
+
+int32_t mg_plan_info(const mg_plan* p, int32_t* info) {
+  info[0] = static_cast<int32_t>(p->rd.steps.size());
+  info[1] = p->rd.buffer_rows;
+  info[2] = p->rd.num_inputs;
+  info[3] = p->rd.output_begin;
+  info[4] = static_cast<int32_t>(p->rd.flat.edges.size());
+  info[5] = static_cast<int32_t>(p->rd.schedule.type_string.size());
+  return MG_OK;
+}
+
+int32_t mg_plan_type_codes(const mg_plan* p, char* buf, int32_t cap) {
+  const std::string s = p->rd.schedule.type_codes();
+  if (static_cast<int>(s.size()) + 1 > cap) {
+    g_err = "mg_plan_type_codes: buffer too small";
+    return MG_EINVAL;
+  }
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return MG_OK;
+}
+
+int32_t mg_plan_subsets(const mg_plan* p, int32_t* sizes, int32_t* rows) {
+  int off = 0;
+  for (std::size_t k = 0; k < p->rd.schedule.subsets.size(); ++k) {
+    sizes[k] = static_cast<int32_t>(p->rd.schedule.subsets[k].size());
+    for (int r : p->rd.schedule.subsets[k]) rows[off++] = r;
+  }
+  return MG_OK;
+}
+
+int32_t mg_plan_sigma(const mg_plan* p, int32_t* sigma) {
+  for (std::size_t i = 0; i < p->rd.sigma.size(); ++i) sigma[i] = p->rd.sigma[i];
+  return MG_OK;
+}
+
+int32_t mg_plan_flat(const mg_plan* p, int32_t* types, int32_t* edges) {
+  const FlatGraph& f = p->rd.flat;
+  for (std::size_t i = 0; i < f.node_types.size(); ++i) types[i] = static_cast<int32_t>(f.node_types[i]);
+  for (std::size_t i = 0; i < f.edges.size(); ++i) {
+    edges[4 * i] = f.edges[i].src;
+    edges[4 * i + 1] = f.edges[i].dst;
+    edges[4 * i + 2] = f.edges[i].outlet;
+    edges[4 * i + 3] = f.edges[i].inlet;
+  }
+  return MG_OK;
+}
+
+int32_t mg_plan_step(const mg_plan* p, int32_t k, int32_t* head, int32_t* gather, int32_t* aggregate) {
+  return guarded([&] {
+    const StepIndex& s = p->rd.steps.at(static_cast<std::size_t>(k));
+    head[0] = static_cast<int32_t>(s.type);
+    head[1] = s.param_begin;
+    head[2] = s.param_end;
+    head[3] = s.store_begin;
+    head[4] = s.store_end;
+    head[5] = static_cast<int32_t>(s.gather.size());
+    if (gather) std::copy(s.gather.begin(), s.gather.end(), gather);
+    if (aggregate) std::copy(s.aggregate.begin(), s.aggregate.end(), aggregate);
+  });
+}
+
+int32_t mg_plan_param_source_rows(const mg_plan* p, int32_t t, int32_t* out) {
+  auto it = p->rd.param_source_rows.find(static_cast<NodeType>(t));
+  if (it == p->rd.param_source_rows.end()) return 0;
+  if (out) std::copy(it->second.begin(), it->second.end(), out);
+  return static_cast<int32_t>(it->second.size());
+}
+
+int32_t mg_plan_reorder_params(const mg_plan* p, const double* const* original, const int32_t* rows,
+                               double* const* reordered) {
+  return guarded([&] {
+    ParamStore r = p->rd.reorder_params(make_store(original, rows));
+    for (auto& [t, m] : r.tables) {
+      if (reordered[static_cast<int>(t)]) std::memcpy(reordered[static_cast<int>(t)], m.values.data(), sizeof(double) * m.values.size());
+    }
+  });
+}
+
+int32_t mg_validate_schedule(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne, const int32_t* ts,
+                             int32_t num_subsets, const int32_t* sizes, const int32_t* rows) {
+  return guarded([&] {
+    FlatGraph fg;
+    Graph g = make_graph(types, n, edges, ne);
+    fg.node_types = g.node_types();
+    fg.edges = g.edges();
+    Schedule s;
+    int off = 0;
+    for (int k = 0; k < num_subsets; ++k) {
+      s.type_string.push_back(to_type(ts[k]));
+      s.subsets.emplace_back(rows + off, rows + off + sizes[k]);
+      off += sizes[k];
+    }
+    validate_schedule(fg, s);
+  });
+}
+
+int32_t mg_processors_create(double fs, uint32_t seed, int32_t env_taps, double floor_, int32_t device, mg_processors** out) {
+  return guarded([&] {
+    if (device >= 0 && cudaSetDevice(device) != cudaSuccess) throw std::runtime_error("cudaSetDevice failed");
+    ProcessorConfig c;
+    c.sample_rate = fs;
+    c.reverb_seed = seed;
+    c.envelope_taps = env_taps;
+    c.energy_floor = floor_;
+    auto p = std::make_unique<mg_processors>();
+    p->ps = std::make_unique<ProcessorSet>(c);
+    *out = p.release();
+  });
+}
+
+void mg_processors_destroy(mg_processors* p) { delete p; }
+
+int32_t mg_processors_info(const mg_processors* p, int64_t* info) {
+  info[0] = p->ps->delay_span();
+  info[1] = p->ps->delay_window();
+  info[2] = p->ps->reverb_length();
+  return MG_OK;
+}
+
+DevicePlan& device_plan(const mg_plan* cp);
+
+int32_t mg_render(const mg_plan* p, const mg_processors* procs, const double* const* tables, const int32_t* rows,
+                  const double* sources, int32_t num_sources, int32_t batch, int64_t length, double fs, double* outputs,
+                  double* intermediates) {
+  return guarded([&] {
+    (void)fs;
+    const RenderData& rd = p->rd;
+    if (num_sources != rd.num_inputs) {
+      throw std::invalid_argument("render: expected " + std::to_string(rd.num_inputs) + " sources, got " +
+                                  std::to_string(num_sources));
+    }
+    if (num_sources == 0) throw std::invalid_argument("render: graph has no input nodes to take signal shape from");
+    const std::size_t stride = static_cast<std::size_t>(batch) * 2 * static_cast<std::size_t>(length);
+    std::vector<const double*> src;
+    for (int k = 0; k < num_sources; ++k) src.push_back(sources + stride * k);
+    std::vector<double*> outs, inter;
+    for (int r = rd.output_begin; r < rd.buffer_rows; ++r) outs.push_back(outputs + stride * (r - rd.output_begin));
+    for (int r = 0; intermediates && r < rd.buffer_rows; ++r) inter.push_back(intermediates + stride * r);
+    render_host(rd, *procs->ps, make_store(tables, rows), src.data(), batch, static_cast<long>(length), outs.data(),
+                intermediates ? inter.data() : nullptr, &device_plan(p));
+  });
+}
+
+DevicePlan& device_plan(const mg_plan* cp) {
+  auto* p = const_cast<mg_plan*>(cp);
+  std::scoped_lock lock(p->mu);
+  if (!p->dev) p->dev = std::make_unique<DevicePlan>(p->rd);
+  return *p->dev;
+}
+
+int32_t mg_plan_workspace_bytes(const mg_plan* p, const mg_processors* procs, int32_t batch, int64_t length, uint64_t* bytes) {
+  return guarded([&] { *bytes = device_plan(p).workspace_bytes(batch, static_cast<long>(length), *procs->ps); });
+}
+
+int32_t mg_plan_kernel_count(const mg_plan* p, int32_t batch, int64_t length, int32_t* count) {
+  return guarded([&] { *count = device_plan(p).kernels_per_render(batch, static_cast<long>(length)); });
+}
+
+int32_t mg_render_arena(const mg_plan* p, const mg_processors* procs, const double* const* d_tables, float* d_arena,
+                        int32_t batch, int64_t length, void* d_ws, uint64_t ws_bytes, void* stream) {
+  return guarded([&] {
+    render_arena(device_plan(p), *procs->ps, d_tables, d_arena, batch, static_cast<long>(length), d_ws, ws_bytes,
+                 static_cast<cudaStream_t>(stream));
+  });
+}
+
+int32_t mg_render_arena_profiled(const mg_plan* cp, const mg_processors* procs, const double* const* d_tables,
+                                 float* d_arena, int32_t batch, int64_t length, void* d_ws, uint64_t ws_bytes,
+                                 void* stream, float* step_ms) {
+  return guarded([&] {
+    auto* p = const_cast<mg_plan*>(cp);
+    DevicePlan& dp = device_plan(p);
+    {
+      std::scoped_lock lock(p->mu);
+      while (p->events.size() < 2 * p->rd.steps.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) throw std::runtime_error("cudaEventCreate failed");
+        p->events.push_back(e);
+      }
+    }
+    auto s = static_cast<cudaStream_t>(stream);
+    render_arena(dp, *procs->ps, d_tables, d_arena, batch, static_cast<long>(length), d_ws, ws_bytes, s, p->events.data());
+    if (step_ms) {
+      if (cudaStreamSynchronize(s) != cudaSuccess) throw std::runtime_error("render failed");
+      for (std::size_t k = 0; k < p->rd.steps.size(); ++k) {
+        cudaEventElapsedTime(&step_ms[k], p->events[2 * k], p->events[2 * k + 1]);
+      }
+    }
+  });
+}
+
+int32_t mg_process(const mg_processors* procs, int32_t t, const double* in, double* out, int32_t slots, int32_t batch,
+                   int64_t length, const double* params, int32_t param_rows, int32_t param_offset) {
+  return guarded([&] {
+    const NodeType type = to_type(t);
+    ParamMatrix m;
+    const ParamMatrix* pm = nullptr;
+    if (params) {
+      m = ParamMatrix(param_rows, param_width(type));
+      std::memcpy(m.values.data(), params, sizeof(double) * m.values.size());
+      pm = &m;
+    }
+    procs->ps->process(type, in, out, slots, batch, static_cast<long>(length), pm, param_offset);
+  });
+}
+
+int32_t mg_reverb_kernel(const mg_processors* procs, const double* row, double* left, double* right) {
+  return guarded([&] {
+    auto [l, r] = procs->ps->reverb_kernel({row, static_cast<std::size_t>(param_width(NodeType::Reverb))});
+    std::memcpy(left, l.data(), sizeof(double) * l.size());
+    std::memcpy(right, r.data(), sizeof(double) * r.size());
+  });
+}
+
+int32_t mg_delay_kernel(const mg_processors* procs, const double* row, int32_t channel, double* kernel, int64_t* positions) {
+  return guarded([&] {
+    std::span<const double> r{row, static_cast<std::size_t>(param_width(NodeType::Delay))};
+    if (positions) {
+      auto pos = procs->ps->delay_positions(r, channel);
+      for (std::size_t i = 0; i < pos.size(); ++i) positions[i] = pos[i];
+    }
+    if (kernel) {
+      auto k = procs->ps->delay_kernel(r, channel);
+      std::memcpy(kernel, k.data(), sizeof(double) * k.size());
+    }
+  });
+}
+
+double mg_compressor_gain_log(double g, double t, double w, double r) { return compressor_gain_log(g, t, w, r); }
+double mg_noisegate_gain_log(double g, double t, double w, double r) { return noisegate_gain_log(g, t, w, r); }
+
+int32_t mg_check_param_row(int32_t t, const double* row) {
+  return guarded([&] {
+    const NodeType type = to_type(t);
+    check_param_row(type, {row, static_cast<std::size_t>(param_width(type))});
+  });
+}
+
+int32_t mg_generate_console(int32_t tracks, double prune, uint32_t seed, int32_t* types, int32_t cap_nodes, int32_t* edges,
+                            int32_t cap_edges, int32_t* nn, int32_t* ne) {
+  return guarded([&] { export_graph(workload::generate_console(tracks, prune, seed), types, cap_nodes, edges, cap_edges, nn, ne); });
+}
+
+int32_t mg_random_legal_params(const int32_t* types, int32_t n, uint32_t seed, double* const* tables) {
+  return guarded([&] {
+    std::vector<NodeType> tv(static_cast<std::size_t>(n));
+    for (int i = 0; i < n; ++i) tv[static_cast<std::size_t>(i)] = to_type(types[i]);
+    ParamStore s = workload::random_legal_params(tv, seed);
+    for (auto& [t, m] : s.tables) {
+      if (tables[static_cast<int>(t)]) std::memcpy(tables[static_cast<int>(t)], m.values.data(), sizeof(double) * m.values.size());
+    }
+  });
+}
+
+int32_t mg_default_param_row(int32_t t, double* row) {
+  return guarded([&] {
+    const NodeType type = to_type(t);
+    default_param_row(type, {row, static_cast<std::size_t>(param_width(type))});
+  });
+}
+
+int32_t mg_uniform_noise(int64_t n, uint32_t seed, double* out) {
+  return guarded([&] {
+    auto v = dsp::uniform_noise(static_cast<long>(n), seed);
+    std::memcpy(out, v.data(), sizeof(double) * v.size());
+  });
+}
+
+}  // extern "C"

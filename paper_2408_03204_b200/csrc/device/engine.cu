@@ -1,0 +1,534 @@
+// Render engine: processor constants, device step table, step dispatch, host-buffer API.
+//
+// Reference call stack this replaces (`render.cpp:14-81`, `processors.cpp:151-282`):
+// render() allocates a double arena, then per step zero-fills step_in/step_out, sums the
+// gathered rows, runs ProcessorSet::process and memcpy's the result back. Here the arena
+// is fp32 in HBM and each step is one fused launch sequence that gathers straight from the
+// arena rows and stores straight into the step's contiguous output rows (the contiguity
+// is what node reordering buys, `schedule.cpp:397-413`): no step_in/step_out buffers.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <numbers>
+#include <random>
+#include <stdexcept>
+#include <string>
+
+#include "launch.hpp"
+#include "mixgraph_b200/render.hpp"
+
+namespace mixgraph {
+
+namespace {
+
+[[noreturn]] void fail(const std::string& msg) { throw std::invalid_argument(msg); }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string("cuda: ") + what + ": " + cudaGetErrorString(e));
+}
+
+std::string tname(NodeType t) { return std::string(type_name(t)); }
+
+// Grow-only device allocation.
+struct DeviceBuffer {
+  void* ptr = nullptr;
+  std::size_t cap = 0;
+  void* ensure(std::size_t bytes) {
+    if (bytes > cap) {
+      if (ptr) cudaFree(ptr);
+      ptr = nullptr;
+      cap = 0;
+      cuda_check(cudaMalloc(&ptr, bytes), "cudaMalloc");
+      cap = bytes;
+    }
+    return ptr;
+  }
+  ~DeviceBuffer() {
+    if (ptr) cudaFree(ptr);
+  }
+};
+
+// Per-thread, per-device resources of the host-buffer API (render / process).
+struct Engine {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  DeviceBuffer arena, ws, params, staging, aux;
+  ~Engine() {
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+Engine& engine_for(int device) {
+  thread_local std::map<int, std::unique_ptr<Engine>> engines;
+  auto& e = engines[device];
+  if (!e) {
+    e = std::make_unique<Engine>();
+    e->device = device;
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  }
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  return *e;
+}
+
+inline std::size_t align256(std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255); }
+
+std::size_t eq_ws_bytes(int slots) { return align256(sizeof(float) * 2048 * slots) + align256(sizeof(float) * mgb::kEqFft * slots); }
+
+}  // namespace
+
+struct DeviceConstants {
+  int device = 0;
+  float2* stft_mid = nullptr;
+  float2* stft_side = nullptr;
+  int frames = 0;
+  ~DeviceConstants() {
+    if (stft_mid) cudaFree(stft_mid);
+    if (stft_side) cudaFree(stft_side);
+  }
+};
+
+// ---- scalar reference semantics (processors.cpp:110-149) ------------------------------
+
+double compressor_gain_log(double g_u, double threshold, double knee, double ratio) {
+  if (g_u >= threshold + knee) return threshold + (g_u - threshold) / ratio;
+  if (g_u < threshold - knee) return g_u;
+  const double d = g_u - threshold + knee;
+  return g_u + (1.0 / ratio - 1.0) * d * d / (4.0 * knee);
+}
+
+double noisegate_gain_log(double g_u, double threshold, double knee, double ratio) {
+  if (g_u >= threshold + knee) return g_u;
+  if (g_u < threshold - knee) return threshold + ratio * (g_u - threshold);
+  const double d = g_u - threshold - knee;
+  return g_u + (1.0 - ratio) * d * d / (4.0 * knee);
+}
+
+void check_param_row(NodeType type, std::span<const double> row) {
+  const std::string name = tname(type);
+  for (double v : row) {
+    if (!std::isfinite(v)) fail(name + ": non-finite parameter value");
+  }
+  if (type == NodeType::Compressor || type == NodeType::Noisegate) {
+    if (!(row[0] > 0.0 && row[0] < 1.0)) fail(name + ": alpha must be in (0, 1)");
+    if (!(row[2] > 0.0)) fail(name + ": knee half-width must be positive");
+    if (!(row[3] >= 1.0)) fail(name + ": ratio must be >= 1");
+  } else if (type == NodeType::Delay) {
+    for (int tap = 0; tap < 2 * kDelayTapsPerChannel; ++tap) {
+      if (std::hypot(row[static_cast<std::size_t>(tap * kDelayTapStride)], row[static_cast<std::size_t>(tap * kDelayTapStride + 1)]) >
+          1.0 + 1e-9) {
+        fail("delay: angular frequency outside the unit disk");
+      }
+    }
+  }
+}
+
+namespace dsp {
+// dsp.cpp:222-230: mt19937(seed), 2 * (u32 * 2^-32) - 1.
+std::vector<double> uniform_noise(long n, std::uint32_t seed) {
+  std::mt19937 gen(seed);
+  std::vector<double> out(static_cast<std::size_t>(n));
+  for (auto& v : out) v = 2.0 * (static_cast<double>(gen()) * (1.0 / 4294967296.0)) - 1.0;
+  return out;
+}
+}  // namespace dsp
+
+// ---- ProcessorSet -----------------------------------------------------------------------
+
+ProcessorSet::ProcessorSet(const ProcessorConfig& config) : config_(config) {
+  if (!(config_.sample_rate > 0)) fail("sample rate must be positive");
+  delay_span_ = std::lround(kDelaySeconds * config_.sample_rate);
+  delay_window_ = static_cast<int>(std::lround(kDelayWindowSeconds * config_.sample_rate));
+  reverb_length_ = std::lround(kReverbSeconds * config_.sample_rate);
+  noise_mid_ = dsp::uniform_noise(reverb_length_, config_.reverb_seed);
+  noise_side_ = dsp::uniform_noise(reverb_length_, config_.reverb_seed + 1);
+
+  dev_ = std::make_unique<DeviceConstants>();
+  cuda_check(cudaGetDevice(&dev_->device), "cudaGetDevice");
+  dev_->frames = static_cast<int>((reverb_length_ + kReverbStftHop - 1) / kReverbStftHop);
+  const std::size_t stft_bytes = sizeof(float2) * static_cast<std::size_t>(dev_->frames) * (kReverbStftLength / 2 + 1);
+  cuda_check(cudaMalloc(&dev_->stft_mid, stft_bytes > 0 ? stft_bytes : 8), "cudaMalloc");
+  cuda_check(cudaMalloc(&dev_->stft_side, stft_bytes > 0 ? stft_bytes : 8), "cudaMalloc");
+  if (dev_->frames > 0) {
+    Engine& e = engine_for(dev_->device);
+    auto* d_noise = static_cast<double*>(e.aux.ensure(sizeof(double) * 2 * static_cast<std::size_t>(reverb_length_)));
+    cuda_check(cudaMemcpyAsync(d_noise, noise_mid_.data(), sizeof(double) * reverb_length_, cudaMemcpyHostToDevice, e.stream), "H2D");
+    cuda_check(cudaMemcpyAsync(d_noise + reverb_length_, noise_side_.data(), sizeof(double) * reverb_length_, cudaMemcpyHostToDevice, e.stream), "H2D");
+    mgb::launch_noise_stft(d_noise, reverb_length_, dev_->frames, dev_->stft_mid, e.stream);
+    mgb::launch_noise_stft(d_noise + reverb_length_, reverb_length_, dev_->frames, dev_->stft_side, e.stream);
+    cuda_check(cudaStreamSynchronize(e.stream), "noise stft");
+  }
+}
+
+ProcessorSet::~ProcessorSet() = default;
+
+namespace {
+
+mgb::ReverbConst reverb_const(const ProcessorSet& p) {
+  return {p.device().stft_mid, p.device().stft_side, p.device().frames, p.reverb_length()};
+}
+mgb::DelayConst delay_const(const ProcessorSet& p) { return {p.delay_span(), p.delay_window()}; }
+
+std::size_t step_ws_bytes(NodeType t, int slots, int batch, long length, const ProcessorSet& p) {
+  switch (t) {
+    case NodeType::Eq: return eq_ws_bytes(slots);
+    case NodeType::Compressor:
+    case NodeType::Noisegate: return mgb::dyn_workspace_bytes(slots, batch, length);
+    case NodeType::Reverb:
+      return mgb::conv_workspace_bytes(mgb::conv_geom(length, p.reverb_length()), slots, batch, p.reverb_length());
+    case NodeType::Delay:
+      return mgb::conv_workspace_bytes(mgb::conv_geom(length, p.delay_span()), slots, batch, p.delay_span());
+    default: return 0;
+  }
+}
+
+int step_kernels(NodeType t) {
+  switch (t) {
+    case NodeType::Eq: return 3;
+    case NodeType::Compressor:
+    case NodeType::Noisegate: return 1;
+    case NodeType::Reverb:
+    case NodeType::Delay: return 6;
+    default: return 1;
+  }
+}
+
+// One step on the device. a.params points at the step's first parameter row.
+void run_step(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, void* ws, cudaStream_t s) {
+  switch (t) {
+    case NodeType::In:
+    case NodeType::Out:
+    case NodeType::Mix: mgb::launch_pointwise(mgb::PointOp::Copy, a, s); break;
+    case NodeType::Gain: mgb::launch_pointwise(mgb::PointOp::Gain, a, s); break;
+    case NodeType::Imager: mgb::launch_pointwise(mgb::PointOp::Imager, a, s); break;
+    case NodeType::Eq: {
+      auto* taps = static_cast<float*>(ws);
+      auto* resp = reinterpret_cast<float*>(static_cast<char*>(ws) + align256(sizeof(float) * 2048 * a.slots));
+      mgb::launch_eq(a, taps, resp, s);
+      break;
+    }
+    case NodeType::Compressor:
+    case NodeType::Noisegate:
+      mgb::launch_dynamics(t == NodeType::Noisegate, a, p.config().envelope_taps, p.config().energy_floor, ws, s);
+      break;
+    case NodeType::Reverb: mgb::launch_reverb(a, reverb_const(p), ws, s); break;
+    case NodeType::Delay: mgb::launch_delay(a, delay_const(p), ws, s); break;
+  }
+}
+
+}  // namespace
+
+// ---- DevicePlan -------------------------------------------------------------------------
+
+DevicePlan::DevicePlan(const RenderData& rd) : rd_(rd) {
+  std::vector<int> host;
+  std::vector<char> written(static_cast<std::size_t>(rd.buffer_rows), 0);
+  for (int r = 0; r < rd.num_inputs && r < rd.buffer_rows; ++r) written[static_cast<std::size_t>(r)] = 1;
+  for (const StepIndex& st : rd.steps) {
+    const int slots = st.store_end - st.store_begin;
+    rp_off_.push_back(static_cast<long>(host.size()));
+    std::size_t e = 0;
+    for (int s = 0; s <= slots; ++s) {
+      while (e < st.aggregate.size() && st.aggregate[e] < s) ++e;
+      host.push_back(static_cast<int>(e));
+    }
+    col_off_.push_back(static_cast<long>(host.size()));
+    for (int g : st.gather) {
+      host.push_back(g);
+      // A row read before any step stored it holds zeros in the reference (render.cpp:33).
+      if (!written[static_cast<std::size_t>(g)]) {
+        written[static_cast<std::size_t>(g)] = 1;
+        zero_rows_.push_back(g);
+      }
+    }
+    for (int r = st.store_begin; r < st.store_end; ++r) written[static_cast<std::size_t>(r)] = 1;
+  }
+  if (!host.empty()) {
+    cuda_check(cudaMalloc(&d_index_, sizeof(int) * host.size()), "cudaMalloc");
+    cuda_check(cudaMemcpy(d_index_, host.data(), sizeof(int) * host.size(), cudaMemcpyHostToDevice), "H2D plan");
+  }
+}
+
+DevicePlan::~DevicePlan() {
+  if (d_index_) cudaFree(d_index_);
+}
+
+const int* DevicePlan::row_ptr(int step) const { return d_index_ + rp_off_[static_cast<std::size_t>(step)]; }
+const int* DevicePlan::col(int step) const { return d_index_ + col_off_[static_cast<std::size_t>(step)]; }
+
+std::size_t DevicePlan::workspace_bytes(int batch, long length, const ProcessorSet& procs) const {
+  std::size_t m = 256;
+  for (const StepIndex& st : rd_.steps) {
+    m = std::max(m, step_ws_bytes(st.type, st.store_end - st.store_begin, batch, length, procs));
+  }
+  return m;
+}
+
+int DevicePlan::kernels_per_render(int, long) const {
+  int k = 0;
+  for (const StepIndex& st : rd_.steps) k += step_kernels(st.type);
+  return k;
+}
+
+void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const double* const* param_tables, float* arena,
+                  int batch, long length, void* workspace, std::size_t workspace_bytes, cudaStream_t stream,
+                  cudaEvent_t* step_events) {
+  const RenderData& rd = plan.data();
+  if (workspace_bytes < plan.workspace_bytes(batch, length, procs)) fail("render_arena: workspace too small");
+  const long rowstride = static_cast<long>(batch) * 2 * length;
+  for (int r : plan.zero_rows()) {
+    cuda_check(cudaMemsetAsync(arena + r * rowstride, 0, sizeof(float) * rowstride, stream), "memset");
+  }
+  for (std::size_t k = 0; k < rd.steps.size(); ++k) {
+    const StepIndex& st = rd.steps[k];
+    const int width = param_width(st.type);
+    mgb::StepArgs a{};
+    a.src = arena;
+    a.dst = arena + st.store_begin * rowstride;
+    a.row_ptr = plan.row_ptr(static_cast<int>(k));
+    a.col = plan.col(static_cast<int>(k));
+    a.params = nullptr;
+    if (width > 0) {
+      const double* table = param_tables ? param_tables[static_cast<int>(st.type)] : nullptr;
+      if (!table) fail("render: missing parameter table for " + tname(st.type));
+      a.params = table + static_cast<long>(st.param_begin) * width;
+    }
+    a.slots = st.store_end - st.store_begin;
+    a.batch = batch;
+    a.length = length;
+    a.rowstride = rowstride;
+    if (step_events) cuda_check(cudaEventRecord(step_events[2 * k], stream), "event");
+    run_step(st.type, a, procs, workspace, stream);
+    if (step_events) cuda_check(cudaEventRecord(step_events[2 * k + 1], stream), "event");
+  }
+  cuda_check(cudaGetLastError(), "render_arena launch");
+}
+
+// ---- host-buffer API ----------------------------------------------------------------------
+
+void ProcessorSet::process_device(NodeType type, const float* in, float* out, int slots, int batch, long length,
+                                  const double* params, int param_offset, cudaStream_t stream) const {
+  // Identity CSR: slot s reads input row s.
+  Engine& e = engine_for(dev_->device);
+  std::vector<int> idx(static_cast<std::size_t>(2 * slots + 1));
+  for (int s = 0; s <= slots; ++s) idx[static_cast<std::size_t>(s)] = s;
+  for (int s = 0; s < slots; ++s) idx[static_cast<std::size_t>(slots + 1 + s)] = s;
+  const std::size_t ws_bytes = std::max<std::size_t>(256, step_ws_bytes(type, slots, batch, length, *this));
+  char* aux = static_cast<char*>(e.aux.ensure(align256(sizeof(int) * idx.size()) + ws_bytes));
+  cuda_check(cudaMemcpyAsync(aux, idx.data(), sizeof(int) * idx.size(), cudaMemcpyHostToDevice, stream), "H2D csr");
+  mgb::StepArgs a{};
+  a.src = in;
+  a.dst = out;
+  a.row_ptr = reinterpret_cast<const int*>(aux);
+  a.col = reinterpret_cast<const int*>(aux) + slots + 1;
+  a.params = params ? params + static_cast<long>(param_offset) * param_width(type) : nullptr;
+  a.slots = slots;
+  a.batch = batch;
+  a.length = length;
+  a.rowstride = static_cast<long>(batch) * 2 * length;
+  run_step(type, a, *this, aux + align256(sizeof(int) * idx.size()), stream);
+  cuda_check(cudaGetLastError(), "process launch");
+  // The CSR lives in a reused staging buffer: finish before it can be overwritten.
+  cuda_check(cudaStreamSynchronize(stream), "process");
+}
+
+void ProcessorSet::process(NodeType type, const double* in, double* out, int slots, int batch, long length,
+                           const ParamMatrix* params, int param_offset) const {
+  const int width = param_width(type);
+  const std::string name = tname(type);
+  if (width > 0) {
+    if (params == nullptr) fail(name + ": missing parameters");
+    if (params->cols != width) fail(name + ": parameter row width mismatch");
+    if (param_offset < 0 || param_offset + slots > params->rows) fail(name + ": parameter rows out of range");
+    for (int s = 0; s < slots; ++s) check_param_row(type, params->row(param_offset + s));
+  }
+  if (slots <= 0 || batch <= 0 || length <= 0) return;
+  Engine& e = engine_for(dev_->device);
+  const std::size_t n = static_cast<std::size_t>(slots) * batch * 2 * static_cast<std::size_t>(length);
+  auto* stage = static_cast<double*>(e.staging.ensure(sizeof(double) * n));
+  auto* io = static_cast<float*>(e.arena.ensure(sizeof(float) * 2 * n));
+  double* d_par = nullptr;
+  if (width > 0) {
+    d_par = static_cast<double*>(e.params.ensure(sizeof(double) * static_cast<std::size_t>(slots) * width));
+    cuda_check(cudaMemcpyAsync(d_par, params->row(param_offset).data(), sizeof(double) * static_cast<std::size_t>(slots) * width,
+                               cudaMemcpyHostToDevice, e.stream), "H2D params");
+  }
+  cuda_check(cudaMemcpyAsync(stage, in, sizeof(double) * n, cudaMemcpyHostToDevice, e.stream), "H2D in");
+  mgb::launch_f64_to_f32(stage, io, static_cast<long>(n), e.stream);
+  process_device(type, io, io + n, slots, batch, length, d_par, 0, e.stream);
+  mgb::launch_f32_to_f64(io + n, stage, static_cast<long>(n), e.stream);
+  cuda_check(cudaMemcpyAsync(out, stage, sizeof(double) * n, cudaMemcpyDeviceToHost, e.stream), "D2H out");
+  cuda_check(cudaStreamSynchronize(e.stream), "process");
+}
+
+AudioBuffer ProcessorSet::process_node(NodeType type, const AudioBuffer& input, std::span<const double> params) const {
+  if (input.channels != 2) fail("process_node: processors are stereo (2 channels)");
+  const int width = param_width(type);
+  if (static_cast<int>(params.size()) != width) {
+    fail(tname(type) + ": expected " + std::to_string(width) + " parameters");
+  }
+  AudioBuffer out(input.batch, 2, input.length, input.sample_rate);
+  ParamMatrix table(width > 0 ? 1 : 0, width);
+  if (width > 0) std::copy(params.begin(), params.end(), table.row(0).begin());
+  process(type, input.samples.data(), out.samples.data(), 1, input.batch, input.length, width > 0 ? &table : nullptr, 0);
+  return out;
+}
+
+std::pair<std::vector<double>, std::vector<double>> ProcessorSet::reverb_kernel(std::span<const double> params) const {
+  Engine& e = engine_for(dev_->device);
+  const long len = reverb_length_;
+  auto* d_row = static_cast<double*>(e.params.ensure(sizeof(double) * param_width(NodeType::Reverb)));
+  auto* d_ir = static_cast<float2*>(e.arena.ensure(sizeof(float2) * static_cast<std::size_t>(len) + 16));
+  cuda_check(cudaMemcpyAsync(d_row, params.data(), sizeof(double) * param_width(NodeType::Reverb), cudaMemcpyHostToDevice, e.stream), "H2D");
+  mgb::launch_reverb_ir(d_row, 1, reverb_const(*this), d_ir, len, e.stream);
+  std::vector<float> h(static_cast<std::size_t>(2 * len));
+  cuda_check(cudaMemcpyAsync(h.data(), d_ir, sizeof(float2) * static_cast<std::size_t>(len), cudaMemcpyDeviceToHost, e.stream), "D2H");
+  cuda_check(cudaStreamSynchronize(e.stream), "reverb_kernel");
+  std::vector<double> l(static_cast<std::size_t>(len)), r(static_cast<std::size_t>(len));
+  for (long i = 0; i < len; ++i) {
+    l[static_cast<std::size_t>(i)] = h[static_cast<std::size_t>(2 * i)];
+    r[static_cast<std::size_t>(i)] = h[static_cast<std::size_t>(2 * i + 1)];
+  }
+  return {std::move(l), std::move(r)};
+}
+
+std::vector<double> ProcessorSet::delay_kernel(std::span<const double> params, int channel) const {
+  Engine& e = engine_for(dev_->device);
+  const long span = delay_span_;
+  auto* d_row = static_cast<double*>(e.params.ensure(sizeof(double) * param_width(NodeType::Delay)));
+  auto* d_ir = static_cast<float2*>(e.arena.ensure(sizeof(float2) * static_cast<std::size_t>(span) + 16));
+  cuda_check(cudaMemcpyAsync(d_row, params.data(), sizeof(double) * param_width(NodeType::Delay), cudaMemcpyHostToDevice, e.stream), "H2D");
+  mgb::launch_delay_ir(d_row, 1, delay_const(*this), d_ir, span, e.stream);
+  std::vector<float> h(static_cast<std::size_t>(2 * span));
+  cuda_check(cudaMemcpyAsync(h.data(), d_ir, sizeof(float2) * static_cast<std::size_t>(span), cudaMemcpyDeviceToHost, e.stream), "D2H");
+  cuda_check(cudaStreamSynchronize(e.stream), "delay_kernel");
+  std::vector<double> k(static_cast<std::size_t>(span));
+  for (long i = 0; i < span; ++i) k[static_cast<std::size_t>(i)] = h[static_cast<std::size_t>(2 * i + channel)];
+  return k;
+}
+
+std::vector<long> ProcessorSet::delay_positions(std::span<const double> params, int channel) const {
+  // processors.cpp:189-208 (fp64, same libm on the host); the device kernel mirrors it.
+  std::vector<long> pos(kDelayTapsPerChannel, -1);
+  for (int m = 0; m < kDelayTapsPerChannel; ++m) {
+    const std::size_t base = static_cast<std::size_t>(channel * kDelayTapsPerChannel + m) * kDelayTapStride;
+    double mx = params[base + 2];
+    for (int k = 1; k < kDelayFirBins; ++k) mx = std::max(mx, params[base + 2 + static_cast<std::size_t>(k)]);
+    if (mx <= kDelayDisabledLogMag) continue;
+    const double frac = -std::atan2(params[base + 1], params[base]) / (2.0 * std::numbers::pi);
+    long d = std::lround(frac * static_cast<double>(delay_span_));
+    d %= delay_span_;
+    if (d < 0) d += delay_span_;
+    const long lo = static_cast<long>(m) * delay_window_;
+    const long hi = std::min(static_cast<long>(m + 1) * delay_window_, delay_span_) - 1;
+    pos[static_cast<std::size_t>(m)] = std::clamp(d, lo, hi);
+  }
+  return pos;
+}
+
+void render_host(const RenderData& rd, const ProcessorSet& procs, const ParamStore& params,
+                 const double* const* sources, int batch, long length, double* const* outputs,
+                 double* const* intermediates, const DevicePlan* cached_plan) {
+  // Per-step parameter checks, in step order (render.cpp:49-56, processors.cpp:232-247).
+  for (const StepIndex& st : rd.steps) {
+    const int width = param_width(st.type);
+    if (width == 0) continue;
+    auto it = params.tables.find(st.type);
+    if (it == params.tables.end()) fail("render: missing parameter table for " + tname(st.type));
+    const ParamMatrix& m = it->second;
+    const int slots = st.store_end - st.store_begin;
+    if (m.cols != width) fail(tname(st.type) + ": parameter row width mismatch");
+    if (st.param_begin < 0 || st.param_begin + slots > m.rows) fail(tname(st.type) + ": parameter rows out of range");
+    for (int s = 0; s < slots; ++s) check_param_row(st.type, m.row(st.param_begin + s));
+  }
+
+  Engine& e = engine_for(procs.device().device);
+  const long stride = static_cast<long>(batch) * 2 * length;
+  const std::size_t rows = static_cast<std::size_t>(rd.buffer_rows);
+  std::unique_ptr<DevicePlan> own;
+  if (!cached_plan) own = std::make_unique<DevicePlan>(rd);
+  const DevicePlan& plan = cached_plan ? *cached_plan : *own;
+  const std::size_t ws_bytes = plan.workspace_bytes(batch, length, procs);
+  auto* arena = static_cast<float*>(e.arena.ensure(sizeof(float) * rows * stride + 16));
+  void* ws = e.ws.ensure(ws_bytes);
+
+  // Parameters: every table, one upload.
+  std::size_t total = 0;
+  for (const auto& [t, m] : params.tables) total += m.values.size();
+  auto* d_par = static_cast<double*>(e.params.ensure(sizeof(double) * (total + 1)));
+  const double* tables[kNumNodeTypes] = {};
+  std::vector<double> host;
+  host.reserve(total);
+  for (const auto& [t, m] : params.tables) {
+    tables[static_cast<int>(t)] = d_par + host.size();
+    host.insert(host.end(), m.values.begin(), m.values.end());
+  }
+  if (!host.empty()) {
+    cuda_check(cudaMemcpyAsync(d_par, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice, e.stream), "H2D params");
+  }
+  // Sources (double, caller memory) -> staging -> fp32 arena rows [0, K).
+  const std::size_t n_src = static_cast<std::size_t>(rd.num_inputs) * stride;
+  auto* stage = static_cast<double*>(e.staging.ensure(sizeof(double) * std::max<std::size_t>(n_src, rows * stride) + 16));
+  for (int k = 0; k < rd.num_inputs; ++k) {
+    cuda_check(cudaMemcpyAsync(stage + static_cast<std::size_t>(k) * stride, sources[k], sizeof(double) * stride,
+                               cudaMemcpyHostToDevice, e.stream), "H2D sources");
+  }
+  mgb::launch_f64_to_f32(stage, arena, static_cast<long>(n_src), e.stream);
+  render_arena(plan, procs, tables, arena, batch, length, ws, ws_bytes, e.stream);
+
+  // Rows back to double on the device, then straight into the caller's buffers.
+  const long first = intermediates ? 0 : rd.output_begin;
+  mgb::launch_f32_to_f64(arena + first * stride, stage, (rd.buffer_rows - first) * stride, e.stream);
+  auto row_of = [&](long r) { return stage + static_cast<std::size_t>(r - first) * stride; };
+  for (int r = rd.output_begin; r < rd.buffer_rows; ++r) {
+    cuda_check(cudaMemcpyAsync(outputs[r - rd.output_begin], row_of(r), sizeof(double) * stride, cudaMemcpyDeviceToHost,
+                               e.stream), "D2H outputs");
+  }
+  for (int r = 0; intermediates && r < rd.buffer_rows; ++r) {
+    cuda_check(cudaMemcpyAsync(intermediates[r], row_of(rd.sigma[static_cast<std::size_t>(r)]), sizeof(double) * stride,
+                               cudaMemcpyDeviceToHost, e.stream), "D2H intermediates");
+  }
+  cuda_check(cudaStreamSynchronize(e.stream), "render");
+}
+
+RenderResult render(const RenderData& rd, const ProcessorSet& procs, const ParamStore& params,
+                    const std::vector<AudioBuffer>& sources, const RenderOptions& options) {
+  // render.cpp:17-30
+  if (static_cast<int>(sources.size()) != rd.num_inputs) {
+    fail("render: expected " + std::to_string(rd.num_inputs) + " sources, got " + std::to_string(sources.size()));
+  }
+  if (sources.empty()) fail("render: graph has no input nodes to take signal shape from");
+  const int batch = sources[0].batch;
+  const long length = sources[0].length;
+  const double fs = sources[0].sample_rate;
+  for (const AudioBuffer& s : sources) {
+    if (s.channels != 2) fail("render: sources must be stereo");
+    if (s.batch != batch || s.length != length || s.sample_rate != fs) {
+      fail("render: sources must share batch, length and sample rate");
+    }
+  }
+  RenderResult result;
+  std::vector<const double*> src;
+  for (const AudioBuffer& s : sources) src.push_back(s.samples.data());
+  std::vector<double*> outs, inter;
+  for (int r = rd.output_begin; r < rd.buffer_rows; ++r) {
+    result.outputs.emplace_back(batch, 2, length, fs);
+  }
+  for (auto& o : result.outputs) outs.push_back(o.samples.data());
+  if (options.keep_intermediates) {
+    for (int r = 0; r < rd.buffer_rows; ++r) result.intermediates.emplace_back(batch, 2, length, fs);
+    for (auto& o : result.intermediates) inter.push_back(o.samples.data());
+  }
+  render_host(rd, procs, params, src.data(), batch, length, outs.data(), options.keep_intermediates ? inter.data() : nullptr,
+              nullptr);
+  return result;
+}
+
+RenderResult render(const RenderData& rd, const ProcessorSet& procs, const std::vector<AudioBuffer>& sources,
+                    const RenderOptions& options) {
+  return render(rd, procs, rd.flat.params, sources, options);
+}
+
+}  // namespace mixgraph

@@ -1,0 +1,521 @@
+// K8/K9 (reverb) and K10/K11 (multitap delay): long causal convolutions.
+//
+// Reference: the reverb step builds a stereo impulse response from a masked noise STFT
+// (`processors.cpp:162-187`, istft `dsp.cpp:165-190`) and the delay step builds a sparse
+// multitap kernel (`processors.cpp:189-227`); both then run fft_convolve(Causal) per
+// (batch, channel) with a zero-padded next_pow2(L + taps - 1) FFT (`dsp.cpp:64-86`), which
+// re-transforms the kernel on every call.
+//
+// Device plan per step (N = 2^a >= L + taps - 1, N = N1 * N2):
+//   ir build      -> packed kernel h = h_L + i h_R (one complex signal per node)
+//   cols_fwd<K>   -> column FFTs of h (length N1, stride N2) x four-step twiddle
+//   rows<SPEC>    -> row FFTs: P = FFT_N(h) in the transposed (k1 + N1*k2) order
+//   cols_fwd<S>   -> same for the signal x = u_L + i u_R, gathered from the arena (Eq. 1b)
+//   rows<CONV>    -> row FFTs of x, channel split by conjugate pairing of rows k1 / N1-k1,
+//                    Z = X_L H_L + i X_R H_R, inverse row FFTs x inverse twiddle
+//   cols_inv      -> inverse column FFTs, real part -> left, imag part -> right, store the
+//                    first L samples into the arena.
+// The spectrum stays in four-step (transposed) order: forward and inverse are mirror
+// images, so no transpose pass is ever made. Each pass is one smem-resident batch of FFTs.
+#include <cmath>
+#include <stdexcept>
+
+#include "fft_smem.cuh"
+#include "launch.hpp"
+
+namespace mgb {
+
+namespace {
+
+constexpr int kColElems = 8192;  // complex elements per column tile (64 KiB)
+constexpr int kColThreads = 512;
+
+inline std::size_t align256(std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255); }
+
+struct ConvWs {
+  float2* ir;
+  float2* P;
+  float2* X;
+};
+
+ConvWs carve(void* ws, const ConvGeom& g, int slots, long taps) {
+  char* p = static_cast<char*>(ws);
+  ConvWs w;
+  w.ir = reinterpret_cast<float2*>(p);
+  p += align256(sizeof(float2) * static_cast<std::size_t>(slots) * taps);
+  w.P = reinterpret_cast<float2*>(p);
+  p += align256(sizeof(float2) * static_cast<std::size_t>(slots) * g.n);
+  w.X = reinterpret_cast<float2*>(p);
+  return w;
+}
+
+enum class ColSrc { Kernel, Signal };
+
+// ---- pass 1: column FFTs (forward) ------------------------------------------------------
+// grid (N2 / C, items); item = slot (kernel) or slot*B + b (signal).
+template <int LN1, ColSrc SRC>
+__global__ void __launch_bounds__(kColThreads) cols_fwd(StepArgs a, const float2* ir, long taps, int log_n,
+                                                        float2* out) {
+  constexpr int N1 = 1 << LN1;
+  constexpr int C = kColElems / N1;
+  constexpr int FS = N1 + 1;
+  extern __shared__ float2 tile[];
+  const int log_n2 = log_n - LN1;
+  const long N2 = 1L << log_n2;
+  const long N = 1L << log_n;
+  const int item = blockIdx.y;
+  const long col0 = static_cast<long>(blockIdx.x) * C;
+  int slot = item, b = 0, e0 = 0, e1 = 0;
+  long len = taps;
+  if constexpr (SRC == ColSrc::Signal) {
+    slot = item / a.batch;
+    b = item - slot * a.batch;
+    e0 = __ldg(a.row_ptr + slot);
+    e1 = __ldg(a.row_ptr + slot + 1);
+    len = a.length;
+  }
+  for (int idx = threadIdx.x; idx < kColElems; idx += kColThreads) {
+    const int c = idx % C, n1 = idx / C;
+    const long n = static_cast<long>(n1) * N2 + col0 + c;
+    float2 v = make_float2(0.f, 0.f);
+    if (n < len) {
+      if constexpr (SRC == ColSrc::Signal) v = gather2(a, e0, e1, b, n);
+      else v = __ldg(ir + static_cast<long>(item) * taps + n);
+    }
+    tile[c * FS + n1] = v;
+  }
+  __syncthreads();
+  fft_pow2<LN1, C, kColThreads, -1>(tile, FS);
+  float2* o = out + static_cast<long>(item) * N;
+  const float inv_n = 2.f / static_cast<float>(N);
+  for (int idx = threadIdx.x; idx < kColElems; idx += kColThreads) {
+    const int c = idx % C, k1 = idx / C;
+    const long n2 = col0 + c;
+    const float2 w = expi_pi(-static_cast<float>(n2 * k1) * inv_n);
+    o[static_cast<long>(k1) * N2 + n2] = cmul(tile[c * FS + k1], w);
+  }
+}
+
+// ---- pass 3 (last): inverse column FFTs, store into the arena --------------------------
+template <int LN1>
+__global__ void __launch_bounds__(kColThreads) cols_inv(StepArgs a, int log_n, const float2* X) {
+  constexpr int N1 = 1 << LN1;
+  constexpr int C = kColElems / N1;
+  constexpr int FS = N1 + 1;
+  extern __shared__ float2 tile[];
+  const long N2 = 1L << (log_n - LN1);
+  const long N = 1L << log_n;
+  const int item = blockIdx.y;
+  const int slot = item / a.batch, b = item - slot * a.batch;
+  const long col0 = static_cast<long>(blockIdx.x) * C;
+  const float2* x = X + static_cast<long>(item) * N;
+  for (int idx = threadIdx.x; idx < kColElems; idx += kColThreads) {
+    const int c = idx % C, k1 = idx / C;
+    tile[c * FS + k1] = x[static_cast<long>(k1) * N2 + col0 + c];
+  }
+  __syncthreads();
+  fft_pow2<LN1, C, kColThreads, +1>(tile, FS);
+  float* yl = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length;
+  float* yr = yl + a.length;
+  for (int idx = threadIdx.x; idx < kColElems; idx += kColThreads) {
+    const int c = idx % C, n1 = idx / C;
+    const long n = static_cast<long>(n1) * N2 + col0 + c;
+    if (n < a.length) {
+      const float2 v = tile[c * FS + n1];
+      yl[n] = v.x;
+      yr[n] = v.y;
+    }
+  }
+}
+
+// ---- pass 2: row FFTs ---------------------------------------------------------------------
+__device__ __forceinline__ float2 zmix(float2 xk, float2 xm, float2 pk, float2 pm, float s) {
+  // xm = conj(X[N-k]), pm = conj(P[N-k]):  Z = ((xk+xm)(pk+pm) - i (xk-xm)(pk-pm)) / 4
+  const float2 s1 = cmul(cadd(xk, xm), cadd(pk, pm));
+  const float2 s2 = cmul(csub(xk, xm), csub(pk, pm));
+  return make_float2((s1.x + s2.y) * s, (s1.y - s2.x) * s);
+}
+
+template <int LN2>
+constexpr int row_threads() {
+  constexpr int t = (2 << LN2) / 8;
+  return t < 64 ? 64 : (t > 512 ? 512 : t);
+}
+
+// Forward row FFTs of the packed kernel; one row per CTA. grid (N1, slots)
+template <int LN2>
+__global__ void __launch_bounds__(row_threads<LN2>()) rows_spec(int log_n, float2* P) {
+  constexpr int N2 = 1 << LN2;
+  constexpr int NT = row_threads<LN2>();
+  extern __shared__ float2 row[];
+  const long N = 1L << log_n;
+  float2* p = P + static_cast<long>(blockIdx.y) * N + static_cast<long>(blockIdx.x) * N2;
+  for (int i = threadIdx.x; i < N2; i += NT) row[i] = p[i];
+  __syncthreads();
+  fft_pow2<LN2, 1, NT, -1>(row, N2);
+  for (int i = threadIdx.x; i < N2; i += NT) p[i] = row[i];
+}
+
+// Signal rows k1 = r and N1 - r together: forward FFTs, channel-split product with the
+// kernel spectrum, inverse FFTs, inverse four-step twiddle. grid (N1/2 + 1, slots*B)
+template <int LN2>
+__global__ void __launch_bounds__(row_threads<LN2>()) rows_conv(int log_n, int batch, float2* X, const float2* P) {
+  constexpr int N2 = 1 << LN2;
+  constexpr int NT = row_threads<LN2>();
+  extern __shared__ float2 rows[];  // [2][N2]
+  const long N = 1L << log_n;
+  const int N1 = static_cast<int>(N >> LN2);
+  const int item = blockIdx.y;
+  const int slot = item / batch;
+  const int ra = blockIdx.x, rb = (N1 - ra) & (N1 - 1);
+  const bool self = ra == rb;
+  float2* xa = X + static_cast<long>(item) * N + static_cast<long>(ra) * N2;
+  float2* xb = X + static_cast<long>(item) * N + static_cast<long>(rb) * N2;
+  const float2* pa = P + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
+  const float2* pb = P + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
+  for (int i = threadIdx.x; i < N2; i += NT) {
+    rows[i] = xa[i];
+    rows[N2 + i] = xb[i];
+  }
+  __syncthreads();
+  fft_pow2<LN2, 2, NT, -1>(rows, N2);
+  const float s = 0.25f / static_cast<float>(N);
+  for (int k = threadIdx.x; k < N2; k += NT) {
+    const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
+    if (self && kb < k) continue;
+    const float2 xk = rows[k], xo = rows[N2 + kb];
+    const float2 pk = __ldg(pa + k), po = __ldg(pb + kb);
+    const float2 zk = zmix(xk, cconj(xo), pk, cconj(po), s);
+    const float2 zo = zmix(xo, cconj(xk), po, cconj(pk), s);
+    rows[k] = zk;
+    rows[N2 + kb] = zo;
+    if (self) rows[kb] = zo;
+  }
+  __syncthreads();
+  fft_pow2<LN2, 2, NT, +1>(rows, N2);
+  const float inv_n = 2.f / static_cast<float>(N);
+  for (int i = threadIdx.x; i < N2; i += NT) {
+    xa[i] = cmul(rows[i], expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n));
+    if (!self) xb[i] = cmul(rows[N2 + i], expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n));
+  }
+}
+
+// ---- dispatch -----------------------------------------------------------------------------
+template <int LN1>
+void cols_fwd_t(ColSrc src, const StepArgs& a, const float2* ir, long taps, const ConvGeom& g, int items,
+                float2* out, cudaStream_t s) {
+  constexpr int C = kColElems / (1 << LN1);
+  constexpr int smem = C * ((1 << LN1) + 1) * 8;
+  const dim3 grid(static_cast<unsigned>((1L << g.log_n2) / C), static_cast<unsigned>(items));
+  if (src == ColSrc::Signal) {
+    cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::Signal>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cols_fwd<LN1, ColSrc::Signal><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out);
+  } else {
+    cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::Kernel>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cols_fwd<LN1, ColSrc::Kernel><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out);
+  }
+}
+
+template <int LN1>
+void cols_inv_t(const StepArgs& a, const ConvGeom& g, const float2* X, cudaStream_t s) {
+  constexpr int C = kColElems / (1 << LN1);
+  constexpr int smem = C * ((1 << LN1) + 1) * 8;
+  const dim3 grid(static_cast<unsigned>((1L << g.log_n2) / C), static_cast<unsigned>(a.slots * a.batch));
+  cudaFuncSetAttribute(cols_inv<LN1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cols_inv<LN1><<<grid, kColThreads, smem, s>>>(a, g.log_n, X);
+}
+
+template <int LN2>
+void rows_spec_t(const ConvGeom& g, int slots, float2* P, cudaStream_t s) {
+  const dim3 grid(static_cast<unsigned>(1L << g.log_n1), static_cast<unsigned>(slots));
+  rows_spec<LN2><<<grid, row_threads<LN2>(), (1 << LN2) * 8, s>>>(g.log_n, P);
+}
+
+template <int LN2>
+void rows_conv_t(const ConvGeom& g, int items, int batch, float2* X, const float2* P, cudaStream_t s) {
+  constexpr int smem = 2 * (1 << LN2) * 8;
+  cudaFuncSetAttribute(rows_conv<LN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(items));
+  rows_conv<LN2><<<grid, row_threads<LN2>(), smem, s>>>(g.log_n, batch, X, P);
+}
+
+#define MGB_DISPATCH_LN(var, FN, ...)                  \
+  switch (var) {                                       \
+    case 6: FN<6>(__VA_ARGS__); break;                 \
+    case 7: FN<7>(__VA_ARGS__); break;                 \
+    case 8: FN<8>(__VA_ARGS__); break;                 \
+    case 9: FN<9>(__VA_ARGS__); break;                 \
+    case 10: FN<10>(__VA_ARGS__); break;               \
+    case 11: FN<11>(__VA_ARGS__); break;               \
+    case 12: FN<12>(__VA_ARGS__); break;               \
+    default: throw std::invalid_argument("fft convolution size out of range"); \
+  }
+
+// Spectrum of the packed kernels already written to w.ir, then the signal convolution.
+void run_conv(const StepArgs& a, const ConvGeom& g, const ConvWs& w, long taps, cudaStream_t s) {
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Kernel, a, w.ir, taps, g, a.slots, w.P, s);
+  MGB_DISPATCH_LN(g.log_n2, rows_spec_t, g, a.slots, w.P, s);
+  if (a.batch == 0 || a.length == 0) return;
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, a, nullptr, 0, g, a.slots * a.batch, w.X, s);
+  MGB_DISPATCH_LN(g.log_n2, rows_conv_t, g, a.slots * a.batch, a.batch, w.X, w.P, s);
+  MGB_DISPATCH_LN(g.log_n1, cols_inv_t, a, g, w.X, s);
+}
+
+// ---- reverb impulse response (masked noise STFT -> ISTFT) ----------------------------------
+constexpr int kRevBins = 193;      // kReverbStftLength / 2 + 1
+constexpr int kRevParamBins = 192;
+constexpr int kRevFpc = 8;         // output hops per CTA
+constexpr int kRevThreads = 256;
+
+// grid (ceil(frames / kRevFpc), slots)
+__global__ void __launch_bounds__(kRevThreads) reverb_ir(const double* params, ReverbConst rc, float2* ir,
+                                                         long ir_stride) {
+  __shared__ float2 fr[(kRevFpc + 1) * 384];
+  __shared__ float gain[2][kRevFpc + 1][kRevBins];
+  const int slot = blockIdx.y;
+  const double* row = params + static_cast<long>(slot) * 4 * kRevParamBins;
+  const int m_first = blockIdx.x * kRevFpc - 1;
+  for (int idx = threadIdx.x; idx < 2 * (kRevFpc + 1) * kRevBins; idx += kRevThreads) {
+    const int which = idx / ((kRevFpc + 1) * kRevBins);
+    const int rem = idx - which * (kRevFpc + 1) * kRevBins;
+    const int f = rem / kRevBins, k = rem - f * kRevBins;
+    const int m = m_first + f;
+    const int bin = k < kRevParamBins ? k : kRevParamBins - 1;
+    const double* color = row + which * 2 * kRevParamBins;
+    gain[which][f][k] = (m < 0 || m >= rc.frames) ? 0.f : static_cast<float>(exp(color[bin] + m * color[kRevParamBins + bin]));
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < (kRevFpc + 1) * 384; idx += kRevThreads) {
+    const int f = idx / 384, k = idx - f * 384;
+    const int m = m_first + f;
+    float2 z = make_float2(0.f, 0.f);
+    if (m >= 0 && m < rc.frames) {
+      const bool upper = k > 192;
+      const int kk = upper ? 384 - k : k;
+      float2 M = cscale(rc.stft_mid[static_cast<long>(m) * kRevBins + kk], gain[0][f][kk]);
+      float2 S = cscale(rc.stft_side[static_cast<long>(m) * kRevBins + kk], gain[1][f][kk]);
+      if (upper) {
+        M = cconj(M);
+        S = cconj(S);
+      }
+      z = make_float2(M.x - S.y, M.y + S.x);  // M + i S: both inverse transforms are real
+    }
+    fr[idx] = z;
+  }
+  __syncthreads();
+  fft_384<kRevFpc + 1, kRevThreads, +1>(fr, 384);
+  const long i0 = static_cast<long>(blockIdx.x) * kRevFpc * 192;
+  for (int t = threadIdx.x; t < kRevFpc * 192; t += kRevThreads) {
+    const long i = i0 + t;
+    if (i >= rc.length) break;
+    const int o = t % 192;
+    const int f1 = t / 192 + 1;  // local frame starting in this hop
+    float2 v = fr[f1 * 384 + o];
+    double cover;
+    {
+      double sn, cs;
+      sincospi(2.0 * o / 384.0, &sn, &cs);
+      cover = 0.5 - 0.5 * cs;
+    }
+    if (i >= 192) {
+      const float2 u = fr[(f1 - 1) * 384 + o + 192];
+      v = cadd(v, u);
+      double sn, cs;
+      sincospi(2.0 * (o + 192) / 384.0, &sn, &cs);
+      cover += 0.5 - 0.5 * cs;
+    }
+    const float sc = cover > 1e-8 ? static_cast<float>(1.0 / (384.0 * cover)) : 0.f;
+    const float mid = v.x * sc, side = v.y * sc;
+    ir[static_cast<long>(slot) * ir_stride + i] = make_float2(0.5f * (mid + side), 0.5f * (mid - side));
+  }
+}
+
+// ---- multitap delay kernel -------------------------------------------------------------------
+constexpr int kTaps = 40;       // 2 channels x 20
+constexpr int kTapStride = 22;  // [re, im, 20 log-mags]
+constexpr int kFir = 39;
+constexpr int kFirHalf = 19;
+
+// grid (slots); ir[slot] must be zero on [0, span).
+__global__ void __launch_bounds__(1024) delay_ir(const double* params, DelayConst dc, float2* ir, long ir_stride) {
+  __shared__ long long pos[kTaps];
+  __shared__ double mag[kTaps][20];
+  __shared__ double cos39[kFir];
+  __shared__ float coef[kTaps][kFir];
+  const int slot = blockIdx.x;
+  const double* row = params + static_cast<long>(slot) * kTaps * kTapStride;
+  const int t = threadIdx.x;
+  if (t < kTaps) {
+    // processors.cpp:189-208 in fp64: disabled taps, angle -> grid delay, window clamp.
+    const double* tap = row + t * kTapStride;
+    double mx = tap[2];
+    for (int k = 1; k < 20; ++k) mx = fmax(mx, tap[2 + k]);
+    long long d = -1;
+    if (!(mx <= -60.0)) {
+      const int m = t % 20;
+      const double frac = -atan2(tap[1], tap[0]) / (2.0 * 3.14159265358979323846);
+      d = llround(frac * static_cast<double>(dc.span));
+      d %= dc.span;
+      if (d < 0) d += dc.span;
+      const long long lo = static_cast<long long>(m) * dc.window;
+      const long long hi = min(static_cast<long long>(m + 1) * dc.window, static_cast<long long>(dc.span)) - 1;
+      d = d < lo ? lo : (d > hi ? hi : d);
+    }
+    pos[t] = d;
+  }
+  if (t < kTaps * 20) mag[t / 20][t % 20] = exp(row[(t / 20) * kTapStride + 2 + t % 20]);
+  if (t < kFir) {
+    double s, c;
+    sincospi(2.0 * t / kFir, &s, &c);
+    cos39[t] = c;
+  }
+  __syncthreads();
+  // 39-tap zero-phase FIR per tap (dsp.cpp:106-136 as the exact cosine sum).
+  for (int q = t; q < kTaps * kFir; q += blockDim.x) {
+    const int tap = q / kFir, n = q % kFir;
+    const int j = n >= kFirHalf ? n - kFirHalf : kFirHalf - n;
+    double acc = 0.0;
+    int idx = 0;
+    for (int k = 0; k < kFir; ++k) {
+      acc = fma(mag[tap][k <= kFirHalf ? k : kFir - k], cos39[idx], acc);
+      idx += j;
+      if (idx >= kFir) idx -= kFir;
+    }
+    double s, c;
+    sincospi(2.0 * n / (kFir - 1), &s, &c);
+    coef[tap][n] = static_cast<float>((0.5 - 0.5 * c) * acc / kFir);
+  }
+  __syncthreads();
+  // Scatter in tap order so overlapping FIRs accumulate deterministically.
+  float2* h = ir + static_cast<long>(slot) * ir_stride;
+  for (int m = 0; m < 20; ++m) {
+    if (t < 2 * kFir) {
+      const int c = t / kFir, n = t % kFir;
+      const int tap = c * 20 + m;
+      const long long d = pos[tap];
+      if (d >= 0) {
+        const long long i = d + n - kFirHalf;
+        if (i >= 0 && i < dc.span) {
+          float* dstp = reinterpret_cast<float*>(h + i) + c;
+          *dstp += coef[tap][n];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---- noise STFT (ProcessorSet construction) ---------------------------------------------------
+// grid (frames): one frame per CTA, fp64 direct DFT of the periodic-Hann windowed frame.
+__global__ void __launch_bounds__(256) noise_stft(const double* noise, long length, float2* out) {
+  __shared__ double xw[384];
+  __shared__ double cs[384], sn[384];
+  const int m = blockIdx.x;
+  for (int i = threadIdx.x; i < 384; i += blockDim.x) {
+    const long idx = static_cast<long>(m) * 192 + i;
+    double s, c;
+    sincospi(2.0 * i / 384.0, &s, &c);
+    xw[i] = idx < length ? noise[idx] * (0.5 - 0.5 * c) : 0.0;
+    cs[i] = c;
+    sn[i] = s;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < kRevBins; k += blockDim.x) {
+    double re = 0.0, im = 0.0;
+    int idx = 0;
+    for (int i = 0; i < 384; ++i) {
+      re = fma(xw[i], cs[idx], re);
+      im = fma(-xw[i], sn[idx], im);
+      idx += k;
+      if (idx >= 384) idx -= 384;
+    }
+    out[static_cast<long>(m) * kRevBins + k] = make_float2(static_cast<float>(re), static_cast<float>(im));
+  }
+}
+
+__global__ void f64_to_f32(const double* in, float* out, long n) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n; i += static_cast<long>(gridDim.x) * blockDim.x) {
+    out[i] = static_cast<float>(in[i]);
+  }
+}
+
+__global__ void f32_to_f64(const float* in, double* out, long n) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n; i += static_cast<long>(gridDim.x) * blockDim.x) {
+    out[i] = static_cast<double>(in[i]);
+  }
+}
+
+unsigned grid_for(long n) {
+  long b = (n + 255) / 256;
+  if (b < 1) b = 1;
+  if (b > 148L * 16) b = 148L * 16;
+  return static_cast<unsigned>(b);
+}
+
+}  // namespace
+
+ConvGeom conv_geom(long length, long taps) {
+  const long full = length + taps - 1;
+  ConvGeom g;
+  int a = 13;  // N1 * N2 >= one column tile
+  while ((1L << a) < full) ++a;
+  if (a > 24) throw std::invalid_argument("fft convolution: signal too long (L + taps - 1 > 2^24)");
+  g.log_n = a;
+  g.log_n1 = a / 2;
+  g.log_n2 = a - a / 2;
+  g.n = 1L << a;
+  return g;
+}
+
+std::size_t conv_workspace_bytes(const ConvGeom& g, int slots, int batch, long taps) {
+  return align256(sizeof(float2) * static_cast<std::size_t>(slots) * taps) +
+         align256(sizeof(float2) * static_cast<std::size_t>(slots) * g.n) +
+         align256(sizeof(float2) * static_cast<std::size_t>(slots) * batch * g.n);
+}
+
+void launch_reverb_ir(const double* params, int slots, const ReverbConst& rc, float2* ir, long ir_stride,
+                      cudaStream_t s) {
+  if (slots == 0) return;
+  const dim3 grid(static_cast<unsigned>((rc.frames + kRevFpc - 1) / kRevFpc), static_cast<unsigned>(slots));
+  reverb_ir<<<grid, kRevThreads, 0, s>>>(params, rc, ir, ir_stride);
+}
+
+void launch_delay_ir(const double* params, int slots, const DelayConst& dc, float2* ir, long ir_stride,
+                     cudaStream_t s) {
+  if (slots == 0) return;
+  for (int i = 0; i < slots; ++i) {
+    cudaMemsetAsync(ir + static_cast<long>(i) * ir_stride, 0, sizeof(float2) * static_cast<std::size_t>(dc.span), s);
+  }
+  delay_ir<<<slots, 1024, 0, s>>>(params, dc, ir, ir_stride);
+}
+
+void launch_reverb(const StepArgs& a, const ReverbConst& rc, void* ws, cudaStream_t s) {
+  if (a.slots == 0) return;
+  const ConvGeom g = conv_geom(a.length, rc.length);
+  const ConvWs w = carve(ws, g, a.slots, rc.length);
+  launch_reverb_ir(a.params, a.slots, rc, w.ir, rc.length, s);
+  run_conv(a, g, w, rc.length, s);
+}
+
+void launch_delay(const StepArgs& a, const DelayConst& dc, void* ws, cudaStream_t s) {
+  if (a.slots == 0) return;
+  const ConvGeom g = conv_geom(a.length, dc.span);
+  const ConvWs w = carve(ws, g, a.slots, dc.span);
+  cudaMemsetAsync(w.ir, 0, sizeof(float2) * static_cast<std::size_t>(a.slots) * dc.span, s);
+  delay_ir<<<a.slots, 1024, 0, s>>>(a.params, dc, w.ir, dc.span);
+  run_conv(a, g, w, dc.span, s);
+}
+
+void launch_noise_stft(const double* noise, long length, int frames, float2* out, cudaStream_t s) {
+  noise_stft<<<frames, 256, 0, s>>>(noise, length, out);
+}
+
+void launch_f64_to_f32(const double* in, float* out, long n, cudaStream_t s) {
+  if (n > 0) f64_to_f32<<<grid_for(n), 256, 0, s>>>(in, out, n);
+}
+
+void launch_f32_to_f64(const float* in, double* out, long n, cudaStream_t s) {
+  if (n > 0) f32_to_f64<<<grid_for(n), 256, 0, s>>>(in, out, n);
+}
+
+}  // namespace mgb

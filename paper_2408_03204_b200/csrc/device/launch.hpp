@@ -1,0 +1,67 @@
+// Host-side launchers for the per-step kernels (one translation unit per kernel family).
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "step_common.cuh"
+
+namespace mgb {
+
+enum class PointOp : int { Copy = 0, Gain = 1, Imager = 2 };
+
+// Gather-sum + copy / gain / imager + store (mix, out, gain, imager steps).
+void launch_pointwise(PointOp op, const StepArgs& a, cudaStream_t s);
+
+// EQ: FIR design (fp64 cosine sum, `dsp.cpp:106-136`) -> 8192-bin zero-phase response ->
+// overlap-save convolution fused with the gather and the store.
+constexpr int kEqFft = 8192;
+constexpr int kEqHalf = 1023;
+constexpr int kEqValid = kEqFft - 2 * kEqHalf;
+void launch_eq(const StepArgs& a, float* taps_ws /*slots*2048*/, float* resp_ws /*slots*8192*/, cudaStream_t s);
+
+// Compressor / noisegate: chained (decoupled look-back) scan of the energy envelope.
+constexpr int kDynThreads = 256;
+constexpr int kDynPerThread = 16;
+constexpr int kDynTile = kDynThreads * kDynPerThread;
+std::size_t dyn_workspace_bytes(int slots, int batch, long length);
+void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double energy_floor, void* ws,
+                     cudaStream_t s);
+
+// FFT convolution with a long causal kernel (reverb, delay): four-step FFT of size N.
+struct ConvGeom {
+  int log_n = 0, log_n1 = 0, log_n2 = 0;
+  long n = 0;
+};
+ConvGeom conv_geom(long length, long taps);
+std::size_t conv_workspace_bytes(const ConvGeom& g, int slots, int batch, long taps);
+
+struct ReverbConst {
+  const float2* stft_mid;  // [frames][193]
+  const float2* stft_side;
+  int frames;
+  long length;  // reverb_length
+};
+struct DelayConst {
+  long span;
+  int window;
+};
+
+void launch_reverb(const StepArgs& a, const ReverbConst& rc, void* ws, cudaStream_t s);
+void launch_delay(const StepArgs& a, const DelayConst& dc, void* ws, cudaStream_t s);
+
+// Kernel-only entry points (for ProcessorSet::reverb_kernel / delay_kernel).
+void launch_reverb_ir(const double* params, int slots, const ReverbConst& rc, float2* ir, long ir_stride,
+                      cudaStream_t s);
+void launch_delay_ir(const double* params, int slots, const DelayConst& dc, float2* ir, long ir_stride,
+                     cudaStream_t s);
+
+// Noise STFT for the reverb (ProcessorSet construction, `processors.cpp:151-160`).
+void launch_noise_stft(const double* noise, long length, int frames, float2* out, cudaStream_t s);
+
+// Arena conversion helpers for the host-buffer API.
+void launch_f64_to_f32(const double* in, float* out, long n, cudaStream_t s);
+void launch_f32_to_f64(const float* in, double* out, long n, cudaStream_t s);
+
+}  // namespace mgb

@@ -1,0 +1,119 @@
+// K1-K4: fused gather-sum (Eq. 1b) + mix/out copy, gain, imager + arena store.
+//
+// Reference: gather `render.cpp:44-48`, store `render.cpp:59-60`, copy_slot
+// `processors.cpp:18-20`, gain_slot `:22-32` (y_c = exp(p_c) u_c), imager_slot `:34-49`
+// (m = l + r, s = exp(p) (l - r), y_l = (m + s)/2, y_r = (m - s)/2).
+// HBM-bound: per node-sample it moves 8*(deg_in + 1) bytes. One thread owns 4 consecutive
+// samples of both channels of one (slot, batch) row; float4 loads/stores when L % 4 == 0.
+#include "launch.hpp"
+
+namespace mgb {
+
+namespace {
+
+template <PointOp OP>
+__device__ __forceinline__ void apply(float& l, float& r, float g0, float g1) {
+  if constexpr (OP == PointOp::Gain) {
+    l *= g0;
+    r *= g1;
+  } else if constexpr (OP == PointOp::Imager) {
+    const float mid = l + r;
+    const float side = g0 * (l - r);
+    l = 0.5f * (mid + side);
+    r = 0.5f * (mid - side);
+  }
+}
+
+template <PointOp OP>
+__device__ __forceinline__ void coeffs(const StepArgs& a, int slot, float& g0, float& g1) {
+  g0 = g1 = 1.f;
+  if constexpr (OP == PointOp::Gain) {
+    g0 = static_cast<float>(exp(a.params[2 * slot]));
+    g1 = static_cast<float>(exp(a.params[2 * slot + 1]));
+  } else if constexpr (OP == PointOp::Imager) {
+    g0 = static_cast<float>(exp(a.params[slot]));
+  }
+}
+
+// grid.y = slot*B + b; grid.x strides over float4 groups of the row.
+template <PointOp OP>
+__global__ void __launch_bounds__(256) pointwise_vec4(StepArgs a) {
+  const int sb = blockIdx.y;
+  const int slot = sb / a.batch, b = sb - slot * a.batch;
+  const int e0 = __ldg(a.row_ptr + slot), e1 = __ldg(a.row_ptr + slot + 1);
+  float g0, g1;
+  coeffs<OP>(a, slot, g0, g1);
+  const long n4 = a.length >> 2;
+  const long boff = static_cast<long>(b) * 2 * a.length;
+  float4* outl = reinterpret_cast<float4*>(a.dst + static_cast<long>(slot) * a.rowstride + boff);
+  float4* outr = reinterpret_cast<float4*>(a.dst + static_cast<long>(slot) * a.rowstride + boff + a.length);
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n4; i += static_cast<long>(gridDim.x) * blockDim.x) {
+    float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
+    int e = e0;
+    for (; e + 1 < e1; e += 2) {  // two edges in flight
+      const float4* p0 = reinterpret_cast<const float4*>(a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff);
+      const float4* p1 = reinterpret_cast<const float4*>(a.src + static_cast<long>(__ldg(a.col + e + 1)) * a.rowstride + boff);
+      const float4 l0 = __ldg(p0 + i), r0 = __ldg(p0 + n4 + i);
+      const float4 l1 = __ldg(p1 + i), r1 = __ldg(p1 + n4 + i);
+      l = f4add(f4add(l, l0), l1);
+      r = f4add(f4add(r, r0), r1);
+    }
+    if (e < e1) {
+      const float4* p0 = reinterpret_cast<const float4*>(a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff);
+      l = f4add(l, __ldg(p0 + i));
+      r = f4add(r, __ldg(p0 + n4 + i));
+    }
+    apply<OP>(l.x, r.x, g0, g1);
+    apply<OP>(l.y, r.y, g0, g1);
+    apply<OP>(l.z, r.z, g0, g1);
+    apply<OP>(l.w, r.w, g0, g1);
+    outl[i] = l;  // default policy: the next step reads these rows back from L2
+    outr[i] = r;
+  }
+}
+
+template <PointOp OP>
+__global__ void __launch_bounds__(256) pointwise_scalar(StepArgs a) {
+  const int sb = blockIdx.y;
+  const int slot = sb / a.batch, b = sb - slot * a.batch;
+  const int e0 = __ldg(a.row_ptr + slot), e1 = __ldg(a.row_ptr + slot + 1);
+  float g0, g1;
+  coeffs<OP>(a, slot, g0, g1);
+  float* out = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length;
+  for (long n = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; n < a.length; n += static_cast<long>(gridDim.x) * blockDim.x) {
+    float2 v = gather2(a, e0, e1, b, n);
+    apply<OP>(v.x, v.y, g0, g1);
+    out[n] = v.x;
+    out[n + a.length] = v.y;
+  }
+}
+
+template <PointOp OP>
+void launch_op(const StepArgs& a, cudaStream_t s) {
+  const int rows = a.slots * a.batch;
+  if (rows == 0 || a.length == 0) return;
+  const bool vec = (a.length % 4) == 0;
+  const long items = vec ? a.length / 4 : a.length;
+  // ~2 float4 groups per thread per row keeps >= 8 loads in flight per thread at deg 1.
+  long blocks = (items + 256 * 2 - 1) / (256 * 2);
+  if (blocks < 1) blocks = 1;
+  if (blocks > 4096) blocks = 4096;
+  dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(rows));
+  if (vec) {
+    pointwise_vec4<OP><<<grid, 256, 0, s>>>(a);
+  } else {
+    pointwise_scalar<OP><<<grid, 256, 0, s>>>(a);
+  }
+}
+
+}  // namespace
+
+void launch_pointwise(PointOp op, const StepArgs& a, cudaStream_t s) {
+  switch (op) {
+    case PointOp::Copy: launch_op<PointOp::Copy>(a, s); break;
+    case PointOp::Gain: launch_op<PointOp::Gain>(a, s); break;
+    case PointOp::Imager: launch_op<PointOp::Imager>(a, s); break;
+  }
+}
+
+}  // namespace mgb

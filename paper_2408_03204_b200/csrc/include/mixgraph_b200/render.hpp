@@ -1,0 +1,154 @@
+// Batched processors and the renderer (host API over the B200 engine).
+//
+// Drop-in for `proj/include/mixgraph/processors.hpp:15-76`, `render.hpp:11-32` and
+// `audio_buffer.hpp:7-32`: same types, signatures, argument meaning and exceptions. The
+// difference is where the work runs: a ProcessorSet owns device-resident constants (the
+// reverb noise STFT) on the CUDA device current at construction, and render()/process()
+// execute every step as sm_100a kernels over one fp32 HBM arena; host buffers are
+// double, as in the reference, and converted at the boundary. There is no CPU fallback:
+// without a usable CUDA device these calls throw std::runtime_error.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <utility>
+#include <vector>
+
+#include "mixgraph_b200/schedule.hpp"
+
+typedef struct CUstream_st* cudaStream_t;
+typedef struct CUevent_st* cudaEvent_t;
+
+namespace mixgraph {
+
+struct AudioBuffer {
+  int batch = 1;
+  int channels = 2;
+  long length = 0;
+  double sample_rate = 44100.0;
+  std::vector<double> samples;  // [b][c][n]
+
+  AudioBuffer() = default;
+  AudioBuffer(int batch_, int channels_, long length_, double sample_rate_)
+      : batch(batch_), channels(channels_), length(length_), sample_rate(sample_rate_),
+        samples(static_cast<std::size_t>(batch_) * channels_ * length_, 0.0) {}
+  double* channel(int b, int c) { return samples.data() + (static_cast<std::size_t>(b) * channels + c) * length; }
+  const double* channel(int b, int c) const { return samples.data() + (static_cast<std::size_t>(b) * channels + c) * length; }
+  double& at(int b, int c, long n) { return channel(b, c)[n]; }
+  double at(int b, int c, long n) const { return channel(b, c)[n]; }
+};
+
+struct ProcessorConfig {
+  double sample_rate = 44100.0;
+  std::uint32_t reverb_seed = 0;
+  int envelope_taps = 32768;
+  double energy_floor = 1e-7;
+};
+
+struct DeviceConstants;  // engine-internal
+
+class ProcessorSet {
+ public:
+  explicit ProcessorSet(const ProcessorConfig& config = {});
+  ~ProcessorSet();
+  ProcessorSet(const ProcessorSet&) = delete;
+  ProcessorSet& operator=(const ProcessorSet&) = delete;
+
+  const ProcessorConfig& config() const { return config_; }
+  long delay_span() const { return delay_span_; }
+  int delay_window() const { return delay_window_; }
+  long reverb_length() const { return reverb_length_; }
+  const std::vector<double>& reverb_noise_mid() const { return noise_mid_; }
+  const std::vector<double>& reverb_noise_side() const { return noise_side_; }
+
+  // Host-buffer operator (reference signature): in/out [slots][batch][2][length] double.
+  void process(NodeType type, const double* in, double* out, int slots, int batch, long length,
+               const ParamMatrix* params, int param_offset) const;
+  AudioBuffer process_node(NodeType type, const AudioBuffer& input, std::span<const double> params) const;
+
+  // Device operator: in/out device fp32 [slots][batch][2][length]; params device fp64
+  // [>= param_offset + slots][param_width(type)]. Asynchronous on `stream`; no validation.
+  void process_device(NodeType type, const float* in, float* out, int slots, int batch, long length,
+                      const double* params, int param_offset, cudaStream_t stream) const;
+
+  std::pair<std::vector<double>, std::vector<double>> reverb_kernel(std::span<const double> params) const;
+  std::vector<double> delay_kernel(std::span<const double> params, int channel) const;
+  std::vector<long> delay_positions(std::span<const double> params, int channel) const;
+
+  const DeviceConstants& device() const { return *dev_; }
+
+ private:
+  ProcessorConfig config_;
+  long delay_span_ = 0;
+  int delay_window_ = 0;
+  long reverb_length_ = 0;
+  std::vector<double> noise_mid_, noise_side_;
+  std::unique_ptr<DeviceConstants> dev_;
+};
+
+double compressor_gain_log(double g_u, double threshold, double knee_half_width, double ratio);
+double noisegate_gain_log(double g_u, double threshold, double knee_half_width, double ratio);
+void check_param_row(NodeType type, std::span<const double> row);
+
+namespace dsp {
+std::vector<double> uniform_noise(long n, std::uint32_t seed);
+}
+
+struct RenderOptions {
+  bool keep_intermediates = false;
+};
+
+struct RenderResult {
+  std::vector<AudioBuffer> outputs;
+  std::vector<AudioBuffer> intermediates;
+};
+
+RenderResult render(const RenderData& rd, const ProcessorSet& processors, const ParamStore& params,
+                    const std::vector<AudioBuffer>& sources, const RenderOptions& options = {});
+RenderResult render(const RenderData& rd, const ProcessorSet& processors, const std::vector<AudioBuffer>& sources,
+                    const RenderOptions& options = {});
+
+// ---- device-resident render (the B200 hot path) ---------------------------------------
+//
+// `step_events`, when given, holds 2 * num_steps events recorded around every step (per-step
+// device timing for the benchmark's roofline breakdown).
+// A DevicePlan is RenderData's step table uploaded once: per step a CSR (row_ptr over the
+// step's slots, col = gathered arena rows). render_arena() runs every step on `stream`
+// over an arena of rd.buffer_rows rows x [batch][2][length] fp32 whose rows
+// [0, num_inputs) hold the sources; outputs land in rows [output_begin, buffer_rows).
+// `param_tables[t]` is a device pointer to the REORDERED fp64 table of NodeType t
+// (RenderData::reorder_params layout), or null when the plan has no step of that type.
+class DevicePlan {
+ public:
+  explicit DevicePlan(const RenderData& rd);
+  ~DevicePlan();
+  DevicePlan(const DevicePlan&) = delete;
+  DevicePlan& operator=(const DevicePlan&) = delete;
+
+  const RenderData& data() const { return rd_; }
+  const int* row_ptr(int step) const;
+  const int* col(int step) const;
+  const std::vector<int>& zero_rows() const { return zero_rows_; }
+  std::size_t workspace_bytes(int batch, long length, const ProcessorSet& procs) const;
+  int kernels_per_render(int batch, long length) const;
+
+ private:
+  const RenderData& rd_;
+  int* d_index_ = nullptr;
+  std::vector<long> rp_off_, col_off_;
+  std::vector<int> zero_rows_;
+};
+
+// Host-buffer render over caller pointers (no intermediate host copies): sources[k] and
+// outputs[o] each point at [batch][2][length] doubles (pinned memory makes the copies
+// asynchronous DMA); intermediates (original row order) may be null. `plan` may be null.
+void render_host(const RenderData& rd, const ProcessorSet& processors, const ParamStore& params,
+                 const double* const* sources, int batch, long length, double* const* outputs,
+                 double* const* intermediates, const DevicePlan* plan);
+
+void render_arena(const DevicePlan& plan, const ProcessorSet& processors, const double* const* param_tables,
+                  float* arena, int batch, long length, void* workspace, std::size_t workspace_bytes,
+                  cudaStream_t stream, cudaEvent_t* step_events = nullptr);
+
+}  // namespace mixgraph

@@ -1,0 +1,79 @@
+"""Device-resident render path: one fp32 HBM arena per (plan, batch, length).
+
+Wraps ``mg_render_arena`` (include/mixgraph_b200.h). torch is used only for device memory,
+streams and events (plumbing); all arithmetic runs in the library's sm_100a kernels.
+
+Arena layout: ``arena[row, b, c, n]`` with rows in render (reordered) order; rows
+``[0, num_inputs)`` are the sources, rows ``[output_begin, buffer_rows)`` the outputs
+(`render.cpp:32-37,63-69`). Parameter tables live on the device in fp64, render order.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Dict, Optional
+
+import numpy as np
+import torch
+
+from . import NUM_NODE_TYPES, ProcessorSet, RenderData, _check, _lib, _u64, _vp, param_width
+
+
+class DeviceRenderer:
+    def __init__(self, rd: RenderData, procs: ProcessorSet, batch: int, length: int,
+                 params: Optional[Dict[int, np.ndarray]] = None, device: Optional[torch.device] = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("DeviceRenderer needs a CUDA device (there is no CPU fallback)")
+        self.rd, self.procs = rd, procs
+        self.batch, self.length = int(batch), int(length)
+        self.device = device or torch.device("cuda", procs.device)
+        self.arena = torch.zeros((rd.buffer_rows, self.batch, 2, self.length), dtype=torch.float32, device=self.device)
+        ws = _u64()
+        _check(_lib.mg_plan_workspace_bytes(rd.handle, procs.handle, self.batch, self.length, ctypes.byref(ws)))
+        self.workspace_bytes = int(ws.value)
+        self.workspace = torch.empty(self.workspace_bytes, dtype=torch.uint8, device=self.device)
+        self.tables: Dict[int, torch.Tensor] = {}
+        self._ptrs = (_vp * NUM_NODE_TYPES)()
+        self.set_params(rd.flat.params if params is None else params)
+
+    def set_params(self, params: Dict[int, np.ndarray]) -> None:
+        """Upload render-order parameter tables (RenderData.reorder_params layout)."""
+        self.tables = {}
+        for t in range(NUM_NODE_TYPES):
+            self._ptrs[t] = None
+        for t, m in params.items():
+            a = torch.as_tensor(np.ascontiguousarray(m, dtype=np.float64).reshape(-1, param_width(t)))
+            d = a.to(self.device)
+            self.tables[int(t)] = d
+            self._ptrs[int(t)] = d.data_ptr()
+
+    @property
+    def sources(self) -> torch.Tensor:
+        return self.arena[: self.rd.num_inputs]
+
+    @property
+    def outputs(self) -> torch.Tensor:
+        return self.arena[self.rd.output_begin:]
+
+    def kernel_count(self) -> int:
+        return self.rd.kernel_count(self.batch, self.length)
+
+    def render(self, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """Enqueue every render step on `stream` (default: torch's current stream)."""
+        s = stream or torch.cuda.current_stream(self.device)
+        _check(_lib.mg_render_arena(self.rd.handle, self.procs.handle, self._ptrs,
+                                    ctypes.c_void_p(self.arena.data_ptr()), self.batch, self.length,
+                                    ctypes.c_void_p(self.workspace.data_ptr()), self.workspace_bytes,
+                                    ctypes.c_void_p(s.cuda_stream)))
+        return self.outputs
+
+    def render_profiled(self, stream: Optional[torch.cuda.Stream] = None, sync: bool = False) -> Optional[np.ndarray]:
+        """Same as render() with CUDA events around every step on the launching stream. With
+        sync=True, waits and returns per-step device times (ms, one per RenderData step)."""
+        s = stream or torch.cuda.current_stream(self.device)
+        out = np.zeros(len(self.rd.steps), dtype=np.float32) if sync else None
+        _check(_lib.mg_render_arena_profiled(self.rd.handle, self.procs.handle, self._ptrs,
+                                             ctypes.c_void_p(self.arena.data_ptr()), self.batch, self.length,
+                                             ctypes.c_void_p(self.workspace.data_ptr()), self.workspace_bytes,
+                                             ctypes.c_void_p(s.cuda_stream),
+                                             None if out is None else out.ctypes.data_as(ctypes.c_void_p)))
+        return out

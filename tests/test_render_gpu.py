@@ -1,0 +1,345 @@
+"""GPU parity: the CUDA render path (through the C ABI) against the compiled reference.
+
+Tolerance (north star): rel-L-inf = max|a-b| / max|b| <= 1e-4 against the reference's
+double-precision output (`tests/support/test_util.cpp:126-135`), fp32 device arithmetic.
+Cases follow `proj/tests/test_render.cpp` and `test_processors.cpp`, plus full-size
+BASELINE configurations checked directly against the reference renderer.
+"""
+import numpy as np
+import pytest
+
+from conftest import cuda_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+TOL = 1e-4
+N = None
+
+
+@pytest.fixture(scope="module")
+def procs_small(mg):
+    return mg.ProcessorSet(sample_rate=2000.0)
+
+
+def rel(a, b):
+    from oracle.ref import rel_linf
+    return rel_linf(a, b)
+
+
+def make(mg, t, e):
+    return mg.to_flat(mg.Graph.from_arrays(t, e))
+
+
+def render_both(mg, ref, t, e, params, src, fs, strategy=1, procs=None, **cfg):
+    fg = make(mg, t, e)
+    rd = mg.compute_render_data(fg, strategy)
+    procs = procs or mg.ProcessorSet(sample_rate=fs, **cfg)
+    got = mg.render(rd, procs, rd.reorder_params(params), src)
+    want = ref.Plan(t, e, strategy).render(params, src, sample_rate=fs, **cfg)
+    return got, want
+
+
+# ---- processors -----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("t", [2, 3, 7, 4, 5, 6, 8, 9])
+@pytest.mark.parametrize("fs,length", [(1000.0, 600), (44100.0, 8192), (44100.0, 5001)])
+def test_processor_matches_reference(mg, ref, t, fs, length):
+    rng = np.random.default_rng(t * 31 + length)
+    slots, batch = 3, 2
+    params = None
+    if mg.param_width(t):
+        g = mg.Graph()
+        for _ in range(slots):
+            g.add_node(t)
+        gt, ge = g.arrays()
+        params = ref.random_legal_params(gt, ge, 43 + t)[t]
+    x = rng.uniform(-1, 1, size=(slots, batch, 2, length))
+    procs = mg.ProcessorSet(sample_rate=fs)
+    got = procs.process(t, x, slots, batch, length, params, 0)
+    want = ref.process(t, x, slots, batch, length, params, 0, sample_rate=fs)
+    for s in range(slots):
+        assert rel(got[s], want[s]) < TOL, (t, s)
+
+
+def test_gain_and_imager_known_answers(mg):
+    procs = mg.ProcessorSet()
+    rng = np.random.default_rng(3)
+    u = rng.uniform(-1, 1, size=(2, 2, 500))
+    u32 = u.astype(np.float32).astype(np.float64)
+    assert np.array_equal(procs.process_node(mg.NodeType.GAIN, u, [0.0, 0.0]), u32)
+    ones = np.ones((1, 2, 100))
+    y = procs.process_node(mg.NodeType.GAIN, ones, [np.log(2.0), 0.0])
+    assert abs(y[0, 0, 50] - 2.0) < 1e-6 and abs(y[0, 1, 50] - 1.0) < 1e-6
+    hard = np.zeros((1, 2, 64))
+    hard[0, 0] = 1.0
+    y = procs.process_node(mg.NodeType.IMAGER, hard, [np.log(0.5)])
+    assert abs(y[0, 0, 10] - 0.75) < 1e-6 and abs(y[0, 1, 10] - 0.25) < 1e-6
+
+
+def test_eq_flat_and_constant(mg):
+    procs = mg.ProcessorSet()
+    u = np.random.default_rng(7).uniform(-1, 1, size=(1, 2, 4000))
+    assert rel(procs.process_node(mg.NodeType.EQ, u, np.zeros(1024)), u) < 1e-5
+    assert rel(procs.process_node(mg.NodeType.EQ, u, np.full(1024, -0.4)), u * np.exp(-0.4)) < 1e-5
+
+
+def test_reverb_kernel_matches_reference(mg, ref):
+    for fs in (2000.0, 44100.0):
+        procs = mg.ProcessorSet(sample_rate=fs)
+        g = mg.Graph()
+        g.add_node(mg.NodeType.REVERB)
+        gt, ge = g.arrays()
+        row = ref.random_legal_params(gt, ge, 11)[8][0]
+        l, r = procs.reverb_kernel(row)
+        wl, wr = ref.reverb_kernel(row, sample_rate=fs)
+        assert rel(l, wl) < TOL and rel(r, wr) < TOL
+
+
+def test_delay_positions_and_kernel(mg, ref):
+    procs = mg.ProcessorSet()
+    g = mg.Graph()
+    g.add_node(mg.NodeType.DELAY)
+    gt, ge = g.arrays()
+    for seed in range(5):
+        row = ref.random_legal_params(gt, ge, seed)[9][0]
+        for c in (0, 1):
+            k, pos = ref.delay_kernel(row, c)
+            assert procs.delay_positions(row, c) == pos
+            assert rel(procs.delay_kernel(row, c), k) < 1e-5
+    # test_processors.cpp:388-414
+    row = np.zeros(880)
+    for tap in range(40):
+        row[tap * 22] = 1.0
+        row[tap * 22 + 2: tap * 22 + 22] = -80.0
+
+    def enable(r, tap, d, span):
+        a = -2 * np.pi * d / span
+        r[tap * 22], r[tap * 22 + 1] = np.cos(a), np.sin(a)
+        r[tap * 22 + 2: tap * 22 + 22] = 0.0
+
+    enable(row, 0, 100, procs.delay_span)
+    enable(row, 1, 4600, procs.delay_span)
+    pos = procs.delay_positions(row, 0)
+    assert pos[:3] == [100, 4600, -1]
+    imp = np.zeros((1, 2, 6000))
+    imp[0, 0, 0] = 1.0
+    y = procs.process_node(mg.NodeType.DELAY, imp, row)
+    assert abs(y[0, 0, 100] - 1.0) < 1e-5 and abs(y[0, 0, 4600] - 1.0) < 1e-5 and abs(y[0, 0, 2000]) < 1e-6
+
+
+def test_dynamics_long_envelope_correction(mg, ref):
+    # alpha -> 1 with envelope_taps < L exercises the a^Ne * e[n-Ne] term of the scan.
+    rng = np.random.default_rng(9)
+    x = rng.uniform(-1, 1, size=(2, 1, 2, 20000)) * np.linspace(0.01, 1, 20000)
+    params = np.array([[0.99995, -2.0, 0.5, 4.0], [0.9999, -1.0, 0.3, 6.0]])
+    for t in (5, 6):
+        procs = mg.ProcessorSet(sample_rate=44100.0, envelope_taps=4096)
+        got = procs.process(t, x, 2, 1, 20000, params, 0)
+        want = ref.process(t, x, 2, 1, 20000, params, 0, envelope_taps=4096)
+        assert rel(got, want) < TOL
+
+
+def test_quiet_signal_passes_compressor(mg):
+    procs = mg.ProcessorSet()
+    u = np.random.default_rng(19).uniform(-1, 1, size=(1, 2, 1000)) * 1e-6
+    y = procs.process_node(mg.NodeType.COMPRESSOR, u, [0.99, -1.0, 0.5, 8.0])
+    assert np.array_equal(y, u.astype(np.float32).astype(np.float64))
+
+
+def test_parameter_validation_throws(mg):
+    procs = mg.ProcessorSet()
+    u = np.zeros((1, 2, 16))
+    for bad in ([1.5, -1, 0.5, 4], [0.9, -1, -0.5, 4], [0.9, -1, 0.5, 0.5], [0.9, np.nan, 0.5, 4]):
+        with pytest.raises(ValueError):
+            procs.process_node(mg.NodeType.COMPRESSOR, u, bad)
+
+
+# ---- whole renders ---------------------------------------------------------------------------
+
+def test_random_dags_match_reference_and_oracle(mg, ref, procs_small):
+    # test_render.cpp:90-106: batched vs per-node reference, fs = 2000, L = 2048.
+    for seed in range(13, 21):
+        t, e = ref.random_dag(seed, 5, 25)
+        params = ref.random_legal_params(t, e, seed)
+        src = np.random.default_rng(seed).uniform(-1, 1, size=(int(np.sum(t == 0)), 1, 2, 2048))
+        got, want = render_both(mg, ref, t, e, params, src, 2000.0, procs=procs_small)
+        assert rel(got, want) < TOL
+        slow = ref.render_reference(t, e, params, src, sample_rate=2000.0)
+        assert rel(got, slow) < TOL
+
+
+@pytest.mark.parametrize("strategy", [0, 1, 2, 3])
+def test_strategies_render_same_audio(mg, ref, procs_small, strategy):
+    for seed in range(40, 44):
+        t, e = ref.random_dag(seed, 8, 25)
+        params = ref.random_legal_params(t, e, seed)
+        src = np.random.default_rng(seed).uniform(-1, 1, size=(int(np.sum(t == 0)), 1, 2, 1024))
+        got, want = render_both(mg, ref, t, e, params, src, 2000.0, strategy, procs=procs_small)
+        assert rel(got, want) < TOL
+
+
+def test_config2_full_size_matches_reference(mg, ref):
+    # BASELINE config 2: console(16, p=.3, seed=16), stereo 2^17 @ 44.1 kHz, sources as bench.cpp:33-40.
+    t, e = ref.console(16, 0.3, 16)
+    L = 1 << 17
+    params = ref.random_legal_params(t, e, 2024)
+    src = np.stack([ref.uniform_noise(2 * L, 1000 + k).reshape(1, 2, L) for k in range(16)])
+    got, want = render_both(mg, ref, t, e, params, src, 44100.0)
+    assert got.shape == want.shape == (1, 1, 2, L)
+    assert rel(got, want) < TOL
+
+
+def test_config1_chain_matches_reference(mg, ref):
+    # BASELINE config 1: in -> (g -> e) x 4 -> out, stereo 2^16.
+    g = mg.Graph()
+    g.add_serial_chain([0] + [3, 4] * 4 + [1])
+    t, e = g.arrays()
+    L = 1 << 16
+    params = ref.random_legal_params(t, e, 1)
+    src = ref.uniform_noise(2 * L, 1000).reshape(1, 1, 2, L)
+    got, want = render_both(mg, ref, t, e, params, src, 44100.0)
+    assert rel(got, want) < TOL
+
+
+def test_one_by_one_quirk_renders_like_reference(mg, ref):
+    g = mg.Graph()
+    for ty in (0, 3, 2, 4, 4, 1):
+        g.add_node(ty)
+    for s, d in ((0, 1), (1, 2), (1, 2), (0, 3), (3, 4), (4, 2), (2, 5)):
+        g.connect(s, d)
+    t, e = g.arrays()
+    params = ref.random_legal_params(t, e, 5)
+    src = np.random.default_rng(5).uniform(-1, 1, size=(1, 1, 2, 3000))
+    got, want = render_both(mg, ref, t, e, params, src, 44100.0, strategy=0)
+    assert rel(got, want) < TOL
+
+
+def test_known_answer_renders(mg):
+    procs = mg.ProcessorSet()
+    rng = np.random.default_rng(3)
+    # zero-gain chain is the identity (test_render.cpp:22-32)
+    g = mg.Graph()
+    g.add_serial_chain([0, 3, 1])
+    rd = mg.compute_render_data(mg.to_flat(g))
+    s = rng.uniform(-1, 1, size=(1, 1, 2, 1024))
+    assert np.array_equal(mg.render(rd, procs, None, s), s.astype(np.float32).astype(np.float64))
+    # mix sums, parallel edges double, unconnected nodes are silent (:34-88)
+    g = mg.Graph()
+    a, b, m, o = g.add_node(0), g.add_node(0), g.add_node(2), g.add_node(1)
+    g.connect(a, m)
+    g.connect(b, m)
+    g.connect(m, o)
+    rd = mg.compute_render_data(mg.to_flat(g))
+    s = rng.uniform(-1, 1, size=(2, 1, 2, 513)).astype(np.float32).astype(np.float64)
+    assert np.array_equal(mg.render(rd, procs, None, s)[0], (s[0] + s[1]).astype(np.float32))
+    g = mg.Graph()
+    i, m, o = g.add_node(0), g.add_node(2), g.add_node(1)
+    g.connect(i, m)
+    g.connect(i, m)
+    g.connect(m, o)
+    rd = mg.compute_render_data(mg.to_flat(g))
+    s = rng.uniform(-1, 1, size=(1, 1, 2, 256)).astype(np.float32).astype(np.float64)
+    assert np.array_equal(mg.render(rd, procs, None, s)[0], 2 * s[0])
+    g = mg.Graph()
+    i, o1, eq, o2 = g.add_node(0), g.add_node(1), g.add_node(4), g.add_node(1)
+    g.connect(i, o1)
+    g.connect(eq, o2)
+    rd = mg.compute_render_data(mg.to_flat(g))
+    out = mg.render(rd, procs, None, s)
+    assert np.array_equal(out[0], s[0]) and not np.any(out[1])
+
+
+def test_intermediates_in_original_order(mg):
+    g = mg.Graph()
+    g.add_serial_chain([0, 3, 1])
+    fg = mg.to_flat(g)
+    fg.params[mg.NodeType.GAIN][0] = np.log(3.0)
+    rd = mg.compute_render_data(fg)
+    procs = mg.ProcessorSet()
+    s = np.random.default_rng(31).uniform(-1, 1, size=(1, 1, 2, 128))
+    out, inter = mg.render(rd, procs, None, s, keep_intermediates=True)
+    assert inter.shape[0] == 3
+    assert rel(inter[0], s[0]) < 1e-7 and np.array_equal(inter[2], out[0])
+    assert rel(inter[1], 3 * s[0]) < 1e-6
+
+
+def test_render_rejects_malformed_inputs(mg):
+    g = mg.Graph()
+    g.add_serial_chain([0, 3, 1])
+    rd = mg.compute_render_data(mg.to_flat(g))
+    procs = mg.ProcessorSet()
+    with pytest.raises(ValueError):
+        mg.render(rd, procs, None, np.zeros((2, 1, 2, 64)))
+    bad = {k: v.copy() for k, v in rd.flat.params.items()}
+    bad[mg.NodeType.GAIN][0, 0] = np.nan
+    with pytest.raises(ValueError):
+        mg.render(rd, procs, bad, np.zeros((1, 1, 2, 64)))
+
+
+def test_union_renders_like_parts(mg, ref, procs_small):
+    # test_render.cpp:132-160
+    t1, e1 = ref.random_dag(19, 5, 15)
+    t2, e2 = ref.random_dag(20, 5, 15)
+    g = mg.disjoint_union([mg.Graph.from_arrays(t1, e1), mg.Graph.from_arrays(t2, e2)])
+    tu, eu = g.arrays()
+    p1, p2 = ref.random_legal_params(t1, e1, 1), ref.random_legal_params(t2, e2, 2)
+    pu = mg.concat_params([p1, p2])
+    rng = np.random.default_rng(19)
+    s1 = rng.uniform(-1, 1, size=(int(np.sum(t1 == 0)), 1, 2, 1024))
+    s2 = rng.uniform(-1, 1, size=(int(np.sum(t2 == 0)), 1, 2, 1024))
+    r1, _ = render_both(mg, ref, t1, e1, p1, s1, 2000.0, procs=procs_small)
+    r2, _ = render_both(mg, ref, t2, e2, p2, s2, 2000.0, procs=procs_small)
+    ru, _ = render_both(mg, ref, tu, eu, pu, np.concatenate([s1, s2]), 2000.0, procs=procs_small)
+    assert rel(ru[: len(r1)], r1) < 1e-6 and rel(ru[len(r1):], r2) < 1e-6
+
+
+def test_batch_equals_singles(mg, ref, procs_small):
+    # test_render.cpp:162-192 (source-level batching)
+    t, e = ref.random_dag(23, 6, 20)
+    params = ref.random_legal_params(t, e, 23)
+    fg = make(mg, t, e)
+    rd = mg.compute_render_data(fg)
+    P = rd.reorder_params(params)
+    src = np.random.default_rng(23).uniform(-1, 1, size=(int(np.sum(t == 0)), 3, 2, 800))
+    big = mg.render(rd, procs_small, P, src)
+    for b in range(3):
+        one = mg.render(rd, procs_small, P, src[:, b:b + 1])
+        assert np.max(np.abs(big[:, b] - one[:, 0])) < 1e-6
+
+
+def test_lti_graph_is_linear(mg, ref, procs_small):
+    g = mg.Graph()
+    i = g.add_node(0)
+    a, b = g.add_serial_chain([4, 7, 3, 9])
+    o = g.add_node(1)
+    g.connect(i, a)
+    g.connect(b, o)
+    g.connect(i, o)
+    t, e = g.arrays()
+    params = ref.random_legal_params(t, e, 29)
+    rd = mg.compute_render_data(make(mg, t, e))
+    P = rd.reorder_params(params)
+    rng = np.random.default_rng(29)
+    s1, s2 = rng.uniform(-1, 1, size=(2, 1, 1, 2, 1024))
+    y = mg.render(rd, procs_small, P, 0.8 * s1 - 0.6 * s2)
+    y1, y2 = mg.render(rd, procs_small, P, s1), mg.render(rd, procs_small, P, s2)
+    assert rel(y, 0.8 * y1 - 0.6 * y2) < TOL
+
+
+def test_device_path_equals_host_path(mg, ref):
+    import torch
+    t, e = ref.console(4, 0.0, 3)
+    L = 20000
+    params = ref.random_legal_params(t, e, 4)
+    rd = mg.compute_render_data(make(mg, t, e))
+    procs = mg.ProcessorSet()
+    P = rd.reorder_params(params)
+    src = np.random.default_rng(4).uniform(-1, 1, size=(rd.num_inputs, 1, 2, L))
+    host = mg.render(rd, procs, P, src)
+    dr = mg.DeviceRenderer(rd, procs, 1, L, P)
+    dr.sources.copy_(torch.as_tensor(src, dtype=torch.float32))
+    out = dr.render().cpu().numpy()
+    torch.cuda.synchronize()
+    assert np.array_equal(out, host.astype(np.float32))
+    want = ref.Plan(t, e, 1).render(params, src)
+    assert rel(out, want) < TOL
