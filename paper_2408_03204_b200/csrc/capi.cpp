@@ -24,6 +24,7 @@ struct mg_plan {
   std::unique_ptr<DevicePlan> dev;  // uploaded lazily on first device render
   std::vector<cudaEvent_t> events;  // per-step timing events (profiled renders)
   std::mutex mu;
+  std::mutex render_mu;  // serialises enqueue: the plan's fork/join events are shared
   ~mg_plan() {
     for (cudaEvent_t e : events) cudaEventDestroy(e);
   }
@@ -268,8 +269,10 @@ int32_t mg_render(const mg_plan* p, const mg_processors* procs, const double* co
     std::vector<double*> outs, inter;
     for (int r = rd.output_begin; r < rd.buffer_rows; ++r) outs.push_back(outputs + stride * (r - rd.output_begin));
     for (int r = 0; intermediates && r < rd.buffer_rows; ++r) inter.push_back(intermediates + stride * r);
+    DevicePlan& dp = device_plan(p);
+    std::scoped_lock lock(const_cast<mg_plan*>(p)->render_mu);
     render_host(rd, *procs->ps, make_store(tables, rows), src.data(), batch, static_cast<long>(length), outs.data(),
-                intermediates ? inter.data() : nullptr, &device_plan(p));
+                intermediates ? inter.data() : nullptr, &dp);
   });
 }
 
@@ -291,7 +294,9 @@ int32_t mg_plan_kernel_count(const mg_plan* p, int32_t batch, int64_t length, in
 int32_t mg_render_arena(const mg_plan* p, const mg_processors* procs, const double* const* d_tables, float* d_arena,
                         int32_t batch, int64_t length, void* d_ws, uint64_t ws_bytes, void* stream) {
   return guarded([&] {
-    render_arena(device_plan(p), *procs->ps, d_tables, d_arena, batch, static_cast<long>(length), d_ws, ws_bytes,
+    DevicePlan& dp = device_plan(p);
+    std::scoped_lock lock(const_cast<mg_plan*>(p)->render_mu);
+    render_arena(dp, *procs->ps, d_tables, d_arena, batch, static_cast<long>(length), d_ws, ws_bytes,
                  static_cast<cudaStream_t>(stream));
   });
 }
@@ -311,6 +316,7 @@ int32_t mg_render_arena_profiled(const mg_plan* cp, const mg_processors* procs, 
       }
     }
     auto s = static_cast<cudaStream_t>(stream);
+    std::scoped_lock rlock(p->render_mu);
     render_arena(dp, *procs->ps, d_tables, d_arena, batch, static_cast<long>(length), d_ws, ws_bytes, s, p->events.data());
     if (step_ms) {
       if (cudaStreamSynchronize(s) != cudaSuccess) throw std::runtime_error("render failed");

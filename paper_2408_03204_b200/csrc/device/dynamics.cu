@@ -116,7 +116,7 @@ __device__ __forceinline__ void compose(float& A, float& B, float Ap, float Bp) 
 }
 
 template <bool GATE, bool VEC>
-__global__ void __launch_bounds__(kDynThreads) dyn_scan(StepArgs a, int env_taps, double floor_, int tiles_per_seq,
+__global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_taps, double floor_, int tiles_per_seq,
                                                          unsigned long long* status, unsigned int* ticket) {
   __shared__ float wA[kDynThreads / 32], wB[kDynThreads / 32];
   __shared__ float s_carry;
@@ -196,62 +196,73 @@ __global__ void __launch_bounds__(kDynThreads) dyn_scan(StepArgs a, int env_taps
   const float tileB = wB[kDynThreads / 32 - 1];
   const float tileA = wA[kDynThreads / 32 - 1];
 
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
+    // Warp-parallel decoupled look-back: lane l inspects tile (tile-1-l) of this sequence,
+    // weight A^l with A = a^4096; stop at the nearest inclusive prefix or once A^l underflows.
     cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> mine(status[tk]);
     float carry = 0.f;
     if (tile > 0) {
-      mine.store(kFlagAgg | __float_as_uint(tileB), cuda::memory_order_relaxed);
-      float SA = 1.f, SB = 0.f;
-      for (int q = tk - 1;; --q) {
-        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[q]);
-        unsigned long long w;
-        do {
-          w = st.load(cuda::memory_order_relaxed);
-        } while ((w >> 32) == 0);
-        const float v = __uint_as_float(static_cast<unsigned int>(w & 0xffffffffu));
-        if ((w & ~0xffffffffull) == kFlagInc) {
-          carry = fmaf(SA, v, SB);
-          break;
+      if (lane == 0) mine.store(kFlagAgg | __float_as_uint(tileB), cuda::memory_order_relaxed);
+      const float wl = powf(p.atile, static_cast<float>(lane));
+      const float w32 = powf(p.atile, 32.f);
+      float mult = 1.f;
+      int base = tk - 1, remaining = tile;
+      while (true) {
+        const bool valid = lane < remaining;
+        unsigned long long w = 0;
+        if (valid) {
+          cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[base - lane]);
+          do {
+            w = st.load(cuda::memory_order_relaxed);
+          } while ((w >> 32) == 0);
         }
-        SB = fmaf(SA, v, SB);
-        SA *= p.atile;
-        if (SA == 0.f) {
-          carry = SB;
-          break;
-        }
+        const unsigned inc = __ballot_sync(0xffffffffu, valid && (w & ~0xffffffffull) == kFlagInc);
+        const int first = inc ? __ffs(inc) - 1 : 32;
+        float part = (valid && lane <= first) ? wl * __uint_as_float(static_cast<unsigned int>(w & 0xffffffffu)) : 0.f;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+        carry = fmaf(mult, part, carry);
+        mult *= w32;
+        if (inc || remaining <= 32 || mult == 0.f) break;
+        base -= 32;
+        remaining -= 32;
       }
     }
-    mine.store(kFlagInc | __float_as_uint(fmaf(tileA, carry, tileB)), cuda::memory_order_relaxed);
-    s_carry = carry;
+    if (lane == 0) {
+      mine.store(kFlagInc | __float_as_uint(fmaf(tileA, carry, tileB)), cuda::memory_order_relaxed);
+      s_carry = carry;
+    }
   }
   __syncthreads();
 
-  // Replay the recurrence from this thread's true start state and apply the gain.
+  // Replay the recurrence from this thread's true start state, apply the gain, store.
   float g = fmaf(xA, s_carry, xB);
-  float yl[kDynPerThread], yr[kDynPerThread];
-#pragma unroll
-  for (int k = 0; k < kDynPerThread; ++k) {
-    const float m = ul[k] + ur[k];
-    g = fmaf(p.a, g, p.oma * (m * m - eo[k]));
-    const float gn = gain_of<GATE>(g, p);
-    yl[k] = gn * ul[k];
-    yr[k] = gn * ur[k];
-  }
   if (n0 >= a.length) return;
   float* ol = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length + n0;
   float* orr = ol + a.length;
-  if (VEC && n0 + kDynPerThread <= a.length) {
+  const bool full = VEC && n0 + kDynPerThread <= a.length;
 #pragma unroll
-    for (int q = 0; q < kDynPerThread / 4; ++q) {
-      reinterpret_cast<float4*>(ol)[q] = make_float4(yl[4 * q], yl[4 * q + 1], yl[4 * q + 2], yl[4 * q + 3]);
-      reinterpret_cast<float4*>(orr)[q] = make_float4(yr[4 * q], yr[4 * q + 1], yr[4 * q + 2], yr[4 * q + 3]);
+  for (int q = 0; q < kDynPerThread / 4; ++q) {
+    float yl[4], yr[4];
+#pragma unroll
+    for (int k4 = 0; k4 < 4; ++k4) {
+      const int k = 4 * q + k4;
+      const float m = ul[k] + ur[k];
+      g = fmaf(p.a, g, p.oma * (m * m - eo[k]));
+      const float gn = gain_of<GATE>(g, p);
+      yl[k4] = gn * ul[k];
+      yr[k4] = gn * ur[k];
     }
-  } else {
+    if (full) {
+      reinterpret_cast<float4*>(ol)[q] = make_float4(yl[0], yl[1], yl[2], yl[3]);
+      reinterpret_cast<float4*>(orr)[q] = make_float4(yr[0], yr[1], yr[2], yr[3]);
+    } else {
 #pragma unroll
-    for (int k = 0; k < kDynPerThread; ++k) {
-      if (n0 + k < a.length) {
-        ol[k] = yl[k];
-        orr[k] = yr[k];
+      for (int k4 = 0; k4 < 4; ++k4) {
+        if (n0 + 4 * q + k4 < a.length) {
+          ol[4 * q + k4] = yl[k4];
+          orr[4 * q + k4] = yr[k4];
+        }
       }
     }
   }

@@ -75,7 +75,10 @@ Engine& engine_for(int device) {
 
 inline std::size_t align256(std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255); }
 
-std::size_t eq_ws_bytes(int slots) { return align256(sizeof(float) * 2048 * slots) + align256(sizeof(float) * mgb::kEqFft * slots); }
+// EQ prologue region: taps [slots][2048] f32 + magnitudes [slots][1024] f64, then the
+// response [slots][8192] f32 (run_prologue / run_main locate it the same way).
+std::size_t eq_taps_bytes(int slots) { return align256((sizeof(float) * 2048 + sizeof(double) * 1024) * slots); }
+std::size_t eq_ws_bytes(int slots) { return eq_taps_bytes(slots) + align256(sizeof(float) * mgb::kEqFft * slots); }
 
 }  // namespace
 
@@ -147,6 +150,7 @@ ProcessorSet::ProcessorSet(const ProcessorConfig& config) : config_(config) {
 
   dev_ = std::make_unique<DeviceConstants>();
   cuda_check(cudaGetDevice(&dev_->device), "cudaGetDevice");
+  mgb::twiddle_table(dev_->device);
   dev_->frames = static_cast<int>((reverb_length_ + kReverbStftHop - 1) / kReverbStftHop);
   const std::size_t stft_bytes = sizeof(float2) * static_cast<std::size_t>(dev_->frames) * (kReverbStftLength / 2 + 1);
   cuda_check(cudaMalloc(&dev_->stft_mid, stft_bytes > 0 ? stft_bytes : 8), "cudaMalloc");
@@ -171,22 +175,33 @@ mgb::ReverbConst reverb_const(const ProcessorSet& p) {
 }
 mgb::DelayConst delay_const(const ProcessorSet& p) { return {p.delay_span(), p.delay_window()}; }
 
-std::size_t step_ws_bytes(NodeType t, int slots, int batch, long length, const ProcessorSet& p) {
+bool has_prologue(NodeType t) { return t == NodeType::Eq || t == NodeType::Reverb || t == NodeType::Delay; }
+
+// Parameter-only work (FIR design, impulse responses, kernel spectra) lives in a per-step
+// persistent region so it can run ahead on a side stream; audio work uses a shared region.
+std::size_t prologue_bytes(NodeType t, int slots, long length, const ProcessorSet& p) {
   switch (t) {
     case NodeType::Eq: return eq_ws_bytes(slots);
+    case NodeType::Reverb:
+      return mgb::conv_prologue_bytes(mgb::conv_geom(length, p.reverb_length()), slots, p.reverb_length());
+    case NodeType::Delay: return mgb::conv_prologue_bytes(mgb::conv_geom(length, p.delay_span()), slots, p.delay_span());
+    default: return 0;
+  }
+}
+
+std::size_t main_bytes(NodeType t, int slots, int batch, long length, const ProcessorSet& p) {
+  switch (t) {
     case NodeType::Compressor:
     case NodeType::Noisegate: return mgb::dyn_workspace_bytes(slots, batch, length);
-    case NodeType::Reverb:
-      return mgb::conv_workspace_bytes(mgb::conv_geom(length, p.reverb_length()), slots, batch, p.reverb_length());
-    case NodeType::Delay:
-      return mgb::conv_workspace_bytes(mgb::conv_geom(length, p.delay_span()), slots, batch, p.delay_span());
+    case NodeType::Reverb: return mgb::conv_main_bytes(mgb::conv_geom(length, p.reverb_length()), slots, batch);
+    case NodeType::Delay: return mgb::conv_main_bytes(mgb::conv_geom(length, p.delay_span()), slots, batch);
     default: return 0;
   }
 }
 
 int step_kernels(NodeType t) {
   switch (t) {
-    case NodeType::Eq: return 3;
+    case NodeType::Eq: return 4;
     case NodeType::Compressor:
     case NodeType::Noisegate: return 1;
     case NodeType::Reverb:
@@ -195,27 +210,48 @@ int step_kernels(NodeType t) {
   }
 }
 
-// One step on the device. a.params points at the step's first parameter row.
-void run_step(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, void* ws, cudaStream_t s) {
+void run_prologue(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, void* pws, cudaStream_t s) {
+  switch (t) {
+    case NodeType::Eq: {
+      auto* taps = static_cast<float*>(pws);
+      auto* resp = reinterpret_cast<float*>(static_cast<char*>(pws) + eq_taps_bytes(a.slots));
+      mgb::launch_eq_prologue(a, taps, resp, s);
+      break;
+    }
+    case NodeType::Reverb: mgb::launch_conv_prologue(true, a, reverb_const(p), delay_const(p), pws, s); break;
+    case NodeType::Delay: mgb::launch_conv_prologue(false, a, reverb_const(p), delay_const(p), pws, s); break;
+    default: break;
+  }
+}
+
+// One step's audio pass. a.params points at the step's first parameter row.
+void run_main(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, void* pws, void* mws, cudaStream_t s) {
   switch (t) {
     case NodeType::In:
     case NodeType::Out:
     case NodeType::Mix: mgb::launch_pointwise(mgb::PointOp::Copy, a, s); break;
     case NodeType::Gain: mgb::launch_pointwise(mgb::PointOp::Gain, a, s); break;
     case NodeType::Imager: mgb::launch_pointwise(mgb::PointOp::Imager, a, s); break;
-    case NodeType::Eq: {
-      auto* taps = static_cast<float*>(ws);
-      auto* resp = reinterpret_cast<float*>(static_cast<char*>(ws) + align256(sizeof(float) * 2048 * a.slots));
-      mgb::launch_eq(a, taps, resp, s);
+    case NodeType::Eq:
+      mgb::launch_eq_main(a, reinterpret_cast<float*>(static_cast<char*>(pws) + eq_taps_bytes(a.slots)), s);
       break;
-    }
     case NodeType::Compressor:
     case NodeType::Noisegate:
-      mgb::launch_dynamics(t == NodeType::Noisegate, a, p.config().envelope_taps, p.config().energy_floor, ws, s);
+      mgb::launch_dynamics(t == NodeType::Noisegate, a, p.config().envelope_taps, p.config().energy_floor, mws, s);
       break;
-    case NodeType::Reverb: mgb::launch_reverb(a, reverb_const(p), ws, s); break;
-    case NodeType::Delay: mgb::launch_delay(a, delay_const(p), ws, s); break;
+    case NodeType::Reverb: mgb::launch_conv_main(a, p.reverb_length(), pws, mws, s); break;
+    case NodeType::Delay: mgb::launch_conv_main(a, p.delay_span(), pws, mws, s); break;
   }
+}
+
+std::size_t step_ws_bytes(NodeType t, int slots, int batch, long length, const ProcessorSet& p) {
+  return align256(prologue_bytes(t, slots, length, p)) + main_bytes(t, slots, batch, length, p);
+}
+
+void run_step(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, void* ws, cudaStream_t s) {
+  const std::size_t pb = align256(prologue_bytes(t, a.slots, a.length, p));
+  run_prologue(t, a, p, ws, s);
+  run_main(t, a, p, ws, static_cast<char*>(ws) + pb, s);
 }
 
 }  // namespace
@@ -249,21 +285,36 @@ DevicePlan::DevicePlan(const RenderData& rd) : rd_(rd) {
     cuda_check(cudaMalloc(&d_index_, sizeof(int) * host.size()), "cudaMalloc");
     cuda_check(cudaMemcpy(d_index_, host.data(), sizeof(int) * host.size(), cudaMemcpyHostToDevice), "H2D plan");
   }
+  cuda_check(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking), "cudaStreamCreate");
+  events_.resize(rd.steps.size() + 1);
+  for (auto& ev : events_) cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
 }
 
 DevicePlan::~DevicePlan() {
+  for (cudaEvent_t ev : events_) cudaEventDestroy(ev);
+  if (aux_) cudaStreamDestroy(aux_);
   if (d_index_) cudaFree(d_index_);
 }
 
 const int* DevicePlan::row_ptr(int step) const { return d_index_ + rp_off_[static_cast<std::size_t>(step)]; }
 const int* DevicePlan::col(int step) const { return d_index_ + col_off_[static_cast<std::size_t>(step)]; }
 
-std::size_t DevicePlan::workspace_bytes(int batch, long length, const ProcessorSet& procs) const {
-  std::size_t m = 256;
+DevicePlan::Layout DevicePlan::layout(int batch, long length, const ProcessorSet& procs) const {
+  Layout l;
+  std::size_t off = 0, main = 256;
   for (const StepIndex& st : rd_.steps) {
-    m = std::max(m, step_ws_bytes(st.type, st.store_end - st.store_begin, batch, length, procs));
+    const int slots = st.store_end - st.store_begin;
+    l.prologue_off.push_back(off);
+    off += align256(prologue_bytes(st.type, slots, length, procs));
+    main = std::max(main, main_bytes(st.type, slots, batch, length, procs));
   }
-  return m;
+  l.main_off = off;
+  l.total = off + align256(main);
+  return l;
+}
+
+std::size_t DevicePlan::workspace_bytes(int batch, long length, const ProcessorSet& procs) const {
+  return layout(batch, length, procs).total;
 }
 
 int DevicePlan::kernels_per_render(int, long) const {
@@ -274,17 +325,18 @@ int DevicePlan::kernels_per_render(int, long) const {
 
 void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const double* const* param_tables, float* arena,
                   int batch, long length, void* workspace, std::size_t workspace_bytes, cudaStream_t stream,
-                  cudaEvent_t* step_events) {
+                  cudaEvent_t* step_events, bool hoist) {
   const RenderData& rd = plan.data();
-  if (workspace_bytes < plan.workspace_bytes(batch, length, procs)) fail("render_arena: workspace too small");
+  const DevicePlan::Layout lay = plan.layout(batch, length, procs);
+  if (workspace_bytes < lay.total) fail("render_arena: workspace too small");
+  char* ws = static_cast<char*>(workspace);
   const long rowstride = static_cast<long>(batch) * 2 * length;
-  for (int r : plan.zero_rows()) {
-    cuda_check(cudaMemsetAsync(arena + r * rowstride, 0, sizeof(float) * rowstride, stream), "memset");
-  }
+  const float2* tw = mgb::twiddle_table(procs.device().device);
+  std::vector<mgb::StepArgs> args(rd.steps.size());
   for (std::size_t k = 0; k < rd.steps.size(); ++k) {
     const StepIndex& st = rd.steps[k];
     const int width = param_width(st.type);
-    mgb::StepArgs a{};
+    mgb::StepArgs& a = args[k];
     a.src = arena;
     a.dst = arena + st.store_begin * rowstride;
     a.row_ptr = plan.row_ptr(static_cast<int>(k));
@@ -295,12 +347,34 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
       if (!table) fail("render: missing parameter table for " + tname(st.type));
       a.params = table + static_cast<long>(st.param_begin) * width;
     }
+    a.tw = tw;
     a.slots = st.store_end - st.store_begin;
     a.batch = batch;
     a.length = length;
     a.rowstride = rowstride;
+  }
+  for (int r : plan.zero_rows()) {
+    cuda_check(cudaMemsetAsync(arena + r * rowstride, 0, sizeof(float) * rowstride, stream), "memset");
+  }
+  // Parameter-only prologues (EQ design, reverb/delay impulse responses and their spectra)
+  // depend on nothing the render computes: fork them onto the plan's side stream so they
+  // overlap the earlier steps, and join each one right before its step's audio pass.
+  const cudaEvent_t* ev = plan.events();
+  if (hoist) {
+    cuda_check(cudaEventRecord(ev[0], stream), "event");
+    cuda_check(cudaStreamWaitEvent(plan.aux_stream(), ev[0], 0), "wait");
+    for (std::size_t k = 0; k < rd.steps.size(); ++k) {
+      if (!has_prologue(rd.steps[k].type)) continue;
+      run_prologue(rd.steps[k].type, args[k], procs, ws + lay.prologue_off[k], plan.aux_stream());
+      cuda_check(cudaEventRecord(ev[k + 1], plan.aux_stream()), "event");
+    }
+  }
+  for (std::size_t k = 0; k < rd.steps.size(); ++k) {
+    const NodeType t = rd.steps[k].type;
+    if (hoist && has_prologue(t)) cuda_check(cudaStreamWaitEvent(stream, ev[k + 1], 0), "wait");
     if (step_events) cuda_check(cudaEventRecord(step_events[2 * k], stream), "event");
-    run_step(st.type, a, procs, workspace, stream);
+    if (!hoist) run_prologue(t, args[k], procs, ws + lay.prologue_off[k], stream);
+    run_main(t, args[k], procs, ws + lay.prologue_off[k], ws + lay.main_off, stream);
     if (step_events) cuda_check(cudaEventRecord(step_events[2 * k + 1], stream), "event");
   }
   cuda_check(cudaGetLastError(), "render_arena launch");
@@ -327,6 +401,7 @@ void ProcessorSet::process_device(NodeType type, const float* in, float* out, in
   a.slots = slots;
   a.batch = batch;
   a.length = length;
+  a.tw = mgb::twiddle_table(dev_->device);
   a.rowstride = static_cast<long>(batch) * 2 * length;
   run_step(type, a, *this, aux + align256(sizeof(int) * idx.size()), stream);
   cuda_check(cudaGetLastError(), "process launch");

@@ -24,28 +24,45 @@ namespace {
 constexpr int kN = 2047;  // kEqFirLength
 constexpr int kLogFft = 13;
 static_assert((1 << kLogFft) == kEqFft, "EQ FFT size");
+constexpr int kEqBuf = padded(kEqFft);
+constexpr int kEqOut = 6144;  // outputs per block (of the 8192 - 2046 = 6146 non-wrapped)
+constexpr int kEqSmem = kEqBuf * 8;
 
-__global__ void __launch_bounds__(256) eq_design(const double* params, float* taps) {
-  __shared__ double cos_tab[kN];
+// Taps by the exact cosine sum raw[j] = (m0 + 2 sum_{k=1}^{1023} m_k cos(2 pi k j / 2047)) / 2047
+// in fp64. One warp per tap j; lane l sums k in [1 + 32 l, 32 l + 32] with the Chebyshev
+// recurrence c_{k+1} = 2 cos(theta) c_k - c_{k-1} started from the fp64 cos table (error
+// ~1e-14 over 32 steps); lanes are reduced with xor-shuffles in a fixed order.
+// grid (1024 / 8, slots) x 256 threads (8 taps per CTA).
+constexpr int kDesignSplit = 32;
+// exp of the 1024 log-magnitudes of every slot, once (fp64). grid (slots) x 1024.
+__global__ void __launch_bounds__(1024) eq_mags(const double* params, double* mags) {
+  const long i = static_cast<long>(blockIdx.x) * (kEqHalf + 1) + threadIdx.x;
+  mags[i] = exp(params[i]);
+}
+
+__global__ void __launch_bounds__(256) eq_design(const double* __restrict__ mag_g, float* taps, const double* __restrict__ cos_tab) {
   __shared__ double mags[kEqHalf + 1];
   const int slot = blockIdx.y;
-  const double* lm = params + static_cast<long>(slot) * (kEqHalf + 1);
-  for (int k = threadIdx.x; k < kN; k += blockDim.x) {
-    double s, c;
-    sincospi(2.0 * k / kN, &s, &c);
-    cos_tab[k] = c;
-  }
-  for (int k = threadIdx.x; k <= kEqHalf; k += blockDim.x) mags[k] = exp(lm[k]);
+  for (int k = threadIdx.x; k <= kEqHalf; k += blockDim.x) mags[k] = __ldg(mag_g + static_cast<long>(slot) * (kEqHalf + 1) + k);
   __syncthreads();
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;  // 0..1023: |time index| from centre
-  if (j > kEqHalf) return;
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (256 / kDesignSplit) + threadIdx.x / kDesignSplit;  // 0..1023
+  const int k0 = 1 + 32 * lane;
+  const int k1 = lane == 31 ? kEqHalf : k0 + 31;
+  double c_prev = __ldg(cos_tab + (static_cast<long>(k0 - 1) * j) % kN);
+  double c_cur = __ldg(cos_tab + (static_cast<long>(k0) * j) % kN);
+  const double two_c = 2.0 * __ldg(cos_tab + j);
   double acc = 0.0;
-  int idx = 0;  // (k*j) mod N
-  for (int k = 1; k <= kEqHalf; ++k) {
-    idx += j;
-    if (idx >= kN) idx -= kN;
-    acc = fma(mags[k], cos_tab[idx], acc);
+#pragma unroll 4
+  for (int k = k0; k <= k1; ++k) {
+    acc = fma(mags[k], c_cur, acc);
+    const double nxt = fma(two_c, c_cur, -c_prev);
+    c_prev = c_cur;
+    c_cur = nxt;
   }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane != 0) return;
   const double raw = (mags[0] + 2.0 * acc) / kN;
   double s, c;
   sincospi(2.0 * (kEqHalf + j) / (kN - 1), &s, &c);
@@ -55,7 +72,7 @@ __global__ void __launch_bounds__(256) eq_design(const double* params, float* ta
   t[kEqHalf - j] = static_cast<float>(w * raw);
 }
 
-__global__ void __launch_bounds__(512) eq_response(const float* taps, float* resp) {
+__global__ void __launch_bounds__(512) eq_response(const float* taps, float* resp, const float2* tw) {
   extern __shared__ float2 buf[];
   const int slot = blockIdx.x;
   const float* t = taps + static_cast<long>(slot) * 2048;
@@ -63,59 +80,108 @@ __global__ void __launch_bounds__(512) eq_response(const float* taps, float* res
     float v = 0.f;
     if (i <= kEqHalf) v = t[kEqHalf + i];
     else if (i >= kEqFft - kEqHalf) v = t[kEqHalf - (kEqFft - i)];
-    buf[i] = make_float2(v, 0.f);
+    buf[sidx(i)] = make_float2(v, 0.f);
   }
   __syncthreads();
-  fft_pow2<kLogFft, 1, 512, -1>(buf, kEqFft);
+  fft_pow2<kLogFft, 1, 512, -1>(buf, kEqBuf, tw);
   float* r = resp + static_cast<long>(slot) * kEqFft;
-  for (int i = threadIdx.x; i < kEqFft; i += blockDim.x) r[i] = buf[i].x * (1.f / kEqFft);
+  for (int i = threadIdx.x; i < kEqFft; i += blockDim.x) r[i] = buf[sidx(i)].x * (1.f / kEqFft);
 }
 
-// grid (blocks per signal, slots*B)
-__global__ void __launch_bounds__(512) eq_conv(StepArgs a, const float* resp) {
+// grid (blocks per signal, slots*B). Block covers outputs [out0, out0 + 6144) from the
+// 8192-sample window starting at out0 - 1024 (both 4-aligned: float4 loads/stores when
+// L % 4 == 0); the circular convolution is exact for window indices [1023, 7168].
+__global__ void __launch_bounds__(512, 2) eq_conv(StepArgs a, const float* resp) {
   extern __shared__ float2 buf[];
   const int sb = blockIdx.y;
   const int slot = sb / a.batch, b = sb - slot * a.batch;
   const int e0 = __ldg(a.row_ptr + slot), e1 = __ldg(a.row_ptr + slot + 1);
-  const long out0 = static_cast<long>(blockIdx.x) * kEqValid;
-  const long s0 = out0 - kEqHalf;
-  for (int t = threadIdx.x; t < kEqFft; t += blockDim.x) {
-    const long pos = s0 + t;
-    buf[t] = (pos >= 0 && pos < a.length) ? gather2(a, e0, e1, b, pos) : make_float2(0.f, 0.f);
+  const long out0 = static_cast<long>(blockIdx.x) * kEqOut;
+  const long s0 = out0 - (kEqHalf + 1);
+  const long boff = static_cast<long>(b) * 2 * a.length;
+  const bool vec = (a.length & 3) == 0;
+  for (int t4 = threadIdx.x; t4 < kEqFft / 4; t4 += blockDim.x) {
+    const long pos = s0 + 4 * t4;
+    float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
+    if (vec && pos >= 0 && pos + 4 <= a.length) {
+      for (int e = e0; e < e1; ++e) {
+        const float* p = a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff + pos;
+        l = f4add(l, __ldg(reinterpret_cast<const float4*>(p)));
+        r = f4add(r, __ldg(reinterpret_cast<const float4*>(p + a.length)));
+      }
+    } else {
+      float lv[4] = {0.f, 0.f, 0.f, 0.f}, rv[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (pos + u >= 0 && pos + u < a.length) {
+          const float2 v = gather2(a, e0, e1, b, pos + u);
+          lv[u] = v.x;
+          rv[u] = v.y;
+        }
+      }
+      l = make_float4(lv[0], lv[1], lv[2], lv[3]);
+      r = make_float4(rv[0], rv[1], rv[2], rv[3]);
+    }
+    buf[sidx(4 * t4)] = make_float2(l.x, r.x);
+    buf[sidx(4 * t4 + 1)] = make_float2(l.y, r.y);
+    buf[sidx(4 * t4 + 2)] = make_float2(l.z, r.z);
+    buf[sidx(4 * t4 + 3)] = make_float2(l.w, r.w);
   }
   __syncthreads();
-  fft_pow2<kLogFft, 1, 512, -1>(buf, kEqFft);
-  const float* r = resp + static_cast<long>(slot) * kEqFft;
-  for (int t = threadIdx.x; t < kEqFft; t += blockDim.x) buf[t] = cscale(buf[t], __ldg(r + t));
+  fft_pow2<kLogFft, 1, 512, -1>(buf, kEqBuf, a.tw);
+  const float* rs = resp + static_cast<long>(slot) * kEqFft;
+  for (int t = threadIdx.x; t < kEqFft; t += blockDim.x) buf[sidx(t)] = cscale(buf[sidx(t)], __ldg(rs + t));
   __syncthreads();
-  fft_pow2<kLogFft, 1, 512, +1>(buf, kEqFft);
-  float* yl = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length;
+  fft_pow2<kLogFft, 1, 512, +1>(buf, kEqBuf, a.tw);
+  float* yl = a.dst + static_cast<long>(slot) * a.rowstride + boff;
   float* yr = yl + a.length;
-  for (int t = threadIdx.x; t < kEqValid; t += blockDim.x) {
-    const long pos = out0 + t;
-    if (pos < a.length) {
-      const float2 v = buf[kEqHalf + t];
-      yl[pos] = v.x;
-      yr[pos] = v.y;
+  for (int t4 = threadIdx.x; t4 < kEqOut / 4; t4 += blockDim.x) {
+    const long pos = out0 + 4 * t4;
+    const int w = kEqHalf + 1 + 4 * t4;
+    const float2 v0 = buf[sidx(w)], v1 = buf[sidx(w + 1)], v2 = buf[sidx(w + 2)], v3 = buf[sidx(w + 3)];
+    if (vec && pos + 4 <= a.length) {
+      *reinterpret_cast<float4*>(yl + pos) = make_float4(v0.x, v1.x, v2.x, v3.x);
+      *reinterpret_cast<float4*>(yr + pos) = make_float4(v0.y, v1.y, v2.y, v3.y);
+    } else {
+      const float2 vv[4] = {v0, v1, v2, v3};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (pos + u < a.length) {
+          yl[pos + u] = vv[u].x;
+          yr[pos + u] = vv[u].y;
+        }
+      }
     }
   }
 }
 
 }  // namespace
 
-void launch_eq(const StepArgs& a, float* taps_ws, float* resp_ws, cudaStream_t s) {
+void eq_setup() {
+  static const bool done = [] {
+    cudaFuncSetAttribute(eq_response, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqSmem);
+    cudaFuncSetAttribute(eq_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqSmem);
+    cudaFuncSetAttribute(eq_conv, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    return true;
+  }();
+  (void)done;
+}
+
+void launch_eq_prologue(const StepArgs& a, float* taps_ws, float* resp_ws, cudaStream_t s) {
   if (a.slots == 0) return;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(eq_response, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqFft * 8);
-    cudaFuncSetAttribute(eq_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqFft * 8);
-    configured = true;
-  }
-  eq_design<<<dim3(4, a.slots), 256, 0, s>>>(a.params, taps_ws);
-  eq_response<<<a.slots, 512, kEqFft * 8, s>>>(taps_ws, resp_ws);
-  if (a.batch == 0 || a.length == 0) return;
-  const long blocks = (a.length + kEqValid - 1) / kEqValid;
-  eq_conv<<<dim3(static_cast<unsigned>(blocks), a.slots * a.batch), 512, kEqFft * 8, s>>>(a, resp_ws);
+  eq_setup();
+  // taps_ws holds [slots][2048] floats followed by [slots][1024] doubles of magnitudes.
+  auto* mags = reinterpret_cast<double*>(taps_ws + 2048L * a.slots);
+  eq_mags<<<a.slots, kEqHalf + 1, 0, s>>>(a.params, mags);
+  eq_design<<<dim3(1024 / (256 / kDesignSplit), a.slots), 256, 0, s>>>(mags, taps_ws, cos_table(a.tw));
+  eq_response<<<a.slots, 512, kEqSmem, s>>>(taps_ws, resp_ws, a.tw);
+}
+
+void launch_eq_main(const StepArgs& a, const float* resp_ws, cudaStream_t s) {
+  if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
+  eq_setup();
+  const long blocks = (a.length + kEqOut - 1) / kEqOut;
+  eq_conv<<<dim3(static_cast<unsigned>(blocks), a.slots * a.batch), 512, kEqSmem, s>>>(a, resp_ws);
 }
 
 }  // namespace mgb

@@ -5,8 +5,7 @@
 // the register-resident radix-R DFTs have constant twiddles. A pass reads every butterfly
 // input into registers, barriers, then writes the outputs in place (Stockham auto-sort:
 // natural order in, natural order out, no bit reversal). Pass twiddles
-// exp(dir*2*pi*i * j*r / (Ns*R)) come from sincospif (full fp32 accuracy) for the powers
-// r = 1, 2, 4 (and 8) and at most two complex products for the rest.
+// exp(dir*2*pi*i * j*r / (Ns*R)) are read from a precomputed fp64-rounded table.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -84,6 +83,31 @@ struct Dft<8, DIR> {
 };
 
 template <int DIR>
+struct Dft<16, DIR> {
+  static __device__ __forceinline__ void run(float2* v) {
+    float2 e[8], o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      e[k] = v[2 * k];
+      o[k] = v[2 * k + 1];
+    }
+    Dft<8, DIR>::run(e);
+    Dft<8, DIR>::run(o);
+    // o[k] *= exp(dir*2*pi*i*k/16)
+    constexpr float c1 = 0.92387953251128675613f, s1 = 0.38268343236508977173f, h = 0.70710678118654752440f;
+    constexpr float cs[8] = {1.f, c1, h, s1, 0.f, -s1, -h, -c1};
+    constexpr float sn[8] = {0.f, s1, h, c1, 1.f, c1, h, s1};
+#pragma unroll
+    for (int k = 1; k < 8; ++k) o[k] = cmul(o[k], make_float2(cs[k], DIR * sn[k]));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      v[k] = cadd(e[k], o[k]);
+      v[k + 8] = csub(e[k], o[k]);
+    }
+  }
+};
+
+template <int DIR>
 struct Dft<3, DIR> {
   static __device__ __forceinline__ void run(float2* v) {
     constexpr float c = -0.5f;
@@ -113,15 +137,83 @@ __device__ __forceinline__ void pass_twiddles(float x, float2* w) {
   }
 }
 
+// Forward twiddle table: tw[k] = exp(-2*pi*i*k / kTwN), fp32 rounded from fp64, built once
+// per device (twiddle_table() in tables.cu). Every pow2 transform up to kTwN points reads its
+// pass twiddles from it (L1-resident, 64 KiB) instead of evaluating sin/cos per butterfly.
+constexpr int kTwN = 8192;
+
+// Bank-conflict-free smem layout for pow2 transforms: one float2 of padding per 16 elements.
+// With the radix-16 first pass below, every Stockham pass then reads 16-aligned runs and
+// writes either runs of >= 16 (NS >= 16) or the stride-17 pattern of the first pass — both
+// hit 16 distinct 8-byte bank pairs per half-warp.
+__host__ __device__ constexpr int sidx(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int padded(int n) { return n + (n >> 4); }
+
 // One Stockham pass of radix R over COUNT independent transforms of size N held in smem
 // at buf[f*FSTRIDE + i]; NS = product of earlier radices; NTHR threads participate.
-template <int N, int R, int NS, int COUNT, int NTHR, int DIR>
-__device__ __forceinline__ void stockham_pass(float2* buf, int fstride) {
+// Twiddles exp(dir*2*pi*i * jm*r / (NS*R)) come from `tw` when given (N | kTwN), else sincospif.
+// Table twiddles for one butterfly: loads w^1, w^2, w^4, w^8 (as many as R needs) from the
+// forward table at stride `step` and conjugates them for the inverse transform.
+template <int R, int DIR>
+struct TwBase {
+  float2 w[4];
+  __device__ __forceinline__ void load(const float2* __restrict__ tw, int step) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if ((1 << i) < R) {
+        float2 v = tw[step << i];
+        if (DIR > 0) v.y = -v.y;
+        w[i] = v;
+      }
+    }
+  }
+  // v[r] *= w^r for r = 1..R-1 (w^3 = w w^2, w^5..w^7 via w^4, w^9..w^15 via w^8: <= 3 products)
+  __device__ __forceinline__ void apply(float2* v) const {
+    float2 p[16];
+    p[1] = w[0];
+    if constexpr (R > 2) p[2] = w[1];
+    if constexpr (R > 3) p[3] = cmul(w[0], w[1]);
+    if constexpr (R > 4) {
+      p[4] = w[2];
+      p[5] = cmul(p[1], p[4]);
+      p[6] = cmul(p[2], p[4]);
+      p[7] = cmul(p[3], p[4]);
+    }
+    if constexpr (R > 8) {
+      p[8] = w[3];
+#pragma unroll
+      for (int r = 9; r < 16; ++r) p[r] = cmul(p[r - 8], p[8]);
+    }
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], p[r]);
+  }
+};
+
+// One Stockham pass of radix R over COUNT independent transforms of size N held in smem
+// at buf[f*fstride + i] (padded layout when PAD); NS = product of earlier radices; NTHR
+// threads participate. Twiddles exp(dir*2*pi*i * jm*r / (NS*R)) come from the table `tw`
+// (TWN entries) when given, else sincospif; table loads are issued before the barrier-
+// separated smem reads so their latency overlaps them.
+template <int N, int R, int NS, int COUNT, int NTHR, int DIR, int TWN = kTwN, bool PAD = true>
+__device__ __forceinline__ void stockham_pass(float2* buf, int fstride, const float2* __restrict__ tw) {
   constexpr int M = N / R;                 // butterflies per transform
   constexpr int TOTAL = COUNT * M;
   constexpr int PER = (TOTAL + NTHR - 1) / NTHR;
   const int tid = threadIdx.x;
   float2 v[PER][R];
+  TwBase<R, DIR> twb[PER];
+  if constexpr (NS > 1) {
+    if (tw != nullptr) {
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int b = tid + q * NTHR;
+        if (TOTAL % NTHR == 0 || b < TOTAL) {
+          const int j = b % M;
+          twb[q].load(tw, (j % NS) * (TWN / (NS * R)));
+        }
+      }
+    }
+  }
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
     const int b = tid + q * NTHR;
@@ -129,7 +221,7 @@ __device__ __forceinline__ void stockham_pass(float2* buf, int fstride) {
       const int f = b / M, j = b - f * M;
       const float2* base = buf + f * fstride;
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[q][r] = base[j + r * M];
+      for (int r = 0; r < R; ++r) v[q][r] = base[PAD ? sidx(j + r * M) : j + r * M];
     }
   }
   __syncthreads();
@@ -140,45 +232,53 @@ __device__ __forceinline__ void stockham_pass(float2* buf, int fstride) {
       const int f = b / M, j = b - f * M;
       const int jm = j % NS;
       if constexpr (NS > 1) {
-        float2 w[R];
-        pass_twiddles<R, DIR>(2.f * static_cast<float>(jm) / static_cast<float>(NS * R), w);
+        if (tw != nullptr) {
+          twb[q].apply(v[q]);
+        } else {
+          float2 w[R];
+          pass_twiddles<R, DIR>(2.f * static_cast<float>(jm) / static_cast<float>(NS * R), w);
 #pragma unroll
-        for (int r = 1; r < R; ++r) v[q][r] = cmul(v[q][r], w[r]);
+          for (int r = 1; r < R; ++r) v[q][r] = cmul(v[q][r], w[r]);
+        }
       }
       Dft<R, DIR>::run(v[q]);
-      float2* base = buf + f * fstride + (j / NS) * NS * R + jm;
+      float2* base = buf + f * fstride;
+      const int o0 = (j / NS) * NS * R + jm;
 #pragma unroll
-      for (int r = 0; r < R; ++r) base[r * NS] = v[q][r];
+      for (int r = 0; r < R; ++r) base[PAD ? sidx(o0 + r * NS) : o0 + r * NS] = v[q][r];
     }
   }
   __syncthreads();
 }
 
-// Power-of-two FFT: radix-8 passes, finishing with radix 4/2 (or 4+4 when 16 remain).
+// Power-of-two FFT on the padded layout: a radix-16 first pass, then radix-8 passes,
+// finishing with radix 4/2 (or 4+4 when 16 remain). Element i of transform f lives at
+// buf[f*fstride + sidx(i)].
 template <int LOG2N, int LOGNS, int COUNT, int NTHR, int DIR>
 struct Pow2Fft {
-  static __device__ __forceinline__ void run(float2* buf, int fstride) {
+  static __device__ __forceinline__ void run(float2* buf, int fstride, const float2* tw) {
     constexpr int REM = LOG2N - LOGNS;
     if constexpr (REM > 0) {
-      constexpr int RL = (REM == 4 || REM == 2) ? 2 : (REM == 1 ? 1 : 3);
-      stockham_pass<(1 << LOG2N), (1 << RL), (1 << LOGNS), COUNT, NTHR, DIR>(buf, fstride);
-      Pow2Fft<LOG2N, LOGNS + RL, COUNT, NTHR, DIR>::run(buf, fstride);
+      constexpr int RL = (LOGNS == 0 && REM >= 4) ? 4 : ((REM == 4 || REM == 2) ? 2 : (REM == 1 ? 1 : 3));
+      stockham_pass<(1 << LOG2N), (1 << RL), (1 << LOGNS), COUNT, NTHR, DIR>(buf, fstride, tw);
+      Pow2Fft<LOG2N, LOGNS + RL, COUNT, NTHR, DIR>::run(buf, fstride, tw);
     }
   }
 };
 
 template <int LOG2N, int COUNT, int NTHR, int DIR>
-__device__ __forceinline__ void fft_pow2(float2* buf, int fstride) {
-  Pow2Fft<LOG2N, 0, COUNT, NTHR, DIR>::run(buf, fstride);
+__device__ __forceinline__ void fft_pow2(float2* buf, int fstride, const float2* tw) {
+  static_assert((1 << LOG2N) <= kTwN, "pow2 smem FFT larger than the twiddle table");
+  Pow2Fft<LOG2N, 0, COUNT, NTHR, DIR>::run(buf, fstride, tw);
 }
 
-// 384 = 3 * 8 * 4 * 4 (reverb STFT frames).
+// 384 = 3 * 8 * 4 * 4 (reverb STFT frames); tw384[k] = exp(-2*pi*i*k/384), usually in smem.
 template <int COUNT, int NTHR, int DIR>
-__device__ __forceinline__ void fft_384(float2* buf, int fstride) {
-  stockham_pass<384, 3, 1, COUNT, NTHR, DIR>(buf, fstride);
-  stockham_pass<384, 8, 3, COUNT, NTHR, DIR>(buf, fstride);
-  stockham_pass<384, 4, 24, COUNT, NTHR, DIR>(buf, fstride);
-  stockham_pass<384, 4, 96, COUNT, NTHR, DIR>(buf, fstride);
+__device__ __forceinline__ void fft_384(float2* buf, int fstride, const float2* tw384) {
+  stockham_pass<384, 3, 1, COUNT, NTHR, DIR, 384, false>(buf, fstride, tw384);
+  stockham_pass<384, 8, 3, COUNT, NTHR, DIR, 384, false>(buf, fstride, tw384);
+  stockham_pass<384, 4, 24, COUNT, NTHR, DIR, 384, false>(buf, fstride, tw384);
+  stockham_pass<384, 4, 96, COUNT, NTHR, DIR, 384, false>(buf, fstride, tw384);
 }
 
 }  // namespace mgb

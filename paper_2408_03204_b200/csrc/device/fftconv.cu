@@ -32,23 +32,6 @@ constexpr int kColThreads = 512;
 
 inline std::size_t align256(std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255); }
 
-struct ConvWs {
-  float2* ir;
-  float2* P;
-  float2* X;
-};
-
-ConvWs carve(void* ws, const ConvGeom& g, int slots, long taps) {
-  char* p = static_cast<char*>(ws);
-  ConvWs w;
-  w.ir = reinterpret_cast<float2*>(p);
-  p += align256(sizeof(float2) * static_cast<std::size_t>(slots) * taps);
-  w.P = reinterpret_cast<float2*>(p);
-  p += align256(sizeof(float2) * static_cast<std::size_t>(slots) * g.n);
-  w.X = reinterpret_cast<float2*>(p);
-  return w;
-}
-
 enum class ColSrc { Kernel, Signal };
 
 // ---- pass 1: column FFTs (forward) ------------------------------------------------------
@@ -58,7 +41,7 @@ __global__ void __launch_bounds__(kColThreads) cols_fwd(StepArgs a, const float2
                                                         float2* out) {
   constexpr int N1 = 1 << LN1;
   constexpr int C = kColElems / N1;
-  constexpr int FS = N1 + 1;
+  constexpr int FS = padded(N1) + 1;
   extern __shared__ float2 tile[];
   const int log_n2 = log_n - LN1;
   const long N2 = 1L << log_n2;
@@ -74,25 +57,42 @@ __global__ void __launch_bounds__(kColThreads) cols_fwd(StepArgs a, const float2
     e1 = __ldg(a.row_ptr + slot + 1);
     len = a.length;
   }
-  for (int idx = threadIdx.x; idx < kColElems; idx += kColThreads) {
+  // Stage all of this thread's loads in registers before any smem store (max loads in flight).
+  constexpr int EPT = kColElems / kColThreads;
+  float2 vals[EPT];
+  const float* one = nullptr;  // in-degree-1 fast path
+  if constexpr (SRC == ColSrc::Signal) {
+    if (e1 - e0 == 1) one = a.src + static_cast<long>(__ldg(a.col + e0)) * a.rowstride + static_cast<long>(b) * 2 * a.length;
+  }
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) {
+    const int idx = threadIdx.x + q * kColThreads;
     const int c = idx % C, n1 = idx / C;
     const long n = static_cast<long>(n1) * N2 + col0 + c;
     float2 v = make_float2(0.f, 0.f);
     if (n < len) {
-      if constexpr (SRC == ColSrc::Signal) v = gather2(a, e0, e1, b, n);
-      else v = __ldg(ir + static_cast<long>(item) * taps + n);
+      if constexpr (SRC == ColSrc::Signal) {
+        v = one ? make_float2(__ldg(one + n), __ldg(one + a.length + n)) : gather2(a, e0, e1, b, n);
+      } else {
+        v = __ldg(ir + static_cast<long>(item) * taps + n);
+      }
     }
-    tile[c * FS + n1] = v;
+    vals[q] = v;
+  }
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) {
+    const int idx = threadIdx.x + q * kColThreads;
+    tile[(idx % C) * FS + sidx(idx / C)] = vals[q];
   }
   __syncthreads();
-  fft_pow2<LN1, C, kColThreads, -1>(tile, FS);
+  fft_pow2<LN1, C, kColThreads, -1>(tile, FS, a.tw);
   float2* o = out + static_cast<long>(item) * N;
   const float inv_n = 2.f / static_cast<float>(N);
   for (int idx = threadIdx.x; idx < kColElems; idx += kColThreads) {
     const int c = idx % C, k1 = idx / C;
     const long n2 = col0 + c;
     const float2 w = expi_pi(-static_cast<float>(n2 * k1) * inv_n);
-    o[static_cast<long>(k1) * N2 + n2] = cmul(tile[c * FS + k1], w);
+    o[static_cast<long>(k1) * N2 + n2] = cmul(tile[c * FS + sidx(k1)], w);
   }
 }
 
@@ -101,7 +101,7 @@ template <int LN1>
 __global__ void __launch_bounds__(kColThreads) cols_inv(StepArgs a, int log_n, const float2* X) {
   constexpr int N1 = 1 << LN1;
   constexpr int C = kColElems / N1;
-  constexpr int FS = N1 + 1;
+  constexpr int FS = padded(N1) + 1;
   extern __shared__ float2 tile[];
   const long N2 = 1L << (log_n - LN1);
   const long N = 1L << log_n;
@@ -111,17 +111,17 @@ __global__ void __launch_bounds__(kColThreads) cols_inv(StepArgs a, int log_n, c
   const float2* x = X + static_cast<long>(item) * N;
   for (int idx = threadIdx.x; idx < kColElems; idx += kColThreads) {
     const int c = idx % C, k1 = idx / C;
-    tile[c * FS + k1] = x[static_cast<long>(k1) * N2 + col0 + c];
+    tile[c * FS + sidx(k1)] = x[static_cast<long>(k1) * N2 + col0 + c];
   }
   __syncthreads();
-  fft_pow2<LN1, C, kColThreads, +1>(tile, FS);
+  fft_pow2<LN1, C, kColThreads, +1>(tile, FS, a.tw);
   float* yl = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length;
   float* yr = yl + a.length;
   for (int idx = threadIdx.x; idx < kColElems; idx += kColThreads) {
     const int c = idx % C, n1 = idx / C;
     const long n = static_cast<long>(n1) * N2 + col0 + c;
     if (n < a.length) {
-      const float2 v = tile[c * FS + n1];
+      const float2 v = tile[c * FS + sidx(n1)];
       yl[n] = v.x;
       yr[n] = v.y;
     }
@@ -144,22 +144,22 @@ constexpr int row_threads() {
 
 // Forward row FFTs of the packed kernel; one row per CTA. grid (N1, slots)
 template <int LN2>
-__global__ void __launch_bounds__(row_threads<LN2>()) rows_spec(int log_n, float2* P) {
+__global__ void __launch_bounds__(row_threads<LN2>()) rows_spec(int log_n, float2* P, const float2* tw) {
   constexpr int N2 = 1 << LN2;
   constexpr int NT = row_threads<LN2>();
   extern __shared__ float2 row[];
   const long N = 1L << log_n;
   float2* p = P + static_cast<long>(blockIdx.y) * N + static_cast<long>(blockIdx.x) * N2;
-  for (int i = threadIdx.x; i < N2; i += NT) row[i] = p[i];
+  for (int i = threadIdx.x; i < N2; i += NT) row[sidx(i)] = p[i];
   __syncthreads();
-  fft_pow2<LN2, 1, NT, -1>(row, N2);
-  for (int i = threadIdx.x; i < N2; i += NT) p[i] = row[i];
+  fft_pow2<LN2, 1, NT, -1>(row, padded(N2), tw);
+  for (int i = threadIdx.x; i < N2; i += NT) p[i] = row[sidx(i)];
 }
 
 // Signal rows k1 = r and N1 - r together: forward FFTs, channel-split product with the
 // kernel spectrum, inverse FFTs, inverse four-step twiddle. grid (N1/2 + 1, slots*B)
 template <int LN2>
-__global__ void __launch_bounds__(row_threads<LN2>()) rows_conv(int log_n, int batch, float2* X, const float2* P) {
+__global__ void __launch_bounds__(row_threads<LN2>()) rows_conv(int log_n, int batch, float2* X, const float2* P, const float2* tw) {
   constexpr int N2 = 1 << LN2;
   constexpr int NT = row_threads<LN2>();
   extern __shared__ float2 rows[];  // [2][N2]
@@ -173,30 +173,47 @@ __global__ void __launch_bounds__(row_threads<LN2>()) rows_conv(int log_n, int b
   float2* xb = X + static_cast<long>(item) * N + static_cast<long>(rb) * N2;
   const float2* pa = P + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
   const float2* pb = P + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
+  constexpr int RS = padded(N2);  // second row's offset
   for (int i = threadIdx.x; i < N2; i += NT) {
-    rows[i] = xa[i];
-    rows[N2 + i] = xb[i];
+    rows[sidx(i)] = xa[i];
+    rows[RS + sidx(i)] = xb[i];
   }
   __syncthreads();
-  fft_pow2<LN2, 2, NT, -1>(rows, N2);
+  // The kernel spectrum values this thread pairs are fetched before the forward FFT so
+  // their latency hides behind it.
+  constexpr int KPT = (N2 + NT - 1) / NT;
+  float2 pkv[KPT], pov[KPT];
+#pragma unroll
+  for (int q = 0; q < KPT; ++q) {
+    const int k = threadIdx.x + q * NT;
+    if (k < N2) {
+      const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
+      pkv[q] = __ldg(pa + k);
+      pov[q] = __ldg(pb + kb);
+    }
+  }
+  fft_pow2<LN2, 2, NT, -1>(rows, RS, tw);
   const float s = 0.25f / static_cast<float>(N);
-  for (int k = threadIdx.x; k < N2; k += NT) {
+#pragma unroll
+  for (int q = 0; q < KPT; ++q) {
+    const int k = threadIdx.x + q * NT;
+    if (k >= N2) continue;
     const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
     if (self && kb < k) continue;
-    const float2 xk = rows[k], xo = rows[N2 + kb];
-    const float2 pk = __ldg(pa + k), po = __ldg(pb + kb);
+    const float2 xk = rows[sidx(k)], xo = rows[RS + sidx(kb)];
+    const float2 pk = pkv[q], po = pov[q];
     const float2 zk = zmix(xk, cconj(xo), pk, cconj(po), s);
     const float2 zo = zmix(xo, cconj(xk), po, cconj(pk), s);
-    rows[k] = zk;
-    rows[N2 + kb] = zo;
-    if (self) rows[kb] = zo;
+    rows[sidx(k)] = zk;
+    rows[RS + sidx(kb)] = zo;
+    if (self) rows[sidx(kb)] = zo;
   }
   __syncthreads();
-  fft_pow2<LN2, 2, NT, +1>(rows, N2);
+  fft_pow2<LN2, 2, NT, +1>(rows, RS, tw);
   const float inv_n = 2.f / static_cast<float>(N);
   for (int i = threadIdx.x; i < N2; i += NT) {
-    xa[i] = cmul(rows[i], expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n));
-    if (!self) xb[i] = cmul(rows[N2 + i], expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n));
+    xa[i] = cmul(rows[sidx(i)], expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n));
+    if (!self) xb[i] = cmul(rows[RS + sidx(i)], expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n));
   }
 }
 
@@ -205,13 +222,19 @@ template <int LN1>
 void cols_fwd_t(ColSrc src, const StepArgs& a, const float2* ir, long taps, const ConvGeom& g, int items,
                 float2* out, cudaStream_t s) {
   constexpr int C = kColElems / (1 << LN1);
-  constexpr int smem = C * ((1 << LN1) + 1) * 8;
+  constexpr int smem = C * (padded(1 << LN1) + 1) * 8;
   const dim3 grid(static_cast<unsigned>((1L << g.log_n2) / C), static_cast<unsigned>(items));
-  if (src == ColSrc::Signal) {
+  static const bool done = [] {
     cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::Signal>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::Kernel>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::Signal>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::Kernel>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    return true;
+  }();
+  (void)done;
+  if (src == ColSrc::Signal) {
     cols_fwd<LN1, ColSrc::Signal><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out);
   } else {
-    cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::Kernel>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cols_fwd<LN1, ColSrc::Kernel><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out);
   }
 }
@@ -219,24 +242,34 @@ void cols_fwd_t(ColSrc src, const StepArgs& a, const float2* ir, long taps, cons
 template <int LN1>
 void cols_inv_t(const StepArgs& a, const ConvGeom& g, const float2* X, cudaStream_t s) {
   constexpr int C = kColElems / (1 << LN1);
-  constexpr int smem = C * ((1 << LN1) + 1) * 8;
+  constexpr int smem = C * (padded(1 << LN1) + 1) * 8;
   const dim3 grid(static_cast<unsigned>((1L << g.log_n2) / C), static_cast<unsigned>(a.slots * a.batch));
-  cudaFuncSetAttribute(cols_inv<LN1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  static const bool done = [] {
+    cudaFuncSetAttribute(cols_inv<LN1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(cols_inv<LN1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    return true;
+  }();
+  (void)done;
   cols_inv<LN1><<<grid, kColThreads, smem, s>>>(a, g.log_n, X);
 }
 
 template <int LN2>
-void rows_spec_t(const ConvGeom& g, int slots, float2* P, cudaStream_t s) {
+void rows_spec_t(const ConvGeom& g, int slots, float2* P, const float2* tw, cudaStream_t s) {
   const dim3 grid(static_cast<unsigned>(1L << g.log_n1), static_cast<unsigned>(slots));
-  rows_spec<LN2><<<grid, row_threads<LN2>(), (1 << LN2) * 8, s>>>(g.log_n, P);
+  rows_spec<LN2><<<grid, row_threads<LN2>(), padded(1 << LN2) * 8, s>>>(g.log_n, P, tw);
 }
 
 template <int LN2>
-void rows_conv_t(const ConvGeom& g, int items, int batch, float2* X, const float2* P, cudaStream_t s) {
-  constexpr int smem = 2 * (1 << LN2) * 8;
-  cudaFuncSetAttribute(rows_conv<LN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+void rows_conv_t(const ConvGeom& g, int items, int batch, float2* X, const float2* P, const float2* tw,
+                 cudaStream_t s) {
+  constexpr int smem = 2 * padded(1 << LN2) * 8;
+  static const bool done = [] {
+    cudaFuncSetAttribute(rows_conv<LN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    return true;
+  }();
+  (void)done;
   const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(items));
-  rows_conv<LN2><<<grid, row_threads<LN2>(), smem, s>>>(g.log_n, batch, X, P);
+  rows_conv<LN2><<<grid, row_threads<LN2>(), smem, s>>>(g.log_n, batch, X, P, tw);
 }
 
 #define MGB_DISPATCH_LN(var, FN, ...)                  \
@@ -251,14 +284,10 @@ void rows_conv_t(const ConvGeom& g, int items, int batch, float2* X, const float
     default: throw std::invalid_argument("fft convolution size out of range"); \
   }
 
-// Spectrum of the packed kernels already written to w.ir, then the signal convolution.
-void run_conv(const StepArgs& a, const ConvGeom& g, const ConvWs& w, long taps, cudaStream_t s) {
-  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Kernel, a, w.ir, taps, g, a.slots, w.P, s);
-  MGB_DISPATCH_LN(g.log_n2, rows_spec_t, g, a.slots, w.P, s);
-  if (a.batch == 0 || a.length == 0) return;
-  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, a, nullptr, 0, g, a.slots * a.batch, w.X, s);
-  MGB_DISPATCH_LN(g.log_n2, rows_conv_t, g, a.slots * a.batch, a.batch, w.X, w.P, s);
-  MGB_DISPATCH_LN(g.log_n1, cols_inv_t, a, g, w.X, s);
+// Kernel spectrum P (four-step order) of the packed kernels in `ir` ([slots][taps]).
+void kernel_spectrum(const StepArgs& a, const ConvGeom& g, const float2* ir, long taps, float2* P, cudaStream_t s) {
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Kernel, a, ir, taps, g, a.slots, P, s);
+  MGB_DISPATCH_LN(g.log_n2, rows_spec_t, g, a.slots, P, a.tw, s);
 }
 
 // ---- reverb impulse response (masked noise STFT -> ISTFT) ----------------------------------
@@ -267,14 +296,31 @@ constexpr int kRevParamBins = 192;
 constexpr int kRevFpc = 8;         // output hops per CTA
 constexpr int kRevThreads = 256;
 
-// grid (ceil(frames / kRevFpc), slots)
+// grid (ceil(frames / kRevFpc), slots). Each CTA inverse-transforms frames m0-1 .. m0+7
+// (mid and side packed as one complex transform each) and overlap-adds hops m0 .. m0+7.
 __global__ void __launch_bounds__(kRevThreads) reverb_ir(const double* params, ReverbConst rc, float2* ir,
                                                          long ir_stride) {
   __shared__ float2 fr[(kRevFpc + 1) * 384];
   __shared__ float gain[2][kRevFpc + 1][kRevBins];
+  __shared__ float2 tw384[384];
+  __shared__ float inv_cover[2][192];  // [first hop | later hops]: 1 / (384 * sum of Hann windows)
   const int slot = blockIdx.y;
   const double* row = params + static_cast<long>(slot) * 4 * kRevParamBins;
   const int m_first = blockIdx.x * kRevFpc - 1;
+  for (int k = threadIdx.x; k < 384; k += kRevThreads) {
+    double sn, cs;
+    sincospi(-2.0 * k / 384.0, &sn, &cs);
+    tw384[k] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
+    if (k < 192) {
+      // dsp.cpp:165-190: periodic Hann cover, out = cover > 1e-8 ? sum / cover : 0.
+      double s0, c0, s1, c1;
+      sincospi(2.0 * k / 384.0, &s0, &c0);
+      sincospi(2.0 * (k + 192) / 384.0, &s1, &c1);
+      const double w0 = 0.5 - 0.5 * c0, w1 = 0.5 - 0.5 * c1;
+      inv_cover[0][k] = w0 > 1e-8 ? static_cast<float>(1.0 / (384.0 * w0)) : 0.f;
+      inv_cover[1][k] = (w0 + w1) > 1e-8 ? static_cast<float>(1.0 / (384.0 * (w0 + w1))) : 0.f;
+    }
+  }
   for (int idx = threadIdx.x; idx < 2 * (kRevFpc + 1) * kRevBins; idx += kRevThreads) {
     const int which = idx / ((kRevFpc + 1) * kRevBins);
     const int rem = idx - which * (kRevFpc + 1) * kRevBins;
@@ -282,7 +328,8 @@ __global__ void __launch_bounds__(kRevThreads) reverb_ir(const double* params, R
     const int m = m_first + f;
     const int bin = k < kRevParamBins ? k : kRevParamBins - 1;
     const double* color = row + which * 2 * kRevParamBins;
-    gain[which][f][k] = (m < 0 || m >= rc.frames) ? 0.f : static_cast<float>(exp(color[bin] + m * color[kRevParamBins + bin]));
+    // exp(H0 + m * Hdecay), exponent formed in fp64 (processors.cpp:171-175)
+    gain[which][f][k] = (m < 0 || m >= rc.frames) ? 0.f : expf(static_cast<float>(color[bin] + m * color[kRevParamBins + bin]));
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < (kRevFpc + 1) * 384; idx += kRevThreads) {
@@ -292,8 +339,8 @@ __global__ void __launch_bounds__(kRevThreads) reverb_ir(const double* params, R
     if (m >= 0 && m < rc.frames) {
       const bool upper = k > 192;
       const int kk = upper ? 384 - k : k;
-      float2 M = cscale(rc.stft_mid[static_cast<long>(m) * kRevBins + kk], gain[0][f][kk]);
-      float2 S = cscale(rc.stft_side[static_cast<long>(m) * kRevBins + kk], gain[1][f][kk]);
+      float2 M = cscale(__ldg(rc.stft_mid + static_cast<long>(m) * kRevBins + kk), gain[0][f][kk]);
+      float2 S = cscale(__ldg(rc.stft_side + static_cast<long>(m) * kRevBins + kk), gain[1][f][kk]);
       if (upper) {
         M = cconj(M);
         S = cconj(S);
@@ -303,7 +350,7 @@ __global__ void __launch_bounds__(kRevThreads) reverb_ir(const double* params, R
     fr[idx] = z;
   }
   __syncthreads();
-  fft_384<kRevFpc + 1, kRevThreads, +1>(fr, 384);
+  fft_384<kRevFpc + 1, kRevThreads, +1>(fr, 384, tw384);
   const long i0 = static_cast<long>(blockIdx.x) * kRevFpc * 192;
   for (int t = threadIdx.x; t < kRevFpc * 192; t += kRevThreads) {
     const long i = i0 + t;
@@ -311,20 +358,11 @@ __global__ void __launch_bounds__(kRevThreads) reverb_ir(const double* params, R
     const int o = t % 192;
     const int f1 = t / 192 + 1;  // local frame starting in this hop
     float2 v = fr[f1 * 384 + o];
-    double cover;
-    {
-      double sn, cs;
-      sincospi(2.0 * o / 384.0, &sn, &cs);
-      cover = 0.5 - 0.5 * cs;
-    }
+    float sc = inv_cover[0][o];
     if (i >= 192) {
-      const float2 u = fr[(f1 - 1) * 384 + o + 192];
-      v = cadd(v, u);
-      double sn, cs;
-      sincospi(2.0 * (o + 192) / 384.0, &sn, &cs);
-      cover += 0.5 - 0.5 * cs;
+      v = cadd(v, fr[(f1 - 1) * 384 + o + 192]);
+      sc = inv_cover[1][o];
     }
-    const float sc = cover > 1e-8 ? static_cast<float>(1.0 / (384.0 * cover)) : 0.f;
     const float mid = v.x * sc, side = v.y * sc;
     ir[static_cast<long>(slot) * ir_stride + i] = make_float2(0.5f * (mid + side), 0.5f * (mid - side));
   }
@@ -467,10 +505,13 @@ ConvGeom conv_geom(long length, long taps) {
   return g;
 }
 
-std::size_t conv_workspace_bytes(const ConvGeom& g, int slots, int batch, long taps) {
+std::size_t conv_prologue_bytes(const ConvGeom& g, int slots, long taps) {
   return align256(sizeof(float2) * static_cast<std::size_t>(slots) * taps) +
-         align256(sizeof(float2) * static_cast<std::size_t>(slots) * g.n) +
-         align256(sizeof(float2) * static_cast<std::size_t>(slots) * batch * g.n);
+         align256(sizeof(float2) * static_cast<std::size_t>(slots) * g.n);
+}
+
+std::size_t conv_main_bytes(const ConvGeom& g, int slots, int batch) {
+  return align256(sizeof(float2) * static_cast<std::size_t>(slots) * batch * g.n);
 }
 
 void launch_reverb_ir(const double* params, int slots, const ReverbConst& rc, float2* ir, long ir_stride,
@@ -483,27 +524,37 @@ void launch_reverb_ir(const double* params, int slots, const ReverbConst& rc, fl
 void launch_delay_ir(const double* params, int slots, const DelayConst& dc, float2* ir, long ir_stride,
                      cudaStream_t s) {
   if (slots == 0) return;
-  for (int i = 0; i < slots; ++i) {
-    cudaMemsetAsync(ir + static_cast<long>(i) * ir_stride, 0, sizeof(float2) * static_cast<std::size_t>(dc.span), s);
+  if (ir_stride == dc.span) {
+    cudaMemsetAsync(ir, 0, sizeof(float2) * static_cast<std::size_t>(slots) * dc.span, s);
+  } else {
+    for (int i = 0; i < slots; ++i) {
+      cudaMemsetAsync(ir + static_cast<long>(i) * ir_stride, 0, sizeof(float2) * static_cast<std::size_t>(dc.span), s);
+    }
   }
   delay_ir<<<slots, 1024, 0, s>>>(params, dc, ir, ir_stride);
 }
 
-void launch_reverb(const StepArgs& a, const ReverbConst& rc, void* ws, cudaStream_t s) {
+void launch_conv_prologue(bool reverb, const StepArgs& a, const ReverbConst& rc, const DelayConst& dc, void* ws,
+                          cudaStream_t s) {
   if (a.slots == 0) return;
-  const ConvGeom g = conv_geom(a.length, rc.length);
-  const ConvWs w = carve(ws, g, a.slots, rc.length);
-  launch_reverb_ir(a.params, a.slots, rc, w.ir, rc.length, s);
-  run_conv(a, g, w, rc.length, s);
+  const long taps = reverb ? rc.length : dc.span;
+  const ConvGeom g = conv_geom(a.length, taps);
+  auto* ir = static_cast<float2*>(ws);
+  auto* P = reinterpret_cast<float2*>(static_cast<char*>(ws) + align256(sizeof(float2) * static_cast<std::size_t>(a.slots) * taps));
+  if (reverb) launch_reverb_ir(a.params, a.slots, rc, ir, taps, s);
+  else launch_delay_ir(a.params, a.slots, dc, ir, taps, s);
+  kernel_spectrum(a, g, ir, taps, P, s);
 }
 
-void launch_delay(const StepArgs& a, const DelayConst& dc, void* ws, cudaStream_t s) {
-  if (a.slots == 0) return;
-  const ConvGeom g = conv_geom(a.length, dc.span);
-  const ConvWs w = carve(ws, g, a.slots, dc.span);
-  cudaMemsetAsync(w.ir, 0, sizeof(float2) * static_cast<std::size_t>(a.slots) * dc.span, s);
-  delay_ir<<<a.slots, 1024, 0, s>>>(a.params, dc, w.ir, dc.span);
-  run_conv(a, g, w, dc.span, s);
+void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, void* ws, cudaStream_t s) {
+  if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
+  const ConvGeom g = conv_geom(a.length, taps);
+  const auto* P = reinterpret_cast<const float2*>(static_cast<const char*>(prologue_ws) +
+                                                  align256(sizeof(float2) * static_cast<std::size_t>(a.slots) * taps));
+  auto* X = static_cast<float2*>(ws);
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, a, nullptr, 0, g, a.slots * a.batch, X, s);
+  MGB_DISPATCH_LN(g.log_n2, rows_conv_t, g, a.slots * a.batch, a.batch, X, P, a.tw, s);
+  MGB_DISPATCH_LN(g.log_n1, cols_inv_t, a, g, X, s);
 }
 
 void launch_noise_stft(const double* noise, long length, int frames, float2* out, cudaStream_t s) {

@@ -14,12 +14,13 @@ enum class PointOp : int { Copy = 0, Gain = 1, Imager = 2 };
 // Gather-sum + copy / gain / imager + store (mix, out, gain, imager steps).
 void launch_pointwise(PointOp op, const StepArgs& a, cudaStream_t s);
 
-// EQ: FIR design (fp64 cosine sum, `dsp.cpp:106-136`) -> 8192-bin zero-phase response ->
-// overlap-save convolution fused with the gather and the store.
+// EQ: FIR design (fp64 cosine sum, `dsp.cpp:106-136`) -> 8192-bin zero-phase response
+// (prologue: parameters only) ; overlap-save convolution fused with gather and store (main).
 constexpr int kEqFft = 8192;
 constexpr int kEqHalf = 1023;
 constexpr int kEqValid = kEqFft - 2 * kEqHalf;
-void launch_eq(const StepArgs& a, float* taps_ws /*slots*2048*/, float* resp_ws /*slots*8192*/, cudaStream_t s);
+void launch_eq_prologue(const StepArgs& a, float* taps_ws /*slots*2048*/, float* resp_ws /*slots*8192*/, cudaStream_t s);
+void launch_eq_main(const StepArgs& a, const float* resp_ws, cudaStream_t s);
 
 // Compressor / noisegate: chained (decoupled look-back) scan of the energy envelope.
 constexpr int kDynThreads = 256;
@@ -35,7 +36,6 @@ struct ConvGeom {
   long n = 0;
 };
 ConvGeom conv_geom(long length, long taps);
-std::size_t conv_workspace_bytes(const ConvGeom& g, int slots, int batch, long taps);
 
 struct ReverbConst {
   const float2* stft_mid;  // [frames][193]
@@ -48,8 +48,14 @@ struct DelayConst {
   int window;
 };
 
-void launch_reverb(const StepArgs& a, const ReverbConst& rc, void* ws, cudaStream_t s);
-void launch_delay(const StepArgs& a, const DelayConst& dc, void* ws, cudaStream_t s);
+// Prologue (parameters only): impulse responses + their spectra into `ws`
+// (conv_prologue_bytes). Main (audio): gather -> FFT -> product -> inverse -> arena, using
+// the prologue's spectra and a transient buffer of conv_main_bytes.
+std::size_t conv_prologue_bytes(const ConvGeom& g, int slots, long taps);
+std::size_t conv_main_bytes(const ConvGeom& g, int slots, int batch);
+void launch_conv_prologue(bool reverb, const StepArgs& a, const ReverbConst& rc, const DelayConst& dc, void* ws,
+                          cudaStream_t s);
+void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, void* ws, cudaStream_t s);
 
 // Kernel-only entry points (for ProcessorSet::reverb_kernel / delay_kernel).
 void launch_reverb_ir(const double* params, int slots, const ReverbConst& rc, float2* ir, long ir_stride,
@@ -59,6 +65,13 @@ void launch_delay_ir(const double* params, int slots, const DelayConst& dc, floa
 
 // Noise STFT for the reverb (ProcessorSet construction, `processors.cpp:151-160`).
 void launch_noise_stft(const double* noise, long length, int frames, float2* out, cudaStream_t s);
+
+// Per-device constant tables, built on first use with a synchronous upload (call it before
+// any stream capture; ProcessorSet does): kTwN forward twiddles (float2), followed by
+// kCosN doubles cos(2 pi m / 2047) for the EQ FIR design (cos_table()).
+constexpr int kCosN = 2047;
+const float2* twiddle_table(int device);
+inline const double* cos_table(const float2* tw) { return reinterpret_cast<const double*>(tw + 8192); }
 
 // Arena conversion helpers for the host-buffer API.
 void launch_f64_to_f32(const double* in, float* out, long n, cudaStream_t s);

@@ -50,15 +50,21 @@ __global__ void __launch_bounds__(256) pointwise_vec4(StepArgs a) {
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n4; i += static_cast<long>(gridDim.x) * blockDim.x) {
     float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
     int e = e0;
-    for (; e + 1 < e1; e += 2) {  // two edges in flight
-      const float4* p0 = reinterpret_cast<const float4*>(a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff);
-      const float4* p1 = reinterpret_cast<const float4*>(a.src + static_cast<long>(__ldg(a.col + e + 1)) * a.rowstride + boff);
-      const float4 l0 = __ldg(p0 + i), r0 = __ldg(p0 + n4 + i);
-      const float4 l1 = __ldg(p1 + i), r1 = __ldg(p1 + n4 + i);
-      l = f4add(f4add(l, l0), l1);
-      r = f4add(f4add(r, r0), r1);
+    for (; e + 3 < e1; e += 4) {  // four edges (8 loads) in flight; sums stay in edge order
+      float4 lv[4], rv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float4* p = reinterpret_cast<const float4*>(a.src + static_cast<long>(__ldg(a.col + e + u)) * a.rowstride + boff);
+        lv[u] = __ldg(p + i);
+        rv[u] = __ldg(p + n4 + i);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        l = f4add(l, lv[u]);
+        r = f4add(r, rv[u]);
+      }
     }
-    if (e < e1) {
+    for (; e < e1; ++e) {
       const float4* p0 = reinterpret_cast<const float4*>(a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff);
       l = f4add(l, __ldg(p0 + i));
       r = f4add(r, __ldg(p0 + n4 + i));
@@ -94,8 +100,9 @@ void launch_op(const StepArgs& a, cudaStream_t s) {
   if (rows == 0 || a.length == 0) return;
   const bool vec = (a.length % 4) == 0;
   const long items = vec ? a.length / 4 : a.length;
-  // ~2 float4 groups per thread per row keeps >= 8 loads in flight per thread at deg 1.
-  long blocks = (items + 256 * 2 - 1) / (256 * 2);
+  // One float4 group per thread when that is needed to fill ~4 CTAs per SM, else two.
+  const long per = static_cast<long>(rows) * ((items + 255) / 256) < 4 * 148 ? 1 : 2;
+  long blocks = (items + 256 * per - 1) / (256 * per);
   if (blocks < 1) blocks = 1;
   if (blocks > 4096) blocks = 4096;
   dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(rows));

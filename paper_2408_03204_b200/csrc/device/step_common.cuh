@@ -20,6 +20,7 @@ struct StepArgs {
   const int* row_ptr;    // [slots+1]
   const int* col;        // [nnz] source rows
   const double* params;  // first parameter row of the step (row-major, width per type)
+  const float2* tw;      // twiddle table (fft_smem.cuh kTwN entries)
   int slots;
   int batch;
   long length;           // L

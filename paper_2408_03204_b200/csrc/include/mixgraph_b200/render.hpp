@@ -133,8 +133,21 @@ class DevicePlan {
   std::size_t workspace_bytes(int batch, long length, const ProcessorSet& procs) const;
   int kernels_per_render(int batch, long length) const;
 
+  // Workspace: one persistent region per step for its parameter-only prologue, then one
+  // transient region shared by every step's audio pass.
+  struct Layout {
+    std::vector<std::size_t> prologue_off;
+    std::size_t main_off = 0;
+    std::size_t total = 0;
+  };
+  Layout layout(int batch, long length, const ProcessorSet& procs) const;
+  cudaStream_t aux_stream() const { return aux_; }
+  const cudaEvent_t* events() const { return events_.data(); }
+
  private:
   const RenderData& rd_;
+  cudaStream_t aux_ = nullptr;
+  std::vector<cudaEvent_t> events_;  // [0] fork, [k+1] prologue of step k done
   int* d_index_ = nullptr;
   std::vector<long> rp_off_, col_off_;
   std::vector<int> zero_rows_;
@@ -149,6 +162,6 @@ void render_host(const RenderData& rd, const ProcessorSet& processors, const Par
 
 void render_arena(const DevicePlan& plan, const ProcessorSet& processors, const double* const* param_tables,
                   float* arena, int batch, long length, void* workspace, std::size_t workspace_bytes,
-                  cudaStream_t stream, cudaEvent_t* step_events = nullptr);
+                  cudaStream_t stream, cudaEvent_t* step_events = nullptr, bool hoist = true);
 
 }  // namespace mixgraph

@@ -66,6 +66,16 @@ class DeviceRenderer:
                                     ctypes.c_void_p(s.cuda_stream)))
         return self.outputs
 
+    def capture(self) -> "torch.cuda.CUDAGraph":
+        """Capture one full render (main stream + the side-stream prologues) as a CUDA graph;
+        replay() re-runs it on the current arena, parameters and workspace pointers."""
+        self.render()  # one-time kernel attribute setup happens outside the capture
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.render()
+        return g
+
     def render_profiled(self, stream: Optional[torch.cuda.Stream] = None, sync: bool = False) -> Optional[np.ndarray]:
         """Same as render() with CUDA events around every step on the launching stream. With
         sync=True, waits and returns per-step device times (ms, one per RenderData step)."""
