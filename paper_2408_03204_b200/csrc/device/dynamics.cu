@@ -8,11 +8,11 @@
 // The truncated FIR is exactly the linear recurrence
 //     g[n] = a*g[n-1] + (1-a)*(e[n] - a^Ne * e[n-Ne]),   g[-1] = 0,
 // so instead of the reference's 2^18-point FFTs per (node, batch) this is a scan of affine
-// maps x -> A x + B. Tile = 256 threads x 16 samples. Within a tile: per-thread serial
+// maps x -> A x + B. Tile = 256 threads x 8 samples. Within a tile: per-thread serial
 // recurrence, warp shuffles, one smem level. Across tiles: decoupled look-back over a
 // per-tile status word (flag | fp32 value) in a single 64-bit store; tile order comes from
 // an atomic ticket so every waited-on tile was scheduled earlier. All aggregates of full
-// tiles share A = a^4096, so a status word only needs B. The look-back stops as soon as the
+// tiles share A = a^2048, so a status word only needs B. The look-back stops as soon as the
 // accumulated multiplier underflows to 0 (it does within a few tiles for a <= 0.999).
 // The a^Ne correction term re-gathers e[n - Ne]; it is skipped when a^Ne < 1e-30.
 #include <cuda/atomic>
@@ -76,7 +76,7 @@ __device__ __forceinline__ float gain_of(float g, const DynParams& p) {
   return expf(gy - gu);
 }
 
-// Gather-sum of the slot's inputs at 16 consecutive samples starting at n0 (n0 % 16 == 0).
+// Gather-sum of the slot's inputs at kDynPerThread consecutive samples from n0.
 template <bool VEC>
 __device__ __forceinline__ void load16(const StepArgs& a, int e0, int e1, int b, long n0, float* ul, float* ur) {
 #pragma unroll
@@ -116,7 +116,7 @@ __device__ __forceinline__ void compose(float& A, float& B, float Ap, float Bp) 
 }
 
 template <bool GATE, bool VEC>
-__global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_taps, double floor_, int tiles_per_seq,
+__global__ void __launch_bounds__(kDynThreads, 4) dyn_scan(StepArgs a, int env_taps, double floor_, int tiles_per_seq,
                                                          unsigned long long* status, unsigned int* ticket) {
   __shared__ float wA[kDynThreads / 32], wB[kDynThreads / 32];
   __shared__ float s_carry;
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
 
   if (warp == 0) {
     // Warp-parallel decoupled look-back: lane l inspects tile (tile-1-l) of this sequence,
-    // weight A^l with A = a^4096; stop at the nearest inclusive prefix or once A^l underflows.
+    // weight A^l with A = a^2048 (a^tile); stop at the nearest inclusive prefix or once A^l underflows.
     cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> mine(status[tk]);
     float carry = 0.f;
     if (tile > 0) {

@@ -29,9 +29,8 @@ constexpr int kEqOut = 6144;  // outputs per block (of the 8192 - 2046 = 6146 no
 constexpr int kEqSmem = kEqBuf * 8;
 
 // Taps by the exact cosine sum raw[j] = (m0 + 2 sum_{k=1}^{1023} m_k cos(2 pi k j / 2047)) / 2047
-// in fp64. One warp per tap j; lane l sums k in [1 + 32 l, 32 l + 32] with the Chebyshev
-// recurrence c_{k+1} = 2 cos(theta) c_k - c_{k-1} started from the fp64 cos table (error
-// ~1e-14 over 32 steps); lanes are reduced with xor-shuffles in a fixed order.
+// in fp64. One warp per tap j; each lane runs a 32-term Chebyshev recurrence started from
+// the fp64 cos table (error ~1e-12); lanes are reduced with xor-shuffles in a fixed order.
 // grid (1024 / 8, slots) x 256 threads (8 taps per CTA).
 constexpr int kDesignSplit = 32;
 // exp of the 1024 log-magnitudes of every slot, once (fp64). grid (slots) x 1024.
@@ -45,16 +44,17 @@ __global__ void __launch_bounds__(256) eq_design(const double* __restrict__ mag_
   const int slot = blockIdx.y;
   for (int k = threadIdx.x; k <= kEqHalf; k += blockDim.x) mags[k] = __ldg(mag_g + static_cast<long>(slot) * (kEqHalf + 1) + k);
   __syncthreads();
+  // Lane l sums k = 1 + l + 32 i (i < 32, k <= 1023): consecutive lanes read consecutive
+  // magnitudes (no bank conflicts); the stride-32 recurrence is
+  // cos((k + 32) t) = 2 cos(32 t) cos(k t) - cos((k - 32) t).
   const int lane = threadIdx.x & 31;
   const int j = blockIdx.x * (256 / kDesignSplit) + threadIdx.x / kDesignSplit;  // 0..1023
-  const int k0 = 1 + 32 * lane;
-  const int k1 = lane == 31 ? kEqHalf : k0 + 31;
-  double c_prev = __ldg(cos_tab + (static_cast<long>(k0 - 1) * j) % kN);
-  double c_cur = __ldg(cos_tab + (static_cast<long>(k0) * j) % kN);
-  const double two_c = 2.0 * __ldg(cos_tab + j);
+  double c_prev = __ldg(cos_tab + (static_cast<long>(31 - lane) * j) % kN);  // cos((1 + l - 32) t)
+  double c_cur = __ldg(cos_tab + (static_cast<long>(1 + lane) * j) % kN);
+  const double two_c = 2.0 * __ldg(cos_tab + (32L * j) % kN);
   double acc = 0.0;
 #pragma unroll 4
-  for (int k = k0; k <= k1; ++k) {
+  for (int k = 1 + lane; k <= kEqHalf; k += 32) {
     acc = fma(mags[k], c_cur, acc);
     const double nxt = fma(two_c, c_cur, -c_prev);
     c_prev = c_cur;

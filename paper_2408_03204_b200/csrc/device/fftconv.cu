@@ -37,7 +37,7 @@ enum class ColSrc { Kernel, Signal };
 // ---- pass 1: column FFTs (forward) ------------------------------------------------------
 // grid (N2 / C, items); item = slot (kernel) or slot*B + b (signal).
 template <int LN1, ColSrc SRC>
-__global__ void __launch_bounds__(kColThreads) cols_fwd(StepArgs a, const float2* ir, long taps, int log_n,
+__global__ void __launch_bounds__(kColThreads, 2) cols_fwd(StepArgs a, const float2* ir, long taps, int log_n,
                                                         float2* out) {
   constexpr int N1 = 1 << LN1;
   constexpr int C = kColElems / N1;
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kColThreads) cols_fwd(StepArgs a, const float2
 
 // ---- pass 3 (last): inverse column FFTs, store into the arena --------------------------
 template <int LN1>
-__global__ void __launch_bounds__(kColThreads) cols_inv(StepArgs a, int log_n, const float2* X) {
+__global__ void __launch_bounds__(kColThreads, 2) cols_inv(StepArgs a, int log_n, const float2* X) {
   constexpr int N1 = 1 << LN1;
   constexpr int C = kColElems / N1;
   constexpr int FS = padded(N1) + 1;
@@ -109,9 +109,17 @@ __global__ void __launch_bounds__(kColThreads) cols_inv(StepArgs a, int log_n, c
   const int slot = item / a.batch, b = item - slot * a.batch;
   const long col0 = static_cast<long>(blockIdx.x) * C;
   const float2* x = X + static_cast<long>(item) * N;
-  for (int idx = threadIdx.x; idx < kColElems; idx += kColThreads) {
-    const int c = idx % C, k1 = idx / C;
-    tile[c * FS + sidx(k1)] = x[static_cast<long>(k1) * N2 + col0 + c];
+  constexpr int EPT = kColElems / kColThreads;
+  float2 vals[EPT];
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) {
+    const int idx = threadIdx.x + q * kColThreads;
+    vals[q] = __ldg(x + static_cast<long>(idx / C) * N2 + col0 + idx % C);
+  }
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) {
+    const int idx = threadIdx.x + q * kColThreads;
+    tile[(idx % C) * FS + sidx(idx / C)] = vals[q];
   }
   __syncthreads();
   fft_pow2<LN1, C, kColThreads, +1>(tile, FS, a.tw);

@@ -24,7 +24,7 @@ void launch_eq_main(const StepArgs& a, const float* resp_ws, cudaStream_t s);
 
 // Compressor / noisegate: chained (decoupled look-back) scan of the energy envelope.
 constexpr int kDynThreads = 256;
-constexpr int kDynPerThread = 16;
+constexpr int kDynPerThread = 8;
 constexpr int kDynTile = kDynThreads * kDynPerThread;
 std::size_t dyn_workspace_bytes(int slots, int batch, long length);
 void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double energy_floor, void* ws,
