@@ -9,11 +9,11 @@
 //     g[n] = a*g[n-1] + (1-a)*(e[n] - a^Ne * e[n-Ne]),   g[-1] = 0,
 // so instead of the reference's 2^18-point FFTs per (node, batch) this is a scan of affine
 // maps x -> A x + B. Tile = 256 threads x 8 samples. Within a tile: per-thread serial
-// recurrence, warp shuffles, one smem level. Across tiles: decoupled look-back over a
-// per-tile status word (flag | fp32 value) in a single 64-bit store; tile order comes from
-// an atomic ticket so every waited-on tile was scheduled earlier. All aggregates of full
-// tiles share A = a^2048, so a status word only needs B. The look-back stops as soon as the
-// accumulated multiplier underflows to 0 (it does within a few tiles for a <= 0.999).
+// recurrence, warp shuffles, one smem level. Across tiles: every tile publishes its
+// aggregate (flag | fp32 B in one 64-bit store; all full tiles share A = a^2048) and sums
+// its predecessors' aggregates in a fixed order (see the carry block), so results are
+// bit-reproducible; tile order comes from an atomic ticket so every waited-on tile was
+// scheduled earlier.
 // The a^Ne correction term re-gathers e[n - Ne]; it is skipped when a^Ne < 1e-30.
 #include <cuda/atomic>
 
@@ -24,7 +24,6 @@ namespace mgb {
 namespace {
 
 constexpr unsigned long long kFlagAgg = 1ull << 32;
-constexpr unsigned long long kFlagInc = 2ull << 32;
 
 struct DynParams {
   float a, oma, aN, a16, atile;
@@ -194,44 +193,32 @@ __global__ void __launch_bounds__(kDynThreads, 4) dyn_scan(StepArgs a, int env_t
     compose(xA, xB, pA, pB);
   }
   const float tileB = wB[kDynThreads / 32 - 1];
-  const float tileA = wA[kDynThreads / 32 - 1];
 
   if (warp == 0) {
-    // Warp-parallel decoupled look-back: lane l inspects tile (tile-1-l) of this sequence,
-    // weight A^l with A = a^2048 (a^tile); stop at the nearest inclusive prefix or once A^l underflows.
+    // Cross-tile carry, deterministic: publish this tile's aggregate B, then
+    //   carry = sum_{d >= 0} A^d * B_{tile-1-d},   A = a^tile_len,
+    // summed lane-strided (d = lane + 32 i) and tree-reduced in a fixed order. Only
+    // aggregates are read (no chain of inclusive prefixes), so no tile waits on another
+    // tile's look-back, and the value never depends on timing. Windows stop once the
+    // largest remaining weight A^d underflows to exactly 0 (all later terms are +0).
     cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> mine(status[tk]);
-    float carry = 0.f;
-    if (tile > 0) {
-      if (lane == 0) mine.store(kFlagAgg | __float_as_uint(tileB), cuda::memory_order_relaxed);
-      const float wl = powf(p.atile, static_cast<float>(lane));
-      const float w32 = powf(p.atile, 32.f);
-      float mult = 1.f;
-      int base = tk - 1, remaining = tile;
-      while (true) {
-        const bool valid = lane < remaining;
-        unsigned long long w = 0;
-        if (valid) {
-          cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[base - lane]);
-          do {
-            w = st.load(cuda::memory_order_relaxed);
-          } while ((w >> 32) == 0);
-        }
-        const unsigned inc = __ballot_sync(0xffffffffu, valid && (w & ~0xffffffffull) == kFlagInc);
-        const int first = inc ? __ffs(inc) - 1 : 32;
-        float part = (valid && lane <= first) ? wl * __uint_as_float(static_cast<unsigned int>(w & 0xffffffffu)) : 0.f;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-        carry = fmaf(mult, part, carry);
-        mult *= w32;
-        if (inc || remaining <= 32 || mult == 0.f) break;
-        base -= 32;
-        remaining -= 32;
+    if (lane == 0) mine.store(kFlagAgg | __float_as_uint(tileB), cuda::memory_order_relaxed);
+    float part = 0.f;
+    for (int d0 = 0; d0 < tile; d0 += 32) {
+      if (powf(p.atile, static_cast<float>(d0)) == 0.f) break;
+      const int d = d0 + lane;
+      if (d < tile) {
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[tk - 1 - d]);
+        unsigned long long w;
+        do {
+          w = st.load(cuda::memory_order_relaxed);
+        } while ((w >> 32) == 0);
+        part = fmaf(powf(p.atile, static_cast<float>(d)), __uint_as_float(static_cast<unsigned int>(w & 0xffffffffu)), part);
       }
     }
-    if (lane == 0) {
-      mine.store(kFlagInc | __float_as_uint(fmaf(tileA, carry, tileB)), cuda::memory_order_relaxed);
-      s_carry = carry;
-    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+    if (lane == 0) s_carry = part;
   }
   __syncthreads();
 
