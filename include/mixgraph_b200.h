@@ -39,6 +39,7 @@ extern "C" {
 
 typedef struct mg_plan mg_plan;             /* RenderData (+ its device step table) */
 typedef struct mg_processors mg_processors; /* ProcessorSet (device constants) */
+typedef struct mg_graph mg_graph;           /* one captured device render (CUDA graph) */
 
 const char* mg_last_error(void);
 int32_t mg_abi_version(void);
@@ -102,6 +103,15 @@ int32_t mg_render_arena(const mg_plan* plan, const mg_processors* procs, const d
 int32_t mg_render_arena_profiled(const mg_plan* plan, const mg_processors* procs, const double* const* d_tables,
                                  float* d_arena, int32_t batch, int64_t length, void* d_workspace,
                                  uint64_t workspace_bytes, void* stream, float* step_ms);
+
+/* Capture one device render (same arguments as mg_render_arena) into a CUDA graph whose
+ * kernel nodes keep their stream priorities (main path high, parameter prologues low);
+ * mg_render_graph_launch replays it on `stream`. Arena, tables and workspace are baked in. */
+int32_t mg_render_graph_create(const mg_plan* plan, const mg_processors* procs, const double* const* d_tables,
+                               float* d_arena, int32_t batch, int64_t length, void* d_workspace,
+                               uint64_t workspace_bytes, mg_graph** out);
+int32_t mg_render_graph_launch(const mg_graph* graph, void* stream);
+void mg_render_graph_destroy(mg_graph* graph);
 
 /* ProcessorSet::process (processors.cpp:229-282): in/out [slots][B][2][L] host double;
  * params [param_rows][width] (NULL for in/out/mix). */

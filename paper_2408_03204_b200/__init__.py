@@ -68,6 +68,9 @@ _sig("mg_plan_workspace_bytes", _i32, _vp, _vp, _i32, _i64, _P(_u64))
 _sig("mg_plan_kernel_count", _i32, _vp, _i32, _i64, _P(_i32))
 _sig("mg_render_arena", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp)
 _sig("mg_render_arena_profiled", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp, _vp)
+_sig("mg_render_graph_create", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _P(_vp))
+_sig("mg_render_graph_launch", _i32, _vp, _vp)
+_sig("mg_render_graph_destroy", None, _vp)
 _sig("mg_process", _i32, _vp, _i32, _vp, _vp, _i32, _i32, _i64, _vp, _i32, _i32)
 _sig("mg_reverb_kernel", _i32, _vp, _vp, _vp, _vp)
 _sig("mg_delay_kernel", _i32, _vp, _vp, _i32, _vp, _vp)

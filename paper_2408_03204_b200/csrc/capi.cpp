@@ -30,6 +30,10 @@ struct mg_plan {
   }
 };
 
+struct mg_graph {
+  std::unique_ptr<RenderGraph> g;
+};
+
 struct mg_processors {
   std::unique_ptr<ProcessorSet> ps;
 };
@@ -326,6 +330,25 @@ int32_t mg_render_arena_profiled(const mg_plan* cp, const mg_processors* procs, 
     }
   });
 }
+
+int32_t mg_render_graph_create(const mg_plan* p, const mg_processors* procs, const double* const* d_tables,
+                               float* d_arena, int32_t batch, int64_t length, void* d_ws, uint64_t ws_bytes,
+                               mg_graph** out) {
+  return guarded([&] {
+    DevicePlan& dp = device_plan(p);
+    std::scoped_lock lock(const_cast<mg_plan*>(p)->render_mu);
+    auto g = std::make_unique<mg_graph>();
+    g->g = std::make_unique<RenderGraph>(dp, *procs->ps, d_tables, d_arena, batch, static_cast<long>(length), d_ws,
+                                         ws_bytes);
+    *out = g.release();
+  });
+}
+
+int32_t mg_render_graph_launch(const mg_graph* g, void* stream) {
+  return guarded([&] { g->g->launch(static_cast<cudaStream_t>(stream)); });
+}
+
+void mg_render_graph_destroy(mg_graph* g) { delete g; }
 
 int32_t mg_process(const mg_processors* procs, int32_t t, const double* in, double* out, int32_t slots, int32_t batch,
                    int64_t length, const double* params, int32_t param_rows, int32_t param_offset) {

@@ -8,9 +8,9 @@
 // The truncated FIR is exactly the linear recurrence
 //     g[n] = a*g[n-1] + (1-a)*(e[n] - a^Ne * e[n-Ne]),   g[-1] = 0,
 // so instead of the reference's 2^18-point FFTs per (node, batch) this is a scan of affine
-// maps x -> A x + B. Tile = 256 threads x 8 samples. Within a tile: per-thread serial
+// maps x -> A x + B. Tile = 512 threads x 8 samples. Within a tile: per-thread serial
 // recurrence, warp shuffles, one smem level. Across tiles: every tile publishes its
-// aggregate (flag | fp32 B in one 64-bit store; all full tiles share A = a^2048) and sums
+// aggregate (flag | fp32 B in one 64-bit store; all full tiles share A = a^4096) and sums
 // its predecessors' aggregates in a fixed order (see the carry block), so results are
 // bit-reproducible; tile order comes from an atomic ticket so every waited-on tile was
 // scheduled earlier.
@@ -115,15 +115,18 @@ __device__ __forceinline__ void compose(float& A, float& B, float Ap, float Bp) 
 }
 
 template <bool GATE, bool VEC>
-__global__ void __launch_bounds__(kDynThreads, 4) dyn_scan(StepArgs a, int env_taps, double floor_, int tiles_per_seq,
+__global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_taps, double floor_, int tiles_per_seq,
                                                          unsigned long long* status, unsigned int* ticket) {
   __shared__ float wA[kDynThreads / 32], wB[kDynThreads / 32];
   __shared__ float s_carry;
   __shared__ int s_ticket;
   if (threadIdx.x == 0) s_ticket = static_cast<int>(atomicAdd(ticket, 1u));
   __syncthreads();
+  // Tickets interleave sequences (all tile-0s, then all tile-1s, ...): a tile's
+  // predecessors were dispatched `nseq` tickets earlier, so the carry rarely waits.
   const int tk = s_ticket;
-  const int seq = tk / tiles_per_seq, tile = tk - seq * tiles_per_seq;
+  const int nseq = a.slots * a.batch;
+  const int tile = tk / nseq, seq = tk - tile * nseq;
   const int slot = seq / a.batch, b = seq - slot * a.batch;
   const int e0 = __ldg(a.row_ptr + slot), e1 = __ldg(a.row_ptr + slot + 1);
   const DynParams p = load_params(a.params + 4L * slot, env_taps, floor_, a.length);
@@ -201,14 +204,15 @@ __global__ void __launch_bounds__(kDynThreads, 4) dyn_scan(StepArgs a, int env_t
     // aggregates are read (no chain of inclusive prefixes), so no tile waits on another
     // tile's look-back, and the value never depends on timing. Windows stop once the
     // largest remaining weight A^d underflows to exactly 0 (all later terms are +0).
-    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> mine(status[tk]);
+    // status is indexed [seq][tile]
+    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> mine(status[static_cast<long>(seq) * tiles_per_seq + tile]);
     if (lane == 0) mine.store(kFlagAgg | __float_as_uint(tileB), cuda::memory_order_relaxed);
     float part = 0.f;
     for (int d0 = 0; d0 < tile; d0 += 32) {
       if (powf(p.atile, static_cast<float>(d0)) == 0.f) break;
       const int d = d0 + lane;
       if (d < tile) {
-        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[tk - 1 - d]);
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[static_cast<long>(seq) * tiles_per_seq + tile - 1 - d]);
         unsigned long long w;
         do {
           w = st.load(cuda::memory_order_relaxed);

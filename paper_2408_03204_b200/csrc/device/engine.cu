@@ -8,6 +8,8 @@
 // is what node reordering buys, `schedule.cpp:397-413`): no step_in/step_out buffers.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -171,7 +173,8 @@ ProcessorSet::~ProcessorSet() = default;
 namespace {
 
 mgb::ReverbConst reverb_const(const ProcessorSet& p) {
-  return {p.device().stft_mid, p.device().stft_side, p.device().frames, p.reverb_length()};
+  return {p.device().stft_mid, p.device().stft_side, p.device().frames, p.reverb_length(),
+          mgb::twiddle_table(p.device().device)};
 }
 mgb::DelayConst delay_const(const ProcessorSet& p) { return {p.delay_span(), p.delay_window()}; }
 
@@ -191,6 +194,7 @@ std::size_t prologue_bytes(NodeType t, int slots, long length, const ProcessorSe
 
 std::size_t main_bytes(NodeType t, int slots, int batch, long length, const ProcessorSet& p) {
   switch (t) {
+    case NodeType::Eq: return mgb::eq_spectrum_bytes(slots, batch, length);
     case NodeType::Compressor:
     case NodeType::Noisegate: return mgb::dyn_workspace_bytes(slots, batch, length);
     case NodeType::Reverb: return mgb::conv_main_bytes(mgb::conv_geom(length, p.reverb_length()), slots, batch);
@@ -285,7 +289,11 @@ DevicePlan::DevicePlan(const RenderData& rd) : rd_(rd) {
     cuda_check(cudaMalloc(&d_index_, sizeof(int) * host.size()), "cudaMalloc");
     cuda_check(cudaMemcpy(d_index_, host.data(), sizeof(int) * host.size(), cudaMemcpyHostToDevice), "H2D plan");
   }
-  cuda_check(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking), "cudaStreamCreate");
+  // Prologues are off the critical path: lowest priority, so the CTA scheduler prefers the
+  // main stream's kernels whenever both have work (honoured inside RenderGraph too).
+  int least = 0, greatest = 0;
+  cuda_check(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
+  cuda_check(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, least), "cudaStreamCreate");
   events_.resize(rd.steps.size() + 1);
   for (auto& ev : events_) cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
 }
@@ -359,9 +367,16 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
   // Parameter-only prologues (EQ design, reverb/delay impulse responses and their spectra)
   // depend on nothing the render computes: fork them onto the plan's side stream so they
   // overlap the earlier steps, and join each one right before its step's audio pass.
+  // MGB_NO_HOIST=1 runs every prologue inline (diagnostics: isolated per-step costs).
+  static const bool no_hoist = [] { const char* v = std::getenv("MGB_NO_HOIST"); return v && v[0] == '1'; }();
+  if (no_hoist) hoist = false;
+  // A first-step EQ starts its response-independent forward FFTs before the prologues are
+  // enqueued, so its grid reaches the GPU ahead of the side stream's grids.
+  const bool split_first = hoist && !rd.steps.empty() && rd.steps[0].type == NodeType::Eq;
   const cudaEvent_t* ev = plan.events();
   if (hoist) {
-    cuda_check(cudaEventRecord(ev[0], stream), "event");
+    cuda_check(cudaEventRecord(ev[0], stream), "event");  // fork point: before any render work
+    if (split_first) mgb::launch_eq_forward(args[0], reinterpret_cast<float2*>(ws + lay.main_off), stream);
     cuda_check(cudaStreamWaitEvent(plan.aux_stream(), ev[0], 0), "wait");
     for (std::size_t k = 0; k < rd.steps.size(); ++k) {
       if (!has_prologue(rd.steps[k].type)) continue;
@@ -371,14 +386,81 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
   }
   for (std::size_t k = 0; k < rd.steps.size(); ++k) {
     const NodeType t = rd.steps[k].type;
-    if (hoist && has_prologue(t)) cuda_check(cudaStreamWaitEvent(stream, ev[k + 1], 0), "wait");
+    char* pws = ws + lay.prologue_off[k];
+    char* mws = ws + lay.main_off;
+    // The first step has nothing to hide its prologue behind: an EQ there runs its
+    // response-independent forward FFTs before joining the prologue, the rest after.
+    const bool split_eq = hoist && k == 0 && t == NodeType::Eq;
     if (step_events) cuda_check(cudaEventRecord(step_events[2 * k], stream), "event");
-    if (!hoist) run_prologue(t, args[k], procs, ws + lay.prologue_off[k], stream);
-    run_main(t, args[k], procs, ws + lay.prologue_off[k], ws + lay.main_off, stream);
+    // (forward FFTs of a split first EQ were enqueued before the prologues, see above)
+    if (hoist && has_prologue(t)) cuda_check(cudaStreamWaitEvent(stream, ev[k + 1], 0), "wait");
+    if (!hoist) run_prologue(t, args[k], procs, pws, stream);
+    if (split_eq) {
+      mgb::launch_eq_inverse(args[k], reinterpret_cast<float*>(pws + eq_taps_bytes(args[k].slots)),
+                             reinterpret_cast<float2*>(mws), stream);
+    } else {
+      run_main(t, args[k], procs, pws, mws, stream);
+    }
     if (step_events) cuda_check(cudaEventRecord(step_events[2 * k + 1], stream), "event");
   }
   cuda_check(cudaGetLastError(), "render_arena launch");
 }
+
+// ---- RenderGraph ------------------------------------------------------------------------
+
+RenderGraph::RenderGraph(const DevicePlan& plan, const ProcessorSet& procs, const double* const* param_tables,
+                         float* arena, int batch, long length, void* workspace, std::size_t workspace_bytes) {
+  int least = 0, greatest = 0;
+  cuda_check(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
+  cudaStream_t cap = nullptr;
+  cuda_check(cudaStreamCreateWithPriority(&cap, cudaStreamNonBlocking, greatest), "cudaStreamCreate");
+  // One eager render first: one-time kernel attribute setup must not happen under capture.
+  render_arena(plan, procs, param_tables, arena, batch, length, workspace, workspace_bytes, cap);
+  cuda_check(cudaStreamSynchronize(cap), "warm-up render");
+  cuda_check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
+  try {
+    render_arena(plan, procs, param_tables, arena, batch, length, workspace, workspace_bytes, cap);
+  } catch (...) {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(cap, &g);
+    if (g) cudaGraphDestroy(g);
+    cudaStreamDestroy(cap);
+    throw;
+  }
+  cuda_check(cudaStreamEndCapture(cap, &graph_), "end capture");
+  cudaStreamDestroy(cap);
+  // Node priorities: prologue kernels (parameter-only, off the critical path) lowest, audio
+  // kernels highest, so when both are runnable the CTA scheduler serves the main path.
+  std::size_t n = 0;
+  cuda_check(cudaGraphGetNodes(graph_, nullptr, &n), "graph nodes");
+  std::vector<cudaGraphNode_t> nodes(n);
+  cuda_check(cudaGraphGetNodes(graph_, nodes.data(), &n), "graph nodes");
+  int low = 0, high = 0;
+  for (cudaGraphNode_t node : nodes) {
+    cudaGraphNodeType type;
+    cuda_check(cudaGraphNodeGetType(node, &type), "node type");
+    if (type != cudaGraphNodeTypeKernel) continue;
+    cudaKernelNodeParams kp{};
+    cuda_check(cudaGraphKernelNodeGetParams(node, &kp), "kernel params");
+    cudaLaunchAttributeValue v{};
+    const bool pro = mgb::is_prologue_kernel(kp.func);
+    v.priority = pro ? least : greatest;
+    (pro ? low : high)++;
+    cuda_check(cudaGraphKernelNodeSetAttribute(node, cudaLaunchAttributePriority, &v), "node priority");
+  }
+  if (const char* dbg = std::getenv("MGB_DEBUG"); dbg && dbg[0] == '1') {
+    std::fprintf(stderr, "[mgb] render graph: %zu nodes, %d prologue kernels (priority %d), %d main kernels (priority %d)\n",
+                 n, low, least, high, greatest);
+  }
+  cuda_check(cudaGraphInstantiateWithFlags(&exec_, graph_, cudaGraphInstantiateFlagUseNodePriority), "instantiate");
+}
+
+RenderGraph::~RenderGraph() {
+  if (exec_) cudaGraphExecDestroy(exec_);
+  if (graph_) cudaGraphDestroy(graph_);
+}
+
+void RenderGraph::launch(cudaStream_t stream) const { cuda_check(cudaGraphLaunch(exec_, stream), "graph launch"); }
 
 // ---- host-buffer API ----------------------------------------------------------------------
 
@@ -473,7 +555,7 @@ std::vector<double> ProcessorSet::delay_kernel(std::span<const double> params, i
   Engine& e = engine_for(dev_->device);
   const long span = delay_span_;
   auto* d_row = static_cast<double*>(e.params.ensure(sizeof(double) * param_width(NodeType::Delay)));
-  auto* d_ir = static_cast<float2*>(e.arena.ensure(sizeof(float2) * static_cast<std::size_t>(span) + 16));
+  auto* d_ir = static_cast<float2*>(e.arena.ensure(sizeof(float2) * static_cast<std::size_t>(span) + 40 * 40 * 4 + 16));
   cuda_check(cudaMemcpyAsync(d_row, params.data(), sizeof(double) * param_width(NodeType::Delay), cudaMemcpyHostToDevice, e.stream), "H2D");
   mgb::launch_delay_ir(d_row, 1, delay_const(*this), d_ir, span, e.stream);
   std::vector<float> h(static_cast<std::size_t>(2 * span));

@@ -91,7 +91,8 @@ __global__ void __launch_bounds__(512) eq_response(const float* taps, float* res
 // grid (blocks per signal, slots*B). Block covers outputs [out0, out0 + 6144) from the
 // 8192-sample window starting at out0 - 1024 (both 4-aligned: float4 loads/stores when
 // L % 4 == 0); the circular convolution is exact for window indices [1023, 7168].
-__global__ void __launch_bounds__(512, 2) eq_conv(StepArgs a, const float* resp) {
+template <int MODE>
+__global__ void __launch_bounds__(512, 2) eq_conv(StepArgs a, const float* resp, float2* spec) {
   extern __shared__ float2 buf[];
   const int sb = blockIdx.y;
   const int slot = sb / a.batch, b = sb - slot * a.batch;
@@ -100,6 +101,13 @@ __global__ void __launch_bounds__(512, 2) eq_conv(StepArgs a, const float* resp)
   const long s0 = out0 - (kEqHalf + 1);
   const long boff = static_cast<long>(b) * 2 * a.length;
   const bool vec = (a.length & 3) == 0;
+  float2* sp = spec + (static_cast<long>(sb) * gridDim.x + blockIdx.x) * kEqFft;  // MODE 1/2 scratch
+  const float* rs = resp + static_cast<long>(slot) * kEqFft;
+  if constexpr (MODE == 2) {
+    // spectrum computed earlier by MODE 1: load it with the response product fused
+    for (int t = threadIdx.x; t < kEqFft; t += blockDim.x) buf[sidx(t)] = cscale(__ldg(sp + t), __ldg(rs + t));
+    __syncthreads();
+  } else {
   for (int t4 = threadIdx.x; t4 < kEqFft / 4; t4 += blockDim.x) {
     const long pos = s0 + 4 * t4;
     float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
@@ -129,9 +137,13 @@ __global__ void __launch_bounds__(512, 2) eq_conv(StepArgs a, const float* resp)
   }
   __syncthreads();
   fft_pow2<kLogFft, 1, 512, -1>(buf, kEqBuf, a.tw);
-  const float* rs = resp + static_cast<long>(slot) * kEqFft;
+  if constexpr (MODE == 1) {
+    for (int t = threadIdx.x; t < kEqFft; t += blockDim.x) sp[t] = buf[sidx(t)];
+    return;
+  }
   for (int t = threadIdx.x; t < kEqFft; t += blockDim.x) buf[sidx(t)] = cscale(buf[sidx(t)], __ldg(rs + t));
   __syncthreads();
+  }
   fft_pow2<kLogFft, 1, 512, +1>(buf, kEqBuf, a.tw);
   float* yl = a.dst + static_cast<long>(slot) * a.rowstride + boff;
   float* yr = yl + a.length;
@@ -160,8 +172,10 @@ __global__ void __launch_bounds__(512, 2) eq_conv(StepArgs a, const float* resp)
 void eq_setup() {
   static const bool done = [] {
     cudaFuncSetAttribute(eq_response, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqSmem);
-    cudaFuncSetAttribute(eq_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqSmem);
-    cudaFuncSetAttribute(eq_conv, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    for (auto fn : {eq_conv<0>, eq_conv<1>, eq_conv<2>}) {
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqSmem);
+      cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
     return true;
   }();
   (void)done;
@@ -172,16 +186,40 @@ void launch_eq_prologue(const StepArgs& a, float* taps_ws, float* resp_ws, cudaS
   eq_setup();
   // taps_ws holds [slots][2048] floats followed by [slots][1024] doubles of magnitudes.
   auto* mags = reinterpret_cast<double*>(taps_ws + 2048L * a.slots);
+  note_prologue_kernel(reinterpret_cast<const void*>(eq_mags));
+  note_prologue_kernel(reinterpret_cast<const void*>(eq_design));
+  note_prologue_kernel(reinterpret_cast<const void*>(eq_response));
   eq_mags<<<a.slots, kEqHalf + 1, 0, s>>>(a.params, mags);
   eq_design<<<dim3(1024 / (256 / kDesignSplit), a.slots), 256, 0, s>>>(mags, taps_ws, cos_table(a.tw));
   eq_response<<<a.slots, 512, kEqSmem, s>>>(taps_ws, resp_ws, a.tw);
 }
 
+std::size_t eq_spectrum_bytes(int slots, int batch, long length) {
+  return sizeof(float2) * kEqFft * static_cast<std::size_t>(slots) * batch * ((length + kEqOut - 1) / kEqOut);
+}
+
+namespace {
+dim3 eq_grid(const StepArgs& a) {
+  return dim3(static_cast<unsigned>((a.length + kEqOut - 1) / kEqOut), static_cast<unsigned>(a.slots * a.batch));
+}
+}  // namespace
+
 void launch_eq_main(const StepArgs& a, const float* resp_ws, cudaStream_t s) {
   if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
   eq_setup();
-  const long blocks = (a.length + kEqOut - 1) / kEqOut;
-  eq_conv<<<dim3(static_cast<unsigned>(blocks), a.slots * a.batch), 512, kEqSmem, s>>>(a, resp_ws);
+  eq_conv<0><<<eq_grid(a), 512, kEqSmem, s>>>(a, resp_ws, nullptr);
+}
+
+void launch_eq_forward(const StepArgs& a, float2* spectrum, cudaStream_t s) {
+  if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
+  eq_setup();
+  eq_conv<1><<<eq_grid(a), 512, kEqSmem, s>>>(a, nullptr, spectrum);
+}
+
+void launch_eq_inverse(const StepArgs& a, const float* resp_ws, const float2* spectrum, cudaStream_t s) {
+  if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
+  eq_setup();
+  eq_conv<2><<<eq_grid(a), 512, kEqSmem, s>>>(a, resp_ws, const_cast<float2*>(spectrum));
 }
 
 }  // namespace mgb

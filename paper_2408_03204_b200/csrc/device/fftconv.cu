@@ -32,6 +32,11 @@ constexpr int kColThreads = 512;
 
 inline std::size_t align256(std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255); }
 
+// Packed impulse responses [slots][taps] float2, plus room for the delay tap records.
+inline std::size_t ir_bytes(int slots, long taps) {
+  return align256(sizeof(float2) * static_cast<std::size_t>(slots) * taps + sizeof(float) * 40 * 40 * slots);
+}
+
 enum class ColSrc { Kernel, Signal };
 
 // ---- pass 1: column FFTs (forward) ------------------------------------------------------
@@ -88,11 +93,12 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_fwd(StepArgs a, const flo
   fft_pow2<LN1, C, kColThreads, -1>(tile, FS, a.tw);
   float2* o = out + static_cast<long>(item) * N;
   const float inv_n = 2.f / static_cast<float>(N);
+#pragma unroll 4
   for (int idx = threadIdx.x; idx < kColElems; idx += kColThreads) {
     const int c = idx % C, k1 = idx / C;
     const long n2 = col0 + c;
-    const float2 w = expi_pi(-static_cast<float>(n2 * k1) * inv_n);
-    o[static_cast<long>(k1) * N2 + n2] = cmul(tile[c * FS + sidx(k1)], w);
+    // four-step twiddle exp(-2 pi i n2 k1 / N); n2 k1 < N <= 2^24 is exact in fp32
+    o[static_cast<long>(k1) * N2 + n2] = cmul(tile[c * FS + sidx(k1)], expi_pi(-static_cast<float>(n2 * k1) * inv_n));
   }
 }
 
@@ -243,6 +249,7 @@ void cols_fwd_t(ColSrc src, const StepArgs& a, const float2* ir, long taps, cons
   if (src == ColSrc::Signal) {
     cols_fwd<LN1, ColSrc::Signal><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out);
   } else {
+    note_prologue_kernel(reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::Kernel>));
     cols_fwd<LN1, ColSrc::Kernel><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out);
   }
 }
@@ -264,6 +271,7 @@ void cols_inv_t(const StepArgs& a, const ConvGeom& g, const float2* X, cudaStrea
 template <int LN2>
 void rows_spec_t(const ConvGeom& g, int slots, float2* P, const float2* tw, cudaStream_t s) {
   const dim3 grid(static_cast<unsigned>(1L << g.log_n1), static_cast<unsigned>(slots));
+  note_prologue_kernel(reinterpret_cast<const void*>(rows_spec<LN2>));
   rows_spec<LN2><<<grid, row_threads<LN2>(), padded(1 << LN2) * 8, s>>>(g.log_n, P, tw);
 }
 
@@ -311,23 +319,13 @@ __global__ void __launch_bounds__(kRevThreads) reverb_ir(const double* params, R
   __shared__ float2 fr[(kRevFpc + 1) * 384];
   __shared__ float gain[2][kRevFpc + 1][kRevBins];
   __shared__ float2 tw384[384];
-  __shared__ float inv_cover[2][192];  // [first hop | later hops]: 1 / (384 * sum of Hann windows)
+  __shared__ float2 inv_cover[192];  // .x first hop, .y later hops
   const int slot = blockIdx.y;
   const double* row = params + static_cast<long>(slot) * 4 * kRevParamBins;
   const int m_first = blockIdx.x * kRevFpc - 1;
   for (int k = threadIdx.x; k < 384; k += kRevThreads) {
-    double sn, cs;
-    sincospi(-2.0 * k / 384.0, &sn, &cs);
-    tw384[k] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
-    if (k < 192) {
-      // dsp.cpp:165-190: periodic Hann cover, out = cover > 1e-8 ? sum / cover : 0.
-      double s0, c0, s1, c1;
-      sincospi(2.0 * k / 384.0, &s0, &c0);
-      sincospi(2.0 * (k + 192) / 384.0, &s1, &c1);
-      const double w0 = 0.5 - 0.5 * c0, w1 = 0.5 - 0.5 * c1;
-      inv_cover[0][k] = w0 > 1e-8 ? static_cast<float>(1.0 / (384.0 * w0)) : 0.f;
-      inv_cover[1][k] = (w0 + w1) > 1e-8 ? static_cast<float>(1.0 / (384.0 * (w0 + w1))) : 0.f;
-    }
+    tw384[k] = __ldg(tw384_table(rc.consts) + k);
+    if (k < 192) inv_cover[k] = __ldg(cover_table(rc.consts) + k);
   }
   for (int idx = threadIdx.x; idx < 2 * (kRevFpc + 1) * kRevBins; idx += kRevThreads) {
     const int which = idx / ((kRevFpc + 1) * kRevBins);
@@ -366,10 +364,10 @@ __global__ void __launch_bounds__(kRevThreads) reverb_ir(const double* params, R
     const int o = t % 192;
     const int f1 = t / 192 + 1;  // local frame starting in this hop
     float2 v = fr[f1 * 384 + o];
-    float sc = inv_cover[0][o];
+    float sc = inv_cover[o].x;
     if (i >= 192) {
       v = cadd(v, fr[(f1 - 1) * 384 + o + 192]);
-      sc = inv_cover[1][o];
+      sc = inv_cover[o].y;
     }
     const float mid = v.x * sc, side = v.y * sc;
     ir[static_cast<long>(slot) * ir_stride + i] = make_float2(0.5f * (mid + side), 0.5f * (mid - side));
@@ -381,33 +379,34 @@ constexpr int kTaps = 40;       // 2 channels x 20
 constexpr int kTapStride = 22;  // [re, im, 20 log-mags]
 constexpr int kFir = 39;
 constexpr int kFirHalf = 19;
+constexpr int kTapRec = 40;     // per tap: [position as float bits, 39 coefficients]
 
-// grid (slots); ir[slot] must be zero on [0, span).
-__global__ void __launch_bounds__(1024) delay_ir(const double* params, DelayConst dc, float2* ir, long ir_stride) {
-  __shared__ long long pos[kTaps];
+// Per slot: fp64 tap positions (processors.cpp:189-208: disabled taps, angle -> grid delay,
+// window clamp) and the 39-tap zero-phase FIRs (dsp.cpp:106-136 as the exact cosine sum).
+// Output taps[slot][tap][kTapRec]. grid (slots) x 1024.
+__global__ void __launch_bounds__(1024) delay_taps(const double* params, DelayConst dc, float* taps) {
   __shared__ double mag[kTaps][20];
   __shared__ double cos39[kFir];
-  __shared__ float coef[kTaps][kFir];
   const int slot = blockIdx.x;
   const double* row = params + static_cast<long>(slot) * kTaps * kTapStride;
+  float* out = taps + static_cast<long>(slot) * kTaps * kTapRec;
   const int t = threadIdx.x;
   if (t < kTaps) {
-    // processors.cpp:189-208 in fp64: disabled taps, angle -> grid delay, window clamp.
     const double* tap = row + t * kTapStride;
     double mx = tap[2];
     for (int k = 1; k < 20; ++k) mx = fmax(mx, tap[2 + k]);
-    long long d = -1;
+    int d = -1;
     if (!(mx <= -60.0)) {
       const int m = t % 20;
       const double frac = -atan2(tap[1], tap[0]) / (2.0 * 3.14159265358979323846);
-      d = llround(frac * static_cast<double>(dc.span));
-      d %= dc.span;
-      if (d < 0) d += dc.span;
+      long long dd = llround(frac * static_cast<double>(dc.span));
+      dd %= dc.span;
+      if (dd < 0) dd += dc.span;
       const long long lo = static_cast<long long>(m) * dc.window;
       const long long hi = min(static_cast<long long>(m + 1) * dc.window, static_cast<long long>(dc.span)) - 1;
-      d = d < lo ? lo : (d > hi ? hi : d);
+      d = static_cast<int>(dd < lo ? lo : (dd > hi ? hi : dd));
     }
-    pos[t] = d;
+    out[t * kTapRec] = __int_as_float(d);
   }
   if (t < kTaps * 20) mag[t / 20][t % 20] = exp(row[(t / 20) * kTapStride + 2 + t % 20]);
   if (t < kFir) {
@@ -416,7 +415,6 @@ __global__ void __launch_bounds__(1024) delay_ir(const double* params, DelayCons
     cos39[t] = c;
   }
   __syncthreads();
-  // 39-tap zero-phase FIR per tap (dsp.cpp:106-136 as the exact cosine sum).
   for (int q = t; q < kTaps * kFir; q += blockDim.x) {
     const int tap = q / kFir, n = q % kFir;
     const int j = n >= kFirHalf ? n - kFirHalf : kFirHalf - n;
@@ -429,26 +427,35 @@ __global__ void __launch_bounds__(1024) delay_ir(const double* params, DelayCons
     }
     double s, c;
     sincospi(2.0 * n / (kFir - 1), &s, &c);
-    coef[tap][n] = static_cast<float>((0.5 - 0.5 * c) * acc / kFir);
+    out[tap * kTapRec + 1 + n] = static_cast<float>((0.5 - 0.5 * c) * acc / kFir);
   }
+}
+
+// Dense multitap kernel (processors.cpp:210-227): every sample i of [0, span) sums, in tap
+// order, the FIR taps of the (at most a few) windows whose clamped position lies within
+// +-19 of i. Writes every sample (no memset, no scatter, deterministic).
+// grid (ceil(span / 256), 2 channels, slots) x 256.
+__global__ void __launch_bounds__(256) delay_dense(const float* taps, DelayConst dc, float2* ir, long ir_stride) {
+  __shared__ float rec[20][kTapRec];
+  const int c = blockIdx.y, slot = blockIdx.z;
+  const float* in = taps + (static_cast<long>(slot) * kTaps + c * 20) * kTapRec;
+  for (int q = threadIdx.x; q < 20 * kTapRec; q += blockDim.x) rec[q / kTapRec][q % kTapRec] = __ldg(in + q);
   __syncthreads();
-  // Scatter in tap order so overlapping FIRs accumulate deterministically.
-  float2* h = ir + static_cast<long>(slot) * ir_stride;
-  for (int m = 0; m < 20; ++m) {
-    if (t < 2 * kFir) {
-      const int c = t / kFir, n = t % kFir;
-      const int tap = c * 20 + m;
-      const long long d = pos[tap];
-      if (d >= 0) {
-        const long long i = d + n - kFirHalf;
-        if (i >= 0 && i < dc.span) {
-          float* dstp = reinterpret_cast<float*>(h + i) + c;
-          *dstp += coef[tap][n];
-        }
-      }
-    }
-    __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= dc.span) return;
+  // Windows that can reach this CTA's samples (same range for every thread of the CTA).
+  const int w = dc.window;
+  const int first = blockIdx.x * blockDim.x;
+  int m0 = (first - kFirHalf) / w - 1, m1 = (first + static_cast<int>(blockDim.x) + kFirHalf) / w;
+  m0 = m0 < 0 ? 0 : m0;
+  m1 = m1 > 19 ? 19 : m1;
+  float acc = 0.f;
+  for (int m = m0; m <= m1; ++m) {
+    const int d = __float_as_int(rec[m][0]);
+    const int j = i - d + kFirHalf;
+    if (d >= 0 && j >= 0 && j < kFir) acc += rec[m][1 + j];
   }
+  reinterpret_cast<float*>(ir + static_cast<long>(slot) * ir_stride + i)[c] = acc;
 }
 
 // ---- noise STFT (ProcessorSet construction) ---------------------------------------------------
@@ -514,8 +521,7 @@ ConvGeom conv_geom(long length, long taps) {
 }
 
 std::size_t conv_prologue_bytes(const ConvGeom& g, int slots, long taps) {
-  return align256(sizeof(float2) * static_cast<std::size_t>(slots) * taps) +
-         align256(sizeof(float2) * static_cast<std::size_t>(slots) * g.n);
+  return ir_bytes(slots, taps) + align256(sizeof(float2) * static_cast<std::size_t>(slots) * g.n);
 }
 
 std::size_t conv_main_bytes(const ConvGeom& g, int slots, int batch) {
@@ -526,20 +532,20 @@ void launch_reverb_ir(const double* params, int slots, const ReverbConst& rc, fl
                       cudaStream_t s) {
   if (slots == 0) return;
   const dim3 grid(static_cast<unsigned>((rc.frames + kRevFpc - 1) / kRevFpc), static_cast<unsigned>(slots));
+  note_prologue_kernel(reinterpret_cast<const void*>(reverb_ir));
   reverb_ir<<<grid, kRevThreads, 0, s>>>(params, rc, ir, ir_stride);
 }
 
 void launch_delay_ir(const double* params, int slots, const DelayConst& dc, float2* ir, long ir_stride,
                      cudaStream_t s) {
   if (slots == 0) return;
-  if (ir_stride == dc.span) {
-    cudaMemsetAsync(ir, 0, sizeof(float2) * static_cast<std::size_t>(slots) * dc.span, s);
-  } else {
-    for (int i = 0; i < slots; ++i) {
-      cudaMemsetAsync(ir + static_cast<long>(i) * ir_stride, 0, sizeof(float2) * static_cast<std::size_t>(dc.span), s);
-    }
-  }
-  delay_ir<<<slots, 1024, 0, s>>>(params, dc, ir, ir_stride);
+  // Tap records live right after the kernels' IR rows ([slots][ir_stride] float2).
+  auto* taps = reinterpret_cast<float*>(ir + static_cast<long>(slots) * ir_stride);
+  note_prologue_kernel(reinterpret_cast<const void*>(delay_taps));
+  note_prologue_kernel(reinterpret_cast<const void*>(delay_dense));
+  delay_taps<<<slots, 1024, 0, s>>>(params, dc, taps);
+  const dim3 grid(static_cast<unsigned>((dc.span + 255) / 256), 2, static_cast<unsigned>(slots));
+  delay_dense<<<grid, 256, 0, s>>>(taps, dc, ir, ir_stride);
 }
 
 void launch_conv_prologue(bool reverb, const StepArgs& a, const ReverbConst& rc, const DelayConst& dc, void* ws,
@@ -548,7 +554,7 @@ void launch_conv_prologue(bool reverb, const StepArgs& a, const ReverbConst& rc,
   const long taps = reverb ? rc.length : dc.span;
   const ConvGeom g = conv_geom(a.length, taps);
   auto* ir = static_cast<float2*>(ws);
-  auto* P = reinterpret_cast<float2*>(static_cast<char*>(ws) + align256(sizeof(float2) * static_cast<std::size_t>(a.slots) * taps));
+  auto* P = reinterpret_cast<float2*>(static_cast<char*>(ws) + ir_bytes(a.slots, taps));
   if (reverb) launch_reverb_ir(a.params, a.slots, rc, ir, taps, s);
   else launch_delay_ir(a.params, a.slots, dc, ir, taps, s);
   kernel_spectrum(a, g, ir, taps, P, s);
@@ -557,8 +563,7 @@ void launch_conv_prologue(bool reverb, const StepArgs& a, const ReverbConst& rc,
 void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, void* ws, cudaStream_t s) {
   if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
   const ConvGeom g = conv_geom(a.length, taps);
-  const auto* P = reinterpret_cast<const float2*>(static_cast<const char*>(prologue_ws) +
-                                                  align256(sizeof(float2) * static_cast<std::size_t>(a.slots) * taps));
+  const auto* P = reinterpret_cast<const float2*>(static_cast<const char*>(prologue_ws) + ir_bytes(a.slots, taps));
   auto* X = static_cast<float2*>(ws);
   MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, a, nullptr, 0, g, a.slots * a.batch, X, s);
   MGB_DISPATCH_LN(g.log_n2, rows_conv_t, g, a.slots * a.batch, a.batch, X, P, a.tw, s);

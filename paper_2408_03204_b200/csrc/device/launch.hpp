@@ -21,9 +21,15 @@ constexpr int kEqHalf = 1023;
 constexpr int kEqValid = kEqFft - 2 * kEqHalf;
 void launch_eq_prologue(const StepArgs& a, float* taps_ws /*slots*2048*/, float* resp_ws /*slots*8192*/, cudaStream_t s);
 void launch_eq_main(const StepArgs& a, const float* resp_ws, cudaStream_t s);
+// Split form of launch_eq_main for a step whose prologue is still running: the forward
+// window FFTs (no response needed) go first into `spectrum` (eq_spectrum_bytes), then the
+// response product + inverse once the prologue is done.
+std::size_t eq_spectrum_bytes(int slots, int batch, long length);
+void launch_eq_forward(const StepArgs& a, float2* spectrum, cudaStream_t s);
+void launch_eq_inverse(const StepArgs& a, const float* resp_ws, const float2* spectrum, cudaStream_t s);
 
 // Compressor / noisegate: chained (decoupled look-back) scan of the energy envelope.
-constexpr int kDynThreads = 256;
+constexpr int kDynThreads = 512;
 constexpr int kDynPerThread = 8;
 constexpr int kDynTile = kDynThreads * kDynPerThread;
 std::size_t dyn_workspace_bytes(int slots, int batch, long length);
@@ -42,6 +48,7 @@ struct ReverbConst {
   const float2* stft_side;
   int frames;
   long length;  // reverb_length
+  const float2* consts;  // twiddle_table(): 384-point twiddles and OLA covers
 };
 struct DelayConst {
   long span;
@@ -70,8 +77,18 @@ void launch_noise_stft(const double* noise, long length, int frames, float2* out
 // any stream capture; ProcessorSet does): kTwN forward twiddles (float2), followed by
 // kCosN doubles cos(2 pi m / 2047) for the EQ FIR design (cos_table()).
 constexpr int kCosN = 2047;
+constexpr int kTw384Off = 8192 + kCosN;      // float2 offset of the 384-point twiddles
+constexpr int kCoverOff = kTw384Off + 384;   // float2 offset of the reverb inverse covers
+constexpr int kConstFloat2s = kCoverOff + 192;
 const float2* twiddle_table(int device);
-inline const double* cos_table(const float2* tw) { return reinterpret_cast<const double*>(tw + 8192); }
+__host__ __device__ inline const double* cos_table(const float2* tw) { return reinterpret_cast<const double*>(tw + 8192); }
+__host__ __device__ inline const float2* tw384_table(const float2* tw) { return tw + kTw384Off; }
+// .x = 1/(384 w(o)) for the first hop, .y = 1/(384 (w(o) + w(o+192))) afterwards
+__host__ __device__ inline const float2* cover_table(const float2* tw) { return tw + kCoverOff; }
+
+// Kernels that only run in parameter-only prologues (RenderGraph gives them low priority).
+void note_prologue_kernel(const void* fn);
+bool is_prologue_kernel(const void* fn);
 
 // Arena conversion helpers for the host-buffer API.
 void launch_f64_to_f32(const double* in, float* out, long n, cudaStream_t s);

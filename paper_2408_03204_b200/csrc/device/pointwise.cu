@@ -11,6 +11,8 @@ namespace mgb {
 
 namespace {
 
+constexpr int kPwThreads = 128;
+
 template <PointOp OP>
 __device__ __forceinline__ void apply(float& l, float& r, float g0, float g1) {
   if constexpr (OP == PointOp::Gain) {
@@ -35,47 +37,50 @@ __device__ __forceinline__ void coeffs(const StepArgs& a, int slot, float& g0, f
   }
 }
 
-// grid.y = slot*B + b; grid.x strides over float4 groups of the row.
+// grid.y = slot*B + b; one float4 group of both channels per thread (grid sized so every
+// thread has exactly one). A step only reads rows stored by earlier steps (or zeroed rows),
+// never its own output rows, so src and dst never alias (restrict is valid). Edges are
+// consumed 8 at a time (16 independent 16-byte loads in flight), summed in edge order.
 template <PointOp OP>
-__global__ void __launch_bounds__(256) pointwise_vec4(StepArgs a) {
+__global__ void __launch_bounds__(kPwThreads) pointwise_vec4(StepArgs a) {
   const int sb = blockIdx.y;
   const int slot = sb / a.batch, b = sb - slot * a.batch;
+  const long n4 = a.length >> 2;
+  const long i = blockIdx.x * static_cast<long>(kPwThreads) + threadIdx.x;
+  if (i >= n4) return;
   const int e0 = __ldg(a.row_ptr + slot), e1 = __ldg(a.row_ptr + slot + 1);
+  const long boff = static_cast<long>(b) * 2 * a.length;
+  const float* __restrict__ src = a.src;
+  float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
+  int e = e0;
+  for (; e + 7 < e1; e += 8) {
+    float4 lv[8], rv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const float4* p = reinterpret_cast<const float4*>(src + static_cast<long>(__ldg(a.col + e + u)) * a.rowstride + boff);
+      lv[u] = __ldg(p + i);
+      rv[u] = __ldg(p + n4 + i);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      l = f4add(l, lv[u]);
+      r = f4add(r, rv[u]);
+    }
+  }
+  for (; e < e1; ++e) {
+    const float4* p = reinterpret_cast<const float4*>(src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff);
+    l = f4add(l, __ldg(p + i));
+    r = f4add(r, __ldg(p + n4 + i));
+  }
   float g0, g1;
   coeffs<OP>(a, slot, g0, g1);
-  const long n4 = a.length >> 2;
-  const long boff = static_cast<long>(b) * 2 * a.length;
-  float4* outl = reinterpret_cast<float4*>(a.dst + static_cast<long>(slot) * a.rowstride + boff);
-  float4* outr = reinterpret_cast<float4*>(a.dst + static_cast<long>(slot) * a.rowstride + boff + a.length);
-  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n4; i += static_cast<long>(gridDim.x) * blockDim.x) {
-    float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
-    int e = e0;
-    for (; e + 3 < e1; e += 4) {  // four edges (8 loads) in flight; sums stay in edge order
-      float4 lv[4], rv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float4* p = reinterpret_cast<const float4*>(a.src + static_cast<long>(__ldg(a.col + e + u)) * a.rowstride + boff);
-        lv[u] = __ldg(p + i);
-        rv[u] = __ldg(p + n4 + i);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        l = f4add(l, lv[u]);
-        r = f4add(r, rv[u]);
-      }
-    }
-    for (; e < e1; ++e) {
-      const float4* p0 = reinterpret_cast<const float4*>(a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff);
-      l = f4add(l, __ldg(p0 + i));
-      r = f4add(r, __ldg(p0 + n4 + i));
-    }
-    apply<OP>(l.x, r.x, g0, g1);
-    apply<OP>(l.y, r.y, g0, g1);
-    apply<OP>(l.z, r.z, g0, g1);
-    apply<OP>(l.w, r.w, g0, g1);
-    outl[i] = l;  // default policy: the next step reads these rows back from L2
-    outr[i] = r;
-  }
+  apply<OP>(l.x, r.x, g0, g1);
+  apply<OP>(l.y, r.y, g0, g1);
+  apply<OP>(l.z, r.z, g0, g1);
+  apply<OP>(l.w, r.w, g0, g1);
+  float* __restrict__ out = a.dst + static_cast<long>(slot) * a.rowstride + boff;
+  reinterpret_cast<float4*>(out)[i] = l;
+  reinterpret_cast<float4*>(out + a.length)[i] = r;
 }
 
 template <PointOp OP>
@@ -99,18 +104,15 @@ void launch_op(const StepArgs& a, cudaStream_t s) {
   const int rows = a.slots * a.batch;
   if (rows == 0 || a.length == 0) return;
   const bool vec = (a.length % 4) == 0;
-  const long items = vec ? a.length / 4 : a.length;
-  // One float4 group per thread when that is needed to fill ~4 CTAs per SM, else two.
-  const long per = static_cast<long>(rows) * ((items + 255) / 256) < 4 * 148 ? 1 : 2;
-  long blocks = (items + 256 * per - 1) / (256 * per);
-  if (blocks < 1) blocks = 1;
+  if (vec) {
+    const dim3 grid(static_cast<unsigned>((a.length / 4 + kPwThreads - 1) / kPwThreads), static_cast<unsigned>(rows));
+    pointwise_vec4<OP><<<grid, kPwThreads, 0, s>>>(a);
+    return;
+  }
+  long blocks = (a.length + 255) / 256;
   if (blocks > 4096) blocks = 4096;
   dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(rows));
-  if (vec) {
-    pointwise_vec4<OP><<<grid, 256, 0, s>>>(a);
-  } else {
-    pointwise_scalar<OP><<<grid, 256, 0, s>>>(a);
-  }
+  pointwise_scalar<OP><<<grid, 256, 0, s>>>(a);
 }
 
 }  // namespace

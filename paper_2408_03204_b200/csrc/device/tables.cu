@@ -2,6 +2,7 @@
 #include <cmath>
 #include <map>
 #include <mutex>
+#include <set>
 #include <stdexcept>
 #include <vector>
 
@@ -16,14 +17,27 @@ const float2* twiddle_table(int device) {
   std::scoped_lock lock(mu);
   auto it = tables.find(device);
   if (it != tables.end()) return it->second;
-  // [kTwN float2 twiddles][kCosN doubles: cos(2 pi m / 2047)] in one allocation.
-  std::vector<float2> host(kTwN + kCosN);
+  // One allocation (float2 units): [kTwN twiddles][kCosN doubles cos(2 pi m / 2047)]
+  // [384 twiddles exp(-2 pi i k / 384)][192 float2: inverse Hann covers for the reverb OLA].
+  std::vector<float2> host(kConstFloat2s);
   for (int k = 0; k < kTwN; ++k) {
     const double a = -2.0 * 3.14159265358979323846 * static_cast<double>(k) / kTwN;
     host[static_cast<std::size_t>(k)] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
   }
   auto* cosd = reinterpret_cast<double*>(host.data() + kTwN);
   for (int m = 0; m < kCosN; ++m) cosd[m] = std::cos(2.0 * 3.14159265358979323846 * m / kCosN);
+  for (int k = 0; k < 384; ++k) {
+    const double a = -2.0 * 3.14159265358979323846 * k / 384.0;
+    host[static_cast<std::size_t>(kTw384Off + k)] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+  }
+  for (int o = 0; o < 192; ++o) {
+    // dsp.cpp:165-190: periodic Hann cover; out = cover > 1e-8 ? sum / cover : 0 (IFFT 1/384 folded in)
+    const double w0 = 0.5 - 0.5 * std::cos(2.0 * 3.14159265358979323846 * o / 384.0);
+    const double w1 = 0.5 - 0.5 * std::cos(2.0 * 3.14159265358979323846 * (o + 192) / 384.0);
+    host[static_cast<std::size_t>(kCoverOff + o)] =
+        make_float2(w0 > 1e-8 ? static_cast<float>(1.0 / (384.0 * w0)) : 0.f,
+                    (w0 + w1) > 1e-8 ? static_cast<float>(1.0 / (384.0 * (w0 + w1))) : 0.f);
+  }
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
@@ -36,6 +50,24 @@ const float2* twiddle_table(int device) {
   cudaSetDevice(prev);
   tables.emplace(device, d);
   return d;
+}
+
+namespace {
+std::mutex g_prologue_mu;
+std::set<const void*>& prologue_set() {
+  static std::set<const void*> s;
+  return s;
+}
+}  // namespace
+
+void note_prologue_kernel(const void* fn) {
+  std::scoped_lock lock(g_prologue_mu);
+  prologue_set().insert(fn);
+}
+
+bool is_prologue_kernel(const void* fn) {
+  std::scoped_lock lock(g_prologue_mu);
+  return prologue_set().count(fn) != 0;
 }
 
 }  // namespace mgb

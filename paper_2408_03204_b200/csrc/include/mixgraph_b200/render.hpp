@@ -153,6 +153,25 @@ class DevicePlan {
   std::vector<int> zero_rows_;
 };
 
+// A whole render (main stream + side-stream prologues) captured once and instantiated as
+// a CUDA graph with node priorities: launch() replays it on any stream. Pointers, shapes and
+// parameter tables are baked in (update the tables' contents in place between launches).
+typedef struct CUgraph_st* cudaGraph_t;
+typedef struct CUgraphExec_st* cudaGraphExec_t;
+class RenderGraph {
+ public:
+  RenderGraph(const DevicePlan& plan, const ProcessorSet& processors, const double* const* param_tables, float* arena,
+              int batch, long length, void* workspace, std::size_t workspace_bytes);
+  ~RenderGraph();
+  RenderGraph(const RenderGraph&) = delete;
+  RenderGraph& operator=(const RenderGraph&) = delete;
+  void launch(cudaStream_t stream) const;
+
+ private:
+  cudaGraph_t graph_ = nullptr;
+  cudaGraphExec_t exec_ = nullptr;
+};
+
 // Host-buffer render over caller pointers (no intermediate host copies): sources[k] and
 // outputs[o] each point at [batch][2][length] doubles (pinned memory makes the copies
 // asynchronous DMA); intermediates (original row order) may be null. `plan` may be null.

@@ -66,15 +66,11 @@ class DeviceRenderer:
                                     ctypes.c_void_p(s.cuda_stream)))
         return self.outputs
 
-    def capture(self) -> "torch.cuda.CUDAGraph":
-        """Capture one full render (main stream + the side-stream prologues) as a CUDA graph;
-        replay() re-runs it on the current arena, parameters and workspace pointers."""
-        self.render()  # one-time kernel attribute setup happens outside the capture
-        torch.cuda.synchronize(self.device)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self.render()
-        return g
+    def capture(self) -> "RenderGraph":
+        """Capture one full render (main stream + side-stream prologues) as a CUDA graph
+        instantiated with node priorities (mg_render_graph_create); replay() re-runs it on
+        the current arena, parameter tables and workspace (contents may change in place)."""
+        return RenderGraph(self)
 
     def render_profiled(self, stream: Optional[torch.cuda.Stream] = None, sync: bool = False) -> Optional[np.ndarray]:
         """Same as render() with CUDA events around every step on the launching stream. With
@@ -87,3 +83,22 @@ class DeviceRenderer:
                                              ctypes.c_void_p(s.cuda_stream),
                                              None if out is None else out.ctypes.data_as(ctypes.c_void_p)))
         return out
+
+
+class RenderGraph:
+    def __init__(self, dr: DeviceRenderer):
+        self._dr = dr  # keeps the arena / workspace / tables alive
+        self._h = ctypes.c_void_p()
+        _check(_lib.mg_render_graph_create(dr.rd.handle, dr.procs.handle, dr._ptrs,
+                                           ctypes.c_void_p(dr.arena.data_ptr()), dr.batch, dr.length,
+                                           ctypes.c_void_p(dr.workspace.data_ptr()), dr.workspace_bytes,
+                                           ctypes.byref(self._h)))
+
+    def replay(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        s = stream or torch.cuda.current_stream(self._dr.device)
+        _check(_lib.mg_render_graph_launch(self._h, ctypes.c_void_p(s.cuda_stream)))
+
+    def __del__(self, _destroy=_lib.mg_render_graph_destroy):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            _destroy(h)

@@ -7,7 +7,7 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-n
 rows = list(csv.reader(out.splitlines()))
 h = rows[1]
 si, ss = h.index("Source"), h.index("Warp Stall Sampling (All Samples)")
-body = [r for r in rows[2:] if len(r) == len(h)]
+body = [r for r in rows[2:] if len(r) == len(h) and r[ss].isdigit()]
 tot = sum(int(r[ss]) for r in body) or 1
 print(f"total samples {tot}, instructions {len(body)}")
 for r in sorted(body, key=lambda r: -int(r[ss]))[:n]:
