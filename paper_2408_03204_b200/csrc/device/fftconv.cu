@@ -93,12 +93,19 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_fwd(StepArgs a, const flo
   fft_pow2<LN1, C, kColThreads, -1>(tile, FS, a.tw);
   float2* o = out + static_cast<long>(item) * N;
   const float inv_n = 2.f / static_cast<float>(N);
-#pragma unroll 4
-  for (int idx = threadIdx.x; idx < kColElems; idx += kColThreads) {
-    const int c = idx % C, k1 = idx / C;
-    const long n2 = col0 + c;
-    // four-step twiddle exp(-2 pi i n2 k1 / N); n2 k1 < N <= 2^24 is exact in fp32
-    o[static_cast<long>(k1) * N2 + n2] = cmul(tile[c * FS + sidx(k1)], expi_pi(-static_cast<float>(n2 * k1) * inv_n));
+  // Four-step twiddle exp(-2 pi i n2 k1 / N). This thread's elements share n2 and step k1 by
+  // kColThreads / C, so the twiddles are geometric: exact anchors (sincospif; n2 k1 < N <=
+  // 2^24 is exact in fp32) every 4 elements, <= 3 chained products in between.
+  constexpr int KSTEP = kColThreads / C;
+  const int c = threadIdx.x % C, k1_0 = threadIdx.x / C;
+  const long n2 = col0 + c;
+  const float2 step = expi_pi(-static_cast<float>(n2 * KSTEP) * inv_n);
+  float2 w = make_float2(1.f, 0.f);
+#pragma unroll
+  for (int q = 0; q < kColElems / kColThreads; ++q) {
+    const int k1 = k1_0 + q * KSTEP;
+    w = (q % 4 == 0) ? expi_pi(-static_cast<float>(n2 * k1) * inv_n) : cmul(w, step);
+    o[static_cast<long>(k1) * N2 + n2] = cmul(tile[c * FS + sidx(k1)], w);
   }
 }
 
@@ -150,32 +157,37 @@ __device__ __forceinline__ float2 zmix(float2 xk, float2 xm, float2 pk, float2 p
   return make_float2((s1.x + s2.y) * s, (s1.y - s2.x) * s);
 }
 
-template <int LN2>
+// Threads = radix-16 butterflies of the first pass (COUNT rows of 2^LN2 points), so no
+// thread idles in it; later radix-8/4 passes give each thread 2 or 4 butterflies.
+template <int LN2, int COUNT>
 constexpr int row_threads() {
-  constexpr int t = (2 << LN2) / 8;
-  return t < 64 ? 64 : (t > 512 ? 512 : t);
+  constexpr int t = COUNT * (1 << LN2) / 16;
+  return t < 32 ? 32 : (t > 512 ? 512 : t);
 }
+constexpr int kSpecRows = 4;  // kernel-spectrum rows per CTA
 
-// Forward row FFTs of the packed kernel; one row per CTA. grid (N1, slots)
+// Forward row FFTs of the packed kernel, kSpecRows consecutive rows per CTA.
+// grid (N1 / kSpecRows, slots)
 template <int LN2>
-__global__ void __launch_bounds__(row_threads<LN2>()) rows_spec(int log_n, float2* P, const float2* tw) {
+__global__ void __launch_bounds__(row_threads<LN2, kSpecRows>()) rows_spec(int log_n, float2* P, const float2* tw) {
   constexpr int N2 = 1 << LN2;
-  constexpr int NT = row_threads<LN2>();
+  constexpr int NT = row_threads<LN2, kSpecRows>();
+  constexpr int RS = padded(N2);
   extern __shared__ float2 row[];
   const long N = 1L << log_n;
-  float2* p = P + static_cast<long>(blockIdx.y) * N + static_cast<long>(blockIdx.x) * N2;
-  for (int i = threadIdx.x; i < N2; i += NT) row[sidx(i)] = p[i];
+  float2* p = P + static_cast<long>(blockIdx.y) * N + static_cast<long>(blockIdx.x) * kSpecRows * N2;
+  for (int i = threadIdx.x; i < kSpecRows * N2; i += NT) row[(i / N2) * RS + sidx(i % N2)] = p[i];
   __syncthreads();
-  fft_pow2<LN2, 1, NT, -1>(row, padded(N2), tw);
-  for (int i = threadIdx.x; i < N2; i += NT) p[i] = row[sidx(i)];
+  fft_pow2<LN2, kSpecRows, NT, -1>(row, RS, tw);
+  for (int i = threadIdx.x; i < kSpecRows * N2; i += NT) p[i] = row[(i / N2) * RS + sidx(i % N2)];
 }
 
 // Signal rows k1 = r and N1 - r together: forward FFTs, channel-split product with the
 // kernel spectrum, inverse FFTs, inverse four-step twiddle. grid (N1/2 + 1, slots*B)
 template <int LN2>
-__global__ void __launch_bounds__(row_threads<LN2>()) rows_conv(int log_n, int batch, float2* X, const float2* P, const float2* tw) {
+__global__ void __launch_bounds__(row_threads<LN2, 2>()) rows_conv(int log_n, int batch, float2* X, const float2* P, const float2* tw) {
   constexpr int N2 = 1 << LN2;
-  constexpr int NT = row_threads<LN2>();
+  constexpr int NT = row_threads<LN2, 2>();
   extern __shared__ float2 rows[];  // [2][N2]
   const long N = 1L << log_n;
   const int N1 = static_cast<int>(N >> LN2);
@@ -225,9 +237,23 @@ __global__ void __launch_bounds__(row_threads<LN2>()) rows_conv(int log_n, int b
   __syncthreads();
   fft_pow2<LN2, 2, NT, +1>(rows, RS, tw);
   const float inv_n = 2.f / static_cast<float>(N);
-  for (int i = threadIdx.x; i < N2; i += NT) {
-    xa[i] = cmul(rows[sidx(i)], expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n));
-    if (!self) xb[i] = cmul(rows[RS + sidx(i)], expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n));
+  // Inverse four-step twiddle exp(+2 pi i k1 i / N): geometric in this thread's i (step NT),
+  // exact anchors every 4 elements as in cols_fwd.
+  const float2 step_a = expi_pi(static_cast<float>(static_cast<long>(ra) * NT) * inv_n);
+  const float2 step_b = expi_pi(static_cast<float>(static_cast<long>(rb) * NT) * inv_n);
+  float2 wa = make_float2(1.f, 0.f), wb = wa;
+#pragma unroll
+  for (int q = 0; q < N2 / NT; ++q) {
+    const int i = threadIdx.x + q * NT;
+    if (q % 4 == 0) {
+      wa = expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n);
+      wb = expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n);
+    } else {
+      wa = cmul(wa, step_a);
+      wb = cmul(wb, step_b);
+    }
+    xa[i] = cmul(rows[sidx(i)], wa);
+    if (!self) xb[i] = cmul(rows[RS + sidx(i)], wb);
   }
 }
 
@@ -270,9 +296,9 @@ void cols_inv_t(const StepArgs& a, const ConvGeom& g, const float2* X, cudaStrea
 
 template <int LN2>
 void rows_spec_t(const ConvGeom& g, int slots, float2* P, const float2* tw, cudaStream_t s) {
-  const dim3 grid(static_cast<unsigned>(1L << g.log_n1), static_cast<unsigned>(slots));
+  const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / kSpecRows), static_cast<unsigned>(slots));
   note_prologue_kernel(reinterpret_cast<const void*>(rows_spec<LN2>));
-  rows_spec<LN2><<<grid, row_threads<LN2>(), padded(1 << LN2) * 8, s>>>(g.log_n, P, tw);
+  rows_spec<LN2><<<grid, row_threads<LN2, kSpecRows>(), kSpecRows * padded(1 << LN2) * 8, s>>>(g.log_n, P, tw);
 }
 
 template <int LN2>
@@ -285,7 +311,7 @@ void rows_conv_t(const ConvGeom& g, int items, int batch, float2* X, const float
   }();
   (void)done;
   const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(items));
-  rows_conv<LN2><<<grid, row_threads<LN2>(), smem, s>>>(g.log_n, batch, X, P, tw);
+  rows_conv<LN2><<<grid, row_threads<LN2, 2>(), smem, s>>>(g.log_n, batch, X, P, tw);
 }
 
 #define MGB_DISPATCH_LN(var, FN, ...)                  \
