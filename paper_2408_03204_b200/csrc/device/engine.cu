@@ -293,14 +293,14 @@ DevicePlan::DevicePlan(const RenderData& rd) : rd_(rd) {
   // main stream's kernels whenever both have work (honoured inside RenderGraph too).
   int least = 0, greatest = 0;
   cuda_check(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
-  cuda_check(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, least), "cudaStreamCreate");
+  for (auto& a : aux_) cuda_check(cudaStreamCreateWithPriority(&a, cudaStreamNonBlocking, least), "cudaStreamCreate");
   events_.resize(rd.steps.size() + 1);
   for (auto& ev : events_) cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
 }
 
 DevicePlan::~DevicePlan() {
   for (cudaEvent_t ev : events_) cudaEventDestroy(ev);
-  if (aux_) cudaStreamDestroy(aux_);
+  for (cudaStream_t a : aux_) if (a) cudaStreamDestroy(a);
   if (d_index_) cudaFree(d_index_);
 }
 
@@ -377,11 +377,16 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
   if (hoist) {
     cuda_check(cudaEventRecord(ev[0], stream), "event");  // fork point: before any render work
     if (split_first) mgb::launch_eq_forward(args[0], reinterpret_cast<float2*>(ws + lay.main_off), stream);
-    cuda_check(cudaStreamWaitEvent(plan.aux_stream(), ev[0], 0), "wait");
+    for (cudaStream_t a : plan.aux_streams()) cuda_check(cudaStreamWaitEvent(a, ev[0], 0), "wait");
+    int next = 0;  // independent prologues round-robin over the side streams
     for (std::size_t k = 0; k < rd.steps.size(); ++k) {
       if (!has_prologue(rd.steps[k].type)) continue;
-      run_prologue(rd.steps[k].type, args[k], procs, ws + lay.prologue_off[k], plan.aux_stream());
-      cuda_check(cudaEventRecord(ev[k + 1], plan.aux_stream()), "event");
+      // One side stream: prologues then complete in the order their steps need them (more
+      // side streams let later prologues steal SMs from earlier ones; measured slower).
+      cudaStream_t a = plan.aux_streams()[0];
+      ++next;
+      run_prologue(rd.steps[k].type, args[k], procs, ws + lay.prologue_off[k], a);
+      cuda_check(cudaEventRecord(ev[k + 1], a), "event");
     }
   }
   for (std::size_t k = 0; k < rd.steps.size(); ++k) {

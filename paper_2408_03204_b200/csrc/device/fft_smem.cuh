@@ -273,12 +273,13 @@ __device__ __forceinline__ void fft_pow2(float2* buf, int fstride, const float2*
 }
 
 // 384 = 3 * 8 * 4 * 4 (reverb STFT frames); tw384[k] = exp(-2*pi*i*k/384), usually in smem.
+// Element i of transform f lives at buf[f*fstride + sidx(i)] (padded layout).
 template <int COUNT, int NTHR, int DIR>
 __device__ __forceinline__ void fft_384(float2* buf, int fstride, const float2* tw384) {
-  stockham_pass<384, 3, 1, COUNT, NTHR, DIR, 384, false>(buf, fstride, tw384);
-  stockham_pass<384, 8, 3, COUNT, NTHR, DIR, 384, false>(buf, fstride, tw384);
-  stockham_pass<384, 4, 24, COUNT, NTHR, DIR, 384, false>(buf, fstride, tw384);
-  stockham_pass<384, 4, 96, COUNT, NTHR, DIR, 384, false>(buf, fstride, tw384);
+  stockham_pass<384, 3, 1, COUNT, NTHR, DIR, 384>(buf, fstride, tw384);
+  stockham_pass<384, 8, 3, COUNT, NTHR, DIR, 384>(buf, fstride, tw384);
+  stockham_pass<384, 4, 24, COUNT, NTHR, DIR, 384>(buf, fstride, tw384);
+  stockham_pass<384, 4, 96, COUNT, NTHR, DIR, 384>(buf, fstride, tw384);
 }
 
 }  // namespace mgb

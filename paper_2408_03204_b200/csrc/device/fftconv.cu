@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(row_threads<LN2, kSpecRows>()) rows_spec(int l
 // Signal rows k1 = r and N1 - r together: forward FFTs, channel-split product with the
 // kernel spectrum, inverse FFTs, inverse four-step twiddle. grid (N1/2 + 1, slots*B)
 template <int LN2>
-__global__ void __launch_bounds__(row_threads<LN2, 2>()) rows_conv(int log_n, int batch, float2* X, const float2* P, const float2* tw) {
+__global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2, 2>()) rows_conv(int log_n, int batch, float2* X, const float2* P, const float2* tw) {
   constexpr int N2 = 1 << LN2;
   constexpr int NT = row_threads<LN2, 2>();
   extern __shared__ float2 rows[];  // [2][N2]
@@ -335,15 +335,19 @@ void kernel_spectrum(const StepArgs& a, const ConvGeom& g, const float2* ir, lon
 // ---- reverb impulse response (masked noise STFT -> ISTFT) ----------------------------------
 constexpr int kRevBins = 193;      // kReverbStftLength / 2 + 1
 constexpr int kRevParamBins = 192;
-constexpr int kRevFpc = 8;         // output hops per CTA
-constexpr int kRevThreads = 256;
+constexpr int kRevFpc = 16;        // output hops per CTA (frames computed: kRevFpc + 1)
+constexpr int kRevThreads = 512;
+constexpr int kRevFS = padded(384);  // frame stride in smem (padded layout)
 
-// grid (ceil(frames / kRevFpc), slots). Each CTA inverse-transforms frames m0-1 .. m0+7
-// (mid and side packed as one complex transform each) and overlap-adds hops m0 .. m0+7.
-__global__ void __launch_bounds__(kRevThreads) reverb_ir(const double* params, ReverbConst rc, float2* ir,
+// grid (ceil(frames / kRevFpc), slots). Each CTA inverse-transforms frames m0-1 .. m0+15
+// (mid and side packed as one complex transform each) and overlap-adds hops m0 .. m0+15.
+// The per-bin mask exp(H0 + m Hdecay) is geometric in the frame index m: one exact expf
+// anchor per bin for the CTA's first frame and the ratio exp(Hdecay), both with fp64
+// exponents (processors.cpp:171-175), then <= 16 products.
+__global__ void __launch_bounds__(kRevThreads, 2) reverb_ir(const double* params, ReverbConst rc, float2* ir,
                                                          long ir_stride) {
-  __shared__ float2 fr[(kRevFpc + 1) * 384];
-  __shared__ float gain[2][kRevFpc + 1][kRevBins];
+  extern __shared__ float2 fr[];  // [(kRevFpc + 1)][kRevFS]
+  __shared__ float base[2][kRevBins], ratio[2][kRevBins];
   __shared__ float2 tw384[384];
   __shared__ float2 inv_cover[192];  // .x first hop, .y later hops
   const int slot = blockIdx.y;
@@ -353,46 +357,50 @@ __global__ void __launch_bounds__(kRevThreads) reverb_ir(const double* params, R
     tw384[k] = __ldg(tw384_table(rc.consts) + k);
     if (k < 192) inv_cover[k] = __ldg(cover_table(rc.consts) + k);
   }
-  for (int idx = threadIdx.x; idx < 2 * (kRevFpc + 1) * kRevBins; idx += kRevThreads) {
-    const int which = idx / ((kRevFpc + 1) * kRevBins);
-    const int rem = idx - which * (kRevFpc + 1) * kRevBins;
-    const int f = rem / kRevBins, k = rem - f * kRevBins;
-    const int m = m_first + f;
+  for (int idx = threadIdx.x; idx < 2 * kRevBins; idx += kRevThreads) {
+    const int which = idx / kRevBins, k = idx - which * kRevBins;
     const int bin = k < kRevParamBins ? k : kRevParamBins - 1;
     const double* color = row + which * 2 * kRevParamBins;
-    // exp(H0 + m * Hdecay), exponent formed in fp64 (processors.cpp:171-175)
-    gain[which][f][k] = (m < 0 || m >= rc.frames) ? 0.f : expf(static_cast<float>(color[bin] + m * color[kRevParamBins + bin]));
+    const double decay = color[kRevParamBins + bin];
+    base[which][k] = expf(static_cast<float>(color[bin] + m_first * decay));
+    ratio[which][k] = expf(static_cast<float>(decay));
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < (kRevFpc + 1) * 384; idx += kRevThreads) {
-    const int f = idx / 384, k = idx - f * 384;
-    const int m = m_first + f;
-    float2 z = make_float2(0.f, 0.f);
-    if (m >= 0 && m < rc.frames) {
-      const bool upper = k > 192;
-      const int kk = upper ? 384 - k : k;
-      float2 M = cscale(__ldg(rc.stft_mid + static_cast<long>(m) * kRevBins + kk), gain[0][f][kk]);
-      float2 S = cscale(__ldg(rc.stft_side + static_cast<long>(m) * kRevBins + kk), gain[1][f][kk]);
-      if (upper) {
-        M = cconj(M);
-        S = cconj(S);
+  // Fill: thread owns one (bin-pair k, kk) column across all frames, walking the gains.
+  for (int k = threadIdx.x; k < 384; k += kRevThreads) {
+    const bool upper = k > 192;
+    const int kk = upper ? 384 - k : k;
+    float gm = base[0][kk], gs = base[1][kk];
+    const float rm = ratio[0][kk], rs = ratio[1][kk];
+    for (int f = 0; f <= kRevFpc; ++f) {
+      const int m = m_first + f;
+      float2 z = make_float2(0.f, 0.f);
+      if (m >= 0 && m < rc.frames) {
+        float2 M = cscale(__ldg(rc.stft_mid + static_cast<long>(m) * kRevBins + kk), gm);
+        float2 S = cscale(__ldg(rc.stft_side + static_cast<long>(m) * kRevBins + kk), gs);
+        if (upper) {
+          M = cconj(M);
+          S = cconj(S);
+        }
+        z = make_float2(M.x - S.y, M.y + S.x);  // M + i S: both inverse transforms are real
       }
-      z = make_float2(M.x - S.y, M.y + S.x);  // M + i S: both inverse transforms are real
+      fr[f * kRevFS + sidx(k)] = z;
+      gm *= rm;
+      gs *= rs;
     }
-    fr[idx] = z;
   }
   __syncthreads();
-  fft_384<kRevFpc + 1, kRevThreads, +1>(fr, 384, tw384);
+  fft_384<kRevFpc + 1, kRevThreads, +1>(fr, kRevFS, tw384);
   const long i0 = static_cast<long>(blockIdx.x) * kRevFpc * 192;
   for (int t = threadIdx.x; t < kRevFpc * 192; t += kRevThreads) {
     const long i = i0 + t;
     if (i >= rc.length) break;
     const int o = t % 192;
     const int f1 = t / 192 + 1;  // local frame starting in this hop
-    float2 v = fr[f1 * 384 + o];
+    float2 v = fr[f1 * kRevFS + sidx(o)];
     float sc = inv_cover[o].x;
     if (i >= 192) {
-      v = cadd(v, fr[(f1 - 1) * 384 + o + 192]);
+      v = cadd(v, fr[(f1 - 1) * kRevFS + sidx(o + 192)]);
       sc = inv_cover[o].y;
     }
     const float mid = v.x * sc, side = v.y * sc;
@@ -559,7 +567,12 @@ void launch_reverb_ir(const double* params, int slots, const ReverbConst& rc, fl
   if (slots == 0) return;
   const dim3 grid(static_cast<unsigned>((rc.frames + kRevFpc - 1) / kRevFpc), static_cast<unsigned>(slots));
   note_prologue_kernel(reinterpret_cast<const void*>(reverb_ir));
-  reverb_ir<<<grid, kRevThreads, 0, s>>>(params, rc, ir, ir_stride);
+  static const bool done = [] {
+    cudaFuncSetAttribute(reverb_ir, cudaFuncAttributeMaxDynamicSharedMemorySize, (kRevFpc + 1) * kRevFS * 8);
+    return true;
+  }();
+  (void)done;
+  reverb_ir<<<grid, kRevThreads, (kRevFpc + 1) * kRevFS * 8, s>>>(params, rc, ir, ir_stride);
 }
 
 void launch_delay_ir(const double* params, int slots, const DelayConst& dc, float2* ir, long ir_stride,

@@ -9,6 +9,7 @@
 // without a usable CUDA device these calls throw std::runtime_error.
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <memory>
 #include <span>
@@ -141,12 +142,12 @@ class DevicePlan {
     std::size_t total = 0;
   };
   Layout layout(int batch, long length, const ProcessorSet& procs) const;
-  cudaStream_t aux_stream() const { return aux_; }
+  const std::array<cudaStream_t, 4>& aux_streams() const { return aux_; }
   const cudaEvent_t* events() const { return events_.data(); }
 
  private:
   const RenderData& rd_;
-  cudaStream_t aux_ = nullptr;
+  std::array<cudaStream_t, 4> aux_{};  // low-priority side streams for the prologues
   std::vector<cudaEvent_t> events_;  // [0] fork, [k+1] prologue of step k done
   int* d_index_ = nullptr;
   std::vector<long> rp_off_, col_off_;

@@ -8,6 +8,9 @@ import argparse
 import os
 import sys
 
+if "--serial" in sys.argv:  # every prologue inline on the main stream: isolated kernel times
+    os.environ["MGB_NO_HOIST"] = "1"
+
 import numpy as np
 import torch
 
@@ -20,6 +23,7 @@ import paper_2408_03204_b200 as mg  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--serial", action="store_true")
     ap.add_argument("--length", type=int, default=1 << 17)
     args = ap.parse_args()
     L = args.length
