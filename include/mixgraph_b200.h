@@ -40,6 +40,7 @@ extern "C" {
 typedef struct mg_plan mg_plan;             /* RenderData (+ its device step table) */
 typedef struct mg_processors mg_processors; /* ProcessorSet (device constants) */
 typedef struct mg_graph mg_graph;           /* one captured device render (CUDA graph) */
+typedef struct mg_pipeline mg_pipeline;     /* streaming host-buffer renders (RenderPipeline) */
 
 const char* mg_last_error(void);
 int32_t mg_abi_version(void);
@@ -112,6 +113,18 @@ int32_t mg_render_graph_create(const mg_plan* plan, const mg_processors* procs, 
                                uint64_t workspace_bytes, mg_graph** out);
 int32_t mg_render_graph_launch(const mg_graph* graph, void* stream);
 void mg_render_graph_destroy(mg_graph* graph);
+
+/* Streaming host-buffer renders: submit() enqueues H2D (params + sources), the render graph
+ * and D2H (outputs) on three chained streams over `depth` rotating arenas, so consecutive
+ * renders overlap their PCIe copies with kernels. f32_io selects float host audio (else
+ * double, as render()). sources [K][B][2][L], outputs [num_outputs][B][2][L]; tables in
+ * render order, validated like mg_render. Host buffers must stay valid until sync(). */
+int32_t mg_pipeline_create(const mg_plan* plan, const mg_processors* procs, int32_t batch, int64_t length,
+                           int32_t f32_io, int32_t depth, mg_pipeline** out);
+int32_t mg_pipeline_submit(mg_pipeline* pipe, const double* const* tables, const int32_t* rows, const void* sources,
+                           void* outputs);
+int32_t mg_pipeline_sync(mg_pipeline* pipe);
+void mg_pipeline_destroy(mg_pipeline* pipe);
 
 /* ProcessorSet::process (processors.cpp:229-282): in/out [slots][B][2][L] host double;
  * params [param_rows][width] (NULL for in/out/mix). */

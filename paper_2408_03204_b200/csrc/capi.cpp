@@ -34,6 +34,11 @@ struct mg_graph {
   std::unique_ptr<RenderGraph> g;
 };
 
+struct mg_pipeline {
+  std::unique_ptr<RenderPipeline> p;
+  const mg_plan* plan;
+};
+
 struct mg_processors {
   std::unique_ptr<ProcessorSet> ps;
 };
@@ -349,6 +354,38 @@ int32_t mg_render_graph_launch(const mg_graph* g, void* stream) {
 }
 
 void mg_render_graph_destroy(mg_graph* g) { delete g; }
+
+int32_t mg_pipeline_create(const mg_plan* p, const mg_processors* procs, int32_t batch, int64_t length, int32_t f32_io,
+                           int32_t depth, mg_pipeline** out) {
+  return guarded([&] {
+    DevicePlan& dp = device_plan(p);
+    std::scoped_lock lock(const_cast<mg_plan*>(p)->render_mu);
+    auto q = std::make_unique<mg_pipeline>();
+    q->plan = p;
+    q->p = std::make_unique<RenderPipeline>(dp, *procs->ps, batch, static_cast<long>(length), f32_io != 0, depth);
+    *out = q.release();
+  });
+}
+
+int32_t mg_pipeline_submit(mg_pipeline* q, const double* const* tables, const int32_t* rows, const void* sources,
+                           void* outputs) {
+  return guarded([&] {
+    const RenderData& rd = q->plan->rd;
+    // sources / outputs are contiguous [K][B][2][L] / [O][B][2][L] host arrays
+    std::vector<const void*> src;
+    std::vector<void*> dst;
+    const std::size_t bytes = q->p->bytes_per_signal();
+    for (int k = 0; k < rd.num_inputs; ++k) src.push_back(static_cast<const char*>(sources) + bytes * k);
+    for (int o = 0; o < rd.buffer_rows - rd.output_begin; ++o) dst.push_back(static_cast<char*>(outputs) + bytes * o);
+    q->p->submit(make_store(tables, rows), src.data(), dst.data());
+  });
+}
+
+int32_t mg_pipeline_sync(mg_pipeline* q) {
+  return guarded([&] { q->p->sync(); });
+}
+
+void mg_pipeline_destroy(mg_pipeline* q) { delete q; }
 
 int32_t mg_process(const mg_processors* procs, int32_t t, const double* in, double* out, int32_t slots, int32_t batch,
                    int64_t length, const double* params, int32_t param_rows, int32_t param_offset) {

@@ -467,6 +467,131 @@ RenderGraph::~RenderGraph() {
 
 void RenderGraph::launch(cudaStream_t stream) const { cuda_check(cudaGraphLaunch(exec_, stream), "graph launch"); }
 
+// ---- RenderPipeline -----------------------------------------------------------------------
+
+namespace {
+void validate_params(const RenderData& rd, const ParamStore& params) {
+  // Per-step parameter checks, in step order (render.cpp:49-56, processors.cpp:232-247).
+  for (const StepIndex& st : rd.steps) {
+    const int width = param_width(st.type);
+    if (width == 0) continue;
+    auto it = params.tables.find(st.type);
+    if (it == params.tables.end()) fail("render: missing parameter table for " + tname(st.type));
+    const ParamMatrix& m = it->second;
+    const int slots = st.store_end - st.store_begin;
+    if (m.cols != width) fail(tname(st.type) + ": parameter row width mismatch");
+    if (st.param_begin < 0 || st.param_begin + slots > m.rows) fail(tname(st.type) + ": parameter rows out of range");
+    for (int s = 0; s < slots; ++s) check_param_row(st.type, m.row(st.param_begin + s));
+  }
+}
+}  // namespace
+
+struct RenderPipeline::Slot {
+  DeviceBuffer arena, ws, params, staging;
+  const double* tables[kNumNodeTypes] = {};
+  std::size_t table_rows[kNumNodeTypes] = {};
+  std::unique_ptr<RenderGraph> graph;
+  cudaEvent_t h2d = nullptr, done = nullptr, d2h = nullptr;
+  ~Slot() {
+    for (cudaEvent_t e : {h2d, done, d2h}) {
+      if (e) cudaEventDestroy(e);
+    }
+  }
+};
+
+RenderPipeline::RenderPipeline(const DevicePlan& plan, const ProcessorSet& procs, int batch, long length, bool f32_io,
+                               int depth)
+    : plan_(plan), procs_(procs), batch_(batch), length_(length), f32_(f32_io),
+      stride_(static_cast<long>(batch) * 2 * length) {
+  if (depth < 1) fail("RenderPipeline: depth must be >= 1");
+  cuda_check(cudaSetDevice(procs.device().device), "cudaSetDevice");
+  int least = 0, greatest = 0;
+  cuda_check(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
+  cuda_check(cudaStreamCreateWithPriority(&h2d_, cudaStreamNonBlocking, greatest), "stream");
+  cuda_check(cudaStreamCreateWithPriority(&compute_, cudaStreamNonBlocking, greatest), "stream");
+  cuda_check(cudaStreamCreateWithPriority(&d2h_, cudaStreamNonBlocking, greatest), "stream");
+  const RenderData& rd = plan.data();
+  const std::size_t rows = static_cast<std::size_t>(rd.buffer_rows);
+  const std::size_t ws_bytes = plan.workspace_bytes(batch, length, procs);
+  for (int d = 0; d < depth; ++d) {
+    auto s = std::make_unique<Slot>();
+    auto* arena = static_cast<float*>(s->arena.ensure(sizeof(float) * rows * stride_ + 16));
+    void* ws = s->ws.ensure(ws_bytes);
+    // Fixed device tables (the graph bakes their addresses), filled with default rows.
+    std::size_t total = 0;
+    for (const auto& [t, src] : rd.param_source_rows) total += src.size() * static_cast<std::size_t>(param_width(t));
+    auto* dpar = static_cast<double*>(s->params.ensure(sizeof(double) * (total + 1)));
+    std::vector<double> host;
+    for (const auto& [t, src] : rd.param_source_rows) {
+      s->tables[static_cast<int>(t)] = dpar + host.size();
+      s->table_rows[static_cast<int>(t)] = src.size();
+      std::vector<double> row(static_cast<std::size_t>(param_width(t)));
+      default_param_row(t, row);
+      for (std::size_t r = 0; r < src.size(); ++r) host.insert(host.end(), row.begin(), row.end());
+    }
+    if (!host.empty()) cuda_check(cudaMemcpy(dpar, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice), "H2D");
+    if (!f32_) s->staging.ensure(sizeof(double) * rows * stride_ + 16);
+    cuda_check(cudaMemset(arena, 0, sizeof(float) * rows * stride_), "memset");
+    s->graph = std::make_unique<RenderGraph>(plan, procs, s->tables, arena, batch, length, ws, ws_bytes);
+    for (cudaEvent_t* e : {&s->h2d, &s->done, &s->d2h}) cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+    slots_.push_back(std::move(s));
+  }
+  cuda_check(cudaDeviceSynchronize(), "pipeline setup");
+}
+
+RenderPipeline::~RenderPipeline() {
+  if (compute_) cudaStreamSynchronize(compute_);
+  if (d2h_) cudaStreamSynchronize(d2h_);
+  slots_.clear();
+  for (cudaStream_t st : {h2d_, compute_, d2h_}) {
+    if (st) cudaStreamDestroy(st);
+  }
+}
+
+void RenderPipeline::submit(const ParamStore& params, const void* const* sources, void* const* outputs) {
+  const RenderData& rd = plan_.data();
+  validate_params(rd, params);
+  Slot& s = *slots_[next_ % slots_.size()];
+  const bool reused = next_ >= slots_.size();
+  ++next_;
+  auto* arena = static_cast<float*>(s.arena.ptr);
+  // Inputs: the slot's previous render must have consumed its sources and params.
+  if (reused) cuda_check(cudaStreamWaitEvent(h2d_, s.done, 0), "wait");
+  for (const auto& [t, m] : params.tables) {
+    const int ti = static_cast<int>(t);
+    if (!s.tables[ti]) continue;
+    if (static_cast<std::size_t>(m.rows) != s.table_rows[ti]) fail("RenderPipeline: parameter table shape changed");
+    cuda_check(cudaMemcpyAsync(const_cast<double*>(s.tables[ti]), m.values.data(), sizeof(double) * m.values.size(),
+                               cudaMemcpyHostToDevice, h2d_), "H2D params");
+  }
+  const std::size_t bytes = (f32_ ? sizeof(float) : sizeof(double)) * static_cast<std::size_t>(stride_);
+  char* dst = f32_ ? reinterpret_cast<char*>(arena) : static_cast<char*>(s.staging.ptr);
+  for (int k = 0; k < rd.num_inputs; ++k) {
+    cuda_check(cudaMemcpyAsync(dst + bytes * k, sources[k], bytes, cudaMemcpyHostToDevice, h2d_), "H2D sources");
+  }
+  cuda_check(cudaEventRecord(s.h2d, h2d_), "event");
+  // Compute: after the inputs landed and the slot's previous outputs were read back.
+  cuda_check(cudaStreamWaitEvent(compute_, s.h2d, 0), "wait");
+  if (reused) cuda_check(cudaStreamWaitEvent(compute_, s.d2h, 0), "wait");
+  if (!f32_) mgb::launch_f64_to_f32(static_cast<const double*>(s.staging.ptr), arena, rd.num_inputs * stride_, compute_);
+  s.graph->launch(compute_);
+  const long n_out = (rd.buffer_rows - rd.output_begin) * stride_;
+  if (!f32_) mgb::launch_f32_to_f64(arena + rd.output_begin * stride_, static_cast<double*>(s.staging.ptr), n_out, compute_);
+  cuda_check(cudaEventRecord(s.done, compute_), "event");
+  // Outputs.
+  cuda_check(cudaStreamWaitEvent(d2h_, s.done, 0), "wait");
+  const char* src = f32_ ? reinterpret_cast<const char*>(arena + rd.output_begin * stride_) : static_cast<const char*>(s.staging.ptr);
+  for (int o = 0; o < rd.buffer_rows - rd.output_begin; ++o) {
+    cuda_check(cudaMemcpyAsync(outputs[o], src + bytes * o, bytes, cudaMemcpyDeviceToHost, d2h_), "D2H outputs");
+  }
+  cuda_check(cudaEventRecord(s.d2h, d2h_), "event");
+}
+
+void RenderPipeline::sync() {
+  cuda_check(cudaStreamSynchronize(d2h_), "pipeline sync");
+  cuda_check(cudaStreamSynchronize(compute_), "pipeline sync");
+}
+
 // ---- host-buffer API ----------------------------------------------------------------------
 
 void ProcessorSet::process_device(NodeType type, const float* in, float* out, int slots, int batch, long length,

@@ -173,6 +173,37 @@ class RenderGraph {
   cudaGraphExec_t exec_ = nullptr;
 };
 
+// Streaming host API: renders submitted back to back overlap their host<->device copies with
+// the previous render's kernels. `depth` arenas rotate; an H2D copy stream, a compute
+// stream (graph replays) and a D2H copy stream are chained with events, so PCIe traffic in
+// both directions runs concurrently with the GPU work. Host audio is float (f32_io, copied
+// straight into the arena) or double (converted on the device). Host buffers passed to
+// submit() must stay valid (and should be pinned) until sync().
+class RenderPipeline {
+ public:
+  RenderPipeline(const DevicePlan& plan, const ProcessorSet& processors, int batch, long length, bool f32_io,
+                 int depth = 2);
+  ~RenderPipeline();
+  RenderPipeline(const RenderPipeline&) = delete;
+  RenderPipeline& operator=(const RenderPipeline&) = delete;
+  // params in render order (RenderData::reorder_params); validated like render().
+  void submit(const ParamStore& params, const void* const* sources, void* const* outputs);
+  void sync();
+  std::size_t bytes_per_signal() const { return (f32_ ? sizeof(float) : sizeof(double)) * static_cast<std::size_t>(stride_); }
+
+ private:
+  struct Slot;
+  const DevicePlan& plan_;
+  const ProcessorSet& procs_;
+  int batch_;
+  long length_;
+  bool f32_;
+  long stride_;
+  std::vector<std::unique_ptr<Slot>> slots_;
+  cudaStream_t h2d_ = nullptr, compute_ = nullptr, d2h_ = nullptr;
+  std::size_t next_ = 0;
+};
+
 // Host-buffer render over caller pointers (no intermediate host copies): sources[k] and
 // outputs[o] each point at [batch][2][length] doubles (pinned memory makes the copies
 // asynchronous DMA); intermediates (original row order) may be null. `plan` may be null.

@@ -102,3 +102,56 @@ class RenderGraph:
         h, self._h = getattr(self, "_h", None), None
         if h:
             _destroy(h)
+
+
+class RenderPipeline:
+    """Streaming host-buffer renders (mg_pipeline_*): submit() returns immediately; the H2D
+    copies of render i+1 overlap the kernels of render i. `dtype` is the host audio type
+    (np.float32: copied straight into the arena; np.float64: reference AudioBuffer precision,
+    converted on the device). Host arrays should be pinned (see `pinned`) and must stay alive
+    until sync() — the pipeline keeps references until then."""
+
+    def __init__(self, rd: RenderData, procs: ProcessorSet, batch: int, length: int, dtype=np.float32, depth: int = 2):
+        from . import _tables  # noqa: F401
+        self.rd, self.procs = rd, procs
+        self.batch, self.length = int(batch), int(length)
+        self.dtype = np.dtype(dtype)
+        if self.dtype not in (np.dtype(np.float32), np.dtype(np.float64)):
+            raise ValueError("RenderPipeline: dtype must be float32 or float64")
+        self._h = ctypes.c_void_p()
+        _check(_lib.mg_pipeline_create(rd.handle, procs.handle, self.batch, self.length,
+                                       int(self.dtype == np.float32), int(depth), ctypes.byref(self._h)))
+        self._keep = []
+
+    def pinned(self, shape) -> np.ndarray:
+        """A page-locked host array of this pipeline's dtype."""
+        tdt = torch.float32 if self.dtype == np.float32 else torch.float64
+        t = torch.empty(tuple(shape), dtype=tdt, pin_memory=True)
+        arr = t.numpy()
+        self._keep.append(t)
+        return arr
+
+    def submit(self, params: Dict[int, np.ndarray], sources: np.ndarray, out: np.ndarray) -> None:
+        from . import _tables
+        k = self.rd.num_inputs
+        o = self.rd.buffer_rows - self.rd.output_begin
+        want_s = (k, self.batch, 2, self.length)
+        want_o = (o, self.batch, 2, self.length)
+        for a, shape in ((sources, want_s), (out, want_o)):
+            if a.shape != shape:
+                raise ValueError(f"RenderPipeline: expected {shape}, got {a.shape}")
+            if a.dtype != self.dtype or not a.flags.c_contiguous:
+                raise ValueError(f"RenderPipeline: arrays must be contiguous {self.dtype}")
+        ptrs, rows, keep = _tables(params)
+        _check(_lib.mg_pipeline_submit(self._h, ptrs, rows.ctypes.data_as(_vp),
+                                       ctypes.c_void_p(sources.ctypes.data), ctypes.c_void_p(out.ctypes.data)))
+        self._keep.append((sources, out))
+
+    def sync(self) -> None:
+        _check(_lib.mg_pipeline_sync(self._h))
+        self._keep = [x for x in self._keep if isinstance(x, torch.Tensor)]
+
+    def __del__(self, _destroy=_lib.mg_pipeline_destroy):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            _destroy(h)

@@ -356,3 +356,26 @@ def test_renders_are_bit_reproducible(mg, ref):
     first = mg.render(rd, procs, P, src)
     for _ in range(3):
         assert np.array_equal(mg.render(rd, procs, P, src), first)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_render_pipeline_matches_render(mg, ref, dtype):
+    # Streaming host API: three back-to-back submits with different sources and parameters.
+    t, e = ref.console(3, 0.0, 9)
+    L = 30000
+    rd = mg.compute_render_data(make(mg, t, e))
+    procs = mg.ProcessorSet()
+    pipe = mg.RenderPipeline(rd, procs, 1, L, dtype=dtype, depth=2)
+    cases = []
+    for i in range(3):
+        P = rd.reorder_params(ref.random_legal_params(t, e, 100 + i))
+        src = pipe.pinned((rd.num_inputs, 1, 2, L))
+        src[...] = np.random.default_rng(i).uniform(-1, 1, size=src.shape)
+        out = pipe.pinned((1, 1, 2, L))
+        pipe.submit(P, src, out)
+        cases.append((P, np.array(src, dtype=np.float64), out))
+    pipe.sync()
+    for P, src, out in cases:
+        want = mg.render(rd, procs, P, src.astype(np.float32).astype(np.float64))
+        assert np.array_equal(out.astype(np.float64), want.astype(np.float32).astype(np.float64)) if dtype == np.float32 \
+            else np.array_equal(out, want)
