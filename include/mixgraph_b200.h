@@ -100,10 +100,11 @@ int32_t mg_render_arena(const mg_plan* plan, const mg_processors* procs, const d
                         int32_t batch, int64_t length, void* d_workspace, uint64_t workspace_bytes, void* stream);
 
 /* Same as mg_render_arena with a device event pair recorded around every step; when step_ms
- * is non-NULL the call synchronises `stream` and writes each step's duration (ms). */
+ * is non-NULL the call synchronises `stream` and writes each step's duration (ms). hoist = 0
+ * runs each step's parameter prologue inline (isolated per-step costs). */
 int32_t mg_render_arena_profiled(const mg_plan* plan, const mg_processors* procs, const double* const* d_tables,
                                  float* d_arena, int32_t batch, int64_t length, void* d_workspace,
-                                 uint64_t workspace_bytes, void* stream, float* step_ms);
+                                 uint64_t workspace_bytes, void* stream, float* step_ms, int32_t hoist);
 
 /* Capture one device render (same arguments as mg_render_arena) into a CUDA graph whose
  * kernel nodes keep their stream priorities (main path high, parameter prologues low);
@@ -125,6 +126,12 @@ int32_t mg_pipeline_submit(mg_pipeline* pipe, const double* const* tables, const
                            void* outputs);
 int32_t mg_pipeline_sync(mg_pipeline* pipe);
 void mg_pipeline_destroy(mg_pipeline* pipe);
+
+/* Per-step device time (ms; prologue + audio pass of step k) averaged over `reps`
+ * back-to-back repetitions between one event pair, after one full render. Synchronous. */
+int32_t mg_profile_steps(const mg_plan* plan, const mg_processors* procs, const double* const* d_tables,
+                         float* d_arena, int32_t batch, int64_t length, void* d_workspace, uint64_t workspace_bytes,
+                         void* stream, int32_t reps, float* step_ms);
 
 /* ProcessorSet::process (processors.cpp:229-282): in/out [slots][B][2][L] host double;
  * params [param_rows][width] (NULL for in/out/mix). */

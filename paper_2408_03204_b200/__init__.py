@@ -67,7 +67,8 @@ _sig("mg_render", _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i64, _dbl, _vp, _v
 _sig("mg_plan_workspace_bytes", _i32, _vp, _vp, _i32, _i64, _P(_u64))
 _sig("mg_plan_kernel_count", _i32, _vp, _i32, _i64, _P(_i32))
 _sig("mg_render_arena", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp)
-_sig("mg_render_arena_profiled", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp, _vp)
+_sig("mg_render_arena_profiled", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp, _vp, _i32)
+_sig("mg_profile_steps", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp, _i32, _vp)
 _sig("mg_render_graph_create", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _P(_vp))
 _sig("mg_render_graph_launch", _i32, _vp, _vp)
 _sig("mg_render_graph_destroy", None, _vp)

@@ -312,7 +312,7 @@ int32_t mg_render_arena(const mg_plan* p, const mg_processors* procs, const doub
 
 int32_t mg_render_arena_profiled(const mg_plan* cp, const mg_processors* procs, const double* const* d_tables,
                                  float* d_arena, int32_t batch, int64_t length, void* d_ws, uint64_t ws_bytes,
-                                 void* stream, float* step_ms) {
+                                 void* stream, float* step_ms, int32_t hoist) {
   return guarded([&] {
     auto* p = const_cast<mg_plan*>(cp);
     DevicePlan& dp = device_plan(p);
@@ -326,13 +326,24 @@ int32_t mg_render_arena_profiled(const mg_plan* cp, const mg_processors* procs, 
     }
     auto s = static_cast<cudaStream_t>(stream);
     std::scoped_lock rlock(p->render_mu);
-    render_arena(dp, *procs->ps, d_tables, d_arena, batch, static_cast<long>(length), d_ws, ws_bytes, s, p->events.data());
+    render_arena(dp, *procs->ps, d_tables, d_arena, batch, static_cast<long>(length), d_ws, ws_bytes, s, p->events.data(), hoist != 0);
     if (step_ms) {
       if (cudaStreamSynchronize(s) != cudaSuccess) throw std::runtime_error("render failed");
       for (std::size_t k = 0; k < p->rd.steps.size(); ++k) {
         cudaEventElapsedTime(&step_ms[k], p->events[2 * k], p->events[2 * k + 1]);
       }
     }
+  });
+}
+
+int32_t mg_profile_steps(const mg_plan* p, const mg_processors* procs, const double* const* d_tables, float* d_arena,
+                         int32_t batch, int64_t length, void* d_ws, uint64_t ws_bytes, void* stream, int32_t reps,
+                         float* step_ms) {
+  return guarded([&] {
+    DevicePlan& dp = device_plan(p);
+    std::scoped_lock lock(const_cast<mg_plan*>(p)->render_mu);
+    profile_steps(dp, *procs->ps, d_tables, d_arena, batch, static_cast<long>(length), d_ws, ws_bytes,
+                  static_cast<cudaStream_t>(stream), reps, step_ms);
   });
 }
 

@@ -411,6 +411,54 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
   cuda_check(cudaGetLastError(), "render_arena launch");
 }
 
+// ---- per-step micro-benchmark ---------------------------------------------------------------
+
+void profile_steps(const DevicePlan& plan, const ProcessorSet& procs, const double* const* param_tables, float* arena,
+                   int batch, long length, void* workspace, std::size_t workspace_bytes, cudaStream_t stream, int reps,
+                   float* step_ms) {
+  const RenderData& rd = plan.data();
+  const DevicePlan::Layout lay = plan.layout(batch, length, procs);
+  if (workspace_bytes < lay.total) fail("profile_steps: workspace too small");
+  // One full render so every row holds its real data; then each step (prologue + audio pass)
+  // is re-run `reps` times back to back between one event pair (idempotent: same inputs,
+  // same outputs), which amortises launch and event overheads out of the per-step time.
+  render_arena(plan, procs, param_tables, arena, batch, length, workspace, workspace_bytes, stream, nullptr, false);
+  char* ws = static_cast<char*>(workspace);
+  const long rowstride = static_cast<long>(batch) * 2 * length;
+  const float2* tw = mgb::twiddle_table(procs.device().device);
+  cudaEvent_t e0, e1;
+  cuda_check(cudaEventCreate(&e0), "event");
+  cuda_check(cudaEventCreate(&e1), "event");
+  for (std::size_t k = 0; k < rd.steps.size(); ++k) {
+    const StepIndex& st = rd.steps[k];
+    const int width = param_width(st.type);
+    mgb::StepArgs a{};
+    a.src = arena;
+    a.dst = arena + st.store_begin * rowstride;
+    a.row_ptr = plan.row_ptr(static_cast<int>(k));
+    a.col = plan.col(static_cast<int>(k));
+    a.params = width > 0 ? param_tables[static_cast<int>(st.type)] + static_cast<long>(st.param_begin) * width : nullptr;
+    a.tw = tw;
+    a.slots = st.store_end - st.store_begin;
+    a.batch = batch;
+    a.length = length;
+    a.rowstride = rowstride;
+    run_prologue(st.type, a, procs, ws + lay.prologue_off[k], stream);
+    cuda_check(cudaEventRecord(e0, stream), "event");
+    for (int r = 0; r < reps; ++r) {
+      run_prologue(st.type, a, procs, ws + lay.prologue_off[k], stream);
+      run_main(st.type, a, procs, ws + lay.prologue_off[k], ws + lay.main_off, stream);
+    }
+    cuda_check(cudaEventRecord(e1, stream), "event");
+    cuda_check(cudaEventSynchronize(e1), "sync");
+    float ms = 0.f;
+    cuda_check(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+    step_ms[k] = ms / static_cast<float>(reps);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
 // ---- RenderGraph ------------------------------------------------------------------------
 
 RenderGraph::RenderGraph(const DevicePlan& plan, const ProcessorSet& procs, const double* const* param_tables,

@@ -154,6 +154,12 @@ class DevicePlan {
   std::vector<int> zero_rows_;
 };
 
+// Per-step device time (prologue + audio pass of step k, ms) from `reps` back-to-back
+// repetitions between one CUDA event pair on `stream` (after one full render). Diagnostic.
+void profile_steps(const DevicePlan& plan, const ProcessorSet& processors, const double* const* param_tables,
+                   float* arena, int batch, long length, void* workspace, std::size_t workspace_bytes,
+                   cudaStream_t stream, int reps, float* step_ms);
+
 // A whole render (main stream + side-stream prologues) captured once and instantiated as
 // a CUDA graph with node priorities: launch() replays it on any stream. Pointers, shapes and
 // parameter tables are baked in (update the tables' contents in place between launches).

@@ -72,17 +72,31 @@ class DeviceRenderer:
         the current arena, parameter tables and workspace (contents may change in place)."""
         return RenderGraph(self)
 
-    def render_profiled(self, stream: Optional[torch.cuda.Stream] = None, sync: bool = False) -> Optional[np.ndarray]:
+    def render_profiled(self, stream: Optional[torch.cuda.Stream] = None, sync: bool = False,
+                        hoist: bool = True) -> Optional[np.ndarray]:
         """Same as render() with CUDA events around every step on the launching stream. With
-        sync=True, waits and returns per-step device times (ms, one per RenderData step)."""
+        sync=True, waits and returns per-step device times (ms, one per RenderData step);
+        hoist=False runs each step's parameter prologue inline (isolated per-step costs)."""
         s = stream or torch.cuda.current_stream(self.device)
         out = np.zeros(len(self.rd.steps), dtype=np.float32) if sync else None
         _check(_lib.mg_render_arena_profiled(self.rd.handle, self.procs.handle, self._ptrs,
                                              ctypes.c_void_p(self.arena.data_ptr()), self.batch, self.length,
                                              ctypes.c_void_p(self.workspace.data_ptr()), self.workspace_bytes,
                                              ctypes.c_void_p(s.cuda_stream),
-                                             None if out is None else out.ctypes.data_as(ctypes.c_void_p)))
+                                             None if out is None else out.ctypes.data_as(ctypes.c_void_p),
+                                             int(hoist)))
         return out
+
+
+def profile_steps(dr: "DeviceRenderer", reps: int = 20, stream: Optional[torch.cuda.Stream] = None) -> np.ndarray:
+    """Per-step device time in ms (prologue + audio pass of each RenderData step), each step
+    repeated `reps` times back to back between one CUDA event pair (mg_profile_steps)."""
+    s = stream or torch.cuda.current_stream(dr.device)
+    out = np.zeros(len(dr.rd.steps), dtype=np.float32)
+    _check(_lib.mg_profile_steps(dr.rd.handle, dr.procs.handle, dr._ptrs, ctypes.c_void_p(dr.arena.data_ptr()),
+                                 dr.batch, dr.length, ctypes.c_void_p(dr.workspace.data_ptr()), dr.workspace_bytes,
+                                 ctypes.c_void_p(s.cuda_stream), int(reps), out.ctypes.data_as(ctypes.c_void_p)))
+    return out
 
 
 class RenderGraph:
