@@ -208,8 +208,8 @@ int step_kernels(NodeType t) {
     case NodeType::Eq: return 4;
     case NodeType::Compressor:
     case NodeType::Noisegate: return 1;
-    case NodeType::Reverb:
-    case NodeType::Delay: return 6;
+    case NodeType::Reverb: return 6;  // impulse responses, kernel spectrum (2), audio pass (3)
+    case NodeType::Delay: return 7;   // tap records, dense kernel, kernel spectrum (2), audio pass (3)
     default: return 1;
   }
 }
@@ -246,6 +246,29 @@ void run_main(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, void* p
     case NodeType::Reverb: mgb::launch_conv_main(a, p.reverb_length(), pws, mws, s); break;
     case NodeType::Delay: mgb::launch_conv_main(a, p.delay_span(), pws, mws, s); break;
   }
+}
+
+bool is_pointwise(NodeType t) {
+  return t == NodeType::In || t == NodeType::Out || t == NodeType::Mix || t == NodeType::Gain || t == NodeType::Imager;
+}
+
+mgb::PointOp point_op(NodeType t) {
+  return t == NodeType::Gain ? mgb::PointOp::Gain : t == NodeType::Imager ? mgb::PointOp::Imager : mgb::PointOp::Copy;
+}
+
+bool chainable(NodeType t, int slots, int batch, long length) {
+  return is_pointwise(t) && length % 4 == 0 && slots >= 1 && slots * batch <= mgb::kPwChainMaxRows;
+}
+
+// Length of the fused pointwise run starting at step k (1 = launch the step on its own).
+int chain_length(const RenderData& rd, std::size_t k, int batch, long length) {
+  int n = 0;
+  while (k + n < rd.steps.size() && n < mgb::kPwChainMax) {
+    const StepIndex& st = rd.steps[k + n];
+    if (!chainable(st.type, st.store_end - st.store_begin, batch, length)) break;
+    ++n;
+  }
+  return n >= 2 ? n : 1;
 }
 
 std::size_t step_ws_bytes(NodeType t, int slots, int batch, long length, const ProcessorSet& p) {
@@ -325,9 +348,15 @@ std::size_t DevicePlan::workspace_bytes(int batch, long length, const ProcessorS
   return layout(batch, length, procs).total;
 }
 
-int DevicePlan::kernels_per_render(int, long) const {
+int DevicePlan::kernels_per_render(int batch, long length) const {
   int k = 0;
-  for (const StepIndex& st : rd_.steps) k += step_kernels(st.type);
+  for (std::size_t i = 0; i < rd_.steps.size();) {
+    const int n = chain_length(rd_, i, batch, length);
+    k += n > 1 ? 1 : step_kernels(rd_.steps[i].type);
+    i += static_cast<std::size_t>(n);
+  }
+  // A first-step EQ is split into forward and inverse launches (render_arena, hoisted).
+  if (!rd_.steps.empty() && rd_.steps[0].type == NodeType::Eq) ++k;
   return k;
 }
 
@@ -391,6 +420,20 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
   }
   for (std::size_t k = 0; k < rd.steps.size(); ++k) {
     const NodeType t = rd.steps[k].type;
+    // Runs of small pointwise steps (latency-bound) go out as one launch, unless per-step
+    // events were asked for.
+    const int chain = step_events ? 1 : chain_length(rd, k, batch, length);
+    if (chain > 1) {
+      mgb::PwChain c{};
+      c.n = chain;
+      for (int j = 0; j < chain; ++j) {
+        c.step[j] = args[k + j];
+        c.op[j] = point_op(rd.steps[k + j].type);
+      }
+      mgb::launch_pointwise_chain(c, stream);
+      k += static_cast<std::size_t>(chain - 1);
+      continue;
+    }
     char* pws = ws + lay.prologue_off[k];
     char* mws = ws + lay.main_off;
     // The first step has nothing to hide its prologue behind: an EQ there runs its

@@ -88,11 +88,28 @@ __global__ void __launch_bounds__(512) eq_response(const float* taps, float* res
   for (int i = threadIdx.x; i < kEqFft; i += blockDim.x) r[i] = buf[sidx(i)].x * (1.f / kEqFft);
 }
 
-// grid (blocks per signal, slots*B). Block covers outputs [out0, out0 + 6144) from the
-// 8192-sample window starting at out0 - 1024 (both 4-aligned: float4 loads/stores when
-// L % 4 == 0); the circular convolution is exact for window indices [1023, 7168].
-template <int MODE>
-__global__ void __launch_bounds__(512, 2) eq_conv(StepArgs a, const float* resp, float2* spec) {
+// Window geometry per FFT size: 8192 (6144 outputs per block, the throughput choice) or
+// 4096 (2048 outputs per block: 2.2x less FFT work per CTA and 3x the CTAs, for steps whose
+// 8192 grid would not fill the GPU, e.g. a 1-slot bus EQ). The taps span +-1023 < 2048, so
+// the 4096-point response is exactly every other bin of the 8192-point one.
+template <int LOG> struct EqWin {
+  static constexpr int kFft = 1 << LOG;
+  static constexpr int kOut = LOG == 13 ? 6144 : 2048;
+  static constexpr int kThreads = LOG == 13 ? 512 : 256;
+  static constexpr int kMinBlocks = 2;
+  static constexpr int kSmem = padded(kFft) * 8;
+  static_assert(kOut <= kFft - 2 * kEqHalf, "EQ block larger than the non-wrapped window");
+};
+
+// grid (blocks per signal, slots*B). Block covers outputs [out0, out0 + kOut) from the
+// kFft-sample window starting at out0 - 1024 (both 4-aligned: float4 loads/stores when
+// L % 4 == 0); the circular convolution is exact for window indices [1023, kFft - 1024].
+template <int MODE, int LOG>
+__global__ void __launch_bounds__(EqWin<LOG>::kThreads, EqWin<LOG>::kMinBlocks) eq_conv(StepArgs a, const float* resp, float2* spec) {
+  using W = EqWin<LOG>;
+  constexpr int kEqFft = W::kFft, kEqOut = W::kOut, kNt = W::kThreads;
+  constexpr int kRs = kEqFft == 8192 ? 1 : 8192 / kEqFft;   // response bin stride
+  const float rscale = static_cast<float>(kRs);            // response is prescaled by 1/8192
   extern __shared__ float2 buf[];
   const int sb = blockIdx.y;
   const int slot = sb / a.batch, b = sb - slot * a.batch;
@@ -102,10 +119,10 @@ __global__ void __launch_bounds__(512, 2) eq_conv(StepArgs a, const float* resp,
   const long boff = static_cast<long>(b) * 2 * a.length;
   const bool vec = (a.length & 3) == 0;
   float2* sp = spec + (static_cast<long>(sb) * gridDim.x + blockIdx.x) * kEqFft;  // MODE 1/2 scratch
-  const float* rs = resp + static_cast<long>(slot) * kEqFft;
+  const float* rs = resp + static_cast<long>(slot) * 8192;
   if constexpr (MODE == 2) {
     // spectrum computed earlier by MODE 1: load it with the response product fused
-    for (int t = threadIdx.x; t < kEqFft; t += blockDim.x) buf[sidx(t)] = cscale(__ldg(sp + t), __ldg(rs + t));
+    for (int t = threadIdx.x; t < kEqFft; t += blockDim.x) buf[sidx(t)] = cscale(__ldg(sp + t), rscale * __ldg(rs + kRs * t));
     __syncthreads();
   } else {
   for (int t4 = threadIdx.x; t4 < kEqFft / 4; t4 += blockDim.x) {
@@ -136,15 +153,15 @@ __global__ void __launch_bounds__(512, 2) eq_conv(StepArgs a, const float* resp,
     buf[sidx(4 * t4 + 3)] = make_float2(l.w, r.w);
   }
   __syncthreads();
-  fft_pow2<kLogFft, 1, 512, -1>(buf, kEqBuf, a.tw);
+  fft_pow2<LOG, 1, kNt, -1>(buf, padded(kEqFft), a.tw);
   if constexpr (MODE == 1) {
     for (int t = threadIdx.x; t < kEqFft; t += blockDim.x) sp[t] = buf[sidx(t)];
     return;
   }
-  for (int t = threadIdx.x; t < kEqFft; t += blockDim.x) buf[sidx(t)] = cscale(buf[sidx(t)], __ldg(rs + t));
+  for (int t = threadIdx.x; t < kEqFft; t += blockDim.x) buf[sidx(t)] = cscale(buf[sidx(t)], rscale * __ldg(rs + kRs * t));
   __syncthreads();
   }
-  fft_pow2<kLogFft, 1, 512, +1>(buf, kEqBuf, a.tw);
+  fft_pow2<LOG, 1, kNt, +1>(buf, padded(kEqFft), a.tw);
   float* yl = a.dst + static_cast<long>(slot) * a.rowstride + boff;
   float* yr = yl + a.length;
   for (int t4 = threadIdx.x; t4 < kEqOut / 4; t4 += blockDim.x) {
@@ -172,7 +189,7 @@ __global__ void __launch_bounds__(512, 2) eq_conv(StepArgs a, const float* resp,
 void eq_setup() {
   static const bool done = [] {
     cudaFuncSetAttribute(eq_response, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqSmem);
-    for (auto fn : {eq_conv<0>, eq_conv<1>, eq_conv<2>}) {
+    for (auto fn : {eq_conv<0, 13>, eq_conv<1, 13>, eq_conv<2, 13>, eq_conv<0, 12>}) {
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqSmem);
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     }
@@ -199,27 +216,47 @@ std::size_t eq_spectrum_bytes(int slots, int batch, long length) {
 }
 
 namespace {
+template <int LOG>
 dim3 eq_grid(const StepArgs& a) {
-  return dim3(static_cast<unsigned>((a.length + kEqOut - 1) / kEqOut), static_cast<unsigned>(a.slots * a.batch));
+  constexpr int out = EqWin<LOG>::kOut;
+  return dim3(static_cast<unsigned>((a.length + out - 1) / out), static_cast<unsigned>(a.slots * a.batch));
+}
+
+int sm_count() {
+  static const int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
 }
 }  // namespace
+
+bool eq_uses_small_window(const StepArgs& a) {
+  const dim3 g = eq_grid<13>(a);
+  return static_cast<long>(g.x) * g.y < sm_count();
+}
 
 void launch_eq_main(const StepArgs& a, const float* resp_ws, cudaStream_t s) {
   if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
   eq_setup();
-  eq_conv<0><<<eq_grid(a), 512, kEqSmem, s>>>(a, resp_ws, nullptr);
+  if (eq_uses_small_window(a)) {
+    eq_conv<0, 12><<<eq_grid<12>(a), EqWin<12>::kThreads, EqWin<12>::kSmem, s>>>(a, resp_ws, nullptr);
+    return;
+  }
+  eq_conv<0, 13><<<eq_grid<13>(a), 512, kEqSmem, s>>>(a, resp_ws, nullptr);
 }
 
 void launch_eq_forward(const StepArgs& a, float2* spectrum, cudaStream_t s) {
   if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
   eq_setup();
-  eq_conv<1><<<eq_grid(a), 512, kEqSmem, s>>>(a, nullptr, spectrum);
+  eq_conv<1, 13><<<eq_grid<13>(a), 512, kEqSmem, s>>>(a, nullptr, spectrum);
 }
 
 void launch_eq_inverse(const StepArgs& a, const float* resp_ws, const float2* spectrum, cudaStream_t s) {
   if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
   eq_setup();
-  eq_conv<2><<<eq_grid(a), 512, kEqSmem, s>>>(a, resp_ws, const_cast<float2*>(spectrum));
+  eq_conv<2, 13><<<eq_grid<13>(a), 512, kEqSmem, s>>>(a, resp_ws, const_cast<float2*>(spectrum));
 }
 
 }  // namespace mgb

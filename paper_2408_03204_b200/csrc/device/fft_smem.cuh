@@ -220,8 +220,16 @@ __device__ __forceinline__ void stockham_pass(float2* buf, int fstride, const fl
     if (TOTAL % NTHR == 0 || b < TOTAL) {
       const int f = b / M, j = b - f * M;
       const float2* base = buf + f * fstride;
+      if constexpr (PAD && M % 16 == 0) {
+        // j + r*M with M a multiple of 16: sidx(j + r*M) = sidx(j) + r*padded(M), so every
+        // load is one base register plus an immediate offset (no per-element index math).
+        const float2* lb = base + sidx(j);
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[q][r] = base[PAD ? sidx(j + r * M) : j + r * M];
+        for (int r = 0; r < R; ++r) v[q][r] = lb[r * padded(M)];
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[q][r] = base[PAD ? sidx(j + r * M) : j + r * M];
+      }
     }
   }
   __syncthreads();
@@ -244,8 +252,18 @@ __device__ __forceinline__ void stockham_pass(float2* buf, int fstride, const fl
       Dft<R, DIR>::run(v[q]);
       float2* base = buf + f * fstride;
       const int o0 = (j / NS) * NS * R + jm;
+      if constexpr (PAD && NS % 16 == 0) {
+        float2* sb = base + sidx(o0);  // o0 + r*NS, NS a multiple of 16: immediate offsets
 #pragma unroll
-      for (int r = 0; r < R; ++r) base[PAD ? sidx(o0 + r * NS) : o0 + r * NS] = v[q][r];
+        for (int r = 0; r < R; ++r) sb[r * padded(NS)] = v[q][r];
+      } else if constexpr (PAD && NS == 1 && R == 16) {
+        float2* sb = base + 17 * j;    // o0 = 16 j: sidx(16 j + r) = 17 j + r
+#pragma unroll
+        for (int r = 0; r < R; ++r) sb[r] = v[q][r];
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) base[PAD ? sidx(o0 + r * NS) : o0 + r * NS] = v[q][r];
+      }
     }
   }
   __syncthreads();

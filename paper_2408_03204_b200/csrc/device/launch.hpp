@@ -14,6 +14,18 @@ enum class PointOp : int { Copy = 0, Gain = 1, Imager = 2 };
 // Gather-sum + copy / gain / imager + store (mix, out, gain, imager steps).
 void launch_pointwise(PointOp op, const StepArgs& a, cudaStream_t s);
 
+// A run of consecutive small pointwise steps (each slots*batch <= kPwChainMaxRows, L % 4 == 0)
+// in one launch, steps applied in order per sample group (latency-bound bus tails).
+constexpr int kPwChainMax = 8;
+constexpr int kPwChainMaxRows = 4;
+struct PwChain {
+  StepArgs step[kPwChainMax];
+  PointOp op[kPwChainMax];
+  int n;
+};
+bool pointwise_chain_ok(const StepArgs& a);
+void launch_pointwise_chain(const PwChain& c, cudaStream_t s);
+
 // EQ: FIR design (fp64 cosine sum, `dsp.cpp:106-136`) -> 8192-bin zero-phase response
 // (prologue: parameters only) ; overlap-save convolution fused with gather and store (main).
 constexpr int kEqFft = 8192;

@@ -115,7 +115,60 @@ void launch_op(const StepArgs& a, cudaStream_t s) {
   pointwise_scalar<OP><<<grid, 256, 0, s>>>(a);
 }
 
+// A run of consecutive small pointwise steps (the 1-slot bus tail: imager -> gain -> out) in
+// one launch. Every step is sample-local, so the thread owning float4 group i of batch row b
+// computes group i of every slot of every step in step order: a later step's gather reads
+// rows this same thread stored moments earlier (plain loads, not the non-coherent __ldg path,
+// so program order makes them visible). Results are identical to the per-step launches.
+__global__ void __launch_bounds__(kPwThreads) pointwise_chain_vec4(PwChain c) {
+  const int b = blockIdx.y;
+  const long i = blockIdx.x * static_cast<long>(kPwThreads) + threadIdx.x;
+  for (int k = 0; k < c.n; ++k) {
+    const StepArgs& a = c.step[k];
+    const long n4 = a.length >> 2;
+    if (i >= n4) return;
+    const long boff = static_cast<long>(b) * 2 * a.length;
+    for (int slot = 0; slot < a.slots; ++slot) {
+      const int e0 = a.row_ptr[slot], e1 = a.row_ptr[slot + 1];
+      float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
+      for (int e = e0; e < e1; ++e) {
+        const float4* p = reinterpret_cast<const float4*>(a.src + static_cast<long>(a.col[e]) * a.rowstride + boff);
+        l = f4add(l, p[i]);
+        r = f4add(r, p[n4 + i]);
+      }
+      float g0 = 1.f, g1 = 1.f;
+      switch (c.op[k]) {
+        case PointOp::Gain:
+          coeffs<PointOp::Gain>(a, slot, g0, g1);
+          apply<PointOp::Gain>(l.x, r.x, g0, g1), apply<PointOp::Gain>(l.y, r.y, g0, g1);
+          apply<PointOp::Gain>(l.z, r.z, g0, g1), apply<PointOp::Gain>(l.w, r.w, g0, g1);
+          break;
+        case PointOp::Imager:
+          coeffs<PointOp::Imager>(a, slot, g0, g1);
+          apply<PointOp::Imager>(l.x, r.x, g0, g1), apply<PointOp::Imager>(l.y, r.y, g0, g1);
+          apply<PointOp::Imager>(l.z, r.z, g0, g1), apply<PointOp::Imager>(l.w, r.w, g0, g1);
+          break;
+        default: break;
+      }
+      float* out = a.dst + static_cast<long>(slot) * a.rowstride + boff;
+      reinterpret_cast<float4*>(out)[i] = l;
+      reinterpret_cast<float4*>(out + a.length)[i] = r;
+    }
+  }
+}
+
 }  // namespace
+
+bool pointwise_chain_ok(const StepArgs& a) {
+  return a.length % 4 == 0 && a.slots >= 1 && a.slots * a.batch <= kPwChainMaxRows;
+}
+
+void launch_pointwise_chain(const PwChain& c, cudaStream_t s) {
+  if (c.n <= 0) return;
+  const StepArgs& a = c.step[0];
+  const dim3 grid(static_cast<unsigned>((a.length / 4 + kPwThreads - 1) / kPwThreads), static_cast<unsigned>(a.batch));
+  pointwise_chain_vec4<<<grid, kPwThreads, 0, s>>>(c);
+}
 
 void launch_pointwise(PointOp op, const StepArgs& a, cudaStream_t s) {
   switch (op) {
