@@ -26,12 +26,12 @@ namespace {
 constexpr unsigned long long kFlagAgg = 1ull << 32;
 
 struct DynParams {
-  float a, oma, aN, a16, atile;
+  float a, oma, aN, a16, atile, atile32;
   float T, W, R, invR, floor_;
   int Ne;
 };
 
-__device__ __forceinline__ DynParams load_params(const double* row, int env_taps, double floor_, long L) {
+__device__ __noinline__ DynParams load_params(const double* row, int env_taps, double floor_, long L) {
   DynParams p;
   const double a = row[0];
   p.a = static_cast<float>(a);
@@ -41,6 +41,7 @@ __device__ __forceinline__ DynParams load_params(const double* row, int env_taps
   p.aN = aN < 1e-30 ? 0.f : static_cast<float>(aN);
   p.a16 = static_cast<float>(pow(a, static_cast<double>(kDynPerThread)));
   p.atile = static_cast<float>(pow(a, static_cast<double>(kDynTile)));
+  p.atile32 = static_cast<float>(pow(a, 32.0 * kDynTile));
   p.T = static_cast<float>(row[1]);
   p.W = static_cast<float>(row[2]);
   p.R = static_cast<float>(row[3]);
@@ -120,41 +121,54 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
   __shared__ float wA[kDynThreads / 32], wB[kDynThreads / 32];
   __shared__ float s_carry;
   __shared__ int s_ticket;
-  if (threadIdx.x == 0) s_ticket = static_cast<int>(atomicAdd(ticket, 1u));
-  __syncthreads();
+  __shared__ DynParams s_p;
   // Tickets interleave sequences (all tile-0s, then all tile-1s, ...): a tile's
   // predecessors were dispatched `nseq` tickets earlier, so the carry rarely waits.
-  const int tk = s_ticket;
   const int nseq = a.slots * a.batch;
+  if (threadIdx.x == 0) {
+    // One thread derives the slot's fp64 constants (pow) and broadcasts them.
+    const int tk = static_cast<int>(atomicAdd(ticket, 1u));
+    s_ticket = tk;
+    s_p = load_params(a.params + 4L * ((tk % nseq) / a.batch), env_taps, floor_, a.length);
+  }
+  __syncthreads();
+  const int tk = s_ticket;
   const int tile = tk / nseq, seq = tk - tile * nseq;
   const int slot = seq / a.batch, b = seq - slot * a.batch;
   const int e0 = __ldg(a.row_ptr + slot), e1 = __ldg(a.row_ptr + slot + 1);
-  const DynParams p = load_params(a.params + 4L * slot, env_taps, floor_, a.length);
+  const DynParams p = s_p;
 
   const long n0 = static_cast<long>(tile) * kDynTile + static_cast<long>(threadIdx.x) * kDynPerThread;
-  float ul[kDynPerThread], ur[kDynPerThread], eo[kDynPerThread];
-  load16<VEC>(a, e0, e1, b, n0, ul, ur);
-  const bool corr = p.aN != 0.f;
-  if (corr) {
-    float ol[kDynPerThread], orr[kDynPerThread];
-    load16<VEC>(a, e0, e1, b, n0 - p.Ne, ol, orr);
+  // drive[k] = (1-a) (e[n] - a^Ne e[n-Ne]) is all the scan keeps in registers; the input
+  // samples are gathered again (L2-resident) for the output pass, so nothing else stays live
+  // across the carry wait (no spills at 64 registers).
+  float drive[kDynPerThread];
+  {
+    float ul[kDynPerThread], ur[kDynPerThread], eo[kDynPerThread];
+    load16<VEC>(a, e0, e1, b, n0, ul, ur);
+    if (p.aN != 0.f) {
+      float ol[kDynPerThread], orr[kDynPerThread];
+      load16<VEC>(a, e0, e1, b, n0 - p.Ne, ol, orr);
+#pragma unroll
+      for (int k = 0; k < kDynPerThread; ++k) {
+        const float m = ol[k] + orr[k];
+        eo[k] = p.aN * (m * m);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kDynPerThread; ++k) eo[k] = 0.f;
+    }
 #pragma unroll
     for (int k = 0; k < kDynPerThread; ++k) {
-      const float m = ol[k] + orr[k];
-      eo[k] = p.aN * (m * m);
+      const float m = ul[k] + ur[k];
+      drive[k] = p.oma * (m * m - eo[k]);
     }
-  } else {
-#pragma unroll
-    for (int k = 0; k < kDynPerThread; ++k) eo[k] = 0.f;
   }
 
   // Thread-local recurrence from 0.
   float B = 0.f;
 #pragma unroll
-  for (int k = 0; k < kDynPerThread; ++k) {
-    const float m = ul[k] + ur[k];
-    B = fmaf(p.a, B, p.oma * (m * m - eo[k]));
-  }
+  for (int k = 0; k < kDynPerThread; ++k) B = fmaf(p.a, B, drive[k]);
   float A = p.a16;
 
   // Warp inclusive scan of affine maps.
@@ -208,8 +222,11 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
     cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> mine(status[static_cast<long>(seq) * tiles_per_seq + tile]);
     if (lane == 0) mine.store(kFlagAgg | __float_as_uint(tileB), cuda::memory_order_relaxed);
     float part = 0.f;
-    for (int d0 = 0; d0 < tile; d0 += 32) {
-      if (powf(p.atile, static_cast<float>(d0)) == 0.f) break;
+    // weight A^d = A^lane * (A^32)^(d0/32): one powf per lane, then exact-order products
+    const float wl = tile > 0 ? powf(p.atile, static_cast<float>(lane)) : 0.f;
+    float w32 = 1.f;  // (A^32)^(d0/32)
+    for (int d0 = 0; d0 < tile; d0 += 32, w32 *= p.atile32) {
+      if (w32 == 0.f) break;
       const int d = d0 + lane;
       if (d < tile) {
         cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[static_cast<long>(seq) * tiles_per_seq + tile - 1 - d]);
@@ -217,7 +234,7 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
         do {
           w = st.load(cuda::memory_order_relaxed);
         } while ((w >> 32) == 0);
-        part = fmaf(powf(p.atile, static_cast<float>(d)), __uint_as_float(static_cast<unsigned int>(w & 0xffffffffu)), part);
+        part = fmaf(wl * w32, __uint_as_float(static_cast<unsigned int>(w & 0xffffffffu)), part);
       }
     }
 #pragma unroll
@@ -229,6 +246,8 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
   // Replay the recurrence from this thread's true start state, apply the gain, store.
   float g = fmaf(xA, s_carry, xB);
   if (n0 >= a.length) return;
+  float ul[kDynPerThread], ur[kDynPerThread];
+  load16<VEC>(a, e0, e1, b, n0, ul, ur);
   float* ol = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length + n0;
   float* orr = ol + a.length;
   const bool full = VEC && n0 + kDynPerThread <= a.length;
@@ -238,8 +257,7 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
 #pragma unroll
     for (int k4 = 0; k4 < 4; ++k4) {
       const int k = 4 * q + k4;
-      const float m = ul[k] + ur[k];
-      g = fmaf(p.a, g, p.oma * (m * m - eo[k]));
+      g = fmaf(p.a, g, drive[k]);
       const float gn = gain_of<GATE>(g, p);
       yl[k4] = gn * ul[k];
       yr[k4] = gn * ur[k];
