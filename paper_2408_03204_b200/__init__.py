@@ -12,6 +12,7 @@ module fails loudly if the shared library is missing.
 from __future__ import annotations
 
 import ctypes
+import functools
 import enum
 import os
 from dataclasses import dataclass, field
@@ -321,46 +322,69 @@ class RenderData:
 
     def __init__(self, handle, fg: FlatGraph):
         self._h = handle
+        self._fg = fg
         info = np.zeros(6, dtype=np.int32)
         _check(_lib.mg_plan_info(self._h, _ptr(info)))
-        n_steps, self.buffer_rows, self.num_inputs, self.output_begin, n_edges, n_ts = (int(x) for x in info)
-        buf = ctypes.create_string_buffer(n_ts + 1)
-        _check(_lib.mg_plan_type_codes(self._h, buf, n_ts + 1))
-        sizes = np.zeros(n_ts, dtype=np.int32)
-        rows = np.zeros(fg.num_nodes(), dtype=np.int32)
+        self.num_steps, self.buffer_rows, self.num_inputs, self.output_begin, self._n_edges, self._n_ts = \
+            (int(x) for x in info)
+
+    # The schedule, sigma, flat graph and step table are materialised as Python objects only
+    # when asked for (parity tests, inspection); the render path needs just the handle.
+    @functools.cached_property
+    def schedule(self) -> "Schedule":
+        buf = ctypes.create_string_buffer(self._n_ts + 1)
+        _check(_lib.mg_plan_type_codes(self._h, buf, self._n_ts + 1))
+        sizes = np.zeros(self._n_ts, dtype=np.int32)
+        rows = np.zeros(self._fg.num_nodes(), dtype=np.int32)
         _check(_lib.mg_plan_subsets(self._h, _ptr(sizes), _ptr(rows)))
         subsets, off = [], 0
-        for s in sizes:
-            subsets.append([int(r) for r in rows[off:off + s]])
-            off += int(s)
-        self.schedule = Schedule([type_from_code(c) for c in buf.value.decode()], subsets)
-        sig = np.zeros(fg.num_nodes(), dtype=np.int32)
+        for sz in sizes:
+            subsets.append([int(r) for r in rows[off:off + sz]])
+            off += int(sz)
+        return Schedule([type_from_code(c) for c in buf.value.decode()], subsets)
+
+    @functools.cached_property
+    def sigma(self) -> List[int]:
+        sig = np.zeros(self._fg.num_nodes(), dtype=np.int32)
         _check(_lib.mg_plan_sigma(self._h, _ptr(sig)))
-        self.sigma = [int(x) for x in sig]
-        ft = np.zeros(fg.num_nodes(), dtype=np.int32)
+        return [int(x) for x in sig]
+
+    @functools.cached_property
+    def flat(self) -> "FlatGraph":
+        n_edges = self._n_edges
+        ft = np.zeros(self._fg.num_nodes(), dtype=np.int32)
         fe = np.zeros((max(n_edges, 1), 4), dtype=np.int32)
         _check(_lib.mg_plan_flat(self._h, _ptr(ft), _ptr(fe)))
-        self.flat = FlatGraph([NodeType(int(t)) for t in ft], [tuple(int(v) for v in r) for r in fe[:n_edges]],
-                              {}, fg.num_inputs, fg.num_outputs)
-        self.steps: List[StepIndex] = []
+        flat = FlatGraph([NodeType(int(t)) for t in ft], [tuple(int(v) for v in r) for r in fe[:n_edges]],
+                         {}, self._fg.num_inputs, self._fg.num_outputs)
+        if self._fg.params:
+            flat.params = self.reorder_params(self._fg.params)
+        return flat
+
+    @functools.cached_property
+    def steps(self) -> List["StepIndex"]:
+        out: List[StepIndex] = []
         head = np.zeros(6, dtype=np.int32)
-        for k in range(n_steps):
+        for k in range(self.num_steps):
             _check(_lib.mg_plan_step(self._h, k, _ptr(head), None, None))
             g = np.zeros(max(int(head[5]), 1), dtype=np.int32)
             a = np.zeros(max(int(head[5]), 1), dtype=np.int32)
             _check(_lib.mg_plan_step(self._h, k, _ptr(head), _ptr(g), _ptr(a)))
             m = int(head[5])
-            self.steps.append(StepIndex(NodeType(int(head[0])), [int(x) for x in g[:m]], [int(x) for x in a[:m]],
-                                        int(head[1]), int(head[2]), int(head[3]), int(head[4])))
-        self.param_source_rows: Dict[NodeType, List[int]] = {}
+            out.append(StepIndex(NodeType(int(head[0])), [int(x) for x in g[:m]], [int(x) for x in a[:m]],
+                                 int(head[1]), int(head[2]), int(head[3]), int(head[4])))
+        return out
+
+    @functools.cached_property
+    def param_source_rows(self) -> Dict[NodeType, List[int]]:
+        out: Dict[NodeType, List[int]] = {}
         for t in range(NUM_NODE_TYPES):
             n = int(_lib.mg_plan_param_source_rows(self._h, t, None))
             if n > 0:
-                out = np.zeros(n, dtype=np.int32)
-                _lib.mg_plan_param_source_rows(self._h, t, _ptr(out))
-                self.param_source_rows[NodeType(t)] = [int(x) for x in out]
-        if fg.params:
-            self.flat.params = self.reorder_params(fg.params)
+                rows = np.zeros(n, dtype=np.int32)
+                _lib.mg_plan_param_source_rows(self._h, t, _ptr(rows))
+                out[NodeType(t)] = [int(x) for x in rows]
+        return out
 
     @property
     def handle(self):

@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -128,7 +129,16 @@ int32_t mg_plan_create(const int32_t* types, int32_t n, const int32_t* edges, in
                        int32_t beam_width, int32_t optimal_cap, mg_plan** out) {
   return guarded([&] {
     if (strategy < 0 || strategy > 3) throw std::invalid_argument("unknown strategy");
-    FlatGraph fg = to_flat(make_graph(types, n, edges, ne));
+    // to_flat without the default parameter tables: C-ABI renders always pass their own
+    // tables, and building/reordering defaults (tens of MB for a 64-graph union) would
+    // dominate the plan build.
+    const Graph g = make_graph(types, n, edges, ne);
+    g.validate();
+    FlatGraph fg;
+    fg.node_types = g.node_types();
+    fg.edges = g.edges();
+    fg.num_inputs = static_cast<int>(std::count(fg.node_types.begin(), fg.node_types.end(), NodeType::In));
+    fg.num_outputs = static_cast<int>(std::count(fg.node_types.begin(), fg.node_types.end(), NodeType::Out));
     ScheduleOptions o;
     o.strategy = static_cast<Strategy>(strategy);
     o.beam_width = beam_width;

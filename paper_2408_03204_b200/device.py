@@ -78,7 +78,7 @@ class DeviceRenderer:
         sync=True, waits and returns per-step device times (ms, one per RenderData step);
         hoist=False runs each step's parameter prologue inline (isolated per-step costs)."""
         s = stream or torch.cuda.current_stream(self.device)
-        out = np.zeros(len(self.rd.steps), dtype=np.float32) if sync else None
+        out = np.zeros(self.rd.num_steps, dtype=np.float32) if sync else None
         _check(_lib.mg_render_arena_profiled(self.rd.handle, self.procs.handle, self._ptrs,
                                              ctypes.c_void_p(self.arena.data_ptr()), self.batch, self.length,
                                              ctypes.c_void_p(self.workspace.data_ptr()), self.workspace_bytes,
@@ -92,7 +92,7 @@ def profile_steps(dr: "DeviceRenderer", reps: int = 20, stream: Optional[torch.c
     """Per-step device time in ms (prologue + audio pass of each RenderData step), each step
     repeated `reps` times back to back between one CUDA event pair (mg_profile_steps)."""
     s = stream or torch.cuda.current_stream(dr.device)
-    out = np.zeros(len(dr.rd.steps), dtype=np.float32)
+    out = np.zeros(dr.rd.num_steps, dtype=np.float32)
     _check(_lib.mg_profile_steps(dr.rd.handle, dr.procs.handle, dr._ptrs, ctypes.c_void_p(dr.arena.data_ptr()),
                                  dr.batch, dr.length, ctypes.c_void_p(dr.workspace.data_ptr()), dr.workspace_bytes,
                                  ctypes.c_void_p(s.cuda_stream), int(reps), out.ctypes.data_as(ctypes.c_void_p)))
