@@ -31,23 +31,33 @@ struct DynParams {
   int Ne;
 };
 
-__device__ __noinline__ DynParams load_params(const double* row, int env_taps, double floor_, long L) {
-  DynParams p;
+// Slot constants, derived by warp 0 of each CTA: lanes 0-3 evaluate the four fp64 powers
+// a^Ne, a^8, a^tile, a^(32 tile) side by side (one pow latency), lane 0 assembles.
+__device__ __forceinline__ void derive_params(const double* row, int env_taps, double floor_, long L, int lane,
+                                              DynParams* out) {
   const double a = row[0];
+  const int Ne = static_cast<int>(env_taps < L ? env_taps : L);
+  const double e = lane == 0 ? static_cast<double>(Ne)
+                 : lane == 1 ? static_cast<double>(kDynPerThread)
+                 : lane == 2 ? static_cast<double>(kDynTile) : 32.0 * kDynTile;
+  const double pw = lane < 4 ? pow(a, e) : 0.0;
+  const double aN = __shfl_sync(0xffffffffu, pw, 0), a16 = __shfl_sync(0xffffffffu, pw, 1);
+  const double atile = __shfl_sync(0xffffffffu, pw, 2), atile32 = __shfl_sync(0xffffffffu, pw, 3);
+  if (lane != 0) return;
+  DynParams p;
   p.a = static_cast<float>(a);
   p.oma = static_cast<float>(1.0 - a);
-  p.Ne = static_cast<int>(env_taps < L ? env_taps : L);
-  const double aN = pow(a, static_cast<double>(p.Ne));
+  p.Ne = Ne;
   p.aN = aN < 1e-30 ? 0.f : static_cast<float>(aN);
-  p.a16 = static_cast<float>(pow(a, static_cast<double>(kDynPerThread)));
-  p.atile = static_cast<float>(pow(a, static_cast<double>(kDynTile)));
-  p.atile32 = static_cast<float>(pow(a, 32.0 * kDynTile));
+  p.a16 = static_cast<float>(a16);
+  p.atile = static_cast<float>(atile);
+  p.atile32 = static_cast<float>(atile32);
   p.T = static_cast<float>(row[1]);
   p.W = static_cast<float>(row[2]);
   p.R = static_cast<float>(row[3]);
   p.invR = static_cast<float>(1.0 / row[3]);
   p.floor_ = static_cast<float>(floor_);
-  return p;
+  *out = p;
 }
 
 template <bool GATE>
@@ -125,11 +135,12 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
   // Tickets interleave sequences (all tile-0s, then all tile-1s, ...): a tile's
   // predecessors were dispatched `nseq` tickets earlier, so the carry rarely waits.
   const int nseq = a.slots * a.batch;
-  if (threadIdx.x == 0) {
-    // One thread derives the slot's fp64 constants (pow) and broadcasts them.
-    const int tk = static_cast<int>(atomicAdd(ticket, 1u));
-    s_ticket = tk;
-    s_p = load_params(a.params + 4L * ((tk % nseq) / a.batch), env_taps, floor_, a.length);
+  if (threadIdx.x < 32) {
+    int tk = 0;
+    if (threadIdx.x == 0) tk = static_cast<int>(atomicAdd(ticket, 1u));
+    tk = __shfl_sync(0xffffffffu, tk, 0);
+    if (threadIdx.x == 0) s_ticket = tk;
+    derive_params(a.params + 4L * ((tk % nseq) / a.batch), env_taps, floor_, a.length, threadIdx.x, &s_p);
   }
   __syncthreads();
   const int tk = s_ticket;

@@ -76,8 +76,10 @@ def main():
     # order: a prologue pair (cols_fwd<.., 0>, rows_spec) belongs to the reverb_ir / delay_dense
     # that precedes it; main triples (cols_fwd<.., 1>, rows_conv, cols_inv) follow the step
     # order reverb then delay (config 2's type string ...rd...).
-    start = next(i for i, r in enumerate(recs) if "eq_conv<1>" in r["kernel"])
-    end = next((i for i in range(start + 1, len(recs)) if "eq_conv<1>" in recs[i]["kernel"]), len(recs))
+    first = lambda k: "eq_conv<1>" in k or "eq_conv<1," in k  # noqa: E731  (split first-step EQ)
+    start = next(i for i, r in enumerate(recs) if first(r["kernel"]))
+    end = next((i for i in range(start + 1, len(recs)) if first(recs[i]["kernel"]) or "mgb::" not in recs[i]["kernel"]),
+               len(recs))
     traffic, per_kernel = {}, []
     owner, main_seen = None, 0
     for r in recs[start:end]:
@@ -99,6 +101,8 @@ def main():
             step = "gain"
         elif "pointwise_vec4<2>" in k:
             step = "imager"
+        elif "pointwise_chain" in k:
+            step = "imager+gain+out (fused chain)"
         elif "reverb_ir" in k or "delay_" in k or "rows_spec" in k or ", 0>(" in k:
             step = owner
         elif "cols_fwd" in k or "rows_conv" in k or "cols_inv" in k:
