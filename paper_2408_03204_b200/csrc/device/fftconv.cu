@@ -176,7 +176,18 @@ __global__ void __launch_bounds__(row_threads<LN2, kSpecRows>()) rows_spec(int l
   extern __shared__ float2 row[];
   const long N = 1L << log_n;
   float2* p = P + static_cast<long>(blockIdx.y) * N + static_cast<long>(blockIdx.x) * kSpecRows * N2;
-  for (int i = threadIdx.x; i < kSpecRows * N2; i += NT) row[(i / N2) * RS + sidx(i % N2)] = p[i];
+  // All of this thread's loads are issued before any smem store (loads in flight, not a
+  // load -> store dependency per element).
+  constexpr int PER = kSpecRows * N2 / NT;
+  static_assert(PER * NT == kSpecRows * N2, "rows_spec: threads must tile the rows");
+  float2 v[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) v[q] = p[threadIdx.x + q * NT];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int i = threadIdx.x + q * NT;
+    row[(i / N2) * RS + sidx(i % N2)] = v[q];
+  }
   __syncthreads();
   fft_pow2<LN2, kSpecRows, NT, -1>(row, RS, tw);
   for (int i = threadIdx.x; i < kSpecRows * N2; i += NT) p[i] = row[(i / N2) * RS + sidx(i % N2)];
@@ -200,9 +211,20 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2,
   const float2* pa = P + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
   const float2* pb = P + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
   constexpr int RS = padded(N2);  // second row's offset
-  for (int i = threadIdx.x; i < N2; i += NT) {
-    rows[sidx(i)] = xa[i];
-    rows[RS + sidx(i)] = xb[i];
+  {
+    constexpr int PER = N2 / NT;
+    static_assert(PER * NT == N2, "rows_conv: threads must tile a row");
+    float2 va[PER], vb[PER];  // loads in flight before any smem store
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      va[q] = xa[threadIdx.x + q * NT];
+      vb[q] = xb[threadIdx.x + q * NT];
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      rows[sidx(threadIdx.x + q * NT)] = va[q];
+      rows[RS + sidx(threadIdx.x + q * NT)] = vb[q];
+    }
   }
   __syncthreads();
   // The kernel spectrum values this thread pairs are fetched before the forward FFT so
