@@ -209,7 +209,7 @@ int step_kernels(NodeType t) {
     case NodeType::Compressor:
     case NodeType::Noisegate: return 1;
     case NodeType::Reverb: return 6;  // impulse responses, kernel spectrum (2), audio pass (3)
-    case NodeType::Delay: return 7;   // tap records, dense kernel, kernel spectrum (2), audio pass (3)
+    case NodeType::Delay: return 6;   // tap records, kernel spectrum (2), audio pass (3)
     default: return 1;
   }
 }

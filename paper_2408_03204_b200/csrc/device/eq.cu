@@ -121,36 +121,61 @@ __global__ void __launch_bounds__(EqWin<LOG>::kThreads, EqWin<LOG>::kMinBlocks) 
   float2* sp = spec + (static_cast<long>(sb) * gridDim.x + blockIdx.x) * kEqFft;  // MODE 1/2 scratch
   const float* rs = resp + static_cast<long>(slot) * 8192;
   if constexpr (MODE == 2) {
-    // spectrum computed earlier by MODE 1: load it with the response product fused
-    for (int t = threadIdx.x; t < kEqFft; t += blockDim.x) buf[sidx(t)] = cscale(__ldg(sp + t), rscale * __ldg(rs + kRs * t));
+    // spectrum computed earlier by MODE 1: load it with the response product fused; loads
+    // are issued 8 at a time ahead of their smem stores.
+    constexpr int PER = kEqFft / kNt;
+    static_assert(PER % 8 == 0, "eq_conv: spectrum load chunking");
+#pragma unroll
+    for (int q0 = 0; q0 < PER; q0 += 8) {
+      float2 v[8];
+      float r[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int t = threadIdx.x + (q0 + q) * kNt;
+        v[q] = __ldg(sp + t);
+        r[q] = __ldg(rs + kRs * t);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) buf[sidx(threadIdx.x + (q0 + q) * kNt)] = cscale(v[q], rscale * r[q]);
+    }
     __syncthreads();
   } else {
-  for (int t4 = threadIdx.x; t4 < kEqFft / 4; t4 += blockDim.x) {
-    const long pos = s0 + 4 * t4;
-    float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
-    if (vec && pos >= 0 && pos + 4 <= a.length) {
-      for (int e = e0; e < e1; ++e) {
-        const float* p = a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff + pos;
-        l = f4add(l, __ldg(reinterpret_cast<const float4*>(p)));
-        r = f4add(r, __ldg(reinterpret_cast<const float4*>(p + a.length)));
-      }
-    } else {
-      float lv[4] = {0.f, 0.f, 0.f, 0.f}, rv[4] = {0.f, 0.f, 0.f, 0.f};
+  // Gather-sum of the window, edges outermost so every float4 group of this thread is in
+  // flight at once; per element the sum runs in edge order (as the reference's gather).
+  constexpr int G = kEqFft / 4 / kNt;  // float4 groups per thread
+  static_assert(G * 4 * kNt == kEqFft, "eq_conv: threads must tile the window");
+  float4 lg[G], rg[G];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (pos + u >= 0 && pos + u < a.length) {
-          const float2 v = gather2(a, e0, e1, b, pos + u);
-          lv[u] = v.x;
-          rv[u] = v.y;
+  for (int g = 0; g < G; ++g) lg[g] = rg[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int e = e0; e < e1; ++e) {
+    const float* p = a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const long pos = s0 + 4 * (threadIdx.x + g * kNt);
+      if (vec && pos >= 0 && pos + 4 <= a.length) {
+        lg[g] = f4add(lg[g], __ldg(reinterpret_cast<const float4*>(p + pos)));
+        rg[g] = f4add(rg[g], __ldg(reinterpret_cast<const float4*>(p + a.length + pos)));
+      } else {
+        float lv[4] = {lg[g].x, lg[g].y, lg[g].z, lg[g].w}, rv[4] = {rg[g].x, rg[g].y, rg[g].z, rg[g].w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (pos + u >= 0 && pos + u < a.length) {
+            lv[u] += __ldg(p + pos + u);
+            rv[u] += __ldg(p + a.length + pos + u);
+          }
         }
+        lg[g] = make_float4(lv[0], lv[1], lv[2], lv[3]);
+        rg[g] = make_float4(rv[0], rv[1], rv[2], rv[3]);
       }
-      l = make_float4(lv[0], lv[1], lv[2], lv[3]);
-      r = make_float4(rv[0], rv[1], rv[2], rv[3]);
     }
-    buf[sidx(4 * t4)] = make_float2(l.x, r.x);
-    buf[sidx(4 * t4 + 1)] = make_float2(l.y, r.y);
-    buf[sidx(4 * t4 + 2)] = make_float2(l.z, r.z);
-    buf[sidx(4 * t4 + 3)] = make_float2(l.w, r.w);
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int t4 = threadIdx.x + g * kNt;
+    buf[sidx(4 * t4)] = make_float2(lg[g].x, rg[g].x);
+    buf[sidx(4 * t4 + 1)] = make_float2(lg[g].y, rg[g].y);
+    buf[sidx(4 * t4 + 2)] = make_float2(lg[g].z, rg[g].z);
+    buf[sidx(4 * t4 + 3)] = make_float2(lg[g].w, rg[g].w);
   }
   __syncthreads();
   fft_pow2<LOG, 1, kNt, -1>(buf, padded(kEqFft), a.tw);

@@ -37,13 +37,40 @@ inline std::size_t ir_bytes(int slots, long taps) {
   return align256(sizeof(float2) * static_cast<std::size_t>(slots) * taps + sizeof(float) * 40 * 40 * slots);
 }
 
-enum class ColSrc { Kernel, Signal };
+// Multitap delay tap records (delay_taps): 2 channels x 20 taps, each [position as float
+// bits, 39 FIR coefficients].
+constexpr int kTaps = 40;       // 2 channels x 20
+constexpr int kTapStride = 22;  // parameter row: per tap [re, im, 20 log-mags]
+constexpr int kFir = 39;
+constexpr int kFirHalf = 19;
+constexpr int kTapRec = 40;
+
+// Dense multitap kernel value at sample i of channel c (processors.cpp:210-227): the FIR
+// taps of the windows whose clamped position lies within +-19 of i, summed in tap order.
+// Positions are clamped into [m w, (m+1) w) with w > 2*19, so only windows i/w - 1 .. i/w + 1
+// can reach i.
+__device__ __forceinline__ float delay_tap_sum(const float* rec, int c, long i, int window) {
+  const int m = static_cast<int>(i / window);
+  const int m0 = m > 0 ? m - 1 : 0, m1 = m < 19 ? m + 1 : 19;
+  float acc = 0.f;
+  for (int mm = m0; mm <= m1; ++mm) {
+    const float* r = rec + (c * 20 + mm) * kTapRec;
+    const int d = __float_as_int(r[0]);
+    const long j = i - d + kFirHalf;
+    if (d >= 0 && j >= 0 && j < kFir) acc += r[1 + j];
+  }
+  return acc;
+}
+
+// Column-pass input: the packed kernel from an IR buffer, the arena signal (gathered), or
+// the multitap delay kernel synthesised from its tap records (no dense IR in memory).
+enum class ColSrc { Kernel, Signal, DelayTaps };
 
 // ---- pass 1: column FFTs (forward) ------------------------------------------------------
 // grid (N2 / C, items); item = slot (kernel) or slot*B + b (signal).
 template <int LN1, ColSrc SRC>
 __global__ void __launch_bounds__(kColThreads, 2) cols_fwd(StepArgs a, const float2* ir, long taps, int log_n,
-                                                        float2* out) {
+                                                        float2* out, int window) {
   constexpr int N1 = 1 << LN1;
   constexpr int C = kColElems / N1;
   constexpr int FS = padded(N1) + 1;
@@ -62,6 +89,12 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_fwd(StepArgs a, const flo
     e1 = __ldg(a.row_ptr + slot + 1);
     len = a.length;
   }
+  __shared__ float rec[SRC == ColSrc::DelayTaps ? kTaps * kTapRec : 1];
+  if constexpr (SRC == ColSrc::DelayTaps) {
+    const float* in = reinterpret_cast<const float*>(ir) + static_cast<long>(item) * kTaps * kTapRec;
+    for (int q = threadIdx.x; q < kTaps * kTapRec; q += kColThreads) rec[q] = __ldg(in + q);
+    __syncthreads();
+  }
   // Stage all of this thread's loads in registers before any smem store (max loads in flight).
   constexpr int EPT = kColElems / kColThreads;
   float2 vals[EPT];
@@ -78,6 +111,8 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_fwd(StepArgs a, const flo
     if (n < len) {
       if constexpr (SRC == ColSrc::Signal) {
         v = one ? make_float2(__ldg(one + n), __ldg(one + a.length + n)) : gather2(a, e0, e1, b, n);
+      } else if constexpr (SRC == ColSrc::DelayTaps) {
+        v = make_float2(delay_tap_sum(rec, 0, n, window), delay_tap_sum(rec, 1, n, window));
       } else {
         v = __ldg(ir + static_cast<long>(item) * taps + n);
       }
@@ -282,7 +317,7 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2,
 // ---- dispatch -----------------------------------------------------------------------------
 template <int LN1>
 void cols_fwd_t(ColSrc src, const StepArgs& a, const float2* ir, long taps, const ConvGeom& g, int items,
-                float2* out, cudaStream_t s) {
+                float2* out, int window, cudaStream_t s) {
   constexpr int C = kColElems / (1 << LN1);
   constexpr int smem = C * (padded(1 << LN1) + 1) * 8;
   const dim3 grid(static_cast<unsigned>((1L << g.log_n2) / C), static_cast<unsigned>(items));
@@ -291,14 +326,19 @@ void cols_fwd_t(ColSrc src, const StepArgs& a, const float2* ir, long taps, cons
     cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::Kernel>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::Signal>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::Kernel>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::DelayTaps>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::DelayTaps>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     return true;
   }();
   (void)done;
   if (src == ColSrc::Signal) {
-    cols_fwd<LN1, ColSrc::Signal><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out);
+    cols_fwd<LN1, ColSrc::Signal><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out, window);
+  } else if (src == ColSrc::DelayTaps) {
+    note_prologue_kernel(reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::DelayTaps>));
+    cols_fwd<LN1, ColSrc::DelayTaps><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out, window);
   } else {
     note_prologue_kernel(reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::Kernel>));
-    cols_fwd<LN1, ColSrc::Kernel><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out);
+    cols_fwd<LN1, ColSrc::Kernel><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out, window);
   }
 }
 
@@ -349,8 +389,9 @@ void rows_conv_t(const ConvGeom& g, int items, int batch, float2* X, const float
   }
 
 // Kernel spectrum P (four-step order) of the packed kernels in `ir` ([slots][taps]).
-void kernel_spectrum(const StepArgs& a, const ConvGeom& g, const float2* ir, long taps, float2* P, cudaStream_t s) {
-  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Kernel, a, ir, taps, g, a.slots, P, s);
+void kernel_spectrum(ColSrc src, const StepArgs& a, const ConvGeom& g, const float2* ir, long taps, int window,
+                     float2* P, cudaStream_t s) {
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, src, a, ir, taps, g, a.slots, P, window, s);
   MGB_DISPATCH_LN(g.log_n2, rows_spec_t, g, a.slots, P, a.tw, s);
 }
 
@@ -431,29 +472,30 @@ __global__ void __launch_bounds__(kRevThreads, 2) reverb_ir(const double* params
 }
 
 // ---- multitap delay kernel -------------------------------------------------------------------
-constexpr int kTaps = 40;       // 2 channels x 20
-constexpr int kTapStride = 22;  // [re, im, 20 log-mags]
-constexpr int kFir = 39;
-constexpr int kFirHalf = 19;
-constexpr int kTapRec = 40;     // per tap: [position as float bits, 39 coefficients]
 
-// Per slot: fp64 tap positions (processors.cpp:189-208: disabled taps, angle -> grid delay,
-// window clamp) and the 39-tap zero-phase FIRs (dsp.cpp:106-136 as the exact cosine sum).
-// Output taps[slot][tap][kTapRec]. grid (slots) x 1024.
-__global__ void __launch_bounds__(1024) delay_taps(const double* params, DelayConst dc, float* taps) {
-  __shared__ double mag[kTaps][20];
+// Per tap record: fp64 position (processors.cpp:189-208: disabled taps, angle -> grid
+// delay, window clamp) and the 39-tap zero-phase FIR (dsp.cpp:106-136 as the exact cosine
+// sum). Output taps[slot][tap][kTapRec]. grid (kTaps, slots) x 64: one CTA per tap, one
+// thread per coefficient.
+__global__ void __launch_bounds__(64) delay_taps(const double* params, DelayConst dc, float* taps) {
+  __shared__ double mag[20];
   __shared__ double cos39[kFir];
-  const int slot = blockIdx.x;
-  const double* row = params + static_cast<long>(slot) * kTaps * kTapStride;
-  float* out = taps + static_cast<long>(slot) * kTaps * kTapRec;
+  const int tapi = blockIdx.x, slot = blockIdx.y;
+  const double* tap = params + static_cast<long>(slot) * kTaps * kTapStride + tapi * kTapStride;
+  float* out = taps + (static_cast<long>(slot) * kTaps + tapi) * kTapRec;
   const int t = threadIdx.x;
-  if (t < kTaps) {
-    const double* tap = row + t * kTapStride;
+  if (t < 20) mag[t] = exp(tap[2 + t]);
+  if (t < kFir) {
+    double sk, ck;
+    sincospi(2.0 * t / kFir, &sk, &ck);
+    cos39[t] = ck;
+  }
+  if (t == 63) {  // second warp (lanes >= 39 idle in the FIR): the position
     double mx = tap[2];
     for (int k = 1; k < 20; ++k) mx = fmax(mx, tap[2 + k]);
     int d = -1;
     if (!(mx <= -60.0)) {
-      const int m = t % 20;
+      const int m = tapi % 20;
       const double frac = -atan2(tap[1], tap[0]) / (2.0 * 3.14159265358979323846);
       long long dd = llround(frac * static_cast<double>(dc.span));
       dd %= dc.span;
@@ -462,29 +504,22 @@ __global__ void __launch_bounds__(1024) delay_taps(const double* params, DelayCo
       const long long hi = min(static_cast<long long>(m + 1) * dc.window, static_cast<long long>(dc.span)) - 1;
       d = static_cast<int>(dd < lo ? lo : (dd > hi ? hi : dd));
     }
-    out[t * kTapRec] = __int_as_float(d);
-  }
-  if (t < kTaps * 20) mag[t / 20][t % 20] = exp(row[(t / 20) * kTapStride + 2 + t % 20]);
-  if (t < kFir) {
-    double s, c;
-    sincospi(2.0 * t / kFir, &s, &c);
-    cos39[t] = c;
+    out[0] = __int_as_float(d);
   }
   __syncthreads();
-  for (int q = t; q < kTaps * kFir; q += blockDim.x) {
-    const int tap = q / kFir, n = q % kFir;
-    const int j = n >= kFirHalf ? n - kFirHalf : kFirHalf - n;
-    double acc = 0.0;
-    int idx = 0;
-    for (int k = 0; k < kFir; ++k) {
-      acc = fma(mag[tap][k <= kFirHalf ? k : kFir - k], cos39[idx], acc);
-      idx += j;
-      if (idx >= kFir) idx -= kFir;
-    }
-    double s, c;
-    sincospi(2.0 * n / (kFir - 1), &s, &c);
-    out[tap * kTapRec + 1 + n] = static_cast<float>((0.5 - 0.5 * c) * acc / kFir);
+  if (t >= kFir) return;
+  const int n = t;
+  const int j = n >= kFirHalf ? n - kFirHalf : kFirHalf - n;
+  double acc = 0.0;
+  int idx = 0;
+  for (int k = 0; k < kFir; ++k) {
+    acc = fma(mag[k <= kFirHalf ? k : kFir - k], cos39[idx], acc);
+    idx += j;
+    if (idx >= kFir) idx -= kFir;
   }
+  double s, c;
+  sincospi(2.0 * n / (kFir - 1), &s, &c);
+  out[1 + n] = static_cast<float>((0.5 - 0.5 * c) * acc / kFir);
 }
 
 // Dense multitap kernel (processors.cpp:210-227): every sample i of [0, span) sums, in tap
@@ -604,7 +639,7 @@ void launch_delay_ir(const double* params, int slots, const DelayConst& dc, floa
   auto* taps = reinterpret_cast<float*>(ir + static_cast<long>(slots) * ir_stride);
   note_prologue_kernel(reinterpret_cast<const void*>(delay_taps));
   note_prologue_kernel(reinterpret_cast<const void*>(delay_dense));
-  delay_taps<<<slots, 1024, 0, s>>>(params, dc, taps);
+  delay_taps<<<dim3(kTaps, slots), 64, 0, s>>>(params, dc, taps);
   const dim3 grid(static_cast<unsigned>((dc.span + 255) / 256), 2, static_cast<unsigned>(slots));
   delay_dense<<<grid, 256, 0, s>>>(taps, dc, ir, ir_stride);
 }
@@ -616,9 +651,16 @@ void launch_conv_prologue(bool reverb, const StepArgs& a, const ReverbConst& rc,
   const ConvGeom g = conv_geom(a.length, taps);
   auto* ir = static_cast<float2*>(ws);
   auto* P = reinterpret_cast<float2*>(static_cast<char*>(ws) + ir_bytes(a.slots, taps));
-  if (reverb) launch_reverb_ir(a.params, a.slots, rc, ir, taps, s);
-  else launch_delay_ir(a.params, a.slots, dc, ir, taps, s);
-  kernel_spectrum(a, g, ir, taps, P, s);
+  if (reverb) {
+    launch_reverb_ir(a.params, a.slots, rc, ir, taps, s);
+    kernel_spectrum(ColSrc::Kernel, a, g, ir, taps, 0, P, s);
+  } else {
+    // Tap records only; the column pass synthesises the dense kernel on the fly.
+    auto* rec = reinterpret_cast<float*>(ir + static_cast<long>(a.slots) * taps);
+    note_prologue_kernel(reinterpret_cast<const void*>(delay_taps));
+    delay_taps<<<dim3(kTaps, a.slots), 64, 0, s>>>(a.params, dc, rec);
+    kernel_spectrum(ColSrc::DelayTaps, a, g, reinterpret_cast<const float2*>(rec), taps, dc.window, P, s);
+  }
 }
 
 void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, void* ws, cudaStream_t s) {
@@ -626,7 +668,7 @@ void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, voi
   const ConvGeom g = conv_geom(a.length, taps);
   const auto* P = reinterpret_cast<const float2*>(static_cast<const char*>(prologue_ws) + ir_bytes(a.slots, taps));
   auto* X = static_cast<float2*>(ws);
-  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, a, nullptr, 0, g, a.slots * a.batch, X, s);
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, a, nullptr, 0, g, a.slots * a.batch, X, 0, s);
   MGB_DISPATCH_LN(g.log_n2, rows_conv_t, g, a.slots * a.batch, a.batch, X, P, a.tw, s);
   MGB_DISPATCH_LN(g.log_n1, cols_inv_t, a, g, X, s);
 }
