@@ -290,17 +290,17 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
 
 }  // namespace
 
-std::size_t dyn_workspace_bytes(int slots, int batch, long length) {
+std::size_t dyn_sync_bytes(int slots, int batch, long length) {
   const long tiles = (length + kDynTile - 1) / kDynTile;
   return 256 + sizeof(unsigned long long) * static_cast<std::size_t>(slots) * batch * tiles;
 }
 
 void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double energy_floor, void* ws,
-                     cudaStream_t s) {
+                     bool zero_sync, cudaStream_t s) {
   if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
   const int tiles = static_cast<int>((a.length + kDynTile - 1) / kDynTile);
   const long total = static_cast<long>(a.slots) * a.batch * tiles;
-  cudaMemsetAsync(ws, 0, dyn_workspace_bytes(a.slots, a.batch, a.length), s);
+  if (zero_sync) cudaMemsetAsync(ws, 0, dyn_sync_bytes(a.slots, a.batch, a.length), s);
   auto* ticket = static_cast<unsigned int*>(ws);
   auto* status = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 256);
   const long ne = envelope_taps < a.length ? envelope_taps : a.length;

@@ -192,11 +192,19 @@ std::size_t prologue_bytes(NodeType t, int slots, long length, const ProcessorSe
   }
 }
 
+// Per-render synchronisation words (scan tickets and tile status): zero at the
+// start of every step run. render_arena clears all steps' words with one memset.
+std::size_t sync_bytes(NodeType t, int slots, int batch, long length) {
+  switch (t) {
+    case NodeType::Compressor:
+    case NodeType::Noisegate: return mgb::dyn_sync_bytes(slots, batch, length);
+    default: return 0;
+  }
+}
+
 std::size_t main_bytes(NodeType t, int slots, int batch, long length, const ProcessorSet& p) {
   switch (t) {
     case NodeType::Eq: return mgb::eq_spectrum_bytes(slots, batch, length);
-    case NodeType::Compressor:
-    case NodeType::Noisegate: return mgb::dyn_workspace_bytes(slots, batch, length);
     case NodeType::Reverb: return mgb::conv_main_bytes(mgb::conv_geom(length, p.reverb_length()), slots, batch);
     case NodeType::Delay: return mgb::conv_main_bytes(mgb::conv_geom(length, p.delay_span()), slots, batch);
     default: return 0;
@@ -229,7 +237,8 @@ void run_prologue(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, voi
 }
 
 // One step's audio pass. a.params points at the step's first parameter row.
-void run_main(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, void* pws, void* mws, cudaStream_t s) {
+void run_main(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, void* pws, void* mws, void* sws, bool zero_sync,
+              cudaStream_t s) {
   switch (t) {
     case NodeType::In:
     case NodeType::Out:
@@ -241,7 +250,8 @@ void run_main(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, void* p
       break;
     case NodeType::Compressor:
     case NodeType::Noisegate:
-      mgb::launch_dynamics(t == NodeType::Noisegate, a, p.config().envelope_taps, p.config().energy_floor, mws, s);
+      mgb::launch_dynamics(t == NodeType::Noisegate, a, p.config().envelope_taps, p.config().energy_floor, sws, zero_sync,
+                           s);
       break;
     case NodeType::Reverb: mgb::launch_conv_main(a, p.reverb_length(), pws, mws, s); break;
     case NodeType::Delay: mgb::launch_conv_main(a, p.delay_span(), pws, mws, s); break;
@@ -272,13 +282,15 @@ int chain_length(const RenderData& rd, std::size_t k, int batch, long length) {
 }
 
 std::size_t step_ws_bytes(NodeType t, int slots, int batch, long length, const ProcessorSet& p) {
-  return align256(prologue_bytes(t, slots, length, p)) + main_bytes(t, slots, batch, length, p);
+  return align256(prologue_bytes(t, slots, length, p)) + align256(sync_bytes(t, slots, batch, length)) +
+         main_bytes(t, slots, batch, length, p);
 }
 
 void run_step(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, void* ws, cudaStream_t s) {
   const std::size_t pb = align256(prologue_bytes(t, a.slots, a.length, p));
+  const std::size_t sb = align256(sync_bytes(t, a.slots, a.batch, a.length));
   run_prologue(t, a, p, ws, s);
-  run_main(t, a, p, ws, static_cast<char*>(ws) + pb, s);
+  run_main(t, a, p, ws, static_cast<char*>(ws) + pb + sb, static_cast<char*>(ws) + pb, true, s);
 }
 
 }  // namespace
@@ -339,6 +351,12 @@ DevicePlan::Layout DevicePlan::layout(int batch, long length, const ProcessorSet
     off += align256(prologue_bytes(st.type, slots, length, procs));
     main = std::max(main, main_bytes(st.type, slots, batch, length, procs));
   }
+  l.sync_begin = off;
+  for (const StepIndex& st : rd_.steps) {
+    l.sync_off.push_back(off);
+    off += align256(sync_bytes(st.type, st.store_end - st.store_begin, batch, length));
+  }
+  l.sync_bytes = off - l.sync_begin;
   l.main_off = off;
   l.total = off + align256(main);
   return l;
@@ -418,6 +436,9 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
       cuda_check(cudaEventRecord(ev[k + 1], a), "event");
     }
   }
+  // Every step's synchronisation words, cleared once (one memset node instead of one per
+  // scan step on the critical path).
+  if (lay.sync_bytes) cuda_check(cudaMemsetAsync(ws + lay.sync_begin, 0, lay.sync_bytes, stream), "memset sync");
   for (std::size_t k = 0; k < rd.steps.size(); ++k) {
     const NodeType t = rd.steps[k].type;
     // Runs of small pointwise steps (latency-bound) go out as one launch, unless per-step
@@ -447,7 +468,7 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
       mgb::launch_eq_inverse(args[k], reinterpret_cast<float*>(pws + eq_taps_bytes(args[k].slots)),
                              reinterpret_cast<float2*>(mws), stream);
     } else {
-      run_main(t, args[k], procs, pws, mws, stream);
+      run_main(t, args[k], procs, pws, mws, ws + lay.sync_off[k], false, stream);
     }
     if (step_events) cuda_check(cudaEventRecord(step_events[2 * k + 1], stream), "event");
   }
@@ -490,7 +511,7 @@ void profile_steps(const DevicePlan& plan, const ProcessorSet& procs, const doub
     cuda_check(cudaEventRecord(e0, stream), "event");
     for (int r = 0; r < reps; ++r) {
       run_prologue(st.type, a, procs, ws + lay.prologue_off[k], stream);
-      run_main(st.type, a, procs, ws + lay.prologue_off[k], ws + lay.main_off, stream);
+      run_main(st.type, a, procs, ws + lay.prologue_off[k], ws + lay.main_off, ws + lay.sync_off[k], true, stream);
     }
     cuda_check(cudaEventRecord(e1, stream), "event");
     cuda_check(cudaEventSynchronize(e1), "sync");

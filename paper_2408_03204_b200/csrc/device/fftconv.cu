@@ -246,6 +246,19 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2,
   const float2* pa = P + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
   const float2* pb = P + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
   constexpr int RS = padded(N2);  // second row's offset
+  // The kernel spectrum values this thread pairs are issued first, so their latency hides
+  // behind the row loads and the forward FFT.
+  constexpr int KPT = (N2 + NT - 1) / NT;
+  float2 pkv[KPT], pov[KPT];
+#pragma unroll
+  for (int q = 0; q < KPT; ++q) {
+    const int k = threadIdx.x + q * NT;
+    if (k < N2) {
+      const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
+      pkv[q] = __ldg(pa + k);
+      pov[q] = __ldg(pb + kb);
+    }
+  }
   {
     constexpr int PER = N2 / NT;
     static_assert(PER * NT == N2, "rows_conv: threads must tile a row");
@@ -262,19 +275,6 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2,
     }
   }
   __syncthreads();
-  // The kernel spectrum values this thread pairs are fetched before the forward FFT so
-  // their latency hides behind it.
-  constexpr int KPT = (N2 + NT - 1) / NT;
-  float2 pkv[KPT], pov[KPT];
-#pragma unroll
-  for (int q = 0; q < KPT; ++q) {
-    const int k = threadIdx.x + q * NT;
-    if (k < N2) {
-      const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
-      pkv[q] = __ldg(pa + k);
-      pov[q] = __ldg(pb + kb);
-    }
-  }
   fft_pow2<LN2, 2, NT, -1>(rows, RS, tw);
   const float s = 0.25f / static_cast<float>(N);
 #pragma unroll
@@ -321,7 +321,7 @@ void cols_fwd_t(ColSrc src, const StepArgs& a, const float2* ir, long taps, cons
   constexpr int C = kColElems / (1 << LN1);
   constexpr int smem = C * (padded(1 << LN1) + 1) * 8;
   const dim3 grid(static_cast<unsigned>((1L << g.log_n2) / C), static_cast<unsigned>(items));
-  static const bool done = [] {
+  static const bool attrs_set = [] {
     cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::Signal>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::Kernel>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::Signal>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -330,7 +330,7 @@ void cols_fwd_t(ColSrc src, const StepArgs& a, const float2* ir, long taps, cons
     cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::DelayTaps>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     return true;
   }();
-  (void)done;
+  (void)attrs_set;
   if (src == ColSrc::Signal) {
     cols_fwd<LN1, ColSrc::Signal><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out, window);
   } else if (src == ColSrc::DelayTaps) {
@@ -619,6 +619,7 @@ std::size_t conv_main_bytes(const ConvGeom& g, int slots, int batch) {
   return align256(sizeof(float2) * static_cast<std::size_t>(slots) * batch * g.n);
 }
 
+
 void launch_reverb_ir(const double* params, int slots, const ReverbConst& rc, float2* ir, long ir_stride,
                       cudaStream_t s) {
   if (slots == 0) return;
@@ -668,8 +669,9 @@ void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, voi
   const ConvGeom g = conv_geom(a.length, taps);
   const auto* P = reinterpret_cast<const float2*>(static_cast<const char*>(prologue_ws) + ir_bytes(a.slots, taps));
   auto* X = static_cast<float2*>(ws);
-  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, a, nullptr, 0, g, a.slots * a.batch, X, 0, s);
-  MGB_DISPATCH_LN(g.log_n2, rows_conv_t, g, a.slots * a.batch, a.batch, X, P, a.tw, s);
+  const int items = a.slots * a.batch;
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, a, nullptr, 0, g, items, X, 0, s);
+  MGB_DISPATCH_LN(g.log_n2, rows_conv_t, g, items, a.batch, X, P, a.tw, s);
   MGB_DISPATCH_LN(g.log_n1, cols_inv_t, a, g, X, s);
 }
 

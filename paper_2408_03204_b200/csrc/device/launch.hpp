@@ -44,9 +44,12 @@ void launch_eq_inverse(const StepArgs& a, const float* resp_ws, const float2* sp
 constexpr int kDynThreads = 512;
 constexpr int kDynPerThread = 8;
 constexpr int kDynTile = kDynThreads * kDynPerThread;
-std::size_t dyn_workspace_bytes(int slots, int batch, long length);
-void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double energy_floor, void* ws,
-                     cudaStream_t s);
+// `sync` (dyn_sync_bytes: tile ticket + per-tile status words) must be zero on entry; with
+// zero_sync the launcher clears it itself, otherwise the caller did (render_arena clears
+// every step's sync words with one memset per render).
+std::size_t dyn_sync_bytes(int slots, int batch, long length);
+void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double energy_floor, void* sync,
+                     bool zero_sync, cudaStream_t s);
 
 // FFT convolution with a long causal kernel (reverb, delay): four-step FFT of size N.
 struct ConvGeom {

@@ -134,10 +134,12 @@ class DevicePlan {
   std::size_t workspace_bytes(int batch, long length, const ProcessorSet& procs) const;
   int kernels_per_render(int batch, long length) const;
 
-  // Workspace: one persistent region per step for its parameter-only prologue, then one
-  // transient region shared by every step's audio pass.
+  // Workspace: one persistent region per step for its parameter-only prologue, the steps'
+  // synchronisation words, then one transient region shared by every step's audio pass.
   struct Layout {
     std::vector<std::size_t> prologue_off;
+    std::vector<std::size_t> sync_off;  // per step: scan tickets / pass counters (zeroed per render)
+    std::size_t sync_begin = 0, sync_bytes = 0;
     std::size_t main_off = 0;
     std::size_t total = 0;
   };
