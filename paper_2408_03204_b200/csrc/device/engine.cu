@@ -678,8 +678,20 @@ void RenderPipeline::submit(const ParamStore& params, const void* const* sources
   }
   const std::size_t bytes = (f32_ ? sizeof(float) : sizeof(double)) * static_cast<std::size_t>(stride_);
   char* dst = f32_ ? reinterpret_cast<char*>(arena) : static_cast<char*>(s.staging.ptr);
-  for (int k = 0; k < rd.num_inputs; ++k) {
-    cuda_check(cudaMemcpyAsync(dst + bytes * k, sources[k], bytes, cudaMemcpyHostToDevice, h2d_), "H2D sources");
+  // Sources laid out back to back in host memory (one [K][B][2][L] array, the usual case)
+  // go over PCIe as one transfer instead of K.
+  auto contiguous = [&](const void* const* ptrs, int n) {
+    for (int k = 1; k < n; ++k) {
+      if (static_cast<const char*>(ptrs[k]) != static_cast<const char*>(ptrs[0]) + bytes * k) return false;
+    }
+    return n > 0;
+  };
+  if (contiguous(sources, rd.num_inputs)) {
+    cuda_check(cudaMemcpyAsync(dst, sources[0], bytes * rd.num_inputs, cudaMemcpyHostToDevice, h2d_), "H2D sources");
+  } else {
+    for (int k = 0; k < rd.num_inputs; ++k) {
+      cuda_check(cudaMemcpyAsync(dst + bytes * k, sources[k], bytes, cudaMemcpyHostToDevice, h2d_), "H2D sources");
+    }
   }
   cuda_check(cudaEventRecord(s.h2d, h2d_), "event");
   // Compute: after the inputs landed and the slot's previous outputs were read back.
@@ -693,8 +705,13 @@ void RenderPipeline::submit(const ParamStore& params, const void* const* sources
   // Outputs.
   cuda_check(cudaStreamWaitEvent(d2h_, s.done, 0), "wait");
   const char* src = f32_ ? reinterpret_cast<const char*>(arena + rd.output_begin * stride_) : static_cast<const char*>(s.staging.ptr);
-  for (int o = 0; o < rd.buffer_rows - rd.output_begin; ++o) {
-    cuda_check(cudaMemcpyAsync(outputs[o], src + bytes * o, bytes, cudaMemcpyDeviceToHost, d2h_), "D2H outputs");
+  const int n_outs = rd.buffer_rows - rd.output_begin;
+  if (contiguous(outputs, n_outs)) {
+    cuda_check(cudaMemcpyAsync(outputs[0], src, bytes * n_outs, cudaMemcpyDeviceToHost, d2h_), "D2H outputs");
+  } else {
+    for (int o = 0; o < n_outs; ++o) {
+      cuda_check(cudaMemcpyAsync(outputs[o], src + bytes * o, bytes, cudaMemcpyDeviceToHost, d2h_), "D2H outputs");
+    }
   }
   cuda_check(cudaEventRecord(s.d2h, d2h_), "event");
 }
