@@ -422,6 +422,35 @@ def compute_render_data(fg: FlatGraph, strategy: int = Strategy.GREEDY, beam_wid
     return RenderData(h, fg)
 
 
+class _ArrayGraph:
+    """Minimal FlatGraph stand-in over (types, edges) int32 arrays (no Python node lists)."""
+
+    def __init__(self, types: np.ndarray, edges: np.ndarray):
+        self._t = np.ascontiguousarray(types, dtype=np.int32)
+        self._e = np.ascontiguousarray(np.asarray(edges, dtype=np.int32).reshape(-1, 4))
+        self.params: Dict[NodeType, np.ndarray] = {}
+        self.num_inputs = int(np.count_nonzero(self._t == int(NodeType.IN)))
+        self.num_outputs = int(np.count_nonzero(self._t == int(NodeType.OUT)))
+
+    def num_nodes(self) -> int:
+        return len(self._t)
+
+    def arrays(self) -> Tuple[np.ndarray, np.ndarray]:
+        return self._t, self._e
+
+
+def compute_render_data_arrays(types: np.ndarray, edges: np.ndarray, strategy: int = Strategy.GREEDY,
+                               beam_width: int = 32, optimal_node_cap: int = 256) -> RenderData:
+    """compute_render_data straight from int32 arrays (types [V], edges [E, 4]) — the fast
+    path for large unions whose topology changes every batch (no Python graph objects)."""
+    ag = _ArrayGraph(types, edges)
+    t, e = ag.arrays()
+    h = _vp()
+    _check(_lib.mg_plan_create(_ptr(t), len(t), _ptr(e), len(e), int(strategy), int(beam_width),
+                               int(optimal_node_cap), ctypes.byref(h)))
+    return RenderData(h, ag)
+
+
 def make_schedule(fg: FlatGraph, strategy: int = Strategy.GREEDY, beam_width: int = 32,
                   optimal_node_cap: int = 256) -> Schedule:
     """`schedule.cpp:325-338` (returned from the full plan build)."""
@@ -545,14 +574,19 @@ def render(rd: RenderData, procs: ProcessorSet, params: Optional[Dict[int, np.nd
 
 # ---- workload generators (bit-identical to the reference's) ------------------------------------
 
-def generate_console(tracks: int, prune: float = 0.0, seed: int = 0) -> Graph:
-    """`console.cpp:10-44`."""
+def generate_console_arrays(tracks: int, prune: float = 0.0, seed: int = 0) -> Tuple[np.ndarray, np.ndarray]:
+    """`console.cpp:10-44` as (types [V], edges [E, 4]) int32 arrays."""
     cap_n, cap_e = 8 * tracks + 16, 10 * tracks + 16
     t = np.zeros(cap_n, dtype=np.int32)
     e = np.zeros((cap_e, 4), dtype=np.int32)
     nn, ne = _i32(), _i32()
     _check(_lib.mg_generate_console(tracks, prune, seed, _ptr(t), cap_n, _ptr(e), cap_e, ctypes.byref(nn), ctypes.byref(ne)))
-    return Graph.from_arrays(t[:nn.value], e[:ne.value])
+    return t[:nn.value].copy(), e[:ne.value].copy()
+
+
+def generate_console(tracks: int, prune: float = 0.0, seed: int = 0) -> Graph:
+    """`console.cpp:10-44`."""
+    return Graph.from_arrays(*generate_console_arrays(tracks, prune, seed))
 
 
 def random_legal_params(node_types: Sequence[int], seed: int) -> Dict[NodeType, np.ndarray]:
@@ -581,7 +615,8 @@ from .device import DeviceRenderer, RenderPipeline  # noqa: E402  (torch-backed 
 
 __all__ = [
     "NodeType", "Strategy", "Graph", "FlatGraph", "RenderData", "StepIndex", "Schedule", "ProcessorSet",
-    "DeviceRenderer", "RenderPipeline", "to_flat", "disjoint_union", "default_params", "default_param_row", "concat_params",
+    "DeviceRenderer", "RenderPipeline", "to_flat", "disjoint_union", "compute_render_data_arrays",
+    "generate_console_arrays", "default_params", "default_param_row", "concat_params",
     "compute_render_data", "make_schedule", "validate_schedule", "render", "param_width", "type_code", "type_name",
     "generate_console", "random_legal_params", "uniform_noise", "compressor_gain_log", "noisegate_gain_log",
     "check_param_row", "LIB_PATH",

@@ -20,17 +20,33 @@ from . import NUM_NODE_TYPES, ProcessorSet, RenderData, _check, _lib, _u64, _vp,
 
 class DeviceRenderer:
     def __init__(self, rd: RenderData, procs: ProcessorSet, batch: int, length: int,
-                 params: Optional[Dict[int, np.ndarray]] = None, device: Optional[torch.device] = None):
+                 params: Optional[Dict[int, np.ndarray]] = None, device: Optional[torch.device] = None,
+                 arena_pool: Optional[torch.Tensor] = None, workspace_pool: Optional[torch.Tensor] = None):
+        """`arena_pool` (fp32) / `workspace_pool` (uint8): optional preallocated device buffers
+        at least as large as this plan needs, reused across plans whose topology changes every
+        step (no per-plan allocation). The arena view is NOT zeroed in that case."""
         if not torch.cuda.is_available():
             raise RuntimeError("DeviceRenderer needs a CUDA device (there is no CPU fallback)")
         self.rd, self.procs = rd, procs
         self.batch, self.length = int(batch), int(length)
         self.device = device or torch.device("cuda", procs.device)
-        self.arena = torch.zeros((rd.buffer_rows, self.batch, 2, self.length), dtype=torch.float32, device=self.device)
+        shape = (rd.buffer_rows, self.batch, 2, self.length)
+        if arena_pool is None:
+            self.arena = torch.zeros(shape, dtype=torch.float32, device=self.device)
+        else:
+            need = rd.buffer_rows * self.batch * 2 * self.length
+            if arena_pool.dtype != torch.float32 or arena_pool.numel() < need:
+                raise ValueError(f"DeviceRenderer: arena_pool must be float32 with >= {need} elements")
+            self.arena = arena_pool.reshape(-1)[:need].view(shape)
         ws = _u64()
         _check(_lib.mg_plan_workspace_bytes(rd.handle, procs.handle, self.batch, self.length, ctypes.byref(ws)))
         self.workspace_bytes = int(ws.value)
-        self.workspace = torch.empty(self.workspace_bytes, dtype=torch.uint8, device=self.device)
+        if workspace_pool is None:
+            self.workspace = torch.empty(self.workspace_bytes, dtype=torch.uint8, device=self.device)
+        else:
+            if workspace_pool.dtype != torch.uint8 or workspace_pool.numel() < self.workspace_bytes:
+                raise ValueError(f"DeviceRenderer: workspace_pool must be uint8 with >= {self.workspace_bytes} bytes")
+            self.workspace = workspace_pool.reshape(-1)[:self.workspace_bytes]
         self.tables: Dict[int, torch.Tensor] = {}
         self._ptrs = (_vp * NUM_NODE_TYPES)()
         self.set_params(rd.flat.params if params is None else params)
