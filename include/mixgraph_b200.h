@@ -127,6 +127,28 @@ int32_t mg_pipeline_submit(mg_pipeline* pipe, const double* const* tables, const
 int32_t mg_pipeline_sync(mg_pipeline* pipe);
 void mg_pipeline_destroy(mg_pipeline* pipe);
 
+/* Renders of plans whose topology changes every batch (BASELINE config 3), no per-plan
+ * allocation or synchronisation: device pools sized once from a capacity (cap[4] = arena
+ * rows, workspace bytes, step-table ints, parameter doubles; mg_batch_capacity gives one
+ * plan's needs, take the max over the plans to render), `depth` rotating slots. submit()
+ * takes parameter tables in ORIGINAL row order (reorder_params is done on the device,
+ * schedule.cpp:454-471; missing/misshaped tables fail like it), validates them when
+ * `validate` (processors.cpp:132-149), and sources fp32 [source_rows][B][2][L] (input k
+ * takes row k % source_rows; device or host memory); outputs: host fp32
+ * [num_outputs][B][2][L] or NULL. The plan must stay alive until its slot is reused
+ * (`depth` submits later) or mg_batch_sync. Replaces, per batch, compute_render_data's
+ * consumer loop in bench.cpp:52-57 with a re-drawn graph. */
+typedef struct mg_batch mg_batch;
+int32_t mg_batch_capacity(const mg_plan* plan, const mg_processors* procs, int32_t batch, int64_t length, uint64_t* cap);
+int32_t mg_batch_create(const mg_processors* procs, int32_t batch, int64_t length, const uint64_t* cap, int32_t depth,
+                        mg_batch** out);
+int32_t mg_batch_submit(mg_batch* b, const mg_plan* plan, const double* const* tables, const int32_t* rows,
+                        int32_t validate, const float* sources, int32_t source_rows, int32_t sources_on_device,
+                        float* outputs);
+int32_t mg_batch_sync(mg_batch* b);
+int32_t mg_batch_last_arena(const mg_batch* b, void** arena);
+void mg_batch_destroy(mg_batch* b);
+
 /* Per-step device time (ms; prologue + audio pass of step k) averaged over `reps`
  * back-to-back repetitions between one event pair, after one full render. Synchronous. */
 int32_t mg_profile_steps(const mg_plan* plan, const mg_processors* procs, const double* const* d_tables,

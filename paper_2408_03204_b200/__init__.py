@@ -79,6 +79,12 @@ _sig("mg_pipeline_create", _i32, _vp, _vp, _i32, _i64, _i32, _i32, _P(_vp))
 _sig("mg_pipeline_submit", _i32, _vp, _vp, _vp, _vp, _vp)
 _sig("mg_pipeline_sync", _i32, _vp)
 _sig("mg_pipeline_destroy", None, _vp)
+_sig("mg_batch_capacity", _i32, _vp, _vp, _i32, _i64, _vp)
+_sig("mg_batch_create", _i32, _vp, _i32, _i64, _vp, _i32, _P(_vp))
+_sig("mg_batch_submit", _i32, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp)
+_sig("mg_batch_sync", _i32, _vp)
+_sig("mg_batch_last_arena", _i32, _vp, _P(_vp))
+_sig("mg_batch_destroy", None, _vp)
 _sig("mg_process", _i32, _vp, _i32, _vp, _vp, _i32, _i32, _i64, _vp, _i32, _i32)
 _sig("mg_reverb_kernel", _i32, _vp, _vp, _vp, _vp)
 _sig("mg_delay_kernel", _i32, _vp, _vp, _i32, _vp, _vp)
@@ -611,11 +617,11 @@ def uniform_noise(n: int, seed: int) -> np.ndarray:
     return out
 
 
-from .device import DeviceRenderer, RenderPipeline  # noqa: E402  (torch-backed device path)
+from .device import BatchRenderer, DeviceRenderer, RenderPipeline  # noqa: E402  (torch-backed device path)
 
 __all__ = [
     "NodeType", "Strategy", "Graph", "FlatGraph", "RenderData", "StepIndex", "Schedule", "ProcessorSet",
-    "DeviceRenderer", "RenderPipeline", "to_flat", "disjoint_union", "compute_render_data_arrays",
+    "BatchRenderer", "DeviceRenderer", "RenderPipeline", "to_flat", "disjoint_union", "compute_render_data_arrays",
     "generate_console_arrays", "default_params", "default_param_row", "concat_params",
     "compute_render_data", "make_schedule", "validate_schedule", "render", "param_width", "type_code", "type_name",
     "generate_console", "random_legal_params", "uniform_noise", "compressor_gain_log", "noisegate_gain_log",

@@ -40,6 +40,10 @@ struct mg_pipeline {
   const mg_plan* plan;
 };
 
+struct mg_batch {
+  std::unique_ptr<BatchRenderer> b;
+};
+
 struct mg_processors {
   std::unique_ptr<ProcessorSet> ps;
 };
@@ -407,6 +411,47 @@ int32_t mg_pipeline_sync(mg_pipeline* q) {
 }
 
 void mg_pipeline_destroy(mg_pipeline* q) { delete q; }
+
+int32_t mg_batch_capacity(const mg_plan* p, const mg_processors* procs, int32_t batch, int64_t length, uint64_t* cap) {
+  return guarded([&] {
+    const BatchRenderer::Capacity c = BatchRenderer::capacity_for(p->rd, *procs->ps, batch, static_cast<long>(length));
+    cap[0] = c.rows;
+    cap[1] = c.workspace_bytes;
+    cap[2] = c.index_ints;
+    cap[3] = c.param_doubles;
+  });
+}
+
+int32_t mg_batch_create(const mg_processors* procs, int32_t batch, int64_t length, const uint64_t* cap, int32_t depth,
+                        mg_batch** out) {
+  return guarded([&] {
+    BatchRenderer::Capacity c;
+    c.rows = cap[0];
+    c.workspace_bytes = cap[1];
+    c.index_ints = cap[2];
+    c.param_doubles = cap[3];
+    auto b = std::make_unique<mg_batch>();
+    b->b = std::make_unique<BatchRenderer>(*procs->ps, batch, static_cast<long>(length), c, depth);
+    *out = b.release();
+  });
+}
+
+int32_t mg_batch_submit(mg_batch* b, const mg_plan* p, const double* const* tables, const int32_t* rows, int32_t validate,
+                        const float* sources, int32_t source_rows, int32_t sources_on_device, float* outputs) {
+  return guarded([&] {
+    b->b->submit(p->rd, tables, rows, validate != 0, sources, source_rows, sources_on_device != 0, outputs);
+  });
+}
+
+int32_t mg_batch_sync(mg_batch* b) {
+  return guarded([&] { b->b->sync(); });
+}
+
+int32_t mg_batch_last_arena(const mg_batch* b, void** arena) {
+  return guarded([&] { *arena = b->b->last_arena(); });
+}
+
+void mg_batch_destroy(mg_batch* b) { delete b; }
 
 int32_t mg_process(const mg_processors* procs, int32_t t, const double* in, double* out, int32_t slots, int32_t batch,
                    int64_t length, const double* params, int32_t param_rows, int32_t param_offset) {

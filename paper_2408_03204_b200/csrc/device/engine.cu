@@ -297,11 +297,11 @@ void run_step(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, void* w
 
 // ---- DevicePlan -------------------------------------------------------------------------
 
-DevicePlan::DevicePlan(const RenderData& rd) : rd_(rd) {
-  std::vector<int> host;
-  std::vector<char> written(static_cast<std::size_t>(rd.buffer_rows), 0);
-  for (int r = 0; r < rd.num_inputs && r < rd.buffer_rows; ++r) written[static_cast<std::size_t>(r)] = 1;
-  for (const StepIndex& st : rd.steps) {
+void DevicePlan::build_index() {
+  std::vector<int>& host = host_;
+  std::vector<char> written(static_cast<std::size_t>(rd_.buffer_rows), 0);
+  for (int r = 0; r < rd_.num_inputs && r < rd_.buffer_rows; ++r) written[static_cast<std::size_t>(r)] = 1;
+  for (const StepIndex& st : rd_.steps) {
     const int slots = st.store_end - st.store_begin;
     rp_off_.push_back(static_cast<long>(host.size()));
     std::size_t e = 0;
@@ -320,9 +320,15 @@ DevicePlan::DevicePlan(const RenderData& rd) : rd_(rd) {
     }
     for (int r = st.store_begin; r < st.store_end; ++r) written[static_cast<std::size_t>(r)] = 1;
   }
-  if (!host.empty()) {
-    cuda_check(cudaMalloc(&d_index_, sizeof(int) * host.size()), "cudaMalloc");
-    cuda_check(cudaMemcpy(d_index_, host.data(), sizeof(int) * host.size(), cudaMemcpyHostToDevice), "H2D plan");
+}
+
+DevicePlan::DevicePlan(const RenderData& rd) : rd_(rd) {
+  build_index();
+  if (!host_.empty()) {
+    int* d = nullptr;
+    cuda_check(cudaMalloc(&d, sizeof(int) * host_.size()), "cudaMalloc");
+    cuda_check(cudaMemcpy(d, host_.data(), sizeof(int) * host_.size(), cudaMemcpyHostToDevice), "H2D plan");
+    d_index_ = d;
   }
   // Prologues are off the critical path: lowest priority, so the CTA scheduler prefers the
   // main stream's kernels whenever both have work (honoured inside RenderGraph too).
@@ -333,10 +339,19 @@ DevicePlan::DevicePlan(const RenderData& rd) : rd_(rd) {
   for (auto& ev : events_) cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
 }
 
+DevicePlan::DevicePlan(const RenderData& rd, Deferred) : rd_(rd), owned_(false) { build_index(); }
+
+void DevicePlan::attach(const int* device_index, const std::array<cudaStream_t, 4>& aux, const cudaEvent_t* events) {
+  d_index_ = device_index;
+  aux_ = aux;
+  borrowed_events_ = events;
+}
+
 DevicePlan::~DevicePlan() {
+  if (!owned_) return;
   for (cudaEvent_t ev : events_) cudaEventDestroy(ev);
   for (cudaStream_t a : aux_) if (a) cudaStreamDestroy(a);
-  if (d_index_) cudaFree(d_index_);
+  if (d_index_) cudaFree(const_cast<int*>(d_index_));
 }
 
 const int* DevicePlan::row_ptr(int step) const { return d_index_ + rp_off_[static_cast<std::size_t>(step)]; }
@@ -719,6 +734,204 @@ void RenderPipeline::submit(const ParamStore& params, const void* const* sources
 void RenderPipeline::sync() {
   cuda_check(cudaStreamSynchronize(d2h_), "pipeline sync");
   cuda_check(cudaStreamSynchronize(compute_), "pipeline sync");
+}
+
+// ---- BatchRenderer ---------------------------------------------------------------------------
+
+void BatchRenderer::Capacity::grow(const Capacity& o) {
+  rows = std::max(rows, o.rows);
+  workspace_bytes = std::max(workspace_bytes, o.workspace_bytes);
+  index_ints = std::max(index_ints, o.index_ints);
+  param_doubles = std::max(param_doubles, o.param_doubles);
+}
+
+namespace {
+std::size_t param_src_ints(const RenderData& rd) {
+  std::size_t n = 0;
+  for (const auto& [t, src] : rd.param_source_rows) n += src.size();
+  return n;
+}
+std::size_t param_doubles_of(const RenderData& rd) {
+  std::size_t n = 0;
+  for (const auto& [t, src] : rd.param_source_rows) n += src.size() * static_cast<std::size_t>(param_width(t));
+  return n;
+}
+}  // namespace
+
+BatchRenderer::Capacity BatchRenderer::capacity_for(const RenderData& rd, const ProcessorSet& procs, int batch,
+                                                    long length) {
+  DevicePlan plan(rd, DevicePlan::Deferred{});
+  Capacity c;
+  c.rows = static_cast<std::size_t>(rd.buffer_rows);
+  c.workspace_bytes = plan.workspace_bytes(batch, length, procs);
+  c.index_ints = plan.host_index().size() + param_src_ints(rd);
+  c.param_doubles = param_doubles_of(rd);
+  return c;
+}
+
+struct BatchRenderer::Slot {
+  DeviceBuffer arena, ws, index, porig, prender;
+  void* pinned = nullptr;  // [index ints][pad][orig params]
+  std::unique_ptr<DevicePlan> plan;
+  cudaEvent_t h2d = nullptr, done = nullptr, d2h = nullptr;
+  bool used = false;
+  ~Slot() {
+    for (cudaEvent_t e : {h2d, done, d2h}) {
+      if (e) cudaEventDestroy(e);
+    }
+    if (pinned) cudaFreeHost(pinned);
+  }
+};
+
+BatchRenderer::BatchRenderer(const ProcessorSet& procs, int batch, long length, const Capacity& cap, int depth)
+    : procs_(procs), batch_(batch), length_(length), stride_(static_cast<long>(batch) * 2 * length), cap_(cap) {
+  if (depth < 1) fail("BatchRenderer: depth must be >= 1");
+  if (batch < 1 || length < 1) fail("BatchRenderer: batch and length must be positive");
+  cuda_check(cudaSetDevice(procs.device().device), "cudaSetDevice");
+  int least = 0, greatest = 0;
+  cuda_check(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
+  cuda_check(cudaStreamCreateWithPriority(&h2d_, cudaStreamNonBlocking, greatest), "stream");
+  cuda_check(cudaStreamCreateWithPriority(&compute_, cudaStreamNonBlocking, greatest), "stream");
+  cuda_check(cudaStreamCreateWithPriority(&d2h_, cudaStreamNonBlocking, greatest), "stream");
+  for (auto& a : aux_) cuda_check(cudaStreamCreateWithPriority(&a, cudaStreamNonBlocking, least), "stream");
+  const std::size_t index_bytes = align256(sizeof(int) * (cap.index_ints + 1));
+  for (int d = 0; d < depth; ++d) {
+    auto s = std::make_unique<Slot>();
+    s->arena.ensure(sizeof(float) * cap.rows * static_cast<std::size_t>(stride_) + 16);
+    s->ws.ensure(std::max<std::size_t>(cap.workspace_bytes, 256));
+    s->index.ensure(index_bytes);
+    s->porig.ensure(sizeof(double) * (cap.param_doubles + 1));
+    s->prender.ensure(sizeof(double) * (cap.param_doubles + 1));
+    cuda_check(cudaHostAlloc(&s->pinned, index_bytes + sizeof(double) * (cap.param_doubles + 1), cudaHostAllocDefault),
+               "cudaHostAlloc");
+    for (cudaEvent_t* e : {&s->h2d, &s->done, &s->d2h}) cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+    slots_.push_back(std::move(s));
+  }
+  cuda_check(cudaDeviceSynchronize(), "BatchRenderer setup");
+}
+
+BatchRenderer::~BatchRenderer() {
+  for (cudaStream_t st : {compute_, d2h_, h2d_}) {
+    if (st) cudaStreamSynchronize(st);
+  }
+  slots_.clear();
+  for (cudaEvent_t e : step_events_) cudaEventDestroy(e);
+  for (cudaStream_t a : aux_) if (a) cudaStreamDestroy(a);
+  for (cudaStream_t st : {h2d_, compute_, d2h_}) {
+    if (st) cudaStreamDestroy(st);
+  }
+}
+
+void BatchRenderer::submit(const RenderData& rd, const double* const* orig_tables, const int* orig_rows, bool validate,
+                           const float* sources, int source_rows, bool sources_on_device, float* outputs) {
+  cuda_check(cudaSetDevice(procs_.device().device), "cudaSetDevice");
+  auto plan = std::make_unique<DevicePlan>(rd, DevicePlan::Deferred{});
+  const std::vector<int>& idx = plan->host_index();
+  const std::size_t n_idx = idx.size() + param_src_ints(rd);
+  const std::size_t n_par = param_doubles_of(rd);
+  const std::size_t ws_bytes = plan->workspace_bytes(batch_, length_, procs_);
+  if (static_cast<std::size_t>(rd.buffer_rows) > cap_.rows || n_idx > cap_.index_ints || n_par > cap_.param_doubles ||
+      ws_bytes > cap_.workspace_bytes) {
+    fail("BatchRenderer: plan exceeds the renderer's capacity");
+  }
+  if (rd.num_inputs > 0 && (sources == nullptr || source_rows < 1)) fail("BatchRenderer: missing sources");
+  // Parameter tables: the reference's reorder_params checks (schedule.cpp:454-471), then the
+  // per-row checks render() applies (processors.cpp:132-149).
+  for (const auto& [t, src] : rd.param_source_rows) {
+    const int ti = static_cast<int>(t);
+    if (!orig_tables || !orig_tables[ti] || !orig_rows || orig_rows[ti] != static_cast<int>(src.size())) {
+      fail("reorder_params: missing or misshaped table for " + tname(t));
+    }
+    if (validate) {
+      const std::size_t w = static_cast<std::size_t>(param_width(t));
+      for (std::size_t r = 0; r < src.size(); ++r) check_param_row(t, {orig_tables[ti] + r * w, w});
+    }
+  }
+  while (step_events_.size() < rd.steps.size() + 1) {
+    cudaEvent_t e = nullptr;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    step_events_.push_back(e);
+  }
+
+  Slot& s = *slots_[next_ % slots_.size()];
+  ++next_;
+  // The pinned staging is rewritten on the host: its previous upload must have finished.
+  if (s.used) cuda_check(cudaEventSynchronize(s.h2d), "BatchRenderer staging");
+  int* pin_idx = static_cast<int*>(s.pinned);
+  std::memcpy(pin_idx, idx.data(), sizeof(int) * idx.size());
+  const std::size_t index_bytes = align256(sizeof(int) * (cap_.index_ints + 1));
+  auto* pin_par = reinterpret_cast<double*>(static_cast<char*>(s.pinned) + index_bytes);
+  int* dev_idx = static_cast<int*>(s.index.ptr);
+  auto* dev_orig = static_cast<double*>(s.porig.ptr);
+  auto* dev_render = static_cast<double*>(s.prender.ptr);
+  mgb::ParamGather g{};
+  const double* tables[kNumNodeTypes] = {};
+  std::size_t io = idx.size(), po = 0;
+  for (const auto& [t, src] : rd.param_source_rows) {
+    const int ti = static_cast<int>(t);
+    const std::size_t w = static_cast<std::size_t>(param_width(t));
+    std::memcpy(pin_idx + io, src.data(), sizeof(int) * src.size());
+    std::memcpy(pin_par + po, orig_tables[ti], sizeof(double) * src.size() * w);
+    g.in[ti] = dev_orig + po;
+    g.src_rows[ti] = dev_idx + io;
+    g.out[ti] = dev_render + po;
+    g.rows[ti] = static_cast<int>(src.size());
+    g.width[ti] = static_cast<int>(w);
+    tables[ti] = dev_render + po;
+    io += src.size();
+    po += src.size() * w;
+  }
+  float* arena = static_cast<float*>(s.arena.ptr);
+  // Uploads: the slot's previous render must be done with its device tables and arena.
+  if (s.used) cuda_check(cudaStreamWaitEvent(h2d_, s.done, 0), "wait");
+  if (n_idx) cuda_check(cudaMemcpyAsync(dev_idx, pin_idx, sizeof(int) * n_idx, cudaMemcpyHostToDevice, h2d_), "H2D plan");
+  if (n_par) cuda_check(cudaMemcpyAsync(dev_orig, pin_par, sizeof(double) * n_par, cudaMemcpyHostToDevice, h2d_), "H2D params");
+  const std::size_t row_bytes = sizeof(float) * static_cast<std::size_t>(stride_);
+  if (!sources_on_device && rd.num_inputs > 0) {
+    // Host sources: consecutive inputs that map to consecutive source rows go as one copy.
+    for (int k = 0; k < rd.num_inputs;) {
+      const int r0 = k % source_rows;
+      const int n = std::min(rd.num_inputs - k, source_rows - r0);
+      cuda_check(cudaMemcpyAsync(arena + static_cast<long>(k) * stride_, sources + static_cast<long>(r0) * stride_,
+                                 row_bytes * n, cudaMemcpyHostToDevice, h2d_), "H2D sources");
+      k += n;
+    }
+  }
+  cuda_check(cudaEventRecord(s.h2d, h2d_), "event");
+  // Compute: after the uploads, and after the slot's previous outputs were read back.
+  cuda_check(cudaStreamWaitEvent(compute_, s.h2d, 0), "wait");
+  if (s.used) cuda_check(cudaStreamWaitEvent(compute_, s.d2h, 0), "wait");
+  if (sources_on_device && rd.num_inputs > 0) {
+    for (int k = 0; k < rd.num_inputs;) {
+      const int r0 = k % source_rows;
+      const int n = std::min(rd.num_inputs - k, source_rows - r0);
+      cuda_check(cudaMemcpyAsync(arena + static_cast<long>(k) * stride_, sources + static_cast<long>(r0) * stride_,
+                                 row_bytes * n, cudaMemcpyDeviceToDevice, compute_), "D2D sources");
+      k += n;
+    }
+  }
+  mgb::launch_param_gather(g, compute_);
+  plan->attach(dev_idx, aux_, step_events_.data());
+  s.plan = std::move(plan);  // the previous plan of this slot is no longer referenced by queued work
+  render_arena(*s.plan, procs_, tables, arena, batch_, length_, s.ws.ptr, cap_.workspace_bytes, compute_);
+  cuda_check(cudaEventRecord(s.done, compute_), "event");
+  if (outputs) {
+    cuda_check(cudaStreamWaitEvent(d2h_, s.done, 0), "wait");
+    const int n_outs = rd.buffer_rows - rd.output_begin;
+    cuda_check(cudaMemcpyAsync(outputs, arena + static_cast<long>(rd.output_begin) * stride_, row_bytes * n_outs,
+                               cudaMemcpyDeviceToHost, d2h_), "D2H outputs");
+  }
+  cuda_check(cudaEventRecord(s.d2h, d2h_), "event");
+  s.used = true;
+}
+
+void BatchRenderer::sync() {
+  for (cudaStream_t st : {h2d_, compute_, d2h_}) cuda_check(cudaStreamSynchronize(st), "BatchRenderer sync");
+}
+
+float* BatchRenderer::last_arena() const {
+  if (next_ == 0) return nullptr;
+  return static_cast<float*>(slots_[(next_ - 1) % slots_.size()]->arena.ptr);
 }
 
 // ---- host-buffer API ----------------------------------------------------------------------

@@ -105,6 +105,18 @@ __host__ __device__ inline const float2* cover_table(const float2* tw) { return 
 void note_prologue_kernel(const void* fn);
 bool is_prologue_kernel(const void* fn);
 
+// Parameter reorder on the device (`schedule.cpp:454-471`, RenderData::reorder_params):
+// out[t][r][:] = in[t][src_rows[t][r]][:] for every type with rows (BatchRenderer uploads the
+// ORIGINAL-order tables and the plan's param_source_rows, and gathers here).
+struct ParamGather {
+  const double* in[10];
+  const int* src_rows[10];
+  double* out[10];
+  int rows[10];
+  int width[10];
+};
+void launch_param_gather(const ParamGather& g, cudaStream_t s);
+
 // Arena conversion helpers for the host-buffer API.
 void launch_f64_to_f32(const double* in, float* out, long n, cudaStream_t s);
 void launch_f32_to_f64(const float* in, double* out, long n, cudaStream_t s);

@@ -5,6 +5,8 @@
 // (m = l + r, s = exp(p) (l - r), y_l = (m + s)/2, y_r = (m - s)/2).
 // HBM-bound: per node-sample it moves 8*(deg_in + 1) bytes. One thread owns 4 consecutive
 // samples of both channels of one (slot, batch) row; float4 loads/stores when L % 4 == 0.
+#include <algorithm>
+
 #include "launch.hpp"
 
 namespace mgb {
@@ -157,7 +159,33 @@ __global__ void __launch_bounds__(kPwThreads) pointwise_chain_vec4(PwChain c) {
   }
 }
 
+// grid (ceil(max rows*width / 256 / 4), 10 types): one thread per 4 consecutive values.
+__global__ void param_gather(ParamGather g) {
+  const int t = blockIdx.y;
+  const int rows = g.rows[t], w = g.width[t];
+  const long n = static_cast<long>(rows) * w;
+  for (long i = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x * 4) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const long e = i + j;
+      if (e < n) {
+        const long r = e / w, c = e - r * w;
+        g.out[t][e] = __ldg(g.in[t] + static_cast<long>(__ldg(g.src_rows[t] + r)) * w + c);
+      }
+    }
+  }
+}
+
 }  // namespace
+
+void launch_param_gather(const ParamGather& g, cudaStream_t s) {
+  long most = 0;
+  for (int t = 0; t < 10; ++t) most = std::max(most, static_cast<long>(g.rows[t]) * g.width[t]);
+  if (most == 0) return;
+  const long blocks = std::min<long>((most + 1023) / 1024, 148L * 8);
+  param_gather<<<dim3(static_cast<unsigned>(blocks), 10), 256, 0, s>>>(g);
+}
 
 bool pointwise_chain_ok(const StepArgs& a) {
   return a.length % 4 == 0 && a.slots >= 1 && a.slots * a.batch <= kPwChainMaxRows;

@@ -123,6 +123,13 @@ RenderResult render(const RenderData& rd, const ProcessorSet& processors, const 
 class DevicePlan {
  public:
   explicit DevicePlan(const RenderData& rd);
+  // Borrowed residency (BatchRenderer): the step table is built on the host only; the owner
+  // uploads host_index() to device memory it manages and calls attach() with that address
+  // and with side streams / >= num_steps + 1 events it owns. No allocation, no sync.
+  struct Deferred {};
+  DevicePlan(const RenderData& rd, Deferred);
+  void attach(const int* device_index, const std::array<cudaStream_t, 4>& aux, const cudaEvent_t* events);
+  const std::vector<int>& host_index() const { return host_; }
   ~DevicePlan();
   DevicePlan(const DevicePlan&) = delete;
   DevicePlan& operator=(const DevicePlan&) = delete;
@@ -145,13 +152,17 @@ class DevicePlan {
   };
   Layout layout(int batch, long length, const ProcessorSet& procs) const;
   const std::array<cudaStream_t, 4>& aux_streams() const { return aux_; }
-  const cudaEvent_t* events() const { return events_.data(); }
+  const cudaEvent_t* events() const { return borrowed_events_ ? borrowed_events_ : events_.data(); }
 
  private:
+  void build_index();
   const RenderData& rd_;
+  bool owned_ = true;
   std::array<cudaStream_t, 4> aux_{};  // low-priority side streams for the prologues
   std::vector<cudaEvent_t> events_;  // [0] fork, [k+1] prologue of step k done
-  int* d_index_ = nullptr;
+  const cudaEvent_t* borrowed_events_ = nullptr;
+  const int* d_index_ = nullptr;
+  std::vector<int> host_;
   std::vector<long> rp_off_, col_off_;
   std::vector<int> zero_rows_;
 };
@@ -208,6 +219,52 @@ class RenderPipeline {
   bool f32_;
   long stride_;
   std::vector<std::unique_ptr<Slot>> slots_;
+  cudaStream_t h2d_ = nullptr, compute_ = nullptr, d2h_ = nullptr;
+  std::size_t next_ = 0;
+};
+
+// Renders a stream of plans whose topology changes every batch (BASELINE config 3: 64
+// random consoles per step, render order recomputed per batch). Nothing is allocated or
+// synchronised per plan: the arena, workspace, step tables and parameter tables live in
+// device pools sized once (Capacity), `depth` slots rotate, and each submit() packs the new
+// step table and the ORIGINAL-order parameter tables (as a dataset holds them) into pinned
+// staging, uploads them on a copy stream and reorders the parameters on the device
+// (`schedule.cpp:454-471`) before the render. The host therefore prepares batch i+1 while
+// the GPU renders batch i. `rd` must stay alive until its slot is reused (`depth` submits
+// later) or sync().
+class BatchRenderer {
+ public:
+  struct Capacity {
+    std::size_t rows = 0, workspace_bytes = 0, index_ints = 0, param_doubles = 0;
+    void grow(const Capacity& o);
+  };
+  static Capacity capacity_for(const RenderData& rd, const ProcessorSet& processors, int batch, long length);
+  BatchRenderer(const ProcessorSet& processors, int batch, long length, const Capacity& cap, int depth = 2);
+  ~BatchRenderer();
+  BatchRenderer(const BatchRenderer&) = delete;
+  BatchRenderer& operator=(const BatchRenderer&) = delete;
+  // orig_tables[t]: host fp64 [orig_rows[t]][param_width(t)] in original row order (null for
+  // types without parameters); validated like render() when `validate`. sources: fp32
+  // [source_rows][batch][2][length]; input k of the plan takes row k % source_rows (device
+  // memory: copied on the device; host memory: should be pinned). outputs: host fp32
+  // [num_outputs][batch][2][length], or null to keep them on the device (outputs()).
+  void submit(const RenderData& rd, const double* const* orig_tables, const int* orig_rows, bool validate,
+              const float* sources, int source_rows, bool sources_on_device, float* outputs);
+  void sync();
+  // Device arena of the most recent submit ([buffer_rows][batch][2][length] fp32).
+  float* last_arena() const;
+  cudaStream_t compute_stream() const { return compute_; }
+
+ private:
+  struct Slot;
+  const ProcessorSet& procs_;
+  int batch_;
+  long length_;
+  long stride_;
+  Capacity cap_;
+  std::vector<std::unique_ptr<Slot>> slots_;
+  std::array<cudaStream_t, 4> aux_{};
+  std::vector<cudaEvent_t> step_events_;
   cudaStream_t h2d_ = nullptr, compute_ = nullptr, d2h_ = nullptr;
   std::size_t next_ = 0;
 };

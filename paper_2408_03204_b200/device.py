@@ -185,3 +185,86 @@ class RenderPipeline:
         h, self._h = getattr(self, "_h", None), None
         if h:
             _destroy(h)
+
+
+class BatchRenderer:
+    """Renders of plans whose topology changes every batch (mg_batch_*, BASELINE config 3).
+
+    Device pools are sized once (`capacity`: [arena rows, workspace bytes, step-table ints,
+    parameter doubles], e.g. the max of `BatchRenderer.capacity_of(rd, ...)` over a dataset);
+    submit() packs the plan's step table and the ORIGINAL-order parameter tables into pinned
+    staging, uploads them on a copy stream, reorders the parameters on the device and enqueues
+    the render, without allocating or synchronising — the host prepares batch i+1 while the
+    GPU renders batch i. Plans and host arrays are kept alive until their slot is reused."""
+
+    def __init__(self, procs: ProcessorSet, batch: int, length: int, capacity, depth: int = 2):
+        self.procs, self.batch, self.length, self.depth = procs, int(batch), int(length), int(depth)
+        cap = np.ascontiguousarray(np.asarray(capacity, dtype=np.uint64).reshape(4))
+        self.capacity = cap
+        self._h = ctypes.c_void_p()
+        _check(_lib.mg_batch_create(procs.handle, self.batch, self.length, cap.ctypes.data_as(_vp), self.depth,
+                                    ctypes.byref(self._h)))
+        self._keep = [None] * self.depth
+        self._n = 0
+
+    @staticmethod
+    def capacity_of(rd: RenderData, procs: ProcessorSet, batch: int, length: int) -> np.ndarray:
+        cap = np.zeros(4, dtype=np.uint64)
+        _check(_lib.mg_batch_capacity(rd.handle, procs.handle, int(batch), int(length), cap.ctypes.data_as(_vp)))
+        return cap
+
+    def submit(self, rd: RenderData, params: Dict[int, np.ndarray], sources, outputs: Optional[np.ndarray] = None,
+               validate: bool = True) -> None:
+        """`params`: per-type tables in ORIGINAL row order; `sources`: float32
+        [rows][batch][2][length] torch CUDA tensor (device) or numpy array (host, ideally
+        pinned); input k of the plan takes source row k % rows. `outputs`: optional host
+        float32 [num_outputs][batch][2][length] array filled asynchronously (valid after sync)."""
+        from . import _tables
+        ptrs, rows, keep = _tables(params)
+        if isinstance(sources, torch.Tensor):
+            if not sources.is_cuda or sources.dtype != torch.float32 or not sources.is_contiguous():
+                raise ValueError("BatchRenderer: device sources must be a contiguous float32 CUDA tensor")
+            src_ptr, src_rows, on_dev = sources.data_ptr(), int(sources.shape[0]), 1
+            row = sources[0].numel()
+        else:
+            if sources.dtype != np.float32 or not sources.flags.c_contiguous:
+                raise ValueError("BatchRenderer: host sources must be contiguous float32")
+            src_ptr, src_rows, on_dev = sources.ctypes.data, int(sources.shape[0]), 0
+            row = sources[0].size
+        if row != self.batch * 2 * self.length:
+            raise ValueError(f"BatchRenderer: source rows must be [{self.batch}][2][{self.length}]")
+        out_ptr = None
+        if outputs is not None:
+            want = (rd.buffer_rows - rd.output_begin, self.batch, 2, self.length)
+            if outputs.shape != want or outputs.dtype != np.float32 or not outputs.flags.c_contiguous:
+                raise ValueError(f"BatchRenderer: outputs must be contiguous float32 {want}")
+            out_ptr = outputs.ctypes.data
+        _check(_lib.mg_batch_submit(self._h, rd.handle, ptrs, rows.ctypes.data_as(_vp), int(bool(validate)),
+                                    ctypes.c_void_p(src_ptr), src_rows, on_dev, out_ptr))
+        self._keep[self._n % self.depth] = (rd, keep, sources, outputs)
+        self._n += 1
+
+    def sync(self) -> None:
+        _check(_lib.mg_batch_sync(self._h))
+
+    def last_outputs(self) -> torch.Tensor:
+        """Device view of the most recent submit's output rows (valid after sync)."""
+        rd = self._keep[(self._n - 1) % self.depth][0]
+        p = ctypes.c_void_p()
+        _check(_lib.mg_batch_last_arena(self._h, ctypes.byref(p)))
+        n = rd.buffer_rows * self.batch * 2 * self.length
+        arena = _device_view(p.value, n, self.procs.device).view(rd.buffer_rows, self.batch, 2, self.length)
+        return arena[rd.output_begin:]
+
+    def __del__(self, _destroy=_lib.mg_batch_destroy):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            _destroy(h)
+
+
+def _device_view(ptr: int, n: int, device: int) -> torch.Tensor:
+    """A float32 torch view of `n` elements of library-owned device memory (no copy)."""
+    class _Iface:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3, "strides": None}
+    with torch.cuda.device(device):
+        return torch.as_tensor(_Iface(), device=f"cuda:{device}")

@@ -379,3 +379,64 @@ def test_render_pipeline_matches_render(mg, ref, dtype):
         want = mg.render(rd, procs, P, src.astype(np.float32).astype(np.float64))
         assert np.array_equal(out.astype(np.float64), want.astype(np.float32).astype(np.float64)) if dtype == np.float32 \
             else np.array_equal(out, want)
+
+
+def _random_union(mg, sharding, seed, graphs):
+    rng = np.random.default_rng(seed)
+    members = [mg.generate_console_arrays(int(rng.integers(2, 9)), 0.3, 50 * seed + i) for i in range(graphs)]
+    return sharding.union_arrays(members)
+
+
+@pytest.mark.parametrize("on_device", [True, False])
+def test_batch_renderer_redrawn_topologies(mg, ref, on_device):
+    # Config-3 style: a different union every submit, original-order parameters reordered on
+    # the device, sources cycled from a bank; every render equals the blocking render().
+    import torch
+    from paper_2408_03204_b200 import sharding
+    L = 12000
+    procs = mg.ProcessorSet()
+    bank = np.random.default_rng(1).uniform(-1, 1, size=(5, 1, 2, L)).astype(np.float32)
+    batches = []
+    for i in range(4):
+        t, e = _random_union(mg, sharding, i, 3 + i)
+        batches.append((t, e, mg.compute_render_data_arrays(t, e), mg.random_legal_params(t, 70 + i)))
+    cap = np.zeros(4, dtype=np.uint64)
+    for _, _, rd, _ in batches:
+        cap = np.maximum(cap, mg.BatchRenderer.capacity_of(rd, procs, 1, L))
+    br = mg.BatchRenderer(procs, 1, L, cap, depth=2)
+    src = torch.as_tensor(bank).cuda() if on_device else bank
+    outs = []
+    for t, e, rd, params in batches:
+        out = np.zeros((rd.buffer_rows - rd.output_begin, 1, 2, L), dtype=np.float32)
+        br.submit(rd, params, src, out)
+        outs.append(out)
+    br.sync()
+    for (t, e, rd, params), out in zip(batches, outs):
+        k = rd.num_inputs
+        s = bank[np.arange(k) % len(bank)].astype(np.float64)
+        want = mg.render(rd, procs, rd.reorder_params(params), s)
+        assert np.array_equal(out.astype(np.float64), want)
+    t, e, rd, params = batches[-1]
+    assert rel(outs[-1], ref.Plan(t, e, 1).render(params, bank[np.arange(rd.num_inputs) % 5].astype(np.float64))) < TOL
+    dev_out = br.last_outputs().cpu().numpy()
+    assert np.array_equal(dev_out, outs[-1])
+
+
+def test_batch_renderer_rejects_bad_params(mg):
+    from paper_2408_03204_b200 import sharding
+    L = 4096
+    procs = mg.ProcessorSet()
+    t, e = _random_union(mg, sharding, 9, 2)
+    rd = mg.compute_render_data_arrays(t, e)
+    br = mg.BatchRenderer(procs, 1, L, mg.BatchRenderer.capacity_of(rd, procs, 1, L))
+    src = np.zeros((1, 1, 2, L), dtype=np.float32)
+    params = mg.random_legal_params(t, 3)
+    bad = {k: v.copy() for k, v in params.items()}
+    bad[mg.NodeType.COMPRESSOR][0, 0] = 1.5
+    with pytest.raises(ValueError, match="alpha"):
+        br.submit(rd, bad, src)
+    short = {k: v for k, v in params.items() if k != mg.NodeType.EQ}
+    with pytest.raises(ValueError, match="missing or misshaped"):
+        br.submit(rd, short, src)
+    br.submit(rd, params, src)
+    br.sync()
