@@ -595,6 +595,50 @@ def generate_console(tracks: int, prune: float = 0.0, seed: int = 0) -> Graph:
     return Graph.from_arrays(*generate_console_arrays(tracks, prune, seed))
 
 
+def generate_large_console_arrays(tracks: int = 64) -> Tuple[np.ndarray, np.ndarray]:
+    """BASELINE config 4's pruning-scale graph (SURVEY.md §8d recipe; not producible by
+    generate_console, which tops out at 8K+6 nodes): per track in -> e c n s g e c n s g (a
+    doubled channel strip), whose last gain feeds the mix bus directly and through two sends
+    (delay -> gain, reverb -> gain); bus mix -> e c s g -> out. 15 nodes and 17 edges per track
+    (64 tracks: 966 nodes, 1093 edges). Insertion order follows console.cpp (per-track nodes,
+    then the bus). Synthetic: no RNG, parameters come from random_legal_params."""
+    if tracks < 1:
+        raise ValueError("generate_large_console: need at least one track")
+    T = NodeType
+    types, edges, sends = [], [], []
+
+    def node(t):
+        types.append(int(t))
+        return len(types) - 1
+
+    def chain(ts):
+        ids = [node(t) for t in ts]
+        for a, b in zip(ids, ids[1:]):
+            edges.append((a, b))
+        return ids[0], ids[-1]
+
+    strip = [T.EQ, T.COMPRESSOR, T.NOISEGATE, T.IMAGER, T.GAIN] * 2
+    for _ in range(tracks):
+        i = node(T.IN)
+        first, last = chain(strip)
+        edges.append((i, first))
+        for fx in (T.DELAY, T.REVERB):
+            s0, s1 = chain([fx, T.GAIN])
+            edges.append((last, s0))
+            sends.append(s1)
+        sends.append(last)
+    bus = node(T.MIX)
+    for s in sends:
+        edges.append((s, bus))
+    b0, b1 = chain([T.EQ, T.COMPRESSOR, T.IMAGER, T.GAIN])
+    edges.append((bus, b0))
+    out = node(T.OUT)
+    edges.append((b1, out))
+    e = np.zeros((len(edges), 4), dtype=np.int32)
+    e[:, :2] = np.asarray(edges, dtype=np.int32)
+    return np.asarray(types, dtype=np.int32), e
+
+
 def random_legal_params(node_types: Sequence[int], seed: int) -> Dict[NodeType, np.ndarray]:
     """`tests/support/test_util.cpp:63-113` with a fresh mt19937(seed), original row order."""
     counts: Dict[int, int] = {}
@@ -622,7 +666,7 @@ from .device import BatchRenderer, DeviceRenderer, RenderPipeline  # noqa: E402 
 __all__ = [
     "NodeType", "Strategy", "Graph", "FlatGraph", "RenderData", "StepIndex", "Schedule", "ProcessorSet",
     "BatchRenderer", "DeviceRenderer", "RenderPipeline", "to_flat", "disjoint_union", "compute_render_data_arrays",
-    "generate_console_arrays", "default_params", "default_param_row", "concat_params",
+    "generate_console_arrays", "generate_large_console_arrays", "default_params", "default_param_row", "concat_params",
     "compute_render_data", "make_schedule", "validate_schedule", "render", "param_width", "type_code", "type_name",
     "generate_console", "random_legal_params", "uniform_noise", "compressor_gain_log", "noisegate_gain_log",
     "check_param_row", "LIB_PATH",

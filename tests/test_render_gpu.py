@@ -440,3 +440,53 @@ def test_batch_renderer_rejects_bad_params(mg):
         br.submit(rd, short, src)
     br.submit(rd, params, src)
     br.sync()
+
+
+def _track_params(mg, t, params, tracks, k):
+    """Parameter rows of track k of generate_large_console(tracks), as a 1-track table set
+    (rows of each type are numbered in node insertion order; tracks come first)."""
+    per = {}
+    for ty in set(int(x) for x in t[:15]):
+        if mg.param_width(ty):
+            per[ty] = int(np.sum(t[:15] == ty))
+    small = {}
+    for ty, n in per.items():
+        tab = params[mg.NodeType(ty)]
+        small[mg.NodeType(ty)] = tab[k * n:(k + 1) * n]
+    # bus rows (one eq, comp, imager, gain) follow all track rows of their type
+    for ty in (mg.NodeType.EQ, mg.NodeType.COMPRESSOR, mg.NodeType.IMAGER, mg.NodeType.GAIN):
+        n = per[int(ty)]
+        small[ty] = np.concatenate([small[ty], params[ty][tracks * n:tracks * n + 1]])
+    return small
+
+
+def test_config4_large_graph_full_size(mg, ref):
+    # BASELINE config 4: 64 tracks, 966 nodes, 10 s stereo (L = 441000, 2^20-point reverb
+    # convolutions). The full graph is checked track by track: each track's strip and send
+    # outputs (intermediates) equal a 1-track graph rendered with that track's parameters,
+    # and the 1-track graph matches the reference renderer at full length.
+    L, tracks = 441000, 64
+    t, e = mg.generate_large_console_arrays(tracks)
+    assert len(t) == 966 and len(e) == 1093
+    params = mg.random_legal_params(t, 44)
+    k_src = 3
+    src = np.stack([mg.uniform_noise(2 * L, 1000 + (k % k_src)).reshape(1, 2, L) for k in range(tracks)])
+    import torch
+    procs = mg.ProcessorSet()
+    rd = mg.compute_render_data_arrays(t, e)
+    dr = mg.DeviceRenderer(rd, procs, 1, L, rd.reorder_params(params))
+    dr.sources.copy_(torch.as_tensor(src, dtype=torch.float32))
+    out = dr.render().cpu().numpy()
+    assert np.isfinite(out).all() and np.abs(out).max() > 0
+    sigma = np.asarray(rd.sigma)
+    t1, e1 = mg.generate_large_console_arrays(1)
+    rd1 = mg.compute_render_data_arrays(t1, e1)
+    for k in (0, 37, 63):
+        p1 = _track_params(mg, t, params, tracks, k)
+        y1, i1 = mg.render(rd1, procs, rd1.reorder_params(p1), src[k:k + 1], keep_intermediates=True)
+        rows = torch.as_tensor(sigma[15 * k:15 * k + 15], device=dr.arena.device)
+        big = dr.arena.index_select(0, rows).cpu().numpy()
+        assert rel(big, i1[:15]) < 1e-5, k
+        if k == 37:
+            want = ref.Plan(t1, e1, 1).render(p1, src[k:k + 1])
+            assert rel(y1, want) < TOL
