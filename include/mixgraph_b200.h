@@ -127,6 +127,20 @@ int32_t mg_pipeline_submit(mg_pipeline* pipe, const double* const* tables, const
 int32_t mg_pipeline_sync(mg_pipeline* pipe);
 void mg_pipeline_destroy(mg_pipeline* pipe);
 
+/* Reverse-mode pass over a device render (parameter gradients, BASELINE configs 4/5; the
+ * reference has no autodiff — fit.cpp:70-82 takes central differences, which the tests
+ * compare against). d_arena / d_workspace: those of the mg_render_arena call that produced
+ * the forward, the workspace sized by mg_backward_workspace_bytes (>= the forward's).
+ * d_adjoint [rows][B][2][L] fp32: rows [output_begin, rows) hold dL/d(outputs) on entry;
+ * on return rows [0, num_inputs) hold dL/d(sources) (other rows: dL/d(node inputs)).
+ * d_grad_tables[t]: device fp64 tables shaped like d_tables[t] (render order), overwritten.
+ * Delay tap positions are piecewise constant: their (Re z, Im z) gradients are 0. */
+int32_t mg_backward_workspace_bytes(const mg_plan* plan, const mg_processors* procs, int32_t batch, int64_t length,
+                                    uint64_t* bytes);
+int32_t mg_render_backward_arena(const mg_plan* plan, const mg_processors* procs, const double* const* d_tables,
+                                 const float* d_arena, float* d_adjoint, double* const* d_grad_tables, int32_t batch,
+                                 int64_t length, void* d_workspace, uint64_t workspace_bytes, void* stream);
+
 /* Renders of plans whose topology changes every batch (BASELINE config 3), no per-plan
  * allocation or synchronisation: device pools sized once from a capacity (cap[4] = arena
  * rows, workspace bytes, step-table ints, parameter doubles; mg_batch_capacity gives one

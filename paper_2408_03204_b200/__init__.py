@@ -79,6 +79,8 @@ _sig("mg_pipeline_create", _i32, _vp, _vp, _i32, _i64, _i32, _i32, _P(_vp))
 _sig("mg_pipeline_submit", _i32, _vp, _vp, _vp, _vp, _vp)
 _sig("mg_pipeline_sync", _i32, _vp)
 _sig("mg_pipeline_destroy", None, _vp)
+_sig("mg_backward_workspace_bytes", _i32, _vp, _vp, _i32, _i64, _P(_u64))
+_sig("mg_render_backward_arena", _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp)
 _sig("mg_batch_capacity", _i32, _vp, _vp, _i32, _i64, _vp)
 _sig("mg_batch_create", _i32, _vp, _i32, _i64, _vp, _i32, _P(_vp))
 _sig("mg_batch_submit", _i32, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp)
@@ -405,6 +407,17 @@ class RenderData:
             optrs[int(t)] = m.ctypes.data
         _check(_lib.mg_plan_reorder_params(self._h, ptrs, _ptr(rows), optrs))
         del keep
+        return out
+
+    def original_order(self, render_order: Dict[int, np.ndarray]) -> Dict[NodeType, np.ndarray]:
+        """Inverse of reorder_params: per-type tables (e.g. gradients) from render order back
+        to the original row order (`schedule.cpp:515-523` param_source_rows)."""
+        out = {}
+        for t, src in self.param_source_rows.items():
+            m = np.asarray(render_order[t])
+            o = np.empty_like(m)
+            o[np.asarray(src, dtype=np.int64)] = m
+            out[NodeType(t)] = o
         return out
 
     def kernel_count(self, batch: int, length: int) -> int:

@@ -412,6 +412,22 @@ int32_t mg_pipeline_sync(mg_pipeline* q) {
 
 void mg_pipeline_destroy(mg_pipeline* q) { delete q; }
 
+int32_t mg_backward_workspace_bytes(const mg_plan* p, const mg_processors* procs, int32_t batch, int64_t length,
+                                    uint64_t* bytes) {
+  return guarded([&] { *bytes = device_plan(p).backward_workspace_bytes(batch, static_cast<long>(length), *procs->ps); });
+}
+
+int32_t mg_render_backward_arena(const mg_plan* p, const mg_processors* procs, const double* const* d_tables,
+                                 const float* d_arena, float* d_adjoint, double* const* d_grad_tables, int32_t batch,
+                                 int64_t length, void* d_workspace, uint64_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    DevicePlan& dp = device_plan(p);
+    std::scoped_lock lock(const_cast<mg_plan*>(p)->render_mu);
+    backward_arena(dp, *procs->ps, d_tables, d_arena, d_adjoint, d_grad_tables, batch, static_cast<long>(length),
+                   d_workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int32_t mg_batch_capacity(const mg_plan* p, const mg_processors* procs, int32_t batch, int64_t length, uint64_t* cap) {
   return guarded([&] {
     const BatchRenderer::Capacity c = BatchRenderer::capacity_for(p->rd, *procs->ps, batch, static_cast<long>(length));

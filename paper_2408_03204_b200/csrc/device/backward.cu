@@ -1,0 +1,196 @@
+// Reverse-mode pass over a rendered arena: parameter gradients (BASELINE configs 4/5, the
+// optimisation setting).
+//
+// The reference has no autodiff (`SPEC.md:14`): its only gradient is the central
+// difference of `fit.cpp:70-82`, which is what the tests compare these kernels with. The
+// pass runs the steps in reverse. For a node v with aggregated input X_v (Eq. 1b) and output
+// Y_v, the adjoint arena holds dL/dX_v in v's row; dL/dY_v is the sum of dL/dX_w over v's
+// consumer edges (a transposed CSR, gathered in a fixed order, so no atomics). Per type:
+//   mix/out/in  dX = dY
+//   gain        dX = e^p dY (the forward kernel on the adjoint arena);  dp_c = sum dY_c Y_c
+//   imager      dX = M dY (M symmetric: forward kernel);  dp = sum (dY_l - dY_r)(Y_l - Y_r)/2
+//   eq          dX = h (x) dY (zero-phase h is even: forward kernel);  dh = corr(dY, X) then
+//               through zero_phase_fir (`dsp.cpp:106-136`): a cosine sum in fp64
+//   comp/gate   reverse affine scan (dynamics.cu)
+//   reverb/delay  dX = corr(dY, h) (conjugate kernel spectrum), dh = corr(dY, X), then
+//               through the ISTFT (`dsp.cpp:165-190`) / the tap FIRs (fftconv.cu)
+// This file: the pointwise parameter reductions and the EQ correlation + FIR adjoint.
+#include <algorithm>
+
+#include "fft_smem.cuh"
+#include "launch.hpp"
+
+namespace mgb {
+
+namespace {
+
+constexpr int kPgThreads = 256;
+constexpr int kPgPer = 8;  // samples per thread
+
+// Partial sums of the pointwise parameter gradients. grid (blocks, slots*B).
+// out[(sb * gridDim.x + blk) * 2 + j] (fp64).
+template <PointOp OP>
+__global__ void __launch_bounds__(kPgThreads) pw_param_grad(StepArgs fw, StepArgs bw, double* out) {
+  __shared__ double red[kPgThreads / 32][2];
+  const int sb = blockIdx.y;
+  const int slot = sb / fw.batch, b = sb - slot * fw.batch;
+  const int e0 = __ldg(bw.row_ptr + slot), e1 = __ldg(bw.row_ptr + slot + 1);
+  const float* y = fw.dst + static_cast<long>(slot) * fw.rowstride + static_cast<long>(b) * 2 * fw.length;
+  double s0 = 0.0, s1 = 0.0;
+  const long n0 = (static_cast<long>(blockIdx.x) * kPgThreads + threadIdx.x) * kPgPer;
+  for (int k = 0; k < kPgPer; ++k) {
+    const long n = n0 + k;
+    if (n >= fw.length) break;
+    const float2 dy = gather2(bw, e0, e1, b, n);
+    const float yl = __ldg(y + n), yr = __ldg(y + fw.length + n);
+    if constexpr (OP == PointOp::Gain) {
+      s0 += static_cast<double>(dy.x * yl);
+      s1 += static_cast<double>(dy.y * yr);
+    } else {
+      s0 += 0.5 * static_cast<double>((dy.x - dy.y) * (yl - yr));
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, off);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[warp][0] = s0;
+    red[warp][1] = s1;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double t = 0.0;
+    for (int w = 0; w < kPgThreads / 32; ++w) t += red[w][threadIdx.x];
+    out[(static_cast<long>(sb) * gridDim.x + blockIdx.x) * 2 + threadIdx.x] = t;
+  }
+}
+
+// grid (slots) x 32: grad[slot][j] = sum over rows_per_slot partial rows (fixed order).
+__global__ void reduce_partials(const double* partial, int rows_per_slot, int stride, int width, double* grad,
+                                int grad_width) {
+  const int slot = blockIdx.x;
+  for (int j = threadIdx.x; j < width; j += blockDim.x) {
+    double t = 0.0;
+    for (int r = 0; r < rows_per_slot; ++r) t += partial[(static_cast<long>(slot) * rows_per_slot + r) * stride + j];
+    grad[static_cast<long>(slot) * grad_width + j] = t;
+  }
+}
+
+// ---- EQ ---------------------------------------------------------------------------------------
+constexpr int kCorrLog = 13;
+constexpr int kCorrFft = 1 << kCorrLog;
+constexpr int kCorrOut = 6144;  // outputs per block (as the forward's 8192 window)
+constexpr int kCorrThreads = 512;
+constexpr int kCorrFS = padded(kCorrFft);
+
+// count samples of (gathered) signal from position `start` into buf[sidx(i)] (channels as
+// re/im), zeros outside [0, L) and for i >= count.
+__device__ __forceinline__ void load_window(const StepArgs& a, int e0, int e1, int b, long start, int count,
+                                            float2* buf) {
+  for (int i = threadIdx.x; i < kCorrFft; i += kCorrThreads) {
+    const long n = start + i;
+    float2 v = make_float2(0.f, 0.f);
+    if (i < count && n >= 0 && n < a.length) v = gather2(a, e0, e1, b, n);
+    buf[sidx(i)] = v;
+  }
+}
+
+// dh[j] for one output block: with W = x[out0 - 1024 + u] (u < 8192) and D = dy[out0 + v]
+// (v < 6144, zero-padded), sum_v D[v] W[v + s] = IFFT(conj(D^) W^)[s]; tap j = 2047 - s.
+// Channels packed as re/im: the real part of the product sums both channels' correlations.
+// grid (blocks, slots*B); out[(sb * gridDim.x + blk) * 2048 + j].
+__global__ void __launch_bounds__(kCorrThreads, 1) eq_corr(StepArgs fw, StepArgs bw, float* out) {
+  extern __shared__ float2 buf[];  // [2][kCorrFS]: window, dy block
+  const int sb = blockIdx.y;
+  const int slot = sb / fw.batch, b = sb - slot * fw.batch;
+  const long out0 = static_cast<long>(blockIdx.x) * kCorrOut;
+  load_window(fw, __ldg(fw.row_ptr + slot), __ldg(fw.row_ptr + slot + 1), b, out0 - (kEqHalf + 1), kCorrFft, buf);
+  load_window(bw, __ldg(bw.row_ptr + slot), __ldg(bw.row_ptr + slot + 1), b, out0, kCorrOut, buf + kCorrFS);
+  __syncthreads();
+  fft_pow2<kCorrLog, 2, kCorrThreads, -1>(buf, kCorrFS, fw.tw);
+  for (int k = threadIdx.x; k < kCorrFft; k += kCorrThreads) {
+    const float2 w = buf[sidx(k)], d = buf[kCorrFS + sidx(k)];
+    buf[kCorrFS + sidx(k)] = cmul(cconj(d), w);
+  }
+  __syncthreads();
+  fft_pow2<kCorrLog, 1, kCorrThreads, +1>(buf + kCorrFS, kCorrFS, fw.tw);
+  float* o = out + (static_cast<long>(sb) * gridDim.x + blockIdx.x) * 2048;
+  for (int j = threadIdx.x; j < 2 * kEqHalf + 1; j += kCorrThreads) {
+    o[j] = buf[kCorrFS + sidx(2 * kEqHalf + 1 - j)].x * (1.f / kCorrFft);
+  }
+}
+
+// Per slot: dtaps = sum of the block partials (fixed order), then the zero_phase_fir adjoint
+//   d lm[q] = (m_q / N) e^{lm[q]} sum_t dtaps[t] hann[t] cos(2 pi q (t - c) / N),
+// m_0 = 1, m_q = 2 (N = 2047, c = 1023). grid (slots) x 1024, fp64.
+__global__ void __launch_bounds__(1024) eq_grad(const float* partial, int rows_per_slot, const double* params,
+                                                const double* __restrict__ cos_tab, double* grad) {
+  constexpr int N = 2 * kEqHalf + 1, C = kEqHalf;
+  __shared__ double sym[kEqHalf + 1];  // S_j = (dh w)[c + j] + (dh w)[c - j], S_0 = (dh w)[c]
+  const int slot = blockIdx.x;
+  const float* p = partial + static_cast<long>(slot) * rows_per_slot * 2048;
+  const int j = threadIdx.x;  // 0..1023
+  double hi = 0.0, lo = 0.0;
+  for (int r = 0; r < rows_per_slot; ++r) {
+    hi += p[static_cast<long>(r) * 2048 + C + j];
+    if (j > 0) lo += p[static_cast<long>(r) * 2048 + C - j];
+  }
+  double s, c;
+  sincospi(2.0 * (C + j) / (N - 1), &s, &c);
+  const double w = 0.5 - 0.5 * c;  // symmetric Hann, w(c + j) == w(c - j)
+  sym[j] = w * (hi + lo);
+  __syncthreads();
+  const int q = threadIdx.x;
+  double acc = 0.0;
+  int idx = 0;
+  for (int t = 0; t <= kEqHalf; ++t) {
+    acc = fma(sym[t], __ldg(cos_tab + idx), acc);
+    idx += q;
+    if (idx >= N) idx -= N;
+  }
+  const double lm = params[static_cast<long>(slot) * (kEqHalf + 1) + q];
+  grad[static_cast<long>(slot) * (kEqHalf + 1) + q] = (q == 0 ? 1.0 : 2.0) / N * exp(lm) * acc;
+}
+
+}  // namespace
+
+std::size_t pw_grad_bytes(int slots, int batch, long length) {
+  const long blocks = (length + kPgThreads * kPgPer - 1) / (kPgThreads * kPgPer);
+  return sizeof(double) * 2 * static_cast<std::size_t>(slots) * batch * blocks;
+}
+
+void launch_pointwise_param_grad(PointOp op, const StepArgs& fw, const StepArgs& bw, void* ws, double* grad,
+                                 cudaStream_t s) {
+  if (fw.slots == 0 || op == PointOp::Copy) return;
+  const long blocks = (fw.length + kPgThreads * kPgPer - 1) / (kPgThreads * kPgPer);
+  const dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(fw.slots * fw.batch));
+  auto* part = static_cast<double*>(ws);
+  if (op == PointOp::Gain) pw_param_grad<PointOp::Gain><<<grid, kPgThreads, 0, s>>>(fw, bw, part);
+  else pw_param_grad<PointOp::Imager><<<grid, kPgThreads, 0, s>>>(fw, bw, part);
+  const int width = op == PointOp::Gain ? 2 : 1;
+  reduce_partials<<<fw.slots, 32, 0, s>>>(part, static_cast<int>(blocks) * fw.batch, 2, width, grad, width);
+}
+
+std::size_t eq_grad_bytes(int slots, int batch, long length) {
+  const long blocks = (length + kCorrOut - 1) / kCorrOut;
+  return sizeof(float) * 2048 * static_cast<std::size_t>(slots) * batch * blocks;
+}
+
+void launch_eq_param_grad(const StepArgs& fw, const StepArgs& bw, void* ws, double* grad, cudaStream_t s) {
+  if (fw.slots == 0) return;
+  static const bool done = [] {
+    cudaFuncSetAttribute(eq_corr, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kCorrFS * 8);
+    return true;
+  }();
+  (void)done;
+  const long blocks = (fw.length + kCorrOut - 1) / kCorrOut;
+  auto* part = static_cast<float*>(ws);
+  eq_corr<<<dim3(static_cast<unsigned>(blocks), static_cast<unsigned>(fw.slots * fw.batch)), kCorrThreads,
+            2 * kCorrFS * 8, s>>>(fw, bw, part);
+  eq_grad<<<fw.slots, 1024, 0, s>>>(part, static_cast<int>(blocks) * fw.batch, fw.params, cos_table(fw.tw), grad);
+}
+
+}  // namespace mgb

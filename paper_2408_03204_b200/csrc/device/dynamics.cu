@@ -31,6 +31,17 @@ struct DynParams {
   int Ne;
 };
 
+struct DynBwd {
+  StepArgs fw, bw;     // forward (arena, forward CSR, params) / backward (input grads, consumer CSR)
+  const float* env;    // [seq][L] envelope from the forward scan
+  float2* agg;         // [seq][tiles] tile map vectors (pass 0)
+  float2* carry;       // [seq][tiles] (w, v) at each tile's right end
+  double* partial;     // [seq][tiles][5]
+  int env_taps;
+  double floor_;
+  int tiles;
+};
+
 // Slot constants, derived by warp 0 of each CTA: lanes 0-3 evaluate the four fp64 powers
 // a^Ne, a^8, a^tile, a^(32 tile) side by side (one pow latency), lane 0 assembles.
 __device__ __forceinline__ void derive_params(const double* row, int env_taps, double floor_, long L, int lane,
@@ -125,9 +136,11 @@ __device__ __forceinline__ void compose(float& A, float& B, float Ap, float Bp) 
   A = A * Ap;
 }
 
-template <bool GATE, bool VEC>
+// ENV: also store the envelope g[n] to env[(slot*B + b)*L + n] (backward pass recompute).
+template <bool GATE, bool VEC, bool ENV = false>
 __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_taps, double floor_, int tiles_per_seq,
-                                                         unsigned long long* status, unsigned int* ticket) {
+                                                         unsigned long long* status, unsigned int* ticket,
+                                                         float* env = nullptr) {
   __shared__ float wA[kDynThreads / 32], wB[kDynThreads / 32];
   __shared__ float s_carry;
   __shared__ int s_ticket;
@@ -269,6 +282,9 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
     for (int k4 = 0; k4 < 4; ++k4) {
       const int k = 4 * q + k4;
       g = fmaf(p.a, g, drive[k]);
+      if constexpr (ENV) {
+        if (n0 + k < a.length) env[static_cast<long>(seq) * a.length + n0 + k] = g;
+      }
       const float gn = gain_of<GATE>(g, p);
       yl[k4] = gn * ul[k];
       yr[k4] = gn * ur[k];
@@ -288,7 +304,327 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
   }
 }
 
+// ---- backward (parameter gradients; no reference counterpart, see backward.cu) -------------
+//
+// Given dy (gathered over the consumers' input gradients) and the forward quantities
+// (u gathered from the arena, envelope g stored by dyn_scan<.., ENV>):
+//   gain = exp(G_y - G_u), dD = (dy_l u_l + dy_r u_r) gain, dG_u = dD (dG_y/dG_u - 1),
+//   dg = dG_u / g (g above the floor, else 0),
+//   w[m] = a w[m+1] + dg[m] - a^Ne dg[m+Ne]                (de = (1-a) w),
+//   v[m] = a v[m+1] + w[m+1] - Ne a^(Ne-1) dg[m+Ne]        (v = d w / d a),
+//   du_c = gain dy_c + 2 mid de,
+//   d a = -sum dg g / (1-a) + (1-a) sum e v,  dT/dW/dR = sum dD dG_y/d{T,W,R}.
+// (w, v) is a reverse scan of affine maps with matrix [[a,0],[1,a]]^k = [[a^k,0],[k a^(k-1),a^k]]:
+// pass 0 reduces each tile to its map, dyn_bwd_carry chains the tiles per sequence (fp64,
+// serial, fixed order), pass 1 replays each tile from its carry. Deterministic.
+struct DynMap {
+  float p, q, cw, cv;
+};
+// A o B (B applied first)
+__device__ __forceinline__ DynMap dmap_compose(const DynMap& A, const DynMap& B) {
+  DynMap r;
+  r.p = A.p * B.p;
+  r.q = fmaf(A.q, B.p, A.p * B.q);
+  r.cw = fmaf(A.p, B.cw, A.cw);
+  r.cv = fmaf(A.q, B.cw, fmaf(A.p, B.cv, A.cv));
+  return r;
+}
+__device__ __forceinline__ DynMap dmap_shfl_down(const DynMap& m, int off) {
+  DynMap r;
+  r.p = __shfl_down_sync(0xffffffffu, m.p, off);
+  r.q = __shfl_down_sync(0xffffffffu, m.q, off);
+  r.cw = __shfl_down_sync(0xffffffffu, m.cw, off);
+  r.cv = __shfl_down_sync(0xffffffffu, m.cv, off);
+  return r;
+}
+
+// Knee derivatives at G = G_u: returns dG_y/dG_u, accumulates dG_y/d{T,W,R} * dD.
+template <bool GATE>
+__device__ __forceinline__ float knee_grad(float gu, const DynParams& p, float dD, float* acc) {
+  if (!GATE) {
+    if (gu >= p.T + p.W) {
+      acc[0] += dD * (1.f - p.invR);
+      acc[2] += dD * (-(gu - p.T) * p.invR * p.invR);
+      return p.invR;
+    }
+    if (gu < p.T - p.W) return 1.f;
+    const float d = gu - p.T + p.W, k = p.invR - 1.f, h = d / (2.f * p.W);
+    acc[0] += dD * (-k * h);
+    acc[1] += dD * (k * (h - h * h));
+    acc[2] += dD * (-(d * d) / (4.f * p.W) * p.invR * p.invR);
+    return 1.f + k * h;
+  }
+  if (gu >= p.T + p.W) return 1.f;
+  if (gu < p.T - p.W) {
+    acc[0] += dD * (1.f - p.R);
+    acc[2] += dD * (gu - p.T);
+    return p.R;
+  }
+  const float d = gu - p.T - p.W, k = 1.f - p.R, h = d / (2.f * p.W);
+  acc[0] += dD * (-k * h);
+  acc[1] += dD * (k * (-h - h * h));
+  acc[2] += dD * (-(d * d) / (4.f * p.W));
+  return 1.f + k * h;
+}
+
+// Per-sample local gradient terms at kDynPerThread consecutive samples from n0.
+template <bool GATE, bool VEC>
+__device__ __forceinline__ void dyn_local(const DynBwd& d, const DynParams& p, int fe0, int fe1, int be0, int be1, int seq,
+                                          int b, long n0, float* ul, float* ur, float* dyl, float* dyr, float* gain,
+                                          float* dg, float* acc, float* dgg) {
+  load16<VEC>(d.fw, fe0, fe1, b, n0, ul, ur);
+  load16<VEC>(d.bw, be0, be1, b, n0, dyl, dyr);
+  const long L = d.fw.length;
+#pragma unroll
+  for (int k = 0; k < kDynPerThread; ++k) {
+    const long n = n0 + k;
+    dg[k] = 0.f;
+    gain[k] = 0.f;
+    if (n < 0 || n >= L) continue;
+    const float g = __ldg(d.env + static_cast<long>(seq) * L + n);
+    const float gu = logf(fmaxf(g, p.floor_));
+    float gy;
+    if (!GATE) {
+      if (gu >= p.T + p.W) gy = p.T + (gu - p.T) * p.invR;
+      else if (gu < p.T - p.W) gy = gu;
+      else { const float q = gu - p.T + p.W; gy = gu + (p.invR - 1.f) * q * q / (4.f * p.W); }
+    } else {
+      if (gu >= p.T + p.W) gy = gu;
+      else if (gu < p.T - p.W) gy = p.T + p.R * (gu - p.T);
+      else { const float q = gu - p.T - p.W; gy = gu + (1.f - p.R) * q * q / (4.f * p.W); }
+    }
+    gain[k] = expf(gy - gu);
+    const float dD = (dyl[k] * ul[k] + dyr[k] * ur[k]) * gain[k];
+    float tmp[3] = {0.f, 0.f, 0.f};
+    const float slope = knee_grad<GATE>(gu, p, dD, acc ? acc : tmp);
+    const float dgu = dD * (slope - 1.f);
+    dg[k] = g > p.floor_ ? dgu / g : 0.f;
+    if (dgg) *dgg += dg[k] * g;
+  }
+}
+
+template <bool GATE, bool VEC, int PASS>
+__global__ void __launch_bounds__(kDynThreads) dyn_bwd(DynBwd d) {
+  __shared__ DynParams s_p;
+  __shared__ DynMap wmap[kDynThreads / 32];
+  __shared__ float2 s_carry;
+  __shared__ double red[kDynThreads / 32][5];
+  const int tile = blockIdx.x, seq = blockIdx.y;
+  const int slot = seq / d.fw.batch, b = seq - slot * d.fw.batch;
+  if (threadIdx.x < 32) derive_params(d.fw.params + 4L * slot, d.env_taps, d.floor_, d.fw.length, threadIdx.x, &s_p);
+  if (PASS == 1 && threadIdx.x == 0) s_carry = d.carry[static_cast<long>(seq) * d.tiles + tile];
+  __syncthreads();
+  const DynParams p = s_p;
+  const int fe0 = __ldg(d.fw.row_ptr + slot), fe1 = __ldg(d.fw.row_ptr + slot + 1);
+  const int be0 = __ldg(d.bw.row_ptr + slot), be1 = __ldg(d.bw.row_ptr + slot + 1);
+  const long n0 = static_cast<long>(tile) * kDynTile + static_cast<long>(threadIdx.x) * kDynPerThread;
+  constexpr int K = kDynPerThread;
+  float ul[K], ur[K], dyl[K], dyr[K], gain[K], dg[K];
+  float acc[3] = {0.f, 0.f, 0.f}, dgg = 0.f;
+  dyn_local<GATE, VEC>(d, p, fe0, fe1, be0, be1, seq, b, n0, ul, ur, dyl, dyr, gain, dg, PASS ? acc : nullptr,
+                       PASS ? &dgg : nullptr);
+  // Truncation terms a^Ne dg[m+Ne] (skipped when a^Ne < 1e-30, as the forward does).
+  float ta[K], tb[K];
+  const float nb = p.aN != 0.f ? static_cast<float>(p.Ne) * p.aN / p.a : 0.f;
+#pragma unroll
+  for (int k = 0; k < K; ++k) ta[k] = tb[k] = 0.f;
+  if (p.aN != 0.f) {
+    float u2l[K], u2r[K], d2l[K], d2r[K], g2[K], dg2[K];
+    dyn_local<GATE, VEC>(d, p, fe0, fe1, be0, be1, seq, b, n0 + p.Ne, u2l, u2r, d2l, d2r, g2, dg2, nullptr, nullptr);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      ta[k] = p.aN * dg2[k];
+      tb[k] = nb * dg2[k];
+    }
+  }
+  // This thread's map over its K samples (right end -> left end), from zero state.
+  DynMap m;
+  {
+    float cw = 0.f, cv = 0.f;
+#pragma unroll
+    for (int k = K - 1; k >= 0; --k) {
+      cv = fmaf(p.a, cv, cw - tb[k]);
+      cw = fmaf(p.a, cw, dg[k] - ta[k]);
+    }
+    m.p = p.a16;  // a^K (derive_params: a16 holds a^kDynPerThread)
+    m.q = static_cast<float>(K) * p.a16 / p.a;
+    m.cw = cw;
+    m.cv = cv;
+  }
+  // Reverse inclusive scan: thread t gets F_t o F_t+1 o ... (within its warp), then warps.
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  DynMap inc = m;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const DynMap o = dmap_shfl_down(inc, off);
+    if (lane + off < 32) inc = dmap_compose(inc, o);
+  }
+  if (lane == 0) wmap[warp] = inc;
+  DynMap exc = dmap_shfl_down(inc, 1);  // F_t+1 o ... o F_(warp end)
+  if (lane == 31) exc = DynMap{1.f, 0.f, 0.f, 0.f};
+  __syncthreads();
+  if (warp == 0) {
+    constexpr int NW = kDynThreads / 32;
+    DynMap t = lane < NW ? wmap[lane] : DynMap{1.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int off = 1; off < NW; off <<= 1) {
+      const DynMap o = dmap_shfl_down(t, off);
+      if (lane + off < NW) t = dmap_compose(t, o);
+    }
+    if (lane < NW) wmap[lane] = t;  // warp w: composition of warps w .. NW-1
+  }
+  __syncthreads();
+  if constexpr (PASS == 0) {
+    if (threadIdx.x == 0) d.agg[static_cast<long>(seq) * d.tiles + tile] = make_float2(wmap[0].cw, wmap[0].cv);
+    return;
+  } else {
+    // State at this thread's right end: warps after this one, then the lanes after it.
+    float w = s_carry.x, v = s_carry.y;
+    if (warp + 1 < kDynThreads / 32) {
+      const DynMap t = wmap[warp + 1];
+      const float w2 = fmaf(t.p, w, t.cw);
+      v = fmaf(t.q, w, fmaf(t.p, v, t.cv));
+      w = w2;
+    }
+    {
+      const float w2 = fmaf(exc.p, w, exc.cw);
+      v = fmaf(exc.q, w, fmaf(exc.p, v, exc.cv));
+      w = w2;
+    }
+    double ev = 0.0;
+    float* dl = d.bw.dst + static_cast<long>(slot) * d.bw.rowstride + static_cast<long>(b) * 2 * d.bw.length;
+    float* dr = dl + d.bw.length;
+#pragma unroll
+    for (int k = K - 1; k >= 0; --k) {
+      const float vn = fmaf(p.a, v, w - tb[k]);
+      w = fmaf(p.a, w, dg[k] - ta[k]);
+      v = vn;
+      const long n = n0 + k;
+      if (n < d.fw.length) {
+        const float mid = ul[k] + ur[k];
+        const float dmid = 2.f * mid * (p.oma * w);
+        dl[n] = fmaf(gain[k], dyl[k], dmid);
+        dr[n] = fmaf(gain[k], dyr[k], dmid);
+        ev += static_cast<double>(mid * mid) * v;
+      }
+    }
+    // Block reduction of [sum dD dGy/dT, /dW, /dR, sum dg g, sum e v] in fixed order.
+    double vals[5] = {acc[0], acc[1], acc[2], dgg, ev};
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) vals[j] += __shfl_xor_sync(0xffffffffu, vals[j], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < 5; ++j) red[warp][j] = vals[j];
+    }
+    __syncthreads();
+    if (threadIdx.x < 5) {
+      double t = 0.0;
+      for (int w2 = 0; w2 < kDynThreads / 32; ++w2) t += red[w2][threadIdx.x];
+      d.partial[(static_cast<long>(seq) * d.tiles + tile) * 5 + threadIdx.x] = t;
+    }
+  }
+}
+
+// Per sequence: chain the tile maps from the last tile back (fp64), state at each tile's right end.
+__global__ void dyn_bwd_carry(DynBwd d, int nseq) {
+  const int seq = blockIdx.x * blockDim.x + threadIdx.x;
+  if (seq >= nseq) return;
+  const int slot = seq / d.fw.batch;
+  const double a = d.fw.params[4L * slot];
+  const double pT = pow(a, static_cast<double>(kDynTile));
+  const double qT = static_cast<double>(kDynTile) * pow(a, static_cast<double>(kDynTile - 1));
+  double w = 0.0, v = 0.0;
+  for (int t = d.tiles - 1; t >= 0; --t) {
+    const long i = static_cast<long>(seq) * d.tiles + t;
+    d.carry[i] = make_float2(static_cast<float>(w), static_cast<float>(v));
+    const float2 c = d.agg[i];
+    const double w2 = pT * w + c.x;
+    v = qT * w + pT * v + c.y;
+    w = w2;
+  }
+}
+
+// grid (slots) x 32: sum the partials over batch and tiles (fixed order) into the grad row.
+__global__ void dyn_bwd_reduce(DynBwd d, double* grad) {
+  const int slot = blockIdx.x;
+  const int lane = threadIdx.x;
+  double s[5] = {0, 0, 0, 0, 0};
+  const long n = static_cast<long>(d.fw.batch) * d.tiles;
+  for (long i = lane; i < n; i += 32) {
+    const double* q = d.partial + (static_cast<long>(slot) * n + i) * 5;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) s[j] += q[j];
+  }
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s[j] += __shfl_xor_sync(0xffffffffu, s[j], off);
+  }
+  if (lane != 0) return;
+  const double a = d.fw.params[4L * slot];
+  double* g = grad + 4L * slot;
+  g[0] = -s[3] / (1.0 - a) + (1.0 - a) * s[4];
+  g[1] = s[0];
+  g[2] = s[1];
+  g[3] = s[2];
+}
+
 }  // namespace
+
+std::size_t dyn_bwd_bytes(int slots, int batch, long length) {
+  const std::size_t seqs = static_cast<std::size_t>(slots) * batch;
+  const std::size_t tiles = static_cast<std::size_t>((length + kDynTile - 1) / kDynTile);
+  auto al = [](std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255); };
+  return al(sizeof(float) * seqs * length) + 2 * al(sizeof(float2) * seqs * tiles) + al(sizeof(double) * 5 * seqs * tiles) +
+         dyn_sync_bytes(slots, batch, length);
+}
+
+void launch_dynamics_backward(bool gate, const StepArgs& fw, const StepArgs& bw, int envelope_taps,
+                              double energy_floor, void* ws, double* grad, cudaStream_t s) {
+  if (fw.slots == 0 || fw.batch == 0 || fw.length == 0) return;
+  auto al = [](std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255); };
+  const int tiles = static_cast<int>((fw.length + kDynTile - 1) / kDynTile);
+  const std::size_t seqs = static_cast<std::size_t>(fw.slots) * fw.batch;
+  char* p = static_cast<char*>(ws);
+  DynBwd d;
+  d.fw = fw;
+  d.bw = bw;
+  d.env = reinterpret_cast<float*>(p);
+  p += al(sizeof(float) * seqs * fw.length);
+  d.agg = reinterpret_cast<float2*>(p);
+  p += al(sizeof(float2) * seqs * tiles);
+  d.carry = reinterpret_cast<float2*>(p);
+  p += al(sizeof(float2) * seqs * tiles);
+  d.partial = reinterpret_cast<double*>(p);
+  p += al(sizeof(double) * 5 * seqs * tiles);
+  d.env_taps = envelope_taps;
+  d.floor_ = energy_floor;
+  d.tiles = tiles;
+  // 1. Re-run the forward scan storing the envelope (outputs rewritten bit-identically).
+  cudaMemsetAsync(p, 0, dyn_sync_bytes(fw.slots, fw.batch, fw.length), s);
+  auto* ticket = reinterpret_cast<unsigned int*>(p);
+  auto* status = reinterpret_cast<unsigned long long*>(p + 256);
+  const long ne = envelope_taps < fw.length ? envelope_taps : fw.length;
+  const bool vec = (fw.length % 4 == 0) && (ne % 4 == 0);
+  const dim3 fgrid(static_cast<unsigned>(seqs * tiles));
+  float* env = const_cast<float*>(d.env);
+  const dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(seqs));
+#define MGB_DYN_BWD(G, V)                                                                                  \
+  dyn_scan<G, V, true><<<fgrid, kDynThreads, 0, s>>>(fw, envelope_taps, energy_floor, tiles, status, ticket, env); \
+  dyn_bwd<G, V, 0><<<grid, kDynThreads, 0, s>>>(d);                                                        \
+  dyn_bwd_carry<<<static_cast<unsigned>((seqs + 127) / 128), 128, 0, s>>>(d, static_cast<int>(seqs));        \
+  dyn_bwd<G, V, 1><<<grid, kDynThreads, 0, s>>>(d);
+  if (gate) {
+    if (vec) { MGB_DYN_BWD(true, true) } else { MGB_DYN_BWD(true, false) }
+  } else {
+    if (vec) { MGB_DYN_BWD(false, true) } else { MGB_DYN_BWD(false, false) }
+  }
+#undef MGB_DYN_BWD
+  dyn_bwd_reduce<<<fw.slots, 32, 0, s>>>(d, grad);
+}
 
 std::size_t dyn_sync_bytes(int slots, int batch, long length) {
   const long tiles = (length + kDynTile - 1) / kDynTile;

@@ -320,6 +320,30 @@ void DevicePlan::build_index() {
     }
     for (int r = st.store_begin; r < st.store_end; ++r) written[static_cast<std::size_t>(r)] = 1;
   }
+  // Transposed table: consumers of each row over the edges whose source the forward read
+  // after it was written (a row read before its step ran contributed silence).
+  std::vector<std::vector<int>> cons(static_cast<std::size_t>(rd_.buffer_rows));
+  std::vector<char> done(static_cast<std::size_t>(rd_.buffer_rows), 0);
+  for (int r = 0; r < rd_.num_inputs && r < rd_.buffer_rows; ++r) done[static_cast<std::size_t>(r)] = 1;
+  for (const StepIndex& st : rd_.steps) {
+    for (std::size_t e = 0; e < st.gather.size(); ++e) {
+      const int g = st.gather[e];
+      if (done[static_cast<std::size_t>(g)]) cons[static_cast<std::size_t>(g)].push_back(st.store_begin + st.aggregate[e]);
+    }
+    for (int r = st.store_begin; r < st.store_end; ++r) done[static_cast<std::size_t>(r)] = 1;
+  }
+  auto emit = [&](int r0, int r1) {
+    trp_off_.push_back(static_cast<long>(host.size()));
+    int n = 0;
+    for (int r = r0; r <= r1; ++r) {
+      host.push_back(n);
+      if (r < r1) n += static_cast<int>(cons[static_cast<std::size_t>(r)].size());
+    }
+    tcol_off_.push_back(static_cast<long>(host.size()));
+    for (int r = r0; r < r1; ++r) host.insert(host.end(), cons[static_cast<std::size_t>(r)].begin(), cons[static_cast<std::size_t>(r)].end());
+  };
+  for (const StepIndex& st : rd_.steps) emit(st.store_begin, st.store_end);
+  emit(0, rd_.num_inputs);
 }
 
 DevicePlan::DevicePlan(const RenderData& rd) : rd_(rd) {
@@ -356,6 +380,8 @@ DevicePlan::~DevicePlan() {
 
 const int* DevicePlan::row_ptr(int step) const { return d_index_ + rp_off_[static_cast<std::size_t>(step)]; }
 const int* DevicePlan::col(int step) const { return d_index_ + col_off_[static_cast<std::size_t>(step)]; }
+const int* DevicePlan::t_row_ptr(int step) const { return d_index_ + trp_off_[static_cast<std::size_t>(step)]; }
+const int* DevicePlan::t_col(int step) const { return d_index_ + tcol_off_[static_cast<std::size_t>(step)]; }
 
 DevicePlan::Layout DevicePlan::layout(int batch, long length, const ProcessorSet& procs) const {
   Layout l;
@@ -379,6 +405,31 @@ DevicePlan::Layout DevicePlan::layout(int batch, long length, const ProcessorSet
 
 std::size_t DevicePlan::workspace_bytes(int batch, long length, const ProcessorSet& procs) const {
   return layout(batch, length, procs).total;
+}
+
+namespace {
+std::size_t bwd_step_bytes(NodeType t, int slots, int batch, long length, const ProcessorSet& p) {
+  switch (t) {
+    case NodeType::Gain:
+    case NodeType::Imager: return mgb::pw_grad_bytes(slots, batch, length);
+    case NodeType::Eq: return mgb::eq_grad_bytes(slots, batch, length);
+    case NodeType::Compressor:
+    case NodeType::Noisegate: return mgb::dyn_bwd_bytes(slots, batch, length);
+    case NodeType::Reverb:
+      return mgb::conv_bwd_bytes(mgb::conv_geom(length, p.reverb_length()), slots, batch, p.reverb_length(), p.device().frames);
+    case NodeType::Delay:
+      return mgb::conv_bwd_bytes(mgb::conv_geom(length, p.delay_span()), slots, batch, p.delay_span(), p.device().frames);
+    default: return 0;
+  }
+}
+}  // namespace
+
+std::size_t DevicePlan::backward_workspace_bytes(int batch, long length, const ProcessorSet& procs) const {
+  std::size_t extra = 256;
+  for (const StepIndex& st : rd_.steps) {
+    extra = std::max(extra, bwd_step_bytes(st.type, st.store_end - st.store_begin, batch, length, procs));
+  }
+  return layout(batch, length, procs).total + align256(extra);
 }
 
 int DevicePlan::kernels_per_render(int batch, long length) const {
@@ -488,6 +539,90 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
     if (step_events) cuda_check(cudaEventRecord(step_events[2 * k + 1], stream), "event");
   }
   cuda_check(cudaGetLastError(), "render_arena launch");
+}
+
+// ---- backward pass ---------------------------------------------------------------------------
+
+void backward_arena(const DevicePlan& plan, const ProcessorSet& procs, const double* const* param_tables,
+                    const float* arena, float* adjoint, double* const* grad_tables, int batch, long length,
+                    void* workspace, std::size_t workspace_bytes, cudaStream_t stream) {
+  const RenderData& rd = plan.data();
+  const DevicePlan::Layout lay = plan.layout(batch, length, procs);
+  if (workspace_bytes < plan.backward_workspace_bytes(batch, length, procs)) fail("backward: workspace too small");
+  char* ws = static_cast<char*>(workspace);
+  char* scratch = ws + lay.total;
+  const long rowstride = static_cast<long>(batch) * 2 * length;
+  const float2* tw = mgb::twiddle_table(procs.device().device);
+  const int nsteps = static_cast<int>(rd.steps.size());
+  for (int k = nsteps - 1; k >= 0; --k) {
+    const StepIndex& st = rd.steps[static_cast<std::size_t>(k)];
+    const NodeType t = st.type;
+    if (t == NodeType::Out || t == NodeType::In) continue;  // out rows hold dL/dY on entry
+    const int width = param_width(t);
+    mgb::StepArgs fw{};
+    fw.src = arena;
+    fw.dst = const_cast<float*>(arena) + st.store_begin * rowstride;
+    fw.row_ptr = plan.row_ptr(k);
+    fw.col = plan.col(k);
+    fw.params = nullptr;
+    double* grad = nullptr;
+    if (width > 0) {
+      const double* table = param_tables ? param_tables[static_cast<int>(t)] : nullptr;
+      if (!table) fail("backward: missing parameter table for " + tname(t));
+      if (!grad_tables || !grad_tables[static_cast<int>(t)]) fail("backward: missing gradient table for " + tname(t));
+      fw.params = table + static_cast<long>(st.param_begin) * width;
+      grad = grad_tables[static_cast<int>(t)] + static_cast<long>(st.param_begin) * width;
+    }
+    fw.tw = tw;
+    fw.slots = st.store_end - st.store_begin;
+    fw.batch = batch;
+    fw.length = length;
+    fw.rowstride = rowstride;
+    mgb::StepArgs bw = fw;
+    bw.src = adjoint;
+    bw.dst = adjoint + st.store_begin * rowstride;
+    bw.row_ptr = plan.t_row_ptr(k);
+    bw.col = plan.t_col(k);
+    char* pws = ws + lay.prologue_off[static_cast<std::size_t>(k)];
+    switch (t) {
+      case NodeType::Mix: mgb::launch_pointwise(mgb::PointOp::Copy, bw, stream); break;
+      case NodeType::Gain:
+      case NodeType::Imager:
+        mgb::launch_pointwise(point_op(t), bw, stream);
+        mgb::launch_pointwise_param_grad(point_op(t), fw, bw, scratch, grad, stream);
+        break;
+      case NodeType::Eq:
+        mgb::launch_eq_main(bw, reinterpret_cast<float*>(pws + eq_taps_bytes(fw.slots)), stream);
+        mgb::launch_eq_param_grad(fw, bw, scratch, grad, stream);
+        break;
+      case NodeType::Compressor:
+      case NodeType::Noisegate:
+        mgb::launch_dynamics_backward(t == NodeType::Noisegate, fw, bw, procs.config().envelope_taps,
+                                      procs.config().energy_floor, scratch, grad, stream);
+        break;
+      case NodeType::Reverb:
+      case NodeType::Delay:
+        mgb::launch_conv_backward(t == NodeType::Reverb, fw, bw, reverb_const(procs), delay_const(procs), pws, scratch,
+                                  grad, stream);
+        break;
+      default: break;
+    }
+  }
+  // Sources: dL/d(source) = sum over the source's consumers.
+  if (rd.num_inputs > 0) {
+    mgb::StepArgs bw{};
+    bw.src = adjoint;
+    bw.dst = adjoint;
+    bw.row_ptr = plan.t_row_ptr(nsteps);
+    bw.col = plan.t_col(nsteps);
+    bw.tw = tw;
+    bw.slots = rd.num_inputs;
+    bw.batch = batch;
+    bw.length = length;
+    bw.rowstride = rowstride;
+    mgb::launch_pointwise(mgb::PointOp::Copy, bw, stream);
+  }
+  cuda_check(cudaGetLastError(), "backward launch");
 }
 
 // ---- per-step micro-benchmark ---------------------------------------------------------------

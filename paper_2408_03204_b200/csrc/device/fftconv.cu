@@ -230,7 +230,9 @@ __global__ void __launch_bounds__(row_threads<LN2, kSpecRows>()) rows_spec(int l
 
 // Signal rows k1 = r and N1 - r together: forward FFTs, channel-split product with the
 // kernel spectrum, inverse FFTs, inverse four-step twiddle. grid (N1/2 + 1, slots*B)
-template <int LN2>
+// CONJ: multiply by conj(H_c) instead (the adjoint, a correlation with the kernel: swapping
+// the paired kernel values P[k] <-> P[N-k] conjugates both channels' kernel spectra).
+template <int LN2, bool CONJ = false>
 __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2, 2>()) rows_conv(int log_n, int batch, float2* X, const float2* P, const float2* tw) {
   constexpr int N2 = 1 << LN2;
   constexpr int NT = row_threads<LN2, 2>();
@@ -284,7 +286,7 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2,
     const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
     if (self && kb < k) continue;
     const float2 xk = rows[sidx(k)], xo = rows[RS + sidx(kb)];
-    const float2 pk = pkv[q], po = pov[q];
+    const float2 pk = CONJ ? pov[q] : pkv[q], po = CONJ ? pkv[q] : pov[q];
     const float2 zk = zmix(xk, cconj(xo), pk, cconj(po), s);
     const float2 zo = zmix(xo, cconj(xk), po, cconj(pk), s);
     rows[sidx(k)] = zk;
@@ -365,16 +367,19 @@ void rows_spec_t(const ConvGeom& g, int slots, float2* P, const float2* tw, cuda
 
 template <int LN2>
 void rows_conv_t(const ConvGeom& g, int items, int batch, float2* X, const float2* P, const float2* tw,
-                 cudaStream_t s) {
+                 cudaStream_t s, bool conj = false) {
   constexpr int smem = 2 * padded(1 << LN2) * 8;
   static const bool done = [] {
     cudaFuncSetAttribute(rows_conv<LN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(rows_conv<LN2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return true;
   }();
   (void)done;
   const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(items));
-  rows_conv<LN2><<<grid, row_threads<LN2, 2>(), smem, s>>>(g.log_n, batch, X, P, tw);
+  if (conj) rows_conv<LN2, true><<<grid, row_threads<LN2, 2>(), smem, s>>>(g.log_n, batch, X, P, tw);
+  else rows_conv<LN2><<<grid, row_threads<LN2, 2>(), smem, s>>>(g.log_n, batch, X, P, tw);
 }
+
 
 #define MGB_DISPATCH_LN(var, FN, ...)                  \
   switch (var) {                                       \
@@ -549,6 +554,226 @@ __global__ void __launch_bounds__(256) delay_dense(const float* taps, DelayConst
   reinterpret_cast<float*>(ir + static_cast<long>(slot) * ir_stride + i)[c] = acc;
 }
 
+// ---- backward (adjoint) kernels -------------------------------------------------------------
+
+// Correlation spectrum of the step's output gradient with its input, summed over the batch:
+// per channel C_c = DY_c conj(X_c), packed C_L + i C_R (both correlations are real). DY and X
+// hold column-stage spectra of the packed signals; conj(X_c) is the spectrum of x_c reversed,
+// whose packed form is Z[N-k], so this is rows_conv's product with the pair swapped. The
+// result (row stage done, inverse twiddled) goes to X's b = 0 item. grid (N1/2 + 1, slots)
+template <int LN2>
+__global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_corr(int log_n, int batch, const float2* DY, float2* X,
+                                                               const float2* tw) {
+  constexpr int N2 = 1 << LN2;
+  constexpr int NT = row_threads<LN2, 4>();
+  constexpr int RS = padded(N2);
+  extern __shared__ float2 rows[];  // [4][RS]: dy a, dy b, x a, x b
+  const long N = 1L << log_n;
+  const int N1 = static_cast<int>(N >> LN2);
+  const int slot = blockIdx.y;
+  const int ra = blockIdx.x, rb = (N1 - ra) & (N1 - 1);
+  const bool self = ra == rb;
+  constexpr int KPT = (N2 + NT - 1) / NT;
+  float2 acck[KPT], acco[KPT];
+#pragma unroll
+  for (int q = 0; q < KPT; ++q) acck[q] = acco[q] = make_float2(0.f, 0.f);
+  const float s = 0.25f / static_cast<float>(N);
+  for (int b = 0; b < batch; ++b) {
+    const long item = static_cast<long>(slot) * batch + b;
+    const float2* da = DY + item * N + static_cast<long>(ra) * N2;
+    const float2* db = DY + item * N + static_cast<long>(rb) * N2;
+    const float2* xa = X + item * N + static_cast<long>(ra) * N2;
+    const float2* xb = X + item * N + static_cast<long>(rb) * N2;
+    for (int i = threadIdx.x; i < N2; i += NT) {
+      rows[sidx(i)] = da[i];
+      rows[RS + sidx(i)] = db[i];
+      rows[2 * RS + sidx(i)] = xa[i];
+      rows[3 * RS + sidx(i)] = xb[i];
+    }
+    __syncthreads();
+    fft_pow2<LN2, 4, NT, -1>(rows, RS, tw);
+#pragma unroll
+    for (int q = 0; q < KPT; ++q) {
+      const int k = threadIdx.x + q * NT;
+      if (k >= N2) continue;
+      const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
+      if (self && kb < k) continue;
+      const float2 dk = rows[sidx(k)], dn = rows[RS + sidx(kb)];
+      const float2 zk = rows[2 * RS + sidx(k)], zn = rows[3 * RS + sidx(kb)];
+      acck[q] = cadd(acck[q], zmix(dk, cconj(dn), zn, cconj(zk), s));
+      acco[q] = cadd(acco[q], zmix(dn, cconj(dk), zk, cconj(zn), s));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < KPT; ++q) {
+    const int k = threadIdx.x + q * NT;
+    if (k >= N2) continue;
+    const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
+    if (self && kb < k) continue;
+    rows[sidx(k)] = acck[q];
+    if (self) rows[sidx(kb)] = acco[q];
+    else rows[RS + sidx(kb)] = acco[q];
+  }
+  __syncthreads();
+  fft_pow2<LN2, 2, NT, +1>(rows, RS, tw);
+  const float inv_n = 2.f / static_cast<float>(N);
+  float2* oa = X + static_cast<long>(slot) * batch * N + static_cast<long>(ra) * N2;
+  float2* ob = X + static_cast<long>(slot) * batch * N + static_cast<long>(rb) * N2;
+  for (int i = threadIdx.x; i < N2; i += NT) {
+    oa[i] = cmul(rows[sidx(i)], expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n));
+    if (!self) ob[i] = cmul(rows[RS + sidx(i)], expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n));
+  }
+}
+
+// Inverse column FFTs of slot items (X at item slot*batch) into a packed kernel-gradient
+// buffer out[slot][taps] (x = left, y = right), first `taps` samples. grid (N2 / C, slots)
+template <int LN1>
+__global__ void __launch_bounds__(kColThreads, 2) cols_inv_buf(int log_n, int batch, const float2* X, float2* out,
+                                                            long taps, const float2* tw) {
+  constexpr int N1 = 1 << LN1;
+  constexpr int C = kColElems / N1;
+  constexpr int FS = padded(N1) + 1;
+  extern __shared__ float2 tile[];
+  const long N2 = 1L << (log_n - LN1);
+  const long N = 1L << log_n;
+  const int slot = blockIdx.y;
+  const long col0 = static_cast<long>(blockIdx.x) * C;
+  const float2* x = X + static_cast<long>(slot) * batch * N;
+  for (int idx = threadIdx.x; idx < kColElems; idx += kColThreads) {
+    tile[(idx % C) * FS + sidx(idx / C)] = __ldg(x + static_cast<long>(idx / C) * N2 + col0 + idx % C);
+  }
+  __syncthreads();
+  fft_pow2<LN1, C, kColThreads, +1>(tile, FS, tw);
+  for (int idx = threadIdx.x; idx < kColElems; idx += kColThreads) {
+    const int c = idx % C, n1 = idx / C;
+    const long n = static_cast<long>(n1) * N2 + col0 + c;
+    if (n < taps) out[static_cast<long>(slot) * taps + n] = tile[c * FS + sidx(n1)];
+  }
+}
+
+// Reverb impulse-response adjoint (istft `dsp.cpp:165-190`, reverb_kernel
+// `processors.cpp:162-187`): per frame m the time gradient of the masked frame is
+// d fr[i] = dM[m hop + i] / (384 cover) (mid; side likewise, dM = (dL + dR)/2,
+// dS = (dL - dR)/2), its forward 384-point FFT DFR gives the mask gradient
+// d a[m][k] = c_k Re(N[m][k] conj(DFR[k])) (c_k = 1 for k = 0, 192, else 2), and
+// a = exp(H0[p] + m Hd[p]), p = min(k, 191). Mid and side packed as one complex FFT.
+// grid (ceil(frames / kRevFpc), slots); out partial[slot][blk][2 which][2][193] fp64.
+__global__ void __launch_bounds__(kRevThreads) reverb_ir_adjoint(const double* params, ReverbConst rc, const float2* dh,
+                                                                double* partial) {
+  extern __shared__ float2 fr[];  // [kRevFpc][kRevFS]
+  __shared__ float2 tw384[384];
+  __shared__ float2 inv_cover[192];
+  const int slot = blockIdx.y;
+  const int m0 = blockIdx.x * kRevFpc;
+  for (int k = threadIdx.x; k < 384; k += kRevThreads) {
+    tw384[k] = __ldg(tw384_table(rc.consts) + k);
+    if (k < 192) inv_cover[k] = __ldg(cover_table(rc.consts) + k);
+  }
+  __syncthreads();
+  const float2* h = dh + static_cast<long>(slot) * rc.length;
+  for (int t = threadIdx.x; t < kRevFpc * 384; t += kRevThreads) {
+    const int f = t / 384, i = t - f * 384;
+    const int m = m0 + f;
+    const long idx = static_cast<long>(m) * 192 + i;
+    float2 z = make_float2(0.f, 0.f);
+    if (m < rc.frames && idx < rc.length) {
+      const float2 g = __ldg(h + idx);
+      const float sc = idx < 192 ? inv_cover[idx].x : inv_cover[idx % 192].y;
+      z = make_float2(0.5f * (g.x + g.y) * sc, 0.5f * (g.x - g.y) * sc);
+    }
+    fr[f * kRevFS + sidx(i)] = z;
+  }
+  __syncthreads();
+  fft_384<kRevFpc, kRevThreads, -1>(fr, kRevFS, tw384);
+  const double* row = params + static_cast<long>(slot) * 4 * kRevParamBins;
+  double* out = partial + (static_cast<long>(slot) * gridDim.x + blockIdx.x) * (4 * kRevBins);
+  for (int item = threadIdx.x; item < 2 * kRevBins; item += kRevThreads) {
+    const int which = item / kRevBins, k = item - which * kRevBins;
+    const int bin = k < kRevParamBins ? k : kRevParamBins - 1;
+    const double* color = row + which * 2 * kRevParamBins;
+    const double c0 = color[bin], dec = color[kRevParamBins + bin];
+    const float2* noise = which == 0 ? rc.stft_mid : rc.stft_side;
+    const float ck = (k == 0 || k == 192) ? 1.f : 2.f;
+    double g0 = 0.0, g1 = 0.0;
+    for (int f = 0; f < kRevFpc; ++f) {
+      const int m = m0 + f;
+      if (m >= rc.frames) break;
+      const float2 zk = fr[f * kRevFS + sidx(k)], zn = fr[f * kRevFS + sidx((384 - k) % 384)];
+      // DFR_M = (Zk + conj Zn)/2, DFR_S = (Zk - conj Zn)/(2i)
+      float2 d;
+      if (which == 0) d = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
+      else d = make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x));
+      const float2 nz = __ldg(noise + static_cast<long>(m) * kRevBins + k);
+      const float da = ck * (nz.x * d.x + nz.y * d.y);
+      const float a = expf(static_cast<float>(c0 + m * dec));
+      g0 += static_cast<double>(da * a);
+      g1 += static_cast<double>(m) * static_cast<double>(da * a);
+    }
+    out[which * 2 * kRevBins + k] = g0;
+    out[which * 2 * kRevBins + kRevBins + k] = g1;
+  }
+}
+
+// grid (slots) x 128: grad row [which][color 192 | decay 192]; bin 192 folds into param 191.
+__global__ void reverb_grad_reduce(const double* partial, int blocks, double* grad) {
+  const int slot = blockIdx.x;
+  for (int item = threadIdx.x; item < 4 * kRevParamBins; item += blockDim.x) {
+    const int which = item / (2 * kRevParamBins), r = item - which * 2 * kRevParamBins;
+    const int kind = r / kRevParamBins, p = r - kind * kRevParamBins;
+    double t = 0.0;
+    for (int bk = 0; bk < blocks; ++bk) {
+      const double* q = partial + (static_cast<long>(slot) * blocks + bk) * (4 * kRevBins) + which * 2 * kRevBins + kind * kRevBins;
+      t += q[p];
+      if (p == kRevParamBins - 1) t += q[kRevBins - 1];
+    }
+    grad[static_cast<long>(slot) * 4 * kRevParamBins + item] = t;
+  }
+}
+
+// Multitap delay adjoint (delay_kernel `processors.cpp:210-227`, zero_phase_fir N = 39):
+// the kernel gradient at the tap's 39 positions d - 19 + j is the FIR gradient; through the
+// design, d lm[q] = (m_q / 39) e^{lm[q]} sum_j dfir[j] hann[j] cos(2 pi q (j - 19) / 39).
+// Positions are piecewise constant in (Re z, Im z) (lround of the angle): gradient 0, as is
+// every gradient of a disabled tap. grid (kTaps, slots) x 64.
+__global__ void __launch_bounds__(64) delay_taps_adjoint(const double* params, const float* taps, const float2* dh,
+                                                         long span, double* grad) {
+  __shared__ double wd[kFir];
+  const int tapi = blockIdx.x, slot = blockIdx.y, t = threadIdx.x;
+  const float* rec = taps + (static_cast<long>(slot) * kTaps + tapi) * kTapRec;
+  const int d = __float_as_int(rec[0]);
+  const double* row = params + static_cast<long>(slot) * kTaps * kTapStride + tapi * kTapStride;
+  double* g = grad + static_cast<long>(slot) * kTaps * kTapStride + tapi * kTapStride;
+  if (d < 0) {
+    if (t < kTapStride) g[t] = 0.0;
+    return;
+  }
+  const int c = tapi / 20;
+  if (t < kFir) {
+    const long idx = static_cast<long>(d) - kFirHalf + t;
+    double v = 0.0;
+    if (idx >= 0 && idx < span) {
+      const float2 q = __ldg(dh + static_cast<long>(slot) * span + idx);
+      v = c == 0 ? q.x : q.y;
+    }
+    double s, co;
+    sincospi(2.0 * t / (kFir - 1), &s, &co);
+    wd[t] = v * (0.5 - 0.5 * co);
+  }
+  __syncthreads();
+  if (t < 20) {
+    double acc = 0.0;
+    for (int j = 0; j < kFir; ++j) {
+      double s, co;
+      sincospi(2.0 * t * (j - kFirHalf) / kFir, &s, &co);
+      acc = fma(wd[j], co, acc);
+    }
+    g[2 + t] = (t == 0 ? 1.0 : 2.0) / kFir * exp(row[2 + t]) * acc;
+  } else if (t < 22) {
+    g[t - 20] = 0.0;
+  }
+}
+
 // ---- noise STFT (ProcessorSet construction) ---------------------------------------------------
 // grid (frames): one frame per CTA, fp64 direct DFT of the periodic-Hann windowed frame.
 __global__ void __launch_bounds__(256) noise_stft(const double* noise, long length, float2* out) {
@@ -673,6 +898,78 @@ void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, voi
   MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, a, nullptr, 0, g, items, X, 0, s);
   MGB_DISPATCH_LN(g.log_n2, rows_conv_t, g, items, a.batch, X, P, a.tw, s);
   MGB_DISPATCH_LN(g.log_n1, cols_inv_t, a, g, X, s);
+}
+
+
+namespace {
+template <int LN2>
+void rows_corr_t(const ConvGeom& g, int slots, int batch, const float2* DY, float2* X, const float2* tw, cudaStream_t s) {
+  constexpr int smem = 4 * padded(1 << LN2) * 8;
+  static const bool done = [] {
+    cudaFuncSetAttribute(rows_corr<LN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    return true;
+  }();
+  (void)done;
+  const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(slots));
+  rows_corr<LN2><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, batch, DY, X, tw);
+}
+
+template <int LN1>
+void cols_inv_buf_t(const ConvGeom& g, int slots, int batch, const float2* X, float2* out, long taps, const float2* tw,
+                    cudaStream_t s) {
+  constexpr int C = kColElems / (1 << LN1);
+  constexpr int smem = C * (padded(1 << LN1) + 1) * 8;
+  static const bool done = [] {
+    cudaFuncSetAttribute(cols_inv_buf<LN1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    return true;
+  }();
+  (void)done;
+  const dim3 grid(static_cast<unsigned>((1L << g.log_n2) / C), static_cast<unsigned>(slots));
+  cols_inv_buf<LN1><<<grid, kColThreads, smem, s>>>(g.log_n, batch, X, out, taps, tw);
+}
+}  // namespace
+
+std::size_t conv_bwd_bytes(const ConvGeom& g, int slots, int batch, long taps, int rev_frames) {
+  const std::size_t spec = align256(sizeof(float2) * static_cast<std::size_t>(slots) * batch * g.n);
+  const std::size_t blocks = static_cast<std::size_t>((rev_frames + kRevFpc - 1) / kRevFpc);
+  return 2 * spec + align256(sizeof(float2) * static_cast<std::size_t>(slots) * taps) +
+         align256(sizeof(double) * static_cast<std::size_t>(slots) * blocks * 4 * kRevBins);
+}
+
+void launch_conv_backward(bool reverb, const StepArgs& fw, const StepArgs& bw, const ReverbConst& rc,
+                          const DelayConst& dc, const void* prologue_ws, void* ws, double* grad, cudaStream_t s) {
+  if (fw.slots == 0 || fw.batch == 0 || fw.length == 0) return;
+  const long taps = reverb ? rc.length : dc.span;
+  const ConvGeom g = conv_geom(fw.length, taps);
+  const auto* P = reinterpret_cast<const float2*>(static_cast<const char*>(prologue_ws) + ir_bytes(fw.slots, taps));
+  const int items = fw.slots * fw.batch;
+  const std::size_t spec = align256(sizeof(float2) * static_cast<std::size_t>(items) * g.n);
+  auto* DY = static_cast<float2*>(ws);
+  auto* X = reinterpret_cast<float2*>(static_cast<char*>(ws) + spec);
+  auto* dh = reinterpret_cast<float2*>(static_cast<char*>(ws) + 2 * spec);
+  auto* part = reinterpret_cast<double*>(static_cast<char*>(ws) + 2 * spec +
+                                         align256(sizeof(float2) * static_cast<std::size_t>(fw.slots) * taps));
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, bw, nullptr, 0, g, items, DY, 0, s);
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, fw, nullptr, 0, g, items, X, 0, s);
+  MGB_DISPATCH_LN(g.log_n2, rows_corr_t, g, fw.slots, fw.batch, DY, X, fw.tw, s);
+  MGB_DISPATCH_LN(g.log_n2, rows_conv_t, g, items, fw.batch, DY, P, fw.tw, s, true);
+  MGB_DISPATCH_LN(g.log_n1, cols_inv_t, bw, g, DY, s);
+  MGB_DISPATCH_LN(g.log_n1, cols_inv_buf_t, g, fw.slots, fw.batch, X, dh, taps, fw.tw, s);
+  if (reverb) {
+    const int blocks = (rc.frames + kRevFpc - 1) / kRevFpc;
+    static const bool done = [] {
+      cudaFuncSetAttribute(reverb_ir_adjoint, cudaFuncAttributeMaxDynamicSharedMemorySize, kRevFpc * kRevFS * 8);
+      return true;
+    }();
+    (void)done;
+    reverb_ir_adjoint<<<dim3(static_cast<unsigned>(blocks), static_cast<unsigned>(fw.slots)), kRevThreads,
+                        kRevFpc * kRevFS * 8, s>>>(fw.params, rc, dh, part);
+    reverb_grad_reduce<<<fw.slots, 128, 0, s>>>(part, blocks, grad);
+  } else {
+    const auto* ir = static_cast<const float2*>(prologue_ws);
+    const auto* rec = reinterpret_cast<const float*>(ir + static_cast<long>(fw.slots) * taps);
+    delay_taps_adjoint<<<dim3(kTaps, fw.slots), 64, 0, s>>>(fw.params, rec, dh, dc.span, grad);
+  }
 }
 
 void launch_noise_stft(const double* noise, long length, int frames, float2* out, cudaStream_t s) {

@@ -51,6 +51,13 @@ std::size_t dyn_sync_bytes(int slots, int batch, long length);
 void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double energy_floor, void* sync,
                      bool zero_sync, cudaStream_t s);
 
+// Backward of a compressor / noisegate step: `bw` gathers dy over the consumers' input
+// gradients (transposed CSR) and stores du into bw.dst; parameter gradients [slots][4] fp64
+// into `grad`. ws: dyn_bwd_bytes.
+std::size_t dyn_bwd_bytes(int slots, int batch, long length);
+void launch_dynamics_backward(bool gate, const StepArgs& fw, const StepArgs& bw, int envelope_taps,
+                              double energy_floor, void* ws, double* grad, cudaStream_t s);
+
 // FFT convolution with a long causal kernel (reverb, delay): four-step FFT of size N.
 struct ConvGeom {
   int log_n = 0, log_n1 = 0, log_n2 = 0;
@@ -78,6 +85,20 @@ std::size_t conv_main_bytes(const ConvGeom& g, int slots, int batch);
 void launch_conv_prologue(bool reverb, const StepArgs& a, const ReverbConst& rc, const DelayConst& dc, void* ws,
                           cudaStream_t s);
 void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, void* ws, cudaStream_t s);
+
+// Backward of a reverb / delay step: dX = correlation with the kernel (stored into bw.dst),
+// kernel gradient = correlation of dY with X, then through the IR build / tap FIRs into
+// `grad` ([slots][768] / [slots][880] fp64). prologue_ws: the forward's prologue region.
+std::size_t conv_bwd_bytes(const ConvGeom& g, int slots, int batch, long taps, int rev_frames);
+void launch_conv_backward(bool reverb, const StepArgs& fw, const StepArgs& bw, const ReverbConst& rc,
+                          const DelayConst& dc, const void* prologue_ws, void* ws, double* grad, cudaStream_t s);
+
+// Pointwise (gain / imager) parameter gradients and the EQ correlation + FIR adjoint.
+std::size_t pw_grad_bytes(int slots, int batch, long length);
+void launch_pointwise_param_grad(PointOp op, const StepArgs& fw, const StepArgs& bw, void* ws, double* grad,
+                                 cudaStream_t s);
+std::size_t eq_grad_bytes(int slots, int batch, long length);
+void launch_eq_param_grad(const StepArgs& fw, const StepArgs& bw, void* ws, double* grad, cudaStream_t s);
 
 // Kernel-only entry points (for ProcessorSet::reverb_kernel / delay_kernel).
 void launch_reverb_ir(const double* params, int slots, const ReverbConst& rc, float2* ir, long ir_stride,

@@ -137,8 +137,15 @@ class DevicePlan {
   const RenderData& data() const { return rd_; }
   const int* row_ptr(int step) const;
   const int* col(int step) const;
+  // Transposed step table (backward pass): for the nodes of step k, the rows of their
+  // consumers, one entry per edge, in (step, slot, edge) order; step num_steps = the sources.
+  // Edges whose source row the forward read as silence (one-by-one quirk) are left out.
+  const int* t_row_ptr(int step) const;
+  const int* t_col(int step) const;
   const std::vector<int>& zero_rows() const { return zero_rows_; }
   std::size_t workspace_bytes(int batch, long length, const ProcessorSet& procs) const;
+  // Workspace for a forward render followed by backward_arena (forward layout + scratch).
+  std::size_t backward_workspace_bytes(int batch, long length, const ProcessorSet& procs) const;
   int kernels_per_render(int batch, long length) const;
 
   // Workspace: one persistent region per step for its parameter-only prologue, the steps'
@@ -163,9 +170,21 @@ class DevicePlan {
   const cudaEvent_t* borrowed_events_ = nullptr;
   const int* d_index_ = nullptr;
   std::vector<int> host_;
-  std::vector<long> rp_off_, col_off_;
+  std::vector<long> rp_off_, col_off_, trp_off_, tcol_off_;
   std::vector<int> zero_rows_;
 };
+
+// Reverse-mode pass over a rendered arena (parameter gradients; the reference has no
+// autodiff, its fit.cpp:70-82 uses central differences). `arena` and `workspace` must be
+// those of the render_arena call that produced the forward (its prologue results are reused;
+// workspace_bytes >= backward_workspace_bytes). `adjoint` ([rows][batch][2][length] fp32):
+// on entry rows [output_begin, rows) hold dL/d(outputs); on exit row r holds dL/d(input of
+// node r) — rows [0, num_inputs) are dL/d(sources). grad_tables[t]: device fp64 tables shaped
+// like param_tables[t] (render order), overwritten with dL/d(params). Delay tap positions
+// (Re z, Im z) are piecewise constant in the forward: their gradient is 0.
+void backward_arena(const DevicePlan& plan, const ProcessorSet& processors, const double* const* param_tables,
+                    const float* arena, float* adjoint, double* const* grad_tables, int batch, long length,
+                    void* workspace, std::size_t workspace_bytes, cudaStream_t stream);
 
 // Per-step device time (prologue + audio pass of step k, ms) from `reps` back-to-back
 // repetitions between one CUDA event pair on `stream` (after one full render). Diagnostic.

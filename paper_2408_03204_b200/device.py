@@ -21,10 +21,12 @@ from . import NUM_NODE_TYPES, ProcessorSet, RenderData, _check, _lib, _u64, _vp,
 class DeviceRenderer:
     def __init__(self, rd: RenderData, procs: ProcessorSet, batch: int, length: int,
                  params: Optional[Dict[int, np.ndarray]] = None, device: Optional[torch.device] = None,
-                 arena_pool: Optional[torch.Tensor] = None, workspace_pool: Optional[torch.Tensor] = None):
+                 arena_pool: Optional[torch.Tensor] = None, workspace_pool: Optional[torch.Tensor] = None,
+                 backward: bool = False):
         """`arena_pool` (fp32) / `workspace_pool` (uint8): optional preallocated device buffers
         at least as large as this plan needs, reused across plans whose topology changes every
-        step (no per-plan allocation). The arena view is NOT zeroed in that case."""
+        step (no per-plan allocation). The arena view is NOT zeroed in that case.
+        `backward`: size the workspace for backward() after render()."""
         if not torch.cuda.is_available():
             raise RuntimeError("DeviceRenderer needs a CUDA device (there is no CPU fallback)")
         self.rd, self.procs = rd, procs
@@ -39,7 +41,9 @@ class DeviceRenderer:
                 raise ValueError(f"DeviceRenderer: arena_pool must be float32 with >= {need} elements")
             self.arena = arena_pool.reshape(-1)[:need].view(shape)
         ws = _u64()
-        _check(_lib.mg_plan_workspace_bytes(rd.handle, procs.handle, self.batch, self.length, ctypes.byref(ws)))
+        fn = _lib.mg_backward_workspace_bytes if backward else _lib.mg_plan_workspace_bytes
+        _check(fn(rd.handle, procs.handle, self.batch, self.length, ctypes.byref(ws)))
+        self.adjoint: Optional[torch.Tensor] = None
         self.workspace_bytes = int(ws.value)
         if workspace_pool is None:
             self.workspace = torch.empty(self.workspace_bytes, dtype=torch.uint8, device=self.device)
@@ -81,6 +85,29 @@ class DeviceRenderer:
                                     ctypes.c_void_p(self.workspace.data_ptr()), self.workspace_bytes,
                                     ctypes.c_void_p(s.cuda_stream)))
         return self.outputs
+
+    def backward(self, grad_outputs: torch.Tensor, stream: Optional[torch.cuda.Stream] = None):
+        """Reverse-mode pass after render() (mg_render_backward_arena): `grad_outputs`
+        [num_outputs][batch][2][length] = dL/d(outputs). Returns (grads, grad_sources): grads
+        per type, device fp64 in render order (rd.original_order maps them back), and
+        dL/d(sources) [num_inputs][batch][2][length] fp32 (a view into the adjoint arena).
+        Needs DeviceRenderer(..., backward=True)."""
+        s = stream or torch.cuda.current_stream(self.device)
+        if self.adjoint is None:
+            self.adjoint = torch.empty_like(self.arena)
+        self.adjoint[self.rd.output_begin:].copy_(grad_outputs)
+        grads: Dict[int, torch.Tensor] = {}
+        gptrs = (_vp * NUM_NODE_TYPES)()
+        for t, tab in self.tables.items():
+            grads[t] = torch.empty_like(tab)
+            gptrs[t] = grads[t].data_ptr()
+        with torch.cuda.stream(s):
+            _check(_lib.mg_render_backward_arena(self.rd.handle, self.procs.handle, self._ptrs,
+                                                 ctypes.c_void_p(self.arena.data_ptr()),
+                                                 ctypes.c_void_p(self.adjoint.data_ptr()), gptrs, self.batch,
+                                                 self.length, ctypes.c_void_p(self.workspace.data_ptr()),
+                                                 self.workspace_bytes, ctypes.c_void_p(s.cuda_stream)))
+        return grads, self.adjoint[: self.rd.num_inputs]
 
     def capture(self) -> "RenderGraph":
         """Capture one full render (main stream + side-stream prologues) as a CUDA graph
