@@ -141,6 +141,16 @@ int32_t mg_render_backward_arena(const mg_plan* plan, const mg_processors* procs
                                  const float* d_arena, float* d_adjoint, double* const* d_grad_tables, int32_t batch,
                                  int64_t length, void* d_workspace, uint64_t workspace_bytes, void* stream);
 
+/* Optimisation helpers on device buffers (fit.cpp:25-96 with analytic gradients): the MSE
+ * loss mean((y - t)^2) into *d_loss (fp64, deterministic) and d_grad = 2 (y - t) / n;
+ * d_scratch >= mg_mse_scratch_bytes(). mg_sgd_step: table -= lr * grad over rows x width,
+ * then fit.cpp:13-21's projection of compressor/noisegate rows into their legal ranges. */
+uint64_t mg_mse_scratch_bytes(void);
+int32_t mg_mse_loss_grad(const float* d_y, const float* d_target, int64_t n, float* d_grad, double* d_loss,
+                         void* d_scratch, void* stream);
+int32_t mg_sgd_step(int32_t node_type, double* d_table, const double* d_grad, int32_t rows, double learning_rate,
+                    void* stream);
+
 /* Renders of plans whose topology changes every batch (BASELINE config 3), no per-plan
  * allocation or synchronisation: device pools sized once from a capacity (cap[4] = arena
  * rows, workspace bytes, step-table ints, parameter doubles; mg_batch_capacity gives one

@@ -62,6 +62,8 @@ def lib():
         sig("ref_delay_kernel", _i32, _dbl, _vp, _i32, _vp, _vp, ctypes.POINTER(_i64))
         sig("ref_zero_phase_fir", _i32, _vp, _i32, _vp)
         sig("ref_uniform_noise", _i32, _i64, _u32, _vp)
+        sig("ref_fit", _i32, _vp, _i32, _vp, _i32, _dbl, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _i32, _i32, _dbl,
+            _dbl, _vp)
         _lib = L
     return _lib
 
@@ -246,6 +248,25 @@ def delay_kernel(row: np.ndarray, channel: int, sample_rate: float = 44100.0):
     pos = np.zeros(20, dtype=np.int64)
     _check(lib().ref_delay_kernel(sample_rate, _p(r), channel, _p(k), _p(pos), ctypes.byref(span)))
     return k, [int(x) for x in pos]
+
+
+def fit(types, edges, params, sources, target, trainable, steps: int, learning_rate: float, fd_step: float = 1e-3,
+        sample_rate: float = 44100.0):
+    """fit.cpp:25-96 (central differences + gradient descent). Returns (params, loss_history)."""
+    types = np.ascontiguousarray(types, dtype=np.int32)
+    edges = np.ascontiguousarray(edges, dtype=np.int32).reshape(-1, 4)
+    src = np.ascontiguousarray(sources, dtype=np.float64)
+    tgt = np.ascontiguousarray(target, dtype=np.float64)
+    k, b, _, n = src.shape
+    ptrs, rows, keep = _table_ptrs(params)
+    out = {t: np.array(v, dtype=np.float64, copy=True) for t, v in params.items()}
+    optrs, _, keep2 = _table_ptrs(out)
+    tr = np.ascontiguousarray([int(t) for t in trainable], dtype=np.int32)
+    hist = np.zeros(steps + 1)
+    _check(lib().ref_fit(_p(types), len(types), _p(edges), len(edges), sample_rate, ptrs, _p(rows), optrs, _p(src),
+                         _p(tgt), b, n, _p(tr), len(tr), steps, learning_rate, fd_step, _p(hist)))
+    del keep, keep2
+    return out, hist
 
 
 def rel_linf(a: np.ndarray, b: np.ndarray) -> float:

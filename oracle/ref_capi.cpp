@@ -23,6 +23,7 @@
 
 #include "mixgraph/console.hpp"
 #include "mixgraph/dsp.hpp"
+#include "mixgraph/fit.hpp"
 #include "mixgraph/graph.hpp"
 #include "mixgraph/processors.hpp"
 #include "mixgraph/reference.hpp"
@@ -281,6 +282,33 @@ int ref_render(const void* p, double fs, uint32_t seed, int32_t env_taps, double
     for (std::size_t i = 0; i < r.outputs.size(); ++i) std::memcpy(outputs + stride * i, r.outputs[i].samples.data(), sizeof(double) * stride);
     for (std::size_t i = 0; intermediates && i < r.intermediates.size(); ++i) {
       std::memcpy(intermediates + stride * i, r.intermediates[i].samples.data(), sizeof(double) * stride);
+    }
+  });
+}
+
+// fit.cpp:25-96 (central-difference gradient descent). trainable: n_trainable NodeType ids;
+// tables: init params (original order), overwritten with the fitted params; loss_history
+// holds steps + 1 values.
+int ref_fit(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne, double fs, const double* const* tables,
+            const int32_t* rows, double* const* out_tables, const double* sources, const double* target, int32_t batch,
+            int64_t length, const int32_t* trainable, int32_t n_trainable, int32_t steps, double learning_rate,
+            double fd_step, double* loss_history) {
+  return guarded([&] {
+    FlatGraph fg = make_flat(types, n, edges, ne);
+    const ProcessorSet& procs = processors_for(fs, 0, 32768, 1e-7);
+    ParamStore init = make_store(tables, rows);
+    auto src = make_sources(sources, fg.num_inputs, batch, length, fs);
+    auto tgt = make_sources(target, fg.num_outputs, batch, length, fs);
+    FitOptions o;
+    o.trainable.clear();
+    for (int i = 0; i < n_trainable; ++i) o.trainable.push_back(static_cast<NodeType>(trainable[i]));
+    o.steps = steps;
+    o.learning_rate = learning_rate;
+    o.fd_step = fd_step;
+    FitResult r = fit(fg, init, procs, src, tgt, o);
+    for (std::size_t i = 0; i < r.loss_history.size(); ++i) loss_history[i] = r.loss_history[i];
+    for (auto& [t, m] : r.params.tables) {
+      if (out_tables[static_cast<int>(t)]) std::memcpy(out_tables[static_cast<int>(t)], m.values.data(), sizeof(double) * m.values.size());
     }
   });
 }

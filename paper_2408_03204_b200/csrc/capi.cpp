@@ -13,6 +13,13 @@
 
 #include "mixgraph_b200/render.hpp"
 
+namespace mgb {  // device/launch.hpp (nvcc-only header): optimisation helpers
+std::size_t mse_scratch_bytes();
+void launch_mse_loss_grad(const float* y, const float* target, long n, float* grad, double* loss, void* scratch,
+                          cudaStream_t s);
+void launch_sgd_step(bool dynamics, double* table, const double* grad, long n, double lr, cudaStream_t s);
+}  // namespace mgb
+
 namespace mixgraph::workload {
 Graph generate_console(int tracks, double prune, std::uint32_t seed);
 ParamStore random_legal_params(const std::vector<NodeType>& types, std::uint32_t seed);
@@ -425,6 +432,26 @@ int32_t mg_render_backward_arena(const mg_plan* p, const mg_processors* procs, c
     std::scoped_lock lock(const_cast<mg_plan*>(p)->render_mu);
     backward_arena(dp, *procs->ps, d_tables, d_arena, d_adjoint, d_grad_tables, batch, static_cast<long>(length),
                    d_workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+  });
+}
+
+uint64_t mg_mse_scratch_bytes(void) { return mgb::mse_scratch_bytes(); }
+
+int32_t mg_mse_loss_grad(const float* d_y, const float* d_target, int64_t n, float* d_grad, double* d_loss,
+                         void* d_scratch, void* stream) {
+  return guarded([&] {
+    mgb::launch_mse_loss_grad(d_y, d_target, static_cast<long>(n), d_grad, d_loss, d_scratch,
+                              static_cast<cudaStream_t>(stream));
+  });
+}
+
+int32_t mg_sgd_step(int32_t node_type, double* d_table, const double* d_grad, int32_t rows, double learning_rate,
+                    void* stream) {
+  return guarded([&] {
+    const NodeType t = to_type(node_type);
+    const bool dyn = t == NodeType::Compressor || t == NodeType::Noisegate;
+    mgb::launch_sgd_step(dyn, d_table, d_grad, static_cast<long>(rows) * param_width(t), learning_rate,
+                         static_cast<cudaStream_t>(stream));
   });
 }
 

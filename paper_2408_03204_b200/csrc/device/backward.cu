@@ -155,7 +155,72 @@ __global__ void __launch_bounds__(1024) eq_grad(const float* partial, int rows_p
   grad[static_cast<long>(slot) * (kEqHalf + 1) + q] = (q == 0 ? 1.0 : 2.0) / N * exp(lm) * acc;
 }
 
+// ---- optimisation helpers (fit.cpp:25-96 with analytic gradients) -----------------------------
+constexpr int kMseBlocks = 592;  // 4 x 148 SMs, fixed (deterministic reduction order)
+constexpr int kMseThreads = 256;
+
+// grad = scale (y - t); per-block partial sums of (y - t)^2 in fp64.
+__global__ void __launch_bounds__(kMseThreads) mse_grad(const float* y, const float* t, long n, float scale, float* g,
+                                                       double* partial) {
+  __shared__ double red[kMseThreads / 32];
+  double acc = 0.0;
+  for (long i = static_cast<long>(blockIdx.x) * kMseThreads + threadIdx.x; i < n; i += static_cast<long>(kMseBlocks) * kMseThreads) {
+    const float d = y[i] - t[i];
+    g[i] = scale * d;
+    acc += static_cast<double>(d) * d;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kMseThreads / 32; ++w) s += red[w];
+    partial[blockIdx.x] = s;
+  }
+}
+
+__global__ void mse_finish(const double* partial, double inv_count, double* loss) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < kMseBlocks; i += 32) s += partial[i];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  (void)red;
+  if (threadIdx.x == 0) *loss = s * inv_count;
+}
+
+// p -= lr g, then the legal-range projection of fit.cpp:13-21 for dynamics rows.
+__global__ void sgd_update(double* p, const double* g, long n, double lr, int dyn) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n; i += static_cast<long>(gridDim.x) * blockDim.x) {
+    double v = p[i] - lr * g[i];
+    if (dyn) {
+      const int c = static_cast<int>(i % 4);
+      if (c == 0) v = fmin(fmax(v, 1e-4), 1.0 - 1e-4);
+      else if (c == 2) v = fmax(v, 1e-3);
+      else if (c == 3) v = fmax(v, 1.0);
+    }
+    p[i] = v;
+  }
+}
+
 }  // namespace
+
+std::size_t mse_scratch_bytes() { return sizeof(double) * kMseBlocks; }
+
+void launch_mse_loss_grad(const float* y, const float* target, long n, float* grad, double* loss, void* scratch,
+                          cudaStream_t s) {
+  auto* part = static_cast<double*>(scratch);
+  const float scale = n > 0 ? 2.f / static_cast<float>(n) : 0.f;
+  mse_grad<<<kMseBlocks, kMseThreads, 0, s>>>(y, target, n, scale, grad, part);
+  mse_finish<<<1, 32, 0, s>>>(part, n > 0 ? 1.0 / static_cast<double>(n) : 0.0, loss);
+}
+
+void launch_sgd_step(bool dynamics, double* table, const double* grad, long n, double lr, cudaStream_t s) {
+  if (n <= 0) return;
+  const long blocks = std::min<long>((n + 255) / 256, 1184);
+  sgd_update<<<static_cast<unsigned>(blocks), 256, 0, s>>>(table, grad, n, lr, dynamics ? 1 : 0);
+}
 
 std::size_t pw_grad_bytes(int slots, int batch, long length) {
   const long blocks = (length + kPgThreads * kPgPer - 1) / (kPgThreads * kPgPer);

@@ -100,6 +100,13 @@ void launch_pointwise_param_grad(PointOp op, const StepArgs& fw, const StepArgs&
 std::size_t eq_grad_bytes(int slots, int batch, long length);
 void launch_eq_param_grad(const StepArgs& fw, const StepArgs& bw, void* ws, double* grad, cudaStream_t s);
 
+// Optimisation helpers: MSE loss (fp64, deterministic) and its output gradient 2 (y - t) / n;
+// plain gradient step with fit.cpp's legal-range projection of dynamics rows.
+std::size_t mse_scratch_bytes();
+void launch_mse_loss_grad(const float* y, const float* target, long n, float* grad, double* loss, void* scratch,
+                          cudaStream_t s);
+void launch_sgd_step(bool dynamics, double* table, const double* grad, long n, double lr, cudaStream_t s);
+
 // Kernel-only entry points (for ProcessorSet::reverb_kernel / delay_kernel).
 void launch_reverb_ir(const double* params, int slots, const ReverbConst& rc, float2* ir, long ir_stride,
                       cudaStream_t s);

@@ -86,21 +86,26 @@ class DeviceRenderer:
                                     ctypes.c_void_p(s.cuda_stream)))
         return self.outputs
 
-    def backward(self, grad_outputs: torch.Tensor, stream: Optional[torch.cuda.Stream] = None):
+    def backward(self, grad_outputs: torch.Tensor, stream: Optional[torch.cuda.Stream] = None,
+                 grads: Optional[Dict[int, torch.Tensor]] = None):
         """Reverse-mode pass after render() (mg_render_backward_arena): `grad_outputs`
         [num_outputs][batch][2][length] = dL/d(outputs). Returns (grads, grad_sources): grads
         per type, device fp64 in render order (rd.original_order maps them back), and
         dL/d(sources) [num_inputs][batch][2][length] fp32 (a view into the adjoint arena).
-        Needs DeviceRenderer(..., backward=True)."""
+        Needs DeviceRenderer(..., backward=True). `grads`: optional preallocated output tables
+        (fp64, shaped like the parameter tables, e.g. views into one flat all-reduce buffer)."""
         s = stream or torch.cuda.current_stream(self.device)
         if self.adjoint is None:
             self.adjoint = torch.empty_like(self.arena)
         self.adjoint[self.rd.output_begin:].copy_(grad_outputs)
-        grads: Dict[int, torch.Tensor] = {}
+        if grads is None:
+            grads = {t: torch.empty_like(tab) for t, tab in self.tables.items()}
         gptrs = (_vp * NUM_NODE_TYPES)()
         for t, tab in self.tables.items():
-            grads[t] = torch.empty_like(tab)
-            gptrs[t] = grads[t].data_ptr()
+            g = grads[t]
+            if g.dtype != torch.float64 or g.shape != tab.shape or not g.is_contiguous():
+                raise ValueError("backward: gradient tables must be contiguous fp64 shaped like the parameters")
+            gptrs[t] = g.data_ptr()
         with torch.cuda.stream(s):
             _check(_lib.mg_render_backward_arena(self.rd.handle, self.procs.handle, self._ptrs,
                                                  ctypes.c_void_p(self.arena.data_ptr()),

@@ -132,3 +132,33 @@ def test_backward_is_deterministic(mg, ref):
     assert np.array_equal(s1, s2)
     for ty in g1:
         assert np.array_equal(g1[ty], g2[ty])
+
+
+@pytest.mark.parametrize("trainable,lr,ptol", [([3, 7], 0.5, 2e-3), ([5, 6], 2e-6, 1e-2)])
+def test_fit_matches_reference_fit(mg, ref, trainable, lr, ptol):
+    # fit.cpp:25-96 takes central differences (fd_step 1e-3) and descends; the analytic
+    # gradients must follow the same trajectory. Dynamics: a small rate keeps the reference's
+    # alpha +- fd_step probes inside (0, 1), and its fd_step = 1e-3 difference of a^k sums is
+    # itself ~0.5% off the derivative in alpha, hence the looser parameter tolerance.
+    from paper_2408_03204_b200 import training
+    t, e = ref.console(1, 0.0, 2)
+    rng = np.random.default_rng(12)
+    L = 1500
+    src = rng.uniform(-1, 1, size=(1, 1, 2, L))
+    params = ref.random_legal_params(t, e, 13)
+    for ty in (5, 6):
+        params[ty][:, 0] = np.minimum(params[ty][:, 0], 0.99)
+    target = ref.Plan(t, e, 1).render(ref.random_legal_params(t, e, 14), src, sample_rate=FS)
+    want_p, want_h = ref.fit(t, e, params, src, target, trainable, 3, lr, sample_rate=FS)
+    procs = mg.ProcessorSet(sample_rate=FS)
+    fg = mg.to_flat(mg.Graph.from_arrays(t, e))
+    got_p, got_h = training.fit(fg, params, procs, src, target, trainable=trainable, steps=3, learning_rate=lr)
+    assert np.all(np.diff(want_h) < 0)
+    assert np.allclose(got_h, want_h, rtol=2e-3, atol=0), (got_h, want_h)
+    for ty in trainable:
+        moved = np.abs(want_p[ty] - params[ty]).max()
+        assert moved > 0
+        assert np.abs(got_p[ty] - want_p[ty]).max() <= ptol * moved + 1e-12, (ty, got_p[ty], want_p[ty])
+    for ty in params:
+        if int(ty) not in trainable:
+            assert np.array_equal(got_p[ty], params[ty])

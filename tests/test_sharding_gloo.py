@@ -72,3 +72,30 @@ def test_lpt_is_deterministic_and_balanced():
         assert sorted(i for x in s for i in x) == list(range(512))
         loads = [sum(costs[i] for i in x) for x in s]
         assert max(loads) - min(loads) <= max(costs)
+
+
+def _grad_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2408_03204_b200.training import reduce_gradients
+    flat = torch.arange(6, dtype=torch.float64) * (rank + 1)
+    views = {3: flat[:2].view(1, 2), 7: flat[2:3].view(1, 1), 5: flat[3:].view(1, 3)}
+    n = reduce_gradients(flat, dist.group.WORLD)
+    out[rank] = (n, {k: v.clone().numpy().tolist() for k, v in views.items()})
+    dist.destroy_process_group()
+
+
+def test_shared_parameter_gradients_all_reduced_two_ranks():
+    # The optimisation config's only collective: one all-reduce of the flat gradient buffer
+    # (per-type tables are views into it), averaged by the world size.
+    world = 2
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_grad_worker, args=(world, port, out), nprocs=world, join=True)
+        res = dict(out)
+    for r in range(world):
+        n, views = res[r]
+        assert n == 2
+        assert views[3] == [[0.0, 3.0]] and views[7] == [[6.0]] and views[5] == [[9.0, 12.0, 15.0]]
