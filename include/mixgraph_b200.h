@@ -141,6 +141,12 @@ int32_t mg_render_backward_arena(const mg_plan* plan, const mg_processors* procs
                                  const float* d_arena, float* d_adjoint, double* const* d_grad_tables, int32_t batch,
                                  int64_t length, void* d_workspace, uint64_t workspace_bytes, void* stream);
 
+/* Execution-strategy switch for the long convolutions (diagnostics and tests): -1 chooses
+ * per step (default: kernel spectra over 64 MiB fuse their row stage into the signal's row
+ * pass), 0 always runs the separate kernel-spectrum row pass, 1 always fuses. Process-wide;
+ * results agree either way. */
+void mg_set_conv_fuse(int32_t mode);
+
 /* Optimisation helpers on device buffers (fit.cpp:25-96 with analytic gradients): the MSE
  * loss mean((y - t)^2) into *d_loss (fp64, deterministic) and d_grad = 2 (y - t) / n;
  * d_scratch >= mg_mse_scratch_bytes(). mg_sgd_step: table -= lr * grad over rows x width,

@@ -81,6 +81,7 @@ _sig("mg_pipeline_sync", _i32, _vp)
 _sig("mg_pipeline_destroy", None, _vp)
 _sig("mg_backward_workspace_bytes", _i32, _vp, _vp, _i32, _i64, _P(_u64))
 _sig("mg_render_backward_arena", _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp)
+_sig("mg_set_conv_fuse", None, _i32)
 _sig("mg_batch_capacity", _i32, _vp, _vp, _i32, _i64, _vp)
 _sig("mg_batch_create", _i32, _vp, _i32, _i64, _vp, _i32, _P(_vp))
 _sig("mg_batch_submit", _i32, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp)
@@ -606,6 +607,11 @@ def generate_console_arrays(tracks: int, prune: float = 0.0, seed: int = 0) -> T
 def generate_console(tracks: int, prune: float = 0.0, seed: int = 0) -> Graph:
     """`console.cpp:10-44`."""
     return Graph.from_arrays(*generate_console_arrays(tracks, prune, seed))
+
+
+def set_conv_fuse(mode: int) -> None:
+    """mg_set_conv_fuse: -1 auto (default), 0 separate kernel-spectrum rows pass, 1 fused."""
+    _lib.mg_set_conv_fuse(int(mode))
 
 
 def generate_large_console_arrays(tracks: int = 64) -> Tuple[np.ndarray, np.ndarray]:

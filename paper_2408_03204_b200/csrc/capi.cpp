@@ -18,6 +18,7 @@ std::size_t mse_scratch_bytes();
 void launch_mse_loss_grad(const float* y, const float* target, long n, float* grad, double* loss, void* scratch,
                           cudaStream_t s);
 void launch_sgd_step(bool dynamics, double* table, const double* grad, long n, double lr, cudaStream_t s);
+void set_conv_fuse(int mode);
 }  // namespace mgb
 
 namespace mixgraph::workload {
@@ -434,6 +435,8 @@ int32_t mg_render_backward_arena(const mg_plan* p, const mg_processors* procs, c
                    d_workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
   });
 }
+
+void mg_set_conv_fuse(int32_t mode) { mgb::set_conv_fuse(mode); }
 
 uint64_t mg_mse_scratch_bytes(void) { return mgb::mse_scratch_bytes(); }
 

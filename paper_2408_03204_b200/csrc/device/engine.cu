@@ -7,7 +7,12 @@
 // arena rows and stores straight into the step's contiguous output rows (the contiguity
 // is what node reordering buys, `schedule.cpp:397-413`): no step_in/step_out buffers.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <thread>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -281,6 +286,16 @@ int chain_length(const RenderData& rd, std::size_t k, int batch, long length) {
   return n >= 2 ? n : 1;
 }
 
+// A first-step EQ whose grid is at most two waves runs its response-independent forward FFTs
+// before its prologue has finished (render_arena); a larger grid keeps the GPU busy anyway and
+// the round trip of the window spectra through memory would only cost bandwidth.
+bool split_first_eq(const RenderData& rd, int batch, long length) {
+  if (rd.steps.empty() || rd.steps[0].type != NodeType::Eq) return false;
+  const long blocks = (length + 6143) / 6144;
+  const long grid = blocks * (rd.steps[0].store_end - rd.steps[0].store_begin) * batch;
+  return grid <= 2L * 2 * 148;
+}
+
 std::size_t step_ws_bytes(NodeType t, int slots, int batch, long length, const ProcessorSet& p) {
   return align256(prologue_bytes(t, slots, length, p)) + align256(sync_bytes(t, slots, batch, length)) +
          main_bytes(t, slots, batch, length, p);
@@ -439,8 +454,8 @@ int DevicePlan::kernels_per_render(int batch, long length) const {
     k += n > 1 ? 1 : step_kernels(rd_.steps[i].type);
     i += static_cast<std::size_t>(n);
   }
-  // A first-step EQ is split into forward and inverse launches (render_arena, hoisted).
-  if (!rd_.steps.empty() && rd_.steps[0].type == NodeType::Eq) ++k;
+  // A first-step EQ may be split into forward and inverse launches (render_arena, hoisted).
+  if (split_first_eq(rd_, batch, length)) ++k;
   return k;
 }
 
@@ -485,7 +500,7 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
   if (no_hoist) hoist = false;
   // A first-step EQ starts its response-independent forward FFTs before the prologues are
   // enqueued, so its grid reaches the GPU ahead of the side stream's grids.
-  const bool split_first = hoist && !rd.steps.empty() && rd.steps[0].type == NodeType::Eq;
+  const bool split_first = hoist && split_first_eq(rd, batch, length);
   const cudaEvent_t* ev = plan.events();
   if (hoist) {
     cuda_check(cudaEventRecord(ev[0], stream), "event");  // fork point: before any render work
@@ -525,7 +540,7 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
     char* mws = ws + lay.main_off;
     // The first step has nothing to hide its prologue behind: an EQ there runs its
     // response-independent forward FFTs before joining the prologue, the rest after.
-    const bool split_eq = hoist && k == 0 && t == NodeType::Eq;
+    const bool split_eq = split_first && k == 0;
     if (step_events) cuda_check(cudaEventRecord(step_events[2 * k], stream), "event");
     // (forward FFTs of a split first EQ were enqueued before the prologues, see above)
     if (hoist && has_prologue(t)) cuda_check(cudaStreamWaitEvent(stream, ev[k + 1], 0), "wait");
@@ -754,15 +769,138 @@ struct RenderPipeline::Slot {
   std::size_t table_rows[kNumNodeTypes] = {};
   std::unique_ptr<RenderGraph> graph;
   cudaEvent_t h2d = nullptr, done = nullptr, d2h = nullptr;
+  float* pin_src = nullptr;  // host-convert mode: pinned fp32 staging
+  float* pin_out = nullptr;
+  std::uint64_t job = 0;     // completion job that reads pin_out (0: none)
   ~Slot() {
     for (cudaEvent_t e : {h2d, done, d2h}) {
       if (e) cudaEventDestroy(e);
     }
+    if (pin_src) cudaFreeHost(pin_src);
+    if (pin_out) cudaFreeHost(pin_out);
+  }
+};
+
+// Host-side double <-> float conversion: a fixed pool of workers splitting each array in
+// equal contiguous chunks, and one completion thread that waits for a render's D2H event
+// and converts its fp32 outputs into the caller's double buffers.
+struct RenderPipeline::HostConvert {
+  int nthreads = 1;
+  std::vector<std::thread> workers;
+  std::mutex mu;  // pool state
+  std::condition_variable cv, cv_done;
+  std::function<void(int)> task;
+  std::uint64_t gen = 0;
+  int remaining = 0;
+  bool stop = false;
+  std::mutex run_mu;  // one parallel job at a time (submit thread and completion thread)
+
+  struct Job {
+    std::uint64_t id;
+    cudaEvent_t ev;
+    const float* src;
+    std::vector<double*> dst;
+    std::size_t n;  // floats per output signal
+  };
+  std::thread completer;
+  std::mutex qmu;
+  std::condition_variable qcv, qdone;
+  std::deque<Job> queue;
+  std::uint64_t next_id = 1, finished = 0;
+  std::string error;
+
+  explicit HostConvert(int n) : nthreads(n) {
+    for (int i = 0; i < nthreads; ++i) {
+      workers.emplace_back([this, i] {
+        std::uint64_t seen = 0;
+        for (;;) {
+          std::function<void(int)> t;
+          {
+            std::unique_lock lk(mu);
+            cv.wait(lk, [&] { return stop || gen != seen; });
+            if (stop) return;
+            seen = gen;
+            t = task;
+          }
+          t(i);
+          std::unique_lock lk(mu);
+          if (--remaining == 0) cv_done.notify_all();
+        }
+      });
+    }
+    completer = std::thread([this] {
+      for (;;) {
+        Job j;
+        {
+          std::unique_lock lk(qmu);
+          qcv.wait(lk, [&] { return stop || !queue.empty(); });
+          if (queue.empty()) return;
+          j = std::move(queue.front());
+        }
+        cudaError_t e = cudaEventSynchronize(j.ev);
+        if (e != cudaSuccess) {
+          std::scoped_lock lk(qmu);
+          error = cudaGetErrorString(e);
+        } else {
+          for (std::size_t o = 0; o < j.dst.size(); ++o) convert(j.src + o * j.n, j.dst[o], j.n);
+        }
+        std::scoped_lock lk(qmu);
+        queue.pop_front();
+        finished = j.id;
+        qdone.notify_all();
+      }
+    });
+  }
+  ~HostConvert() {
+    {
+      std::scoped_lock lk(qmu);
+      stop = true;
+    }
+    qcv.notify_all();
+    if (completer.joinable()) completer.join();
+    {
+      std::scoped_lock lk(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    for (auto& w : workers) w.join();
+  }
+  void parallel(const std::function<void(int)>& f) {
+    std::scoped_lock run(run_mu);
+    {
+      std::scoped_lock lk(mu);
+      task = f;
+      remaining = nthreads;
+      ++gen;
+    }
+    cv.notify_all();
+    std::unique_lock lk(mu);
+    cv_done.wait(lk, [&] { return remaining == 0; });
+  }
+  template <typename A, typename B>
+  void convert(const A* src, B* dst, std::size_t n) {
+    parallel([&](int i) {
+      const std::size_t lo = n * static_cast<std::size_t>(i) / nthreads, hi = n * static_cast<std::size_t>(i + 1) / nthreads;
+      for (std::size_t k = lo; k < hi; ++k) dst[k] = static_cast<B>(src[k]);
+    });
+  }
+  std::uint64_t enqueue(Job j) {
+    std::scoped_lock lk(qmu);
+    j.id = next_id++;
+    const std::uint64_t id = j.id;
+    queue.push_back(std::move(j));
+    qcv.notify_one();
+    return id;
+  }
+  void wait(std::uint64_t id) {
+    std::unique_lock lk(qmu);
+    qdone.wait(lk, [&] { return finished >= id; });
+    if (!error.empty()) throw std::runtime_error("cuda: RenderPipeline outputs: " + error);
   }
 };
 
 RenderPipeline::RenderPipeline(const DevicePlan& plan, const ProcessorSet& procs, int batch, long length, bool f32_io,
-                               int depth)
+                               int depth, int host_threads)
     : plan_(plan), procs_(procs), batch_(batch), length_(length), f32_(f32_io),
       stride_(static_cast<long>(batch) * 2 * length) {
   if (depth < 1) fail("RenderPipeline: depth must be >= 1");
@@ -772,9 +910,18 @@ RenderPipeline::RenderPipeline(const DevicePlan& plan, const ProcessorSet& procs
   cuda_check(cudaStreamCreateWithPriority(&h2d_, cudaStreamNonBlocking, greatest), "stream");
   cuda_check(cudaStreamCreateWithPriority(&compute_, cudaStreamNonBlocking, greatest), "stream");
   cuda_check(cudaStreamCreateWithPriority(&d2h_, cudaStreamNonBlocking, greatest), "stream");
+  if (!f32_) {
+    int n = host_threads;
+    if (n < 0) {
+      const char* v = std::getenv("MGB_PIPELINE_HOST_THREADS");  // diagnostics: 0 = device conversion
+      n = v ? std::atoi(v) : 0;  // measured: PCIe carrying double beats host conversion (0.66 vs 0.77 ms, config 2)
+    }
+    if (n >= 1) conv_ = std::make_unique<HostConvert>(n);
+  }
   const RenderData& rd = plan.data();
   const std::size_t rows = static_cast<std::size_t>(rd.buffer_rows);
   const std::size_t ws_bytes = plan.workspace_bytes(batch, length, procs);
+  const std::size_t n_out = static_cast<std::size_t>(rd.buffer_rows - rd.output_begin);
   for (int d = 0; d < depth; ++d) {
     auto s = std::make_unique<Slot>();
     auto* arena = static_cast<float*>(s->arena.ensure(sizeof(float) * rows * stride_ + 16));
@@ -792,7 +939,14 @@ RenderPipeline::RenderPipeline(const DevicePlan& plan, const ProcessorSet& procs
       for (std::size_t r = 0; r < src.size(); ++r) host.insert(host.end(), row.begin(), row.end());
     }
     if (!host.empty()) cuda_check(cudaMemcpy(dpar, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice), "H2D");
-    if (!f32_) s->staging.ensure(sizeof(double) * rows * stride_ + 16);
+    if (!f32_ && !conv_) s->staging.ensure(sizeof(double) * rows * stride_ + 16);
+    if (conv_) {
+      cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&s->pin_src),
+                               sizeof(float) * std::max<std::size_t>(1, static_cast<std::size_t>(rd.num_inputs)) * stride_,
+                               cudaHostAllocDefault), "cudaHostAlloc");
+      cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&s->pin_out), sizeof(float) * std::max<std::size_t>(1, n_out) * stride_,
+                               cudaHostAllocDefault), "cudaHostAlloc");
+    }
     cuda_check(cudaMemset(arena, 0, sizeof(float) * rows * stride_), "memset");
     s->graph = std::make_unique<RenderGraph>(plan, procs, s->tables, arena, batch, length, ws, ws_bytes);
     for (cudaEvent_t* e : {&s->h2d, &s->done, &s->d2h}) cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
@@ -804,6 +958,7 @@ RenderPipeline::RenderPipeline(const DevicePlan& plan, const ProcessorSet& procs
 RenderPipeline::~RenderPipeline() {
   if (compute_) cudaStreamSynchronize(compute_);
   if (d2h_) cudaStreamSynchronize(d2h_);
+  conv_.reset();  // drains the completion thread
   slots_.clear();
   for (cudaStream_t st : {h2d_, compute_, d2h_}) {
     if (st) cudaStreamDestroy(st);
@@ -817,6 +972,13 @@ void RenderPipeline::submit(const ParamStore& params, const void* const* sources
   const bool reused = next_ >= slots_.size();
   ++next_;
   auto* arena = static_cast<float*>(s.arena.ptr);
+  const std::size_t fbytes = sizeof(float) * static_cast<std::size_t>(stride_);
+  if (conv_ && reused) {
+    // The pinned fp32 staging of this slot is rewritten on the host: its previous upload and
+    // its previous outputs' conversion must be done.
+    cuda_check(cudaEventSynchronize(s.h2d), "pipeline staging");
+    if (s.job) conv_->wait(s.job);
+  }
   // Inputs: the slot's previous render must have consumed its sources and params.
   if (reused) cuda_check(cudaStreamWaitEvent(h2d_, s.done, 0), "wait");
   for (const auto& [t, m] : params.tables) {
@@ -827,7 +989,6 @@ void RenderPipeline::submit(const ParamStore& params, const void* const* sources
                                cudaMemcpyHostToDevice, h2d_), "H2D params");
   }
   const std::size_t bytes = (f32_ ? sizeof(float) : sizeof(double)) * static_cast<std::size_t>(stride_);
-  char* dst = f32_ ? reinterpret_cast<char*>(arena) : static_cast<char*>(s.staging.ptr);
   // Sources laid out back to back in host memory (one [K][B][2][L] array, the usual case)
   // go over PCIe as one transfer instead of K.
   auto contiguous = [&](const void* const* ptrs, int n) {
@@ -836,26 +997,52 @@ void RenderPipeline::submit(const ParamStore& params, const void* const* sources
     }
     return n > 0;
   };
-  if (contiguous(sources, rd.num_inputs)) {
-    cuda_check(cudaMemcpyAsync(dst, sources[0], bytes * rd.num_inputs, cudaMemcpyHostToDevice, h2d_), "H2D sources");
-  } else {
+  if (conv_) {
     for (int k = 0; k < rd.num_inputs; ++k) {
-      cuda_check(cudaMemcpyAsync(dst + bytes * k, sources[k], bytes, cudaMemcpyHostToDevice, h2d_), "H2D sources");
+      conv_->convert(static_cast<const double*>(sources[k]), s.pin_src + static_cast<std::size_t>(k) * stride_,
+                     static_cast<std::size_t>(stride_));
+    }
+    if (rd.num_inputs > 0) {
+      cuda_check(cudaMemcpyAsync(arena, s.pin_src, fbytes * rd.num_inputs, cudaMemcpyHostToDevice, h2d_), "H2D sources");
+    }
+  } else {
+    char* dst = f32_ ? reinterpret_cast<char*>(arena) : static_cast<char*>(s.staging.ptr);
+    if (contiguous(sources, rd.num_inputs)) {
+      cuda_check(cudaMemcpyAsync(dst, sources[0], bytes * rd.num_inputs, cudaMemcpyHostToDevice, h2d_), "H2D sources");
+    } else {
+      for (int k = 0; k < rd.num_inputs; ++k) {
+        cuda_check(cudaMemcpyAsync(dst + bytes * k, sources[k], bytes, cudaMemcpyHostToDevice, h2d_), "H2D sources");
+      }
     }
   }
   cuda_check(cudaEventRecord(s.h2d, h2d_), "event");
   // Compute: after the inputs landed and the slot's previous outputs were read back.
   cuda_check(cudaStreamWaitEvent(compute_, s.h2d, 0), "wait");
   if (reused) cuda_check(cudaStreamWaitEvent(compute_, s.d2h, 0), "wait");
-  if (!f32_) mgb::launch_f64_to_f32(static_cast<const double*>(s.staging.ptr), arena, rd.num_inputs * stride_, compute_);
+  const bool dev_conv = !f32_ && !conv_;
+  if (dev_conv) mgb::launch_f64_to_f32(static_cast<const double*>(s.staging.ptr), arena, rd.num_inputs * stride_, compute_);
   s.graph->launch(compute_);
   const long n_out = (rd.buffer_rows - rd.output_begin) * stride_;
-  if (!f32_) mgb::launch_f32_to_f64(arena + rd.output_begin * stride_, static_cast<double*>(s.staging.ptr), n_out, compute_);
+  if (dev_conv) mgb::launch_f32_to_f64(arena + rd.output_begin * stride_, static_cast<double*>(s.staging.ptr), n_out, compute_);
   cuda_check(cudaEventRecord(s.done, compute_), "event");
   // Outputs.
   cuda_check(cudaStreamWaitEvent(d2h_, s.done, 0), "wait");
-  const char* src = f32_ ? reinterpret_cast<const char*>(arena + rd.output_begin * stride_) : static_cast<const char*>(s.staging.ptr);
   const int n_outs = rd.buffer_rows - rd.output_begin;
+  if (conv_) {
+    if (n_outs > 0) {
+      cuda_check(cudaMemcpyAsync(s.pin_out, arena + rd.output_begin * stride_, fbytes * n_outs, cudaMemcpyDeviceToHost, d2h_),
+                 "D2H outputs");
+    }
+    cuda_check(cudaEventRecord(s.d2h, d2h_), "event");
+    HostConvert::Job j;
+    j.ev = s.d2h;
+    j.src = s.pin_out;
+    j.n = static_cast<std::size_t>(stride_);
+    for (int o = 0; o < n_outs; ++o) j.dst.push_back(static_cast<double*>(outputs[o]));
+    s.job = conv_->enqueue(std::move(j));
+    return;
+  }
+  const char* src = f32_ ? reinterpret_cast<const char*>(arena + rd.output_begin * stride_) : static_cast<const char*>(s.staging.ptr);
   if (contiguous(outputs, n_outs)) {
     cuda_check(cudaMemcpyAsync(outputs[0], src, bytes * n_outs, cudaMemcpyDeviceToHost, d2h_), "D2H outputs");
   } else {
@@ -869,6 +1056,11 @@ void RenderPipeline::submit(const ParamStore& params, const void* const* sources
 void RenderPipeline::sync() {
   cuda_check(cudaStreamSynchronize(d2h_), "pipeline sync");
   cuda_check(cudaStreamSynchronize(compute_), "pipeline sync");
+  if (conv_) {
+    for (auto& s : slots_) {
+      if (s->job) conv_->wait(s->job);
+    }
+  }
 }
 
 // ---- BatchRenderer ---------------------------------------------------------------------------

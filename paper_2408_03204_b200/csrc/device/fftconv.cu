@@ -316,6 +316,85 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2,
   }
 }
 
+
+// rows_conv with the kernel's row stage fused in (large steps, see conv_fuse_kernel_rows):
+// K holds the kernel's COLUMN-stage output (cols_fwd<Kernel>, no rows_spec pass); each CTA
+// transforms the kernel rows ra / rb alongside the signal rows (4 transforms), so the kernel
+// spectrum never makes a round trip through memory. grid (N1/2 + 1, slots*B)
+template <int LN2>
+__global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_conv_fk(int log_n, int batch, float2* X, const float2* K,
+                                                                  const float2* tw) {
+  constexpr int N2 = 1 << LN2;
+  constexpr int NT = row_threads<LN2, 4>();
+  constexpr int RS = padded(N2);
+  extern __shared__ float2 rows[];  // [4][RS]: x a, x b, k a, k b
+  const long N = 1L << log_n;
+  const int N1 = static_cast<int>(N >> LN2);
+  const int item = blockIdx.y;
+  const int slot = item / batch;
+  const int ra = blockIdx.x, rb = (N1 - ra) & (N1 - 1);
+  const bool self = ra == rb;
+  float2* xa = X + static_cast<long>(item) * N + static_cast<long>(ra) * N2;
+  float2* xb = X + static_cast<long>(item) * N + static_cast<long>(rb) * N2;
+  const float2* ka = K + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
+  const float2* kb_ = K + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
+  {
+    constexpr int PER = (N2 + NT - 1) / NT;
+    float2 v[4][PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int i = threadIdx.x + q * NT;
+      if (N2 % NT == 0 || i < N2) {
+        v[0][q] = xa[i];
+        v[1][q] = xb[i];
+        v[2][q] = __ldg(ka + i);
+        v[3][q] = __ldg(kb_ + i);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int i = threadIdx.x + q * NT;
+      if (N2 % NT == 0 || i < N2) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) rows[r * RS + sidx(i)] = v[r][q];
+      }
+    }
+  }
+  __syncthreads();
+  fft_pow2<LN2, 4, NT, -1>(rows, RS, tw);
+  const float s = 0.25f / static_cast<float>(N);
+  constexpr int KPT = (N2 + NT - 1) / NT;
+  float2 zk[KPT], zo[KPT];
+#pragma unroll
+  for (int q = 0; q < KPT; ++q) {
+    const int k = threadIdx.x + q * NT;
+    if (k >= N2) continue;
+    const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
+    const float2 xk = rows[sidx(k)], xo = rows[RS + sidx(kb)];
+    const float2 pk = rows[2 * RS + sidx(k)], po = rows[3 * RS + sidx(kb)];
+    zk[q] = zmix(xk, cconj(xo), pk, cconj(po), s);
+    zo[q] = zmix(xo, cconj(xk), po, cconj(pk), s);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < KPT; ++q) {
+    const int k = threadIdx.x + q * NT;
+    if (k >= N2) continue;
+    const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
+    if (self && kb < k) continue;
+    rows[sidx(k)] = zk[q];
+    if (self) rows[sidx(kb)] = zo[q];
+    else rows[RS + sidx(kb)] = zo[q];
+  }
+  __syncthreads();
+  fft_pow2<LN2, 2, NT, +1>(rows, RS, tw);
+  const float inv_n = 2.f / static_cast<float>(N);
+  for (int i = threadIdx.x; i < N2; i += NT) {
+    xa[i] = cmul(rows[sidx(i)], expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n));
+    if (!self) xb[i] = cmul(rows[RS + sidx(i)], expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n));
+  }
+}
+
 // ---- dispatch -----------------------------------------------------------------------------
 template <int LN1>
 void cols_fwd_t(ColSrc src, const StepArgs& a, const float2* ir, long taps, const ConvGeom& g, int items,
@@ -381,6 +460,19 @@ void rows_conv_t(const ConvGeom& g, int items, int batch, float2* X, const float
 }
 
 
+template <int LN2>
+void rows_conv_fk_t(const ConvGeom& g, int items, int batch, float2* X, const float2* K, const float2* tw,
+                    cudaStream_t s) {
+  constexpr int smem = 4 * padded(1 << LN2) * 8;
+  static const bool done = [] {
+    cudaFuncSetAttribute(rows_conv_fk<LN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    return true;
+  }();
+  (void)done;
+  const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(items));
+  rows_conv_fk<LN2><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, batch, X, K, tw);
+}
+
 #define MGB_DISPATCH_LN(var, FN, ...)                  \
   switch (var) {                                       \
     case 6: FN<6>(__VA_ARGS__); break;                 \
@@ -397,7 +489,8 @@ void rows_conv_t(const ConvGeom& g, int items, int batch, float2* X, const float
 void kernel_spectrum(ColSrc src, const StepArgs& a, const ConvGeom& g, const float2* ir, long taps, int window,
                      float2* P, cudaStream_t s) {
   MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, src, a, ir, taps, g, a.slots, P, window, s);
-  MGB_DISPATCH_LN(g.log_n2, rows_spec_t, g, a.slots, P, a.tw, s);
+  // Large steps leave the row stage to rows_conv_fk (conv_fuse_kernel_rows).
+  if (!conv_fuse_kernel_rows(g, a.slots)) MGB_DISPATCH_LN(g.log_n2, rows_spec_t, g, a.slots, P, a.tw, s);
 }
 
 // ---- reverb impulse response (masked noise STFT -> ISTFT) ----------------------------------
@@ -823,6 +916,16 @@ unsigned grid_for(long n) {
 
 }  // namespace
 
+static int g_conv_fuse = -1;  // -1 auto, 0 never, 1 always (mg_set_conv_fuse; tests)
+void set_conv_fuse(int mode) { g_conv_fuse = mode; }
+
+bool conv_fuse_kernel_rows(const ConvGeom& g, int slots) {
+  if (g_conv_fuse >= 0) return g_conv_fuse == 1;
+  // Kernel spectra that cannot stay in L2 (> 64 MiB over the step) are not worth a separate
+  // rows pass: the signal's row kernel transforms the kernel rows itself.
+  return sizeof(float2) * static_cast<std::size_t>(slots) * static_cast<std::size_t>(g.n) > (64u << 20);
+}
+
 ConvGeom conv_geom(long length, long taps) {
   const long full = length + taps - 1;
   ConvGeom g;
@@ -896,7 +999,11 @@ void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, voi
   auto* X = static_cast<float2*>(ws);
   const int items = a.slots * a.batch;
   MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, a, nullptr, 0, g, items, X, 0, s);
-  MGB_DISPATCH_LN(g.log_n2, rows_conv_t, g, items, a.batch, X, P, a.tw, s);
+  if (conv_fuse_kernel_rows(g, a.slots)) {
+    MGB_DISPATCH_LN(g.log_n2, rows_conv_fk_t, g, items, a.batch, X, P, a.tw, s);
+  } else {
+    MGB_DISPATCH_LN(g.log_n2, rows_conv_t, g, items, a.batch, X, P, a.tw, s);
+  }
   MGB_DISPATCH_LN(g.log_n1, cols_inv_t, a, g, X, s);
 }
 
@@ -941,7 +1048,9 @@ void launch_conv_backward(bool reverb, const StepArgs& fw, const StepArgs& bw, c
   if (fw.slots == 0 || fw.batch == 0 || fw.length == 0) return;
   const long taps = reverb ? rc.length : dc.span;
   const ConvGeom g = conv_geom(fw.length, taps);
-  const auto* P = reinterpret_cast<const float2*>(static_cast<const char*>(prologue_ws) + ir_bytes(fw.slots, taps));
+  auto* P = reinterpret_cast<float2*>(static_cast<char*>(const_cast<void*>(prologue_ws)) + ir_bytes(fw.slots, taps));
+  // A large step's forward left the kernel spectrum at its column stage: finish it in place.
+  if (conv_fuse_kernel_rows(g, fw.slots)) MGB_DISPATCH_LN(g.log_n2, rows_spec_t, g, fw.slots, P, fw.tw, s);
   const int items = fw.slots * fw.batch;
   const std::size_t spec = align256(sizeof(float2) * static_cast<std::size_t>(items) * g.n);
   auto* DY = static_cast<float2*>(ws);

@@ -64,6 +64,10 @@ struct ConvGeom {
   long n = 0;
 };
 ConvGeom conv_geom(long length, long taps);
+// Large steps (kernel spectra beyond L2) fuse the kernel's row stage into the signal's row
+// pass instead of a separate prologue pass.
+bool conv_fuse_kernel_rows(const ConvGeom& g, int slots);
+void set_conv_fuse(int mode);  // -1 auto (default), 0 never, 1 always
 
 struct ReverbConst {
   const float2* stft_mid;  // [frames][193]

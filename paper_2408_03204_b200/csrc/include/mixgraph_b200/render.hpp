@@ -217,10 +217,16 @@ class RenderGraph {
 // both directions runs concurrently with the GPU work. Host audio is float (f32_io, copied
 // straight into the arena) or double (converted on the device). Host buffers passed to
 // submit() must stay valid (and should be pinned) until sync().
+// Double host audio (the reference's AudioBuffer type) crosses PCIe as double and is converted
+// on the device (default). With `host_threads` > 0 it is converted to/from fp32 on host
+// worker threads instead, halving PCIe bytes (sources in submit(), outputs on a completion
+// thread once their D2H landed); measured slower on the B200 boxes' hosts (config 2: 0.77 vs
+// 0.66 ms per render with 8 threads), so the default (< 0: MGB_PIPELINE_HOST_THREADS or 0)
+// keeps device conversion.
 class RenderPipeline {
  public:
   RenderPipeline(const DevicePlan& plan, const ProcessorSet& processors, int batch, long length, bool f32_io,
-                 int depth = 2);
+                 int depth = 2, int host_threads = -1);
   ~RenderPipeline();
   RenderPipeline(const RenderPipeline&) = delete;
   RenderPipeline& operator=(const RenderPipeline&) = delete;
@@ -240,6 +246,8 @@ class RenderPipeline {
   std::vector<std::unique_ptr<Slot>> slots_;
   cudaStream_t h2d_ = nullptr, compute_ = nullptr, d2h_ = nullptr;
   std::size_t next_ = 0;
+  struct HostConvert;  // worker pool + completion thread (double host audio)
+  std::unique_ptr<HostConvert> conv_;
 };
 
 // Renders a stream of plans whose topology changes every batch (BASELINE config 3: 64

@@ -490,3 +490,34 @@ def test_config4_large_graph_full_size(mg, ref):
         if k == 37:
             want = ref.Plan(t1, e1, 1).render(p1, src[k:k + 1])
             assert rel(y1, want) < TOL
+
+
+@pytest.mark.parametrize("L", [8192, 7000])
+def test_fused_kernel_rows_match_separate_pass(mg, ref, L):
+    # Large conv steps transform the kernel rows inside the signal's row pass; forced both
+    # ways on a console the renders agree, and so do the backward passes.
+    import torch
+    t, e = ref.console(6, 0.0, 4)
+    params = ref.random_legal_params(t, e, 5)
+    rd = mg.compute_render_data(make(mg, t, e))
+    procs = mg.ProcessorSet()
+    P = rd.reorder_params(params)
+    src = np.random.default_rng(L).uniform(-1, 1, size=(rd.num_inputs, 1, 2, L))
+    res = []
+    try:
+        for mode in (0, 1):
+            mg.set_conv_fuse(mode)
+            dr = mg.DeviceRenderer(rd, procs, 1, L, P, backward=True)
+            dr.sources.copy_(torch.as_tensor(src, dtype=torch.float32))
+            out = dr.render().clone()
+            w = torch.ones_like(out)
+            g, gs = dr.backward(w)
+            torch.cuda.synchronize()
+            res.append((out.cpu().numpy(), {k: v.cpu().numpy() for k, v in g.items()}, gs.cpu().numpy()))
+    finally:
+        mg.set_conv_fuse(-1)
+    (o0, g0, s0), (o1, g1, s1) = res
+    assert rel(o1, o0) < 1e-5 and rel(s1, s0) < 1e-5
+    for k in g0:
+        assert rel(g1[k], g0[k]) < 1e-4, k  # fp32 noise of small delay gradients (see test_backward_gpu)
+    assert rel(o0, ref.Plan(t, e, 1).render(params, src)) < TOL
