@@ -242,8 +242,14 @@ void run_prologue(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, voi
 }
 
 // One step's audio pass. a.params points at the step's first parameter row.
+// `join`: the step's prologue event when it has not been waited on yet (conv steps join
+// after their signal column pass; every other type joins first).
 void run_main(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, void* pws, void* mws, void* sws, bool zero_sync,
-              cudaStream_t s) {
+              cudaStream_t s, cudaEvent_t join = nullptr) {
+  if (join && t != NodeType::Reverb && t != NodeType::Delay) {
+    cuda_check(cudaStreamWaitEvent(s, join, 0), "wait");
+    join = nullptr;
+  }
   switch (t) {
     case NodeType::In:
     case NodeType::Out:
@@ -258,8 +264,8 @@ void run_main(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, void* p
       mgb::launch_dynamics(t == NodeType::Noisegate, a, p.config().envelope_taps, p.config().energy_floor, sws, zero_sync,
                            s);
       break;
-    case NodeType::Reverb: mgb::launch_conv_main(a, p.reverb_length(), pws, mws, s); break;
-    case NodeType::Delay: mgb::launch_conv_main(a, p.delay_span(), pws, mws, s); break;
+    case NodeType::Reverb: mgb::launch_conv_main(a, p.reverb_length(), pws, mws, s, join); break;
+    case NodeType::Delay: mgb::launch_conv_main(a, p.delay_span(), pws, mws, s, join); break;
   }
 }
 
@@ -376,6 +382,9 @@ DevicePlan::DevicePlan(const RenderData& rd) : rd_(rd) {
   for (auto& a : aux_) cuda_check(cudaStreamCreateWithPriority(&a, cudaStreamNonBlocking, least), "cudaStreamCreate");
   events_.resize(rd.steps.size() + 1);
   for (auto& ev : events_) cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+  cuda_check(cudaStreamCreateWithPriority(&lane_, cudaStreamNonBlocking, greatest), "cudaStreamCreate");
+  lane_events_.resize(2 * rd.steps.size());
+  for (auto& ev : lane_events_) cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
 }
 
 DevicePlan::DevicePlan(const RenderData& rd, Deferred) : rd_(rd), owned_(false) { build_index(); }
@@ -389,6 +398,8 @@ void DevicePlan::attach(const int* device_index, const std::array<cudaStream_t, 
 DevicePlan::~DevicePlan() {
   if (!owned_) return;
   for (cudaEvent_t ev : events_) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : lane_events_) cudaEventDestroy(ev);
+  if (lane_) cudaStreamDestroy(lane_);
   for (cudaStream_t a : aux_) if (a) cudaStreamDestroy(a);
   if (d_index_) cudaFree(const_cast<int*>(d_index_));
 }
@@ -398,9 +409,43 @@ const int* DevicePlan::col(int step) const { return d_index_ + col_off_[static_c
 const int* DevicePlan::t_row_ptr(int step) const { return d_index_ + trp_off_[static_cast<std::size_t>(step)]; }
 const int* DevicePlan::t_col(int step) const { return d_index_ + tcol_off_[static_cast<std::size_t>(step)]; }
 
+namespace {
+// Steps k and k+1 may run side by side (two streams) when both are long convolutions whose
+// grids are small (the kernel spectra fit L2: under one or two waves per pass, e.g. config 2's
+// 12 reverbs and 7 delays) and step k+1 reads none of step k's output rows.
+bool pairable(const RenderData& rd, std::size_t k, long length, const ProcessorSet& p) {
+  if (k + 1 >= rd.steps.size()) return false;
+  static const bool off = [] { const char* v = std::getenv("MGB_NO_LANES"); return v && v[0] == '1'; }();
+  if (off) return false;
+  const StepIndex& a = rd.steps[k];
+  const StepIndex& b = rd.steps[k + 1];
+  auto conv = [](NodeType t) { return t == NodeType::Reverb || t == NodeType::Delay; };
+  if (!conv(a.type) || !conv(b.type)) return false;
+  for (const StepIndex* st : {&a, &b}) {
+    const long taps = st->type == NodeType::Reverb ? p.reverb_length() : p.delay_span();
+    if (mgb::conv_fuse_kernel_rows(mgb::conv_geom(length, taps), st->store_end - st->store_begin)) return false;
+  }
+  for (int g : b.gather) {
+    if (g >= a.store_begin && g < a.store_end) return false;
+  }
+  return true;
+}
+}  // namespace
+
 DevicePlan::Layout DevicePlan::layout(int batch, long length, const ProcessorSet& procs) const {
   Layout l;
-  std::size_t off = 0, main = 256;
+  std::size_t off = 0, main = 256, main2 = 0;
+  l.paired.assign(rd_.steps.size(), 0);
+  if (owned_) {
+    for (std::size_t k = 0; k + 1 < rd_.steps.size(); ++k) {
+      if (pairable(rd_, k, length, procs)) {
+        l.paired[k] = 1;
+        const StepIndex& b = rd_.steps[k + 1];
+        main2 = std::max(main2, main_bytes(b.type, b.store_end - b.store_begin, batch, length, procs));
+        ++k;
+      }
+    }
+  }
   for (const StepIndex& st : rd_.steps) {
     const int slots = st.store_end - st.store_begin;
     l.prologue_off.push_back(off);
@@ -414,7 +459,8 @@ DevicePlan::Layout DevicePlan::layout(int batch, long length, const ProcessorSet
   }
   l.sync_bytes = off - l.sync_begin;
   l.main_off = off;
-  l.total = off + align256(main);
+  l.main2_off = off + align256(main);
+  l.total = l.main2_off + align256(main2);
   return l;
 }
 
@@ -509,9 +555,12 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
     int next = 0;  // independent prologues round-robin over the side streams
     for (std::size_t k = 0; k < rd.steps.size(); ++k) {
       if (!has_prologue(rd.steps[k].type)) continue;
-      // One side stream: prologues then complete in the order their steps need them (more
-      // side streams let later prologues steal SMs from earlier ones; measured slower).
-      cudaStream_t a = plan.aux_streams()[0];
+      // Prologues complete in the order their steps need them on side stream 0, except the
+      // delay's, which gets side stream 1 and so runs beside the reverb's (the delay step's
+      // kernel spectrum was the critical path once conv steps joined their prologue late:
+      // 0.324 -> 0.309 ms per config-2 render). MGB_SIDE_STREAMS=1 restores one stream.
+      static const int nside = [] { const char* v = std::getenv("MGB_SIDE_STREAMS"); return v ? std::atoi(v) : 2; }();
+      cudaStream_t a = plan.aux_streams()[nside >= 2 && rd.steps[k].type == NodeType::Delay ? 1 : 0];
       ++next;
       run_prologue(rd.steps[k].type, args[k], procs, ws + lay.prologue_off[k], a);
       cuda_check(cudaEventRecord(ev[k + 1], a), "event");
@@ -536,6 +585,24 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
       k += static_cast<std::size_t>(chain - 1);
       continue;
     }
+    if (!step_events && lay.paired[k]) {
+      // Steps k and k+1 side by side: k on the lane, k+1 on the main stream, then join.
+      const cudaEvent_t* le = plan.lane_events();
+      cudaStream_t lane = plan.lane();
+      cuda_check(cudaEventRecord(le[2 * k], stream), "event");
+      cuda_check(cudaStreamWaitEvent(lane, le[2 * k], 0), "wait");
+      for (std::size_t j = k; j <= k + 1; ++j) {
+        cudaStream_t st = j == k ? lane : stream;
+        const NodeType tj = rd.steps[j].type;
+        if (!hoist) run_prologue(tj, args[j], procs, ws + lay.prologue_off[j], st);
+        run_main(tj, args[j], procs, ws + lay.prologue_off[j], ws + (j == k ? lay.main_off : lay.main2_off),
+                 ws + lay.sync_off[j], false, st, hoist ? ev[j + 1] : nullptr);
+      }
+      cuda_check(cudaEventRecord(le[2 * k + 1], lane), "event");
+      cuda_check(cudaStreamWaitEvent(stream, le[2 * k + 1], 0), "wait");
+      ++k;
+      continue;
+    }
     char* pws = ws + lay.prologue_off[k];
     char* mws = ws + lay.main_off;
     // The first step has nothing to hide its prologue behind: an EQ there runs its
@@ -543,13 +610,14 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
     const bool split_eq = split_first && k == 0;
     if (step_events) cuda_check(cudaEventRecord(step_events[2 * k], stream), "event");
     // (forward FFTs of a split first EQ were enqueued before the prologues, see above)
-    if (hoist && has_prologue(t)) cuda_check(cudaStreamWaitEvent(stream, ev[k + 1], 0), "wait");
+    const cudaEvent_t join = hoist && has_prologue(t) ? ev[k + 1] : nullptr;
     if (!hoist) run_prologue(t, args[k], procs, pws, stream);
     if (split_eq) {
+      cuda_check(cudaStreamWaitEvent(stream, join, 0), "wait");
       mgb::launch_eq_inverse(args[k], reinterpret_cast<float*>(pws + eq_taps_bytes(args[k].slots)),
                              reinterpret_cast<float2*>(mws), stream);
     } else {
-      run_main(t, args[k], procs, pws, mws, ws + lay.sync_off[k], false, stream);
+      run_main(t, args[k], procs, pws, mws, ws + lay.sync_off[k], false, stream, join);
     }
     if (step_events) cuda_check(cudaEventRecord(step_events[2 * k + 1], stream), "event");
   }

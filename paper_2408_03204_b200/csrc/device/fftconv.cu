@@ -992,13 +992,19 @@ void launch_conv_prologue(bool reverb, const StepArgs& a, const ReverbConst& rc,
   }
 }
 
-void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, void* ws, cudaStream_t s) {
-  if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
+void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, void* ws, cudaStream_t s,
+                      cudaEvent_t kernel_ready) {
+  if (a.slots == 0 || a.batch == 0 || a.length == 0) {
+    if (kernel_ready) cudaStreamWaitEvent(s, kernel_ready, 0);
+    return;
+  }
   const ConvGeom g = conv_geom(a.length, taps);
   const auto* P = reinterpret_cast<const float2*>(static_cast<const char*>(prologue_ws) + ir_bytes(a.slots, taps));
   auto* X = static_cast<float2*>(ws);
   const int items = a.slots * a.batch;
   MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, a, nullptr, 0, g, items, X, 0, s);
+  // The signal's column pass needs no kernel spectrum: join the prologue only here.
+  if (kernel_ready) cudaStreamWaitEvent(s, kernel_ready, 0);
   if (conv_fuse_kernel_rows(g, a.slots)) {
     MGB_DISPATCH_LN(g.log_n2, rows_conv_fk_t, g, items, a.batch, X, P, a.tw, s);
   } else {

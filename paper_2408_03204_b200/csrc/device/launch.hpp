@@ -88,7 +88,9 @@ std::size_t conv_prologue_bytes(const ConvGeom& g, int slots, long taps);
 std::size_t conv_main_bytes(const ConvGeom& g, int slots, int batch);
 void launch_conv_prologue(bool reverb, const StepArgs& a, const ReverbConst& rc, const DelayConst& dc, void* ws,
                           cudaStream_t s);
-void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, void* ws, cudaStream_t s);
+// kernel_ready (optional): event of the prologue, waited on after the signal's column pass.
+void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, void* ws, cudaStream_t s,
+                      cudaEvent_t kernel_ready = nullptr);
 
 // Backward of a reverb / delay step: dX = correlation with the kernel (stored into bw.dst),
 // kernel gradient = correlation of dY with X, then through the IR build / tap FIRs into

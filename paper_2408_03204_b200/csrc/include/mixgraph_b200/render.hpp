@@ -155,10 +155,15 @@ class DevicePlan {
     std::vector<std::size_t> sync_off;  // per step: scan tickets / pass counters (zeroed per render)
     std::size_t sync_begin = 0, sync_bytes = 0;
     std::size_t main_off = 0;
+    std::size_t main2_off = 0;  // second transient region (a step run concurrently with its predecessor)
+    std::vector<char> paired;   // paired[k]: step k runs on the lane beside step k + 1
     std::size_t total = 0;
   };
   Layout layout(int batch, long length, const ProcessorSet& procs) const;
   const std::array<cudaStream_t, 4>& aux_streams() const { return aux_; }
+  // Second high-priority stream for a pair of independent, small conv steps (owned plans only).
+  cudaStream_t lane() const { return lane_; }
+  const cudaEvent_t* lane_events() const { return lane_events_.data(); }
   const cudaEvent_t* events() const { return borrowed_events_ ? borrowed_events_ : events_.data(); }
 
  private:
@@ -167,6 +172,8 @@ class DevicePlan {
   bool owned_ = true;
   std::array<cudaStream_t, 4> aux_{};  // low-priority side streams for the prologues
   std::vector<cudaEvent_t> events_;  // [0] fork, [k+1] prologue of step k done
+  cudaStream_t lane_ = nullptr;
+  std::vector<cudaEvent_t> lane_events_;  // [2k] fork before step k, [2k+1] step k done
   const cudaEvent_t* borrowed_events_ = nullptr;
   const int* d_index_ = nullptr;
   std::vector<int> host_;

@@ -46,21 +46,18 @@ def main():
         torch.cuda.synchronize()
     evs = [e for e in prof.events() if e.device_type.name == "CUDA" and e.time_range.elapsed_us() > 0]
     evs.sort(key=lambda e: e.time_range.start)
-    # split into the 3 renders by large gaps; report the last one
-    groups, cur = [], [evs[0]]
-    for a, b in zip(evs, evs[1:]):
-        if b.time_range.start - a.time_range.end > 30:
-            groups.append(cur)
-            cur = []
-        cur.append(b)
-    groups.append(cur)
+    # split into the 3 renders at each render's first kernel (eq_mags of the first step's
+    # prologue); report the last one
+    firsts = [i for i, e in enumerate(evs) if "eq_mags" in e.name]
+    starts = firsts[::2] if len(firsts) >= 6 else firsts
+    groups = [evs[a:b] for a, b in zip(starts, starts[1:] + [len(evs)])]
     last = groups[-1]
     t0 = last[0].time_range.start
     end = max(e.time_range.end for e in last)
     print(f"renders seen: {len(groups)}; last render span {end - t0:.1f} us, {len(last)} kernels")
     for e in last:
         name = e.name.replace("void ", "").replace("mgb::(anonymous namespace)::", "")[:60]
-        print(f"{e.time_range.start - t0:8.1f} {e.time_range.elapsed_us():8.1f}  {name}")
+        print(f"{e.time_range.start - t0:8.1f} {e.time_range.elapsed_us():8.1f} {e.time_range.end - t0:8.1f}  {name}")
 
 
 if __name__ == "__main__":
