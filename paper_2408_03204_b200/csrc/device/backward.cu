@@ -68,14 +68,84 @@ __global__ void __launch_bounds__(kPgThreads) pw_param_grad(StepArgs fw, StepArg
   }
 }
 
-// grid (slots) x 32: grad[slot][j] = sum over rows_per_slot partial rows (fixed order).
+// Gain / imager backward in one pass (L % 4 == 0): gather dY over the consumer CSR (float4),
+// dX = e^p dY (gain) or M dY (imager, M symmetric) stored into bw.dst, and the per-block
+// partial sums of the parameter gradient (dY . Y). grid (ceil(L/4 / kPbThreads), slots*B).
+constexpr int kPbThreads = 128;
+template <PointOp OP>
+__global__ void __launch_bounds__(kPbThreads) pointwise_bwd(StepArgs fw, StepArgs bw, double* out) {
+  __shared__ double red[kPbThreads / 32][2];
+  const int sb = blockIdx.y;
+  const int slot = sb / fw.batch, b = sb - slot * fw.batch;
+  const long n4 = fw.length >> 2;
+  const long i = blockIdx.x * static_cast<long>(kPbThreads) + threadIdx.x;
+  double s0 = 0.0, s1 = 0.0;
+  if (i < n4) {
+    const int e0 = __ldg(bw.row_ptr + slot), e1 = __ldg(bw.row_ptr + slot + 1);
+    const long boff = static_cast<long>(b) * 2 * fw.length;
+    float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
+    for (int e = e0; e < e1; ++e) {
+      const float4* p = reinterpret_cast<const float4*>(bw.src + static_cast<long>(__ldg(bw.col + e)) * bw.rowstride + boff);
+      l = f4add(l, __ldg(p + i));
+      r = f4add(r, __ldg(p + n4 + i));
+    }
+    const float4* y = reinterpret_cast<const float4*>(fw.dst + static_cast<long>(slot) * fw.rowstride + boff);
+    const float4 yl = __ldg(y + i), yr = __ldg(y + n4 + i);
+    float4 ol, orr;
+    if constexpr (OP == PointOp::Gain) {
+      const float g0 = static_cast<float>(exp(fw.params[2 * slot])), g1 = static_cast<float>(exp(fw.params[2 * slot + 1]));
+      s0 = static_cast<double>(l.x * yl.x + l.y * yl.y + l.z * yl.z + l.w * yl.w);
+      s1 = static_cast<double>(r.x * yr.x + r.y * yr.y + r.z * yr.z + r.w * yr.w);
+      ol = make_float4(g0 * l.x, g0 * l.y, g0 * l.z, g0 * l.w);
+      orr = make_float4(g1 * r.x, g1 * r.y, g1 * r.z, g1 * r.w);
+    } else {
+      const float g = static_cast<float>(exp(fw.params[slot]));
+      s0 = 0.5 * static_cast<double>((l.x - r.x) * (yl.x - yr.x) + (l.y - r.y) * (yl.y - yr.y) +
+                                     (l.z - r.z) * (yl.z - yr.z) + (l.w - r.w) * (yl.w - yr.w));
+      auto mix = [g](float a, float c, float& u, float& w) {
+        const float m = a + c, sd = g * (a - c);
+        u = 0.5f * (m + sd);
+        w = 0.5f * (m - sd);
+      };
+      mix(l.x, r.x, ol.x, orr.x);
+      mix(l.y, r.y, ol.y, orr.y);
+      mix(l.z, r.z, ol.z, orr.z);
+      mix(l.w, r.w, ol.w, orr.w);
+    }
+    float4* d = reinterpret_cast<float4*>(bw.dst + static_cast<long>(slot) * bw.rowstride + boff);
+    d[i] = ol;
+    d[n4 + i] = orr;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, off);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[warp][0] = s0;
+    red[warp][1] = s1;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double t = 0.0;
+    for (int w = 0; w < kPbThreads / 32; ++w) t += red[w][threadIdx.x];
+    out[(static_cast<long>(sb) * gridDim.x + blockIdx.x) * 2 + threadIdx.x] = t;
+  }
+}
+
+// grid (slots) x 32: grad[slot][j] = sum over rows_per_slot partial rows; for narrow tables
+// (width <= 2) one warp per column, lanes strided over the rows, xor-tree in fixed order.
 __global__ void reduce_partials(const double* partial, int rows_per_slot, int stride, int width, double* grad,
                                 int grad_width) {
   const int slot = blockIdx.x;
-  for (int j = threadIdx.x; j < width; j += blockDim.x) {
+  const double* p = partial + static_cast<long>(slot) * rows_per_slot * stride;
+  for (int j = 0; j < width; ++j) {
     double t = 0.0;
-    for (int r = 0; r < rows_per_slot; ++r) t += partial[(static_cast<long>(slot) * rows_per_slot + r) * stride + j];
-    grad[static_cast<long>(slot) * grad_width + j] = t;
+    for (int r = threadIdx.x; r < rows_per_slot; r += 32) t += p[static_cast<long>(r) * stride + j];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if (threadIdx.x == 0) grad[static_cast<long>(slot) * grad_width + j] = t;
   }
 }
 
@@ -98,28 +168,37 @@ __device__ __forceinline__ void load_window(const StepArgs& a, int e0, int e1, i
   }
 }
 
-// dh[j] for one output block: with W = x[out0 - 1024 + u] (u < 8192) and D = dy[out0 + v]
-// (v < 6144, zero-padded), sum_v D[v] W[v + s] = IFFT(conj(D^) W^)[s]; tap j = 2047 - s.
-// Channels packed as re/im: the real part of the product sums both channels' correlations.
-// grid (blocks, slots*B); out[(sb * gridDim.x + blk) * 2048 + j].
-__global__ void __launch_bounds__(kCorrThreads, 1) eq_corr(StepArgs fw, StepArgs bw, float* out) {
-  extern __shared__ float2 buf[];  // [2][kCorrFS]: window, dy block
+// dh[j] over `per` consecutive output blocks: with W = x[out0 - 1024 + u] (u < 8192) and
+// D = dy[out0 + v] (v < 6144, zero-padded), sum_v D[v] W[v + s] = IFFT(conj(D^) W^)[s]; tap
+// j = 2047 - s. The product spectra of the CTA's blocks are summed (fixed order) before ONE
+// inverse transform. Channels packed as re/im: the real part of the product sums both
+// channels' correlations. grid (ceil(blocks / per), slots*B); out[(sb * gridDim.x + cta) * 2048 + j].
+__global__ void __launch_bounds__(kCorrThreads, 1) eq_corr(StepArgs fw, StepArgs bw, int per, float* out) {
+  extern __shared__ float2 buf[];  // [3][kCorrFS]: window, dy block, accumulated product
   const int sb = blockIdx.y;
   const int slot = sb / fw.batch, b = sb - slot * fw.batch;
-  const long out0 = static_cast<long>(blockIdx.x) * kCorrOut;
-  load_window(fw, __ldg(fw.row_ptr + slot), __ldg(fw.row_ptr + slot + 1), b, out0 - (kEqHalf + 1), kCorrFft, buf);
-  load_window(bw, __ldg(bw.row_ptr + slot), __ldg(bw.row_ptr + slot + 1), b, out0, kCorrOut, buf + kCorrFS);
-  __syncthreads();
-  fft_pow2<kCorrLog, 2, kCorrThreads, -1>(buf, kCorrFS, fw.tw);
-  for (int k = threadIdx.x; k < kCorrFft; k += kCorrThreads) {
-    const float2 w = buf[sidx(k)], d = buf[kCorrFS + sidx(k)];
-    buf[kCorrFS + sidx(k)] = cmul(cconj(d), w);
+  float2* acc = buf + 2 * kCorrFS;
+  for (int k = threadIdx.x; k < kCorrFft; k += kCorrThreads) acc[sidx(k)] = make_float2(0.f, 0.f);
+  const long nblk = (fw.length + kCorrOut - 1) / kCorrOut;
+  const int fe0 = __ldg(fw.row_ptr + slot), fe1 = __ldg(fw.row_ptr + slot + 1);
+  const int be0 = __ldg(bw.row_ptr + slot), be1 = __ldg(bw.row_ptr + slot + 1);
+  for (long blk = static_cast<long>(blockIdx.x) * per; blk < nblk && blk < static_cast<long>(blockIdx.x + 1) * per; ++blk) {
+    const long out0 = blk * kCorrOut;
+    __syncthreads();  // previous block's buffers consumed
+    load_window(fw, fe0, fe1, b, out0 - (kEqHalf + 1), kCorrFft, buf);
+    load_window(bw, be0, be1, b, out0, kCorrOut, buf + kCorrFS);
+    __syncthreads();
+    fft_pow2<kCorrLog, 2, kCorrThreads, -1>(buf, kCorrFS, fw.tw);
+    for (int k = threadIdx.x; k < kCorrFft; k += kCorrThreads) {
+      const float2 w = buf[sidx(k)], d = buf[kCorrFS + sidx(k)];
+      acc[sidx(k)] = cadd(acc[sidx(k)], cmul(cconj(d), w));
+    }
   }
   __syncthreads();
-  fft_pow2<kCorrLog, 1, kCorrThreads, +1>(buf + kCorrFS, kCorrFS, fw.tw);
+  fft_pow2<kCorrLog, 1, kCorrThreads, +1>(acc, kCorrFS, fw.tw);
   float* o = out + (static_cast<long>(sb) * gridDim.x + blockIdx.x) * 2048;
   for (int j = threadIdx.x; j < 2 * kEqHalf + 1; j += kCorrThreads) {
-    o[j] = buf[kCorrFS + sidx(2 * kEqHalf + 1 - j)].x * (1.f / kCorrFft);
+    o[j] = acc[sidx(2 * kEqHalf + 1 - j)].x * (1.f / kCorrFft);
   }
 }
 
@@ -223,8 +302,22 @@ void launch_sgd_step(bool dynamics, double* table, const double* grad, long n, d
 }
 
 std::size_t pw_grad_bytes(int slots, int batch, long length) {
-  const long blocks = (length + kPgThreads * kPgPer - 1) / (kPgThreads * kPgPer);
+  const long blocks = std::max((length + kPgThreads * kPgPer - 1) / (kPgThreads * kPgPer),
+                               (length / 4 + kPbThreads - 1) / kPbThreads);
   return sizeof(double) * 2 * static_cast<std::size_t>(slots) * batch * blocks;
+}
+
+bool launch_pointwise_backward(PointOp op, const StepArgs& fw, const StepArgs& bw, void* ws, double* grad,
+                               cudaStream_t s) {
+  if (fw.length % 4 != 0 || op == PointOp::Copy || fw.slots == 0) return false;
+  const long blocks = (fw.length / 4 + kPbThreads - 1) / kPbThreads;
+  const dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(fw.slots * fw.batch));
+  auto* part = static_cast<double*>(ws);
+  if (op == PointOp::Gain) pointwise_bwd<PointOp::Gain><<<grid, kPbThreads, 0, s>>>(fw, bw, part);
+  else pointwise_bwd<PointOp::Imager><<<grid, kPbThreads, 0, s>>>(fw, bw, part);
+  const int width = op == PointOp::Gain ? 2 : 1;
+  reduce_partials<<<fw.slots, 32, 0, s>>>(part, static_cast<int>(blocks) * fw.batch, 2, width, grad, width);
+  return true;
 }
 
 void launch_pointwise_param_grad(PointOp op, const StepArgs& fw, const StepArgs& bw, void* ws, double* grad,
@@ -247,15 +340,20 @@ std::size_t eq_grad_bytes(int slots, int batch, long length) {
 void launch_eq_param_grad(const StepArgs& fw, const StepArgs& bw, void* ws, double* grad, cudaStream_t s) {
   if (fw.slots == 0) return;
   static const bool done = [] {
-    cudaFuncSetAttribute(eq_corr, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kCorrFS * 8);
+    cudaFuncSetAttribute(eq_corr, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * kCorrFS * 8);
     return true;
   }();
   (void)done;
   const long blocks = (fw.length + kCorrOut - 1) / kCorrOut;
+  // Blocks per CTA: fewer inverse transforms, but >= 8 waves of CTAs (1 per SM) over the step.
+  const long items = static_cast<long>(fw.slots) * fw.batch;
+  long per = std::max<long>(1, blocks * items / (8L * 148));
+  per = std::min(per, blocks);
+  const long ctas = (blocks + per - 1) / per;
   auto* part = static_cast<float*>(ws);
-  eq_corr<<<dim3(static_cast<unsigned>(blocks), static_cast<unsigned>(fw.slots * fw.batch)), kCorrThreads,
-            2 * kCorrFS * 8, s>>>(fw, bw, part);
-  eq_grad<<<fw.slots, 1024, 0, s>>>(part, static_cast<int>(blocks) * fw.batch, fw.params, cos_table(fw.tw), grad);
+  eq_corr<<<dim3(static_cast<unsigned>(ctas), static_cast<unsigned>(items)), kCorrThreads, 3 * kCorrFS * 8, s>>>(
+      fw, bw, static_cast<int>(per), part);
+  eq_grad<<<fw.slots, 1024, 0, s>>>(part, static_cast<int>(ctas) * fw.batch, fw.params, cos_table(fw.tw), grad);
 }
 
 }  // namespace mgb

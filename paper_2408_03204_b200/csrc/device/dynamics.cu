@@ -33,7 +33,8 @@ struct DynParams {
 
 struct DynBwd {
   StepArgs fw, bw;     // forward (arena, forward CSR, params) / backward (input grads, consumer CSR)
-  const float* env;    // [seq][L] envelope from the forward scan
+  float* env;          // [seq][L] envelope from the forward scan; pass A overwrites it with the gain
+  float* dg;           // [seq][L] dL/d(envelope)
   float2* agg;         // [seq][tiles] tile map vectors (pass 0)
   float2* carry;       // [seq][tiles] (w, v) at each tile's right end
   double* partial;     // [seq][tiles][5]
@@ -314,9 +315,10 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
 //   v[m] = a v[m+1] + w[m+1] - Ne a^(Ne-1) dg[m+Ne]        (v = d w / d a),
 //   du_c = gain dy_c + 2 mid de,
 //   d a = -sum dg g / (1-a) + (1-a) sum e v,  dT/dW/dR = sum dD dG_y/d{T,W,R}.
-// (w, v) is a reverse scan of affine maps with matrix [[a,0],[1,a]]^k = [[a^k,0],[k a^(k-1),a^k]]:
-// pass 0 reduces each tile to its map, dyn_bwd_carry chains the tiles per sequence (fp64,
-// serial, fixed order), pass 1 replays each tile from its carry. Deterministic.
+// (w, v) is a reverse scan of affine maps with matrix [[a,0],[1,a]]^k = [[a^k,0],[k a^(k-1),a^k]].
+// Passes: the forward scan re-stores the envelope; A computes dg (stored) and the gain (over
+// the envelope); B reduces each tile to its map; dyn_bwd_carry chains the tiles per sequence
+// (fp64, serial, fixed order); D replays each tile from its carry. Deterministic.
 struct DynMap {
   float p, q, cw, cv;
 };
@@ -367,21 +369,32 @@ __device__ __forceinline__ float knee_grad(float gu, const DynParams& p, float d
   return 1.f + k * h;
 }
 
-// Per-sample local gradient terms at kDynPerThread consecutive samples from n0.
+// Pass A: per sample dg = dG_u / g and the gain (overwrites the stored envelope in place),
+// per-tile partial sums of dD dG_y/d{T,W,R} and dg g. grid (tiles, seqs)
 template <bool GATE, bool VEC>
-__device__ __forceinline__ void dyn_local(const DynBwd& d, const DynParams& p, int fe0, int fe1, int be0, int be1, int seq,
-                                          int b, long n0, float* ul, float* ur, float* dyl, float* dyr, float* gain,
-                                          float* dg, float* acc, float* dgg) {
-  load16<VEC>(d.fw, fe0, fe1, b, n0, ul, ur);
-  load16<VEC>(d.bw, be0, be1, b, n0, dyl, dyr);
+__global__ void __launch_bounds__(kDynThreads, 2) dyn_bwd_dg(DynBwd d) {
+  __shared__ DynParams s_p;
+  __shared__ double red[kDynThreads / 32][4];
+  const int tile = blockIdx.x, seq = blockIdx.y;
+  const int slot = seq / d.fw.batch, b = seq - slot * d.fw.batch;
+  if (threadIdx.x < 32) derive_params(d.fw.params + 4L * slot, d.env_taps, d.floor_, d.fw.length, threadIdx.x, &s_p);
+  __syncthreads();
+  const DynParams p = s_p;
   const long L = d.fw.length;
+  const long n0 = static_cast<long>(tile) * kDynTile + static_cast<long>(threadIdx.x) * kDynPerThread;
+  constexpr int K = kDynPerThread;
+  float ul[K], ur[K], dyl[K], dyr[K];
+  load16<VEC>(d.fw, __ldg(d.fw.row_ptr + slot), __ldg(d.fw.row_ptr + slot + 1), b, n0, ul, ur);
+  load16<VEC>(d.bw, __ldg(d.bw.row_ptr + slot), __ldg(d.bw.row_ptr + slot + 1), b, n0, dyl, dyr);
+  float acc[3] = {0.f, 0.f, 0.f};
+  float dgg = 0.f;
+  float* env = d.env + static_cast<long>(seq) * L;
+  float* dgo = d.dg + static_cast<long>(seq) * L;
 #pragma unroll
-  for (int k = 0; k < kDynPerThread; ++k) {
+  for (int k = 0; k < K; ++k) {
     const long n = n0 + k;
-    dg[k] = 0.f;
-    gain[k] = 0.f;
-    if (n < 0 || n >= L) continue;
-    const float g = __ldg(d.env + static_cast<long>(seq) * L + n);
+    if (n >= L) break;
+    const float g = env[n];
     const float gu = logf(fmaxf(g, p.floor_));
     float gy;
     if (!GATE) {
@@ -393,65 +406,89 @@ __device__ __forceinline__ void dyn_local(const DynBwd& d, const DynParams& p, i
       else if (gu < p.T - p.W) gy = p.T + p.R * (gu - p.T);
       else { const float q = gu - p.T - p.W; gy = gu + (1.f - p.R) * q * q / (4.f * p.W); }
     }
-    gain[k] = expf(gy - gu);
-    const float dD = (dyl[k] * ul[k] + dyr[k] * ur[k]) * gain[k];
-    float tmp[3] = {0.f, 0.f, 0.f};
-    const float slope = knee_grad<GATE>(gu, p, dD, acc ? acc : tmp);
-    const float dgu = dD * (slope - 1.f);
-    dg[k] = g > p.floor_ ? dgu / g : 0.f;
-    if (dgg) *dgg += dg[k] * g;
+    const float gain = expf(gy - gu);
+    const float dD = (dyl[k] * ul[k] + dyr[k] * ur[k]) * gain;
+    const float slope = knee_grad<GATE>(gu, p, dD, acc);
+    const float dg = g > p.floor_ ? dD * (slope - 1.f) / g : 0.f;
+    dgg += dg * g;
+    env[n] = gain;
+    dgo[n] = dg;
+  }
+  double vals[4] = {acc[0], acc[1], acc[2], dgg};
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) vals[j] += __shfl_xor_sync(0xffffffffu, vals[j], off);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) red[warp][j] = vals[j];
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double t = 0.0;
+    for (int w = 0; w < kDynThreads / 32; ++w) t += red[w][threadIdx.x];
+    d.partial[(static_cast<long>(seq) * d.tiles + tile) * 5 + threadIdx.x] = t;
   }
 }
 
-template <bool GATE, bool VEC, int PASS>
-__global__ void __launch_bounds__(kDynThreads) dyn_bwd(DynBwd d) {
+// dg at kDynPerThread samples from n0 (0 outside [0, L)).
+__device__ __forceinline__ void load_dg(const float* dg, long L, long n0, float* v) {
+#pragma unroll
+  for (int k = 0; k < kDynPerThread; ++k) {
+    const long n = n0 + k;
+    v[k] = (n >= 0 && n < L) ? __ldg(dg + n) : 0.f;
+  }
+}
+
+// Passes B (PASS 0: tile maps) and D (PASS 1: replay from the carry, du, sum e v) of the
+// reverse scan. grid (tiles, seqs)
+template <bool VEC, int PASS>
+__global__ void __launch_bounds__(kDynThreads, 2) dyn_bwd(DynBwd d) {
   __shared__ DynParams s_p;
   __shared__ DynMap wmap[kDynThreads / 32];
   __shared__ float2 s_carry;
-  __shared__ double red[kDynThreads / 32][5];
+  __shared__ double red[kDynThreads / 32];
   const int tile = blockIdx.x, seq = blockIdx.y;
   const int slot = seq / d.fw.batch, b = seq - slot * d.fw.batch;
   if (threadIdx.x < 32) derive_params(d.fw.params + 4L * slot, d.env_taps, d.floor_, d.fw.length, threadIdx.x, &s_p);
   if (PASS == 1 && threadIdx.x == 0) s_carry = d.carry[static_cast<long>(seq) * d.tiles + tile];
   __syncthreads();
   const DynParams p = s_p;
-  const int fe0 = __ldg(d.fw.row_ptr + slot), fe1 = __ldg(d.fw.row_ptr + slot + 1);
-  const int be0 = __ldg(d.bw.row_ptr + slot), be1 = __ldg(d.bw.row_ptr + slot + 1);
+  const long L = d.fw.length;
   const long n0 = static_cast<long>(tile) * kDynTile + static_cast<long>(threadIdx.x) * kDynPerThread;
   constexpr int K = kDynPerThread;
-  float ul[K], ur[K], dyl[K], dyr[K], gain[K], dg[K];
-  float acc[3] = {0.f, 0.f, 0.f}, dgg = 0.f;
-  dyn_local<GATE, VEC>(d, p, fe0, fe1, be0, be1, seq, b, n0, ul, ur, dyl, dyr, gain, dg, PASS ? acc : nullptr,
-                       PASS ? &dgg : nullptr);
-  // Truncation terms a^Ne dg[m+Ne] (skipped when a^Ne < 1e-30, as the forward does).
-  float ta[K], tb[K];
-  const float nb = p.aN != 0.f ? static_cast<float>(p.Ne) * p.aN / p.a : 0.f;
-#pragma unroll
-  for (int k = 0; k < K; ++k) ta[k] = tb[k] = 0.f;
+  const float* dgs = d.dg + static_cast<long>(seq) * L;
+  // a_k = dg[n] - a^Ne dg[n+Ne], b_k = -Ne a^(Ne-1) dg[n+Ne] (skipped when a^Ne < 1e-30).
+  float av[K], bv[K];
+  load_dg(dgs, L, n0, av);
   if (p.aN != 0.f) {
-    float u2l[K], u2r[K], d2l[K], d2r[K], g2[K], dg2[K];
-    dyn_local<GATE, VEC>(d, p, fe0, fe1, be0, be1, seq, b, n0 + p.Ne, u2l, u2r, d2l, d2r, g2, dg2, nullptr, nullptr);
+    float t2[K];
+    load_dg(dgs, L, n0 + p.Ne, t2);
+    const float nb = static_cast<float>(p.Ne) * p.aN / p.a;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      ta[k] = p.aN * dg2[k];
-      tb[k] = nb * dg2[k];
+      av[k] -= p.aN * t2[k];
+      bv[k] = -nb * t2[k];
     }
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k) bv[k] = 0.f;
   }
-  // This thread's map over its K samples (right end -> left end), from zero state.
   DynMap m;
   {
     float cw = 0.f, cv = 0.f;
 #pragma unroll
     for (int k = K - 1; k >= 0; --k) {
-      cv = fmaf(p.a, cv, cw - tb[k]);
-      cw = fmaf(p.a, cw, dg[k] - ta[k]);
+      cv = fmaf(p.a, cv, cw + bv[k]);
+      cw = fmaf(p.a, cw, av[k]);
     }
-    m.p = p.a16;  // a^K (derive_params: a16 holds a^kDynPerThread)
+    m.p = p.a16;
     m.q = static_cast<float>(K) * p.a16 / p.a;
     m.cw = cw;
     m.cv = cv;
   }
-  // Reverse inclusive scan: thread t gets F_t o F_t+1 o ... (within its warp), then warps.
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   DynMap inc = m;
 #pragma unroll
@@ -460,7 +497,7 @@ __global__ void __launch_bounds__(kDynThreads) dyn_bwd(DynBwd d) {
     if (lane + off < 32) inc = dmap_compose(inc, o);
   }
   if (lane == 0) wmap[warp] = inc;
-  DynMap exc = dmap_shfl_down(inc, 1);  // F_t+1 o ... o F_(warp end)
+  DynMap exc = dmap_shfl_down(inc, 1);
   if (lane == 31) exc = DynMap{1.f, 0.f, 0.f, 0.f};
   __syncthreads();
   if (warp == 0) {
@@ -471,14 +508,12 @@ __global__ void __launch_bounds__(kDynThreads) dyn_bwd(DynBwd d) {
       const DynMap o = dmap_shfl_down(t, off);
       if (lane + off < NW) t = dmap_compose(t, o);
     }
-    if (lane < NW) wmap[lane] = t;  // warp w: composition of warps w .. NW-1
+    if (lane < NW) wmap[lane] = t;
   }
   __syncthreads();
   if constexpr (PASS == 0) {
     if (threadIdx.x == 0) d.agg[static_cast<long>(seq) * d.tiles + tile] = make_float2(wmap[0].cw, wmap[0].cv);
-    return;
   } else {
-    // State at this thread's right end: warps after this one, then the lanes after it.
     float w = s_carry.x, v = s_carry.y;
     if (warp + 1 < kDynThreads / 32) {
       const DynMap t = wmap[warp + 1];
@@ -491,39 +526,42 @@ __global__ void __launch_bounds__(kDynThreads) dyn_bwd(DynBwd d) {
       v = fmaf(exc.q, w, fmaf(exc.p, v, exc.cv));
       w = w2;
     }
-    double ev = 0.0;
-    float* dl = d.bw.dst + static_cast<long>(slot) * d.bw.rowstride + static_cast<long>(b) * 2 * d.bw.length;
-    float* dr = dl + d.bw.length;
+    // Replay right to left: w[m], v[m] per sample.
+    float wv[K], vv[K];
 #pragma unroll
     for (int k = K - 1; k >= 0; --k) {
-      const float vn = fmaf(p.a, v, w - tb[k]);
-      w = fmaf(p.a, w, dg[k] - ta[k]);
+      const float vn = fmaf(p.a, v, w + bv[k]);
+      w = fmaf(p.a, w, av[k]);
       v = vn;
+      wv[k] = w;
+      vv[k] = v;
+    }
+    float ul[K], ur[K], dyl[K], dyr[K];
+    load16<VEC>(d.fw, __ldg(d.fw.row_ptr + slot), __ldg(d.fw.row_ptr + slot + 1), b, n0, ul, ur);
+    load16<VEC>(d.bw, __ldg(d.bw.row_ptr + slot), __ldg(d.bw.row_ptr + slot + 1), b, n0, dyl, dyr);
+    const float* gain = d.env + static_cast<long>(seq) * L;
+    float* dl = d.bw.dst + static_cast<long>(slot) * d.bw.rowstride + static_cast<long>(b) * 2 * L;
+    float* dr = dl + L;
+    double ev = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
       const long n = n0 + k;
-      if (n < d.fw.length) {
-        const float mid = ul[k] + ur[k];
-        const float dmid = 2.f * mid * (p.oma * w);
-        dl[n] = fmaf(gain[k], dyl[k], dmid);
-        dr[n] = fmaf(gain[k], dyr[k], dmid);
-        ev += static_cast<double>(mid * mid) * v;
-      }
+      if (n >= L) break;
+      const float mid = ul[k] + ur[k];
+      const float dmid = 2.f * mid * (p.oma * wv[k]);
+      const float gn = __ldg(gain + n);
+      dl[n] = fmaf(gn, dyl[k], dmid);
+      dr[n] = fmaf(gn, dyr[k], dmid);
+      ev += static_cast<double>(mid * mid) * vv[k];
     }
-    // Block reduction of [sum dD dGy/dT, /dW, /dR, sum dg g, sum e v] in fixed order.
-    double vals[5] = {acc[0], acc[1], acc[2], dgg, ev};
 #pragma unroll
-    for (int j = 0; j < 5; ++j) {
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) vals[j] += __shfl_xor_sync(0xffffffffu, vals[j], off);
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int j = 0; j < 5; ++j) red[warp][j] = vals[j];
-    }
+    for (int off = 16; off > 0; off >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, off);
+    if (lane == 0) red[warp] = ev;
     __syncthreads();
-    if (threadIdx.x < 5) {
+    if (threadIdx.x == 0) {
       double t = 0.0;
-      for (int w2 = 0; w2 < kDynThreads / 32; ++w2) t += red[w2][threadIdx.x];
-      d.partial[(static_cast<long>(seq) * d.tiles + tile) * 5 + threadIdx.x] = t;
+      for (int w2 = 0; w2 < kDynThreads / 32; ++w2) t += red[w2];
+      d.partial[(static_cast<long>(seq) * d.tiles + tile) * 5 + 4] = t;
     }
   }
 }
@@ -578,8 +616,8 @@ std::size_t dyn_bwd_bytes(int slots, int batch, long length) {
   const std::size_t seqs = static_cast<std::size_t>(slots) * batch;
   const std::size_t tiles = static_cast<std::size_t>((length + kDynTile - 1) / kDynTile);
   auto al = [](std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255); };
-  return al(sizeof(float) * seqs * length) + 2 * al(sizeof(float2) * seqs * tiles) + al(sizeof(double) * 5 * seqs * tiles) +
-         dyn_sync_bytes(slots, batch, length);
+  return 2 * al(sizeof(float) * seqs * length) + 2 * al(sizeof(float2) * seqs * tiles) +
+         al(sizeof(double) * 5 * seqs * tiles) + dyn_sync_bytes(slots, batch, length);
 }
 
 void launch_dynamics_backward(bool gate, const StepArgs& fw, const StepArgs& bw, int envelope_taps,
@@ -593,6 +631,8 @@ void launch_dynamics_backward(bool gate, const StepArgs& fw, const StepArgs& bw,
   d.fw = fw;
   d.bw = bw;
   d.env = reinterpret_cast<float*>(p);
+  p += al(sizeof(float) * seqs * fw.length);
+  d.dg = reinterpret_cast<float*>(p);
   p += al(sizeof(float) * seqs * fw.length);
   d.agg = reinterpret_cast<float2*>(p);
   p += al(sizeof(float2) * seqs * tiles);
@@ -610,13 +650,14 @@ void launch_dynamics_backward(bool gate, const StepArgs& fw, const StepArgs& bw,
   const long ne = envelope_taps < fw.length ? envelope_taps : fw.length;
   const bool vec = (fw.length % 4 == 0) && (ne % 4 == 0);
   const dim3 fgrid(static_cast<unsigned>(seqs * tiles));
-  float* env = const_cast<float*>(d.env);
+  float* env = d.env;
   const dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(seqs));
 #define MGB_DYN_BWD(G, V)                                                                                  \
   dyn_scan<G, V, true><<<fgrid, kDynThreads, 0, s>>>(fw, envelope_taps, energy_floor, tiles, status, ticket, env); \
-  dyn_bwd<G, V, 0><<<grid, kDynThreads, 0, s>>>(d);                                                        \
+  dyn_bwd_dg<G, V><<<grid, kDynThreads, 0, s>>>(d);                                                        \
+  dyn_bwd<V, 0><<<grid, kDynThreads, 0, s>>>(d);                                                            \
   dyn_bwd_carry<<<static_cast<unsigned>((seqs + 127) / 128), 128, 0, s>>>(d, static_cast<int>(seqs));        \
-  dyn_bwd<G, V, 1><<<grid, kDynThreads, 0, s>>>(d);
+  dyn_bwd<V, 1><<<grid, kDynThreads, 0, s>>>(d);
   if (gate) {
     if (vec) { MGB_DYN_BWD(true, true) } else { MGB_DYN_BWD(true, false) }
   } else {

@@ -671,8 +671,10 @@ void backward_arena(const DevicePlan& plan, const ProcessorSet& procs, const dou
       case NodeType::Mix: mgb::launch_pointwise(mgb::PointOp::Copy, bw, stream); break;
       case NodeType::Gain:
       case NodeType::Imager:
-        mgb::launch_pointwise(point_op(t), bw, stream);
-        mgb::launch_pointwise_param_grad(point_op(t), fw, bw, scratch, grad, stream);
+        if (!mgb::launch_pointwise_backward(point_op(t), fw, bw, scratch, grad, stream)) {
+          mgb::launch_pointwise(point_op(t), bw, stream);
+          mgb::launch_pointwise_param_grad(point_op(t), fw, bw, scratch, grad, stream);
+        }
         break;
       case NodeType::Eq:
         mgb::launch_eq_main(bw, reinterpret_cast<float*>(pws + eq_taps_bytes(fw.slots)), stream);

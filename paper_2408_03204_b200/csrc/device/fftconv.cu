@@ -29,6 +29,9 @@ namespace {
 
 constexpr int kColElems = 8192;  // complex elements per column tile (64 KiB)
 constexpr int kColThreads = 512;
+#ifndef MGB_RBWD_MINB
+#define MGB_RBWD_MINB 2  // resident CTAs per SM rows_bwd is compiled for (3: spills, measured slower)
+#endif
 
 inline std::size_t align256(std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255); }
 
@@ -230,9 +233,7 @@ __global__ void __launch_bounds__(row_threads<LN2, kSpecRows>()) rows_spec(int l
 
 // Signal rows k1 = r and N1 - r together: forward FFTs, channel-split product with the
 // kernel spectrum, inverse FFTs, inverse four-step twiddle. grid (N1/2 + 1, slots*B)
-// CONJ: multiply by conj(H_c) instead (the adjoint, a correlation with the kernel: swapping
-// the paired kernel values P[k] <-> P[N-k] conjugates both channels' kernel spectra).
-template <int LN2, bool CONJ = false>
+template <int LN2>
 __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2, 2>()) rows_conv(int log_n, int batch, float2* X, const float2* P, const float2* tw) {
   constexpr int N2 = 1 << LN2;
   constexpr int NT = row_threads<LN2, 2>();
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2,
     const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
     if (self && kb < k) continue;
     const float2 xk = rows[sidx(k)], xo = rows[RS + sidx(kb)];
-    const float2 pk = CONJ ? pov[q] : pkv[q], po = CONJ ? pkv[q] : pov[q];
+    const float2 pk = pkv[q], po = pov[q];
     const float2 zk = zmix(xk, cconj(xo), pk, cconj(po), s);
     const float2 zo = zmix(xo, cconj(xk), po, cconj(pk), s);
     rows[sidx(k)] = zk;
@@ -446,17 +447,15 @@ void rows_spec_t(const ConvGeom& g, int slots, float2* P, const float2* tw, cuda
 
 template <int LN2>
 void rows_conv_t(const ConvGeom& g, int items, int batch, float2* X, const float2* P, const float2* tw,
-                 cudaStream_t s, bool conj = false) {
+                 cudaStream_t s) {
   constexpr int smem = 2 * padded(1 << LN2) * 8;
   static const bool done = [] {
     cudaFuncSetAttribute(rows_conv<LN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(rows_conv<LN2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return true;
   }();
   (void)done;
   const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(items));
-  if (conj) rows_conv<LN2, true><<<grid, row_threads<LN2, 2>(), smem, s>>>(g.log_n, batch, X, P, tw);
-  else rows_conv<LN2><<<grid, row_threads<LN2, 2>(), smem, s>>>(g.log_n, batch, X, P, tw);
+  rows_conv<LN2><<<grid, row_threads<LN2, 2>(), smem, s>>>(g.log_n, batch, X, P, tw);
 }
 
 
@@ -649,34 +648,50 @@ __global__ void __launch_bounds__(256) delay_dense(const float* taps, DelayConst
 
 // ---- backward (adjoint) kernels -------------------------------------------------------------
 
-// Correlation spectrum of the step's output gradient with its input, summed over the batch:
-// per channel C_c = DY_c conj(X_c), packed C_L + i C_R (both correlations are real). DY and X
-// hold column-stage spectra of the packed signals; conj(X_c) is the spectrum of x_c reversed,
-// whose packed form is Z[N-k], so this is rows_conv's product with the pair swapped. The
-// result (row stage done, inverse twiddled) goes to X's b = 0 item. grid (N1/2 + 1, slots)
-template <int LN2>
-__global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_corr(int log_n, int batch, const float2* DY, float2* X,
-                                                               const float2* tw) {
+// Backward row pass of a long convolution, fused: per row pair (ra, rb) of slot s, the kernel
+// rows (KFFT: column-stage input, transformed here; else the finished spectrum P), then for
+// every batch item the row FFTs of DY and X and
+//  * the input gradient DY_c conj(H_c) (a correlation with the kernel): rows_conv's product
+//    with the paired kernel values P[k] <-> P[N-k] swapped, which conjugates both channels'
+//    kernel spectra; inverted and stored back into DY;
+//  * the kernel-gradient spectrum sum_b DY_c conj(X_c), packed C_L + i C_R (both real):
+//    conj(X_c) is the spectrum of x_c reversed, whose packed form is Z[N-k], so the same
+//    product with X's pair swapped; inverted into X's b = 0 item at the end.
+// grid (N1/2 + 1, slots)
+template <int LN2, bool KFFT>
+__global__ void __launch_bounds__(row_threads<LN2, 4>(), MGB_RBWD_MINB) rows_bwd(int log_n, int batch, float2* DY, float2* X,
+                                                                 const float2* P, const float2* tw) {
   constexpr int N2 = 1 << LN2;
   constexpr int NT = row_threads<LN2, 4>();
   constexpr int RS = padded(N2);
-  extern __shared__ float2 rows[];  // [4][RS]: dy a, dy b, x a, x b
+  extern __shared__ float2 rows[];  // [8][RS]: dy a, dy b, x a, x b, h a, h b, acc a, acc b
   const long N = 1L << log_n;
   const int N1 = static_cast<int>(N >> LN2);
   const int slot = blockIdx.y;
   const int ra = blockIdx.x, rb = (N1 - ra) & (N1 - 1);
   const bool self = ra == rb;
-  constexpr int KPT = (N2 + NT - 1) / NT;
-  float2 acck[KPT], acco[KPT];
-#pragma unroll
-  for (int q = 0; q < KPT; ++q) acck[q] = acco[q] = make_float2(0.f, 0.f);
+  const float2* pa = P + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
+  const float2* pb = P + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
+  float2* H = rows + 4 * RS;
+  float2* A = rows + 6 * RS;
+  for (int i = threadIdx.x; i < N2; i += NT) {
+    H[sidx(i)] = __ldg(pa + i);
+    H[RS + sidx(i)] = __ldg(pb + i);
+    A[sidx(i)] = A[RS + sidx(i)] = make_float2(0.f, 0.f);
+  }
+  if constexpr (KFFT) {
+    __syncthreads();
+    fft_pow2<LN2, 2, NT, -1>(H, RS, tw);
+  }
   const float s = 0.25f / static_cast<float>(N);
+  const float inv_n = 2.f / static_cast<float>(N);
   for (int b = 0; b < batch; ++b) {
     const long item = static_cast<long>(slot) * batch + b;
-    const float2* da = DY + item * N + static_cast<long>(ra) * N2;
-    const float2* db = DY + item * N + static_cast<long>(rb) * N2;
+    float2* da = DY + item * N + static_cast<long>(ra) * N2;
+    float2* db = DY + item * N + static_cast<long>(rb) * N2;
     const float2* xa = X + item * N + static_cast<long>(ra) * N2;
     const float2* xb = X + item * N + static_cast<long>(rb) * N2;
+    __syncthreads();  // previous item's rows fully consumed
     for (int i = threadIdx.x; i < N2; i += NT) {
       rows[sidx(i)] = da[i];
       rows[RS + sidx(i)] = db[i];
@@ -685,37 +700,36 @@ __global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_corr(int log_n, in
     }
     __syncthreads();
     fft_pow2<LN2, 4, NT, -1>(rows, RS, tw);
-#pragma unroll
-    for (int q = 0; q < KPT; ++q) {
-      const int k = threadIdx.x + q * NT;
-      if (k >= N2) continue;
+    // Each (k, N-k) pair is read and written by one thread only: products in place.
+    for (int k = threadIdx.x; k < N2; k += NT) {
       const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
       if (self && kb < k) continue;
+      const int ob = self ? sidx(kb) : RS + sidx(kb);
       const float2 dk = rows[sidx(k)], dn = rows[RS + sidx(kb)];
-      const float2 zk = rows[2 * RS + sidx(k)], zn = rows[3 * RS + sidx(kb)];
-      acck[q] = cadd(acck[q], zmix(dk, cconj(dn), zn, cconj(zk), s));
-      acco[q] = cadd(acco[q], zmix(dn, cconj(dk), zk, cconj(zn), s));
+      const float2 xk = rows[2 * RS + sidx(k)], xn = rows[3 * RS + sidx(kb)];
+      const float2 hk = H[sidx(k)], hn = H[RS + sidx(kb)];
+      // kernel gradient: DY_c conj(X_c) -> X's pair swapped
+      // (a self-paired bin, k == kb, has one value: written once, as rows_conv does)
+      if (!(self && kb == k)) A[sidx(k)] = cadd(A[sidx(k)], zmix(dk, cconj(dn), xn, cconj(xk), s));
+      A[ob] = cadd(A[ob], zmix(dn, cconj(dk), xk, cconj(xn), s));
+      // input gradient: conj(H_c) -> swapped kernel pair
+      rows[sidx(k)] = zmix(dk, cconj(dn), hn, cconj(hk), s);
+      rows[ob] = zmix(dn, cconj(dk), hk, cconj(hn), s);
     }
     __syncthreads();
-  }
-#pragma unroll
-  for (int q = 0; q < KPT; ++q) {
-    const int k = threadIdx.x + q * NT;
-    if (k >= N2) continue;
-    const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
-    if (self && kb < k) continue;
-    rows[sidx(k)] = acck[q];
-    if (self) rows[sidx(kb)] = acco[q];
-    else rows[RS + sidx(kb)] = acco[q];
+    fft_pow2<LN2, 2, NT, +1>(rows, RS, tw);
+    for (int i = threadIdx.x; i < N2; i += NT) {
+      da[i] = cmul(rows[sidx(i)], expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n));
+      if (!self) db[i] = cmul(rows[RS + sidx(i)], expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n));
+    }
   }
   __syncthreads();
-  fft_pow2<LN2, 2, NT, +1>(rows, RS, tw);
-  const float inv_n = 2.f / static_cast<float>(N);
+  fft_pow2<LN2, 2, NT, +1>(A, RS, tw);
   float2* oa = X + static_cast<long>(slot) * batch * N + static_cast<long>(ra) * N2;
   float2* ob = X + static_cast<long>(slot) * batch * N + static_cast<long>(rb) * N2;
   for (int i = threadIdx.x; i < N2; i += NT) {
-    oa[i] = cmul(rows[sidx(i)], expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n));
-    if (!self) ob[i] = cmul(rows[RS + sidx(i)], expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n));
+    oa[i] = cmul(A[sidx(i)], expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n));
+    if (!self) ob[i] = cmul(A[RS + sidx(i)], expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n));
   }
 }
 
@@ -1016,15 +1030,18 @@ void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, voi
 
 namespace {
 template <int LN2>
-void rows_corr_t(const ConvGeom& g, int slots, int batch, const float2* DY, float2* X, const float2* tw, cudaStream_t s) {
-  constexpr int smem = 4 * padded(1 << LN2) * 8;
+void rows_bwd_t(const ConvGeom& g, int slots, int batch, float2* DY, float2* X, const float2* P, bool kfft,
+                const float2* tw, cudaStream_t s) {
+  constexpr int smem = 8 * padded(1 << LN2) * 8;
   static const bool done = [] {
-    cudaFuncSetAttribute(rows_corr<LN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(rows_bwd<LN2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(rows_bwd<LN2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return true;
   }();
   (void)done;
   const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(slots));
-  rows_corr<LN2><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, batch, DY, X, tw);
+  if (kfft) rows_bwd<LN2, true><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, batch, DY, X, P, tw);
+  else rows_bwd<LN2, false><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, batch, DY, X, P, tw);
 }
 
 template <int LN1>
@@ -1054,9 +1071,9 @@ void launch_conv_backward(bool reverb, const StepArgs& fw, const StepArgs& bw, c
   if (fw.slots == 0 || fw.batch == 0 || fw.length == 0) return;
   const long taps = reverb ? rc.length : dc.span;
   const ConvGeom g = conv_geom(fw.length, taps);
-  auto* P = reinterpret_cast<float2*>(static_cast<char*>(const_cast<void*>(prologue_ws)) + ir_bytes(fw.slots, taps));
-  // A large step's forward left the kernel spectrum at its column stage: finish it in place.
-  if (conv_fuse_kernel_rows(g, fw.slots)) MGB_DISPATCH_LN(g.log_n2, rows_spec_t, g, fw.slots, P, fw.tw, s);
+  const auto* P = reinterpret_cast<const float2*>(static_cast<const char*>(prologue_ws) + ir_bytes(fw.slots, taps));
+  // A large step's forward left the kernel spectrum at its column stage (rows_bwd transforms it).
+  const bool kfft = conv_fuse_kernel_rows(g, fw.slots);
   const int items = fw.slots * fw.batch;
   const std::size_t spec = align256(sizeof(float2) * static_cast<std::size_t>(items) * g.n);
   auto* DY = static_cast<float2*>(ws);
@@ -1066,8 +1083,7 @@ void launch_conv_backward(bool reverb, const StepArgs& fw, const StepArgs& bw, c
                                          align256(sizeof(float2) * static_cast<std::size_t>(fw.slots) * taps));
   MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, bw, nullptr, 0, g, items, DY, 0, s);
   MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, fw, nullptr, 0, g, items, X, 0, s);
-  MGB_DISPATCH_LN(g.log_n2, rows_corr_t, g, fw.slots, fw.batch, DY, X, fw.tw, s);
-  MGB_DISPATCH_LN(g.log_n2, rows_conv_t, g, items, fw.batch, DY, P, fw.tw, s, true);
+  MGB_DISPATCH_LN(g.log_n2, rows_bwd_t, g, fw.slots, fw.batch, DY, X, P, kfft, fw.tw, s);
   MGB_DISPATCH_LN(g.log_n1, cols_inv_t, bw, g, DY, s);
   MGB_DISPATCH_LN(g.log_n1, cols_inv_buf_t, g, fw.slots, fw.batch, X, dh, taps, fw.tw, s);
   if (reverb) {

@@ -101,6 +101,10 @@ void launch_conv_backward(bool reverb, const StepArgs& fw, const StepArgs& bw, c
 
 // Pointwise (gain / imager) parameter gradients and the EQ correlation + FIR adjoint.
 std::size_t pw_grad_bytes(int slots, int batch, long length);
+// dX and the parameter gradient in one pass (returns false when L % 4 != 0: use the two-pass
+// launch_pointwise + launch_pointwise_param_grad).
+bool launch_pointwise_backward(PointOp op, const StepArgs& fw, const StepArgs& bw, void* ws, double* grad,
+                               cudaStream_t s);
 void launch_pointwise_param_grad(PointOp op, const StepArgs& fw, const StepArgs& bw, void* ws, double* grad,
                                  cudaStream_t s);
 std::size_t eq_grad_bytes(int slots, int batch, long length);
