@@ -3,7 +3,7 @@ import os
 import subprocess
 import sys
 
-for v in ("0", "2", "4", "8"):
+for v in (sys.argv[1:] or ["0", "2", "4", "8"]):
     env = dict(os.environ, MGB_PIPELINE_HOST_THREADS=v)
     out = subprocess.run([sys.executable, "-c", """
 import sys, time, json; sys.path.insert(0, '.')

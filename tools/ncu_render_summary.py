@@ -11,6 +11,9 @@ import os
 import subprocess
 import sys
 
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _ncu_csv import raw_rows  # noqa: E402
+
 KEYS = {
     "dur_us": "gpu__time_duration.sum",
     "regs": "launch__registers_per_thread",
@@ -43,8 +46,7 @@ def to_num(v, unit):
 
 def main():
     rep, prefix = sys.argv[1], sys.argv[2]
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(out.splitlines()))
+    rows = raw_rows(rep)
     head, units = rows[0], rows[1]
     col = {n: i for i, n in enumerate(head)}
     recs = []

@@ -3,14 +3,17 @@
 Usage:  python tools/ncu_stalls.py REPORT.ncu-rep [ID ...]
 """
 import csv
+import os
 import subprocess
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _ncu_csv import raw_rows  # noqa: E402
 
 
 def main():
     rep, ids = sys.argv[1], set(sys.argv[2:])
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(out.splitlines()))
+    rows = raw_rows(rep)
     h = rows[0]
     pre, suf = "smsp__average_warps_issue_stalled_", "_per_issue_active.ratio"
     for r in rows[2:]:
