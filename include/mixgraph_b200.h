@@ -209,6 +209,37 @@ int32_t mg_random_legal_params(const int32_t* node_types, int32_t num_nodes, uin
 int32_t mg_default_param_row(int32_t node_type, double* row);
 int32_t mg_uniform_noise(int64_t n, uint32_t seed, double* out);
 
+/* ---- File-level I/O (host only) -------------------------------------------------------
+ * Graph documents: graph_to_json / graph_from_json / save_graph / load_graph
+ * (proj/include/mixgraph/graph_io.hpp:20-24, proj/src/graph_io.cpp:19-127); DOT export
+ * (graph_io.hpp:28, graph_io.cpp:129-143); 32-bit float stereo WAV (wav.hpp:11-12,
+ * wav.cpp:39-133). Text outputs use the two-call idiom: *len receives the byte count
+ * (without the terminating NUL); the text is copied only when cap > *len. Document errors
+ * are MG_EINVAL ("graph document: ..."), WAV errors MG_ERUNTIME ("read_wav: ...",
+ * "write_wav: ..."), as the reference's std::invalid_argument / std::runtime_error. */
+typedef struct mg_doc mg_doc;     /* (Graph, ParamStore) of a parsed graph document */
+typedef struct mg_audio mg_audio; /* AudioBuffer read from a WAV file */
+int32_t mg_graph_to_json(const int32_t* node_types, int32_t num_nodes, const int32_t* edges, int32_t num_edges,
+                         const double* const* tables, const int32_t* rows, char* buf, int64_t cap, int64_t* len);
+int32_t mg_save_graph(const int32_t* node_types, int32_t num_nodes, const int32_t* edges, int32_t num_edges,
+                      const double* const* tables, const int32_t* rows, const char* path);
+int32_t mg_graph_from_json(const char* text, int64_t len, mg_doc** out);
+int32_t mg_load_graph(const char* path, mg_doc** out);
+/* rows[10]: parameter rows per node type, -1 for types without a table */
+int32_t mg_doc_info(const mg_doc* doc, int32_t* num_nodes, int32_t* num_edges, int32_t* rows);
+int32_t mg_doc_graph(const mg_doc* doc, int32_t* node_types, int32_t* edges);
+int32_t mg_doc_params(const mg_doc* doc, int32_t node_type, double* out);
+void mg_doc_destroy(mg_doc* doc);
+int32_t mg_export_dot(const int32_t* node_types, int32_t num_nodes, const int32_t* edges, int32_t num_edges, char* buf,
+                      int64_t cap, int64_t* len);
+/* samples [batch][channels][length]; batch must be 1 and channels 2 (wav.cpp:40-41) */
+int32_t mg_write_wav(const double* samples, int32_t batch, int32_t channels, int64_t length, double sample_rate,
+                     const char* path);
+int32_t mg_read_wav(const char* path, mg_audio** out);
+int32_t mg_audio_info(const mg_audio* audio, int64_t* length, double* sample_rate);
+int32_t mg_audio_samples(const mg_audio* audio, double* out); /* [1][2][length] */
+void mg_audio_destroy(mg_audio* audio);
+
 #ifdef __cplusplus
 }
 #endif

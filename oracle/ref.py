@@ -64,6 +64,17 @@ def lib():
         sig("ref_uniform_noise", _i32, _i64, _u32, _vp)
         sig("ref_fit", _i32, _vp, _i32, _vp, _i32, _dbl, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _i32, _i32, _dbl,
             _dbl, _vp)
+        sig("ref_graph_to_json", _i32, _vp, _i32, _vp, _i32, _vp, _vp, ctypes.c_char_p, _i64, ctypes.POINTER(_i64))
+        sig("ref_save_graph", _i32, _vp, _i32, _vp, _i32, _vp, _vp, ctypes.c_char_p)
+        sig("ref_graph_from_json", _i32, ctypes.c_char_p, ctypes.POINTER(_vp))
+        sig("ref_load_graph", _i32, ctypes.c_char_p, ctypes.POINTER(_vp))
+        sig("ref_doc_info", _i32, _vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), _vp)
+        sig("ref_doc_graph", _i32, _vp, _vp, _vp)
+        sig("ref_doc_params", _i32, _vp, _i32, _vp)
+        sig("ref_doc_destroy", None, _vp)
+        sig("ref_export_dot", _i32, _vp, _i32, _vp, _i32, ctypes.c_char_p, _i64, ctypes.POINTER(_i64))
+        sig("ref_write_wav", _i32, _vp, _i32, _i32, _i64, _dbl, ctypes.c_char_p)
+        sig("ref_read_wav", _i32, ctypes.c_char_p, _vp, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_dbl))
         _lib = L
     return _lib
 
@@ -274,3 +285,80 @@ def rel_linf(a: np.ndarray, b: np.ndarray) -> float:
     a = np.asarray(a, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
     return float(np.max(np.abs(a - b)) / max(float(np.max(np.abs(b))) if b.size else 0.0, 1e-12)) if a.size else 0.0
+
+
+# ---- file-level I/O (graph_io.cpp:19-143, wav.cpp:39-133) -----------------------------------
+
+def _text(fn, *args) -> str:
+    n = _i64()
+    _check(fn(*args, None, 0, ctypes.byref(n)))
+    buf = ctypes.create_string_buffer(n.value + 1)
+    _check(fn(*args, buf, n.value + 1, ctypes.byref(n)))
+    return buf.raw[: n.value].decode()
+
+
+def graph_to_json(types, edges, params: Optional[Dict[int, np.ndarray]] = None) -> str:
+    types = np.ascontiguousarray(types, dtype=np.int32)
+    edges = np.ascontiguousarray(edges, dtype=np.int32).reshape(-1, 4)
+    ptrs, rows, _keep = _table_ptrs(params or {})
+    return _text(lib().ref_graph_to_json, _p(types), len(types), _p(edges), len(edges), ptrs, _p(rows))
+
+
+def _doc(h):
+    try:
+        nn, ne = _i32(), _i32()
+        rows = np.zeros(10, dtype=np.int32)
+        _check(lib().ref_doc_info(h, ctypes.byref(nn), ctypes.byref(ne), _p(rows)))
+        t = np.zeros(nn.value, dtype=np.int32)
+        e = np.zeros((ne.value, 4), dtype=np.int32)
+        _check(lib().ref_doc_graph(h, _p(t), _p(e)))
+        params = {}
+        for ti in range(10):
+            if rows[ti] >= 0:
+                m = np.zeros((int(rows[ti]), WIDTHS[ti]))
+                _check(lib().ref_doc_params(h, ti, _p(m)))
+                params[ti] = m
+        return t, e, params
+    finally:
+        lib().ref_doc_destroy(h)
+
+
+def graph_from_json(text: str):
+    """-> (types, edges[E][4], {type: table})"""
+    h = _vp()
+    _check(lib().ref_graph_from_json(text.encode(), ctypes.byref(h)))
+    return _doc(h)
+
+
+def load_graph(path: str):
+    h = _vp()
+    _check(lib().ref_load_graph(os.fsencode(path), ctypes.byref(h)))
+    return _doc(h)
+
+
+def save_graph(types, edges, params, path: str) -> None:
+    types = np.ascontiguousarray(types, dtype=np.int32)
+    edges = np.ascontiguousarray(edges, dtype=np.int32).reshape(-1, 4)
+    ptrs, rows, _keep = _table_ptrs(params or {})
+    _check(lib().ref_save_graph(_p(types), len(types), _p(edges), len(edges), ptrs, _p(rows), os.fsencode(path)))
+
+
+def export_dot(types, edges) -> str:
+    types = np.ascontiguousarray(types, dtype=np.int32)
+    edges = np.ascontiguousarray(edges, dtype=np.int32).reshape(-1, 4)
+    return _text(lib().ref_export_dot, _p(types), len(types), _p(edges), len(edges))
+
+
+def write_wav(samples: np.ndarray, path: str, sample_rate: float = 44100.0) -> None:
+    a = np.ascontiguousarray(samples, dtype=np.float64)
+    if a.ndim == 2:
+        a = a[None]
+    _check(lib().ref_write_wav(_p(a), a.shape[0], a.shape[1], a.shape[2], float(sample_rate), os.fsencode(path)))
+
+
+def read_wav(path: str):
+    n, fs = _i64(), _dbl()
+    _check(lib().ref_read_wav(os.fsencode(path), None, 0, ctypes.byref(n), ctypes.byref(fs)))
+    out = np.zeros((1, 2, n.value))
+    _check(lib().ref_read_wav(os.fsencode(path), _p(out), out.size, ctypes.byref(n), ctypes.byref(fs)))
+    return out, fs.value

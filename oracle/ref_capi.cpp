@@ -25,6 +25,8 @@
 #include "mixgraph/dsp.hpp"
 #include "mixgraph/fit.hpp"
 #include "mixgraph/graph.hpp"
+#include "mixgraph/graph_io.hpp"
+#include "mixgraph/wav.hpp"
 #include "mixgraph/processors.hpp"
 #include "mixgraph/reference.hpp"
 #include "mixgraph/render.hpp"
@@ -405,5 +407,87 @@ int ref_stft(const double* x, int64_t n, int32_t fft_length, int32_t hop, double
 // processors.cpp:110-130
 double ref_compressor_gain_log(double g, double t, double w, double r) { return compressor_gain_log(g, t, w, r); }
 double ref_noisegate_gain_log(double g, double t, double w, double r) { return noisegate_gain_log(g, t, w, r); }
+
+// ---- file-level I/O (graph_io.cpp:19-143, wav.cpp:39-133) --------------------------------
+
+namespace {
+Graph graph_from_arrays(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne) {
+  Graph g;
+  for (int i = 0; i < n; ++i) g.add_node(static_cast<NodeType>(types[i]));
+  for (int i = 0; i < ne; ++i) g.connect(edges[4 * i], edges[4 * i + 1], edges[4 * i + 2], edges[4 * i + 3]);
+  return g;
+}
+int copy_text(const std::string& s, char* buf, int64_t cap, int64_t* len) {
+  *len = static_cast<int64_t>(s.size());
+  if (buf && static_cast<int64_t>(s.size()) < cap) std::memcpy(buf, s.c_str(), s.size() + 1);
+  return 0;
+}
+}  // namespace
+
+// graph_to_json (graph_io.cpp:19-49); `with_params` = 0 passes an empty ParamStore.
+int ref_graph_to_json(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne, const double* const* tables,
+                      const int32_t* rows, char* buf, int64_t cap, int64_t* len) {
+  return guarded([&] { copy_text(graph_to_json(graph_from_arrays(types, n, edges, ne), make_store(tables, rows)), buf, cap, len); });
+}
+
+// graph_from_json (graph_io.cpp:51-117) -> heap (Graph, ParamStore)
+int ref_graph_from_json(const char* text, void** doc) {
+  return guarded([&] { *doc = new std::pair<Graph, ParamStore>(graph_from_json(text)); });
+}
+int ref_load_graph(const char* path, void** doc) {
+  return guarded([&] { *doc = new std::pair<Graph, ParamStore>(load_graph(path)); });
+}
+int ref_save_graph(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne, const double* const* tables,
+                   const int32_t* rows, const char* path) {
+  return guarded([&] { save_graph(graph_from_arrays(types, n, edges, ne), make_store(tables, rows), path); });
+}
+int ref_doc_info(const void* doc, int32_t* n_nodes, int32_t* n_edges, int32_t* rows) {
+  return guarded([&] {
+    const auto& d = *static_cast<const std::pair<Graph, ParamStore>*>(doc);
+    *n_nodes = d.first.num_nodes();
+    *n_edges = static_cast<int32_t>(d.first.edges().size());
+    for (int t = 0; t < kNumNodeTypes; ++t) {
+      rows[t] = d.second.has(static_cast<NodeType>(t)) ? d.second.table(static_cast<NodeType>(t)).rows : -1;
+    }
+  });
+}
+int ref_doc_graph(const void* doc, int32_t* types, int32_t* edges) {
+  return guarded([&] {
+    const auto& d = *static_cast<const std::pair<Graph, ParamStore>*>(doc);
+    int32_t nn = 0, ne = 0;
+    export_graph(d.first, types, d.first.num_nodes(), edges, static_cast<int32_t>(d.first.edges().size()), &nn, &ne);
+  });
+}
+int ref_doc_params(const void* doc, int32_t type, double* out) {
+  return guarded([&] {
+    const auto& d = *static_cast<const std::pair<Graph, ParamStore>*>(doc);
+    const ParamMatrix& m = d.second.table(static_cast<NodeType>(type));
+    std::memcpy(out, m.values.data(), sizeof(double) * m.values.size());
+  });
+}
+void ref_doc_destroy(void* doc) { delete static_cast<std::pair<Graph, ParamStore>*>(doc); }
+
+// export_dot (graph_io.cpp:129-143)
+int ref_export_dot(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne, char* buf, int64_t cap,
+                   int64_t* len) {
+  return guarded([&] { copy_text(export_dot(graph_from_arrays(types, n, edges, ne)), buf, cap, len); });
+}
+
+// write_wav / read_wav (wav.cpp:39-133); samples [batch][channels][length]
+int ref_write_wav(const double* samples, int32_t batch, int32_t channels, int64_t length, double fs, const char* path) {
+  return guarded([&] {
+    AudioBuffer b(batch, channels, static_cast<long>(length), fs);
+    std::memcpy(b.samples.data(), samples, sizeof(double) * b.samples.size());
+    write_wav(b, path);
+  });
+}
+int ref_read_wav(const char* path, double* out, int64_t cap, int64_t* length, double* fs) {
+  return guarded([&] {
+    const AudioBuffer b = read_wav(path);
+    *length = b.length;
+    *fs = b.sample_rate;
+    if (out && static_cast<int64_t>(b.samples.size()) <= cap) std::memcpy(out, b.samples.data(), sizeof(double) * b.samples.size());
+  });
+}
 
 }  // extern "C"

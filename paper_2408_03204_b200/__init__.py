@@ -98,6 +98,20 @@ _sig("mg_generate_console", _i32, _i32, _dbl, _u32, _vp, _i32, _vp, _i32, _P(_i3
 _sig("mg_random_legal_params", _i32, _vp, _i32, _u32, _vp)
 _sig("mg_default_param_row", _i32, _i32, _vp)
 _sig("mg_uniform_noise", _i32, _i64, _u32, _vp)
+_sig("mg_graph_to_json", _i32, _vp, _i32, _vp, _i32, _vp, _vp, ctypes.c_char_p, _i64, _P(_i64))
+_sig("mg_save_graph", _i32, _vp, _i32, _vp, _i32, _vp, _vp, ctypes.c_char_p)
+_sig("mg_graph_from_json", _i32, ctypes.c_char_p, _i64, _P(_vp))
+_sig("mg_load_graph", _i32, ctypes.c_char_p, _P(_vp))
+_sig("mg_doc_info", _i32, _vp, _P(_i32), _P(_i32), _vp)
+_sig("mg_doc_graph", _i32, _vp, _vp, _vp)
+_sig("mg_doc_params", _i32, _vp, _i32, _vp)
+_sig("mg_doc_destroy", None, _vp)
+_sig("mg_export_dot", _i32, _vp, _i32, _vp, _i32, ctypes.c_char_p, _i64, _P(_i64))
+_sig("mg_write_wav", _i32, _vp, _i32, _i32, _i64, _dbl, ctypes.c_char_p)
+_sig("mg_read_wav", _i32, ctypes.c_char_p, _P(_vp))
+_sig("mg_audio_info", _i32, _vp, _P(_i64), _P(_dbl))
+_sig("mg_audio_samples", _i32, _vp, _vp)
+_sig("mg_audio_destroy", None, _vp)
 
 
 def _check(status: int) -> None:
@@ -690,3 +704,91 @@ __all__ = [
     "generate_console", "random_legal_params", "uniform_noise", "compressor_gain_log", "noisegate_gain_log",
     "check_param_row", "LIB_PATH",
 ]
+
+
+# ---- file-level I/O (graph_io.hpp:20-28, wav.hpp:11-12) -------------------------------------
+
+def _text_call(fn, *args) -> str:
+    n = ctypes.c_int64()
+    _check(fn(*args, None, 0, ctypes.byref(n)))
+    buf = ctypes.create_string_buffer(n.value + 1)
+    _check(fn(*args, buf, n.value + 1, ctypes.byref(n)))
+    return buf.raw[: n.value].decode()
+
+
+def graph_to_json(g: Graph, params: Optional[Dict[int, np.ndarray]] = None) -> str:
+    """`graph_io.cpp:19-49`: sorted keys, two-space indent, shortest round-trip numbers."""
+    t, e = g.arrays()
+    ptrs, rows, _keep = _tables(params or {})
+    return _text_call(_lib.mg_graph_to_json, _ptr(t), len(t), _ptr(e), len(e), ptrs, _ptr(rows))
+
+
+def _doc_out(h) -> Tuple[Graph, Dict[NodeType, np.ndarray]]:
+    try:
+        nn, ne = _i32(), _i32()
+        rows = np.zeros(NUM_NODE_TYPES, dtype=np.int32)
+        _check(_lib.mg_doc_info(h, ctypes.byref(nn), ctypes.byref(ne), _ptr(rows)))
+        t = np.zeros(nn.value, dtype=np.int32)
+        e = np.zeros((ne.value, 4), dtype=np.int32)
+        _check(_lib.mg_doc_graph(h, _ptr(t), _ptr(e)))
+        params: Dict[NodeType, np.ndarray] = {}
+        for ti in range(NUM_NODE_TYPES):
+            if rows[ti] >= 0:
+                m = np.zeros((int(rows[ti]), param_width(ti)), dtype=np.float64)
+                _check(_lib.mg_doc_params(h, ti, _ptr(m)))
+                params[NodeType(ti)] = m
+        return Graph.from_arrays(t, e), params
+    finally:
+        _lib.mg_doc_destroy(h)
+
+
+def graph_from_json(text: str) -> Tuple[Graph, Dict[NodeType, np.ndarray]]:
+    """`graph_io.cpp:51-117`: validated graph + parameter tables (defaults where absent)."""
+    raw = text.encode()
+    h = _vp()
+    _check(_lib.mg_graph_from_json(raw, len(raw), ctypes.byref(h)))
+    return _doc_out(h)
+
+
+def save_graph(g: Graph, params: Optional[Dict[int, np.ndarray]], path: str) -> None:
+    """`graph_io.cpp:119-124`."""
+    t, e = g.arrays()
+    ptrs, rows, _keep = _tables(params or {})
+    _check(_lib.mg_save_graph(_ptr(t), len(t), _ptr(e), len(e), ptrs, _ptr(rows), os.fsencode(path)))
+
+
+def load_graph(path: str) -> Tuple[Graph, Dict[NodeType, np.ndarray]]:
+    """`graph_io.cpp:126-132`."""
+    h = _vp()
+    _check(_lib.mg_load_graph(os.fsencode(path), ctypes.byref(h)))
+    return _doc_out(h)
+
+
+def export_dot(g: Graph) -> str:
+    """`graph_io.cpp:134-143`: deterministic DOT, nodes labelled with their letter code."""
+    t, e = g.arrays()
+    return _text_call(_lib.mg_export_dot, _ptr(t), len(t), _ptr(e), len(e))
+
+
+def write_wav(samples: np.ndarray, path: str, sample_rate: float = 44100.0) -> None:
+    """`wav.cpp:39-83`: samples [1][2][L] (or [2][L]) as 32-bit float stereo PCM."""
+    a = np.ascontiguousarray(samples, dtype=np.float64)
+    if a.ndim == 2:
+        a = a[None]
+    if a.ndim != 3:
+        raise ValueError("write_wav: samples must be [batch][channels][length]")
+    _check(_lib.mg_write_wav(_ptr(a), a.shape[0], a.shape[1], a.shape[2], float(sample_rate), os.fsencode(path)))
+
+
+def read_wav(path: str) -> Tuple[np.ndarray, float]:
+    """`wav.cpp:85-133` -> (samples [1][2][L] float64, sample rate)."""
+    h = _vp()
+    _check(_lib.mg_read_wav(os.fsencode(path), ctypes.byref(h)))
+    try:
+        n, fs = ctypes.c_int64(), ctypes.c_double()
+        _check(_lib.mg_audio_info(h, ctypes.byref(n), ctypes.byref(fs)))
+        out = np.zeros((1, 2, n.value), dtype=np.float64)
+        _check(_lib.mg_audio_samples(h, _ptr(out)))
+        return out, fs.value
+    finally:
+        _lib.mg_audio_destroy(h)

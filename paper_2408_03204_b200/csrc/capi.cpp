@@ -11,6 +11,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "mixgraph_b200/graph_io.hpp"
 #include "mixgraph_b200/render.hpp"
 
 namespace mgb {  // device/launch.hpp (nvcc-only header): optimisation helpers
@@ -50,6 +51,14 @@ struct mg_pipeline {
 
 struct mg_batch {
   std::unique_ptr<BatchRenderer> b;
+};
+
+struct mg_doc {
+  std::pair<Graph, ParamStore> d;
+};
+
+struct mg_audio {
+  AudioBuffer b;
 };
 
 struct mg_processors {
@@ -123,6 +132,19 @@ void export_graph(const Graph& g, int32_t* types, int32_t cap_nodes, int32_t* ed
       edges[4 * i + 3] = e.inlet;
     }
   }
+}
+
+// Graph built through the checked builder (add_node / connect), as the reference's callers do.
+Graph checked_graph(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne) {
+  Graph g;
+  for (int i = 0; i < n; ++i) g.add_node(to_type(types[i]));
+  for (int i = 0; i < ne; ++i) g.connect(edges[4 * i], edges[4 * i + 1], edges[4 * i + 2], edges[4 * i + 3]);
+  return g;
+}
+
+void copy_text(const std::string& s, char* buf, int64_t cap, int64_t* len) {
+  *len = static_cast<int64_t>(s.size());
+  if (buf && static_cast<int64_t>(s.size()) < cap) std::memcpy(buf, s.c_str(), s.size() + 1);
 }
 
 }  // namespace
@@ -575,5 +597,99 @@ int32_t mg_uniform_noise(int64_t n, uint32_t seed, double* out) {
     std::memcpy(out, v.data(), sizeof(double) * v.size());
   });
 }
+
+// ---- file-level I/O (graph_io.cpp:19-143, wav.cpp:39-133) --------------------------------
+
+int32_t mg_graph_to_json(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne, const double* const* tables,
+                         const int32_t* rows, char* buf, int64_t cap, int64_t* len) {
+  return guarded([&] { copy_text(graph_to_json(checked_graph(types, n, edges, ne), make_store(tables, rows)), buf, cap, len); });
+}
+
+int32_t mg_save_graph(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne, const double* const* tables,
+                      const int32_t* rows, const char* path) {
+  return guarded([&] { save_graph(checked_graph(types, n, edges, ne), make_store(tables, rows), path); });
+}
+
+int32_t mg_graph_from_json(const char* text, int64_t len, mg_doc** out) {
+  return guarded([&] {
+    *out = nullptr;
+    auto d = std::make_unique<mg_doc>();
+    d->d = graph_from_json(std::string(text, static_cast<std::size_t>(len)));
+    *out = d.release();
+  });
+}
+
+int32_t mg_load_graph(const char* path, mg_doc** out) {
+  return guarded([&] {
+    *out = nullptr;
+    auto d = std::make_unique<mg_doc>();
+    d->d = load_graph(path);
+    *out = d.release();
+  });
+}
+
+int32_t mg_doc_info(const mg_doc* doc, int32_t* num_nodes, int32_t* num_edges, int32_t* rows) {
+  return guarded([&] {
+    *num_nodes = doc->d.first.num_nodes();
+    *num_edges = static_cast<int32_t>(doc->d.first.edges().size());
+    for (int t = 0; t < kNumNodeTypes; ++t) {
+      const NodeType nt = static_cast<NodeType>(t);
+      rows[t] = doc->d.second.has(nt) ? doc->d.second.table(nt).rows : -1;
+    }
+  });
+}
+
+int32_t mg_doc_graph(const mg_doc* doc, int32_t* types, int32_t* edges) {
+  return guarded([&] {
+    int32_t nn = 0, ne = 0;
+    const Graph& g = doc->d.first;
+    export_graph(g, types, g.num_nodes(), edges, static_cast<int32_t>(g.edges().size()), &nn, &ne);
+  });
+}
+
+int32_t mg_doc_params(const mg_doc* doc, int32_t node_type, double* out) {
+  return guarded([&] {
+    const ParamMatrix& m = doc->d.second.table(to_type(node_type));
+    std::memcpy(out, m.values.data(), sizeof(double) * m.values.size());
+  });
+}
+
+void mg_doc_destroy(mg_doc* doc) { delete doc; }
+
+int32_t mg_export_dot(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne, char* buf, int64_t cap,
+                      int64_t* len) {
+  return guarded([&] { copy_text(export_dot(checked_graph(types, n, edges, ne)), buf, cap, len); });
+}
+
+int32_t mg_write_wav(const double* samples, int32_t batch, int32_t channels, int64_t length, double sample_rate,
+                     const char* path) {
+  return guarded([&] {
+    AudioBuffer b(batch, channels, static_cast<long>(length), sample_rate);
+    std::memcpy(b.samples.data(), samples, sizeof(double) * b.samples.size());
+    write_wav(b, path);
+  });
+}
+
+int32_t mg_read_wav(const char* path, mg_audio** out) {
+  return guarded([&] {
+    *out = nullptr;
+    auto a = std::make_unique<mg_audio>();
+    a->b = read_wav(path);
+    *out = a.release();
+  });
+}
+
+int32_t mg_audio_info(const mg_audio* a, int64_t* length, double* sample_rate) {
+  return guarded([&] {
+    *length = a->b.length;
+    *sample_rate = a->b.sample_rate;
+  });
+}
+
+int32_t mg_audio_samples(const mg_audio* a, double* out) {
+  return guarded([&] { std::memcpy(out, a->b.samples.data(), sizeof(double) * a->b.samples.size()); });
+}
+
+void mg_audio_destroy(mg_audio* a) { delete a; }
 
 }  // extern "C"

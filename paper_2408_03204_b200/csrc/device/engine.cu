@@ -23,6 +23,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "host/convert.hpp"
 #include "launch.hpp"
 #include "mixgraph_b200/render.hpp"
 
@@ -879,9 +880,10 @@ struct RenderPipeline::HostConvert {
   std::uint64_t next_id = 1, finished = 0;
   std::string error;
 
-  explicit HostConvert(int n) : nthreads(n) {
+  HostConvert(int n, int device) : nthreads(n) {
     for (int i = 0; i < nthreads; ++i) {
-      workers.emplace_back([this, i] {
+      workers.emplace_back([this, i, device] {
+        cudaSetDevice(device);  // workers issue their chunks' H2D copies
         std::uint64_t seen = 0;
         for (;;) {
           std::function<void(int)> t;
@@ -935,6 +937,7 @@ struct RenderPipeline::HostConvert {
     cv.notify_all();
     for (auto& w : workers) w.join();
   }
+  // Runs f(0..nthreads) on the workers and the calling thread (index nthreads).
   void parallel(const std::function<void(int)>& f) {
     std::scoped_lock run(run_mu);
     {
@@ -944,15 +947,35 @@ struct RenderPipeline::HostConvert {
       ++gen;
     }
     cv.notify_all();
+    f(nthreads);
     std::unique_lock lk(mu);
     cv_done.wait(lk, [&] { return remaining == 0; });
   }
-  template <typename A, typename B>
-  void convert(const A* src, B* dst, std::size_t n) {
+  void convert(const float* src, double* dst, std::size_t n) {
+    const int parts = nthreads + 1;
     parallel([&](int i) {
-      const std::size_t lo = n * static_cast<std::size_t>(i) / nthreads, hi = n * static_cast<std::size_t>(i + 1) / nthreads;
-      for (std::size_t k = lo; k < hi; ++k) dst[k] = static_cast<B>(src[k]);
+      const std::size_t lo = n * static_cast<std::size_t>(i) / parts, hi = n * static_cast<std::size_t>(i + 1) / parts;
+      hostconv::f32_to_f64(src + lo, dst + lo, hi - lo);
     });
+  }
+  // Sources -> fp32 pinned staging -> device, in 1 MiB chunks claimed from a shared counter.
+  // Each converted chunk goes onto the H2D stream at once, so the DMA of early chunks
+  // overlaps the conversion of later ones (and the next render's conversion overlaps this
+  // render's kernels).
+  void upload(const double* const* src, int nsrc, std::size_t stride, float* pin, float* dev, cudaStream_t st) {
+    constexpr std::size_t kChunk = std::size_t{1} << 18;
+    const std::size_t per = (stride + kChunk - 1) / kChunk, total = per * static_cast<std::size_t>(nsrc);
+    std::atomic<std::size_t> next{0};
+    std::atomic<int> failed{0};
+    parallel([&](int) {
+      for (std::size_t c = next.fetch_add(1); c < total; c = next.fetch_add(1)) {
+        const std::size_t k = c / per, lo = (c % per) * kChunk, n = std::min(kChunk, stride - lo);
+        const std::size_t off = k * stride + lo;
+        hostconv::f64_to_f32(src[k] + lo, pin + off, n);
+        if (cudaMemcpyAsync(dev + off, pin + off, sizeof(float) * n, cudaMemcpyHostToDevice, st) != cudaSuccess) failed = 1;
+      }
+    });
+    if (failed) throw std::runtime_error("cuda: RenderPipeline source upload failed");
   }
   std::uint64_t enqueue(Job j) {
     std::scoped_lock lk(qmu);
@@ -983,10 +1006,14 @@ RenderPipeline::RenderPipeline(const DevicePlan& plan, const ProcessorSet& procs
   if (!f32_) {
     int n = host_threads;
     if (n < 0) {
+      // Default: half the host's hardware threads, at most 8 (config 2 on the 16-thread B200
+      // box hosts: 0.66 ms/render device conversion, 0.48 ms with 8 host threads).
       const char* v = std::getenv("MGB_PIPELINE_HOST_THREADS");  // diagnostics: 0 = device conversion
-      n = v ? std::atoi(v) : 0;  // measured: PCIe carrying double beats host conversion (0.66 vs 0.77 ms, config 2)
+      n = v ? std::atoi(v) : std::clamp(static_cast<int>(std::thread::hardware_concurrency()) / 2 - 1, 0, 7);
     }
-    if (n >= 1) conv_ = std::make_unique<HostConvert>(n);
+    if (n >= 1) conv_ = std::make_unique<HostConvert>(n, procs.device().device);
+    const char* f = std::getenv("MGB_PIPELINE_HOST_FRACTION");  // diagnostics
+    host_fraction_ = f ? std::clamp(std::atof(f), 0.0, 1.0) : kHostFraction;
   }
   const RenderData& rd = plan.data();
   const std::size_t rows = static_cast<std::size_t>(rd.buffer_rows);
@@ -1009,7 +1036,7 @@ RenderPipeline::RenderPipeline(const DevicePlan& plan, const ProcessorSet& procs
       for (std::size_t r = 0; r < src.size(); ++r) host.insert(host.end(), row.begin(), row.end());
     }
     if (!host.empty()) cuda_check(cudaMemcpy(dpar, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice), "H2D");
-    if (!f32_ && !conv_) s->staging.ensure(sizeof(double) * rows * stride_ + 16);
+    if (!f32_) s->staging.ensure(sizeof(double) * rows * stride_ + 16);
     if (conv_) {
       cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&s->pin_src),
                                sizeof(float) * std::max<std::size_t>(1, static_cast<std::size_t>(rd.num_inputs)) * stride_,
@@ -1067,14 +1094,25 @@ void RenderPipeline::submit(const ParamStore& params, const void* const* sources
     }
     return n > 0;
   };
+  // Host-converted double audio: sources [0, kh) are converted to fp32 on the host threads,
+  // the rest cross PCIe as double first (their DMA runs while the host converts) and are
+  // converted on the device. Splitting balances host memory bandwidth against PCIe.
+  int kh = 0;
   if (conv_) {
-    for (int k = 0; k < rd.num_inputs; ++k) {
-      conv_->convert(static_cast<const double*>(sources[k]), s.pin_src + static_cast<std::size_t>(k) * stride_,
-                     static_cast<std::size_t>(stride_));
+    kh = std::min(rd.num_inputs, static_cast<int>(std::ceil(host_fraction_ * rd.num_inputs - 1e-9)));
+    const int kd = rd.num_inputs - kh;
+    if (kd > 0) {
+      char* dst = static_cast<char*>(s.staging.ptr);
+      if (contiguous(sources + kh, kd)) {
+        cuda_check(cudaMemcpyAsync(dst, sources[kh], bytes * kd, cudaMemcpyHostToDevice, h2d_), "H2D sources");
+      } else {
+        for (int k = 0; k < kd; ++k) {
+          cuda_check(cudaMemcpyAsync(dst + bytes * k, sources[kh + k], bytes, cudaMemcpyHostToDevice, h2d_), "H2D sources");
+        }
+      }
     }
-    if (rd.num_inputs > 0) {
-      cuda_check(cudaMemcpyAsync(arena, s.pin_src, fbytes * rd.num_inputs, cudaMemcpyHostToDevice, h2d_), "H2D sources");
-    }
+    conv_->upload(reinterpret_cast<const double* const*>(sources), kh, static_cast<std::size_t>(stride_), s.pin_src, arena,
+                  h2d_);
   } else {
     char* dst = f32_ ? reinterpret_cast<char*>(arena) : static_cast<char*>(s.staging.ptr);
     if (contiguous(sources, rd.num_inputs)) {
@@ -1091,6 +1129,10 @@ void RenderPipeline::submit(const ParamStore& params, const void* const* sources
   if (reused) cuda_check(cudaStreamWaitEvent(compute_, s.d2h, 0), "wait");
   const bool dev_conv = !f32_ && !conv_;
   if (dev_conv) mgb::launch_f64_to_f32(static_cast<const double*>(s.staging.ptr), arena, rd.num_inputs * stride_, compute_);
+  if (conv_ && kh < rd.num_inputs) {
+    mgb::launch_f64_to_f32(static_cast<const double*>(s.staging.ptr), arena + static_cast<long>(kh) * stride_,
+                           (rd.num_inputs - kh) * stride_, compute_);
+  }
   s.graph->launch(compute_);
   const long n_out = (rd.buffer_rows - rd.output_begin) * stride_;
   if (dev_conv) mgb::launch_f32_to_f64(arena + rd.output_begin * stride_, static_cast<double*>(s.staging.ptr), n_out, compute_);

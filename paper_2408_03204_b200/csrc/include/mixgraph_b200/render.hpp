@@ -16,29 +16,13 @@
 #include <utility>
 #include <vector>
 
+#include "mixgraph_b200/audio_buffer.hpp"
 #include "mixgraph_b200/schedule.hpp"
 
 typedef struct CUstream_st* cudaStream_t;
 typedef struct CUevent_st* cudaEvent_t;
 
 namespace mixgraph {
-
-struct AudioBuffer {
-  int batch = 1;
-  int channels = 2;
-  long length = 0;
-  double sample_rate = 44100.0;
-  std::vector<double> samples;  // [b][c][n]
-
-  AudioBuffer() = default;
-  AudioBuffer(int batch_, int channels_, long length_, double sample_rate_)
-      : batch(batch_), channels(channels_), length(length_), sample_rate(sample_rate_),
-        samples(static_cast<std::size_t>(batch_) * channels_ * length_, 0.0) {}
-  double* channel(int b, int c) { return samples.data() + (static_cast<std::size_t>(b) * channels + c) * length; }
-  const double* channel(int b, int c) const { return samples.data() + (static_cast<std::size_t>(b) * channels + c) * length; }
-  double& at(int b, int c, long n) { return channel(b, c)[n]; }
-  double at(int b, int c, long n) const { return channel(b, c)[n]; }
-};
 
 struct ProcessorConfig {
   double sample_rate = 44100.0;
@@ -224,12 +208,13 @@ class RenderGraph {
 // both directions runs concurrently with the GPU work. Host audio is float (f32_io, copied
 // straight into the arena) or double (converted on the device). Host buffers passed to
 // submit() must stay valid (and should be pinned) until sync().
-// Double host audio (the reference's AudioBuffer type) crosses PCIe as double and is converted
-// on the device (default). With `host_threads` > 0 it is converted to/from fp32 on host
-// worker threads instead, halving PCIe bytes (sources in submit(), outputs on a completion
-// thread once their D2H landed); measured slower on the B200 boxes' hosts (config 2: 0.77 vs
-// 0.66 ms per render with 8 threads), so the default (< 0: MGB_PIPELINE_HOST_THREADS or 0)
-// keeps device conversion.
+// Double host audio (the reference's AudioBuffer type) is converted to/from fp32 on host
+// worker threads (`host_threads`; < 0: MGB_PIPELINE_HOST_THREADS, else half the hardware
+// threads up to 8), which halves its PCIe bytes: sources in submit() in 1 MiB chunks whose
+// H2D copies start as each chunk is converted, outputs on a completion thread once their D2H
+// landed. A fraction of the sources (1 - kHostFraction) still crosses PCIe as double and is
+// converted on the device, so host memory bandwidth and PCIe work side by side. With
+// host_threads = 0 every source goes as double (device conversion only).
 class RenderPipeline {
  public:
   RenderPipeline(const DevicePlan& plan, const ProcessorSet& processors, int batch, long length, bool f32_io,
@@ -255,6 +240,8 @@ class RenderPipeline {
   std::size_t next_ = 0;
   struct HostConvert;  // worker pool + completion thread (double host audio)
   std::unique_ptr<HostConvert> conv_;
+  static constexpr double kHostFraction = 1.0;
+  double host_fraction_ = kHostFraction;
 };
 
 // Renders a stream of plans whose topology changes every batch (BASELINE config 3: 64

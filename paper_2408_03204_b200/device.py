@@ -170,7 +170,9 @@ class RenderPipeline:
     """Streaming host-buffer renders (mg_pipeline_*): submit() returns immediately; the H2D
     copies of render i+1 overlap the kernels of render i. `dtype` is the host audio type
     (np.float32: copied straight into the arena; np.float64: reference AudioBuffer precision,
-    converted on the device). Host arrays should be pinned (see `pinned`) and must stay alive
+    converted to fp32 on host worker threads in 1 MiB chunks whose H2D copies start as each
+    chunk is done — half the PCIe bytes; MGB_PIPELINE_HOST_THREADS=0 sends double and
+    converts on the device instead). Host arrays should be pinned (see `pinned`) and must stay alive
     until sync() — the pipeline keeps references until then."""
 
     def __init__(self, rd: RenderData, procs: ProcessorSet, batch: int, length: int, dtype=np.float32, depth: int = 2):

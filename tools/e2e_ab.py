@@ -1,10 +1,11 @@
-"""e2e A/B of RenderPipeline double-audio conversion: host threads vs device (config 2)."""
+"""e2e A/B of RenderPipeline double-audio conversion: host threads / host fraction vs device (config 2)."""
 import os
 import subprocess
 import sys
 
-for v in (sys.argv[1:] or ["0", "2", "4", "8"]):
-    env = dict(os.environ, MGB_PIPELINE_HOST_THREADS=v)
+for v in (sys.argv[1:] or ["0", "2", "4", "8"]):  # THREADS or THREADS:HOST_FRACTION
+    t, _, f = v.partition(":")
+    env = dict(os.environ, MGB_PIPELINE_HOST_THREADS=t, MGB_PIPELINE_HOST_FRACTION=f or "1")
     out = subprocess.run([sys.executable, "-c", """
 import sys, time, json; sys.path.insert(0, '.')
 import numpy as np, bench, paper_2408_03204_b200 as mg
