@@ -141,11 +141,12 @@ __device__ __forceinline__ void compose(float& A, float& B, float Ap, float Bp) 
 template <bool GATE, bool VEC, bool ENV = false>
 __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_taps, double floor_, int tiles_per_seq,
                                                          unsigned long long* status, unsigned int* ticket,
-                                                         float* env = nullptr) {
+                                                         float* env, PwEpi epi) {
   __shared__ float wA[kDynThreads / 32], wB[kDynThreads / 32];
   __shared__ float s_carry;
   __shared__ int s_ticket;
   __shared__ DynParams s_p;
+  __shared__ PwEpiSlots s_epi;
   // Tickets interleave sequences (all tile-0s, then all tile-1s, ...): a tile's
   // predecessors were dispatched `nseq` tickets earlier, so the carry rarely waits.
   const int nseq = a.slots * a.batch;
@@ -155,6 +156,7 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
     tk = __shfl_sync(0xffffffffu, tk, 0);
     if (threadIdx.x == 0) s_ticket = tk;
     derive_params(a.params + 4L * ((tk % nseq) / a.batch), env_taps, floor_, a.length, threadIdx.x, &s_p);
+    if (epi.n > 0 && threadIdx.x == 1) pw_epi_slots(epi, (tk % nseq) / a.batch, s_epi);
   }
   __syncthreads();
   const int tk = s_ticket;
@@ -301,6 +303,12 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
           orr[4 * q + k4] = yr[k4];
         }
       }
+    }
+    if (epi.n > 0) {
+      const long nq = n0 + 4 * q;
+      const long left = a.length - nq;
+      pw_epi_apply(epi, s_epi, a.rowstride, a.length, static_cast<long>(b) * 2 * a.length + nq, yl, yr, full,
+                   left < 0 ? 0 : (left < 4 ? static_cast<int>(left) : 4));
     }
   }
 }
@@ -653,7 +661,7 @@ void launch_dynamics_backward(bool gate, const StepArgs& fw, const StepArgs& bw,
   float* env = d.env;
   const dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(seqs));
 #define MGB_DYN_BWD(G, V)                                                                                  \
-  dyn_scan<G, V, true><<<fgrid, kDynThreads, 0, s>>>(fw, envelope_taps, energy_floor, tiles, status, ticket, env); \
+  dyn_scan<G, V, true><<<fgrid, kDynThreads, 0, s>>>(fw, envelope_taps, energy_floor, tiles, status, ticket, env, PwEpi{}); \
   dyn_bwd_dg<G, V><<<grid, kDynThreads, 0, s>>>(d);                                                        \
   dyn_bwd<V, 0><<<grid, kDynThreads, 0, s>>>(d);                                                            \
   dyn_bwd_carry<<<static_cast<unsigned>((seqs + 127) / 128), 128, 0, s>>>(d, static_cast<int>(seqs));        \
@@ -673,7 +681,7 @@ std::size_t dyn_sync_bytes(int slots, int batch, long length) {
 }
 
 void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double energy_floor, void* ws,
-                     bool zero_sync, cudaStream_t s) {
+                     bool zero_sync, cudaStream_t s, const PwEpi& epi) {
   if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
   const int tiles = static_cast<int>((a.length + kDynTile - 1) / kDynTile);
   const long total = static_cast<long>(a.slots) * a.batch * tiles;
@@ -684,11 +692,11 @@ void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double ene
   const bool vec = (a.length % 4 == 0) && (ne % 4 == 0);
   const dim3 grid(static_cast<unsigned>(total));
   if (gate) {
-    if (vec) dyn_scan<true, true><<<grid, kDynThreads, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, ticket);
-    else dyn_scan<true, false><<<grid, kDynThreads, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, ticket);
+    if (vec) dyn_scan<true, true><<<grid, kDynThreads, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, ticket, nullptr, epi);
+    else dyn_scan<true, false><<<grid, kDynThreads, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, ticket, nullptr, epi);
   } else {
-    if (vec) dyn_scan<false, true><<<grid, kDynThreads, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, ticket);
-    else dyn_scan<false, false><<<grid, kDynThreads, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, ticket);
+    if (vec) dyn_scan<false, true><<<grid, kDynThreads, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, ticket, nullptr, epi);
+    else dyn_scan<false, false><<<grid, kDynThreads, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, ticket, nullptr, epi);
   }
 }
 

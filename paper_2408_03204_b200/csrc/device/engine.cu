@@ -246,7 +246,7 @@ void run_prologue(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, voi
 // `join`: the step's prologue event when it has not been waited on yet (conv steps join
 // after their signal column pass; every other type joins first).
 void run_main(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, void* pws, void* mws, void* sws, bool zero_sync,
-              cudaStream_t s, cudaEvent_t join = nullptr) {
+              cudaStream_t s, cudaEvent_t join = nullptr, const mgb::PwEpi& epi = {}) {
   if (join && t != NodeType::Reverb && t != NodeType::Delay) {
     cuda_check(cudaStreamWaitEvent(s, join, 0), "wait");
     join = nullptr;
@@ -254,16 +254,16 @@ void run_main(NodeType t, const mgb::StepArgs& a, const ProcessorSet& p, void* p
   switch (t) {
     case NodeType::In:
     case NodeType::Out:
-    case NodeType::Mix: mgb::launch_pointwise(mgb::PointOp::Copy, a, s); break;
-    case NodeType::Gain: mgb::launch_pointwise(mgb::PointOp::Gain, a, s); break;
-    case NodeType::Imager: mgb::launch_pointwise(mgb::PointOp::Imager, a, s); break;
+    case NodeType::Mix: mgb::launch_pointwise(mgb::PointOp::Copy, a, s, epi); break;
+    case NodeType::Gain: mgb::launch_pointwise(mgb::PointOp::Gain, a, s, epi); break;
+    case NodeType::Imager: mgb::launch_pointwise(mgb::PointOp::Imager, a, s, epi); break;
     case NodeType::Eq:
       mgb::launch_eq_main(a, reinterpret_cast<float*>(static_cast<char*>(pws) + eq_taps_bytes(a.slots)), s);
       break;
     case NodeType::Compressor:
     case NodeType::Noisegate:
       mgb::launch_dynamics(t == NodeType::Noisegate, a, p.config().envelope_taps, p.config().energy_floor, sws, zero_sync,
-                           s);
+                           s, epi);
       break;
     case NodeType::Reverb: mgb::launch_conv_main(a, p.reverb_length(), pws, mws, s, join); break;
     case NodeType::Delay: mgb::launch_conv_main(a, p.delay_span(), pws, mws, s, join); break;
@@ -291,6 +291,24 @@ int chain_length(const RenderData& rd, std::size_t k, int batch, long length) {
     ++n;
   }
   return n >= 2 ? n : 1;
+}
+
+// Number of pointwise follower steps fused into step k's epilogue (render_arena): the
+// producer is a compressor / noisegate scan or a pointwise step too large for a chain
+// (vector path), the followers the consecutive steps the plan marked as followers.
+// MGB_NO_EPI=1 turns the fusion off (diagnostics / A-B).
+int epi_followers(const DevicePlan& plan, std::size_t k, int batch, long length) {
+  static const bool off = [] { const char* v = std::getenv("MGB_NO_EPI"); return v && v[0] == '1'; }();
+  const RenderData& rd = plan.data();
+  if (off || k + 1 >= rd.steps.size()) return 0;
+  const StepIndex& st = rd.steps[k];
+  const bool dyn = st.type == NodeType::Compressor || st.type == NodeType::Noisegate;
+  const bool pw = is_pointwise(st.type) && st.type != NodeType::In && length % 4 == 0 &&
+                  chain_length(rd, k, batch, length) == 1;
+  if (!dyn && !pw) return 0;
+  int n = 0;
+  while (n < mgb::kPwEpiMax && k + 1 + n < rd.steps.size() && plan.follows(static_cast<int>(k + 1 + n))) ++n;
+  return n;
 }
 
 // A first-step EQ whose grid is at most two waves runs its response-independent forward FFTs
@@ -366,6 +384,31 @@ void DevicePlan::build_index() {
   };
   for (const StepIndex& st : rd_.steps) emit(st.store_begin, st.store_end);
   emit(0, rd_.num_inputs);
+  // Pointwise followers (fused into the previous step's epilogue by render_arena).
+  follow_off_.assign(rd_.steps.size(), -1);
+  for (std::size_t k = 1; k < rd_.steps.size(); ++k) {
+    const StepIndex& st = rd_.steps[k];
+    const StepIndex& pv = rd_.steps[k - 1];
+    const NodeType t = st.type;
+    if (t != NodeType::Gain && t != NodeType::Imager && t != NodeType::Mix && t != NodeType::Out) continue;
+    const int slots = st.store_end - st.store_begin;
+    if (slots == 0 || slots != pv.store_end - pv.store_begin || st.gather.size() != static_cast<std::size_t>(slots)) continue;
+    std::vector<int> map(static_cast<std::size_t>(slots), -1);
+    bool ok = true;
+    for (int e = 0; e < slots && ok; ++e) {
+      const int src = st.gather[static_cast<std::size_t>(e)] - pv.store_begin;
+      ok = st.aggregate[static_cast<std::size_t>(e)] == e && src >= 0 && src < slots && map[static_cast<std::size_t>(src)] < 0;
+      if (ok) map[static_cast<std::size_t>(src)] = e;
+    }
+    if (!ok) continue;
+    follow_off_[k] = static_cast<long>(host.size());
+    host.insert(host.end(), map.begin(), map.end());
+  }
+}
+
+const int* DevicePlan::follow_map(int step) const {
+  const long off = follow_off_[static_cast<std::size_t>(step)];
+  return off < 0 ? nullptr : d_index_ + off;
 }
 
 DevicePlan::DevicePlan(const RenderData& rd) : rd_(rd) {
@@ -499,7 +542,7 @@ int DevicePlan::kernels_per_render(int batch, long length) const {
   for (std::size_t i = 0; i < rd_.steps.size();) {
     const int n = chain_length(rd_, i, batch, length);
     k += n > 1 ? 1 : step_kernels(rd_.steps[i].type);
-    i += static_cast<std::size_t>(n);
+    i += static_cast<std::size_t>(n > 1 ? n : 1 + epi_followers(*this, i, batch, length));
   }
   // A first-step EQ may be split into forward and inverse launches (render_arena, hoisted).
   if (split_first_eq(rd_, batch, length)) ++k;
@@ -586,6 +629,19 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
       k += static_cast<std::size_t>(chain - 1);
       continue;
     }
+    // Pointwise followers ride in this step's epilogue (not with per-step events, nor for a
+    // step that runs on the side lane).
+    mgb::PwEpi epi{};
+    if (!step_events && !lay.paired[k]) {
+      epi.n = epi_followers(plan, k, batch, length);
+      for (int f = 0; f < epi.n; ++f) {
+        const std::size_t j = k + 1 + static_cast<std::size_t>(f);
+        epi.op[f] = point_op(rd.steps[j].type);
+        epi.dst[f] = args[j].dst;
+        epi.map[f] = plan.follow_map(static_cast<int>(j));
+        epi.params[f] = args[j].params;
+      }
+    }
     if (!step_events && lay.paired[k]) {
       // Steps k and k+1 side by side: k on the lane, k+1 on the main stream, then join.
       const cudaEvent_t* le = plan.lane_events();
@@ -618,9 +674,10 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
       mgb::launch_eq_inverse(args[k], reinterpret_cast<float*>(pws + eq_taps_bytes(args[k].slots)),
                              reinterpret_cast<float2*>(mws), stream);
     } else {
-      run_main(t, args[k], procs, pws, mws, ws + lay.sync_off[k], false, stream, join);
+      run_main(t, args[k], procs, pws, mws, ws + lay.sync_off[k], false, stream, join, epi);
     }
     if (step_events) cuda_check(cudaEventRecord(step_events[2 * k + 1], stream), "event");
+    k += static_cast<std::size_t>(epi.n);
   }
   cuda_check(cudaGetLastError(), "render_arena launch");
 }
@@ -1009,7 +1066,11 @@ RenderPipeline::RenderPipeline(const DevicePlan& plan, const ProcessorSet& procs
       // Default: half the host's hardware threads, at most 8 (config 2 on the 16-thread B200
       // box hosts: 0.66 ms/render device conversion, 0.48 ms with 8 host threads).
       const char* v = std::getenv("MGB_PIPELINE_HOST_THREADS");  // diagnostics: 0 = device conversion
-      n = v ? std::atoi(v) : std::clamp(static_cast<int>(std::thread::hardware_concurrency()) / 2 - 1, 0, 7);
+      // Processes sharing the host (torchrun sets LOCAL_WORLD_SIZE) split its threads.
+      const char* lw = std::getenv("LOCAL_WORLD_SIZE");
+      const int procs_on_host = std::max(1, lw ? std::atoi(lw) : 1);
+      const int hw = static_cast<int>(std::thread::hardware_concurrency());
+      n = v ? std::atoi(v) : std::clamp(hw / (2 * procs_on_host) - 1, 0, 7);
     }
     if (n >= 1) conv_ = std::make_unique<HostConvert>(n, procs.device().device);
     const char* f = std::getenv("MGB_PIPELINE_HOST_FRACTION");  // diagnostics

@@ -9,10 +9,10 @@
 
 namespace mgb {
 
-enum class PointOp : int { Copy = 0, Gain = 1, Imager = 2 };
-
-// Gather-sum + copy / gain / imager + store (mix, out, gain, imager steps).
-void launch_pointwise(PointOp op, const StepArgs& a, cudaStream_t s);
+// Gather-sum + copy / gain / imager + store (mix, out, gain, imager steps); `epi`: fused
+// pointwise followers (step_common.cuh), vector path only (pointwise_epi_ok).
+void launch_pointwise(PointOp op, const StepArgs& a, cudaStream_t s, const PwEpi& epi = {});
+bool pointwise_epi_ok(const StepArgs& a);
 
 // A run of consecutive small pointwise steps (each slots*batch <= kPwChainMaxRows, L % 4 == 0)
 // in one launch, steps applied in order per sample group (latency-bound bus tails).
@@ -49,7 +49,7 @@ constexpr int kDynTile = kDynThreads * kDynPerThread;
 // every step's sync words with one memset per render).
 std::size_t dyn_sync_bytes(int slots, int batch, long length);
 void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double energy_floor, void* sync,
-                     bool zero_sync, cudaStream_t s);
+                     bool zero_sync, cudaStream_t s, const PwEpi& epi = {});
 
 // Backward of a compressor / noisegate step: `bw` gathers dy over the consumers' input
 // gradients (transposed CSR) and stores du into bw.dst; parameter gradients [slots][4] fp64

@@ -6,6 +6,7 @@
 // HBM-bound: per node-sample it moves 8*(deg_in + 1) bytes. One thread owns 4 consecutive
 // samples of both channels of one (slot, batch) row; float4 loads/stores when L % 4 == 0.
 #include <algorithm>
+#include <stdexcept>
 
 #include "launch.hpp"
 
@@ -44,7 +45,7 @@ __device__ __forceinline__ void coeffs(const StepArgs& a, int slot, float& g0, f
 // never its own output rows, so src and dst never alias (restrict is valid). Edges are
 // consumed 8 at a time (16 independent 16-byte loads in flight), summed in edge order.
 template <PointOp OP>
-__global__ void __launch_bounds__(kPwThreads) pointwise_vec4(StepArgs a) {
+__global__ void __launch_bounds__(kPwThreads) pointwise_vec4(StepArgs a, PwEpi epi) {
   const int sb = blockIdx.y;
   const int slot = sb / a.batch, b = sb - slot * a.batch;
   const long n4 = a.length >> 2;
@@ -83,6 +84,12 @@ __global__ void __launch_bounds__(kPwThreads) pointwise_vec4(StepArgs a) {
   float* __restrict__ out = a.dst + static_cast<long>(slot) * a.rowstride + boff;
   reinterpret_cast<float4*>(out)[i] = l;
   reinterpret_cast<float4*>(out + a.length)[i] = r;
+  if (epi.n > 0) {
+    PwEpiSlots c;
+    pw_epi_slots(epi, slot, c);
+    const float yl[4] = {l.x, l.y, l.z, l.w}, yr[4] = {r.x, r.y, r.z, r.w};
+    pw_epi_apply(epi, c, a.rowstride, a.length, boff + 4 * i, yl, yr, true, 4);
+  }
 }
 
 template <PointOp OP>
@@ -102,13 +109,13 @@ __global__ void __launch_bounds__(256) pointwise_scalar(StepArgs a) {
 }
 
 template <PointOp OP>
-void launch_op(const StepArgs& a, cudaStream_t s) {
+void launch_op(const StepArgs& a, cudaStream_t s, const PwEpi& epi) {
   const int rows = a.slots * a.batch;
   if (rows == 0 || a.length == 0) return;
   const bool vec = (a.length % 4) == 0;
   if (vec) {
     const dim3 grid(static_cast<unsigned>((a.length / 4 + kPwThreads - 1) / kPwThreads), static_cast<unsigned>(rows));
-    pointwise_vec4<OP><<<grid, kPwThreads, 0, s>>>(a);
+    pointwise_vec4<OP><<<grid, kPwThreads, 0, s>>>(a, epi);
     return;
   }
   long blocks = (a.length + 255) / 256;
@@ -198,11 +205,14 @@ void launch_pointwise_chain(const PwChain& c, cudaStream_t s) {
   pointwise_chain_vec4<<<grid, kPwThreads, 0, s>>>(c);
 }
 
-void launch_pointwise(PointOp op, const StepArgs& a, cudaStream_t s) {
+bool pointwise_epi_ok(const StepArgs& a) { return a.length % 4 == 0; }
+
+void launch_pointwise(PointOp op, const StepArgs& a, cudaStream_t s, const PwEpi& epi) {
+  if (epi.n > 0 && !pointwise_epi_ok(a)) throw std::invalid_argument("launch_pointwise: epilogue needs L % 4 == 0");
   switch (op) {
-    case PointOp::Copy: launch_op<PointOp::Copy>(a, s); break;
-    case PointOp::Gain: launch_op<PointOp::Gain>(a, s); break;
-    case PointOp::Imager: launch_op<PointOp::Imager>(a, s); break;
+    case PointOp::Copy: launch_op<PointOp::Copy>(a, s, epi); break;
+    case PointOp::Gain: launch_op<PointOp::Gain>(a, s, epi); break;
+    case PointOp::Imager: launch_op<PointOp::Imager>(a, s, epi); break;
   }
 }
 

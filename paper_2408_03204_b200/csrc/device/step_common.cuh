@@ -45,4 +45,89 @@ __device__ __forceinline__ float2 gather2(const StepArgs& a, int e0, int e1, int
 
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
 
+enum class PointOp : int { Copy = 0, Gain = 1, Imager = 2 };
+
+// Pointwise followers fused into the epilogue of the step before them. A follower is a
+// gain / imager / copy (mix, out) step whose every node has exactly one input edge, from a
+// distinct node of the previous step (the per-track chain noisegate -> imager -> gain of a
+// console). The producing kernel, holding output y of its slot s at some samples, computes
+// the follower's output for slot map[s] from y with the follower's own arithmetic and
+// stores it into the follower's row, and so on down the run; the followers' own launches and
+// their re-reads of the producer's rows disappear. Values are bit-identical to the separate
+// launches (the gather of one row is 0 + y there, kept here).
+constexpr int kPwEpiMax = 3;
+struct PwEpi {
+  int n = 0;                          // fused follower steps
+  PointOp op[kPwEpiMax] = {};
+  float* dst[kPwEpiMax] = {};         // follower's first output row
+  const int* map[kPwEpiMax] = {};     // previous step's slot -> follower slot
+  const double* params[kPwEpiMax] = {};
+};
+// Per (producer slot): the follower slots and their float coefficients (gain: exp(p_l),
+// exp(p_r); imager: exp(p_s); copy: 1).
+struct PwEpiSlots {
+  int slot[kPwEpiMax];
+  float g0[kPwEpiMax], g1[kPwEpiMax];
+};
+__device__ __forceinline__ void pw_epi_slots(const PwEpi& e, int slot, PwEpiSlots& c) {
+#pragma unroll
+  for (int f = 0; f < kPwEpiMax; ++f) {
+    if (f >= e.n) break;
+    slot = __ldg(e.map[f] + slot);
+    c.slot[f] = slot;
+    c.g0[f] = c.g1[f] = 1.f;
+    if (e.op[f] == PointOp::Gain) {
+      c.g0[f] = static_cast<float>(exp(e.params[f][2 * slot]));
+      c.g1[f] = static_cast<float>(exp(e.params[f][2 * slot + 1]));
+    } else if (e.op[f] == PointOp::Imager) {
+      c.g0[f] = static_cast<float>(exp(e.params[f][slot]));
+    }
+  }
+}
+__device__ __forceinline__ void pw_op(PointOp op, float& l, float& r, float g0, float g1) {
+  if (op == PointOp::Gain) {
+    l *= g0;
+    r *= g1;
+  } else if (op == PointOp::Imager) {
+    const float mid = l + r;
+    const float side = g0 * (l - r);
+    l = 0.5f * (mid + side);
+    r = 0.5f * (mid - side);
+  }
+}
+// Four consecutive samples (offset `off` = b*2*L + n within a row) of both channels; `full`:
+// all four valid and 16-byte aligned, else the first `valid` are stored one by one.
+__device__ __forceinline__ void pw_epi_apply(const PwEpi& e, const PwEpiSlots& c, long rowstride, long L, long off,
+                                             const float (&yl)[4], const float (&yr)[4], bool full, int valid) {
+  float l[4], r[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    l[k] = yl[k];
+    r[k] = yr[k];
+  }
+#pragma unroll
+  for (int f = 0; f < kPwEpiMax; ++f) {
+    if (f >= e.n) break;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      l[k] = 0.f + l[k];
+      r[k] = 0.f + r[k];
+      pw_op(e.op[f], l[k], r[k], c.g0[f], c.g1[f]);
+    }
+    float* out = e.dst[f] + static_cast<long>(c.slot[f]) * rowstride + off;
+    if (full) {
+      *reinterpret_cast<float4*>(out) = make_float4(l[0], l[1], l[2], l[3]);
+      *reinterpret_cast<float4*>(out + L) = make_float4(r[0], r[1], r[2], r[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (k < valid) {
+          out[k] = l[k];
+          out[L + k] = r[k];
+        }
+      }
+    }
+  }
+}
+
 }  // namespace mgb

@@ -127,6 +127,11 @@ class DevicePlan {
   const int* t_row_ptr(int step) const;
   const int* t_col(int step) const;
   const std::vector<int>& zero_rows() const { return zero_rows_; }
+  // Step k (k >= 1) is a pointwise follower of step k-1 (gain / imager / mix / out whose
+  // every node reads exactly one distinct node of step k-1): follow_map(k) maps step k-1's
+  // slots to step k's slots (device); nullptr otherwise.
+  bool follows(int step) const { return follow_off_[static_cast<std::size_t>(step)] >= 0; }
+  const int* follow_map(int step) const;
   std::size_t workspace_bytes(int batch, long length, const ProcessorSet& procs) const;
   // Workspace for a forward render followed by backward_arena (forward layout + scratch).
   std::size_t backward_workspace_bytes(int batch, long length, const ProcessorSet& procs) const;
@@ -161,7 +166,7 @@ class DevicePlan {
   const cudaEvent_t* borrowed_events_ = nullptr;
   const int* d_index_ = nullptr;
   std::vector<int> host_;
-  std::vector<long> rp_off_, col_off_, trp_off_, tcol_off_;
+  std::vector<long> rp_off_, col_off_, trp_off_, tcol_off_, follow_off_;
   std::vector<int> zero_rows_;
 };
 

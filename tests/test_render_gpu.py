@@ -521,3 +521,28 @@ def test_fused_kernel_rows_match_separate_pass(mg, ref, L):
     for k in g0:
         assert rel(g1[k], g0[k]) < 1e-4, k  # fp32 noise of small delay gradients (see test_backward_gpu)
     assert rel(o0, ref.Plan(t, e, 1).render(params, src)) < TOL
+
+
+@pytest.mark.parametrize("tracks,L,batch", [(8, 70000, 2), (8, 70001, 1), (3, 4093, 2)])
+def test_pointwise_epilogue_fusion_is_bit_exact(mg, ref, tracks, L, batch):
+    # Pointwise follower steps (the per-track noisegate -> imager -> gain chain, the bus tail
+    # compressor -> imager -> gain -> out) ride in the previous step's epilogue in render();
+    # render_profiled() launches every step on its own. Every arena row must be identical.
+    import torch
+    from paper_2408_03204_b200.device import DeviceRenderer
+    t, e = ref.console(tracks, 0.3, 7)
+    params = ref.random_legal_params(t, e, 8)
+    rd = mg.compute_render_data(make(mg, t, e))
+    procs = mg.ProcessorSet()
+    P = rd.reorder_params(params)
+    src = np.random.default_rng(3).uniform(-1, 1, size=(rd.num_inputs, batch, 2, L))
+    dr = DeviceRenderer(rd, procs, batch, L, P)
+    dr.sources.copy_(torch.as_tensor(src, dtype=torch.float32))
+    dr.render()
+    fused = dr.arena.clone()
+    dr.arena[rd.num_inputs:].fill_(float("nan"))
+    dr.render_profiled(sync=True)
+    torch.cuda.synchronize()
+    assert torch.equal(fused.view(torch.int32), dr.arena.view(torch.int32))
+    want = ref.Plan(t, e, 1).render(params, src)
+    assert rel(fused[rd.output_begin:].cpu().numpy(), want) < TOL
