@@ -44,7 +44,7 @@ __device__ __forceinline__ void coeffs(const StepArgs& a, int slot, float& g0, f
 // thread has exactly one). A step only reads rows stored by earlier steps (or zeroed rows),
 // never its own output rows, so src and dst never alias (restrict is valid). Edges are
 // consumed 8 at a time (16 independent 16-byte loads in flight), summed in edge order.
-template <PointOp OP>
+template <PointOp OP, bool EPI>
 __global__ void __launch_bounds__(kPwThreads) pointwise_vec4(StepArgs a, PwEpi epi) {
   const int sb = blockIdx.y;
   const int slot = sb / a.batch, b = sb - slot * a.batch;
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kPwThreads) pointwise_vec4(StepArgs a, PwEpi e
   float* __restrict__ out = a.dst + static_cast<long>(slot) * a.rowstride + boff;
   reinterpret_cast<float4*>(out)[i] = l;
   reinterpret_cast<float4*>(out + a.length)[i] = r;
-  if (epi.n > 0) {
+  if constexpr (EPI) {
     PwEpiSlots c;
     pw_epi_slots(epi, slot, c);
     const float yl[4] = {l.x, l.y, l.z, l.w}, yr[4] = {r.x, r.y, r.z, r.w};
@@ -115,7 +115,11 @@ void launch_op(const StepArgs& a, cudaStream_t s, const PwEpi& epi) {
   const bool vec = (a.length % 4) == 0;
   if (vec) {
     const dim3 grid(static_cast<unsigned>((a.length / 4 + kPwThreads - 1) / kPwThreads), static_cast<unsigned>(rows));
-    pointwise_vec4<OP><<<grid, kPwThreads, 0, s>>>(a, epi);
+    if (epi.n > 0) {
+      pointwise_vec4<OP, true><<<grid, kPwThreads, 0, s>>>(a, epi);
+    } else {
+      pointwise_vec4<OP, false><<<grid, kPwThreads, 0, s>>>(a, epi);
+    }
     return;
   }
   long blocks = (a.length + 255) / 256;

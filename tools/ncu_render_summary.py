@@ -97,11 +97,11 @@ def main():
             step = "compressor"
         elif "dyn_scan<1" in k:
             step = "noisegate"
-        elif "pointwise_vec4<0>" in k:
+        elif "pointwise_vec4<0" in k:
             step = "mix/out"
-        elif "pointwise_vec4<1>" in k:
+        elif "pointwise_vec4<1" in k:
             step = "gain"
-        elif "pointwise_vec4<2>" in k:
+        elif "pointwise_vec4<2" in k:
             step = "imager"
         elif "pointwise_chain" in k:
             step = "imager+gain+out (fused chain)"
