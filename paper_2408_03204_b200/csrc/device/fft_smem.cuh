@@ -290,6 +290,84 @@ __device__ __forceinline__ void fft_pow2(float2* buf, int fstride, const float2*
   Pow2Fft<LOG2N, 0, COUNT, NTHR, DIR>::run(buf, fstride, tw);
 }
 
+// ---- register-ended transforms ------------------------------------------------------------
+// The same pass plan with its first and/or last pass done straight from / into registers, so
+// the staging smem store before the first pass and the smem read after the last one (and
+// their barriers) disappear: a thread that loaded the 16 inputs of a radix-16 first-pass
+// butterfly from global memory transforms them at once, and a thread that holds the R
+// outputs of a last-pass butterfly writes them to global memory (twiddled) directly.
+__host__ __device__ constexpr int pow2_rl(int log2n, int logns) {
+  return (logns == 0 && log2n - logns >= 4) ? 4
+         : ((log2n - logns == 4 || log2n - logns == 2) ? 2 : (log2n - logns == 1 ? 1 : 3));
+}
+__host__ __device__ constexpr int pow2_last_logns(int log2n) {
+  int ns = 0;
+  while (ns + pow2_rl(log2n, ns) < log2n) ns += pow2_rl(log2n, ns);
+  return ns;
+}
+template <int LOG2N>
+struct Pow2Plan {
+  static constexpr int kLastLogNs = pow2_last_logns(LOG2N);
+  static constexpr int kLastNs = 1 << kLastLogNs;         // butterflies per transform in the last pass
+  static constexpr int kLastR = 1 << (LOG2N - kLastLogNs);
+  static constexpr int kFirstM = (1 << LOG2N) / 16;        // butterflies per transform in the first pass
+  static_assert(LOG2N >= 6 && pow2_rl(LOG2N, 0) == 4 && kLastLogNs >= 4, "register-ended plan needs 2+ passes");
+};
+
+template <int LOG2N, int LOGNS, int LOGEND, int COUNT, int NTHR, int DIR>
+struct Pow2FftRange {
+  static __device__ __forceinline__ void run(float2* buf, int fstride, const float2* tw) {
+    if constexpr (LOGNS < LOGEND) {
+      constexpr int RL = pow2_rl(LOG2N, LOGNS);
+      stockham_pass<(1 << LOG2N), (1 << RL), (1 << LOGNS), COUNT, NTHR, DIR>(buf, fstride, tw);
+      Pow2FftRange<LOG2N, LOGNS + RL, LOGEND, COUNT, NTHR, DIR>::run(buf, fstride, tw);
+    }
+  }
+};
+
+// First pass (radix 16, no twiddles) of butterfly j of the transform at `base`:
+// v[r] = element j + r*N/16 on entry. Writes the pass outputs; the caller barriers.
+template <int DIR>
+__device__ __forceinline__ void fft_first_from_regs(float2 (&v)[16], float2* base, int j) {
+  Dft<16, DIR>::run(v);
+  float2* sb = base + 17 * j;  // outputs 16 j + r: sidx(16 j + r) = 17 j + r
+#pragma unroll
+  for (int r = 0; r < 16; ++r) sb[r] = v[r];
+}
+
+// Passes between the first and the last (they start and end with a barrier).
+template <int LOG2N, int COUNT, int NTHR, int DIR>
+__device__ __forceinline__ void fft_middle(float2* buf, int fstride, const float2* tw) {
+  Pow2FftRange<LOG2N, 4, Pow2Plan<LOG2N>::kLastLogNs, COUNT, NTHR, DIR>::run(buf, fstride, tw);
+}
+
+// Every pass after the first (the first ran from registers; starts and ends with a barrier).
+template <int LOG2N, int COUNT, int NTHR, int DIR>
+__device__ __forceinline__ void fft_after_first(float2* buf, int fstride, const float2* tw) {
+  Pow2FftRange<LOG2N, 4, LOG2N, COUNT, NTHR, DIR>::run(buf, fstride, tw);
+}
+
+// Every pass but the last (smem in, smem out; for a transform whose input was staged in smem).
+template <int LOG2N, int COUNT, int NTHR, int DIR>
+__device__ __forceinline__ void fft_all_but_last(float2* buf, int fstride, const float2* tw) {
+  Pow2FftRange<LOG2N, 0, Pow2Plan<LOG2N>::kLastLogNs, COUNT, NTHR, DIR>::run(buf, fstride, tw);
+}
+
+// Last pass of butterfly j (< kLastNs) of the transform at `base`: on return v[r] = output
+// element j + r*kLastNs (reads smem after the previous pass's barrier; writes nothing).
+template <int LOG2N, int DIR>
+__device__ __forceinline__ void fft_last_to_regs(const float2* base, int j, const float2* __restrict__ tw,
+                                                 float2 (&v)[Pow2Plan<LOG2N>::kLastR]) {
+  constexpr int NS = Pow2Plan<LOG2N>::kLastNs, R = Pow2Plan<LOG2N>::kLastR;
+  TwBase<R, DIR> twb;
+  twb.load(tw, j * (kTwN / (NS * R)));
+  const float2* lb = base + sidx(j);  // inputs j + r*NS, NS a multiple of 16: immediate offsets
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r] = lb[r * padded(NS)];
+  twb.apply(v);
+  Dft<R, DIR>::run(v);
+}
+
 // 384 = 3 * 8 * 4 * 4 (reverb STFT frames); tw384[k] = exp(-2*pi*i*k/384), usually in smem.
 // Element i of transform f lives at buf[f*fstride + sidx(i)] (padded layout).
 template <int COUNT, int NTHR, int DIR>

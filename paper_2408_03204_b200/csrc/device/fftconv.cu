@@ -122,28 +122,33 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_fwd(StepArgs a, const flo
     }
     vals[q] = v;
   }
-#pragma unroll
-  for (int q = 0; q < EPT; ++q) {
-    const int idx = threadIdx.x + q * kColThreads;
-    tile[(idx % C) * FS + sidx(idx / C)] = vals[q];
-  }
+  // vals[q] = element j + q*N1/16 of column c (j = threadIdx.x / C): exactly the inputs of
+  // radix-16 first-pass butterfly j, so the first pass runs from registers.
+  const int c = threadIdx.x % C, jt = threadIdx.x / C;
+  fft_first_from_regs<-1>(vals, tile + c * FS, jt);
   __syncthreads();
-  fft_pow2<LN1, C, kColThreads, -1>(tile, FS, a.tw);
+  fft_middle<LN1, C, kColThreads, -1>(tile, FS, a.tw);
+  // Last pass into registers, four-step twiddle exp(-2 pi i n2 k1 / N), store. Outputs of
+  // butterfly j are k1 = j + r*NS: geometric in r, exact anchors (sincospif; n2 k1 < N <=
+  // 2^24 is exact in fp32) every 4 outputs, <= 3 chained products in between.
+  using Plan = Pow2Plan<LN1>;
+  constexpr int NS = Plan::kLastNs, R = Plan::kLastR, JSTEP = kColThreads / C;
   float2* o = out + static_cast<long>(item) * N;
   const float inv_n = 2.f / static_cast<float>(N);
-  // Four-step twiddle exp(-2 pi i n2 k1 / N). This thread's elements share n2 and step k1 by
-  // kColThreads / C, so the twiddles are geometric: exact anchors (sincospif; n2 k1 < N <=
-  // 2^24 is exact in fp32) every 4 elements, <= 3 chained products in between.
-  constexpr int KSTEP = kColThreads / C;
-  const int c = threadIdx.x % C, k1_0 = threadIdx.x / C;
   const long n2 = col0 + c;
-  const float2 step = expi_pi(-static_cast<float>(n2 * KSTEP) * inv_n);
-  float2 w = make_float2(1.f, 0.f);
+  const float2 step = expi_pi(-static_cast<float>(n2 * NS) * inv_n);
 #pragma unroll
-  for (int q = 0; q < kColElems / kColThreads; ++q) {
-    const int k1 = k1_0 + q * KSTEP;
-    w = (q % 4 == 0) ? expi_pi(-static_cast<float>(n2 * k1) * inv_n) : cmul(w, step);
-    o[static_cast<long>(k1) * N2 + n2] = cmul(tile[c * FS + sidx(k1)], w);
+  for (int p = 0; p < NS / JSTEP; ++p) {
+    const int j = jt + p * JSTEP;
+    float2 v[R];
+    fft_last_to_regs<LN1, -1>(tile + c * FS, j, a.tw, v);
+    float2 w = make_float2(1.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int k1 = j + r * NS;
+      w = (r % 4 == 0) ? expi_pi(-static_cast<float>(n2 * k1) * inv_n) : cmul(w, step);
+      o[static_cast<long>(k1) * N2 + n2] = cmul(v[r], w);
+    }
   }
 }
 
@@ -167,22 +172,28 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_inv(StepArgs a, int log_n
     const int idx = threadIdx.x + q * kColThreads;
     vals[q] = __ldg(x + static_cast<long>(idx / C) * N2 + col0 + idx % C);
   }
-#pragma unroll
-  for (int q = 0; q < EPT; ++q) {
-    const int idx = threadIdx.x + q * kColThreads;
-    tile[(idx % C) * FS + sidx(idx / C)] = vals[q];
-  }
+  // First pass from registers (vals[q] = element j + q*N1/16 of column c), last pass into
+  // registers and straight to the arena (outputs n1 = j + r*NS of column c).
+  const int c = threadIdx.x % C, jt = threadIdx.x / C;
+  fft_first_from_regs<+1>(vals, tile + c * FS, jt);
   __syncthreads();
-  fft_pow2<LN1, C, kColThreads, +1>(tile, FS, a.tw);
+  fft_middle<LN1, C, kColThreads, +1>(tile, FS, a.tw);
+  using Plan = Pow2Plan<LN1>;
+  constexpr int NS = Plan::kLastNs, R = Plan::kLastR, JSTEP = kColThreads / C;
   float* yl = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length;
   float* yr = yl + a.length;
-  for (int idx = threadIdx.x; idx < kColElems; idx += kColThreads) {
-    const int c = idx % C, n1 = idx / C;
-    const long n = static_cast<long>(n1) * N2 + col0 + c;
-    if (n < a.length) {
-      const float2 v = tile[c * FS + sidx(n1)];
-      yl[n] = v.x;
-      yr[n] = v.y;
+#pragma unroll
+  for (int p = 0; p < NS / JSTEP; ++p) {
+    const int j = jt + p * JSTEP;
+    float2 v[R];
+    fft_last_to_regs<LN1, +1>(tile + c * FS, j, a.tw, v);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const long n = static_cast<long>(j + r * NS) * N2 + col0 + c;
+      if (n < a.length) {
+        yl[n] = v[r].x;
+        yr[n] = v[r].y;
+      }
     }
   }
 }
@@ -249,20 +260,35 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2,
   const float2* pa = P + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
   const float2* pb = P + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
   constexpr int RS = padded(N2);  // second row's offset
-  // The kernel spectrum values this thread pairs are issued first, so their latency hides
+  // The kernel spectrum values this thread pairs are issued early, so their latency hides
   // behind the row loads and the forward FFT.
-  constexpr int KPT = (N2 + NT - 1) / NT;
+  constexpr int KPT = N2 / NT;
+  static_assert(KPT * NT == N2, "rows_conv: threads must tile a row");
   float2 pkv[KPT], pov[KPT];
-#pragma unroll
-  for (int q = 0; q < KPT; ++q) {
-    const int k = threadIdx.x + q * NT;
-    if (k < N2) {
-      const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
-      pkv[q] = __ldg(pa + k);
-      pov[q] = __ldg(pb + kb);
-    }
+#define MGB_PREFETCH_KERNEL_SPECTRUM()                                  \
+  _Pragma("unroll") for (int q = 0; q < KPT; ++q) {                    \
+    const int k = threadIdx.x + q * NT;                                \
+    const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);     \
+    pkv[q] = __ldg(pa + k);                                            \
+    pov[q] = __ldg(pb + kb);                                           \
   }
-  {
+  // Register-ended transforms when the threads are exactly the first pass's butterflies
+  // (every LN2 >= 8): thread t loads the 16 inputs j + r*N2/16 of row t / (N2/16) and runs
+  // that radix-16 butterfly from registers; the inverse's last pass writes global memory.
+  constexpr int M1 = N2 / 16;
+  constexpr bool REG = NT == 2 * M1 && LN2 >= 6;
+  if constexpr (REG) {
+    const int w = threadIdx.x / M1, j = threadIdx.x - (threadIdx.x / M1) * M1;
+    const float2* src = w == 0 ? xa : xb;
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = src[j + r * M1];
+    fft_first_from_regs<-1>(v, rows + w * RS, j);
+    MGB_PREFETCH_KERNEL_SPECTRUM()  // after the first pass: its 16 inputs are no longer live
+    __syncthreads();
+    fft_after_first<LN2, 2, NT, -1>(rows, RS, tw);
+  } else {
+    MGB_PREFETCH_KERNEL_SPECTRUM()
     constexpr int PER = N2 / NT;
     static_assert(PER * NT == N2, "rows_conv: threads must tile a row");
     float2 va[PER], vb[PER];  // loads in flight before any smem store
@@ -276,9 +302,10 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2,
       rows[sidx(threadIdx.x + q * NT)] = va[q];
       rows[RS + sidx(threadIdx.x + q * NT)] = vb[q];
     }
+    __syncthreads();
+    fft_pow2<LN2, 2, NT, -1>(rows, RS, tw);
   }
-  __syncthreads();
-  fft_pow2<LN2, 2, NT, -1>(rows, RS, tw);
+#undef MGB_PREFETCH_KERNEL_SPECTRUM
   const float s = 0.25f / static_cast<float>(N);
 #pragma unroll
   for (int q = 0; q < KPT; ++q) {
@@ -295,8 +322,34 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2,
     if (self) rows[sidx(kb)] = zo;
   }
   __syncthreads();
-  fft_pow2<LN2, 2, NT, +1>(rows, RS, tw);
   const float inv_n = 2.f / static_cast<float>(N);
+  if constexpr (REG) {
+    // Inverse: every pass but the last in smem, the last into registers, then the inverse
+    // four-step twiddle exp(+2 pi i k1 i / N) (outputs i = j + r*NS: geometric in r, exact
+    // anchors every 4) and the store. Half the threads per row, consecutive j per warp.
+    fft_all_but_last<LN2, 2, NT, +1>(rows, RS, tw);
+    constexpr int NS = Pow2Plan<LN2>::kLastNs, R = Pow2Plan<LN2>::kLastR, HT = NT / 2;
+    const int w = threadIdx.x / HT, jt = threadIdx.x - (threadIdx.x / HT) * HT;
+    if (w == 1 && self) return;
+    const int rw = w == 0 ? ra : rb;
+    float2* dst = w == 0 ? xa : xb;
+    const float2 step = expi_pi(static_cast<float>(static_cast<long>(rw) * NS) * inv_n);
+#pragma unroll
+    for (int p = 0; p < NS / HT; ++p) {
+      const int j = jt + p * HT;
+      float2 v[R];
+      fft_last_to_regs<LN2, +1>(rows + w * RS, j, tw, v);
+      float2 wt = make_float2(1.f, 0.f);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = j + r * NS;
+        wt = (r % 4 == 0) ? expi_pi(static_cast<float>(static_cast<long>(rw) * i) * inv_n) : cmul(wt, step);
+        dst[i] = cmul(v[r], wt);
+      }
+    }
+    return;
+  }
+  fft_pow2<LN2, 2, NT, +1>(rows, RS, tw);
   // Inverse four-step twiddle exp(+2 pi i k1 i / N): geometric in this thread's i (step NT),
   // exact anchors every 4 elements as in cols_fwd.
   const float2 step_a = expi_pi(static_cast<float>(static_cast<long>(ra) * NT) * inv_n);

@@ -45,7 +45,7 @@ __device__ __forceinline__ void coeffs(const StepArgs& a, int slot, float& g0, f
 // never its own output rows, so src and dst never alias (restrict is valid). Edges are
 // consumed 8 at a time (16 independent 16-byte loads in flight), summed in edge order.
 template <PointOp OP, bool EPI>
-__global__ void __launch_bounds__(kPwThreads) pointwise_vec4(StepArgs a, PwEpi epi) {
+__device__ __forceinline__ void pointwise_vec4_body(const StepArgs& a, const PwEpi& epi) {
   const int sb = blockIdx.y;
   const int slot = sb / a.batch, b = sb - slot * a.batch;
   const long n4 = a.length >> 2;
@@ -93,6 +93,18 @@ __global__ void __launch_bounds__(kPwThreads) pointwise_vec4(StepArgs a, PwEpi e
 }
 
 template <PointOp OP>
+__global__ void __launch_bounds__(kPwThreads) pointwise_vec4(StepArgs a) {
+  pointwise_vec4_body<OP, false>(a, PwEpi{});
+}
+
+// Same, with the step's pointwise followers in the epilogue (separate kernel: the plain one
+// keeps its small parameter block and register allocation).
+template <PointOp OP>
+__global__ void __launch_bounds__(kPwThreads) pointwise_vec4_epi(StepArgs a, PwEpi epi) {
+  pointwise_vec4_body<OP, true>(a, epi);
+}
+
+template <PointOp OP>
 __global__ void __launch_bounds__(256) pointwise_scalar(StepArgs a) {
   const int sb = blockIdx.y;
   const int slot = sb / a.batch, b = sb - slot * a.batch;
@@ -116,9 +128,9 @@ void launch_op(const StepArgs& a, cudaStream_t s, const PwEpi& epi) {
   if (vec) {
     const dim3 grid(static_cast<unsigned>((a.length / 4 + kPwThreads - 1) / kPwThreads), static_cast<unsigned>(rows));
     if (epi.n > 0) {
-      pointwise_vec4<OP, true><<<grid, kPwThreads, 0, s>>>(a, epi);
+      pointwise_vec4_epi<OP><<<grid, kPwThreads, 0, s>>>(a, epi);
     } else {
-      pointwise_vec4<OP, false><<<grid, kPwThreads, 0, s>>>(a, epi);
+      pointwise_vec4<OP><<<grid, kPwThreads, 0, s>>>(a);
     }
     return;
   }
