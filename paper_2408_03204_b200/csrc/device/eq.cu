@@ -102,8 +102,9 @@ template <int LOG> struct EqWin {
 };
 
 // grid (blocks per signal, slots*B). Block covers outputs [out0, out0 + kOut) from the
-// kFft-sample window starting at out0 - 1024 (both 4-aligned: float4 loads/stores when
-// L % 4 == 0); the circular convolution is exact for window indices [1023, kFft - 1024].
+// kFft-sample window starting at out0 - 1024; the circular convolution is exact for window
+// indices [1023, kFft - 1024]. Window loads feed the first FFT pass directly and the last
+// inverse pass stores directly (register-ended transforms, fft_smem.cuh), both coalesced.
 template <int MODE, int LOG>
 __global__ void __launch_bounds__(EqWin<LOG>::kThreads, EqWin<LOG>::kMinBlocks) eq_conv(StepArgs a, const float* resp, float2* spec) {
   using W = EqWin<LOG>;
@@ -117,7 +118,6 @@ __global__ void __launch_bounds__(EqWin<LOG>::kThreads, EqWin<LOG>::kMinBlocks) 
   const long out0 = static_cast<long>(blockIdx.x) * kEqOut;
   const long s0 = out0 - (kEqHalf + 1);
   const long boff = static_cast<long>(b) * 2 * a.length;
-  const bool vec = (a.length & 3) == 0;
   float2* sp = spec + (static_cast<long>(sb) * gridDim.x + blockIdx.x) * kEqFft;  // MODE 1/2 scratch
   const float* rs = resp + static_cast<long>(slot) * 8192;
   if constexpr (MODE == 2) {
@@ -140,70 +140,71 @@ __global__ void __launch_bounds__(EqWin<LOG>::kThreads, EqWin<LOG>::kMinBlocks) 
     }
     __syncthreads();
   } else {
-  // Gather-sum of the window, edges outermost so every float4 group of this thread is in
-  // flight at once; per element the sum runs in edge order (as the reference's gather).
-  constexpr int G = kEqFft / 4 / kNt;  // float4 groups per thread
-  static_assert(G * 4 * kNt == kEqFft, "eq_conv: threads must tile the window");
-  float4 lg[G], rg[G];
+  // Gather-sum of the window straight into the radix-16 first-pass butterfly this thread
+  // owns (elements t + r*N/16: consecutive threads read consecutive samples), edges
+  // outermost so all 16 sample pairs are in flight at once; per element the sum runs in
+  // edge order (as the reference's gather).
+  constexpr int M1 = kEqFft / 16;
+  static_assert(M1 == kNt, "eq_conv: threads must be the first pass's butterflies");
+  float2 v[16];
 #pragma unroll
-  for (int g = 0; g < G; ++g) lg[g] = rg[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int r = 0; r < 16; ++r) v[r] = make_float2(0.f, 0.f);
   for (int e = e0; e < e1; ++e) {
     const float* p = a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff;
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const long pos = s0 + 4 * (threadIdx.x + g * kNt);
-      if (vec && pos >= 0 && pos + 4 <= a.length) {
-        lg[g] = f4add(lg[g], __ldg(reinterpret_cast<const float4*>(p + pos)));
-        rg[g] = f4add(rg[g], __ldg(reinterpret_cast<const float4*>(p + a.length + pos)));
-      } else {
-        float lv[4] = {lg[g].x, lg[g].y, lg[g].z, lg[g].w}, rv[4] = {rg[g].x, rg[g].y, rg[g].z, rg[g].w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (pos + u >= 0 && pos + u < a.length) {
-            lv[u] += __ldg(p + pos + u);
-            rv[u] += __ldg(p + a.length + pos + u);
-          }
-        }
-        lg[g] = make_float4(lv[0], lv[1], lv[2], lv[3]);
-        rg[g] = make_float4(rv[0], rv[1], rv[2], rv[3]);
+    for (int r = 0; r < 16; ++r) {
+      const long pos = s0 + threadIdx.x + r * M1;
+      if (pos >= 0 && pos < a.length) {
+        v[r].x += __ldg(p + pos);
+        v[r].y += __ldg(p + a.length + pos);
       }
     }
   }
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const int t4 = threadIdx.x + g * kNt;
-    buf[sidx(4 * t4)] = make_float2(lg[g].x, rg[g].x);
-    buf[sidx(4 * t4 + 1)] = make_float2(lg[g].y, rg[g].y);
-    buf[sidx(4 * t4 + 2)] = make_float2(lg[g].z, rg[g].z);
-    buf[sidx(4 * t4 + 3)] = make_float2(lg[g].w, rg[g].w);
-  }
+  fft_first_from_regs<-1>(v, buf, threadIdx.x);
   __syncthreads();
-  fft_pow2<LOG, 1, kNt, -1>(buf, padded(kEqFft), a.tw);
+  fft_middle<LOG, 1, kNt, -1>(buf, padded(kEqFft), a.tw);
+  // Last forward pass into registers: MODE 1 stores the spectrum, MODE 0 multiplies by the
+  // response and writes the product back (in place: after every thread has read its inputs).
+  constexpr int NS = Pow2Plan<LOG>::kLastNs, R = Pow2Plan<LOG>::kLastR, PL = NS / kNt;
+  float2 o[PL][R];
+#pragma unroll
+  for (int p = 0; p < PL; ++p) fft_last_to_regs<LOG, -1>(buf, threadIdx.x + p * kNt, a.tw, o[p]);
   if constexpr (MODE == 1) {
-    for (int t = threadIdx.x; t < kEqFft; t += blockDim.x) sp[t] = buf[sidx(t)];
+#pragma unroll
+    for (int p = 0; p < PL; ++p) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) sp[threadIdx.x + p * kNt + r * NS] = o[p][r];
+    }
     return;
   }
-  for (int t = threadIdx.x; t < kEqFft; t += blockDim.x) buf[sidx(t)] = cscale(buf[sidx(t)], rscale * __ldg(rs + kRs * t));
+  __syncthreads();
+#pragma unroll
+  for (int p = 0; p < PL; ++p) {
+    const int j = threadIdx.x + p * kNt;
+    float2* sb = buf + sidx(j);
+#pragma unroll
+    for (int r = 0; r < R; ++r) sb[r * padded(NS)] = cscale(o[p][r], rscale * __ldg(rs + kRs * (j + r * NS)));
+  }
   __syncthreads();
   }
-  fft_pow2<LOG, 1, kNt, +1>(buf, padded(kEqFft), a.tw);
+  // Inverse: every pass but the last in smem, the last into registers and straight to the
+  // arena (window index w = j + r*NS holds output out0 + w - 1024 for w in [1024, 1024 + kEqOut)).
+  fft_all_but_last<LOG, 1, kNt, +1>(buf, padded(kEqFft), a.tw);
+  constexpr int NS = Pow2Plan<LOG>::kLastNs, R = Pow2Plan<LOG>::kLastR, PL = NS / kNt;
   float* yl = a.dst + static_cast<long>(slot) * a.rowstride + boff;
   float* yr = yl + a.length;
-  for (int t4 = threadIdx.x; t4 < kEqOut / 4; t4 += blockDim.x) {
-    const long pos = out0 + 4 * t4;
-    const int w = kEqHalf + 1 + 4 * t4;
-    const float2 v0 = buf[sidx(w)], v1 = buf[sidx(w + 1)], v2 = buf[sidx(w + 2)], v3 = buf[sidx(w + 3)];
-    if (vec && pos + 4 <= a.length) {
-      *reinterpret_cast<float4*>(yl + pos) = make_float4(v0.x, v1.x, v2.x, v3.x);
-      *reinterpret_cast<float4*>(yr + pos) = make_float4(v0.y, v1.y, v2.y, v3.y);
-    } else {
-      const float2 vv[4] = {v0, v1, v2, v3};
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (pos + u < a.length) {
-          yl[pos + u] = vv[u].x;
-          yr[pos + u] = vv[u].y;
-        }
+  for (int p = 0; p < PL; ++p) {
+    const int j = threadIdx.x + p * kNt;
+    float2 y[R];
+    fft_last_to_regs<LOG, +1>(buf, j, a.tw, y);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int w = j + r * NS;
+      const long pos = out0 + w - (kEqHalf + 1);
+      if (w >= kEqHalf + 1 && w < kEqHalf + 1 + kEqOut && pos < a.length) {
+        yl[pos] = y[r].x;
+        yr[pos] = y[r].y;
       }
     }
   }
