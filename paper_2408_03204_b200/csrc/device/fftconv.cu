@@ -215,6 +215,59 @@ constexpr int row_threads() {
 }
 constexpr int kSpecRows = 4;  // kernel-spectrum rows per CTA
 
+// Register-ended row transforms apply when a CTA's threads are exactly the radix-16 first
+// pass's butterflies over its COUNT rows (row_threads not clamped).
+template <int LN2, int COUNT>
+constexpr bool rows_reg() {
+  return row_threads<LN2, COUNT>() == COUNT * (1 << LN2) / 16 && LN2 >= 6;
+}
+
+// COUNT rows src[w] -> radix-16 first pass from registers into rows + w*RS, barrier, the
+// remaining forward passes (thread t owns butterfly t % (N2/16) of row t / (N2/16)).
+template <int LN2, int COUNT, int NT>
+__device__ __forceinline__ void rows_forward_from_global(float2* rows, int RS, const float2* s0, const float2* s1,
+                                                         const float2* s2, const float2* s3, const float2* tw) {
+  constexpr int M1 = (1 << LN2) / 16;
+  const int w = threadIdx.x / M1, j = threadIdx.x - (threadIdx.x / M1) * M1;
+  const float2* p = w == 0 ? s0 : (w == 1 ? s1 : (w == 2 ? s2 : s3));  // selects, no local array
+  float2 v[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = p[j + r * M1];
+  fft_first_from_regs<-1>(v, rows + w * RS, j);
+  __syncthreads();
+  fft_after_first<LN2, COUNT, NT, -1>(rows, RS, tw);
+}
+
+// Two rows (rows, rows + RS) inverse-transformed in smem up to the last pass, which goes to
+// registers: output i of row w is scaled by the inverse four-step twiddle exp(+2 pi i r_w i / N)
+// (geometric in i = j + r*NS, exact anchors every 4) and stored to dst_w[i]; row b is skipped
+// when it is row a (self-paired rows). Half the threads per row, consecutive j per warp.
+template <int LN2, int NT>
+__device__ __forceinline__ void rows_inverse_to_global(float2* rows, int RS, int ra, int rb, bool self, float2* da,
+                                                       float2* db, float inv_n, const float2* tw) {
+  fft_all_but_last<LN2, 2, NT, +1>(rows, RS, tw);
+  constexpr int NS = Pow2Plan<LN2>::kLastNs, R = Pow2Plan<LN2>::kLastR, HT = NT / 2;
+  static_assert(NS % HT == 0, "rows_inverse_to_global: threads must tile the last pass");
+  const int w = threadIdx.x / HT, jt = threadIdx.x - (threadIdx.x / HT) * HT;
+  if (w == 1 && self) return;
+  const int rw = w == 0 ? ra : rb;
+  float2* dst = w == 0 ? da : db;
+  const float2 step = expi_pi(static_cast<float>(static_cast<long>(rw) * NS) * inv_n);
+#pragma unroll
+  for (int p = 0; p < NS / HT; ++p) {
+    const int j = jt + p * HT;
+    float2 v[R];
+    fft_last_to_regs<LN2, +1>(rows + w * RS, j, tw, v);
+    float2 wt = make_float2(1.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = j + r * NS;
+      wt = (r % 4 == 0) ? expi_pi(static_cast<float>(static_cast<long>(rw) * i) * inv_n) : cmul(wt, step);
+      dst[i] = cmul(v[r], wt);
+    }
+  }
+}
+
 // Forward row FFTs of the packed kernel, kSpecRows consecutive rows per CTA.
 // grid (N1 / kSpecRows, slots)
 template <int LN2>
@@ -227,6 +280,27 @@ __global__ void __launch_bounds__(row_threads<LN2, kSpecRows>()) rows_spec(int l
   float2* p = P + static_cast<long>(blockIdx.y) * N + static_cast<long>(blockIdx.x) * kSpecRows * N2;
   // All of this thread's loads are issued before any smem store (loads in flight, not a
   // load -> store dependency per element).
+  if constexpr (rows_reg<LN2, kSpecRows>()) {
+    constexpr int M1 = N2 / 16;
+    const int w = threadIdx.x / M1, j = threadIdx.x - (threadIdx.x / M1) * M1;
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = p[w * N2 + j + r * M1];
+    fft_first_from_regs<-1>(v, row + w * RS, j);
+    __syncthreads();
+    fft_middle<LN2, kSpecRows, NT, -1>(row, RS, tw);
+    constexpr int NS = Pow2Plan<LN2>::kLastNs, R = Pow2Plan<LN2>::kLastR;
+    static_assert((kSpecRows * NS) % NT == 0, "rows_spec: threads must tile the last pass");
+#pragma unroll
+    for (int q = 0; q < kSpecRows * NS / NT; ++q) {
+      const int bq = threadIdx.x + q * NT, f = bq / NS, jb = bq - f * NS;
+      float2 y[R];
+      fft_last_to_regs<LN2, -1>(row + f * RS, jb, tw, y);
+#pragma unroll
+      for (int r = 0; r < R; ++r) p[f * N2 + jb + r * NS] = y[r];
+    }
+    return;
+  }
   constexpr int PER = kSpecRows * N2 / NT;
   static_assert(PER * NT == kSpecRows * N2, "rows_spec: threads must tile the rows");
   float2 v[PER];
@@ -275,9 +349,10 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2,
   // Register-ended transforms when the threads are exactly the first pass's butterflies
   // (every LN2 >= 8): thread t loads the 16 inputs j + r*N2/16 of row t / (N2/16) and runs
   // that radix-16 butterfly from registers; the inverse's last pass writes global memory.
-  constexpr int M1 = N2 / 16;
-  constexpr bool REG = NT == 2 * M1 && LN2 >= 6;
+  constexpr bool REG = rows_reg<LN2, 2>();
   if constexpr (REG) {
+    // (the kernel-spectrum prefetch is issued after the first pass, registers permitting)
+    constexpr int M1 = N2 / 16;
     const int w = threadIdx.x / M1, j = threadIdx.x - (threadIdx.x / M1) * M1;
     const float2* src = w == 0 ? xa : xb;
     float2 v[16];
@@ -324,29 +399,7 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2,
   __syncthreads();
   const float inv_n = 2.f / static_cast<float>(N);
   if constexpr (REG) {
-    // Inverse: every pass but the last in smem, the last into registers, then the inverse
-    // four-step twiddle exp(+2 pi i k1 i / N) (outputs i = j + r*NS: geometric in r, exact
-    // anchors every 4) and the store. Half the threads per row, consecutive j per warp.
-    fft_all_but_last<LN2, 2, NT, +1>(rows, RS, tw);
-    constexpr int NS = Pow2Plan<LN2>::kLastNs, R = Pow2Plan<LN2>::kLastR, HT = NT / 2;
-    const int w = threadIdx.x / HT, jt = threadIdx.x - (threadIdx.x / HT) * HT;
-    if (w == 1 && self) return;
-    const int rw = w == 0 ? ra : rb;
-    float2* dst = w == 0 ? xa : xb;
-    const float2 step = expi_pi(static_cast<float>(static_cast<long>(rw) * NS) * inv_n);
-#pragma unroll
-    for (int p = 0; p < NS / HT; ++p) {
-      const int j = jt + p * HT;
-      float2 v[R];
-      fft_last_to_regs<LN2, +1>(rows + w * RS, j, tw, v);
-      float2 wt = make_float2(1.f, 0.f);
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = j + r * NS;
-        wt = (r % 4 == 0) ? expi_pi(static_cast<float>(static_cast<long>(rw) * i) * inv_n) : cmul(wt, step);
-        dst[i] = cmul(v[r], wt);
-      }
-    }
+    rows_inverse_to_global<LN2, NT>(rows, RS, ra, rb, self, xa, xb, inv_n, tw);
     return;
   }
   fft_pow2<LN2, 2, NT, +1>(rows, RS, tw);
@@ -392,7 +445,10 @@ __global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_conv_fk(int log_n,
   float2* xb = X + static_cast<long>(item) * N + static_cast<long>(rb) * N2;
   const float2* ka = K + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
   const float2* kb_ = K + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
-  {
+  constexpr bool REG = rows_reg<LN2, 4>();
+  if constexpr (REG) {
+    rows_forward_from_global<LN2, 4, NT>(rows, RS, xa, xb, ka, kb_, tw);
+  } else {
     constexpr int PER = (N2 + NT - 1) / NT;
     float2 v[4][PER];
 #pragma unroll
@@ -413,9 +469,9 @@ __global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_conv_fk(int log_n,
         for (int r = 0; r < 4; ++r) rows[r * RS + sidx(i)] = v[r][q];
       }
     }
+    __syncthreads();
+    fft_pow2<LN2, 4, NT, -1>(rows, RS, tw);
   }
-  __syncthreads();
-  fft_pow2<LN2, 4, NT, -1>(rows, RS, tw);
   const float s = 0.25f / static_cast<float>(N);
   constexpr int KPT = (N2 + NT - 1) / NT;
   float2 zk[KPT], zo[KPT];
@@ -441,8 +497,12 @@ __global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_conv_fk(int log_n,
     else rows[RS + sidx(kb)] = zo[q];
   }
   __syncthreads();
-  fft_pow2<LN2, 2, NT, +1>(rows, RS, tw);
   const float inv_n = 2.f / static_cast<float>(N);
+  if constexpr (REG) {
+    rows_inverse_to_global<LN2, NT>(rows, RS, ra, rb, self, xa, xb, inv_n, tw);
+    return;
+  }
+  fft_pow2<LN2, 2, NT, +1>(rows, RS, tw);
   for (int i = threadIdx.x; i < N2; i += NT) {
     xa[i] = cmul(rows[sidx(i)], expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n));
     if (!self) xb[i] = cmul(rows[RS + sidx(i)], expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n));
@@ -745,14 +805,18 @@ __global__ void __launch_bounds__(row_threads<LN2, 4>(), MGB_RBWD_MINB) rows_bwd
     const float2* xa = X + item * N + static_cast<long>(ra) * N2;
     const float2* xb = X + item * N + static_cast<long>(rb) * N2;
     __syncthreads();  // previous item's rows fully consumed
-    for (int i = threadIdx.x; i < N2; i += NT) {
-      rows[sidx(i)] = da[i];
-      rows[RS + sidx(i)] = db[i];
-      rows[2 * RS + sidx(i)] = xa[i];
-      rows[3 * RS + sidx(i)] = xb[i];
+    if constexpr (rows_reg<LN2, 4>()) {
+      rows_forward_from_global<LN2, 4, NT>(rows, RS, da, db, xa, xb, tw);
+    } else {
+      for (int i = threadIdx.x; i < N2; i += NT) {
+        rows[sidx(i)] = da[i];
+        rows[RS + sidx(i)] = db[i];
+        rows[2 * RS + sidx(i)] = xa[i];
+        rows[3 * RS + sidx(i)] = xb[i];
+      }
+      __syncthreads();
+      fft_pow2<LN2, 4, NT, -1>(rows, RS, tw);
     }
-    __syncthreads();
-    fft_pow2<LN2, 4, NT, -1>(rows, RS, tw);
     // Each (k, N-k) pair is read and written by one thread only: products in place.
     for (int k = threadIdx.x; k < N2; k += NT) {
       const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
@@ -770,16 +834,24 @@ __global__ void __launch_bounds__(row_threads<LN2, 4>(), MGB_RBWD_MINB) rows_bwd
       rows[ob] = zmix(dn, cconj(dk), hk, cconj(hn), s);
     }
     __syncthreads();
-    fft_pow2<LN2, 2, NT, +1>(rows, RS, tw);
-    for (int i = threadIdx.x; i < N2; i += NT) {
-      da[i] = cmul(rows[sidx(i)], expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n));
-      if (!self) db[i] = cmul(rows[RS + sidx(i)], expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n));
+    if constexpr (rows_reg<LN2, 4>()) {
+      rows_inverse_to_global<LN2, NT>(rows, RS, ra, rb, self, da, db, inv_n, tw);
+    } else {
+      fft_pow2<LN2, 2, NT, +1>(rows, RS, tw);
+      for (int i = threadIdx.x; i < N2; i += NT) {
+        da[i] = cmul(rows[sidx(i)], expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n));
+        if (!self) db[i] = cmul(rows[RS + sidx(i)], expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n));
+      }
     }
   }
   __syncthreads();
-  fft_pow2<LN2, 2, NT, +1>(A, RS, tw);
   float2* oa = X + static_cast<long>(slot) * batch * N + static_cast<long>(ra) * N2;
   float2* ob = X + static_cast<long>(slot) * batch * N + static_cast<long>(rb) * N2;
+  if constexpr (rows_reg<LN2, 4>()) {
+    rows_inverse_to_global<LN2, NT>(A, RS, ra, rb, self, oa, ob, inv_n, tw);
+    return;
+  }
+  fft_pow2<LN2, 2, NT, +1>(A, RS, tw);
   for (int i = threadIdx.x; i < N2; i += NT) {
     oa[i] = cmul(A[sidx(i)], expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n));
     if (!self) ob[i] = cmul(A[RS + sidx(i)], expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n));
@@ -800,15 +872,27 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_inv_buf(int log_n, int ba
   const int slot = blockIdx.y;
   const long col0 = static_cast<long>(blockIdx.x) * C;
   const float2* x = X + static_cast<long>(slot) * batch * N;
-  for (int idx = threadIdx.x; idx < kColElems; idx += kColThreads) {
-    tile[(idx % C) * FS + sidx(idx / C)] = __ldg(x + static_cast<long>(idx / C) * N2 + col0 + idx % C);
-  }
+  // Register-ended column transform (as cols_inv): thread (c, j) loads the 16 inputs of its
+  // first-pass butterfly and stores its last-pass outputs.
+  constexpr int M1 = N1 / 16, JSTEP = kColThreads / C;
+  const int c = threadIdx.x % C, jt = threadIdx.x / C;
+  float2 v[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = __ldg(x + static_cast<long>(jt + r * M1) * N2 + col0 + c);
+  fft_first_from_regs<+1>(v, tile + c * FS, jt);
   __syncthreads();
-  fft_pow2<LN1, C, kColThreads, +1>(tile, FS, tw);
-  for (int idx = threadIdx.x; idx < kColElems; idx += kColThreads) {
-    const int c = idx % C, n1 = idx / C;
-    const long n = static_cast<long>(n1) * N2 + col0 + c;
-    if (n < taps) out[static_cast<long>(slot) * taps + n] = tile[c * FS + sidx(n1)];
+  fft_middle<LN1, C, kColThreads, +1>(tile, FS, tw);
+  constexpr int NS = Pow2Plan<LN1>::kLastNs, R = Pow2Plan<LN1>::kLastR;
+#pragma unroll
+  for (int p = 0; p < NS / JSTEP; ++p) {
+    const int j = jt + p * JSTEP;
+    float2 y[R];
+    fft_last_to_regs<LN1, +1>(tile + c * FS, j, tw, y);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const long n = static_cast<long>(j + r * NS) * N2 + col0 + c;
+      if (n < taps) out[static_cast<long>(slot) * taps + n] = y[r];
+    }
   }
 }
 
