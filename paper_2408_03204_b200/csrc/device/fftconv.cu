@@ -29,6 +29,15 @@ namespace {
 
 constexpr int kColElems = 8192;  // complex elements per column tile (64 KiB)
 constexpr int kColThreads = 512;
+#ifndef MGB_RCONV_PREFETCH
+// rows_conv kernel-spectrum staging: 0 loaded at use (default: no registers held across the
+// forward transform, no spills; measured fastest), 1 registers (issued early; spills),
+// 2 cp.async into shared memory (no registers held across the forward transform)
+#define MGB_RCONV_PREFETCH 0
+#endif
+#ifndef MGB_RCONV_THREADS_PER_SM
+#define MGB_RCONV_THREADS_PER_SM 1024  // resident rows_conv threads per SM the register budget is sized for
+#endif
 #ifndef MGB_RBWD_MINB
 #define MGB_RBWD_MINB 2  // resident CTAs per SM rows_bwd is compiled for (3: spills, measured slower)
 #endif
@@ -319,7 +328,7 @@ __global__ void __launch_bounds__(row_threads<LN2, kSpecRows>()) rows_spec(int l
 // Signal rows k1 = r and N1 - r together: forward FFTs, channel-split product with the
 // kernel spectrum, inverse FFTs, inverse four-step twiddle. grid (N1/2 + 1, slots*B)
 template <int LN2>
-__global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2, 2>()) rows_conv(int log_n, int batch, float2* X, const float2* P, const float2* tw) {
+__global__ void __launch_bounds__(row_threads<LN2, 2>(), MGB_RCONV_THREADS_PER_SM / row_threads<LN2, 2>()) rows_conv(int log_n, int batch, float2* X, const float2* P, const float2* tw) {
   constexpr int N2 = 1 << LN2;
   constexpr int NT = row_threads<LN2, 2>();
   extern __shared__ float2 rows[];  // [2][N2]
@@ -338,6 +347,7 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2,
   // behind the row loads and the forward FFT.
   constexpr int KPT = N2 / NT;
   static_assert(KPT * NT == N2, "rows_conv: threads must tile a row");
+#if MGB_RCONV_PREFETCH == 1
   float2 pkv[KPT], pov[KPT];
 #define MGB_PREFETCH_KERNEL_SPECTRUM()                                  \
   _Pragma("unroll") for (int q = 0; q < KPT; ++q) {                    \
@@ -346,6 +356,23 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2,
     pkv[q] = __ldg(pa + k);                                            \
     pov[q] = __ldg(pb + kb);                                           \
   }
+#elif MGB_RCONV_PREFETCH == 2
+  // Each thread copies exactly the kernel values it pairs later (own cp.async group: no
+  // barrier needed before it reads them back).
+  float2* sp = rows + 2 * RS;
+#define MGB_PREFETCH_KERNEL_SPECTRUM()                                                              \
+  _Pragma("unroll") for (int q = 0; q < KPT; ++q) {                                                \
+    const int k = threadIdx.x + q * NT;                                                            \
+    const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);                                 \
+    const unsigned da = static_cast<unsigned>(__cvta_generic_to_shared(sp + sidx(k)));              \
+    const unsigned db = static_cast<unsigned>(__cvta_generic_to_shared(sp + RS + sidx(k)));         \
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(da), "l"(pa + k) : "memory");  \
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(db), "l"(pb + kb) : "memory"); \
+  }                                                                                                \
+  asm volatile("cp.async.commit_group;" ::: "memory");
+#else
+#define MGB_PREFETCH_KERNEL_SPECTRUM()
+#endif
   // Register-ended transforms when the threads are exactly the first pass's butterflies
   // (every LN2 >= 8): thread t loads the 16 inputs j + r*N2/16 of row t / (N2/16) and runs
   // that radix-16 butterfly from registers; the inverse's last pass writes global memory.
@@ -382,6 +409,9 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2,
   }
 #undef MGB_PREFETCH_KERNEL_SPECTRUM
   const float s = 0.25f / static_cast<float>(N);
+#if MGB_RCONV_PREFETCH == 2
+  asm volatile("cp.async.wait_all;" ::: "memory");
+#endif
 #pragma unroll
   for (int q = 0; q < KPT; ++q) {
     const int k = threadIdx.x + q * NT;
@@ -389,7 +419,13 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), 1024 / row_threads<LN2,
     const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
     if (self && kb < k) continue;
     const float2 xk = rows[sidx(k)], xo = rows[RS + sidx(kb)];
+#if MGB_RCONV_PREFETCH == 1
     const float2 pk = pkv[q], po = pov[q];
+#elif MGB_RCONV_PREFETCH == 2
+    const float2 pk = sp[sidx(k)], po = sp[RS + sidx(k)];
+#else
+    const float2 pk = __ldg(pa + k), po = __ldg(pb + kb);
+#endif
     const float2 zk = zmix(xk, cconj(xo), pk, cconj(po), s);
     const float2 zo = zmix(xo, cconj(xk), po, cconj(pk), s);
     rows[sidx(k)] = zk;
@@ -561,7 +597,7 @@ void rows_spec_t(const ConvGeom& g, int slots, float2* P, const float2* tw, cuda
 template <int LN2>
 void rows_conv_t(const ConvGeom& g, int items, int batch, float2* X, const float2* P, const float2* tw,
                  cudaStream_t s) {
-  constexpr int smem = 2 * padded(1 << LN2) * 8;
+  constexpr int smem = (MGB_RCONV_PREFETCH == 2 ? 4 : 2) * padded(1 << LN2) * 8;
   static const bool done = [] {
     cudaFuncSetAttribute(rows_conv<LN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return true;
