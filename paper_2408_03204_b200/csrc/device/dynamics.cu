@@ -46,12 +46,12 @@ struct DynBwd {
 // Slot constants, derived by warp 0 of each CTA: lanes 0-3 evaluate the four fp64 powers
 // a^Ne, a^8, a^tile, a^(32 tile) side by side (one pow latency), lane 0 assembles.
 __device__ __forceinline__ void derive_params(const double* row, int env_taps, double floor_, long L, int lane,
-                                              DynParams* out) {
+                                              DynParams* out, long tile = kDynTile) {
   const double a = row[0];
   const int Ne = static_cast<int>(env_taps < L ? env_taps : L);
   const double e = lane == 0 ? static_cast<double>(Ne)
                  : lane == 1 ? static_cast<double>(kDynPerThread)
-                 : lane == 2 ? static_cast<double>(kDynTile) : 32.0 * kDynTile;
+                 : lane == 2 ? static_cast<double>(tile) : 32.0 * static_cast<double>(tile);
   const double pw = lane < 4 ? pow(a, e) : 0.0;
   const double aN = __shfl_sync(0xffffffffu, pw, 0), a16 = __shfl_sync(0xffffffffu, pw, 1);
   const double atile = __shfl_sync(0xffffffffu, pw, 2), atile32 = __shfl_sync(0xffffffffu, pw, 3);
@@ -131,6 +131,65 @@ __device__ __forceinline__ void load16(const StepArgs& a, int e0, int e1, int b,
   }
 }
 
+// Gather-sum of both channels at 4 consecutive samples from n (edge order per sample).
+template <bool VEC>
+__device__ __forceinline__ void load4(const StepArgs& a, int e0, int e1, int b, long n, float* ul, float* ur) {
+  const long boff = static_cast<long>(b) * 2 * a.length;
+  if (VEC && n >= 0 && n + 4 <= a.length) {
+    float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
+    for (int e = e0; e < e1; ++e) {
+      const float* p = a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff + n;
+      l = f4add(l, __ldg(reinterpret_cast<const float4*>(p)));
+      r = f4add(r, __ldg(reinterpret_cast<const float4*>(p + a.length)));
+    }
+    ul[0] = l.x, ul[1] = l.y, ul[2] = l.z, ul[3] = l.w;
+    ur[0] = r.x, ur[1] = r.y, ur[2] = r.z, ur[3] = r.w;
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) ul[k] = ur[k] = 0.f;
+  for (int e = e0; e < e1; ++e) {
+    const float* p = a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (n + k >= 0 && n + k < a.length) {
+        ul[k] += __ldg(p + n + k);
+        ur[k] += __ldg(p + a.length + n + k);
+      }
+    }
+  }
+}
+
+// mid[k] = l + r of the gathered input at n0 + k (each channel summed in edge order first, as
+// load16 does), four samples at a time, so only one float4 pair per channel is live.
+template <bool VEC>
+__device__ __forceinline__ void load_mid(const StepArgs& a, int e0, int e1, int b, long n0, float* mid) {
+#pragma unroll
+  for (int k = 0; k < kDynPerThread; ++k) mid[k] = 0.f;
+  if (n0 >= a.length || n0 < 0) return;
+  const long boff = static_cast<long>(b) * 2 * a.length;
+  if (VEC && n0 + kDynPerThread <= a.length) {
+#pragma unroll
+    for (int q = 0; q < kDynPerThread / 4; ++q) {
+      float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
+      for (int e = e0; e < e1; ++e) {
+        const float* p = a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff + n0;
+        l = f4add(l, __ldg(reinterpret_cast<const float4*>(p) + q));
+        r = f4add(r, __ldg(reinterpret_cast<const float4*>(p + a.length) + q));
+      }
+      mid[4 * q] = l.x + r.x;
+      mid[4 * q + 1] = l.y + r.y;
+      mid[4 * q + 2] = l.z + r.z;
+      mid[4 * q + 3] = l.w + r.w;
+    }
+  } else {
+    float ul[kDynPerThread], ur[kDynPerThread];
+    load16<false>(a, e0, e1, b, n0, ul, ur);
+#pragma unroll
+    for (int k = 0; k < kDynPerThread; ++k) mid[k] = ul[k] + ur[k];
+  }
+}
+
 __device__ __forceinline__ void compose(float& A, float& B, float Ap, float Bp) {
   // earlier (Ap, Bp) then current (A, B)
   B = fmaf(A, Bp, B);
@@ -138,11 +197,13 @@ __device__ __forceinline__ void compose(float& A, float& B, float Ap, float Bp) 
 }
 
 // ENV: also store the envelope g[n] to env[(slot*B + b)*L + n] (backward pass recompute).
-template <bool GATE, bool VEC, bool ENV = false>
-__global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_taps, double floor_, int tiles_per_seq,
+// NT: threads per tile (tile = NT * kDynPerThread samples); 128 for steps with few sequences,
+// so a single long sequence still spreads over the SMs.
+template <bool GATE, bool VEC, bool ENV = false, int NT = kDynThreads>
+__global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a, int env_taps, double floor_, int tiles_per_seq,
                                                          unsigned long long* status, unsigned int* ticket,
                                                          float* env, PwEpi epi) {
-  __shared__ float wA[kDynThreads / 32], wB[kDynThreads / 32];
+  __shared__ float wA[NT / 32], wB[NT / 32];
   __shared__ float s_carry;
   __shared__ int s_ticket;
   __shared__ DynParams s_p;
@@ -155,7 +216,8 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
     if (threadIdx.x == 0) tk = static_cast<int>(atomicAdd(ticket, 1u));
     tk = __shfl_sync(0xffffffffu, tk, 0);
     if (threadIdx.x == 0) s_ticket = tk;
-    derive_params(a.params + 4L * ((tk % nseq) / a.batch), env_taps, floor_, a.length, threadIdx.x, &s_p);
+    derive_params(a.params + 4L * ((tk % nseq) / a.batch), env_taps, floor_, a.length, threadIdx.x, &s_p,
+                  NT * kDynPerThread);
     if (epi.n > 0 && threadIdx.x == 1) pw_epi_slots(epi, (tk % nseq) / a.batch, s_epi);
   }
   __syncthreads();
@@ -163,32 +225,24 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
   const int tile = tk / nseq, seq = tk - tile * nseq;
   const int slot = seq / a.batch, b = seq - slot * a.batch;
   const int e0 = __ldg(a.row_ptr + slot), e1 = __ldg(a.row_ptr + slot + 1);
-  const DynParams p = s_p;
+  const DynParams& p = s_p;  // read from shared memory where used (frees registers)
 
-  const long n0 = static_cast<long>(tile) * kDynTile + static_cast<long>(threadIdx.x) * kDynPerThread;
+  const long n0 = static_cast<long>(tile) * (NT * kDynPerThread) + static_cast<long>(threadIdx.x) * kDynPerThread;
   // drive[k] = (1-a) (e[n] - a^Ne e[n-Ne]) is all the scan keeps in registers; the input
   // samples are gathered again (L2-resident) for the output pass, so nothing else stays live
   // across the carry wait (no spills at 64 registers).
   float drive[kDynPerThread];
   {
-    float ul[kDynPerThread], ur[kDynPerThread], eo[kDynPerThread];
-    load16<VEC>(a, e0, e1, b, n0, ul, ur);
+    float mid[kDynPerThread];
+    load_mid<VEC>(a, e0, e1, b, n0, mid);
     if (p.aN != 0.f) {
-      float ol[kDynPerThread], orr[kDynPerThread];
-      load16<VEC>(a, e0, e1, b, n0 - p.Ne, ol, orr);
+      float mo[kDynPerThread];
+      load_mid<VEC>(a, e0, e1, b, n0 - p.Ne, mo);
 #pragma unroll
-      for (int k = 0; k < kDynPerThread; ++k) {
-        const float m = ol[k] + orr[k];
-        eo[k] = p.aN * (m * m);
-      }
+      for (int k = 0; k < kDynPerThread; ++k) drive[k] = p.oma * (mid[k] * mid[k] - p.aN * (mo[k] * mo[k]));
     } else {
 #pragma unroll
-      for (int k = 0; k < kDynPerThread; ++k) eo[k] = 0.f;
-    }
-#pragma unroll
-    for (int k = 0; k < kDynPerThread; ++k) {
-      const float m = ul[k] + ur[k];
-      drive[k] = p.oma * (m * m - eo[k]);
+      for (int k = 0; k < kDynPerThread; ++k) drive[k] = p.oma * (mid[k] * mid[k] - 0.f);
     }
   }
 
@@ -218,15 +272,15 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
   }
   __syncthreads();
   if (warp == 0) {
-    float tA = lane < kDynThreads / 32 ? wA[lane] : 1.f;
-    float tB = lane < kDynThreads / 32 ? wB[lane] : 0.f;
+    float tA = lane < NT / 32 ? wA[lane] : 1.f;
+    float tB = lane < NT / 32 ? wB[lane] : 0.f;
 #pragma unroll
-    for (int off = 1; off < kDynThreads / 32; off <<= 1) {
+    for (int off = 1; off < NT / 32; off <<= 1) {
       const float Ap = __shfl_up_sync(0xffffffffu, tA, off);
       const float Bp = __shfl_up_sync(0xffffffffu, tB, off);
       if (lane >= off) compose(tA, tB, Ap, Bp);
     }
-    if (lane < kDynThreads / 32) {
+    if (lane < NT / 32) {
       wA[lane] = tA;  // inclusive warp-level prefix
       wB[lane] = tB;
     }
@@ -236,7 +290,7 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
     float pA = wA[warp - 1], pB = wB[warp - 1];
     compose(xA, xB, pA, pB);
   }
-  const float tileB = wB[kDynThreads / 32 - 1];
+  const float tileB = wB[NT / 32 - 1];
 
   if (warp == 0) {
     // Cross-tile carry, deterministic: publish this tile's aggregate B, then
@@ -273,13 +327,14 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
   // Replay the recurrence from this thread's true start state, apply the gain, store.
   float g = fmaf(xA, s_carry, xB);
   if (n0 >= a.length) return;
-  float ul[kDynPerThread], ur[kDynPerThread];
-  load16<VEC>(a, e0, e1, b, n0, ul, ur);
   float* ol = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length + n0;
   float* orr = ol + a.length;
   const bool full = VEC && n0 + kDynPerThread <= a.length;
 #pragma unroll
   for (int q = 0; q < kDynPerThread / 4; ++q) {
+    // inputs gathered again (L2-resident), four samples at a time
+    float ul[4], ur[4];
+    load4<VEC>(a, e0, e1, b, n0 + 4 * q, ul, ur);
     float yl[4], yr[4];
 #pragma unroll
     for (int k4 = 0; k4 < 4; ++k4) {
@@ -289,8 +344,8 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_scan(StepArgs a, int env_t
         if (n0 + k < a.length) env[static_cast<long>(seq) * a.length + n0 + k] = g;
       }
       const float gn = gain_of<GATE>(g, p);
-      yl[k4] = gn * ul[k];
-      yr[k4] = gn * ur[k];
+      yl[k4] = gn * ul[k4];
+      yr[k4] = gn * ur[k4];
     }
     if (full) {
       reinterpret_cast<float4*>(ol)[q] = make_float4(yl[0], yl[1], yl[2], yl[3]);
@@ -387,7 +442,7 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_bwd_dg(DynBwd d) {
   const int slot = seq / d.fw.batch, b = seq - slot * d.fw.batch;
   if (threadIdx.x < 32) derive_params(d.fw.params + 4L * slot, d.env_taps, d.floor_, d.fw.length, threadIdx.x, &s_p);
   __syncthreads();
-  const DynParams p = s_p;
+  const DynParams& p = s_p;  // read from shared memory where used (frees registers)
   const long L = d.fw.length;
   const long n0 = static_cast<long>(tile) * kDynTile + static_cast<long>(threadIdx.x) * kDynPerThread;
   constexpr int K = kDynPerThread;
@@ -463,7 +518,7 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_bwd(DynBwd d) {
   if (threadIdx.x < 32) derive_params(d.fw.params + 4L * slot, d.env_taps, d.floor_, d.fw.length, threadIdx.x, &s_p);
   if (PASS == 1 && threadIdx.x == 0) s_carry = d.carry[static_cast<long>(seq) * d.tiles + tile];
   __syncthreads();
-  const DynParams p = s_p;
+  const DynParams& p = s_p;  // read from shared memory where used (frees registers)
   const long L = d.fw.length;
   const long n0 = static_cast<long>(tile) * kDynTile + static_cast<long>(threadIdx.x) * kDynPerThread;
   constexpr int K = kDynPerThread;
@@ -675,29 +730,46 @@ void launch_dynamics_backward(bool gate, const StepArgs& fw, const StepArgs& bw,
   dyn_bwd_reduce<<<fw.slots, 32, 0, s>>>(d, grad);
 }
 
+constexpr int kDynSmallThreads = 128;
+constexpr int kDynSmallTile = kDynSmallThreads * kDynPerThread;
+
 std::size_t dyn_sync_bytes(int slots, int batch, long length) {
-  const long tiles = (length + kDynTile - 1) / kDynTile;
+  const long tiles = (length + kDynSmallTile - 1) / kDynSmallTile;  // the finer of the two tilings
   return 256 + sizeof(unsigned long long) * static_cast<std::size_t>(slots) * batch * tiles;
 }
 
 void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double energy_floor, void* ws,
                      bool zero_sync, cudaStream_t s, const PwEpi& epi) {
   if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
-  const int tiles = static_cast<int>((a.length + kDynTile - 1) / kDynTile);
-  const long total = static_cast<long>(a.slots) * a.batch * tiles;
+  const long seqs = static_cast<long>(a.slots) * a.batch;
+  // Few sequences (a bus compressor): 1024-sample tiles of 128 threads, so the step still
+  // spreads over the SMs; otherwise 4096-sample tiles of 512 threads.
+  const bool small = seqs * ((a.length + kDynTile - 1) / kDynTile) < 148;
+  const long tile = small ? kDynSmallTile : kDynTile;
+  const int tiles = static_cast<int>((a.length + tile - 1) / tile);
+  const long total = seqs * tiles;
   if (zero_sync) cudaMemsetAsync(ws, 0, dyn_sync_bytes(a.slots, a.batch, a.length), s);
   auto* ticket = static_cast<unsigned int*>(ws);
   auto* status = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 256);
   const long ne = envelope_taps < a.length ? envelope_taps : a.length;
   const bool vec = (a.length % 4 == 0) && (ne % 4 == 0);
   const dim3 grid(static_cast<unsigned>(total));
-  if (gate) {
-    if (vec) dyn_scan<true, true><<<grid, kDynThreads, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, ticket, nullptr, epi);
-    else dyn_scan<true, false><<<grid, kDynThreads, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, ticket, nullptr, epi);
+#define MGB_DYN_LAUNCH(G, V, T) \
+  dyn_scan<G, V, false, T><<<grid, T, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, ticket, nullptr, epi)
+  if (small) {
+    if (gate) {
+      if (vec) MGB_DYN_LAUNCH(true, true, kDynSmallThreads); else MGB_DYN_LAUNCH(true, false, kDynSmallThreads);
+    } else {
+      if (vec) MGB_DYN_LAUNCH(false, true, kDynSmallThreads); else MGB_DYN_LAUNCH(false, false, kDynSmallThreads);
+    }
   } else {
-    if (vec) dyn_scan<false, true><<<grid, kDynThreads, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, ticket, nullptr, epi);
-    else dyn_scan<false, false><<<grid, kDynThreads, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, ticket, nullptr, epi);
+    if (gate) {
+      if (vec) MGB_DYN_LAUNCH(true, true, kDynThreads); else MGB_DYN_LAUNCH(true, false, kDynThreads);
+    } else {
+      if (vec) MGB_DYN_LAUNCH(false, true, kDynThreads); else MGB_DYN_LAUNCH(false, false, kDynThreads);
+    }
   }
+#undef MGB_DYN_LAUNCH
 }
 
 }  // namespace mgb
