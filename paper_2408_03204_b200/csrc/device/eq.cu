@@ -29,10 +29,12 @@ constexpr int kEqOut = 6144;  // outputs per block (of the 8192 - 2046 = 6146 no
 constexpr int kEqSmem = kEqBuf * 8;
 
 // Taps by the exact cosine sum raw[j] = (m0 + 2 sum_{k=1}^{1023} m_k cos(2 pi k j / 2047)) / 2047
-// in fp64. One warp per tap j; each lane runs a 32-term Chebyshev recurrence started from
-// the fp64 cos table (error ~1e-12); lanes are reduced with xor-shuffles in a fixed order.
-// grid (1024 / 8, slots) x 256 threads (8 taps per CTA).
+// in fp64. One warp per kDesignTpw taps j (independent recurrences interleaved for ILP);
+// each lane runs 32-term Chebyshev recurrences started from the fp64 cos table (error
+// ~1e-12); lanes are reduced with xor-shuffles in a fixed order.
+// grid (1024 / (8 kDesignTpw), slots) x 256 threads (8 kDesignTpw taps per CTA).
 constexpr int kDesignSplit = 32;
+constexpr int kDesignTpw = 4;  // taps per warp
 // exp of the 1024 log-magnitudes of every slot, once (fp64). grid (slots) x 1024.
 __global__ void __launch_bounds__(1024) eq_mags(const double* params, double* mags) {
   const long i = static_cast<long>(blockIdx.x) * (kEqHalf + 1) + threadIdx.x;
@@ -48,22 +50,39 @@ __global__ void __launch_bounds__(256) eq_design(const double* __restrict__ mag_
   // magnitudes (no bank conflicts); the stride-32 recurrence is
   // cos((k + 32) t) = 2 cos(32 t) cos(k t) - cos((k - 32) t).
   const int lane = threadIdx.x & 31;
-  const int j = blockIdx.x * (256 / kDesignSplit) + threadIdx.x / kDesignSplit;  // 0..1023
-  double c_prev = __ldg(cos_tab + (static_cast<long>(31 - lane) * j) % kN);  // cos((1 + l - 32) t)
-  double c_cur = __ldg(cos_tab + (static_cast<long>(1 + lane) * j) % kN);
-  const double two_c = 2.0 * __ldg(cos_tab + (32L * j) % kN);
-  double acc = 0.0;
-#pragma unroll 4
+  const int j0 = (blockIdx.x * (256 / kDesignSplit) + threadIdx.x / kDesignSplit) * kDesignTpw;  // first tap
+  double c_prev[kDesignTpw], c_cur[kDesignTpw], two_c[kDesignTpw], acc[kDesignTpw];
+#pragma unroll
+  for (int q = 0; q < kDesignTpw; ++q) {
+    const long j = j0 + q;
+    c_prev[q] = __ldg(cos_tab + (static_cast<long>(31 - lane) * j) % kN);  // cos((1 + l - 32) t)
+    c_cur[q] = __ldg(cos_tab + (static_cast<long>(1 + lane) * j) % kN);
+    two_c[q] = 2.0 * __ldg(cos_tab + (32L * j) % kN);
+    acc[q] = 0.0;
+  }
+#pragma unroll 2
   for (int k = 1 + lane; k <= kEqHalf; k += 32) {
-    acc = fma(mags[k], c_cur, acc);
-    const double nxt = fma(two_c, c_cur, -c_prev);
-    c_prev = c_cur;
-    c_cur = nxt;
+    const double m = mags[k];
+#pragma unroll
+    for (int q = 0; q < kDesignTpw; ++q) {
+      acc[q] = fma(m, c_cur[q], acc[q]);
+      const double nxt = fma(two_c[q], c_cur[q], -c_prev[q]);
+      c_prev[q] = c_cur[q];
+      c_cur[q] = nxt;
+    }
   }
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane != 0) return;
-  const double raw = (mags[0] + 2.0 * acc) / kN;
+  for (int q = 0; q < kDesignTpw; ++q) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+  }
+  if (lane >= kDesignTpw) return;
+  // lane q writes tap j0 + q
+  double a = acc[0];
+#pragma unroll
+  for (int q = 1; q < kDesignTpw; ++q) a = lane == q ? acc[q] : a;
+  const int j = j0 + lane;
+  const double raw = (mags[0] + 2.0 * a) / kN;
   double s, c;
   sincospi(2.0 * (kEqHalf + j) / (kN - 1), &s, &c);
   const double w = 0.5 - 0.5 * c;  // symmetric Hann; w(half - j) == w(half + j)
@@ -233,7 +252,7 @@ void launch_eq_prologue(const StepArgs& a, float* taps_ws, float* resp_ws, cudaS
   note_prologue_kernel(reinterpret_cast<const void*>(eq_design));
   note_prologue_kernel(reinterpret_cast<const void*>(eq_response));
   eq_mags<<<a.slots, kEqHalf + 1, 0, s>>>(a.params, mags);
-  eq_design<<<dim3(1024 / (256 / kDesignSplit), a.slots), 256, 0, s>>>(mags, taps_ws, cos_table(a.tw));
+  eq_design<<<dim3(1024 / (256 / kDesignSplit * kDesignTpw), a.slots), 256, 0, s>>>(mags, taps_ws, cos_table(a.tw));
   eq_response<<<a.slots, 512, kEqSmem, s>>>(taps_ws, resp_ws, a.tw);
 }
 
