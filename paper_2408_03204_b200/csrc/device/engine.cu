@@ -578,6 +578,7 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
     a.batch = batch;
     a.length = length;
     a.rowstride = rowstride;
+    a.nnz = static_cast<int>(st.gather.size());
   }
   for (int r : plan.zero_rows()) {
     cuda_check(cudaMemsetAsync(arena + r * rowstride, 0, sizeof(float) * rowstride, stream), "memset");
@@ -800,6 +801,7 @@ void profile_steps(const DevicePlan& plan, const ProcessorSet& procs, const doub
     a.batch = batch;
     a.length = length;
     a.rowstride = rowstride;
+    a.nnz = static_cast<int>(st.gather.size());
     run_prologue(st.type, a, procs, ws + lay.prologue_off[k], stream);
     cuda_check(cudaEventRecord(e0, stream), "event");
     for (int r = 0; r < reps; ++r) {

@@ -104,6 +104,67 @@ __global__ void __launch_bounds__(kPwThreads) pointwise_vec4_epi(StepArgs a, PwE
   pointwise_vec4_body<OP, true>(a, epi);
 }
 
+// Aggregation-heavy steps with few output rows (the console's master mix: 35 inputs, one
+// row): the per-row grid of pointwise_vec4 leaves most SMs idle and each thread walks all
+// the edges. Here kWideGroups thread groups each sum a contiguous quarter of the edges (in
+// edge order) for the same 64 float4 positions, and the partial sums are added in group
+// order: ((q0 + q1) + q2) + q3, deterministic. grid (ceil(n4 / 64), slots*B) x 256.
+constexpr int kWideGroups = 4, kWidePos = 64;
+template <PointOp OP>
+__global__ void __launch_bounds__(kWideGroups * kWidePos) pointwise_wide(StepArgs a) {
+  __shared__ float4 pl[kWideGroups][kWidePos], pr[kWideGroups][kWidePos];
+  const int sb = blockIdx.y;
+  const int slot = sb / a.batch, b = sb - slot * a.batch;
+  const long n4 = a.length >> 2;
+  const int g = threadIdx.x / kWidePos, p = threadIdx.x - g * kWidePos;
+  const long i = blockIdx.x * static_cast<long>(kWidePos) + p;
+  const int e0 = __ldg(a.row_ptr + slot), e1 = __ldg(a.row_ptr + slot + 1);
+  const int per = (e1 - e0 + kWideGroups - 1) / kWideGroups;
+  const int ga = e0 + g * per, gb = min(e1, ga + per);
+  const long boff = static_cast<long>(b) * 2 * a.length;
+  float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
+  if (i < n4) {
+    int e = ga;
+    for (; e + 7 < gb; e += 8) {
+      float4 lv[8], rv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float4* q = reinterpret_cast<const float4*>(a.src + static_cast<long>(__ldg(a.col + e + u)) * a.rowstride + boff);
+        lv[u] = __ldg(q + i);
+        rv[u] = __ldg(q + n4 + i);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        l = f4add(l, lv[u]);
+        r = f4add(r, rv[u]);
+      }
+    }
+    for (; e < gb; ++e) {
+      const float4* q = reinterpret_cast<const float4*>(a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff);
+      l = f4add(l, __ldg(q + i));
+      r = f4add(r, __ldg(q + n4 + i));
+    }
+  }
+  pl[g][p] = l;
+  pr[g][p] = r;
+  __syncthreads();
+  if (g != 0 || i >= n4) return;
+#pragma unroll
+  for (int h = 1; h < kWideGroups; ++h) {
+    l = f4add(l, pl[h][p]);
+    r = f4add(r, pr[h][p]);
+  }
+  float g0, g1;
+  coeffs<OP>(a, slot, g0, g1);
+  apply<OP>(l.x, r.x, g0, g1);
+  apply<OP>(l.y, r.y, g0, g1);
+  apply<OP>(l.z, r.z, g0, g1);
+  apply<OP>(l.w, r.w, g0, g1);
+  float* __restrict__ out = a.dst + static_cast<long>(slot) * a.rowstride + boff;
+  reinterpret_cast<float4*>(out)[i] = l;
+  reinterpret_cast<float4*>(out + a.length)[i] = r;
+}
+
 template <PointOp OP>
 __global__ void __launch_bounds__(256) pointwise_scalar(StepArgs a) {
   const int sb = blockIdx.y;
@@ -127,6 +188,13 @@ void launch_op(const StepArgs& a, cudaStream_t s, const PwEpi& epi) {
   const bool vec = (a.length % 4) == 0;
   if (vec) {
     const dim3 grid(static_cast<unsigned>((a.length / 4 + kPwThreads - 1) / kPwThreads), static_cast<unsigned>(rows));
+    // Few rows gathering many inputs: edge-split groups (pointwise_wide), when the plain grid
+    // would be under two waves of the SMs and the rows average 8+ inputs.
+    if (epi.n == 0 && static_cast<long>(grid.x) * grid.y < 2L * 148 && a.nnz >= 8 * a.slots) {
+      const dim3 wgrid(static_cast<unsigned>((a.length / 4 + kWidePos - 1) / kWidePos), static_cast<unsigned>(rows));
+      pointwise_wide<OP><<<wgrid, kWideGroups * kWidePos, 0, s>>>(a);
+      return;
+    }
     if (epi.n > 0) {
       pointwise_vec4_epi<OP><<<grid, kPwThreads, 0, s>>>(a, epi);
     } else {

@@ -25,6 +25,7 @@ struct StepArgs {
   int batch;
   long length;           // L
   long rowstride;        // B*2*L
+  int nnz = 0;           // edges of the step (host hint for launch shapes; 0 = unknown)
 };
 
 __device__ __forceinline__ const float* chan_ptr(const float* base, long row, long rowstride, int b, int c, long L) {
