@@ -180,7 +180,8 @@ int32_t mg_batch_last_arena(const mg_batch* b, void** arena);
 void mg_batch_destroy(mg_batch* b);
 
 /* Per-step device time (ms; prologue + audio pass of step k) averaged over `reps`
- * back-to-back repetitions between one event pair, after one full render. Synchronous. */
+ * back-to-back repetitions replayed as one CUDA graph between one event pair, after one full
+ * render. Synchronous. */
 int32_t mg_profile_steps(const mg_plan* plan, const mg_processors* procs, const double* const* d_tables,
                          float* d_arena, int32_t batch, int64_t length, void* d_workspace, uint64_t workspace_bytes,
                          void* stream, int32_t reps, float* step_ms);

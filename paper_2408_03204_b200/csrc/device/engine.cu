@@ -787,6 +787,9 @@ void profile_steps(const DevicePlan& plan, const ProcessorSet& procs, const doub
   cudaEvent_t e0, e1;
   cuda_check(cudaEventCreate(&e0), "event");
   cuda_check(cudaEventCreate(&e1), "event");
+  cudaStream_t cap = nullptr;
+  cuda_check(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaStreamSynchronize(stream), "sync");
   for (std::size_t k = 0; k < rd.steps.size(); ++k) {
     const StepIndex& st = rd.steps[k];
     const int width = param_width(st.type);
@@ -803,19 +806,32 @@ void profile_steps(const DevicePlan& plan, const ProcessorSet& procs, const doub
     a.rowstride = rowstride;
     a.nnz = static_cast<int>(st.gather.size());
     run_prologue(st.type, a, procs, ws + lay.prologue_off[k], stream);
-    cuda_check(cudaEventRecord(e0, stream), "event");
+    // The reps are captured into a CUDA graph and replayed, so short kernels are timed on
+    // the device without the host's per-launch cost between them.
+    cuda_check(cudaStreamSynchronize(stream), "sync");
+    cuda_check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "capture");
     for (int r = 0; r < reps; ++r) {
-      run_prologue(st.type, a, procs, ws + lay.prologue_off[k], stream);
-      run_main(st.type, a, procs, ws + lay.prologue_off[k], ws + lay.main_off, ws + lay.sync_off[k], true, stream);
+      run_prologue(st.type, a, procs, ws + lay.prologue_off[k], cap);
+      run_main(st.type, a, procs, ws + lay.prologue_off[k], ws + lay.main_off, ws + lay.sync_off[k], true, cap);
     }
-    cuda_check(cudaEventRecord(e1, stream), "event");
+    cudaGraph_t g = nullptr;
+    cuda_check(cudaStreamEndCapture(cap, &g), "capture");
+    cudaGraphExec_t ge = nullptr;
+    cuda_check(cudaGraphInstantiate(&ge, g, 0), "instantiate");
+    cuda_check(cudaGraphLaunch(ge, cap), "graph launch");  // warm
+    cuda_check(cudaEventRecord(e0, cap), "event");
+    cuda_check(cudaGraphLaunch(ge, cap), "graph launch");
+    cuda_check(cudaEventRecord(e1, cap), "event");
     cuda_check(cudaEventSynchronize(e1), "sync");
     float ms = 0.f;
     cuda_check(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
     step_ms[k] = ms / static_cast<float>(reps);
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  cudaStreamDestroy(cap);
 }
 
 // ---- RenderGraph ------------------------------------------------------------------------

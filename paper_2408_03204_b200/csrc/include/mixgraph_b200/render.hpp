@@ -183,7 +183,8 @@ void backward_arena(const DevicePlan& plan, const ProcessorSet& processors, cons
                     void* workspace, std::size_t workspace_bytes, cudaStream_t stream);
 
 // Per-step device time (prologue + audio pass of step k, ms) from `reps` back-to-back
-// repetitions between one CUDA event pair on `stream` (after one full render). Diagnostic.
+// repetitions captured as one CUDA graph and timed between one event pair (after one full
+// render on `stream`; no host launch cost between repetitions). Diagnostic.
 void profile_steps(const DevicePlan& plan, const ProcessorSet& processors, const double* const* param_tables,
                    float* arena, int batch, long length, void* workspace, std::size_t workspace_bytes,
                    cudaStream_t stream, int reps, float* step_ms);
