@@ -159,6 +159,7 @@ ProcessorSet::ProcessorSet(const ProcessorConfig& config) : config_(config) {
   dev_ = std::make_unique<DeviceConstants>();
   cuda_check(cudaGetDevice(&dev_->device), "cudaGetDevice");
   mgb::twiddle_table(dev_->device);
+  mgb::eq_basis(dev_->device);
   dev_->frames = static_cast<int>((reverb_length_ + kReverbStftHop - 1) / kReverbStftHop);
   const std::size_t stft_bytes = sizeof(float2) * static_cast<std::size_t>(dev_->frames) * (kReverbStftLength / 2 + 1);
   cuda_check(cudaMalloc(&dev_->stft_mid, stft_bytes > 0 ? stft_bytes : 8), "cudaMalloc");
@@ -315,7 +316,11 @@ int epi_followers(const DevicePlan& plan, std::size_t k, int batch, long length)
 // before its prologue has finished (render_arena); a larger grid keeps the GPU busy anyway and
 // the round trip of the window spectra through memory would only cost bandwidth.
 bool split_first_eq(const RenderData& rd, int batch, long length) {
-  if (rd.steps.empty() || rd.steps[0].type != NodeType::Eq) return false;
+  // Off by default since the EQ response became one basis product (a few us): the split's
+  // spectrum round trip then costs more than it hides (0.271 -> 0.261 ms per config-2
+  // render). MGB_EQ_SPLIT=1 restores it.
+  static const bool off = [] { const char* v = std::getenv("MGB_EQ_SPLIT"); return !(v && v[0] == '1'); }();
+  if (off || rd.steps.empty() || rd.steps[0].type != NodeType::Eq) return false;
   const long blocks = (length + 6143) / 6144;
   const long grid = blocks * (rd.steps[0].store_end - rd.steps[0].store_begin) * batch;
   return grid <= 2L * 2 * 148;
@@ -593,13 +598,21 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
   // enqueued, so its grid reaches the GPU ahead of the side stream's grids.
   const bool split_first = hoist && split_first_eq(rd, batch, length);
   const cudaEvent_t* ev = plan.events();
+  // MGB_FIRST_PROLOGUE_MAIN=1: an unsplit first-step EQ runs its prologue on the main stream
+  // and the side streams fork after it, so its audio pass reaches the SMs before them.
+  static const bool first_main = [] { const char* v = std::getenv("MGB_FIRST_PROLOGUE_MAIN"); return v && v[0] == '1'; }();
+  const bool first_on_main = hoist && first_main && !split_first && !rd.steps.empty() && rd.steps[0].type == NodeType::Eq;
   if (hoist) {
+    if (first_on_main) {
+      run_prologue(rd.steps[0].type, args[0], procs, ws + lay.prologue_off[0], stream);
+      cuda_check(cudaEventRecord(ev[1], stream), "event");
+    }
     cuda_check(cudaEventRecord(ev[0], stream), "event");  // fork point: before any render work
     if (split_first) mgb::launch_eq_forward(args[0], reinterpret_cast<float2*>(ws + lay.main_off), stream);
     for (cudaStream_t a : plan.aux_streams()) cuda_check(cudaStreamWaitEvent(a, ev[0], 0), "wait");
     int next = 0;  // independent prologues round-robin over the side streams
     for (std::size_t k = 0; k < rd.steps.size(); ++k) {
-      if (!has_prologue(rd.steps[k].type)) continue;
+      if (!has_prologue(rd.steps[k].type) || (k == 0 && first_on_main)) continue;
       // Prologues complete in the order their steps need them on side stream 0, except the
       // delay's, which gets side stream 1 and so runs beside the reverb's (the delay step's
       // kernel spectrum was the critical path once conv steps joined their prologue late:

@@ -14,6 +14,12 @@
 //     gather-sum the block's 8192-sample window (both channels packed as re/im, since the
 //     kernel is real and shared), FFT, multiply by R, inverse FFT, store the 6146 samples
 //     that did not wrap. Arena in -> arena out in one kernel.
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <vector>
+
 #include "fft_smem.cuh"
 #include "launch.hpp"
 
@@ -105,6 +111,169 @@ __global__ void __launch_bounds__(512) eq_response(const float* taps, float* res
   fft_pow2<kLogFft, 1, 512, -1>(buf, kEqBuf, tw);
   float* r = resp + static_cast<long>(slot) * kEqFft;
   for (int i = threadIdx.x; i < kEqFft; i += blockDim.x) r[i] = buf[sidx(i)].x * (1.f / kEqFft);
+}
+
+// ---- response as a product with a fixed basis ---------------------------------------------
+// The 8192-bin response is LINEAR in the magnitudes m_q = exp(lm_q): R = A m with
+// A[k][q] = the response of eq_design/eq_response to the unit spectrum e_q (the cosine sum,
+// the symmetric Hann and the 8192-point DFT are all linear). The basis A^T [1024][kBasisK] is
+// built once per device by running exactly those two kernels on the 1024 unit spectra
+// (eq_basis), so every render's prologue is one small fp32 product (eq_response_basis)
+// instead of the fp64 design + one serial 8192-point FFT per slot. R is real and even:
+// bins k <= 4096 are computed and mirrored.
+constexpr int kBasisTileK = 32;                                          // bins per CTA (one per lane)
+constexpr int kBasisK = ((kEqFft / 2 + 1 + kBasisTileK - 1) / kBasisTileK) * kBasisTileK;  // 4128
+constexpr int kBasisSlots = 16;                                          // slots per CTA
+constexpr int kBasisWarps = 16;                                          // q split over warps
+constexpr int kBasisQ = (kEqHalf + 1) / kBasisWarps;                     // 64 q per warp
+constexpr int kBasisTileBytes = (kEqHalf + 1) * kBasisTileK * 4;         // 128 KiB column block
+constexpr int kBasisMBytes = (kEqHalf + 1) * kBasisSlots * 4;            // magnitude tile, 64 KiB
+constexpr int kBasisSmem = kBasisTileBytes + kBasisMBytes;
+constexpr int kBasisMinSlots = 4;  // fewer slots: the 16.9 MB basis read costs more than the FFT design
+
+// m[group][q][16 slots] = exp(lm) in fp32 (0 past the last slot): the basis kernel's
+// magnitude tiles, built once per step instead of once per basis CTA (129 CTAs each
+// re-reading 128 KiB of fp64 parameters was half of that kernel's L2 traffic and its
+// latency chain). grid (ceil(slots / 16), 8) x 128: thread q writes one 64-byte row.
+__global__ void __launch_bounds__(128) eq_mag_tiles(const double* __restrict__ params, int slots, float4* mt) {
+  const int q = blockIdx.y * 128 + threadIdx.x, s0 = blockIdx.x * kBasisSlots;
+  float v[kBasisSlots];
+#pragma unroll
+  for (int s = 0; s < kBasisSlots; ++s) {
+    v[s] = s0 + s < slots ? expf(static_cast<float>(__ldg(params + static_cast<long>(s0 + s) * (kEqHalf + 1) + q))) : 0.f;
+  }
+  float4* row = mt + (static_cast<long>(blockIdx.x) * (kEqHalf + 1) + q) * (kBasisSlots / 4);
+#pragma unroll
+  for (int g = 0; g < kBasisSlots / 4; ++g) row[g] = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+}
+
+// d = a * b + c on a pair of fp32 lanes (one FFMA2 instruction on sm_100).
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// grid (kBasisK / 32, ceil(slots / 16)) x 512. The basis is stored tiled, [kBasisK / 32][1024 q]
+// [32 bins], so a CTA's column block is one contiguous 128 KiB run, copied into smem with the
+// slot group's magnitude tile (eq_mag_tiles). Lane l of warp w then sums bin k0 + l over q in
+// [64 w, 64 w + 64) for 16 slots (conflict-free basis reads, broadcast float4 magnitude reads,
+// slot pairs in FFMA2); the 16 warp partials are added in warp order.
+__global__ void __launch_bounds__(512, 1) eq_response_basis(const float4* __restrict__ mtiles, int slots,
+                                                            const float* __restrict__ basis, float* resp) {
+  extern __shared__ __align__(128) unsigned char bsm[];
+  float* tile = reinterpret_cast<float*>(bsm);                                    // [1024][32]
+  float4* msm = reinterpret_cast<float4*>(bsm + kBasisTileBytes);                 // [1024][4] float4
+  const int s0 = blockIdx.y * kBasisSlots;
+  const int ns = min(kBasisSlots, slots - s0);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // Basis column block and magnitude tile into smem with cp.async (LDGSTS): every thread has
+  // its 24 16-byte copies in flight at once. (A TMA bulk copy per quarter measured ~24 GB/s
+  // per SM here, a quarter of the HBM share: 10.5 us for this kernel instead of ~5.)
+  {
+    const char* src = reinterpret_cast<const char*>(basis) + static_cast<long>(blockIdx.x) * kBasisTileBytes;
+    const char* msrc = reinterpret_cast<const char*>(mtiles + static_cast<long>(blockIdx.y) * (kEqHalf + 1) * (kBasisSlots / 4));
+#pragma unroll
+    for (int i = 0; i < kBasisTileBytes / (16 * 512); ++i) {
+      const int off = (i * 512 + threadIdx.x) * 16;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(bsm + off)), "l"(src + off) : "memory");
+    }
+#pragma unroll
+    for (int i = 0; i < kBasisMBytes / (16 * 512); ++i) {
+      const int off = (i * 512 + threadIdx.x) * 16;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(bsm + kBasisTileBytes + off)), "l"(msrc + off)
+                   : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+  __syncthreads();
+  float2 acc2[kBasisSlots / 2];                         // slot pairs: one FFMA2 per pair
+#pragma unroll
+  for (int s = 0; s < kBasisSlots / 2; ++s) acc2[s] = make_float2(0.f, 0.f);
+#pragma unroll 8
+  for (int u = 0; u < kBasisQ; ++u) {
+    const int q = w * kBasisQ + u;
+    const float a = tile[q * kBasisTileK + lane];
+    const float2 aa = make_float2(a, a);
+    const float4* mq = msm + q * (kBasisSlots / 4);
+#pragma unroll
+    for (int g = 0; g < kBasisSlots / 4; ++g) {
+      const float4 m = mq[g];
+      acc2[2 * g + 0] = ffma2(aa, make_float2(m.x, m.y), acc2[2 * g + 0]);
+      acc2[2 * g + 1] = ffma2(aa, make_float2(m.z, m.w), acc2[2 * g + 1]);
+    }
+  }
+  float acc[kBasisSlots];
+#pragma unroll
+  for (int s = 0; s < kBasisSlots / 2; ++s) {
+    acc[2 * s] = acc2[s].x;
+    acc[2 * s + 1] = acc2[s].y;
+  }
+  __syncthreads();                                      // tile no longer read: reuse as partials
+  float* part = tile;                                   // [16 warps][16 slots][32 lanes]
+#pragma unroll
+  for (int s = 0; s < kBasisSlots; ++s) part[(w * kBasisSlots + s) * 32 + lane] = acc[s];
+  __syncthreads();
+  {
+    const int i = threadIdx.x;                          // 512 = 16 slots x 32 bins
+    const int s = i >> 5, l = i & 31;
+    float v = part[s * 32 + l];
+#pragma unroll
+    for (int ww = 1; ww < kBasisWarps; ++ww) v += part[(ww * kBasisSlots + s) * 32 + l];
+    const int kk = blockIdx.x * kBasisTileK + l;
+    if (s < ns && kk <= kEqFft / 2) {
+      float* r = resp + static_cast<long>(s0 + s) * kEqFft;
+      r[kk] = v;
+      if (kk > 0 && kk < kEqFft / 2) r[kEqFft - kk] = v;
+    }
+  }
+}
+
+// Basis entries in closed form (fp64). With c = 1023, theta_q = 2 pi q / 2047 and
+// phi_k = 2 pi k / 8192, the design of the unit spectrum e_q (dsp.cpp:106-136) is
+// h_q[j] = w_j c_q cos(j theta_q) / 2047 (c_0 = 1, else 2; symmetric Hann w_j =
+// 0.5 + 0.5 cos(pi j / 1023)), and its 8192-point response is
+// R_q[k] = c_q / (2 * 2047) [F(theta_q + phi_k) + F(theta_q - phi_k)] with the window
+// transform F(x) = sum_j w_j e^{ijx} = D(x)/2 + D(x + pi/1023)/4 + D(x - pi/1023)/4 and the
+// Dirichlet kernel D(x) = sin(2047 x / 2) / sin(x / 2). Every angle is 2 pi n / d with exact
+// integers n, d, reduced before sinpi, so each entry is correct to a few fp64 ulps.
+__device__ double eq_dirichlet(long long n, long long d) {  // D(2 pi n / d)
+  n %= d;
+  if (2 * n > d) n -= d;
+  if (2 * n <= -d) n += d;
+  if (n == 0) return 2047.0;
+  long long m = (2047LL * n) % (2 * d);                      // sin(2047 pi n / d): reduce mod 2d
+  if (m > d) m -= 2 * d;
+  if (m <= -d) m += 2 * d;
+  return sinpi(static_cast<double>(m) / static_cast<double>(d)) / sinpi(static_cast<double>(n) / static_cast<double>(d));
+}
+__device__ double eq_window_transform(long long n, long long d) {  // F(2 pi n / d), d a multiple of 2046
+  const long long s = d / 2046;                                   // pi / 1023 = 2 pi s / d
+  return 0.5 * eq_dirichlet(n, d) + 0.25 * eq_dirichlet(n + s, d) + 0.25 * eq_dirichlet(n - s, d);
+}
+// tiled[(k / 32) * 1024 + q][k % 32] = R_q[k] / 8192 (the response prescale), 0 for k > 4096.
+__global__ void eq_basis_build(float* tiled) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<long>(kBasisK) * (kEqHalf + 1)) return;
+  const int kl = static_cast<int>(i % kBasisTileK);
+  const int q = static_cast<int>((i / kBasisTileK) % (kEqHalf + 1));
+  const int k = static_cast<int>(i / (static_cast<long>(kBasisTileK) * (kEqHalf + 1))) * kBasisTileK + kl;
+  double v = 0.0;
+  if (k <= kEqFft / 2) {
+    constexpr long long d = 2047LL * 8192LL * 2046LL;             // common denominator
+    const long long nq = static_cast<long long>(q) * 8192LL * 2046LL, nk = static_cast<long long>(k) * 2047LL * 2046LL;
+    const double cq = q == 0 ? 1.0 : 2.0;
+    v = cq / (2.0 * 2047.0 * 8192.0) * (eq_window_transform(nq + nk, d) + eq_window_transform(nq - nk, d));
+  }
+  tiled[i] = static_cast<float>(v);
 }
 
 // Window geometry per FFT size: 8192 (6144 outputs per block, the throughput choice) or
@@ -234,6 +403,7 @@ __global__ void __launch_bounds__(EqWin<LOG>::kThreads, EqWin<LOG>::kMinBlocks) 
 void eq_setup() {
   static const bool done = [] {
     cudaFuncSetAttribute(eq_response, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqSmem);
+    cudaFuncSetAttribute(eq_response_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, kBasisSmem);
     for (auto fn : {eq_conv<0, 13>, eq_conv<1, 13>, eq_conv<2, 13>, eq_conv<0, 12>}) {
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqSmem);
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -243,9 +413,50 @@ void eq_setup() {
   (void)done;
 }
 
+// Per-device basis A^T [1024][kBasisK] (see eq_response_basis), built synchronously on first
+// use (ProcessorSet's constructor calls it, before any stream capture).
+const float* eq_basis(int device) {
+  static std::mutex mu;
+  static std::map<int, float*> bases;
+  std::scoped_lock lock(mu);
+  auto it = bases.find(device);
+  if (it != bases.end()) return it->second;
+  eq_setup();
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  float* basis = nullptr;
+  const long n = static_cast<long>(kBasisK) * (kEqHalf + 1);
+  bool ok = cudaMalloc(&basis, sizeof(float) * n) == cudaSuccess;
+  if (ok) {
+    eq_basis_build<<<static_cast<unsigned>((n + 255) / 256), 256>>>(basis);
+    ok = cudaDeviceSynchronize() == cudaSuccess;
+  }
+  cudaSetDevice(prev);
+  if (!ok) {
+    cudaFree(basis);
+    throw std::runtime_error("EQ response basis build failed");
+  }
+  bases.emplace(device, basis);
+  return basis;
+}
+
 void launch_eq_prologue(const StepArgs& a, float* taps_ws, float* resp_ws, cudaStream_t s) {
   if (a.slots == 0) return;
   eq_setup();
+  // MGB_EQ_FFT_DESIGN=1: the per-render fp64 design + 8192-point FFT (diagnostics / A-B).
+  static const bool fft_design = [] { const char* v = std::getenv("MGB_EQ_FFT_DESIGN"); return v && v[0] == '1'; }();
+  if (!fft_design && a.slots >= kBasisMinSlots) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    note_prologue_kernel(reinterpret_cast<const void*>(eq_mag_tiles));
+    note_prologue_kernel(reinterpret_cast<const void*>(eq_response_basis));
+    const int groups = (a.slots + kBasisSlots - 1) / kBasisSlots;
+    auto* mt = reinterpret_cast<float4*>(taps_ws);  // the taps region is unused on this path
+    eq_mag_tiles<<<dim3(groups, (kEqHalf + 1) / 128), 128, 0, s>>>(a.params, a.slots, mt);
+    eq_response_basis<<<dim3(kBasisK / kBasisTileK, groups), 512, kBasisSmem, s>>>(mt, a.slots, eq_basis(dev), resp_ws);
+    return;
+  }
   // taps_ws holds [slots][2048] floats followed by [slots][1024] doubles of magnitudes.
   auto* mags = reinterpret_cast<double*>(taps_ws + 2048L * a.slots);
   note_prologue_kernel(reinterpret_cast<const void*>(eq_mags));

@@ -33,6 +33,8 @@ constexpr int kEqHalf = 1023;
 constexpr int kEqValid = kEqFft - 2 * kEqHalf;
 void launch_eq_prologue(const StepArgs& a, float* taps_ws /*slots*2048*/, float* resp_ws /*slots*8192*/, cudaStream_t s);
 void launch_eq_main(const StepArgs& a, const float* resp_ws, cudaStream_t s);
+// Per-device response basis (1024 x 4128 fp32), built synchronously on first use.
+const float* eq_basis(int device);
 // Split form of launch_eq_main for a step whose prologue is still running: the forward
 // window FFTs (no response needed) go first into `spectrum` (eq_spectrum_bytes), then the
 // response product + inverse once the prologue is done.

@@ -46,11 +46,9 @@ def main():
         torch.cuda.synchronize()
     evs = [e for e in prof.events() if e.device_type.name == "CUDA" and e.time_range.elapsed_us() > 0]
     evs.sort(key=lambda e: e.time_range.start)
-    # split into the 3 renders at each render's first kernel (eq_mags of the first step's
-    # prologue); report the last one
-    firsts = [i for i, e in enumerate(evs) if "eq_mags" in e.name]
-    starts = firsts[::2] if len(firsts) >= 6 else firsts
-    groups = [evs[a:b] for a, b in zip(starts, starts[1:] + [len(evs)])]
+    # the 3 renders launch the same kernels: report the last third
+    n = len(evs) // 3
+    groups = [evs[i * n:(i + 1) * n] for i in range(3)]
     last = groups[-1]
     t0 = last[0].time_range.start
     end = max(e.time_range.end for e in last)
