@@ -602,6 +602,10 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
   // and the side streams fork after it, so its audio pass reaches the SMs before them.
   static const bool first_main = [] { const char* v = std::getenv("MGB_FIRST_PROLOGUE_MAIN"); return v && v[0] == '1'; }();
   const bool first_on_main = hoist && first_main && !split_first && !rd.steps.empty() && rd.steps[0].type == NodeType::Eq;
+  // Every step's synchronisation words, cleared once (one memset node instead of one per
+  // scan step on the critical path), first: a memset node queued behind the fork waits for
+  // SM room like a kernel.
+  if (lay.sync_bytes) cuda_check(cudaMemsetAsync(ws + lay.sync_begin, 0, lay.sync_bytes, stream), "memset sync");
   if (hoist) {
     if (first_on_main) {
       run_prologue(rd.steps[0].type, args[0], procs, ws + lay.prologue_off[0], stream);
@@ -624,9 +628,6 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
       cuda_check(cudaEventRecord(ev[k + 1], a), "event");
     }
   }
-  // Every step's synchronisation words, cleared once (one memset node instead of one per
-  // scan step on the critical path).
-  if (lay.sync_bytes) cuda_check(cudaMemsetAsync(ws + lay.sync_begin, 0, lay.sync_bytes, stream), "memset sync");
   for (std::size_t k = 0; k < rd.steps.size(); ++k) {
     const NodeType t = rd.steps[k].type;
     // Runs of small pointwise steps (latency-bound) go out as one launch, unless per-step
