@@ -17,6 +17,7 @@
 // The a^Ne correction term re-gathers e[n - Ne]; it is skipped when a^Ne < 1e-30.
 #include <cuda/atomic>
 
+#include <cstdlib>
 #include "launch.hpp"
 
 namespace mgb {
@@ -744,8 +745,11 @@ void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double ene
   const long seqs = static_cast<long>(a.slots) * a.batch;
   // Few sequences (a bus compressor): 1024-sample tiles of 128 threads, so the step still
   // spreads over the SMs; otherwise 4096-sample tiles of 512 threads.
-  const bool small = seqs * ((a.length + kDynTile - 1) / kDynTile) < 148;
-  const long tile = small ? kDynSmallTile : kDynTile;
+  // MGB_DYN_NT=128|256|512 forces the tile shape (diagnostics / A-B).
+  static const int force_nt = [] { const char* v = std::getenv("MGB_DYN_NT"); return v ? std::atoi(v) : 0; }();
+  const bool small = force_nt ? force_nt == kDynSmallThreads : seqs * ((a.length + kDynTile - 1) / kDynTile) < 148;
+  const bool mid = force_nt == 256;
+  const long tile = small ? kDynSmallTile : (mid ? 256L * kDynPerThread : kDynTile);
   const int tiles = static_cast<int>((a.length + tile - 1) / tile);
   const long total = seqs * tiles;
   if (zero_sync) cudaMemsetAsync(ws, 0, dyn_sync_bytes(a.slots, a.batch, a.length), s);
@@ -756,7 +760,13 @@ void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double ene
   const dim3 grid(static_cast<unsigned>(total));
 #define MGB_DYN_LAUNCH(G, V, T) \
   dyn_scan<G, V, false, T><<<grid, T, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, ticket, nullptr, epi)
-  if (small) {
+  if (mid) {
+    if (gate) {
+      if (vec) MGB_DYN_LAUNCH(true, true, 256); else MGB_DYN_LAUNCH(true, false, 256);
+    } else {
+      if (vec) MGB_DYN_LAUNCH(false, true, 256); else MGB_DYN_LAUNCH(false, false, 256);
+    }
+  } else if (small) {
     if (gate) {
       if (vec) MGB_DYN_LAUNCH(true, true, kDynSmallThreads); else MGB_DYN_LAUNCH(true, false, kDynSmallThreads);
     } else {
