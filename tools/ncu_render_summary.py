@@ -74,11 +74,12 @@ def main():
                 f"`{os.path.basename(rep)}` (gpurun_out/, not committed).\n\n")
         f.write("\n".join(lines) + "\n")
     # Traffic per render step type over the first render in the capture: from the first
-    # eq_conv<1> (the render's first kernel) up to the next one. Conv kernels are attributed by
+    # render's first kernel up to the next render's. Conv kernels are attributed by
     # order: a prologue pair (cols_fwd<.., 0>, rows_spec) belongs to the reverb_ir / delay_dense
     # that precedes it; main triples (cols_fwd<.., 1>, rows_conv, cols_inv) follow the step
     # order reverb then delay (config 2's type string ...rd...).
-    first = lambda k: "eq_conv<1>" in k or "eq_conv<1," in k  # noqa: E731  (split first-step EQ)
+    # the render's first kernel: the EQ magnitude tiles (basis path) or eq_conv<1> (split EQ)
+    first = lambda k: "eq_mag_tiles" in k or "eq_conv<1>" in k or "eq_conv<1," in k  # noqa: E731
     start = next(i for i, r in enumerate(recs) if first(r["kernel"]))
     end = next((i for i in range(start + 1, len(recs)) if first(recs[i]["kernel"]) or "mgb::" not in recs[i]["kernel"]),
                len(recs))
@@ -97,7 +98,7 @@ def main():
             step = "compressor"
         elif "dyn_scan<1" in k:
             step = "noisegate"
-        elif "pointwise_vec4<0" in k:
+        elif "pointwise_vec4<0" in k or "pointwise_wide<0" in k:
             step = "mix/out"
         elif "pointwise_vec4<1" in k:
             step = "gain"
