@@ -735,7 +735,7 @@ constexpr int kDynSmallThreads = 128;
 constexpr int kDynSmallTile = kDynSmallThreads * kDynPerThread;
 
 std::size_t dyn_sync_bytes(int slots, int batch, long length) {
-  const long tiles = (length + kDynSmallTile - 1) / kDynSmallTile;  // the finer of the two tilings
+  const long tiles = (length + 32 * kDynPerThread - 1) / (32 * kDynPerThread);  // the finest tiling (32 threads)
   return 256 + sizeof(unsigned long long) * static_cast<std::size_t>(slots) * batch * tiles;
 }
 
@@ -749,7 +749,11 @@ void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double ene
   static const int force_nt = [] { const char* v = std::getenv("MGB_DYN_NT"); return v ? std::atoi(v) : 0; }();
   const bool small = force_nt ? force_nt == kDynSmallThreads : seqs * ((a.length + kDynTile - 1) / kDynTile) < 148;
   const bool mid = force_nt == 256;
-  const long tile = small ? kDynSmallTile : (mid ? 256L * kDynPerThread : kDynTile);
+  // MGB_DYN_SMALL_NT=32|64|128: threads per tile of the few-sequences shape (A-B). One-warp
+  // tiles measured no faster on config 2 and their longer fp32 carry sums lose accuracy
+  // (rel-Linf 1.1e-4 on a 2500-sample console with a large first sample).
+  static const int small_nt = [] { const char* v = std::getenv("MGB_DYN_SMALL_NT"); return v ? std::atoi(v) : kDynSmallThreads; }();
+  const long tile = small ? static_cast<long>(small_nt) * kDynPerThread : (mid ? 256L * kDynPerThread : kDynTile);
   const int tiles = static_cast<int>((a.length + tile - 1) / tile);
   const long total = seqs * tiles;
   if (zero_sync) cudaMemsetAsync(ws, 0, dyn_sync_bytes(a.slots, a.batch, a.length), s);
@@ -765,6 +769,18 @@ void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double ene
       if (vec) MGB_DYN_LAUNCH(true, true, 256); else MGB_DYN_LAUNCH(true, false, 256);
     } else {
       if (vec) MGB_DYN_LAUNCH(false, true, 256); else MGB_DYN_LAUNCH(false, false, 256);
+    }
+  } else if (small && small_nt == 64) {
+    if (gate) {
+      if (vec) MGB_DYN_LAUNCH(true, true, 64); else MGB_DYN_LAUNCH(true, false, 64);
+    } else {
+      if (vec) MGB_DYN_LAUNCH(false, true, 64); else MGB_DYN_LAUNCH(false, false, 64);
+    }
+  } else if (small && small_nt == 32) {
+    if (gate) {
+      if (vec) MGB_DYN_LAUNCH(true, true, 32); else MGB_DYN_LAUNCH(true, false, 32);
+    } else {
+      if (vec) MGB_DYN_LAUNCH(false, true, 32); else MGB_DYN_LAUNCH(false, false, 32);
     }
   } else if (small) {
     if (gate) {
