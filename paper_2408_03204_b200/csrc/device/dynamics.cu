@@ -29,6 +29,7 @@ constexpr unsigned long long kFlagAgg = 1ull << 32;
 struct DynParams {
   float a, oma, aN, a16, atile, atile32;
   float T, W, R, invR, floor_;
+  float knee;  // knee-curve coefficient: (1/R - 1) / (4W) compressor, (1 - R) / (4W) gate
   int Ne;
 };
 
@@ -47,7 +48,7 @@ struct DynBwd {
 // Slot constants, derived by warp 0 of each CTA: lanes 0-3 evaluate the four fp64 powers
 // a^Ne, a^8, a^tile, a^(32 tile) side by side (one pow latency), lane 0 assembles.
 __device__ __forceinline__ void derive_params(const double* row, int env_taps, double floor_, long L, int lane,
-                                              DynParams* out, long tile = kDynTile) {
+                                              DynParams* out, long tile = kDynTile, bool gate = false) {
   const double a = row[0];
   const int Ne = static_cast<int>(env_taps < L ? env_taps : L);
   const double e = lane == 0 ? static_cast<double>(Ne)
@@ -69,13 +70,18 @@ __device__ __forceinline__ void derive_params(const double* row, int env_taps, d
   p.W = static_cast<float>(row[2]);
   p.R = static_cast<float>(row[3]);
   p.invR = static_cast<float>(1.0 / row[3]);
+  p.knee = static_cast<float>((gate ? 1.0 - row[3] : 1.0 / row[3] - 1.0) / (4.0 * row[2]));
   p.floor_ = static_cast<float>(floor_);
   *out = p;
 }
 
+// Gain exp(G_y - G_u) at envelope g (processors.cpp:71-130 knee curves). Fast-path math:
+// __logf / __expf (MUFU lg2 / ex2, ~1e-6 relative here) and the knee's division folded into a
+// per-slot coefficient: ~30 fewer instructions per sample than logf / expf / fdiv, in the
+// scan's replay loop that runs once per sample. `gu_out` receives G_u (backward pass).
 template <bool GATE>
-__device__ __forceinline__ float gain_of(float g, const DynParams& p) {
-  const float gu = logf(fmaxf(g, p.floor_));
+__device__ __forceinline__ float gain_of(float g, const DynParams& p, float* gu_out = nullptr) {
+  const float gu = __logf(fmaxf(g, p.floor_));
   float gy;
   if (!GATE) {
     if (gu >= p.T + p.W) {
@@ -84,7 +90,7 @@ __device__ __forceinline__ float gain_of(float g, const DynParams& p) {
       gy = gu;
     } else {
       const float d = gu - p.T + p.W;
-      gy = gu + (p.invR - 1.f) * d * d / (4.f * p.W);
+      gy = fmaf(p.knee * d, d, gu);
     }
   } else {
     if (gu >= p.T + p.W) {
@@ -93,10 +99,11 @@ __device__ __forceinline__ float gain_of(float g, const DynParams& p) {
       gy = p.T + p.R * (gu - p.T);
     } else {
       const float d = gu - p.T - p.W;
-      gy = gu + (1.f - p.R) * d * d / (4.f * p.W);
+      gy = fmaf(p.knee * d, d, gu);
     }
   }
-  return expf(gy - gu);
+  if (gu_out) *gu_out = gu;
+  return __expf(gy - gu);
 }
 
 // Gather-sum of the slot's inputs at kDynPerThread consecutive samples from n0.
@@ -218,7 +225,7 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
     tk = __shfl_sync(0xffffffffu, tk, 0);
     if (threadIdx.x == 0) s_ticket = tk;
     derive_params(a.params + 4L * ((tk % nseq) / a.batch), env_taps, floor_, a.length, threadIdx.x, &s_p,
-                  NT * kDynPerThread);
+                  NT * kDynPerThread, GATE);
     if (epi.n > 0 && threadIdx.x == 1) pw_epi_slots(epi, (tk % nseq) / a.batch, s_epi);
   }
   __syncthreads();
@@ -441,7 +448,7 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_bwd_dg(DynBwd d) {
   __shared__ double red[kDynThreads / 32][4];
   const int tile = blockIdx.x, seq = blockIdx.y;
   const int slot = seq / d.fw.batch, b = seq - slot * d.fw.batch;
-  if (threadIdx.x < 32) derive_params(d.fw.params + 4L * slot, d.env_taps, d.floor_, d.fw.length, threadIdx.x, &s_p);
+  if (threadIdx.x < 32) derive_params(d.fw.params + 4L * slot, d.env_taps, d.floor_, d.fw.length, threadIdx.x, &s_p, kDynTile, GATE);
   __syncthreads();
   const DynParams& p = s_p;  // read from shared memory where used (frees registers)
   const long L = d.fw.length;
@@ -459,18 +466,8 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_bwd_dg(DynBwd d) {
     const long n = n0 + k;
     if (n >= L) break;
     const float g = env[n];
-    const float gu = logf(fmaxf(g, p.floor_));
-    float gy;
-    if (!GATE) {
-      if (gu >= p.T + p.W) gy = p.T + (gu - p.T) * p.invR;
-      else if (gu < p.T - p.W) gy = gu;
-      else { const float q = gu - p.T + p.W; gy = gu + (p.invR - 1.f) * q * q / (4.f * p.W); }
-    } else {
-      if (gu >= p.T + p.W) gy = gu;
-      else if (gu < p.T - p.W) gy = p.T + p.R * (gu - p.T);
-      else { const float q = gu - p.T - p.W; gy = gu + (1.f - p.R) * q * q / (4.f * p.W); }
-    }
-    const float gain = expf(gy - gu);
+    float gu;
+    const float gain = gain_of<GATE>(g, p, &gu);  // the forward's own arithmetic
     const float dD = (dyl[k] * ul[k] + dyr[k] * ur[k]) * gain;
     const float slope = knee_grad<GATE>(gu, p, dD, acc);
     const float dg = g > p.floor_ ? dD * (slope - 1.f) / g : 0.f;
