@@ -219,15 +219,7 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
   // Tickets interleave sequences (all tile-0s, then all tile-1s, ...): a tile's
   // predecessors were dispatched `nseq` tickets earlier, so the carry rarely waits.
   const int nseq = a.slots * a.batch;
-  if (threadIdx.x < 32) {
-    int tk = 0;
-    if (threadIdx.x == 0) tk = static_cast<int>(atomicAdd(ticket, 1u));
-    tk = __shfl_sync(0xffffffffu, tk, 0);
-    if (threadIdx.x == 0) s_ticket = tk;
-    derive_params(a.params + 4L * ((tk % nseq) / a.batch), env_taps, floor_, a.length, threadIdx.x, &s_p,
-                  NT * kDynPerThread, GATE);
-    if (epi.n > 0 && threadIdx.x == 1) pw_epi_slots(epi, (tk % nseq) / a.batch, s_epi);
-  }
+  if (threadIdx.x == 0) s_ticket = static_cast<int>(atomicAdd(ticket, 1u));
   __syncthreads();
   const int tk = s_ticket;
   const int tile = tk / nseq, seq = tk - tile * nseq;
@@ -241,8 +233,16 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
   // across the carry wait (no spills at 64 registers).
   float drive[kDynPerThread];
   {
+    // The tile's own samples are requested first; warp 0 derives the slot constants (fp64
+    // powers) while they are in flight, instead of every warp waiting for them at the barrier
+    // before issuing any load (that barrier was 20 % of the stall samples).
     float mid[kDynPerThread];
     load_mid<VEC>(a, e0, e1, b, n0, mid);
+    if (threadIdx.x < 32) {
+      derive_params(a.params + 4L * slot, env_taps, floor_, a.length, threadIdx.x, &s_p, NT * kDynPerThread, GATE);
+      if (epi.n > 0 && threadIdx.x == 1) pw_epi_slots(epi, slot, s_epi);
+    }
+    __syncthreads();
     if (p.aN != 0.f) {
       float mo[kDynPerThread];
       load_mid<VEC>(a, e0, e1, b, n0 - p.Ne, mo);
