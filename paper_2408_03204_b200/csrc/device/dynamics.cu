@@ -115,7 +115,7 @@ __device__ __forceinline__ void load16(const StepArgs& a, int e0, int e1, int b,
   const long boff = static_cast<long>(b) * 2 * a.length;
   if (VEC && n0 + kDynPerThread <= a.length) {
     for (int e = e0; e < e1; ++e) {
-      const float* p = a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff + n0;
+      const float* p = a.src + edge_row(a, e) * a.rowstride + boff + n0;
 #pragma unroll
       for (int q = 0; q < kDynPerThread / 4; ++q) {
         const float4 l = __ldg(reinterpret_cast<const float4*>(p) + q);
@@ -126,7 +126,7 @@ __device__ __forceinline__ void load16(const StepArgs& a, int e0, int e1, int b,
     }
   } else {
     for (int e = e0; e < e1; ++e) {
-      const float* p = a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff;
+      const float* p = a.src + edge_row(a, e) * a.rowstride + boff;
 #pragma unroll
       for (int k = 0; k < kDynPerThread; ++k) {
         const long n = n0 + k;
@@ -146,7 +146,7 @@ __device__ __forceinline__ void load4(const StepArgs& a, int e0, int e1, int b, 
   if (VEC && n >= 0 && n + 4 <= a.length) {
     float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
     for (int e = e0; e < e1; ++e) {
-      const float* p = a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff + n;
+      const float* p = a.src + edge_row(a, e) * a.rowstride + boff + n;
       l = f4add(l, __ldg(reinterpret_cast<const float4*>(p)));
       r = f4add(r, __ldg(reinterpret_cast<const float4*>(p + a.length)));
     }
@@ -157,7 +157,7 @@ __device__ __forceinline__ void load4(const StepArgs& a, int e0, int e1, int b, 
 #pragma unroll
   for (int k = 0; k < 4; ++k) ul[k] = ur[k] = 0.f;
   for (int e = e0; e < e1; ++e) {
-    const float* p = a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff;
+    const float* p = a.src + edge_row(a, e) * a.rowstride + boff;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if (n + k >= 0 && n + k < a.length) {
@@ -181,7 +181,7 @@ __device__ __forceinline__ void load_mid(const StepArgs& a, int e0, int e1, int 
     for (int q = 0; q < kDynPerThread / 4; ++q) {
       float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
       for (int e = e0; e < e1; ++e) {
-        const float* p = a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff + n0;
+        const float* p = a.src + edge_row(a, e) * a.rowstride + boff + n0;
         l = f4add(l, __ldg(reinterpret_cast<const float4*>(p) + q));
         r = f4add(r, __ldg(reinterpret_cast<const float4*>(p + a.length) + q));
       }
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
   const int tk = s_ticket;
   const int tile = tk / nseq, seq = tk - tile * nseq;
   const int slot = seq / a.batch, b = seq - slot * a.batch;
-  const int e0 = __ldg(a.row_ptr + slot), e1 = __ldg(a.row_ptr + slot + 1);
+  const int e0 = slot_e0(a, slot), e1 = slot_e1(a, slot);
   const DynParams& p = s_p;  // read from shared memory where used (frees registers)
 
   const long n0 = static_cast<long>(tile) * (NT * kDynPerThread) + static_cast<long>(threadIdx.x) * kDynPerThread;

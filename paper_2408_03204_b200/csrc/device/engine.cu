@@ -389,6 +389,18 @@ void DevicePlan::build_index() {
   };
   for (const StepIndex& st : rd_.steps) emit(st.store_begin, st.store_end);
   emit(0, rd_.num_inputs);
+  // Dense steps: one edge per slot, from consecutive rows in slot order.
+  static const bool no_dense = [] { const char* v = std::getenv("MGB_NO_DENSE"); return v && v[0] == '1'; }();
+  dense_.assign(rd_.steps.size(), -1);
+  for (std::size_t k = 0; k < rd_.steps.size() && !no_dense; ++k) {
+    const StepIndex& st = rd_.steps[k];
+    const int slots = st.store_end - st.store_begin;
+    bool ok = slots > 0 && st.gather.size() == static_cast<std::size_t>(slots);
+    for (int e = 0; ok && e < slots; ++e) {
+      ok = st.aggregate[static_cast<std::size_t>(e)] == e && st.gather[static_cast<std::size_t>(e)] == st.gather[0] + e;
+    }
+    if (ok) dense_[k] = st.gather[0];
+  }
   // Pointwise followers (fused into the previous step's epilogue by render_arena).
   follow_off_.assign(rd_.steps.size(), -1);
   for (std::size_t k = 1; k < rd_.steps.size(); ++k) {
@@ -584,6 +596,7 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
     a.length = length;
     a.rowstride = rowstride;
     a.nnz = static_cast<int>(st.gather.size());
+    a.dense = plan.dense_src(static_cast<int>(k));
   }
   for (int r : plan.zero_rows()) {
     cuda_check(cudaMemsetAsync(arena + r * rowstride, 0, sizeof(float) * rowstride, stream), "memset");
@@ -819,6 +832,7 @@ void profile_steps(const DevicePlan& plan, const ProcessorSet& procs, const doub
     a.length = length;
     a.rowstride = rowstride;
     a.nnz = static_cast<int>(st.gather.size());
+    a.dense = plan.dense_src(static_cast<int>(k));
     run_prologue(st.type, a, procs, ws + lay.prologue_off[k], stream);
     // The reps are captured into a CUDA graph and replayed, so short kernels are timed on
     // the device without the host's per-launch cost between them.

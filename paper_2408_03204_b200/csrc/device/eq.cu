@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(EqWin<LOG>::kThreads, EqWin<LOG>::kMinBlocks) 
   extern __shared__ float2 buf[];
   const int sb = blockIdx.y;
   const int slot = sb / a.batch, b = sb - slot * a.batch;
-  const int e0 = __ldg(a.row_ptr + slot), e1 = __ldg(a.row_ptr + slot + 1);
+  const int e0 = slot_e0(a, slot), e1 = slot_e1(a, slot);
   const long out0 = static_cast<long>(blockIdx.x) * kEqOut;
   const long s0 = out0 - (kEqHalf + 1);
   const long boff = static_cast<long>(b) * 2 * a.length;
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(EqWin<LOG>::kThreads, EqWin<LOG>::kMinBlocks) 
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[r] = make_float2(0.f, 0.f);
   for (int e = e0; e < e1; ++e) {
-    const float* p = a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff;
+    const float* p = a.src + edge_row(a, e) * a.rowstride + boff;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       const long pos = s0 + threadIdx.x + r * M1;

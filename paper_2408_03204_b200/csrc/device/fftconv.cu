@@ -97,8 +97,8 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_fwd(StepArgs a, const flo
   if constexpr (SRC == ColSrc::Signal) {
     slot = item / a.batch;
     b = item - slot * a.batch;
-    e0 = __ldg(a.row_ptr + slot);
-    e1 = __ldg(a.row_ptr + slot + 1);
+    e0 = slot_e0(a, slot);
+    e1 = slot_e1(a, slot);
     len = a.length;
   }
   __shared__ float rec[SRC == ColSrc::DelayTaps ? kTaps * kTapRec : 1];
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_fwd(StepArgs a, const flo
   float2 vals[EPT];
   const float* one = nullptr;  // in-degree-1 fast path
   if constexpr (SRC == ColSrc::Signal) {
-    if (e1 - e0 == 1) one = a.src + static_cast<long>(__ldg(a.col + e0)) * a.rowstride + static_cast<long>(b) * 2 * a.length;
+    if (e1 - e0 == 1) one = a.src + edge_row(a, e0) * a.rowstride + static_cast<long>(b) * 2 * a.length;
   }
 #pragma unroll
   for (int q = 0; q < EPT; ++q) {

@@ -51,7 +51,7 @@ __device__ __forceinline__ void pointwise_vec4_body(const StepArgs& a, const PwE
   const long n4 = a.length >> 2;
   const long i = blockIdx.x * static_cast<long>(kPwThreads) + threadIdx.x;
   if (i >= n4) return;
-  const int e0 = __ldg(a.row_ptr + slot), e1 = __ldg(a.row_ptr + slot + 1);
+  const int e0 = slot_e0(a, slot), e1 = slot_e1(a, slot);
   const long boff = static_cast<long>(b) * 2 * a.length;
   const float* __restrict__ src = a.src;
   float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
@@ -60,7 +60,7 @@ __device__ __forceinline__ void pointwise_vec4_body(const StepArgs& a, const PwE
     float4 lv[8], rv[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const float4* p = reinterpret_cast<const float4*>(src + static_cast<long>(__ldg(a.col + e + u)) * a.rowstride + boff);
+      const float4* p = reinterpret_cast<const float4*>(src + edge_row(a, e + u) * a.rowstride + boff);
       lv[u] = __ldg(p + i);
       rv[u] = __ldg(p + n4 + i);
     }
@@ -71,7 +71,7 @@ __device__ __forceinline__ void pointwise_vec4_body(const StepArgs& a, const PwE
     }
   }
   for (; e < e1; ++e) {
-    const float4* p = reinterpret_cast<const float4*>(src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff);
+    const float4* p = reinterpret_cast<const float4*>(src + edge_row(a, e) * a.rowstride + boff);
     l = f4add(l, __ldg(p + i));
     r = f4add(r, __ldg(p + n4 + i));
   }
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kWideGroups * kWidePos) pointwise_wide(StepArg
   const long n4 = a.length >> 2;
   const int g = threadIdx.x / kWidePos, p = threadIdx.x - g * kWidePos;
   const long i = blockIdx.x * static_cast<long>(kWidePos) + p;
-  const int e0 = __ldg(a.row_ptr + slot), e1 = __ldg(a.row_ptr + slot + 1);
+  const int e0 = slot_e0(a, slot), e1 = slot_e1(a, slot);
   const int per = (e1 - e0 + kWideGroups - 1) / kWideGroups;
   const int ga = e0 + g * per, gb = min(e1, ga + per);
   const long boff = static_cast<long>(b) * 2 * a.length;
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kWideGroups * kWidePos) pointwise_wide(StepArg
       float4 lv[8], rv[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const float4* q = reinterpret_cast<const float4*>(a.src + static_cast<long>(__ldg(a.col + e + u)) * a.rowstride + boff);
+        const float4* q = reinterpret_cast<const float4*>(a.src + edge_row(a, e + u) * a.rowstride + boff);
         lv[u] = __ldg(q + i);
         rv[u] = __ldg(q + n4 + i);
       }
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kWideGroups * kWidePos) pointwise_wide(StepArg
       }
     }
     for (; e < gb; ++e) {
-      const float4* q = reinterpret_cast<const float4*>(a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + boff);
+      const float4* q = reinterpret_cast<const float4*>(a.src + edge_row(a, e) * a.rowstride + boff);
       l = f4add(l, __ldg(q + i));
       r = f4add(r, __ldg(q + n4 + i));
     }
@@ -169,7 +169,7 @@ template <PointOp OP>
 __global__ void __launch_bounds__(256) pointwise_scalar(StepArgs a) {
   const int sb = blockIdx.y;
   const int slot = sb / a.batch, b = sb - slot * a.batch;
-  const int e0 = __ldg(a.row_ptr + slot), e1 = __ldg(a.row_ptr + slot + 1);
+  const int e0 = slot_e0(a, slot), e1 = slot_e1(a, slot);
   float g0, g1;
   coeffs<OP>(a, slot, g0, g1);
   float* out = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length;
@@ -222,10 +222,10 @@ __global__ void __launch_bounds__(kPwThreads) pointwise_chain_vec4(PwChain c) {
     if (i >= n4) return;
     const long boff = static_cast<long>(b) * 2 * a.length;
     for (int slot = 0; slot < a.slots; ++slot) {
-      const int e0 = a.row_ptr[slot], e1 = a.row_ptr[slot + 1];
+      const int e0 = slot_e0(a, slot), e1 = slot_e1(a, slot);
       float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
       for (int e = e0; e < e1; ++e) {
-        const float4* p = reinterpret_cast<const float4*>(a.src + static_cast<long>(a.col[e]) * a.rowstride + boff);
+        const float4* p = reinterpret_cast<const float4*>(a.src + edge_row(a, e) * a.rowstride + boff);
         l = f4add(l, p[i]);
         r = f4add(r, p[n4 + i]);
       }

@@ -26,7 +26,18 @@ struct StepArgs {
   long length;           // L
   long rowstride;        // B*2*L
   int nnz = 0;           // edges of the step (host hint for launch shapes; 0 = unknown)
+  int dense = -1;        // >= 0: slot s reads exactly row dense + s (no CSR loads needed)
 };
+
+// CSR access. Dense steps (a track chain's steps read the previous step's rows in order)
+// skip the row_ptr -> col -> sample chain of dependent L2 round trips: only sample loads.
+__device__ __forceinline__ int slot_e0(const StepArgs& a, int slot) { return a.dense >= 0 ? slot : __ldg(a.row_ptr + slot); }
+__device__ __forceinline__ int slot_e1(const StepArgs& a, int slot) {
+  return a.dense >= 0 ? slot + 1 : __ldg(a.row_ptr + slot + 1);
+}
+__device__ __forceinline__ long edge_row(const StepArgs& a, int e) {
+  return a.dense >= 0 ? static_cast<long>(a.dense) + e : static_cast<long>(__ldg(a.col + e));
+}
 
 __device__ __forceinline__ const float* chan_ptr(const float* base, long row, long rowstride, int b, int c, long L) {
   return base + row * rowstride + (static_cast<long>(b) * 2 + c) * L;
@@ -37,7 +48,7 @@ __device__ __forceinline__ float2 gather2(const StepArgs& a, int e0, int e1, int
   float l = 0.f, r = 0.f;
   const long off = static_cast<long>(b) * 2 * a.length + n;
   for (int e = e0; e < e1; ++e) {
-    const float* p = a.src + static_cast<long>(__ldg(a.col + e)) * a.rowstride + off;
+    const float* p = a.src + edge_row(a, e) * a.rowstride + off;
     l += __ldg(p);
     r += __ldg(p + a.length);
   }

@@ -127,6 +127,9 @@ class DevicePlan {
   const int* t_row_ptr(int step) const;
   const int* t_col(int step) const;
   const std::vector<int>& zero_rows() const { return zero_rows_; }
+  // First source row when step k's slot s reads exactly row dense_src(k) + s (one edge per
+  // slot, consecutive rows): its kernels then need no CSR loads. -1 otherwise.
+  int dense_src(int step) const { return dense_[static_cast<std::size_t>(step)]; }
   // Step k (k >= 1) is a pointwise follower of step k-1 (gain / imager / mix / out whose
   // every node reads exactly one distinct node of step k-1): follow_map(k) maps step k-1's
   // slots to step k's slots (device); nullptr otherwise.
@@ -168,6 +171,7 @@ class DevicePlan {
   std::vector<int> host_;
   std::vector<long> rp_off_, col_off_, trp_off_, tcol_off_, follow_off_;
   std::vector<int> zero_rows_;
+  std::vector<int> dense_;
 };
 
 // Reverse-mode pass over a rendered arena (parameter gradients; the reference has no
