@@ -12,8 +12,8 @@
 // recurrence, warp shuffles, one smem level. Across tiles: every tile publishes its
 // aggregate (flag | fp32 B in one 64-bit store; all full tiles share A = a^4096) and sums
 // its predecessors' aggregates in a fixed order (see the carry block), so results are
-// bit-reproducible; tile order comes from an atomic ticket so every waited-on tile was
-// scheduled earlier.
+// bit-reproducible; tile order is the block index (blocks are dispatched in index order, so
+// every waited-on tile was scheduled earlier; MGB_DYN_TICKET=1 takes an atomic ticket instead).
 // The a^Ne correction term re-gathers e[n - Ne]; it is skipped when a^Ne < 1e-30.
 #include <cuda/atomic>
 
@@ -219,9 +219,15 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
   // Tickets interleave sequences (all tile-0s, then all tile-1s, ...): a tile's
   // predecessors were dispatched `nseq` tickets earlier, so the carry rarely waits.
   const int nseq = a.slots * a.batch;
-  if (threadIdx.x == 0) s_ticket = static_cast<int>(atomicAdd(ticket, 1u));
-  __syncthreads();
-  const int tk = s_ticket;
+  // Tile order: the block index (blocks are dispatched in index order, so every tile this
+  // one waits on is resident or done, as in single-pass decoupled look-back scans), or with
+  // `ticket` an atomic ticket (one L2 round trip and a barrier before any load).
+  int tk = static_cast<int>(blockIdx.x);
+  if (ticket != nullptr) {
+    if (threadIdx.x == 0) s_ticket = static_cast<int>(atomicAdd(ticket, 1u));
+    __syncthreads();
+    tk = s_ticket;
+  }
   const int tile = tk / nseq, seq = tk - tile * nseq;
   const int slot = seq / a.batch, b = seq - slot * a.batch;
   const int e0 = slot_e0(a, slot), e1 = slot_e1(a, slot);
@@ -759,8 +765,11 @@ void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double ene
   const long ne = envelope_taps < a.length ? envelope_taps : a.length;
   const bool vec = (a.length % 4 == 0) && (ne % 4 == 0);
   const dim3 grid(static_cast<unsigned>(total));
+  // MGB_DYN_TICKET=1: tile order from an atomic ticket instead of the block index (A-B).
+  static const bool use_ticket = [] { const char* v = std::getenv("MGB_DYN_TICKET"); return v && v[0] == '1'; }();
+  unsigned int* tick = use_ticket ? ticket : nullptr;
 #define MGB_DYN_LAUNCH(G, V, T) \
-  dyn_scan<G, V, false, T><<<grid, T, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, ticket, nullptr, epi)
+  dyn_scan<G, V, false, T><<<grid, T, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, tick, nullptr, epi)
   if (mid) {
     if (gate) {
       if (vec) MGB_DYN_LAUNCH(true, true, 256); else MGB_DYN_LAUNCH(true, false, 256);
