@@ -17,6 +17,8 @@ g = mg.generate_console(16, 0.3, 16)
 fg = mg.to_flat(g)
 rd = mg.compute_render_data(fg)
 P = rd.reorder_params(mg.random_legal_params(fg.node_types, 2024))
+if "MGB_CONV_FUSE" in os.environ:  # A-B: -1 auto, 0 separate kernel-spectrum rows pass, 1 fused
+    mg.set_conv_fuse(int(os.environ["MGB_CONV_FUSE"]))
 procs = mg.ProcessorSet()
 dr = mg.DeviceRenderer(rd, procs, 1, L, P)
 dr.sources.copy_(torch.as_tensor(np.stack([mg.uniform_noise(2 * L, 1000 + k).reshape(1, 2, L)
