@@ -121,7 +121,7 @@ void mg_render_graph_destroy(mg_graph* graph);
  * double, as render()). sources [K][B][2][L], outputs [num_outputs][B][2][L]; tables in
  * render order, validated like mg_render. Host buffers must stay valid until sync(). */
 int32_t mg_pipeline_create(const mg_plan* plan, const mg_processors* procs, int32_t batch, int64_t length,
-                           int32_t f32_io, int32_t depth, mg_pipeline** out);
+                           int32_t f32_io, int32_t depth, int32_t host_threads, mg_pipeline** out);
 int32_t mg_pipeline_submit(mg_pipeline* pipe, const double* const* tables, const int32_t* rows, const void* sources,
                            void* outputs);
 int32_t mg_pipeline_sync(mg_pipeline* pipe);
@@ -146,6 +146,12 @@ int32_t mg_render_backward_arena(const mg_plan* plan, const mg_processors* procs
  * pass), 0 always runs the separate kernel-spectrum row pass, 1 always fuses. Process-wide;
  * results agree either way. */
 void mg_set_conv_fuse(int32_t mode);
+
+/* Transform-size switch for the long convolutions (tests): 0 (default) picks per step the
+ * cheapest segmented overlap-save size (one next_pow2(L + taps - 1) transform, as the
+ * reference's fft_convolve `dsp.cpp:64-86`, whenever that is cheapest); 13..22 forces 2^log_n
+ * points per segment. Applies to plans whose device workspace is sized after the call. */
+void mg_set_conv_log(int32_t log_n);
 
 /* Optimisation helpers on device buffers (fit.cpp:25-96 with analytic gradients): the MSE
  * loss mean((y - t)^2) into *d_loss (fp64, deterministic) and d_grad = 2 (y - t) / n;

@@ -75,13 +75,14 @@ _sig("mg_profile_steps", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp, _
 _sig("mg_render_graph_create", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _P(_vp))
 _sig("mg_render_graph_launch", _i32, _vp, _vp)
 _sig("mg_render_graph_destroy", None, _vp)
-_sig("mg_pipeline_create", _i32, _vp, _vp, _i32, _i64, _i32, _i32, _P(_vp))
+_sig("mg_pipeline_create", _i32, _vp, _vp, _i32, _i64, _i32, _i32, _i32, _P(_vp))
 _sig("mg_pipeline_submit", _i32, _vp, _vp, _vp, _vp, _vp)
 _sig("mg_pipeline_sync", _i32, _vp)
 _sig("mg_pipeline_destroy", None, _vp)
 _sig("mg_backward_workspace_bytes", _i32, _vp, _vp, _i32, _i64, _P(_u64))
 _sig("mg_render_backward_arena", _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp)
 _sig("mg_set_conv_fuse", None, _i32)
+_sig("mg_set_conv_log", None, _i32)
 _sig("mg_batch_capacity", _i32, _vp, _vp, _i32, _i64, _vp)
 _sig("mg_batch_create", _i32, _vp, _i32, _i64, _vp, _i32, _P(_vp))
 _sig("mg_batch_submit", _i32, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp)
@@ -626,6 +627,11 @@ def generate_console(tracks: int, prune: float = 0.0, seed: int = 0) -> Graph:
 def set_conv_fuse(mode: int) -> None:
     """mg_set_conv_fuse: -1 auto (default), 0 separate kernel-spectrum rows pass, 1 fused."""
     _lib.mg_set_conv_fuse(int(mode))
+
+
+def set_conv_log(log_n: int) -> None:
+    """mg_set_conv_log: 0 automatic segment size (default), 13..22 forces 2^log_n-point segments."""
+    _lib.mg_set_conv_log(int(log_n))
 
 
 def generate_large_console_arrays(tracks: int = 64) -> Tuple[np.ndarray, np.ndarray]:

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstring>
 #include <memory>
+#include <map>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -20,6 +21,7 @@ void launch_mse_loss_grad(const float* y, const float* target, long n, float* gr
                           cudaStream_t s);
 void launch_sgd_step(bool dynamics, double* table, const double* grad, long n, double lr, cudaStream_t s);
 void set_conv_fuse(int mode);
+void set_conv_log(int log_n);
 }  // namespace mgb
 
 namespace mixgraph::workload {
@@ -31,7 +33,7 @@ using namespace mixgraph;
 
 struct mg_plan {
   RenderData rd;
-  std::unique_ptr<DevicePlan> dev;  // uploaded lazily on first device render
+  std::map<int, std::unique_ptr<DevicePlan>> dev;  // per device, uploaded lazily on first use
   std::vector<cudaEvent_t> events;  // per-step timing events (profiled renders)
   std::mutex mu;
   std::mutex render_mu;  // serialises enqueue: the plan's fork/join events are shared
@@ -152,7 +154,7 @@ void copy_text(const std::string& s, char* buf, int64_t cap, int64_t* len) {
 extern "C" {
 
 const char* mg_last_error(void) { return g_err.c_str(); }
-int32_t mg_abi_version(void) { return 1; }
+int32_t mg_abi_version(void) { return 2; }
 int32_t mg_param_width(int32_t t) { return (t < 0 || t >= kNumNodeTypes) ? -1 : param_width(static_cast<NodeType>(t)); }
 
 int32_t mg_graph_validate(const int32_t* types, int32_t n, const int32_t* edges, int32_t ne) {
@@ -303,7 +305,7 @@ int32_t mg_processors_info(const mg_processors* p, int64_t* info) {
   return MG_OK;
 }
 
-DevicePlan& device_plan(const mg_plan* cp);
+DevicePlan& device_plan(const mg_plan* cp, const mg_processors* procs);
 
 int32_t mg_render(const mg_plan* p, const mg_processors* procs, const double* const* tables, const int32_t* rows,
                   const double* sources, int32_t num_sources, int32_t batch, int64_t length, double fs, double* outputs,
@@ -322,32 +324,43 @@ int32_t mg_render(const mg_plan* p, const mg_processors* procs, const double* co
     std::vector<double*> outs, inter;
     for (int r = rd.output_begin; r < rd.buffer_rows; ++r) outs.push_back(outputs + stride * (r - rd.output_begin));
     for (int r = 0; intermediates && r < rd.buffer_rows; ++r) inter.push_back(intermediates + stride * r);
-    DevicePlan& dp = device_plan(p);
+    DevicePlan& dp = device_plan(p, procs);
     std::scoped_lock lock(const_cast<mg_plan*>(p)->render_mu);
     render_host(rd, *procs->ps, make_store(tables, rows), src.data(), batch, static_cast<long>(length), outs.data(),
                 intermediates ? inter.data() : nullptr, &dp);
   });
 }
 
-DevicePlan& device_plan(const mg_plan* cp) {
+// The plan's device-side step table, streams and events live on one device: one DevicePlan per
+// device the plan is rendered on (the ProcessorSet's; nullptr: the current device), created
+// and used with that device current.
+DevicePlan& device_plan(const mg_plan* cp, const mg_processors* procs) {
   auto* p = const_cast<mg_plan*>(cp);
+  int device = 0;
+  if (procs) {
+    device = procs->ps->device_id();
+  } else if (cudaGetDevice(&device) != cudaSuccess) {
+    throw std::runtime_error("cudaGetDevice failed");
+  }
+  if (cudaSetDevice(device) != cudaSuccess) throw std::runtime_error("cudaSetDevice failed");
   std::scoped_lock lock(p->mu);
-  if (!p->dev) p->dev = std::make_unique<DevicePlan>(p->rd);
-  return *p->dev;
+  auto& d = p->dev[device];
+  if (!d) d = std::make_unique<DevicePlan>(p->rd);
+  return *d;
 }
 
 int32_t mg_plan_workspace_bytes(const mg_plan* p, const mg_processors* procs, int32_t batch, int64_t length, uint64_t* bytes) {
-  return guarded([&] { *bytes = device_plan(p).workspace_bytes(batch, static_cast<long>(length), *procs->ps); });
+  return guarded([&] { *bytes = device_plan(p, procs).workspace_bytes(batch, static_cast<long>(length), *procs->ps); });
 }
 
 int32_t mg_plan_kernel_count(const mg_plan* p, int32_t batch, int64_t length, int32_t* count) {
-  return guarded([&] { *count = device_plan(p).kernels_per_render(batch, static_cast<long>(length)); });
+  return guarded([&] { *count = device_plan(p, nullptr).kernels_per_render(batch, static_cast<long>(length)); });
 }
 
 int32_t mg_render_arena(const mg_plan* p, const mg_processors* procs, const double* const* d_tables, float* d_arena,
                         int32_t batch, int64_t length, void* d_ws, uint64_t ws_bytes, void* stream) {
   return guarded([&] {
-    DevicePlan& dp = device_plan(p);
+    DevicePlan& dp = device_plan(p, procs);
     std::scoped_lock lock(const_cast<mg_plan*>(p)->render_mu);
     render_arena(dp, *procs->ps, d_tables, d_arena, batch, static_cast<long>(length), d_ws, ws_bytes,
                  static_cast<cudaStream_t>(stream));
@@ -359,7 +372,7 @@ int32_t mg_render_arena_profiled(const mg_plan* cp, const mg_processors* procs, 
                                  void* stream, float* step_ms, int32_t hoist) {
   return guarded([&] {
     auto* p = const_cast<mg_plan*>(cp);
-    DevicePlan& dp = device_plan(p);
+    DevicePlan& dp = device_plan(p, procs);
     {
       std::scoped_lock lock(p->mu);
       while (p->events.size() < 2 * p->rd.steps.size()) {
@@ -384,7 +397,7 @@ int32_t mg_profile_steps(const mg_plan* p, const mg_processors* procs, const dou
                          int32_t batch, int64_t length, void* d_ws, uint64_t ws_bytes, void* stream, int32_t reps,
                          float* step_ms) {
   return guarded([&] {
-    DevicePlan& dp = device_plan(p);
+    DevicePlan& dp = device_plan(p, procs);
     std::scoped_lock lock(const_cast<mg_plan*>(p)->render_mu);
     profile_steps(dp, *procs->ps, d_tables, d_arena, batch, static_cast<long>(length), d_ws, ws_bytes,
                   static_cast<cudaStream_t>(stream), reps, step_ms);
@@ -395,7 +408,7 @@ int32_t mg_render_graph_create(const mg_plan* p, const mg_processors* procs, con
                                float* d_arena, int32_t batch, int64_t length, void* d_ws, uint64_t ws_bytes,
                                mg_graph** out) {
   return guarded([&] {
-    DevicePlan& dp = device_plan(p);
+    DevicePlan& dp = device_plan(p, procs);
     std::scoped_lock lock(const_cast<mg_plan*>(p)->render_mu);
     auto g = std::make_unique<mg_graph>();
     g->g = std::make_unique<RenderGraph>(dp, *procs->ps, d_tables, d_arena, batch, static_cast<long>(length), d_ws,
@@ -411,13 +424,14 @@ int32_t mg_render_graph_launch(const mg_graph* g, void* stream) {
 void mg_render_graph_destroy(mg_graph* g) { delete g; }
 
 int32_t mg_pipeline_create(const mg_plan* p, const mg_processors* procs, int32_t batch, int64_t length, int32_t f32_io,
-                           int32_t depth, mg_pipeline** out) {
+                           int32_t depth, int32_t host_threads, mg_pipeline** out) {
   return guarded([&] {
-    DevicePlan& dp = device_plan(p);
+    DevicePlan& dp = device_plan(p, procs);
     std::scoped_lock lock(const_cast<mg_plan*>(p)->render_mu);
     auto q = std::make_unique<mg_pipeline>();
     q->plan = p;
-    q->p = std::make_unique<RenderPipeline>(dp, *procs->ps, batch, static_cast<long>(length), f32_io != 0, depth);
+    q->p = std::make_unique<RenderPipeline>(dp, *procs->ps, batch, static_cast<long>(length), f32_io != 0, depth,
+                                            host_threads);
     *out = q.release();
   });
 }
@@ -444,14 +458,14 @@ void mg_pipeline_destroy(mg_pipeline* q) { delete q; }
 
 int32_t mg_backward_workspace_bytes(const mg_plan* p, const mg_processors* procs, int32_t batch, int64_t length,
                                     uint64_t* bytes) {
-  return guarded([&] { *bytes = device_plan(p).backward_workspace_bytes(batch, static_cast<long>(length), *procs->ps); });
+  return guarded([&] { *bytes = device_plan(p, procs).backward_workspace_bytes(batch, static_cast<long>(length), *procs->ps); });
 }
 
 int32_t mg_render_backward_arena(const mg_plan* p, const mg_processors* procs, const double* const* d_tables,
                                  const float* d_arena, float* d_adjoint, double* const* d_grad_tables, int32_t batch,
                                  int64_t length, void* d_workspace, uint64_t workspace_bytes, void* stream) {
   return guarded([&] {
-    DevicePlan& dp = device_plan(p);
+    DevicePlan& dp = device_plan(p, procs);
     std::scoped_lock lock(const_cast<mg_plan*>(p)->render_mu);
     backward_arena(dp, *procs->ps, d_tables, d_arena, d_adjoint, d_grad_tables, batch, static_cast<long>(length),
                    d_workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
@@ -459,6 +473,8 @@ int32_t mg_render_backward_arena(const mg_plan* p, const mg_processors* procs, c
 }
 
 void mg_set_conv_fuse(int32_t mode) { mgb::set_conv_fuse(mode); }
+
+void mg_set_conv_log(int32_t log_n) { mgb::set_conv_log(log_n); }
 
 uint64_t mg_mse_scratch_bytes(void) { return mgb::mse_scratch_bytes(); }
 

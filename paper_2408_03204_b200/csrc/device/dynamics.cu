@@ -12,8 +12,10 @@
 // recurrence, warp shuffles, one smem level. Across tiles: every tile publishes its
 // aggregate (flag | fp32 B in one 64-bit store; all full tiles share A = a^4096) and sums
 // its predecessors' aggregates in a fixed order (see the carry block), so results are
-// bit-reproducible; tile order is the block index (blocks are dispatched in index order, so
-// every waited-on tile was scheduled earlier; MGB_DYN_TICKET=1 takes an atomic ticket instead).
+// bit-reproducible; tile order is the block index: a tile waits only on lower block indices,
+// which the hardware dispatches first (the forward-progress assumption of CUB's single-pass
+// decoupled look-back scan, AgentScan's tile_idx = blockIdx.x); the backward's re-store of the
+// envelope takes an atomic ticket instead.
 // The a^Ne correction term re-gathers e[n - Ne]; it is skipped when a^Ne < 1e-30.
 #include <cuda/atomic>
 
@@ -139,35 +141,6 @@ __device__ __forceinline__ void load16(const StepArgs& a, int e0, int e1, int b,
   }
 }
 
-// Gather-sum of both channels at 4 consecutive samples from n (edge order per sample).
-template <bool VEC>
-__device__ __forceinline__ void load4(const StepArgs& a, int e0, int e1, int b, long n, float* ul, float* ur) {
-  const long boff = static_cast<long>(b) * 2 * a.length;
-  if (VEC && n >= 0 && n + 4 <= a.length) {
-    float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
-    for (int e = e0; e < e1; ++e) {
-      const float* p = a.src + edge_row(a, e) * a.rowstride + boff + n;
-      l = f4add(l, __ldg(reinterpret_cast<const float4*>(p)));
-      r = f4add(r, __ldg(reinterpret_cast<const float4*>(p + a.length)));
-    }
-    ul[0] = l.x, ul[1] = l.y, ul[2] = l.z, ul[3] = l.w;
-    ur[0] = r.x, ur[1] = r.y, ur[2] = r.z, ur[3] = r.w;
-    return;
-  }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) ul[k] = ur[k] = 0.f;
-  for (int e = e0; e < e1; ++e) {
-    const float* p = a.src + edge_row(a, e) * a.rowstride + boff;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (n + k >= 0 && n + k < a.length) {
-        ul[k] += __ldg(p + n + k);
-        ur[k] += __ldg(p + a.length + n + k);
-      }
-    }
-  }
-}
-
 // mid[k] = l + r of the gathered input at n0 + k (each channel summed in edge order first, as
 // load16 does), four samples at a time, so only one float4 pair per channel is live.
 template <bool VEC>
@@ -198,6 +171,48 @@ __device__ __forceinline__ void load_mid(const StepArgs& a, int e0, int e1, int 
   }
 }
 
+// load_mid that also stashes the gathered stereo input of this thread's kDynPerThread samples
+// in shared memory (float4 groups at [q][NT]: consecutive threads, consecutive 16-byte words),
+// so the output pass after the carry wait reads it back instead of gathering it again.
+template <bool VEC, int NT>
+__device__ __forceinline__ void load_tile(const StepArgs& a, int e0, int e1, int b, long n0, float* mid, float4* sl,
+                                          float4* sr) {
+  const int t = threadIdx.x;
+  if (n0 >= a.length || n0 < 0) {
+#pragma unroll
+    for (int k = 0; k < kDynPerThread; ++k) mid[k] = 0.f;
+    return;
+  }
+  const long boff = static_cast<long>(b) * 2 * a.length;
+  if (VEC && n0 + kDynPerThread <= a.length) {
+#pragma unroll
+    for (int q = 0; q < kDynPerThread / 4; ++q) {
+      float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
+      for (int e = e0; e < e1; ++e) {
+        const float* p = a.src + edge_row(a, e) * a.rowstride + boff + n0;
+        l = f4add(l, __ldg(reinterpret_cast<const float4*>(p) + q));
+        r = f4add(r, __ldg(reinterpret_cast<const float4*>(p + a.length) + q));
+      }
+      sl[q * NT + t] = l;
+      sr[q * NT + t] = r;
+      mid[4 * q] = l.x + r.x;
+      mid[4 * q + 1] = l.y + r.y;
+      mid[4 * q + 2] = l.z + r.z;
+      mid[4 * q + 3] = l.w + r.w;
+    }
+  } else {
+    float ul[kDynPerThread], ur[kDynPerThread];
+    load16<false>(a, e0, e1, b, n0, ul, ur);
+#pragma unroll
+    for (int q = 0; q < kDynPerThread / 4; ++q) {
+      sl[q * NT + t] = make_float4(ul[4 * q], ul[4 * q + 1], ul[4 * q + 2], ul[4 * q + 3]);
+      sr[q * NT + t] = make_float4(ur[4 * q], ur[4 * q + 1], ur[4 * q + 2], ur[4 * q + 3]);
+    }
+#pragma unroll
+    for (int k = 0; k < kDynPerThread; ++k) mid[k] = ul[k] + ur[k];
+  }
+}
+
 __device__ __forceinline__ void compose(float& A, float& B, float Ap, float Bp) {
   // earlier (Ap, Bp) then current (A, B)
   B = fmaf(A, Bp, B);
@@ -212,6 +227,7 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
                                                          unsigned long long* status, unsigned int* ticket,
                                                          float* env, PwEpi epi) {
   __shared__ float wA[NT / 32], wB[NT / 32];
+  __shared__ float4 s_in[2][kDynPerThread / 4][NT];  // the tile's gathered input (l, r), read once
   __shared__ float s_carry;
   __shared__ int s_ticket;
   __shared__ DynParams s_p;
@@ -234,16 +250,16 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
   const DynParams& p = s_p;  // read from shared memory where used (frees registers)
 
   const long n0 = static_cast<long>(tile) * (NT * kDynPerThread) + static_cast<long>(threadIdx.x) * kDynPerThread;
-  // drive[k] = (1-a) (e[n] - a^Ne e[n-Ne]) is all the scan keeps in registers; the input
-  // samples are gathered again (L2-resident) for the output pass, so nothing else stays live
-  // across the carry wait (no spills at 64 registers).
+  // drive[k] = (1-a) (e[n] - a^Ne e[n-Ne]) is all the scan keeps in registers; the gathered
+  // input samples wait in shared memory for the output pass (read from memory once), so
+  // nothing else stays live across the carry wait (no spills at 64 registers).
   float drive[kDynPerThread];
   {
     // The tile's own samples are requested first; warp 0 derives the slot constants (fp64
     // powers) while they are in flight, instead of every warp waiting for them at the barrier
     // before issuing any load (that barrier was 20 % of the stall samples).
     float mid[kDynPerThread];
-    load_mid<VEC>(a, e0, e1, b, n0, mid);
+    load_tile<VEC, NT>(a, e0, e1, b, n0, mid, &s_in[0][0][0], &s_in[1][0][0]);
     if (threadIdx.x < 32) {
       derive_params(a.params + 4L * slot, env_taps, floor_, a.length, threadIdx.x, &s_p, NT * kDynPerThread, GATE);
       if (epi.n > 0 && threadIdx.x == 1) pw_epi_slots(epi, slot, s_epi);
@@ -346,9 +362,9 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
   const bool full = VEC && n0 + kDynPerThread <= a.length;
 #pragma unroll
   for (int q = 0; q < kDynPerThread / 4; ++q) {
-    // inputs gathered again (L2-resident), four samples at a time
-    float ul[4], ur[4];
-    load4<VEC>(a, e0, e1, b, n0 + 4 * q, ul, ur);
+    // this thread's own stashed input, four samples at a time (no barrier: written by itself)
+    const float4 l4 = s_in[0][q][threadIdx.x], r4 = s_in[1][q][threadIdx.x];
+    const float ul[4] = {l4.x, l4.y, l4.z, l4.w}, ur[4] = {r4.x, r4.y, r4.z, r4.w};
     float yl[4], yr[4];
 #pragma unroll
     for (int k4 = 0; k4 < 4; ++k4) {
@@ -747,48 +763,20 @@ void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double ene
   if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
   const long seqs = static_cast<long>(a.slots) * a.batch;
   // Few sequences (a bus compressor): 1024-sample tiles of 128 threads, so the step still
-  // spreads over the SMs; otherwise 4096-sample tiles of 512 threads.
-  // MGB_DYN_NT=128|256|512 forces the tile shape (diagnostics / A-B).
-  static const int force_nt = [] { const char* v = std::getenv("MGB_DYN_NT"); return v ? std::atoi(v) : 0; }();
-  const bool small = force_nt ? force_nt == kDynSmallThreads : seqs * ((a.length + kDynTile - 1) / kDynTile) < 148;
-  const bool mid = force_nt == 256;
-  // MGB_DYN_SMALL_NT=32|64|128: threads per tile of the few-sequences shape (A-B). One-warp
-  // tiles measured no faster on config 2 and their longer fp32 carry sums lose accuracy
-  // (rel-Linf 1.1e-4 on a 2500-sample console with a large first sample).
-  static const int small_nt = [] { const char* v = std::getenv("MGB_DYN_SMALL_NT"); return v ? std::atoi(v) : kDynSmallThreads; }();
-  const long tile = small ? static_cast<long>(small_nt) * kDynPerThread : (mid ? 256L * kDynPerThread : kDynTile);
+  // spreads over the SMs; otherwise 4096-sample tiles of 512 threads. (One-warp tiles measured
+  // no faster on config 2 and their longer fp32 carry sums lose accuracy.)
+  const bool small = seqs * ((a.length + kDynTile - 1) / kDynTile) < 148;
+  const long tile = small ? static_cast<long>(kDynSmallThreads) * kDynPerThread : kDynTile;
   const int tiles = static_cast<int>((a.length + tile - 1) / tile);
   const long total = seqs * tiles;
   if (zero_sync) cudaMemsetAsync(ws, 0, dyn_sync_bytes(a.slots, a.batch, a.length), s);
-  auto* ticket = static_cast<unsigned int*>(ws);
   auto* status = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 256);
   const long ne = envelope_taps < a.length ? envelope_taps : a.length;
   const bool vec = (a.length % 4 == 0) && (ne % 4 == 0);
   const dim3 grid(static_cast<unsigned>(total));
-  // MGB_DYN_TICKET=1: tile order from an atomic ticket instead of the block index (A-B).
-  static const bool use_ticket = [] { const char* v = std::getenv("MGB_DYN_TICKET"); return v && v[0] == '1'; }();
-  unsigned int* tick = use_ticket ? ticket : nullptr;
 #define MGB_DYN_LAUNCH(G, V, T) \
-  dyn_scan<G, V, false, T><<<grid, T, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, tick, nullptr, epi)
-  if (mid) {
-    if (gate) {
-      if (vec) MGB_DYN_LAUNCH(true, true, 256); else MGB_DYN_LAUNCH(true, false, 256);
-    } else {
-      if (vec) MGB_DYN_LAUNCH(false, true, 256); else MGB_DYN_LAUNCH(false, false, 256);
-    }
-  } else if (small && small_nt == 64) {
-    if (gate) {
-      if (vec) MGB_DYN_LAUNCH(true, true, 64); else MGB_DYN_LAUNCH(true, false, 64);
-    } else {
-      if (vec) MGB_DYN_LAUNCH(false, true, 64); else MGB_DYN_LAUNCH(false, false, 64);
-    }
-  } else if (small && small_nt == 32) {
-    if (gate) {
-      if (vec) MGB_DYN_LAUNCH(true, true, 32); else MGB_DYN_LAUNCH(true, false, 32);
-    } else {
-      if (vec) MGB_DYN_LAUNCH(false, true, 32); else MGB_DYN_LAUNCH(false, false, 32);
-    }
-  } else if (small) {
+  dyn_scan<G, V, false, T><<<grid, T, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, nullptr, nullptr, epi)
+  if (small) {
     if (gate) {
       if (vec) MGB_DYN_LAUNCH(true, true, kDynSmallThreads); else MGB_DYN_LAUNCH(true, false, kDynSmallThreads);
     } else {

@@ -177,6 +177,8 @@ ProcessorSet::ProcessorSet(const ProcessorConfig& config) : config_(config) {
 
 ProcessorSet::~ProcessorSet() = default;
 
+int ProcessorSet::device_id() const { return dev_->device; }
+
 namespace {
 
 mgb::ReverbConst reverb_const(const ProcessorSet& p) {
@@ -211,7 +213,6 @@ std::size_t sync_bytes(NodeType t, int slots, int batch, long length) {
 
 std::size_t main_bytes(NodeType t, int slots, int batch, long length, const ProcessorSet& p) {
   switch (t) {
-    case NodeType::Eq: return mgb::eq_spectrum_bytes(slots, batch, length);
     case NodeType::Reverb: return mgb::conv_main_bytes(mgb::conv_geom(length, p.reverb_length()), slots, batch);
     case NodeType::Delay: return mgb::conv_main_bytes(mgb::conv_geom(length, p.delay_span()), slots, batch);
     default: return 0;
@@ -297,11 +298,9 @@ int chain_length(const RenderData& rd, std::size_t k, int batch, long length) {
 // Number of pointwise follower steps fused into step k's epilogue (render_arena): the
 // producer is a compressor / noisegate scan or a pointwise step too large for a chain
 // (vector path), the followers the consecutive steps the plan marked as followers.
-// MGB_NO_EPI=1 turns the fusion off (diagnostics / A-B).
 int epi_followers(const DevicePlan& plan, std::size_t k, int batch, long length) {
-  static const bool off = [] { const char* v = std::getenv("MGB_NO_EPI"); return v && v[0] == '1'; }();
   const RenderData& rd = plan.data();
-  if (off || k + 1 >= rd.steps.size()) return 0;
+  if (k + 1 >= rd.steps.size()) return 0;
   const StepIndex& st = rd.steps[k];
   const bool dyn = st.type == NodeType::Compressor || st.type == NodeType::Noisegate;
   const bool pw = is_pointwise(st.type) && st.type != NodeType::In && length % 4 == 0 &&
@@ -310,20 +309,6 @@ int epi_followers(const DevicePlan& plan, std::size_t k, int batch, long length)
   int n = 0;
   while (n < mgb::kPwEpiMax && k + 1 + n < rd.steps.size() && plan.follows(static_cast<int>(k + 1 + n))) ++n;
   return n;
-}
-
-// A first-step EQ whose grid is at most two waves runs its response-independent forward FFTs
-// before its prologue has finished (render_arena); a larger grid keeps the GPU busy anyway and
-// the round trip of the window spectra through memory would only cost bandwidth.
-bool split_first_eq(const RenderData& rd, int batch, long length) {
-  // Off by default since the EQ response became one basis product (a few us): the split's
-  // spectrum round trip then costs more than it hides (0.271 -> 0.261 ms per config-2
-  // render). MGB_EQ_SPLIT=1 restores it.
-  static const bool off = [] { const char* v = std::getenv("MGB_EQ_SPLIT"); return !(v && v[0] == '1'); }();
-  if (off || rd.steps.empty() || rd.steps[0].type != NodeType::Eq) return false;
-  const long blocks = (length + 6143) / 6144;
-  const long grid = blocks * (rd.steps[0].store_end - rd.steps[0].store_begin) * batch;
-  return grid <= 2L * 2 * 148;
 }
 
 std::size_t step_ws_bytes(NodeType t, int slots, int batch, long length, const ProcessorSet& p) {
@@ -390,9 +375,8 @@ void DevicePlan::build_index() {
   for (const StepIndex& st : rd_.steps) emit(st.store_begin, st.store_end);
   emit(0, rd_.num_inputs);
   // Dense steps: one edge per slot, from consecutive rows in slot order.
-  static const bool no_dense = [] { const char* v = std::getenv("MGB_NO_DENSE"); return v && v[0] == '1'; }();
   dense_.assign(rd_.steps.size(), -1);
-  for (std::size_t k = 0; k < rd_.steps.size() && !no_dense; ++k) {
+  for (std::size_t k = 0; k < rd_.steps.size(); ++k) {
     const StepIndex& st = rd_.steps[k];
     const int slots = st.store_end - st.store_begin;
     bool ok = slots > 0 && st.gather.size() == static_cast<std::size_t>(slots);
@@ -476,8 +460,6 @@ namespace {
 // 12 reverbs and 7 delays) and step k+1 reads none of step k's output rows.
 bool pairable(const RenderData& rd, std::size_t k, long length, const ProcessorSet& p) {
   if (k + 1 >= rd.steps.size()) return false;
-  static const bool off = [] { const char* v = std::getenv("MGB_NO_LANES"); return v && v[0] == '1'; }();
-  if (off) return false;
   const StepIndex& a = rd.steps[k];
   const StepIndex& b = rd.steps[k + 1];
   auto conv = [](NodeType t) { return t == NodeType::Reverb || t == NodeType::Delay; };
@@ -561,8 +543,6 @@ int DevicePlan::kernels_per_render(int batch, long length) const {
     k += n > 1 ? 1 : step_kernels(rd_.steps[i].type);
     i += static_cast<std::size_t>(n > 1 ? n : 1 + epi_followers(*this, i, batch, length));
   }
-  // A first-step EQ may be split into forward and inverse launches (render_arena, hoisted).
-  if (split_first_eq(rd_, batch, length)) ++k;
   return k;
 }
 
@@ -602,41 +582,24 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
     cuda_check(cudaMemsetAsync(arena + r * rowstride, 0, sizeof(float) * rowstride, stream), "memset");
   }
   // Parameter-only prologues (EQ design, reverb/delay impulse responses and their spectra)
-  // depend on nothing the render computes: fork them onto the plan's side stream so they
-  // overlap the earlier steps, and join each one right before its step's audio pass.
-  // MGB_NO_HOIST=1 runs every prologue inline (diagnostics: isolated per-step costs).
-  static const bool no_hoist = [] { const char* v = std::getenv("MGB_NO_HOIST"); return v && v[0] == '1'; }();
-  if (no_hoist) hoist = false;
-  // A first-step EQ starts its response-independent forward FFTs before the prologues are
-  // enqueued, so its grid reaches the GPU ahead of the side stream's grids.
-  const bool split_first = hoist && split_first_eq(rd, batch, length);
+  // depend on nothing the render computes: fork them onto the plan's side streams so they
+  // overlap the earlier steps, and join each one right before its step's audio pass
+  // (hoist = false runs every prologue inline: isolated per-step costs).
   const cudaEvent_t* ev = plan.events();
-  // MGB_FIRST_PROLOGUE_MAIN=1: an unsplit first-step EQ runs its prologue on the main stream
-  // and the side streams fork after it, so its audio pass reaches the SMs before them.
-  static const bool first_main = [] { const char* v = std::getenv("MGB_FIRST_PROLOGUE_MAIN"); return v && v[0] == '1'; }();
-  const bool first_on_main = hoist && first_main && !split_first && !rd.steps.empty() && rd.steps[0].type == NodeType::Eq;
   // Every step's synchronisation words, cleared once (one memset node instead of one per
   // scan step on the critical path), first: a memset node queued behind the fork waits for
   // SM room like a kernel.
   if (lay.sync_bytes) cuda_check(cudaMemsetAsync(ws + lay.sync_begin, 0, lay.sync_bytes, stream), "memset sync");
   if (hoist) {
-    if (first_on_main) {
-      run_prologue(rd.steps[0].type, args[0], procs, ws + lay.prologue_off[0], stream);
-      cuda_check(cudaEventRecord(ev[1], stream), "event");
-    }
     cuda_check(cudaEventRecord(ev[0], stream), "event");  // fork point: before any render work
-    if (split_first) mgb::launch_eq_forward(args[0], reinterpret_cast<float2*>(ws + lay.main_off), stream);
     for (cudaStream_t a : plan.aux_streams()) cuda_check(cudaStreamWaitEvent(a, ev[0], 0), "wait");
-    int next = 0;  // independent prologues round-robin over the side streams
     for (std::size_t k = 0; k < rd.steps.size(); ++k) {
-      if (!has_prologue(rd.steps[k].type) || (k == 0 && first_on_main)) continue;
+      if (!has_prologue(rd.steps[k].type)) continue;
       // Prologues complete in the order their steps need them on side stream 0, except the
       // delay's, which gets side stream 1 and so runs beside the reverb's (the delay step's
       // kernel spectrum was the critical path once conv steps joined their prologue late:
-      // 0.324 -> 0.309 ms per config-2 render). MGB_SIDE_STREAMS=1 restores one stream.
-      static const int nside = [] { const char* v = std::getenv("MGB_SIDE_STREAMS"); return v ? std::atoi(v) : 2; }();
-      cudaStream_t a = plan.aux_streams()[nside >= 2 && rd.steps[k].type == NodeType::Delay ? 1 : 0];
-      ++next;
+      // 0.324 -> 0.309 ms per config-2 render).
+      cudaStream_t a = plan.aux_streams()[rd.steps[k].type == NodeType::Delay ? 1 : 0];
       run_prologue(rd.steps[k].type, args[k], procs, ws + lay.prologue_off[k], a);
       cuda_check(cudaEventRecord(ev[k + 1], a), "event");
     }
@@ -690,20 +653,10 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
     }
     char* pws = ws + lay.prologue_off[k];
     char* mws = ws + lay.main_off;
-    // The first step has nothing to hide its prologue behind: an EQ there runs its
-    // response-independent forward FFTs before joining the prologue, the rest after.
-    const bool split_eq = split_first && k == 0;
     if (step_events) cuda_check(cudaEventRecord(step_events[2 * k], stream), "event");
-    // (forward FFTs of a split first EQ were enqueued before the prologues, see above)
     const cudaEvent_t join = hoist && has_prologue(t) ? ev[k + 1] : nullptr;
     if (!hoist) run_prologue(t, args[k], procs, pws, stream);
-    if (split_eq) {
-      cuda_check(cudaStreamWaitEvent(stream, join, 0), "wait");
-      mgb::launch_eq_inverse(args[k], reinterpret_cast<float*>(pws + eq_taps_bytes(args[k].slots)),
-                             reinterpret_cast<float2*>(mws), stream);
-    } else {
-      run_main(t, args[k], procs, pws, mws, ws + lay.sync_off[k], false, stream, join, epi);
-    }
+    run_main(t, args[k], procs, pws, mws, ws + lay.sync_off[k], false, stream, join, epi);
     if (step_events) cuda_check(cudaEventRecord(step_events[2 * k + 1], stream), "event");
     k += static_cast<std::size_t>(epi.n);
   }
@@ -891,7 +844,6 @@ RenderGraph::RenderGraph(const DevicePlan& plan, const ProcessorSet& procs, cons
   cuda_check(cudaGraphGetNodes(graph_, nullptr, &n), "graph nodes");
   std::vector<cudaGraphNode_t> nodes(n);
   cuda_check(cudaGraphGetNodes(graph_, nodes.data(), &n), "graph nodes");
-  int low = 0, high = 0;
   for (cudaGraphNode_t node : nodes) {
     cudaGraphNodeType type;
     cuda_check(cudaGraphNodeGetType(node, &type), "node type");
@@ -901,12 +853,7 @@ RenderGraph::RenderGraph(const DevicePlan& plan, const ProcessorSet& procs, cons
     cudaLaunchAttributeValue v{};
     const bool pro = mgb::is_prologue_kernel(kp.func);
     v.priority = pro ? least : greatest;
-    (pro ? low : high)++;
     cuda_check(cudaGraphKernelNodeSetAttribute(node, cudaLaunchAttributePriority, &v), "node priority");
-  }
-  if (const char* dbg = std::getenv("MGB_DEBUG"); dbg && dbg[0] == '1') {
-    std::fprintf(stderr, "[mgb] render graph: %zu nodes, %d prologue kernels (priority %d), %d main kernels (priority %d)\n",
-                 n, low, least, high, greatest);
   }
   cuda_check(cudaGraphInstantiateWithFlags(&exec_, graph_, cudaGraphInstantiateFlagUseNodePriority), "instantiate");
 }
@@ -1068,14 +1015,10 @@ struct RenderPipeline::HostConvert {
   // overlaps the conversion of later ones (and the next render's conversion overlaps this
   // render's kernels).
   void upload(const double* const* src, int nsrc, std::size_t stride, float* pin, float* dev, cudaStream_t st) {
-    // MGB_PIPELINE_CHUNK_LOG2: chunk size in floats (diagnostics / A-B), default 2^18.
-    static const std::size_t kChunk = [] {
-      const char* v = std::getenv("MGB_PIPELINE_CHUNK_LOG2");
-      return std::size_t{1} << (v ? std::clamp(std::atoi(v), 12, 24) : 18);
-    }();
+    // 2^18 floats per chunk (smaller chunks measured slower: concurrent cudaMemcpyAsync calls
+    // contend; one H2D after converting everything measured no faster).
+    constexpr std::size_t kChunk = std::size_t{1} << 18;
     const std::size_t per = (stride + kChunk - 1) / kChunk, total = per * static_cast<std::size_t>(nsrc);
-    // MGB_PIPELINE_ONE_COPY=1: convert everything, then one H2D (diagnostics / A-B).
-    static const bool one_copy = [] { const char* v = std::getenv("MGB_PIPELINE_ONE_COPY"); return v && v[0] == '1'; }();
     std::atomic<std::size_t> next{0};
     std::atomic<int> failed{0};
     parallel([&](int) {
@@ -1083,14 +1026,11 @@ struct RenderPipeline::HostConvert {
         const std::size_t k = c / per, lo = (c % per) * kChunk, n = std::min(kChunk, stride - lo);
         const std::size_t off = k * stride + lo;
         hostconv::f64_to_f32(src[k] + lo, pin + off, n);
-        if (!one_copy && cudaMemcpyAsync(dev + off, pin + off, sizeof(float) * n, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+        if (cudaMemcpyAsync(dev + off, pin + off, sizeof(float) * n, cudaMemcpyHostToDevice, st) != cudaSuccess) {
           failed = 1;
         }
       }
     });
-    if (one_copy && cudaMemcpyAsync(dev, pin, sizeof(float) * stride * nsrc, cudaMemcpyHostToDevice, st) != cudaSuccess) {
-      failed = 1;
-    }
     if (failed) throw std::runtime_error("cuda: RenderPipeline source upload failed");
   }
   std::uint64_t enqueue(Job j) {
@@ -1123,17 +1063,16 @@ RenderPipeline::RenderPipeline(const DevicePlan& plan, const ProcessorSet& procs
     int n = host_threads;
     if (n < 0) {
       // Default: half the host's hardware threads, at most 8 (config 2 on the 16-thread B200
-      // box hosts: 0.66 ms/render device conversion, 0.48 ms with 8 host threads).
-      const char* v = std::getenv("MGB_PIPELINE_HOST_THREADS");  // diagnostics: 0 = device conversion
-      // Processes sharing the host (torchrun sets LOCAL_WORLD_SIZE) split its threads.
+      // box hosts: 0.66 ms/render device conversion, 0.48 ms with 8 host threads). Processes
+      // sharing the host (torchrun sets LOCAL_WORLD_SIZE) split its threads; 0 converts on
+      // the device (double audio crosses PCIe).
       const char* lw = std::getenv("LOCAL_WORLD_SIZE");
       const int procs_on_host = std::max(1, lw ? std::atoi(lw) : 1);
       const int hw = static_cast<int>(std::thread::hardware_concurrency());
-      n = v ? std::atoi(v) : std::clamp(hw / (2 * procs_on_host) - 1, 0, 7);
+      n = std::clamp(hw / (2 * procs_on_host) - 1, 0, 7);
     }
     if (n >= 1) conv_ = std::make_unique<HostConvert>(n, procs.device().device);
-    const char* f = std::getenv("MGB_PIPELINE_HOST_FRACTION");  // diagnostics
-    host_fraction_ = f ? std::clamp(std::atof(f), 0.0, 1.0) : kHostFraction;
+    host_fraction_ = kHostFraction;
   }
   const RenderData& rd = plan.data();
   const std::size_t rows = static_cast<std::size_t>(rd.buffer_rows);
@@ -1198,8 +1137,13 @@ void RenderPipeline::submit(const ParamStore& params, const void* const* sources
     cuda_check(cudaEventSynchronize(s.h2d), "pipeline staging");
     if (conv_ && s.job) conv_->wait(s.job);
   }
-  // Inputs: the slot's previous render must have consumed its sources and params.
-  if (reused) cuda_check(cudaStreamWaitEvent(h2d_, s.done, 0), "wait");
+  // Inputs: the slot's previous render must have consumed its sources and params, and its
+  // outputs must have been read back: in device-conversion mode the fp64 outputs sit in the
+  // same staging buffer the next sources are uploaded into.
+  if (reused) {
+    cuda_check(cudaStreamWaitEvent(h2d_, s.done, 0), "wait");
+    cuda_check(cudaStreamWaitEvent(h2d_, s.d2h, 0), "wait");
+  }
   // Parameters go through pinned staging: a pageable cudaMemcpyAsync waits for the stream's
   // earlier copies (the previous render's sources), which serialised this render's source
   // conversion behind the previous render's whole upload (0.46 -> ~0.36 ms per render e2e).

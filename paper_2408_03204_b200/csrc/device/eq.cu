@@ -293,8 +293,8 @@ template <int LOG> struct EqWin {
 // kFft-sample window starting at out0 - 1024; the circular convolution is exact for window
 // indices [1023, kFft - 1024]. Window loads feed the first FFT pass directly and the last
 // inverse pass stores directly (register-ended transforms, fft_smem.cuh), both coalesced.
-template <int MODE, int LOG>
-__global__ void __launch_bounds__(EqWin<LOG>::kThreads, EqWin<LOG>::kMinBlocks) eq_conv(StepArgs a, const float* resp, float2* spec) {
+template <int LOG>
+__global__ void __launch_bounds__(EqWin<LOG>::kThreads, EqWin<LOG>::kMinBlocks) eq_conv(StepArgs a, const float* resp) {
   using W = EqWin<LOG>;
   constexpr int kEqFft = W::kFft, kEqOut = W::kOut, kNt = W::kThreads;
   constexpr int kRs = kEqFft == 8192 ? 1 : 8192 / kEqFft;   // response bin stride
@@ -306,28 +306,8 @@ __global__ void __launch_bounds__(EqWin<LOG>::kThreads, EqWin<LOG>::kMinBlocks) 
   const long out0 = static_cast<long>(blockIdx.x) * kEqOut;
   const long s0 = out0 - (kEqHalf + 1);
   const long boff = static_cast<long>(b) * 2 * a.length;
-  float2* sp = spec + (static_cast<long>(sb) * gridDim.x + blockIdx.x) * kEqFft;  // MODE 1/2 scratch
   const float* rs = resp + static_cast<long>(slot) * 8192;
-  if constexpr (MODE == 2) {
-    // spectrum computed earlier by MODE 1: load it with the response product fused; loads
-    // are issued 8 at a time ahead of their smem stores.
-    constexpr int PER = kEqFft / kNt;
-    static_assert(PER % 8 == 0, "eq_conv: spectrum load chunking");
-#pragma unroll
-    for (int q0 = 0; q0 < PER; q0 += 8) {
-      float2 v[8];
-      float r[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int t = threadIdx.x + (q0 + q) * kNt;
-        v[q] = __ldg(sp + t);
-        r[q] = __ldg(rs + kRs * t);
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) buf[sidx(threadIdx.x + (q0 + q) * kNt)] = cscale(v[q], rscale * r[q]);
-    }
-    __syncthreads();
-  } else {
+  {
   // Gather-sum of the window straight into the radix-16 first-pass butterfly this thread
   // owns (elements t + r*N/16: consecutive threads read consecutive samples), edges
   // outermost so all 16 sample pairs are in flight at once; per element the sum runs in
@@ -351,20 +331,12 @@ __global__ void __launch_bounds__(EqWin<LOG>::kThreads, EqWin<LOG>::kMinBlocks) 
   fft_first_from_regs<-1>(v, buf, threadIdx.x);
   __syncthreads();
   fft_middle<LOG, 1, kNt, -1>(buf, padded(kEqFft), a.tw);
-  // Last forward pass into registers: MODE 1 stores the spectrum, MODE 0 multiplies by the
-  // response and writes the product back (in place: after every thread has read its inputs).
+  // Last forward pass into registers, multiplied by the response and written back (in place:
+  // after every thread has read its inputs).
   constexpr int NS = Pow2Plan<LOG>::kLastNs, R = Pow2Plan<LOG>::kLastR, PL = NS / kNt;
   float2 o[PL][R];
 #pragma unroll
   for (int p = 0; p < PL; ++p) fft_last_to_regs<LOG, -1>(buf, threadIdx.x + p * kNt, a.tw, o[p]);
-  if constexpr (MODE == 1) {
-#pragma unroll
-    for (int p = 0; p < PL; ++p) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) sp[threadIdx.x + p * kNt + r * NS] = o[p][r];
-    }
-    return;
-  }
   __syncthreads();
 #pragma unroll
   for (int p = 0; p < PL; ++p) {
@@ -404,7 +376,7 @@ void eq_setup() {
   static const bool done = [] {
     cudaFuncSetAttribute(eq_response, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqSmem);
     cudaFuncSetAttribute(eq_response_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, kBasisSmem);
-    for (auto fn : {eq_conv<0, 13>, eq_conv<1, 13>, eq_conv<2, 13>, eq_conv<0, 12>}) {
+    for (auto fn : {eq_conv<13>, eq_conv<12>}) {
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqSmem);
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     }
@@ -444,9 +416,7 @@ const float* eq_basis(int device) {
 void launch_eq_prologue(const StepArgs& a, float* taps_ws, float* resp_ws, cudaStream_t s) {
   if (a.slots == 0) return;
   eq_setup();
-  // MGB_EQ_FFT_DESIGN=1: the per-render fp64 design + 8192-point FFT (diagnostics / A-B).
-  static const bool fft_design = [] { const char* v = std::getenv("MGB_EQ_FFT_DESIGN"); return v && v[0] == '1'; }();
-  if (!fft_design && a.slots >= kBasisMinSlots) {
+  if (a.slots >= kBasisMinSlots) {
     int dev = 0;
     cudaGetDevice(&dev);
     note_prologue_kernel(reinterpret_cast<const void*>(eq_mag_tiles));
@@ -465,10 +435,6 @@ void launch_eq_prologue(const StepArgs& a, float* taps_ws, float* resp_ws, cudaS
   eq_mags<<<a.slots, kEqHalf + 1, 0, s>>>(a.params, mags);
   eq_design<<<dim3(1024 / (256 / kDesignSplit * kDesignTpw), a.slots), 256, 0, s>>>(mags, taps_ws, cos_table(a.tw));
   eq_response<<<a.slots, 512, kEqSmem, s>>>(taps_ws, resp_ws, a.tw);
-}
-
-std::size_t eq_spectrum_bytes(int slots, int batch, long length) {
-  return sizeof(float2) * kEqFft * static_cast<std::size_t>(slots) * batch * ((length + kEqOut - 1) / kEqOut);
 }
 
 namespace {
@@ -497,22 +463,10 @@ void launch_eq_main(const StepArgs& a, const float* resp_ws, cudaStream_t s) {
   if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
   eq_setup();
   if (eq_uses_small_window(a)) {
-    eq_conv<0, 12><<<eq_grid<12>(a), EqWin<12>::kThreads, EqWin<12>::kSmem, s>>>(a, resp_ws, nullptr);
+    eq_conv<12><<<eq_grid<12>(a), EqWin<12>::kThreads, EqWin<12>::kSmem, s>>>(a, resp_ws);
     return;
   }
-  eq_conv<0, 13><<<eq_grid<13>(a), 512, kEqSmem, s>>>(a, resp_ws, nullptr);
-}
-
-void launch_eq_forward(const StepArgs& a, float2* spectrum, cudaStream_t s) {
-  if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
-  eq_setup();
-  eq_conv<1, 13><<<eq_grid<13>(a), 512, kEqSmem, s>>>(a, nullptr, spectrum);
-}
-
-void launch_eq_inverse(const StepArgs& a, const float* resp_ws, const float2* spectrum, cudaStream_t s) {
-  if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
-  eq_setup();
-  eq_conv<2, 13><<<eq_grid<13>(a), 512, kEqSmem, s>>>(a, resp_ws, const_cast<float2*>(spectrum));
+  eq_conv<13><<<eq_grid<13>(a), 512, kEqSmem, s>>>(a, resp_ws);
 }
 
 }  // namespace mgb

@@ -29,18 +29,14 @@ namespace {
 
 constexpr int kColElems = 8192;  // complex elements per column tile (64 KiB)
 constexpr int kColThreads = 512;
-#ifndef MGB_RCONV_PREFETCH
-// rows_conv kernel-spectrum staging: 0 loaded at use (default: no registers held across the
-// forward transform, no spills; measured fastest), 1 registers (issued early; spills),
-// 2 cp.async into shared memory (no registers held across the forward transform)
-#define MGB_RCONV_PREFETCH 0
-#endif
-#ifndef MGB_RCONV_THREADS_PER_SM
-#define MGB_RCONV_THREADS_PER_SM 1024  // resident rows_conv threads per SM the register budget is sized for
-#endif
-#ifndef MGB_RBWD_MINB
-#define MGB_RBWD_MINB 2  // resident CTAs per SM rows_bwd is compiled for (3: spills, measured slower)
-#endif
+// Resident rows_conv threads per SM the register budget is sized for. The kernel spectrum is
+// loaded where it is used (prefetching it into registers spilled; cp.async into shared memory
+// measured no faster).
+constexpr int kRconvThreadsPerSm = 1024;
+// Resident CTAs per SM rows_bwd is compiled for: 2 up to 256-point rows (3 spills, measured
+// slower); 1 from 1024 points, whose 256/512 threads need more than 128/64 registers.
+template <int LN2>
+constexpr int rbwd_min_blocks() { return LN2 >= 10 ? 1 : 2; }
 
 inline std::size_t align256(std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255); }
 
@@ -78,11 +74,30 @@ __device__ __forceinline__ float delay_tap_sum(const float* rec, int c, long i, 
 // the multitap delay kernel synthesised from its tap records (no dense IR in memory).
 enum class ColSrc { Kernel, Signal, DelayTaps };
 
+// Segmented overlap-save (launch.hpp ConvGeom): item = (slot*batch + b)*nseg + j, segment j
+// transforms x[base_j, base_j + N), base_j = max(0, j*seg - pre), and owns the outputs
+// [j*seg, (j+1)*seg). item0: first item of this launch (grids are chunked at 65535 in y).
+struct SegArgs {
+  long seg;
+  long pre;
+  int nseg;
+  int item0;
+  int mask_out;  // gather only the segment's own output samples (dY of the kernel gradient)
+};
+SegArgs seg_args(const ConvGeom& g, int item0 = 0, bool mask_out = false) {
+  return SegArgs{g.seg, g.pre, g.nseg, item0, mask_out ? 1 : 0};
+}
+__host__ __device__ __forceinline__ long seg_base(long seg, long pre, long j) {
+  const long b = j * seg - pre;
+  return b > 0 ? b : 0;
+}
+constexpr int kMaxGridY = 65535;
+
 // ---- pass 1: column FFTs (forward) ------------------------------------------------------
 // grid (N2 / C, items); item = slot (kernel) or slot*B + b (signal).
 template <int LN1, ColSrc SRC>
 __global__ void __launch_bounds__(kColThreads, 2) cols_fwd(StepArgs a, const float2* ir, long taps, int log_n,
-                                                        float2* out, int window) {
+                                                        float2* out, int window, SegArgs sg) {
   constexpr int N1 = 1 << LN1;
   constexpr int C = kColElems / N1;
   constexpr int FS = padded(N1) + 1;
@@ -90,16 +105,20 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_fwd(StepArgs a, const flo
   const int log_n2 = log_n - LN1;
   const long N2 = 1L << log_n2;
   const long N = 1L << log_n;
-  const int item = blockIdx.y;
+  const int item = sg.item0 + blockIdx.y;
   const long col0 = static_cast<long>(blockIdx.x) * C;
   int slot = item, b = 0, e0 = 0, e1 = 0;
-  long len = taps;
+  long base = 0, lo = 0, hi = taps;  // sample m = base + n is loaded when lo <= m < hi
   if constexpr (SRC == ColSrc::Signal) {
-    slot = item / a.batch;
-    b = item - slot * a.batch;
+    const int isb = item / sg.nseg, j = item - isb * sg.nseg;
+    slot = isb / a.batch;
+    b = isb - slot * a.batch;
     e0 = slot_e0(a, slot);
     e1 = slot_e1(a, slot);
-    len = a.length;
+    base = seg_base(sg.seg, sg.pre, j);
+    const long first = static_cast<long>(j) * sg.seg;
+    lo = sg.mask_out ? first : base;
+    hi = min(first + sg.seg, a.length);
   }
   __shared__ float rec[SRC == ColSrc::DelayTaps ? kTaps * kTapRec : 1];
   if constexpr (SRC == ColSrc::DelayTaps) {
@@ -119,10 +138,11 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_fwd(StepArgs a, const flo
     const int idx = threadIdx.x + q * kColThreads;
     const int c = idx % C, n1 = idx / C;
     const long n = static_cast<long>(n1) * N2 + col0 + c;
+    const long m = base + n;
     float2 v = make_float2(0.f, 0.f);
-    if (n < len) {
+    if (m >= lo && m < hi) {
       if constexpr (SRC == ColSrc::Signal) {
-        v = one ? make_float2(__ldg(one + n), __ldg(one + a.length + n)) : gather2(a, e0, e1, b, n);
+        v = one ? make_float2(__ldg(one + m), __ldg(one + a.length + m)) : gather2(a, e0, e1, b, m);
       } else if constexpr (SRC == ColSrc::DelayTaps) {
         v = make_float2(delay_tap_sum(rec, 0, n, window), delay_tap_sum(rec, 1, n, window));
       } else {
@@ -162,16 +182,21 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_fwd(StepArgs a, const flo
 }
 
 // ---- pass 3 (last): inverse column FFTs, store into the arena --------------------------
-template <int LN1>
-__global__ void __launch_bounds__(kColThreads, 2) cols_inv(StepArgs a, int log_n, const float2* X) {
+// BUF: the whole transform goes back into the item's own spectrum in natural order (in place:
+// a CTA owns its columns, and all its loads are consumed before its stores) for conv_ola.
+template <int LN1, bool BUF>
+__global__ void __launch_bounds__(kColThreads, 2) cols_inv(StepArgs a, int log_n, float2* X, SegArgs sg) {
   constexpr int N1 = 1 << LN1;
   constexpr int C = kColElems / N1;
   constexpr int FS = padded(N1) + 1;
   extern __shared__ float2 tile[];
   const long N2 = 1L << (log_n - LN1);
   const long N = 1L << log_n;
-  const int item = blockIdx.y;
-  const int slot = item / a.batch, b = item - slot * a.batch;
+  const int item = sg.item0 + blockIdx.y;
+  const int isb = item / sg.nseg, jseg = item - isb * sg.nseg;
+  const int slot = isb / a.batch, b = isb - slot * a.batch;
+  const long base = seg_base(sg.seg, sg.pre, jseg);
+  const long first = static_cast<long>(jseg) * sg.seg, end = min(first + sg.seg, a.length);
   const long col0 = static_cast<long>(blockIdx.x) * C;
   const float2* x = X + static_cast<long>(item) * N;
   constexpr int EPT = kColElems / kColThreads;
@@ -199,12 +224,36 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_inv(StepArgs a, int log_n
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const long n = static_cast<long>(j + r * NS) * N2 + col0 + c;
-      if (n < a.length) {
-        yl[n] = v[r].x;
-        yr[n] = v[r].y;
+      if constexpr (BUF) {
+        X[static_cast<long>(item) * N + n] = v[r];
+      } else {
+        const long m = base + n;
+        if (m >= first && m < end) {
+          yl[m] = v[r].x;
+          yr[m] = v[r].y;
+        }
       }
     }
   }
+}
+
+// Overlap-add of the segments' input-gradient contributions (backward, nseg > 1): segment j
+// contributes to samples [base_j, (j+1)*seg); each sample sums its segments in order j = m/seg,
+// ..., (m+pre)/seg (fixed order, deterministic). grid (ceil(L/256), slots*batch chunk).
+__global__ void __launch_bounds__(256) conv_ola(StepArgs a, SegArgs sg, long N, const float2* buf) {
+  const long m = static_cast<long>(blockIdx.x) * 256 + threadIdx.x;
+  if (m >= a.length) return;
+  const int isb = sg.item0 + blockIdx.y;
+  const int slot = isb / a.batch, b = isb - slot * a.batch;
+  long jhi = (m + sg.pre) / sg.seg;
+  if (jhi > sg.nseg - 1) jhi = sg.nseg - 1;
+  float2 acc = make_float2(0.f, 0.f);
+  for (long j = m / sg.seg; j <= jhi; ++j) {
+    acc = cadd(acc, __ldg(buf + (static_cast<long>(isb) * sg.nseg + j) * N + (m - seg_base(sg.seg, sg.pre, j))));
+  }
+  float* y = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length;
+  y[m] = acc.x;
+  y[a.length + m] = acc.y;
 }
 
 // ---- pass 2: row FFTs ---------------------------------------------------------------------
@@ -327,14 +376,15 @@ __global__ void __launch_bounds__(row_threads<LN2, kSpecRows>()) rows_spec(int l
 
 // Signal rows k1 = r and N1 - r together: forward FFTs, channel-split product with the
 // kernel spectrum, inverse FFTs, inverse four-step twiddle. grid (N1/2 + 1, slots*B)
+// `batch`: items per slot (batch * segments); item0: first item of this launch.
 template <int LN2>
-__global__ void __launch_bounds__(row_threads<LN2, 2>(), MGB_RCONV_THREADS_PER_SM / row_threads<LN2, 2>()) rows_conv(int log_n, int batch, float2* X, const float2* P, const float2* tw) {
+__global__ void __launch_bounds__(row_threads<LN2, 2>(), kRconvThreadsPerSm / row_threads<LN2, 2>()) rows_conv(int log_n, int batch, float2* X, const float2* P, const float2* tw, int item0) {
   constexpr int N2 = 1 << LN2;
   constexpr int NT = row_threads<LN2, 2>();
   extern __shared__ float2 rows[];  // [2][N2]
   const long N = 1L << log_n;
   const int N1 = static_cast<int>(N >> LN2);
-  const int item = blockIdx.y;
+  const int item = item0 + blockIdx.y;
   const int slot = item / batch;
   const int ra = blockIdx.x, rb = (N1 - ra) & (N1 - 1);
   const bool self = ra == rb;
@@ -343,36 +393,8 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), MGB_RCONV_THREADS_PER_S
   const float2* pa = P + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
   const float2* pb = P + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
   constexpr int RS = padded(N2);  // second row's offset
-  // The kernel spectrum values this thread pairs are issued early, so their latency hides
-  // behind the row loads and the forward FFT.
   constexpr int KPT = N2 / NT;
   static_assert(KPT * NT == N2, "rows_conv: threads must tile a row");
-#if MGB_RCONV_PREFETCH == 1
-  float2 pkv[KPT], pov[KPT];
-#define MGB_PREFETCH_KERNEL_SPECTRUM()                                  \
-  _Pragma("unroll") for (int q = 0; q < KPT; ++q) {                    \
-    const int k = threadIdx.x + q * NT;                                \
-    const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);     \
-    pkv[q] = __ldg(pa + k);                                            \
-    pov[q] = __ldg(pb + kb);                                           \
-  }
-#elif MGB_RCONV_PREFETCH == 2
-  // Each thread copies exactly the kernel values it pairs later (own cp.async group: no
-  // barrier needed before it reads them back).
-  float2* sp = rows + 2 * RS;
-#define MGB_PREFETCH_KERNEL_SPECTRUM()                                                              \
-  _Pragma("unroll") for (int q = 0; q < KPT; ++q) {                                                \
-    const int k = threadIdx.x + q * NT;                                                            \
-    const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);                                 \
-    const unsigned da = static_cast<unsigned>(__cvta_generic_to_shared(sp + sidx(k)));              \
-    const unsigned db = static_cast<unsigned>(__cvta_generic_to_shared(sp + RS + sidx(k)));         \
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(da), "l"(pa + k) : "memory");  \
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(db), "l"(pb + kb) : "memory"); \
-  }                                                                                                \
-  asm volatile("cp.async.commit_group;" ::: "memory");
-#else
-#define MGB_PREFETCH_KERNEL_SPECTRUM()
-#endif
   // Register-ended transforms when the threads are exactly the first pass's butterflies
   // (every LN2 >= 8): thread t loads the 16 inputs j + r*N2/16 of row t / (N2/16) and runs
   // that radix-16 butterfly from registers; the inverse's last pass writes global memory.
@@ -386,11 +408,9 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), MGB_RCONV_THREADS_PER_S
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = src[j + r * M1];
     fft_first_from_regs<-1>(v, rows + w * RS, j);
-    MGB_PREFETCH_KERNEL_SPECTRUM()  // after the first pass: its 16 inputs are no longer live
     __syncthreads();
     fft_after_first<LN2, 2, NT, -1>(rows, RS, tw);
   } else {
-    MGB_PREFETCH_KERNEL_SPECTRUM()
     constexpr int PER = N2 / NT;
     static_assert(PER * NT == N2, "rows_conv: threads must tile a row");
     float2 va[PER], vb[PER];  // loads in flight before any smem store
@@ -407,11 +427,7 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), MGB_RCONV_THREADS_PER_S
     __syncthreads();
     fft_pow2<LN2, 2, NT, -1>(rows, RS, tw);
   }
-#undef MGB_PREFETCH_KERNEL_SPECTRUM
   const float s = 0.25f / static_cast<float>(N);
-#if MGB_RCONV_PREFETCH == 2
-  asm volatile("cp.async.wait_all;" ::: "memory");
-#endif
 #pragma unroll
   for (int q = 0; q < KPT; ++q) {
     const int k = threadIdx.x + q * NT;
@@ -419,13 +435,7 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), MGB_RCONV_THREADS_PER_S
     const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
     if (self && kb < k) continue;
     const float2 xk = rows[sidx(k)], xo = rows[RS + sidx(kb)];
-#if MGB_RCONV_PREFETCH == 1
-    const float2 pk = pkv[q], po = pov[q];
-#elif MGB_RCONV_PREFETCH == 2
-    const float2 pk = sp[sidx(k)], po = sp[RS + sidx(k)];
-#else
     const float2 pk = __ldg(pa + k), po = __ldg(pb + kb);
-#endif
     const float2 zk = zmix(xk, cconj(xo), pk, cconj(po), s);
     const float2 zo = zmix(xo, cconj(xk), po, cconj(pk), s);
     rows[sidx(k)] = zk;
@@ -466,14 +476,14 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), MGB_RCONV_THREADS_PER_S
 // spectrum never makes a round trip through memory. grid (N1/2 + 1, slots*B)
 template <int LN2>
 __global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_conv_fk(int log_n, int batch, float2* X, const float2* K,
-                                                                  const float2* tw) {
+                                                                  const float2* tw, int item0) {
   constexpr int N2 = 1 << LN2;
   constexpr int NT = row_threads<LN2, 4>();
   constexpr int RS = padded(N2);
   extern __shared__ float2 rows[];  // [4][RS]: x a, x b, k a, k b
   const long N = 1L << log_n;
   const int N1 = static_cast<int>(N >> LN2);
-  const int item = blockIdx.y;
+  const int item = item0 + blockIdx.y;
   const int slot = item / batch;
   const int ra = blockIdx.x, rb = (N1 - ra) & (N1 - 1);
   const bool self = ra == rb;
@@ -546,70 +556,94 @@ __global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_conv_fk(int log_n,
 }
 
 // ---- dispatch -----------------------------------------------------------------------------
-template <int LN1>
-void cols_fwd_t(ColSrc src, const StepArgs& a, const float2* ir, long taps, const ConvGeom& g, int items,
-                float2* out, int window, cudaStream_t s) {
-  constexpr int C = kColElems / (1 << LN1);
-  constexpr int smem = C * (padded(1 << LN1) + 1) * 8;
-  const dim3 grid(static_cast<unsigned>((1L << g.log_n2) / C), static_cast<unsigned>(items));
-  static const bool attrs_set = [] {
-    cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::Signal>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::Kernel>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::Signal>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::Kernel>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::DelayTaps>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(cols_fwd<LN1, ColSrc::DelayTaps>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    return true;
-  }();
-  (void)attrs_set;
-  if (src == ColSrc::Signal) {
-    cols_fwd<LN1, ColSrc::Signal><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out, window);
-  } else if (src == ColSrc::DelayTaps) {
-    note_prologue_kernel(reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::DelayTaps>));
-    cols_fwd<LN1, ColSrc::DelayTaps><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out, window);
-  } else {
-    note_prologue_kernel(reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::Kernel>));
-    cols_fwd<LN1, ColSrc::Kernel><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out, window);
-  }
+// Launches over `items` grid rows in chunks of at most kMaxGridY (grid.y limit).
+template <typename F>
+void for_item_chunks(int items, F&& f) {
+  for (int i0 = 0; i0 < items; i0 += kMaxGridY) f(i0, items - i0 < kMaxGridY ? items - i0 : kMaxGridY);
 }
 
 template <int LN1>
-void cols_inv_t(const StepArgs& a, const ConvGeom& g, const float2* X, cudaStream_t s) {
+void cols_fwd_t(ColSrc src, const StepArgs& a, const float2* ir, long taps, const ConvGeom& g, int items,
+                float2* out, int window, bool mask_out, cudaStream_t s) {
   constexpr int C = kColElems / (1 << LN1);
   constexpr int smem = C * (padded(1 << LN1) + 1) * 8;
-  const dim3 grid(static_cast<unsigned>((1L << g.log_n2) / C), static_cast<unsigned>(a.slots * a.batch));
+  static const bool attrs_set = [] {
+    for (const void* fn : {reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::Signal>),
+                           reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::Kernel>),
+                           reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::DelayTaps>)}) {
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
+    return true;
+  }();
+  (void)attrs_set;
+  if (src == ColSrc::DelayTaps) note_prologue_kernel(reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::DelayTaps>));
+  if (src == ColSrc::Kernel) note_prologue_kernel(reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::Kernel>));
+  for_item_chunks(items, [&](int i0, int n) {
+    const dim3 grid(static_cast<unsigned>((1L << g.log_n2) / C), static_cast<unsigned>(n));
+    const SegArgs sg = seg_args(g, i0, mask_out);
+    if (src == ColSrc::Signal) {
+      cols_fwd<LN1, ColSrc::Signal><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out, window, sg);
+    } else if (src == ColSrc::DelayTaps) {
+      cols_fwd<LN1, ColSrc::DelayTaps><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out, window, sg);
+    } else {
+      cols_fwd<LN1, ColSrc::Kernel><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out, window, sg);
+    }
+  });
+}
+
+template <int LN1>
+void cols_inv_t(const StepArgs& a, const ConvGeom& g, float2* X, bool to_buf, cudaStream_t s) {
+  constexpr int C = kColElems / (1 << LN1);
+  constexpr int smem = C * (padded(1 << LN1) + 1) * 8;
   static const bool done = [] {
-    cudaFuncSetAttribute(cols_inv<LN1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(cols_inv<LN1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    for (const void* fn : {reinterpret_cast<const void*>(cols_inv<LN1, false>), reinterpret_cast<const void*>(cols_inv<LN1, true>)}) {
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
     return true;
   }();
   (void)done;
-  cols_inv<LN1><<<grid, kColThreads, smem, s>>>(a, g.log_n, X);
+  for_item_chunks(a.slots * a.batch * g.nseg, [&](int i0, int n) {
+    const dim3 grid(static_cast<unsigned>((1L << g.log_n2) / C), static_cast<unsigned>(n));
+    if (to_buf) cols_inv<LN1, true><<<grid, kColThreads, smem, s>>>(a, g.log_n, X, seg_args(g, i0));
+    else cols_inv<LN1, false><<<grid, kColThreads, smem, s>>>(a, g.log_n, X, seg_args(g, i0));
+  });
 }
 
 template <int LN2>
 void rows_spec_t(const ConvGeom& g, int slots, float2* P, const float2* tw, cudaStream_t s) {
-  const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / kSpecRows), static_cast<unsigned>(slots));
+  constexpr int smem = kSpecRows * padded(1 << LN2) * 8;
+  static const bool done = [] {
+    cudaFuncSetAttribute(rows_spec<LN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    return true;
+  }();
+  (void)done;
   note_prologue_kernel(reinterpret_cast<const void*>(rows_spec<LN2>));
-  rows_spec<LN2><<<grid, row_threads<LN2, kSpecRows>(), kSpecRows * padded(1 << LN2) * 8, s>>>(g.log_n, P, tw);
+  for (int s0 = 0; s0 < slots; s0 += kMaxGridY) {
+    const int n = slots - s0 < kMaxGridY ? slots - s0 : kMaxGridY;
+    const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / kSpecRows), static_cast<unsigned>(n));
+    rows_spec<LN2><<<grid, row_threads<LN2, kSpecRows>(), smem, s>>>(g.log_n, P + static_cast<long>(s0) * g.n, tw);
+  }
 }
 
 template <int LN2>
-void rows_conv_t(const ConvGeom& g, int items, int batch, float2* X, const float2* P, const float2* tw,
+void rows_conv_t(const ConvGeom& g, int items, int per_slot, float2* X, const float2* P, const float2* tw,
                  cudaStream_t s) {
-  constexpr int smem = (MGB_RCONV_PREFETCH == 2 ? 4 : 2) * padded(1 << LN2) * 8;
+  constexpr int smem = 2 * padded(1 << LN2) * 8;
   static const bool done = [] {
     cudaFuncSetAttribute(rows_conv<LN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return true;
   }();
   (void)done;
-  const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(items));
-  rows_conv<LN2><<<grid, row_threads<LN2, 2>(), smem, s>>>(g.log_n, batch, X, P, tw);
+  for_item_chunks(items, [&](int i0, int n) {
+    const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(n));
+    rows_conv<LN2><<<grid, row_threads<LN2, 2>(), smem, s>>>(g.log_n, per_slot, X, P, tw, i0);
+  });
 }
 
-
 template <int LN2>
-void rows_conv_fk_t(const ConvGeom& g, int items, int batch, float2* X, const float2* K, const float2* tw,
+void rows_conv_fk_t(const ConvGeom& g, int items, int per_slot, float2* X, const float2* K, const float2* tw,
                     cudaStream_t s) {
   constexpr int smem = 4 * padded(1 << LN2) * 8;
   static const bool done = [] {
@@ -617,10 +651,13 @@ void rows_conv_fk_t(const ConvGeom& g, int items, int batch, float2* X, const fl
     return true;
   }();
   (void)done;
-  const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(items));
-  rows_conv_fk<LN2><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, batch, X, K, tw);
+  for_item_chunks(items, [&](int i0, int n) {
+    const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(n));
+    rows_conv_fk<LN2><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, per_slot, X, K, tw, i0);
+  });
 }
 
+// log2 of the column length N1 = 2^(a/2) and row length N2 = 2^(a - a/2), a in [13, 22].
 #define MGB_DISPATCH_LN(var, FN, ...)                  \
   switch (var) {                                       \
     case 6: FN<6>(__VA_ARGS__); break;                 \
@@ -629,14 +666,13 @@ void rows_conv_fk_t(const ConvGeom& g, int items, int batch, float2* X, const fl
     case 9: FN<9>(__VA_ARGS__); break;                 \
     case 10: FN<10>(__VA_ARGS__); break;               \
     case 11: FN<11>(__VA_ARGS__); break;               \
-    case 12: FN<12>(__VA_ARGS__); break;               \
     default: throw std::invalid_argument("fft convolution size out of range"); \
   }
 
 // Kernel spectrum P (four-step order) of the packed kernels in `ir` ([slots][taps]).
 void kernel_spectrum(ColSrc src, const StepArgs& a, const ConvGeom& g, const float2* ir, long taps, int window,
                      float2* P, cudaStream_t s) {
-  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, src, a, ir, taps, g, a.slots, P, window, s);
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, src, a, ir, taps, g, a.slots, P, window, false, s);
   // Large steps leave the row stage to rows_conv_fk (conv_fuse_kernel_rows).
   if (!conv_fuse_kernel_rows(g, a.slots)) MGB_DISPATCH_LN(g.log_n2, rows_spec_t, g, a.slots, P, a.tw, s);
 }
@@ -806,17 +842,18 @@ __global__ void __launch_bounds__(256) delay_dense(const float* taps, DelayConst
 //  * the kernel-gradient spectrum sum_b DY_c conj(X_c), packed C_L + i C_R (both real):
 //    conj(X_c) is the spectrum of x_c reversed, whose packed form is Z[N-k], so the same
 //    product with X's pair swapped; inverted into X's b = 0 item at the end.
-// grid (N1/2 + 1, slots)
+// `batch`: items per slot (batch * segments: the kernel gradient sums over both).
+// grid (N1/2 + 1, slots chunk from slot0)
 template <int LN2, bool KFFT>
-__global__ void __launch_bounds__(row_threads<LN2, 4>(), MGB_RBWD_MINB) rows_bwd(int log_n, int batch, float2* DY, float2* X,
-                                                                 const float2* P, const float2* tw) {
+__global__ void __launch_bounds__(row_threads<LN2, 4>(), rbwd_min_blocks<LN2>()) rows_bwd(int log_n, int batch, float2* DY, float2* X,
+                                                                 const float2* P, const float2* tw, int slot0) {
   constexpr int N2 = 1 << LN2;
   constexpr int NT = row_threads<LN2, 4>();
   constexpr int RS = padded(N2);
   extern __shared__ float2 rows[];  // [8][RS]: dy a, dy b, x a, x b, h a, h b, acc a, acc b
   const long N = 1L << log_n;
   const int N1 = static_cast<int>(N >> LN2);
-  const int slot = blockIdx.y;
+  const int slot = slot0 + blockIdx.y;
   const int ra = blockIdx.x, rb = (N1 - ra) & (N1 - 1);
   const bool self = ra == rb;
   const float2* pa = P + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
@@ -898,14 +935,14 @@ __global__ void __launch_bounds__(row_threads<LN2, 4>(), MGB_RBWD_MINB) rows_bwd
 // buffer out[slot][taps] (x = left, y = right), first `taps` samples. grid (N2 / C, slots)
 template <int LN1>
 __global__ void __launch_bounds__(kColThreads, 2) cols_inv_buf(int log_n, int batch, const float2* X, float2* out,
-                                                            long taps, const float2* tw) {
+                                                            long taps, const float2* tw, int slot0) {
   constexpr int N1 = 1 << LN1;
   constexpr int C = kColElems / N1;
   constexpr int FS = padded(N1) + 1;
   extern __shared__ float2 tile[];
   const long N2 = 1L << (log_n - LN1);
   const long N = 1L << log_n;
-  const int slot = blockIdx.y;
+  const int slot = slot0 + blockIdx.y;
   const long col0 = static_cast<long>(blockIdx.x) * C;
   const float2* x = X + static_cast<long>(slot) * batch * N;
   // Register-ended column transform (as cols_inv): thread (c, j) loads the 16 inputs of its
@@ -1113,19 +1150,43 @@ bool conv_fuse_kernel_rows(const ConvGeom& g, int slots) {
   return sizeof(float2) * static_cast<std::size_t>(slots) * static_cast<std::size_t>(g.n) > (64u << 20);
 }
 
+static int g_conv_log = 0;  // 0 automatic (mg_set_conv_log; tests)
+void set_conv_log(int log_n) { g_conv_log = log_n; }
+
+// Transform size: the single next_pow2(L + taps - 1) transform of the reference when it is the
+// cheapest, else the segment size 2^a (>= taps) minimising nseg * N * (log2 N + 6): FFT flops
+// plus the per-point memory passes. E.g. taps 88,200: L = 2^17 -> one 2^18 transform (as the
+// reference); L = 441,000 (10 s) -> three 2^18 segments instead of one 2^20 transform.
 ConvGeom conv_geom(long length, long taps) {
-  const long full = length + taps - 1;
+  if (taps < 1) taps = 1;
+  const long len = length > 0 ? length : 1;
+  int single = kConvMinLog;
+  while (single < 62 && (1L << single) < len + taps - 1) ++single;
+  const int top = g_conv_log > 0 ? kConvMaxLog : (single < kConvMaxLog ? single : kConvMaxLog);
+  int best = -1;
+  double best_cost = 0.0;
+  for (int a = kConvMinLog; a <= top; ++a) {
+    const long n = 1L << a;
+    if (n < taps) continue;
+    const long seg = n - taps + 1;
+    const double cost = static_cast<double>((len + seg - 1) / seg) * static_cast<double>(n) * (a + 6);
+    if (g_conv_log > 0 ? a == g_conv_log : (best < 0 || cost < best_cost)) {
+      best = a;
+      best_cost = cost;
+    }
+  }
+  if (best < 0) {
+    throw std::invalid_argument(g_conv_log > 0 ? "fft convolution: forced transform size out of range"
+                                               : "fft convolution: kernel longer than 2^22 taps");
+  }
   ConvGeom g;
-  int a = 13;  // N1 * N2 >= one column tile
-  while ((1L << a) < full) ++a;
-  // Longer convolutions need 2^11-point row passes, which do not match the reference yet
-  // (measured on B200: wrong delay output, reverb launch failure at L = 2^20 + 64); refuse them
-  // loudly rather than render them wrong.
-  if (a > 20) throw std::invalid_argument("fft convolution: signal too long (L + taps - 1 > 2^20)");
-  g.log_n = a;
-  g.log_n1 = a / 2;
-  g.log_n2 = a - a / 2;
-  g.n = 1L << a;
+  g.log_n = best;
+  g.log_n1 = best / 2;
+  g.log_n2 = best - best / 2;
+  g.n = 1L << best;
+  g.pre = taps - 1;
+  g.seg = g.n - taps + 1;
+  g.nseg = static_cast<int>((len + g.seg - 1) / g.seg);
   return g;
 }
 
@@ -1134,7 +1195,7 @@ std::size_t conv_prologue_bytes(const ConvGeom& g, int slots, long taps) {
 }
 
 std::size_t conv_main_bytes(const ConvGeom& g, int slots, int batch) {
-  return align256(sizeof(float2) * static_cast<std::size_t>(slots) * batch * g.n);
+  return align256(sizeof(float2) * static_cast<std::size_t>(slots) * batch * g.nseg * g.n);
 }
 
 
@@ -1191,22 +1252,23 @@ void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, voi
   const ConvGeom g = conv_geom(a.length, taps);
   const auto* P = reinterpret_cast<const float2*>(static_cast<const char*>(prologue_ws) + ir_bytes(a.slots, taps));
   auto* X = static_cast<float2*>(ws);
-  const int items = a.slots * a.batch;
-  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, a, nullptr, 0, g, items, X, 0, s);
+  const int per_slot = a.batch * g.nseg;
+  const int items = a.slots * per_slot;
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, a, nullptr, 0, g, items, X, 0, false, s);
   // The signal's column pass needs no kernel spectrum: join the prologue only here.
   if (kernel_ready) cudaStreamWaitEvent(s, kernel_ready, 0);
   if (conv_fuse_kernel_rows(g, a.slots)) {
-    MGB_DISPATCH_LN(g.log_n2, rows_conv_fk_t, g, items, a.batch, X, P, a.tw, s);
+    MGB_DISPATCH_LN(g.log_n2, rows_conv_fk_t, g, items, per_slot, X, P, a.tw, s);
   } else {
-    MGB_DISPATCH_LN(g.log_n2, rows_conv_t, g, items, a.batch, X, P, a.tw, s);
+    MGB_DISPATCH_LN(g.log_n2, rows_conv_t, g, items, per_slot, X, P, a.tw, s);
   }
-  MGB_DISPATCH_LN(g.log_n1, cols_inv_t, a, g, X, s);
+  MGB_DISPATCH_LN(g.log_n1, cols_inv_t, a, g, X, false, s);
 }
 
 
 namespace {
 template <int LN2>
-void rows_bwd_t(const ConvGeom& g, int slots, int batch, float2* DY, float2* X, const float2* P, bool kfft,
+void rows_bwd_t(const ConvGeom& g, int slots, int per_slot, float2* DY, float2* X, const float2* P, bool kfft,
                 const float2* tw, cudaStream_t s) {
   constexpr int smem = 8 * padded(1 << LN2) * 8;
   static const bool done = [] {
@@ -1215,13 +1277,15 @@ void rows_bwd_t(const ConvGeom& g, int slots, int batch, float2* DY, float2* X, 
     return true;
   }();
   (void)done;
-  const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(slots));
-  if (kfft) rows_bwd<LN2, true><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, batch, DY, X, P, tw);
-  else rows_bwd<LN2, false><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, batch, DY, X, P, tw);
+  for_item_chunks(slots, [&](int s0, int n) {
+    const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(n));
+    if (kfft) rows_bwd<LN2, true><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, per_slot, DY, X, P, tw, s0);
+    else rows_bwd<LN2, false><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, per_slot, DY, X, P, tw, s0);
+  });
 }
 
 template <int LN1>
-void cols_inv_buf_t(const ConvGeom& g, int slots, int batch, const float2* X, float2* out, long taps, const float2* tw,
+void cols_inv_buf_t(const ConvGeom& g, int slots, int per_slot, const float2* X, float2* out, long taps, const float2* tw,
                     cudaStream_t s) {
   constexpr int C = kColElems / (1 << LN1);
   constexpr int smem = C * (padded(1 << LN1) + 1) * 8;
@@ -1230,13 +1294,15 @@ void cols_inv_buf_t(const ConvGeom& g, int slots, int batch, const float2* X, fl
     return true;
   }();
   (void)done;
-  const dim3 grid(static_cast<unsigned>((1L << g.log_n2) / C), static_cast<unsigned>(slots));
-  cols_inv_buf<LN1><<<grid, kColThreads, smem, s>>>(g.log_n, batch, X, out, taps, tw);
+  for_item_chunks(slots, [&](int s0, int n) {
+    const dim3 grid(static_cast<unsigned>((1L << g.log_n2) / C), static_cast<unsigned>(n));
+    cols_inv_buf<LN1><<<grid, kColThreads, smem, s>>>(g.log_n, per_slot, X, out, taps, tw, s0);
+  });
 }
 }  // namespace
 
 std::size_t conv_bwd_bytes(const ConvGeom& g, int slots, int batch, long taps, int rev_frames) {
-  const std::size_t spec = align256(sizeof(float2) * static_cast<std::size_t>(slots) * batch * g.n);
+  const std::size_t spec = align256(sizeof(float2) * static_cast<std::size_t>(slots) * batch * g.nseg * g.n);
   const std::size_t blocks = static_cast<std::size_t>((rev_frames + kRevFpc - 1) / kRevFpc);
   return 2 * spec + align256(sizeof(float2) * static_cast<std::size_t>(slots) * taps) +
          align256(sizeof(double) * static_cast<std::size_t>(slots) * blocks * 4 * kRevBins);
@@ -1250,18 +1316,29 @@ void launch_conv_backward(bool reverb, const StepArgs& fw, const StepArgs& bw, c
   const auto* P = reinterpret_cast<const float2*>(static_cast<const char*>(prologue_ws) + ir_bytes(fw.slots, taps));
   // A large step's forward left the kernel spectrum at its column stage (rows_bwd transforms it).
   const bool kfft = conv_fuse_kernel_rows(g, fw.slots);
-  const int items = fw.slots * fw.batch;
+  const int per_slot = fw.batch * g.nseg;
+  const int items = fw.slots * per_slot;
   const std::size_t spec = align256(sizeof(float2) * static_cast<std::size_t>(items) * g.n);
   auto* DY = static_cast<float2*>(ws);
   auto* X = reinterpret_cast<float2*>(static_cast<char*>(ws) + spec);
   auto* dh = reinterpret_cast<float2*>(static_cast<char*>(ws) + 2 * spec);
   auto* part = reinterpret_cast<double*>(static_cast<char*>(ws) + 2 * spec +
                                          align256(sizeof(float2) * static_cast<std::size_t>(fw.slots) * taps));
-  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, bw, nullptr, 0, g, items, DY, 0, s);
-  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, fw, nullptr, 0, g, items, X, 0, s);
-  MGB_DISPATCH_LN(g.log_n2, rows_bwd_t, g, fw.slots, fw.batch, DY, X, P, kfft, fw.tw, s);
-  MGB_DISPATCH_LN(g.log_n1, cols_inv_t, bw, g, DY, s);
-  MGB_DISPATCH_LN(g.log_n1, cols_inv_buf_t, g, fw.slots, fw.batch, X, dh, taps, fw.tw, s);
+  // dY masked to each segment's own outputs (kernel gradient), x laid out as in the forward.
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, bw, nullptr, 0, g, items, DY, 0, true, s);
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, fw, nullptr, 0, g, items, X, 0, false, s);
+  MGB_DISPATCH_LN(g.log_n2, rows_bwd_t, g, fw.slots, per_slot, DY, X, P, kfft, fw.tw, s);
+  if (g.nseg == 1) {
+    MGB_DISPATCH_LN(g.log_n1, cols_inv_t, bw, g, DY, false, s);
+  } else {
+    // Each segment's correlation with the kernel covers [base_j, (j+1)*seg): overlap-add.
+    MGB_DISPATCH_LN(g.log_n1, cols_inv_t, bw, g, DY, true, s);
+    for_item_chunks(fw.slots * fw.batch, [&](int i0, int n) {
+      const dim3 grid(static_cast<unsigned>((fw.length + 255) / 256), static_cast<unsigned>(n));
+      conv_ola<<<grid, 256, 0, s>>>(bw, seg_args(g, i0), g.n, DY);
+    });
+  }
+  MGB_DISPATCH_LN(g.log_n1, cols_inv_buf_t, g, fw.slots, per_slot, X, dh, taps, fw.tw, s);
   if (reverb) {
     const int blocks = (rc.frames + kRevFpc - 1) / kRevFpc;
     static const bool done = [] {

@@ -35,12 +35,6 @@ void launch_eq_prologue(const StepArgs& a, float* taps_ws /*slots*2048*/, float*
 void launch_eq_main(const StepArgs& a, const float* resp_ws, cudaStream_t s);
 // Per-device response basis (1024 x 4128 fp32), built synchronously on first use.
 const float* eq_basis(int device);
-// Split form of launch_eq_main for a step whose prologue is still running: the forward
-// window FFTs (no response needed) go first into `spectrum` (eq_spectrum_bytes), then the
-// response product + inverse once the prologue is done.
-std::size_t eq_spectrum_bytes(int slots, int batch, long length);
-void launch_eq_forward(const StepArgs& a, float2* spectrum, cudaStream_t s);
-void launch_eq_inverse(const StepArgs& a, const float* resp_ws, const float2* spectrum, cudaStream_t s);
 
 // Compressor / noisegate: chained (decoupled look-back) scan of the energy envelope.
 constexpr int kDynThreads = 512;
@@ -61,11 +55,23 @@ void launch_dynamics_backward(bool gate, const StepArgs& fw, const StepArgs& bw,
                               double energy_floor, void* ws, double* grad, cudaStream_t s);
 
 // FFT convolution with a long causal kernel (reverb, delay): four-step FFT of size N.
+// Segmented overlap-save: the signal is cut into `nseg` segments of `seg` output samples;
+// segment j transforms x[base_j, base_j + N) with base_j = max(0, j*seg - pre), pre = taps - 1,
+// and keeps its outputs [j*seg, (j+1)*seg). One segment (seg >= L) is the reference's single
+// next_pow2(L + taps - 1) transform (`dsp.cpp:64-86`); longer signals use several segments of
+// the size that minimises the work, so any length renders with N <= 2^kConvMaxLog.
 struct ConvGeom {
   int log_n = 0, log_n1 = 0, log_n2 = 0;
   long n = 0;
+  long seg = 0;  // output samples per segment (N - taps + 1)
+  long pre = 0;  // taps - 1
+  int nseg = 1;
 };
+constexpr int kConvMinLog = 13;
+constexpr int kConvMaxLog = 22;
 ConvGeom conv_geom(long length, long taps);
+// Tests: force the transform size 2^log (0 = automatic); conv_geom throws when 2^log < taps.
+void set_conv_log(int log_n);
 // Large steps (kernel spectra beyond L2) fuse the kernel's row stage into the signal's row
 // pass instead of a separate prologue pass.
 bool conv_fuse_kernel_rows(const ConvGeom& g, int slots);

@@ -62,6 +62,7 @@ class ProcessorSet {
   std::vector<long> delay_positions(std::span<const double> params, int channel) const;
 
   const DeviceConstants& device() const { return *dev_; }
+  int device_id() const;  // the CUDA device the constants live on
 
  private:
   ProcessorConfig config_;
@@ -219,8 +220,8 @@ class RenderGraph {
 // straight into the arena) or double (converted on the device). Host buffers passed to
 // submit() must stay valid (and should be pinned) until sync().
 // Double host audio (the reference's AudioBuffer type) is converted to/from fp32 on host
-// worker threads (`host_threads`; < 0: MGB_PIPELINE_HOST_THREADS, else half the hardware
-// threads up to 8), which halves its PCIe bytes: sources in submit() in 1 MiB chunks whose
+// worker threads (`host_threads`; < 0: half the host's hardware threads per local rank, up
+// to 8), which halves its PCIe bytes: sources in submit() in 1 MiB chunks whose
 // H2D copies start as each chunk is converted, outputs on a completion thread once their D2H
 // landed. A fraction of the sources (1 - kHostFraction) still crosses PCIe as double and is
 // converted on the device, so host memory bandwidth and PCIe work side by side. With

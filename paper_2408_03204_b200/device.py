@@ -56,15 +56,26 @@ class DeviceRenderer:
         self.set_params(rd.flat.params if params is None else params)
 
     def set_params(self, params: Dict[int, np.ndarray]) -> None:
-        """Upload render-order parameter tables (RenderData.reorder_params layout)."""
-        self.tables = {}
+        """Upload render-order parameter tables (RenderData.reorder_params layout).
+
+        After the first upload the tables are rewritten IN PLACE: a captured RenderGraph bakes
+        their device addresses, so a new set must have the same types and shapes (ValueError
+        otherwise; build a new DeviceRenderer for a different table set)."""
+        new = {int(t): torch.as_tensor(np.ascontiguousarray(m, dtype=np.float64).reshape(-1, param_width(int(t))))
+               for t, m in params.items()}
+        if self.tables:
+            if set(new) != set(self.tables) or any(new[t].shape != self.tables[t].shape for t in new):
+                raise ValueError("DeviceRenderer.set_params: parameter tables must keep their types and shapes "
+                                 "(captured render graphs hold their addresses)")
+            for t, a in new.items():
+                self.tables[t].copy_(a)
+            return
         for t in range(NUM_NODE_TYPES):
             self._ptrs[t] = None
-        for t, m in params.items():
-            a = torch.as_tensor(np.ascontiguousarray(m, dtype=np.float64).reshape(-1, param_width(t)))
+        for t, a in new.items():
             d = a.to(self.device)
-            self.tables[int(t)] = d
-            self._ptrs[int(t)] = d.data_ptr()
+            self.tables[t] = d
+            self._ptrs[t] = d.data_ptr()
 
     @property
     def sources(self) -> torch.Tensor:
@@ -171,11 +182,12 @@ class RenderPipeline:
     copies of render i+1 overlap the kernels of render i. `dtype` is the host audio type
     (np.float32: copied straight into the arena; np.float64: reference AudioBuffer precision,
     converted to fp32 on host worker threads in 1 MiB chunks whose H2D copies start as each
-    chunk is done — half the PCIe bytes; MGB_PIPELINE_HOST_THREADS=0 sends double and
-    converts on the device instead). Host arrays should be pinned (see `pinned`) and must stay alive
+    chunk is done — half the PCIe bytes; host_threads=0 sends double and converts on the
+    device instead; -1 picks from the host's core count and LOCAL_WORLD_SIZE). Host arrays should be pinned (see `pinned`) and must stay alive
     until sync() — the pipeline keeps references until then."""
 
-    def __init__(self, rd: RenderData, procs: ProcessorSet, batch: int, length: int, dtype=np.float32, depth: int = 2):
+    def __init__(self, rd: RenderData, procs: ProcessorSet, batch: int, length: int, dtype=np.float32, depth: int = 2,
+                 host_threads: int = -1):
         from . import _tables  # noqa: F401
         self.rd, self.procs = rd, procs
         self.batch, self.length = int(batch), int(length)
@@ -184,7 +196,8 @@ class RenderPipeline:
             raise ValueError("RenderPipeline: dtype must be float32 or float64")
         self._h = ctypes.c_void_p()
         _check(_lib.mg_pipeline_create(rd.handle, procs.handle, self.batch, self.length,
-                                       int(self.dtype == np.float32), int(depth), ctypes.byref(self._h)))
+                                       int(self.dtype == np.float32), int(depth), int(host_threads),
+                                       ctypes.byref(self._h)))
         self._keep = []
 
     def pinned(self, shape) -> np.ndarray:
