@@ -207,12 +207,9 @@ double mg_noisegate_gain_log(double g_u, double threshold, double knee_half_widt
 /* check_param_row (processors.cpp:132-149) */
 int32_t mg_check_param_row(int32_t node_type, const double* row);
 
-/* Synthetic workload generators, bit-identical to the reference's: generate_console
- * (console.cpp:10-44), random_legal_params (tests/support/test_util.cpp:63-113, fresh
- * mt19937(seed), tables in original row order), dsp::uniform_noise (dsp.cpp:222-230). */
-int32_t mg_generate_console(int32_t tracks, double prune, uint32_t seed, int32_t* node_types, int32_t cap_nodes,
-                            int32_t* edges, int32_t cap_edges, int32_t* num_nodes, int32_t* num_edges);
-int32_t mg_random_legal_params(const int32_t* node_types, int32_t num_nodes, uint32_t seed, double* const* tables);
+/* default_param_row (graph.cpp:130-155) and dsp::uniform_noise (dsp.cpp:222-230). The
+ * synthetic workload generators (console, random_legal_params) are test/bench support:
+ * workloads/libmgbwork.so, not part of this library. */
 int32_t mg_default_param_row(int32_t node_type, double* row);
 int32_t mg_uniform_noise(int64_t n, uint32_t seed, double* out);
 

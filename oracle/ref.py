@@ -56,6 +56,8 @@ def lib():
         sig("ref_plan_step", _i32, _vp, _i32, _vp, _vp, _vp)
         sig("ref_plan_param_source_rows", _i32, _vp, _i32, _vp)
         sig("ref_render", _i32, _vp, _dbl, _u32, _i32, _dbl, _vp, _vp, _vp, _i32, _i64, _vp, _vp)
+        sig("ref_render_parallel", _i32, _vp, _dbl, _u32, _i32, _dbl, _vp, _vp, _vp, _i32, _i64, _i32, _vp, _i32,
+            _vp, _vp)
         sig("ref_render_reference", _i32, _vp, _i32, _vp, _i32, _dbl, _u32, _i32, _dbl, _vp, _vp, _vp, _i32, _i64, _vp)
         sig("ref_process", _i32, _i32, _vp, _vp, _i32, _i32, _i64, _vp, _i32, _i32, _dbl, _u32, _i32, _dbl)
         sig("ref_reverb_kernel", _i32, _dbl, _u32, _vp, _vp, _vp, ctypes.POINTER(_i64))
@@ -205,6 +207,25 @@ class Plan:
         _check(lib().ref_render(self.h, sample_rate, reverb_seed, envelope_taps, energy_floor, ptrs, _p(rows), _p(src),
                                 b, n, _p(outs), _p(inter)))
         return (outs, inter) if keep_intermediates else outs
+
+    def render_parallel(self, params: Dict[int, np.ndarray], sources: np.ndarray, sample_rate: float = 44100.0,
+                        threads: Optional[int] = None, keep=None, reverb_seed: int = 0, envelope_taps: int = 32768,
+                        energy_floor: float = 1e-7):
+        """render.cpp:14-81 with each step's slots on `threads` host threads (ref_render_parallel:
+        the reference's own gather order and ProcessorSet::process per slot; rows freed after
+        their last reader). Returns outputs, or (outputs, kept) with kept[j] = the row of
+        ORIGINAL node keep[j] (as render()'s intermediates)."""
+        import os
+        src = np.ascontiguousarray(sources, dtype=np.float64)
+        k, b, _, n = src.shape
+        ptrs, rows, _keep = _table_ptrs(params)
+        outs = np.zeros((self.buffer_rows - self.output_begin, b, 2, n))
+        kk = None if keep is None else np.ascontiguousarray(keep, dtype=np.int32)
+        kept = None if kk is None else np.zeros((len(kk), b, 2, n))
+        _check(lib().ref_render_parallel(self.h, sample_rate, reverb_seed, envelope_taps, energy_floor, ptrs, _p(rows),
+                                         _p(src), b, n, int(threads or os.cpu_count() or 1), _p(kk),
+                                         0 if kk is None else len(kk), _p(outs), _p(kept)))
+        return outs if kk is None else (outs, kept)
 
     def __del__(self):
         h, self.h = getattr(self, "h", None), None

@@ -10,6 +10,8 @@
 // (include/mixgraph_b200.h): `tables[t]` points at a row-major [rows[t]][param_width(t)]
 // double matrix for NodeType t (enum order, `proj/include/mixgraph/types.hpp:12-23`), or
 // is NULL when the graph has no node of that type.
+#include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -18,6 +20,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -285,6 +288,99 @@ int ref_render(const void* p, double fs, uint32_t seed, int32_t env_taps, double
     for (std::size_t i = 0; intermediates && i < r.intermediates.size(); ++i) {
       std::memcpy(intermediates + stride * i, r.intermediates[i].samples.data(), sizeof(double) * stride);
     }
+  });
+}
+
+// render.cpp:14-81 restated with each step's slots spread over `threads` host threads, for
+// full-size parity of the large BASELINE configs on the GPU box's cores (test infrastructure).
+// Per slot it runs exactly the reference's arithmetic: the gather sum ((0 + x0) + x1) + ... in
+// gather order (render.cpp:44-48), then ProcessorSet::process on that one slot
+// (processors.cpp:229-282 loops over slots independently; the set is immutable and shared,
+// processors.hpp:24-25). Rows live from their store to their last reader (outputs and the
+// `keep` nodes to the end), so the fp64 arena of a 966-node 10 s graph never exists at once;
+// a row read before any step stored it reads zeros, as the reference's zero-filled buffer.
+// outputs [num_outputs][B][2][L]; kept [n_keep][B][2][L] = rows sigma[keep[j]] (original ids).
+int ref_render_parallel(const void* p, double fs, uint32_t seed, int32_t env_taps, double floor_,
+                        const double* const* tables, const int32_t* rows, const double* sources, int32_t batch,
+                        int64_t length, int32_t threads, const int32_t* keep, int32_t n_keep, double* outputs,
+                        double* kept) {
+  return guarded([&] {
+    const auto* rd = static_cast<const RenderData*>(p);
+    const ProcessorSet& procs = processors_for(fs, seed, env_taps, floor_);
+    const ParamStore params = rd->reorder_params(make_store(tables, rows));
+    const std::size_t stride = static_cast<std::size_t>(batch) * 2 * static_cast<std::size_t>(length);
+    const int nrows = rd->buffer_rows;
+    // last step reading each row; -1: never read
+    std::vector<int> last(static_cast<std::size_t>(nrows), -1);
+    for (std::size_t k = 0; k < rd->steps.size(); ++k) {
+      for (int g : rd->steps[k].gather) last[static_cast<std::size_t>(g)] = static_cast<int>(k);
+    }
+    std::vector<char> pinned(static_cast<std::size_t>(nrows), 0);
+    for (int r = rd->output_begin; r < nrows; ++r) pinned[static_cast<std::size_t>(r)] = 1;
+    for (int j = 0; j < n_keep; ++j) pinned[static_cast<std::size_t>(rd->sigma.at(static_cast<std::size_t>(keep[j])))] = 1;
+    std::vector<std::unique_ptr<double[]>> buf(static_cast<std::size_t>(nrows));
+    for (int k = 0; k < rd->num_inputs; ++k) {
+      buf[static_cast<std::size_t>(k)] = std::make_unique<double[]>(stride);
+      std::memcpy(buf[static_cast<std::size_t>(k)].get(), sources + stride * k, sizeof(double) * stride);
+    }
+    const int nthreads = std::max(1, threads);
+    for (std::size_t k = 0; k < rd->steps.size(); ++k) {
+      const StepIndex& step = rd->steps[k];
+      const int slots = step.store_end - step.store_begin;
+      const ParamMatrix* table = nullptr;
+      if (param_width(step.type) > 0) {
+        auto it = params.tables.find(step.type);
+        if (it == params.tables.end()) throw std::invalid_argument("render: missing parameter table");
+        table = &it->second;
+      }
+      // edge range [first[s], first[s+1]) of each slot (aggregate is non-decreasing)
+      std::vector<std::size_t> first(static_cast<std::size_t>(slots) + 1, step.gather.size());
+      for (std::size_t i = step.gather.size(); i-- > 0;) first[static_cast<std::size_t>(step.aggregate[i])] = i;
+      for (int s = slots - 1; s >= 0; --s) first[static_cast<std::size_t>(s)] = std::min(first[static_cast<std::size_t>(s)], first[static_cast<std::size_t>(s) + 1]);
+      std::vector<std::unique_ptr<double[]>> out(static_cast<std::size_t>(slots));
+      std::atomic<int> next{0};
+      std::mutex err_mu;
+      std::string err;
+      auto work = [&] {
+        std::vector<double> in(stride);
+        for (int s = next.fetch_add(1); s < slots; s = next.fetch_add(1)) {
+          try {
+            std::fill(in.begin(), in.end(), 0.0);
+            for (std::size_t i = first[static_cast<std::size_t>(s)]; i < first[static_cast<std::size_t>(s) + 1]; ++i) {
+              const double* src = buf[static_cast<std::size_t>(step.gather[i])].get();
+              if (!src) continue;  // never stored: the reference's zero-filled row
+              for (std::size_t j = 0; j < stride; ++j) in[j] += src[j];
+            }
+            auto y = std::make_unique<double[]>(stride);
+            std::fill(y.get(), y.get() + stride, 0.0);
+            procs.process(step.type, in.data(), y.get(), 1, batch, static_cast<long>(length), table, step.param_begin + s);
+            out[static_cast<std::size_t>(s)] = std::move(y);
+          } catch (const std::exception& e) {
+            std::scoped_lock lk(err_mu);
+            if (err.empty()) err = e.what();
+          }
+        }
+      };
+      std::vector<std::thread> pool;
+      for (int t = 1; t < std::min(nthreads, slots); ++t) pool.emplace_back(work);
+      work();
+      for (auto& th : pool) th.join();
+      if (!err.empty()) throw std::invalid_argument(err);
+      for (int s = 0; s < slots; ++s) buf[static_cast<std::size_t>(step.store_begin + s)] = std::move(out[static_cast<std::size_t>(s)]);
+      for (int g : step.gather) {
+        if (last[static_cast<std::size_t>(g)] == static_cast<int>(k) && !pinned[static_cast<std::size_t>(g)]) buf[static_cast<std::size_t>(g)].reset();
+      }
+      for (int r = step.store_begin; r < step.store_end; ++r) {
+        if (last[static_cast<std::size_t>(r)] < 0 && !pinned[static_cast<std::size_t>(r)]) buf[static_cast<std::size_t>(r)].reset();
+      }
+    }
+    auto row_or_zero = [&](int r, double* dst) {
+      const double* src = buf[static_cast<std::size_t>(r)].get();
+      if (src) std::memcpy(dst, src, sizeof(double) * stride);
+      else std::fill(dst, dst + stride, 0.0);
+    };
+    for (int r = rd->output_begin; r < nrows; ++r) row_or_zero(r, outputs + stride * (r - rd->output_begin));
+    for (int j = 0; j < n_keep; ++j) row_or_zero(rd->sigma.at(static_cast<std::size_t>(keep[j])), kept + stride * j);
   });
 }
 

@@ -95,8 +95,6 @@ _sig("mg_delay_kernel", _i32, _vp, _vp, _i32, _vp, _vp)
 _sig("mg_compressor_gain_log", _dbl, _dbl, _dbl, _dbl, _dbl)
 _sig("mg_noisegate_gain_log", _dbl, _dbl, _dbl, _dbl, _dbl)
 _sig("mg_check_param_row", _i32, _i32, _vp)
-_sig("mg_generate_console", _i32, _i32, _dbl, _u32, _vp, _i32, _vp, _i32, _P(_i32), _P(_i32))
-_sig("mg_random_legal_params", _i32, _vp, _i32, _u32, _vp)
 _sig("mg_default_param_row", _i32, _i32, _vp)
 _sig("mg_uniform_noise", _i32, _i64, _u32, _vp)
 _sig("mg_graph_to_json", _i32, _vp, _i32, _vp, _i32, _vp, _vp, ctypes.c_char_p, _i64, _P(_i64))
@@ -607,23 +605,6 @@ def render(rd: RenderData, procs: ProcessorSet, params: Optional[Dict[int, np.nd
     return (outs, inter) if keep_intermediates else outs
 
 
-# ---- workload generators (bit-identical to the reference's) ------------------------------------
-
-def generate_console_arrays(tracks: int, prune: float = 0.0, seed: int = 0) -> Tuple[np.ndarray, np.ndarray]:
-    """`console.cpp:10-44` as (types [V], edges [E, 4]) int32 arrays."""
-    cap_n, cap_e = 8 * tracks + 16, 10 * tracks + 16
-    t = np.zeros(cap_n, dtype=np.int32)
-    e = np.zeros((cap_e, 4), dtype=np.int32)
-    nn, ne = _i32(), _i32()
-    _check(_lib.mg_generate_console(tracks, prune, seed, _ptr(t), cap_n, _ptr(e), cap_e, ctypes.byref(nn), ctypes.byref(ne)))
-    return t[:nn.value].copy(), e[:ne.value].copy()
-
-
-def generate_console(tracks: int, prune: float = 0.0, seed: int = 0) -> Graph:
-    """`console.cpp:10-44`."""
-    return Graph.from_arrays(*generate_console_arrays(tracks, prune, seed))
-
-
 def set_conv_fuse(mode: int) -> None:
     """mg_set_conv_fuse: -1 auto (default), 0 separate kernel-spectrum rows pass, 1 fused."""
     _lib.mg_set_conv_fuse(int(mode))
@@ -632,65 +613,6 @@ def set_conv_fuse(mode: int) -> None:
 def set_conv_log(log_n: int) -> None:
     """mg_set_conv_log: 0 automatic segment size (default), 13..22 forces 2^log_n-point segments."""
     _lib.mg_set_conv_log(int(log_n))
-
-
-def generate_large_console_arrays(tracks: int = 64) -> Tuple[np.ndarray, np.ndarray]:
-    """BASELINE config 4's pruning-scale graph (SURVEY.md §8d recipe; not producible by
-    generate_console, which tops out at 8K+6 nodes): per track in -> e c n s g e c n s g (a
-    doubled channel strip), whose last gain feeds the mix bus directly and through two sends
-    (delay -> gain, reverb -> gain); bus mix -> e c s g -> out. 15 nodes and 17 edges per track
-    (64 tracks: 966 nodes, 1093 edges). Insertion order follows console.cpp (per-track nodes,
-    then the bus). Synthetic: no RNG, parameters come from random_legal_params."""
-    if tracks < 1:
-        raise ValueError("generate_large_console: need at least one track")
-    T = NodeType
-    types, edges, sends = [], [], []
-
-    def node(t):
-        types.append(int(t))
-        return len(types) - 1
-
-    def chain(ts):
-        ids = [node(t) for t in ts]
-        for a, b in zip(ids, ids[1:]):
-            edges.append((a, b))
-        return ids[0], ids[-1]
-
-    strip = [T.EQ, T.COMPRESSOR, T.NOISEGATE, T.IMAGER, T.GAIN] * 2
-    for _ in range(tracks):
-        i = node(T.IN)
-        first, last = chain(strip)
-        edges.append((i, first))
-        for fx in (T.DELAY, T.REVERB):
-            s0, s1 = chain([fx, T.GAIN])
-            edges.append((last, s0))
-            sends.append(s1)
-        sends.append(last)
-    bus = node(T.MIX)
-    for s in sends:
-        edges.append((s, bus))
-    b0, b1 = chain([T.EQ, T.COMPRESSOR, T.IMAGER, T.GAIN])
-    edges.append((bus, b0))
-    out = node(T.OUT)
-    edges.append((b1, out))
-    e = np.zeros((len(edges), 4), dtype=np.int32)
-    e[:, :2] = np.asarray(edges, dtype=np.int32)
-    return np.asarray(types, dtype=np.int32), e
-
-
-def random_legal_params(node_types: Sequence[int], seed: int) -> Dict[NodeType, np.ndarray]:
-    """`tests/support/test_util.cpp:63-113` with a fresh mt19937(seed), original row order."""
-    counts: Dict[int, int] = {}
-    for t in node_types:
-        if param_width(t) > 0:
-            counts[int(t)] = counts.get(int(t), 0) + 1
-    out = {NodeType(t): np.zeros((n, param_width(t))) for t, n in sorted(counts.items())}
-    tt = np.ascontiguousarray(np.asarray([int(x) for x in node_types], dtype=np.int32))
-    ptrs = (_vp * NUM_NODE_TYPES)()
-    for t, m in out.items():
-        ptrs[int(t)] = m.ctypes.data
-    _check(_lib.mg_random_legal_params(_ptr(tt), len(tt), seed, ptrs))
-    return out
 
 
 def uniform_noise(n: int, seed: int) -> np.ndarray:
@@ -705,9 +627,9 @@ from .device import BatchRenderer, DeviceRenderer, RenderPipeline  # noqa: E402 
 __all__ = [
     "NodeType", "Strategy", "Graph", "FlatGraph", "RenderData", "StepIndex", "Schedule", "ProcessorSet",
     "BatchRenderer", "DeviceRenderer", "RenderPipeline", "to_flat", "disjoint_union", "compute_render_data_arrays",
-    "generate_console_arrays", "generate_large_console_arrays", "default_params", "default_param_row", "concat_params",
+    "default_params", "default_param_row", "concat_params",
     "compute_render_data", "make_schedule", "validate_schedule", "render", "param_width", "type_code", "type_name",
-    "generate_console", "random_legal_params", "uniform_noise", "compressor_gain_log", "noisegate_gain_log",
+    "uniform_noise", "compressor_gain_log", "noisegate_gain_log",
     "check_param_row", "LIB_PATH",
 ]
 

@@ -24,11 +24,6 @@ void set_conv_fuse(int mode);
 void set_conv_log(int log_n);
 }  // namespace mgb
 
-namespace mixgraph::workload {
-Graph generate_console(int tracks, double prune, std::uint32_t seed);
-ParamStore random_legal_params(const std::vector<NodeType>& types, std::uint32_t seed);
-}  // namespace mixgraph::workload
-
 using namespace mixgraph;
 
 struct mg_plan {
@@ -581,22 +576,6 @@ int32_t mg_check_param_row(int32_t t, const double* row) {
   return guarded([&] {
     const NodeType type = to_type(t);
     check_param_row(type, {row, static_cast<std::size_t>(param_width(type))});
-  });
-}
-
-int32_t mg_generate_console(int32_t tracks, double prune, uint32_t seed, int32_t* types, int32_t cap_nodes, int32_t* edges,
-                            int32_t cap_edges, int32_t* nn, int32_t* ne) {
-  return guarded([&] { export_graph(workload::generate_console(tracks, prune, seed), types, cap_nodes, edges, cap_edges, nn, ne); });
-}
-
-int32_t mg_random_legal_params(const int32_t* types, int32_t n, uint32_t seed, double* const* tables) {
-  return guarded([&] {
-    std::vector<NodeType> tv(static_cast<std::size_t>(n));
-    for (int i = 0; i < n; ++i) tv[static_cast<std::size_t>(i)] = to_type(types[i]);
-    ParamStore s = workload::random_legal_params(tv, seed);
-    for (auto& [t, m] : s.tables) {
-      if (tables[static_cast<int>(t)]) std::memcpy(tables[static_cast<int>(t)], m.values.data(), sizeof(double) * m.values.size());
-    }
   });
 }
 

@@ -1,0 +1,173 @@
+"""GPU: full-size oracle parity of BASELINE configs 3, 4 and 5 (rel-L-inf <= 1e-4).
+
+The workloads are the benchmark's own (workloads/__init__.py), rendered through the same
+product paths bench.py times (BatchRenderer for the re-drawn / sharded unions, the captured
+DeviceRenderer graph for config 4). The oracle is the reference renderer compiled in
+oracle/_ref, run on the box's host cores:
+  * unions (configs 3, 5): every member graph rendered on its own — the reference's
+    invariant "union render = member renders" (`proj/tests/test_render.cpp:132-160`) — on a
+    pool of host threads (ctypes releases the GIL), each member through render.cpp's loop;
+  * config 4 (one 966-node graph, 10 s): ref_render_parallel, render.cpp's step loop with the
+    slots of each step on all host threads (bit-identical to the reference's render(),
+    tests/test_oracle.py), rows freed after their last reader. The backward pass is checked
+    against central differences of the same oracle on the full graph.
+"""
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+import workloads as wl
+from conftest import cuda_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+TOL = 1e-4
+L = wl.L2
+
+
+def member_slices(members, params):
+    """Per-member parameter tables of a union (concat_params `graph.cpp:171-186`: each type's
+    rows are the members' rows in member order)."""
+    out, off = [], {}
+    for t, _ in members:
+        p = {}
+        for ty, tab in params.items():
+            n = int(np.sum(np.asarray(t) == int(ty)))
+            if n:
+                o = off.get(ty, 0)
+                p[ty] = np.ascontiguousarray(tab[o:o + n])
+                off[ty] = o + n
+        out.append(p)
+    return out
+
+
+def oracle_members(ref, members, member_params, bank):
+    """Reference render of every member, member i's inputs taking bank rows (offset + j) % rows."""
+    offs = np.cumsum([0] + [int(np.sum(t == 0)) for t, _ in members])
+    rows = bank.shape[0]
+
+    def one(i):
+        t, e = members[i]
+        src = bank[[(offs[i] + j) % rows for j in range(offs[i + 1] - offs[i])]]
+        return ref.Plan(t, e, 1).render_parallel(member_params[i], src, threads=1)
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as pool:
+        return list(pool.map(one, range(len(members))))
+
+
+def batch_render(mg, members, params, bank_dev):
+    """The bench's path: union plan, BatchRenderer submit (original-order parameters, device
+    reorder), outputs D2H."""
+    import torch
+    from paper_2408_03204_b200 import sharding
+    t, e = sharding.union_arrays(members)
+    rd = mg.compute_render_data_arrays(t, e)
+    procs = mg.ProcessorSet()
+    br = mg.BatchRenderer(procs, 1, L, mg.BatchRenderer.capacity_of(rd, procs, 1, L), depth=1)
+    out = torch.empty((rd.buffer_rows - rd.output_begin, 1, 2, L), dtype=torch.float32, pin_memory=True).numpy()
+    br.submit(rd, params, bank_dev, out, validate=True)
+    br.sync()
+    return out
+
+
+def check_members(out, want):
+    assert out.shape[0] == len(want)  # one output node per console, in member order
+    errs = [float(np.max(np.abs(out[i] - w[0])) / max(np.max(np.abs(w[0])), 1e-30)) for i, w in enumerate(want)]
+    assert max(errs) < TOL, (int(np.argmax(errs)), max(errs))
+    return max(errs)
+
+
+@pytest.fixture(scope="module")
+def bank():
+    import torch
+    b = wl.source_bank(64, L)
+    return b, torch.as_tensor(b, dtype=torch.float32).cuda()
+
+
+def test_config3_batch_full_size(mg, ref, bank):
+    # BASELINE config 3, batch 0: 64 re-drawn consoles (K in [4, 32], p = 0.3) at 2^17.
+    from paper_2408_03204_b200 import sharding
+    members = wl.config3_members(0)
+    t, _ = sharding.union_arrays(members)
+    params = wl.random_legal_params(t, wl.config3_params_seed(0))
+    out = batch_render(mg, members, params, bank[1])
+    want = oracle_members(ref, members, member_slices(members, params), bank[0])
+    check_members(out, want)
+
+
+def test_config5_shard_full_size(mg, ref, bank):
+    # BASELINE config 5: shard 0 of the 512-console set split over 8 ranks (LPT), rendered as
+    # the bench renders a shard (unions of <= 64 consoles, per-graph parameters).
+    from paper_2408_03204_b200 import sharding
+    graphs = wl.config5_graphs()
+    shard = sharding.lpt_shards([sharding.graph_cost(t, L) for t, _ in graphs], 8)[0]
+    assert 60 <= len(shard) <= 68
+    members = [graphs[i] for i in shard]
+    per = [wl.config5_member_params(i, graphs[i][0]) for i in shard]
+    params = wl.union_params([t for t, _ in members], per)
+    out = batch_render(mg, members, params, bank[1])
+    want = oracle_members(ref, members, per, bank[0])
+    check_members(out, want)
+
+
+@pytest.fixture(scope="module")
+def config4(mg):
+    t, e = wl.generate_large_console_arrays(64)
+    params = wl.random_legal_params(t, 4040)
+    src = wl.sources(64, wl.L4)
+    return t, e, params, src
+
+
+def test_config4_full_graph_forward(mg, ref, config4):
+    # BASELINE config 4: 966 nodes, 10 s. The master output and the taps of three whole tracks
+    # (strip, sends) and the bus chain, against the reference's own render of the full graph.
+    import torch
+    t, e, params, src = config4
+    procs = mg.ProcessorSet()
+    rd = mg.compute_render_data_arrays(t, e)
+    dr = mg.DeviceRenderer(rd, procs, 1, wl.L4, rd.reorder_params(params))
+    dr.sources.copy_(torch.as_tensor(src, dtype=torch.float32))
+    graph = dr.capture()
+    graph.replay()
+    torch.cuda.synchronize()
+    out = dr.outputs.cpu().numpy()
+    keep = [n for k in (0, 31, 63) for n in range(15 * k, 15 * k + 15)] + list(range(960, 966))
+    want, kept = ref.Plan(t, e, 1).render_parallel(params, src, keep=keep)
+    assert ref.rel_linf(out, want) < TOL
+    sigma = np.asarray(rd.sigma)
+    got = dr.arena.index_select(0, torch.as_tensor(sigma[keep], device=dr.arena.device)).cpu().numpy()
+    for j, n in enumerate(keep):
+        assert ref.rel_linf(got[j], kept[j]) < TOL, (n, mg.type_name(int(t[n])))
+
+
+def test_config4_full_graph_backward_spot_check(mg, ref, config4):
+    # Reverse-mode pass of the 966-node 10 s graph (the optimisation config) against central
+    # differences of the reference's own renderer on the full graph, loss = sum(w * out).
+    import torch
+    t, e, params, src = config4
+    procs = mg.ProcessorSet()
+    rd = mg.compute_render_data_arrays(t, e)
+    dr = mg.DeviceRenderer(rd, procs, 1, wl.L4, rd.reorder_params(params), backward=True)
+    dr.sources.copy_(torch.as_tensor(src, dtype=torch.float32))
+    out = dr.render()
+    w = np.random.default_rng(4).uniform(-1, 1, size=tuple(out.shape))
+    grads, _ = dr.backward(torch.as_tensor(w, dtype=torch.float32, device=out.device))
+    torch.cuda.synchronize()
+    g = rd.original_order({k: v.cpu().numpy() for k, v in grads.items()})
+    plan = ref.Plan(t, e, 1)
+    T = mg.NodeType
+    # (type, row, col): bus gain (last gain row), bus EQ magnitude, a track's compressor
+    # threshold, a track's reverb colour bin.
+    picks = [(T.GAIN, params[T.GAIN].shape[0] - 1, 0), (T.EQ, params[T.EQ].shape[0] - 1, 10),
+             (T.COMPRESSOR, 40, 1), (T.REVERB, 17, 5)]
+    for ty, r, c in picks:
+        h = 1e-5 * max(1.0, abs(params[ty][r, c]))
+        hi = {k: np.array(v, copy=True) for k, v in params.items()}
+        lo = {k: np.array(v, copy=True) for k, v in params.items()}
+        hi[ty][r, c] += h
+        lo[ty][r, c] -= h
+        fd = (np.sum(w * plan.render_parallel(hi, src)) - np.sum(w * plan.render_parallel(lo, src))) / (2 * h)
+        scale = max(abs(fd), np.abs(g[ty]).max())
+        assert abs(g[ty][r, c] - fd) <= 2e-3 * scale, (mg.type_name(int(ty)), r, c, g[ty][r, c], fd)

@@ -12,6 +12,8 @@ import os
 import re
 
 import numpy as np
+
+import workloads as wl
 import pytest
 
 import paper_2408_03204_b200 as mg
@@ -42,8 +44,8 @@ def same_values(a, b):
 
 
 def console_doc(tracks=2, seed=5):
-    g = mg.generate_console(tracks, 0.3, seed)
-    P = mg.random_legal_params(mg.to_flat(g).node_types, seed)
+    g = wl.generate_console(tracks, 0.3, seed)
+    P = wl.random_legal_params(mg.to_flat(g).node_types, seed)
     return g, P
 
 
@@ -64,7 +66,7 @@ def test_graph_to_json_matches_reference_layout(tracks, seed):
 
 @needs_ref
 def test_graph_to_json_without_params_is_byte_identical():
-    g = mg.generate_console(3, 0.0, 2)
+    g = wl.generate_console(3, 0.0, 2)
     t, e = g.arrays()
     assert mg.graph_to_json(g, {}) == ref.graph_to_json(t, e, {})
     empty = mg.Graph()
@@ -183,12 +185,12 @@ def test_spec_examples(tmp_path):
 def test_export_dot_matches_reference():
     chain = mg.Graph()
     chain.add_serial_chain([mg.NodeType.IN, mg.NodeType.GAIN, mg.NodeType.OUT])
-    for g in [chain, mg.Graph(), mg.generate_console(2, 0.0, 0), mg.generate_console(8, 0.3, 4)]:
+    for g in [chain, mg.Graph(), wl.generate_console(2, 0.0, 0), wl.generate_console(8, 0.3, 4)]:
         t, e = g.arrays()
         assert mg.export_dot(g) == ref.export_dot(t, e)
     dot = mg.export_dot(chain)
     assert dot.count("[label=") == 3 and dot.count("->") == 2
-    assert mg.export_dot(mg.generate_console(2, 0.0, 0)).count("[label=") == 22
+    assert mg.export_dot(wl.generate_console(2, 0.0, 0)).count("[label=") == 22
     assert mg.export_dot(mg.Graph()) == "digraph {\n  rankdir=LR;\n}\n"
 
 

@@ -44,3 +44,18 @@ def test_reference_known_answers(ref):
     assert ref.Plan(t, e, 1).type_codes == "iecnsgrdmecsgo"
     assert ref.Plan(t, e, 2).type_codes == "iecnsgdrmecsgo"
     assert ref.Plan(t, e, 0).num_steps == 105
+
+
+@pytest.mark.parametrize("tracks,seed,batch", [(4, 7, 1), (9, 3, 2)])
+def test_parallel_oracle_render_equals_reference_render(ref, tracks, seed, batch):
+    # ref_render_parallel (the full-size parity tests' oracle) is render.cpp's loop with each
+    # step's slots on host threads: bit-identical outputs and intermediates.
+    t, e = ref.console(tracks, 0.3, seed)
+    params = ref.random_legal_params(t, e, 11)
+    src = np.random.default_rng(seed).uniform(-1, 1, size=(int(np.sum(t == 0)), batch, 2, 3000))
+    plan = ref.Plan(t, e, 1)
+    want, inter = plan.render(params, src, sample_rate=8000.0, keep_intermediates=True)
+    keep = [0, 3, 5, len(t) - 1]
+    got, kept = plan.render_parallel(params, src, sample_rate=8000.0, threads=4, keep=keep)
+    assert np.array_equal(got, want)
+    assert np.array_equal(kept, inter[keep])

@@ -6,6 +6,8 @@ Cases follow `proj/tests/test_render.cpp` and `test_processors.cpp`, plus full-s
 BASELINE configurations checked directly against the reference renderer.
 """
 import numpy as np
+
+import workloads as wl
 import pytest
 
 from conftest import cuda_ok
@@ -386,7 +388,7 @@ def test_render_pipeline_matches_render(mg, ref, dtype, host_threads):
 
 def _random_union(mg, sharding, seed, graphs):
     rng = np.random.default_rng(seed)
-    members = [mg.generate_console_arrays(int(rng.integers(2, 9)), 0.3, 50 * seed + i) for i in range(graphs)]
+    members = [wl.generate_console_arrays(int(rng.integers(2, 9)), 0.3, 50 * seed + i) for i in range(graphs)]
     return sharding.union_arrays(members)
 
 
@@ -402,7 +404,7 @@ def test_batch_renderer_redrawn_topologies(mg, ref, on_device):
     batches = []
     for i in range(4):
         t, e = _random_union(mg, sharding, i, 3 + i)
-        batches.append((t, e, mg.compute_render_data_arrays(t, e), mg.random_legal_params(t, 70 + i)))
+        batches.append((t, e, mg.compute_render_data_arrays(t, e), wl.random_legal_params(t, 70 + i)))
     cap = np.zeros(4, dtype=np.uint64)
     for _, _, rd, _ in batches:
         cap = np.maximum(cap, mg.BatchRenderer.capacity_of(rd, procs, 1, L))
@@ -433,7 +435,7 @@ def test_batch_renderer_rejects_bad_params(mg):
     rd = mg.compute_render_data_arrays(t, e)
     br = mg.BatchRenderer(procs, 1, L, mg.BatchRenderer.capacity_of(rd, procs, 1, L))
     src = np.zeros((1, 1, 2, L), dtype=np.float32)
-    params = mg.random_legal_params(t, 3)
+    params = wl.random_legal_params(t, 3)
     bad = {k: v.copy() for k, v in params.items()}
     bad[mg.NodeType.COMPRESSOR][0, 0] = 1.5
     with pytest.raises(ValueError, match="alpha"):
@@ -469,9 +471,9 @@ def test_config4_large_graph_full_size(mg, ref):
     # outputs (intermediates) equal a 1-track graph rendered with that track's parameters,
     # and the 1-track graph matches the reference renderer at full length.
     L, tracks = 441000, 64
-    t, e = mg.generate_large_console_arrays(tracks)
+    t, e = wl.generate_large_console_arrays(tracks)
     assert len(t) == 966 and len(e) == 1093
-    params = mg.random_legal_params(t, 44)
+    params = wl.random_legal_params(t, 44)
     k_src = 3
     src = np.stack([mg.uniform_noise(2 * L, 1000 + (k % k_src)).reshape(1, 2, L) for k in range(tracks)])
     import torch
@@ -482,7 +484,7 @@ def test_config4_large_graph_full_size(mg, ref):
     out = dr.render().cpu().numpy()
     assert np.isfinite(out).all() and np.abs(out).max() > 0
     sigma = np.asarray(rd.sigma)
-    t1, e1 = mg.generate_large_console_arrays(1)
+    t1, e1 = wl.generate_large_console_arrays(1)
     rd1 = mg.compute_render_data_arrays(t1, e1)
     for k in (0, 37, 63):
         p1 = _track_params(mg, t, params, tracks, k)

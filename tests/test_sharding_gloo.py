@@ -4,6 +4,8 @@ import os
 import socket
 
 import numpy as np
+
+import workloads as wl
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -23,7 +25,7 @@ def _worker(rank, world, port, out):
     from paper_2408_03204_b200 import sharding
 
     L = 1 << 17
-    graphs = [mg.generate_console(4 + (i * 7) % 29, 0.3, 1000 + i).arrays() for i in range(24)]
+    graphs = [wl.generate_console(4 + (i * 7) % 29, 0.3, 1000 + i).arrays() for i in range(24)]
     costs = [sharding.graph_cost(t, L) for t, _ in graphs]
     shards = sharding.lpt_shards(costs, world)
     mine = shards[rank]

@@ -6,6 +6,8 @@ import re
 
 import numpy as np
 
+import workloads as wl
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -28,23 +30,23 @@ def test_console_generator_matches_reference(mg, ref):
     for k in (1, 2, 5, 16, 32, 64):
         for prune, seed in ((0.0, 0), (0.3, 16), (0.7, 123)):
             t, e = ref.console(k, prune, seed)
-            g = mg.generate_console(k, prune, seed)
+            g = wl.generate_console(k, prune, seed)
             gt, ge = g.arrays()
             assert np.array_equal(gt, t) and np.array_equal(ge, e)
-    assert mg.to_flat(mg.generate_console(8)).num_nodes() == 70  # 8K + 6
+    assert mg.to_flat(wl.generate_console(8)).num_nodes() == 70  # 8K + 6
 
 
 def test_random_legal_params_match_reference(mg, ref):
     for seed in range(6):
         t, e = ref.random_dag(seed, 10, 60)
         want = ref.random_legal_params(t, e, seed + 100)
-        got = mg.random_legal_params(t, seed + 100)
+        got = wl.random_legal_params(t, seed + 100)
         assert sorted(int(k) for k in got) == sorted(want)
         for k, v in want.items():
             assert np.array_equal(got[k], v)
     t, e = ref.console(16, 0.3, 16)
     want = ref.random_legal_params(t, e, 7)
-    got = mg.random_legal_params(t, 7)
+    got = wl.random_legal_params(t, 7)
     for k, v in want.items():
         assert np.array_equal(got[k], v)
 

@@ -1,3 +1,4 @@
+import workloads as wl
 """Same-box A/B timing of library builds: graph-replay ms/render of the config-2 workload.
 
 Usage (GPU box):  python tools/ab_time.py ab/base.so ab/cur.so [...]
@@ -15,8 +16,8 @@ import numpy as np, torch
 sys.path.insert(0, os.environ["MGB_ROOT"])
 import paper_2408_03204_b200 as mg
 L = 1 << 17
-g = mg.generate_console(16, 0.3, 16); fg = mg.to_flat(g); rd = mg.compute_render_data(fg)
-P = rd.reorder_params(mg.random_legal_params(fg.node_types, 2024))
+g = wl.generate_console(16, 0.3, 16); fg = mg.to_flat(g); rd = mg.compute_render_data(fg)
+P = rd.reorder_params(wl.random_legal_params(fg.node_types, 2024))
 src = np.stack([mg.uniform_noise(2 * L, 1000 + k).reshape(1, 2, L) for k in range(rd.num_inputs)])
 dr = mg.DeviceRenderer(rd, mg.ProcessorSet(), 1, L, P)
 dr.sources.copy_(torch.as_tensor(src, dtype=torch.float32))

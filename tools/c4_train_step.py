@@ -5,6 +5,8 @@ import sys
 
 import numpy as np
 
+import workloads as wl
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
@@ -12,9 +14,9 @@ import paper_2408_03204_b200 as mg  # noqa: E402
 from paper_2408_03204_b200 import training  # noqa: E402
 
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 441000
-t, e = mg.generate_large_console_arrays(64)
+t, e = wl.generate_large_console_arrays(64)
 rd = mg.compute_render_data_arrays(t, e)
-P = rd.reorder_params(mg.random_legal_params(t, 4040))
+P = rd.reorder_params(wl.random_legal_params(t, 4040))
 procs = mg.ProcessorSet()
 tr = training.Trainer(rd, procs, 1, L, P, trainable=[int(x) for x in P], learning_rate=1e-3)
 src = torch.rand((rd.num_inputs, 1, 2, L), device="cuda") * 2 - 1

@@ -9,6 +9,8 @@ import time
 
 import numpy as np
 
+import workloads as wl
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch  # noqa: E402
@@ -26,10 +28,10 @@ def main():
     dev = torch.device("cuda", 0)
     rng = np.random.default_rng(st)
     t0 = time.perf_counter()
-    members = [mg.generate_console_arrays(int(rng.integers(4, 33)), 0.3, 1000 * st + i) for i in range(graphs)]
+    members = [wl.generate_console_arrays(int(rng.integers(4, 33)), 0.3, 1000 * st + i) for i in range(graphs)]
     t, e = sharding.union_arrays(members)
     t1 = time.perf_counter()
-    params = mg.random_legal_params(t, 5000 + st)
+    params = wl.random_legal_params(t, 5000 + st)
     t2 = time.perf_counter()
     rd = mg.compute_render_data_arrays(t, e)
     t3 = time.perf_counter()

@@ -1,3 +1,4 @@
+import workloads as wl
 """e2e A/B of RenderPipeline double-audio conversion: host threads / host fraction vs device (config 2)."""
 import os
 import subprocess
@@ -9,8 +10,8 @@ for v in (sys.argv[1:] or ["0", "2", "4", "8"]):  # THREADS or THREADS:HOST_FRAC
     out = subprocess.run([sys.executable, "-c", """
 import sys, time, json; sys.path.insert(0, '.')
 import numpy as np, bench, paper_2408_03204_b200 as mg
-g = mg.generate_console(16, 0.3, 16); fg = mg.to_flat(g); rd = mg.compute_render_data(fg)
-P = rd.reorder_params(mg.random_legal_params(fg.node_types, 2024)); L = 1 << 17
+g = wl.generate_console(16, 0.3, 16); fg = mg.to_flat(g); rd = mg.compute_render_data(fg)
+P = rd.reorder_params(wl.random_legal_params(fg.node_types, 2024)); L = 1 << 17
 src = np.stack([mg.uniform_noise(2 * L, 1000 + k).reshape(1, 2, L) for k in range(rd.num_inputs)])
 procs = mg.ProcessorSet()
 pipe = mg.RenderPipeline(rd, procs, 1, L, dtype=np.float64, depth=2)

@@ -6,15 +6,17 @@ import sys
 
 import numpy as np
 
+import workloads as wl
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2408_03204_b200 as mg  # noqa: E402
 from oracle import ref  # noqa: E402
 
 L = 1 << 17
-g = mg.generate_console(16, 0.3, 16)
+g = wl.generate_console(16, 0.3, 16)
 fg = mg.to_flat(g)
 rd = mg.compute_render_data(fg)
-params = mg.random_legal_params(fg.node_types, 2024)
+params = wl.random_legal_params(fg.node_types, 2024)
 src = np.stack([mg.uniform_noise(2 * L, 1000 + k).reshape(1, 2, L) for k in range(rd.num_inputs)])
 procs = mg.ProcessorSet()
 out = mg.render(rd, procs, rd.reorder_params(params), src)

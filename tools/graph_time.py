@@ -6,6 +6,8 @@ import sys
 
 import numpy as np
 
+import workloads as wl
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
@@ -13,10 +15,10 @@ import paper_2408_03204_b200 as mg  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 L = 1 << 17
-g = mg.generate_console(16, 0.3, 16)
+g = wl.generate_console(16, 0.3, 16)
 fg = mg.to_flat(g)
 rd = mg.compute_render_data(fg)
-P = rd.reorder_params(mg.random_legal_params(fg.node_types, 2024))
+P = rd.reorder_params(wl.random_legal_params(fg.node_types, 2024))
 if "MGB_CONV_FUSE" in os.environ:  # A-B: -1 auto, 0 separate kernel-spectrum rows pass, 1 fused
     mg.set_conv_fuse(int(os.environ["MGB_CONV_FUSE"]))
 procs = mg.ProcessorSet()

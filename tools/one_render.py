@@ -5,6 +5,8 @@ import os
 import sys
 
 import numpy as np
+
+import workloads as wl
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -17,9 +19,9 @@ def main():
     ap.add_argument("--length", type=int, default=1 << 17)
     args = ap.parse_args()
     L = args.length
-    fg = mg.to_flat(mg.generate_console(16, 0.3, 16))
+    fg = mg.to_flat(wl.generate_console(16, 0.3, 16))
     rd = mg.compute_render_data(fg)
-    P = rd.reorder_params(mg.random_legal_params(fg.node_types, 2024))
+    P = rd.reorder_params(wl.random_legal_params(fg.node_types, 2024))
     src = np.stack([mg.uniform_noise(2 * L, 1000 + k).reshape(1, 2, L) for k in range(rd.num_inputs)])
     dr = mg.DeviceRenderer(rd, mg.ProcessorSet(), 1, L, P)
     dr.sources.copy_(torch.as_tensor(src, dtype=torch.float32))

@@ -12,6 +12,8 @@ if "--serial" in sys.argv:  # every prologue inline on the main stream: isolated
     os.environ["MGB_NO_HOIST"] = "1"
 
 import numpy as np
+
+import workloads as wl
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -27,10 +29,10 @@ def main():
     ap.add_argument("--length", type=int, default=1 << 17)
     args = ap.parse_args()
     L = args.length
-    g = mg.generate_console(16, 0.3, 16)
+    g = wl.generate_console(16, 0.3, 16)
     fg = mg.to_flat(g)
     rd = mg.compute_render_data(fg)
-    P = rd.reorder_params(mg.random_legal_params(fg.node_types, 2024))
+    P = rd.reorder_params(wl.random_legal_params(fg.node_types, 2024))
     src = np.stack([mg.uniform_noise(2 * L, 1000 + k).reshape(1, 2, L) for k in range(rd.num_inputs)])
     procs = mg.ProcessorSet()
     dr = mg.DeviceRenderer(rd, procs, 1, L, P)
