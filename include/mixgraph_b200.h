@@ -153,6 +153,11 @@ void mg_set_conv_fuse(int32_t mode);
  * points per segment. Applies to plans whose device workspace is sized after the call. */
 void mg_set_conv_log(int32_t log_n);
 
+/* Arithmetic precision of the FFT-based steps (EQ, reverb, delay): 32 or 64 bits; the arena
+ * stays fp32. Process-wide. */
+void mg_set_fft_precision(int32_t bits);
+int32_t mg_fft_precision(void);
+
 /* Optimisation helpers on device buffers (fit.cpp:25-96 with analytic gradients): the MSE
  * loss mean((y - t)^2) into *d_loss (fp64, deterministic) and d_grad = 2 (y - t) / n;
  * d_scratch >= mg_mse_scratch_bytes(). mg_sgd_step: table -= lr * grad over rows x width,

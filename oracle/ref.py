@@ -57,7 +57,7 @@ def lib():
         sig("ref_plan_param_source_rows", _i32, _vp, _i32, _vp)
         sig("ref_render", _i32, _vp, _dbl, _u32, _i32, _dbl, _vp, _vp, _vp, _i32, _i64, _vp, _vp)
         sig("ref_render_parallel", _i32, _vp, _dbl, _u32, _i32, _dbl, _vp, _vp, _vp, _i32, _i64, _i32, _vp, _i32,
-            _vp, _vp)
+            _vp, _vp, _i32, _dbl)
         sig("ref_render_reference", _i32, _vp, _i32, _vp, _i32, _dbl, _u32, _i32, _dbl, _vp, _vp, _vp, _i32, _i64, _vp)
         sig("ref_process", _i32, _i32, _vp, _vp, _i32, _i32, _i64, _vp, _i32, _i32, _dbl, _u32, _i32, _dbl)
         sig("ref_reverb_kernel", _i32, _dbl, _u32, _vp, _vp, _vp, ctypes.POINTER(_i64))
@@ -210,11 +210,14 @@ class Plan:
 
     def render_parallel(self, params: Dict[int, np.ndarray], sources: np.ndarray, sample_rate: float = 44100.0,
                         threads: Optional[int] = None, keep=None, reverb_seed: int = 0, envelope_taps: int = 32768,
-                        energy_floor: float = 1e-7):
+                        energy_floor: float = 1e-7, round_f32: bool = False, perturb: float = 0.0):
         """render.cpp:14-81 with each step's slots on `threads` host threads (ref_render_parallel:
         the reference's own gather order and ProcessorSet::process per slot; rows freed after
         their last reader). Returns outputs, or (outputs, kept) with kept[j] = the row of
-        ORIGINAL node keep[j] (as render()'s intermediates)."""
+        ORIGINAL node keep[j] (as render()'s intermediates). round_f32 (diagnostic): rows rounded
+        to float between steps (the reference's arithmetic over an fp32 arena). perturb > 0
+        (conditioning probe): uniform noise of amplitude perturb * row peak added to every
+        processed row (the global per-step error of an FFT-based fp32 renderer)."""
         import os
         src = np.ascontiguousarray(sources, dtype=np.float64)
         k, b, _, n = src.shape
@@ -224,7 +227,8 @@ class Plan:
         kept = None if kk is None else np.zeros((len(kk), b, 2, n))
         _check(lib().ref_render_parallel(self.h, sample_rate, reverb_seed, envelope_taps, energy_floor, ptrs, _p(rows),
                                          _p(src), b, n, int(threads or os.cpu_count() or 1), _p(kk),
-                                         0 if kk is None else len(kk), _p(outs), _p(kept)))
+                                         0 if kk is None else len(kk), _p(outs), _p(kept), int(bool(round_f32)),
+                                         float(perturb)))
         return outs if kk is None else (outs, kept)
 
     def __del__(self):

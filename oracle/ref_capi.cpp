@@ -11,6 +11,7 @@
 // double matrix for NodeType t (enum order, `proj/include/mixgraph/types.hpp:12-23`), or
 // is NULL when the graph has no node of that type.
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstdint>
 #include <cstring>
@@ -300,10 +301,15 @@ int ref_render(const void* p, double fs, uint32_t seed, int32_t env_taps, double
 // `keep` nodes to the end), so the fp64 arena of a 966-node 10 s graph never exists at once;
 // a row read before any step stored it reads zeros, as the reference's zero-filled buffer.
 // outputs [num_outputs][B][2][L]; kept [n_keep][B][2][L] = rows sigma[keep[j]] (original ids).
+// round_f32 (diagnostic): every stored row (and the sources) rounded to float, i.e. the
+// reference's fp64 arithmetic with an fp32 arena — the error floor of any fp32-storage renderer.
+// perturb > 0 (conditioning probe): every processed row gets uniform noise of amplitude
+// perturb * (row peak), mt19937(row) — the global per-step error an FFT-based fp32 renderer
+// makes; the output's response to it measures the graph's amplification of such errors.
 int ref_render_parallel(const void* p, double fs, uint32_t seed, int32_t env_taps, double floor_,
                         const double* const* tables, const int32_t* rows, const double* sources, int32_t batch,
                         int64_t length, int32_t threads, const int32_t* keep, int32_t n_keep, double* outputs,
-                        double* kept) {
+                        double* kept, int32_t round_f32, double perturb) {
   return guarded([&] {
     const auto* rd = static_cast<const RenderData*>(p);
     const ProcessorSet& procs = processors_for(fs, seed, env_taps, floor_);
@@ -322,6 +328,10 @@ int ref_render_parallel(const void* p, double fs, uint32_t seed, int32_t env_tap
     for (int k = 0; k < rd->num_inputs; ++k) {
       buf[static_cast<std::size_t>(k)] = std::make_unique<double[]>(stride);
       std::memcpy(buf[static_cast<std::size_t>(k)].get(), sources + stride * k, sizeof(double) * stride);
+      if (round_f32) {
+        double* r = buf[static_cast<std::size_t>(k)].get();
+        for (std::size_t j = 0; j < stride; ++j) r[j] = static_cast<double>(static_cast<float>(r[j]));
+      }
     }
     const int nthreads = std::max(1, threads);
     for (std::size_t k = 0; k < rd->steps.size(); ++k) {
@@ -354,6 +364,15 @@ int ref_render_parallel(const void* p, double fs, uint32_t seed, int32_t env_tap
             auto y = std::make_unique<double[]>(stride);
             std::fill(y.get(), y.get() + stride, 0.0);
             procs.process(step.type, in.data(), y.get(), 1, batch, static_cast<long>(length), table, step.param_begin + s);
+            if (perturb > 0.0) {
+              double peak = 0.0;
+              for (std::size_t j = 0; j < stride; ++j) peak = std::max(peak, std::abs(y[j]));
+              std::mt19937 noise(static_cast<std::uint32_t>(step.store_begin + s));
+              for (std::size_t j = 0; j < stride; ++j) y[j] += perturb * peak * (2.0 * (noise() * (1.0 / 4294967296.0)) - 1.0);
+            }
+            if (round_f32) {
+              for (std::size_t j = 0; j < stride; ++j) y[j] = static_cast<double>(static_cast<float>(y[j]));
+            }
             out[static_cast<std::size_t>(s)] = std::move(y);
           } catch (const std::exception& e) {
             std::scoped_lock lk(err_mu);

@@ -83,6 +83,8 @@ _sig("mg_backward_workspace_bytes", _i32, _vp, _vp, _i32, _i64, _P(_u64))
 _sig("mg_render_backward_arena", _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp)
 _sig("mg_set_conv_fuse", None, _i32)
 _sig("mg_set_conv_log", None, _i32)
+_sig("mg_set_fft_precision", None, _i32)
+_sig("mg_fft_precision", _i32)
 _sig("mg_batch_capacity", _i32, _vp, _vp, _i32, _i64, _vp)
 _sig("mg_batch_create", _i32, _vp, _i32, _i64, _vp, _i32, _P(_vp))
 _sig("mg_batch_submit", _i32, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp)
@@ -608,6 +610,15 @@ def render(rd: RenderData, procs: ProcessorSet, params: Optional[Dict[int, np.nd
 def set_conv_fuse(mode: int) -> None:
     """mg_set_conv_fuse: -1 auto (default), 0 separate kernel-spectrum rows pass, 1 fused."""
     _lib.mg_set_conv_fuse(int(mode))
+
+
+def set_fft_precision(bits: int) -> None:
+    """mg_set_fft_precision: arithmetic of the FFT-based steps, 32 or 64 bits (arena fp32)."""
+    _lib.mg_set_fft_precision(int(bits))
+
+
+def fft_precision() -> int:
+    return int(_lib.mg_fft_precision())
 
 
 def set_conv_log(log_n: int) -> None:

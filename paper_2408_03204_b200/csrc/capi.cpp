@@ -22,6 +22,8 @@ void launch_mse_loss_grad(const float* y, const float* target, long n, float* gr
 void launch_sgd_step(bool dynamics, double* table, const double* grad, long n, double lr, cudaStream_t s);
 void set_conv_fuse(int mode);
 void set_conv_log(int log_n);
+void set_fft_fp64(bool on);
+bool fft_fp64();
 }  // namespace mgb
 
 using namespace mixgraph;
@@ -470,6 +472,9 @@ int32_t mg_render_backward_arena(const mg_plan* p, const mg_processors* procs, c
 void mg_set_conv_fuse(int32_t mode) { mgb::set_conv_fuse(mode); }
 
 void mg_set_conv_log(int32_t log_n) { mgb::set_conv_log(log_n); }
+
+void mg_set_fft_precision(int32_t bits) { mgb::set_fft_fp64(bits == 64); }
+int32_t mg_fft_precision(void) { return mgb::fft_fp64() ? 64 : 32; }
 
 uint64_t mg_mse_scratch_bytes(void) { return mgb::mse_scratch_bytes(); }
 

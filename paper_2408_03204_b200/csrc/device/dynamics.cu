@@ -26,9 +26,8 @@ namespace mgb {
 
 namespace {
 
-constexpr unsigned long long kFlagAgg = 1ull << 32;
-
 struct DynParams {
+  double da, doma, daN, da16, datile, datile32;  // the forward envelope scan runs in fp64
   float a, oma, aN, a16, atile, atile32;
   float T, W, R, invR, floor_;
   float knee;  // knee-curve coefficient: (1/R - 1) / (4W) compressor, (1 - R) / (4W) gate
@@ -61,6 +60,12 @@ __device__ __forceinline__ void derive_params(const double* row, int env_taps, d
   const double atile = __shfl_sync(0xffffffffu, pw, 2), atile32 = __shfl_sync(0xffffffffu, pw, 3);
   if (lane != 0) return;
   DynParams p;
+  p.da = a;
+  p.doma = 1.0 - a;
+  p.daN = aN < 1e-30 ? 0.0 : aN;
+  p.da16 = a16;
+  p.datile = atile;
+  p.datile32 = atile32;
   p.a = static_cast<float>(a);
   p.oma = static_cast<float>(1.0 - a);
   p.Ne = Ne;
@@ -77,13 +82,13 @@ __device__ __forceinline__ void derive_params(const double* row, int env_taps, d
   *out = p;
 }
 
-// Gain exp(G_y - G_u) at envelope g (processors.cpp:71-130 knee curves). Fast-path math:
-// __logf / __expf (MUFU lg2 / ex2, ~1e-6 relative here) and the knee's division folded into a
-// per-slot coefficient: ~30 fewer instructions per sample than logf / expf / fdiv, in the
-// scan's replay loop that runs once per sample. `gu_out` receives G_u (backward pass).
+// Gain exp(G_y - G_u) at envelope g (processors.cpp:71-130 knee curves), correctly rounded
+// logf / expf (the MUFU approximations' ~5e-7 relative error reached the outputs: a gate
+// with ratio R multiplies an error in G_u by R - 1), the knee's division folded into a
+// per-slot coefficient. `gu_out` receives G_u (backward pass).
 template <bool GATE>
 __device__ __forceinline__ float gain_of(float g, const DynParams& p, float* gu_out = nullptr) {
-  const float gu = __logf(fmaxf(g, p.floor_));
+  const float gu = logf(fmaxf(g, p.floor_));
   float gy;
   if (!GATE) {
     if (gu >= p.T + p.W) {
@@ -105,7 +110,7 @@ __device__ __forceinline__ float gain_of(float g, const DynParams& p, float* gu_
     }
   }
   if (gu_out) *gu_out = gu;
-  return __expf(gy - gu);
+  return expf(gy - gu);
 }
 
 // Gather-sum of the slot's inputs at kDynPerThread consecutive samples from n0.
@@ -213,9 +218,10 @@ __device__ __forceinline__ void load_tile(const StepArgs& a, int e0, int e1, int
   }
 }
 
-__device__ __forceinline__ void compose(float& A, float& B, float Ap, float Bp) {
+template <typename T>
+__device__ __forceinline__ void compose(T& A, T& B, T Ap, T Bp) {
   // earlier (Ap, Bp) then current (A, B)
-  B = fmaf(A, Bp, B);
+  B = fma(A, Bp, B);
   A = A * Ap;
 }
 
@@ -226,9 +232,9 @@ template <bool GATE, bool VEC, bool ENV = false, int NT = kDynThreads>
 __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a, int env_taps, double floor_, int tiles_per_seq,
                                                          unsigned long long* status, unsigned int* ticket,
                                                          float* env, PwEpi epi) {
-  __shared__ float wA[NT / 32], wB[NT / 32];
+  __shared__ double wA[NT / 32], wB[NT / 32];
   __shared__ float4 s_in[2][kDynPerThread / 4][NT];  // the tile's gathered input (l, r), read once
-  __shared__ float s_carry;
+  __shared__ double s_carry;
   __shared__ int s_ticket;
   __shared__ DynParams s_p;
   __shared__ PwEpiSlots s_epi;
@@ -252,8 +258,9 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
   const long n0 = static_cast<long>(tile) * (NT * kDynPerThread) + static_cast<long>(threadIdx.x) * kDynPerThread;
   // drive[k] = (1-a) (e[n] - a^Ne e[n-Ne]) is all the scan keeps in registers; the gathered
   // input samples wait in shared memory for the output pass (read from memory once), so
-  // nothing else stays live across the carry wait (no spills at 64 registers).
-  float drive[kDynPerThread];
+  // nothing else stays live across the carry wait. The recurrence runs in fp64: with poles up
+  // to a = 0.9995 an fp32 envelope accumulates ~eps / sqrt(2 (1 - a)) = 2e-6 relative error.
+  double drive[kDynPerThread];
   {
     // The tile's own samples are requested first; warp 0 derives the slot constants (fp64
     // powers) while they are in flight, instead of every warp waiting for them at the barrier
@@ -265,29 +272,35 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
       if (epi.n > 0 && threadIdx.x == 1) pw_epi_slots(epi, slot, s_epi);
     }
     __syncthreads();
-    if (p.aN != 0.f) {
+    if (p.daN != 0.0) {
       float mo[kDynPerThread];
       load_mid<VEC>(a, e0, e1, b, n0 - p.Ne, mo);
 #pragma unroll
-      for (int k = 0; k < kDynPerThread; ++k) drive[k] = p.oma * (mid[k] * mid[k] - p.aN * (mo[k] * mo[k]));
+      for (int k = 0; k < kDynPerThread; ++k) {
+        const double m = mid[k], o = mo[k];
+        drive[k] = p.doma * (m * m - p.daN * (o * o));
+      }
     } else {
 #pragma unroll
-      for (int k = 0; k < kDynPerThread; ++k) drive[k] = p.oma * (mid[k] * mid[k] - 0.f);
+      for (int k = 0; k < kDynPerThread; ++k) {
+        const double m = mid[k];
+        drive[k] = p.doma * (m * m);
+      }
     }
   }
 
   // Thread-local recurrence from 0.
-  float B = 0.f;
+  double B = 0.0;
 #pragma unroll
-  for (int k = 0; k < kDynPerThread; ++k) B = fmaf(p.a, B, drive[k]);
-  float A = p.a16;
+  for (int k = 0; k < kDynPerThread; ++k) B = fma(p.da, B, drive[k]);
+  double A = p.da16;
 
   // Warp inclusive scan of affine maps.
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
-    const float Ap = __shfl_up_sync(0xffffffffu, A, off);
-    const float Bp = __shfl_up_sync(0xffffffffu, B, off);
+    const double Ap = __shfl_up_sync(0xffffffffu, A, off);
+    const double Bp = __shfl_up_sync(0xffffffffu, B, off);
     if (lane >= off) compose(A, B, Ap, Bp);
   }
   if (lane == 31) {
@@ -295,19 +308,19 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
     wB[warp] = B;
   }
   // Exclusive prefix within the warp.
-  float xA = __shfl_up_sync(0xffffffffu, A, 1), xB = __shfl_up_sync(0xffffffffu, B, 1);
+  double xA = __shfl_up_sync(0xffffffffu, A, 1), xB = __shfl_up_sync(0xffffffffu, B, 1);
   if (lane == 0) {
-    xA = 1.f;
-    xB = 0.f;
+    xA = 1.0;
+    xB = 0.0;
   }
   __syncthreads();
   if (warp == 0) {
-    float tA = lane < NT / 32 ? wA[lane] : 1.f;
-    float tB = lane < NT / 32 ? wB[lane] : 0.f;
+    double tA = lane < NT / 32 ? wA[lane] : 1.0;
+    double tB = lane < NT / 32 ? wB[lane] : 0.0;
 #pragma unroll
     for (int off = 1; off < NT / 32; off <<= 1) {
-      const float Ap = __shfl_up_sync(0xffffffffu, tA, off);
-      const float Bp = __shfl_up_sync(0xffffffffu, tB, off);
+      const double Ap = __shfl_up_sync(0xffffffffu, tA, off);
+      const double Bp = __shfl_up_sync(0xffffffffu, tB, off);
       if (lane >= off) compose(tA, tB, Ap, Bp);
     }
     if (lane < NT / 32) {
@@ -317,10 +330,10 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
   }
   __syncthreads();
   if (warp > 0) {  // prepend the previous warps' prefix
-    float pA = wA[warp - 1], pB = wB[warp - 1];
+    const double pA = wA[warp - 1], pB = wB[warp - 1];
     compose(xA, xB, pA, pB);
   }
-  const float tileB = wB[NT / 32 - 1];
+  const double tileB = wB[NT / 32 - 1];
 
   if (warp == 0) {
     // Cross-tile carry, deterministic: publish this tile's aggregate B, then
@@ -329,23 +342,26 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
     // aggregates are read (no chain of inclusive prefixes), so no tile waits on another
     // tile's look-back, and the value never depends on timing. Windows stop once the
     // largest remaining weight A^d underflows to exactly 0 (all later terms are +0).
-    // status is indexed [seq][tile]
+    // status is indexed [seq][tile]: the fp64 aggregate's bits + 1 (0 = not yet published;
+    // the +1 never wraps: an all-ones pattern is a NaN, which an aggregate is not)
     cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> mine(status[static_cast<long>(seq) * tiles_per_seq + tile]);
-    if (lane == 0) mine.store(kFlagAgg | __float_as_uint(tileB), cuda::memory_order_relaxed);
-    float part = 0.f;
-    // weight A^d = A^lane * (A^32)^(d0/32): one powf per lane, then exact-order products
-    const float wl = tile > 0 ? powf(p.atile, static_cast<float>(lane)) : 0.f;
-    float w32 = 1.f;  // (A^32)^(d0/32)
-    for (int d0 = 0; d0 < tile; d0 += 32, w32 *= p.atile32) {
-      if (w32 == 0.f) break;
+    if (lane == 0) {
+      mine.store(static_cast<unsigned long long>(__double_as_longlong(tileB)) + 1ull, cuda::memory_order_relaxed);
+    }
+    double part = 0.0;
+    // weight A^d = A^lane * (A^32)^(d0/32): one pow per lane, then exact-order products
+    const double wl = tile > 0 ? pow(p.datile, static_cast<double>(lane)) : 0.0;
+    double w32 = 1.0;  // (A^32)^(d0/32)
+    for (int d0 = 0; d0 < tile; d0 += 32, w32 *= p.datile32) {
+      if (w32 == 0.0) break;
       const int d = d0 + lane;
       if (d < tile) {
         cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[static_cast<long>(seq) * tiles_per_seq + tile - 1 - d]);
         unsigned long long w;
         do {
           w = st.load(cuda::memory_order_relaxed);
-        } while ((w >> 32) == 0);
-        part = fmaf(wl * w32, __uint_as_float(static_cast<unsigned int>(w & 0xffffffffu)), part);
+        } while (w == 0ull);
+        part = fma(wl * w32, __longlong_as_double(static_cast<long long>(w - 1ull)), part);
       }
     }
 #pragma unroll
@@ -355,7 +371,7 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
   __syncthreads();
 
   // Replay the recurrence from this thread's true start state, apply the gain, store.
-  float g = fmaf(xA, s_carry, xB);
+  double g = fma(xA, s_carry, xB);
   if (n0 >= a.length) return;
   float* ol = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length + n0;
   float* orr = ol + a.length;
@@ -369,11 +385,12 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
 #pragma unroll
     for (int k4 = 0; k4 < 4; ++k4) {
       const int k = 4 * q + k4;
-      g = fmaf(p.a, g, drive[k]);
+      g = fma(p.da, g, drive[k]);
+      const float gf = static_cast<float>(g);
       if constexpr (ENV) {
-        if (n0 + k < a.length) env[static_cast<long>(seq) * a.length + n0 + k] = g;
+        if (n0 + k < a.length) env[static_cast<long>(seq) * a.length + n0 + k] = gf;
       }
-      const float gn = gain_of<GATE>(g, p);
+      const float gn = gain_of<GATE>(gf, p);
       yl[k4] = gn * ul[k4];
       yr[k4] = gn * ur[k4];
     }

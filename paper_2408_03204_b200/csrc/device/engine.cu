@@ -159,6 +159,7 @@ ProcessorSet::ProcessorSet(const ProcessorConfig& config) : config_(config) {
   dev_ = std::make_unique<DeviceConstants>();
   cuda_check(cudaGetDevice(&dev_->device), "cudaGetDevice");
   mgb::twiddle_table(dev_->device);
+  mgb::twiddle_table64(dev_->device);
   mgb::eq_basis(dev_->device);
   dev_->frames = static_cast<int>((reverb_length_ + kReverbStftHop - 1) / kReverbStftHop);
   const std::size_t stft_bytes = sizeof(float2) * static_cast<std::size_t>(dev_->frames) * (kReverbStftLength / 2 + 1);
@@ -555,6 +556,7 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
   char* ws = static_cast<char*>(workspace);
   const long rowstride = static_cast<long>(batch) * 2 * length;
   const float2* tw = mgb::twiddle_table(procs.device().device);
+  const double2* tw64 = mgb::twiddle_table64(procs.device().device);
   std::vector<mgb::StepArgs> args(rd.steps.size());
   for (std::size_t k = 0; k < rd.steps.size(); ++k) {
     const StepIndex& st = rd.steps[k];
@@ -571,6 +573,7 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
       a.params = table + static_cast<long>(st.param_begin) * width;
     }
     a.tw = tw;
+    a.tw64 = tw64;
     a.slots = st.store_end - st.store_begin;
     a.batch = batch;
     a.length = length;
@@ -675,6 +678,7 @@ void backward_arena(const DevicePlan& plan, const ProcessorSet& procs, const dou
   char* scratch = ws + lay.total;
   const long rowstride = static_cast<long>(batch) * 2 * length;
   const float2* tw = mgb::twiddle_table(procs.device().device);
+  const double2* tw64 = mgb::twiddle_table64(procs.device().device);
   const int nsteps = static_cast<int>(rd.steps.size());
   for (int k = nsteps - 1; k >= 0; --k) {
     const StepIndex& st = rd.steps[static_cast<std::size_t>(k)];
@@ -696,6 +700,7 @@ void backward_arena(const DevicePlan& plan, const ProcessorSet& procs, const dou
       grad = grad_tables[static_cast<int>(t)] + static_cast<long>(st.param_begin) * width;
     }
     fw.tw = tw;
+    fw.tw64 = tw64;
     fw.slots = st.store_end - st.store_begin;
     fw.batch = batch;
     fw.length = length;
@@ -740,6 +745,7 @@ void backward_arena(const DevicePlan& plan, const ProcessorSet& procs, const dou
     bw.row_ptr = plan.t_row_ptr(nsteps);
     bw.col = plan.t_col(nsteps);
     bw.tw = tw;
+    bw.tw64 = tw64;
     bw.slots = rd.num_inputs;
     bw.batch = batch;
     bw.length = length;
@@ -764,6 +770,7 @@ void profile_steps(const DevicePlan& plan, const ProcessorSet& procs, const doub
   char* ws = static_cast<char*>(workspace);
   const long rowstride = static_cast<long>(batch) * 2 * length;
   const float2* tw = mgb::twiddle_table(procs.device().device);
+  const double2* tw64 = mgb::twiddle_table64(procs.device().device);
   cudaEvent_t e0, e1;
   cuda_check(cudaEventCreate(&e0), "event");
   cuda_check(cudaEventCreate(&e1), "event");
@@ -780,6 +787,7 @@ void profile_steps(const DevicePlan& plan, const ProcessorSet& procs, const doub
     a.col = plan.col(static_cast<int>(k));
     a.params = width > 0 ? param_tables[static_cast<int>(st.type)] + static_cast<long>(st.param_begin) * width : nullptr;
     a.tw = tw;
+    a.tw64 = tw64;
     a.slots = st.store_end - st.store_begin;
     a.batch = batch;
     a.length = length;
@@ -1466,6 +1474,7 @@ void ProcessorSet::process_device(NodeType type, const float* in, float* out, in
   a.batch = batch;
   a.length = length;
   a.tw = mgb::twiddle_table(dev_->device);
+  a.tw64 = mgb::twiddle_table64(dev_->device);
   a.rowstride = static_cast<long>(batch) * 2 * length;
   run_step(type, a, *this, aux + align256(sizeof(int) * idx.size()), stream);
   cuda_check(cudaGetLastError(), "process launch");

@@ -280,12 +280,12 @@ __global__ void eq_basis_build(float* tiled) {
 // 4096 (2048 outputs per block: 2.2x less FFT work per CTA and 3x the CTAs, for steps whose
 // 8192 grid would not fill the GPU, e.g. a 1-slot bus EQ). The taps span +-1023 < 2048, so
 // the 4096-point response is exactly every other bin of the 8192-point one.
-template <int LOG> struct EqWin {
+template <int LOG, typename C = float2> struct EqWin {
   static constexpr int kFft = 1 << LOG;
   static constexpr int kOut = LOG == 13 ? 6144 : 2048;
   static constexpr int kThreads = LOG == 13 ? 512 : 256;
-  static constexpr int kMinBlocks = 2;
-  static constexpr int kSmem = padded(kFft) * 8;
+  static constexpr int kMinBlocks = sizeof(C) == 8 ? 2 : 1;
+  static constexpr int kSmem = padded(kFft) * static_cast<int>(sizeof(C));
   static_assert(kOut <= kFft - 2 * kEqHalf, "EQ block larger than the non-wrapped window");
 };
 
@@ -293,13 +293,17 @@ template <int LOG> struct EqWin {
 // kFft-sample window starting at out0 - 1024; the circular convolution is exact for window
 // indices [1023, kFft - 1024]. Window loads feed the first FFT pass directly and the last
 // inverse pass stores directly (register-ended transforms, fft_smem.cuh), both coalesced.
-template <int LOG>
-__global__ void __launch_bounds__(EqWin<LOG>::kThreads, EqWin<LOG>::kMinBlocks) eq_conv(StepArgs a, const float* resp) {
-  using W = EqWin<LOG>;
+// C: transform element type (float2, or double2: fp64 arithmetic, fp32 arena in and out).
+template <int LOG, typename C>
+__global__ void __launch_bounds__(EqWin<LOG, C>::kThreads, EqWin<LOG, C>::kMinBlocks) eq_conv(StepArgs a, const float* resp) {
+  using W = EqWin<LOG, C>;
+  using T = RealOf<C>;
   constexpr int kEqFft = W::kFft, kEqOut = W::kOut, kNt = W::kThreads;
   constexpr int kRs = kEqFft == 8192 ? 1 : 8192 / kEqFft;   // response bin stride
-  const float rscale = static_cast<float>(kRs);            // response is prescaled by 1/8192
-  extern __shared__ float2 buf[];
+  const T rscale = static_cast<T>(kRs);                    // response is prescaled by 1/8192
+  extern __shared__ __align__(16) unsigned char eq_smem[];
+  C* buf = reinterpret_cast<C*>(eq_smem);
+  const C* tw = twiddles<C>(a);
   const int sb = blockIdx.y;
   const int slot = sb / a.batch, b = sb - slot * a.batch;
   const int e0 = slot_e0(a, slot), e1 = slot_e1(a, slot);
@@ -314,57 +318,57 @@ __global__ void __launch_bounds__(EqWin<LOG>::kThreads, EqWin<LOG>::kMinBlocks) 
   // edge order (as the reference's gather).
   constexpr int M1 = kEqFft / 16;
   static_assert(M1 == kNt, "eq_conv: threads must be the first pass's butterflies");
-  float2 v[16];
+  C v[16];
 #pragma unroll
-  for (int r = 0; r < 16; ++r) v[r] = make_float2(0.f, 0.f);
+  for (int r = 0; r < 16; ++r) v[r] = Cx<C>::mk(T(0), T(0));
   for (int e = e0; e < e1; ++e) {
     const float* p = a.src + edge_row(a, e) * a.rowstride + boff;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       const long pos = s0 + threadIdx.x + r * M1;
       if (pos >= 0 && pos < a.length) {
-        v[r].x += __ldg(p + pos);
-        v[r].y += __ldg(p + a.length + pos);
+        v[r].x += static_cast<T>(__ldg(p + pos));
+        v[r].y += static_cast<T>(__ldg(p + a.length + pos));
       }
     }
   }
   fft_first_from_regs<-1>(v, buf, threadIdx.x);
   __syncthreads();
-  fft_middle<LOG, 1, kNt, -1>(buf, padded(kEqFft), a.tw);
+  fft_middle<LOG, 1, kNt, -1>(buf, padded(kEqFft), tw);
   // Last forward pass into registers, multiplied by the response and written back (in place:
   // after every thread has read its inputs).
   constexpr int NS = Pow2Plan<LOG>::kLastNs, R = Pow2Plan<LOG>::kLastR, PL = NS / kNt;
-  float2 o[PL][R];
+  C o[PL][R];
 #pragma unroll
-  for (int p = 0; p < PL; ++p) fft_last_to_regs<LOG, -1>(buf, threadIdx.x + p * kNt, a.tw, o[p]);
+  for (int p = 0; p < PL; ++p) fft_last_to_regs<LOG, -1>(buf, threadIdx.x + p * kNt, tw, o[p]);
   __syncthreads();
 #pragma unroll
   for (int p = 0; p < PL; ++p) {
     const int j = threadIdx.x + p * kNt;
-    float2* sb = buf + sidx(j);
+    C* sb = buf + sidx(j);
 #pragma unroll
-    for (int r = 0; r < R; ++r) sb[r * padded(NS)] = cscale(o[p][r], rscale * __ldg(rs + kRs * (j + r * NS)));
+    for (int r = 0; r < R; ++r) sb[r * padded(NS)] = cscale(o[p][r], rscale * static_cast<T>(__ldg(rs + kRs * (j + r * NS))));
   }
   __syncthreads();
   }
   // Inverse: every pass but the last in smem, the last into registers and straight to the
   // arena (window index w = j + r*NS holds output out0 + w - 1024 for w in [1024, 1024 + kEqOut)).
-  fft_all_but_last<LOG, 1, kNt, +1>(buf, padded(kEqFft), a.tw);
+  fft_all_but_last<LOG, 1, kNt, +1>(buf, padded(kEqFft), tw);
   constexpr int NS = Pow2Plan<LOG>::kLastNs, R = Pow2Plan<LOG>::kLastR, PL = NS / kNt;
   float* yl = a.dst + static_cast<long>(slot) * a.rowstride + boff;
   float* yr = yl + a.length;
 #pragma unroll
   for (int p = 0; p < PL; ++p) {
     const int j = threadIdx.x + p * kNt;
-    float2 y[R];
-    fft_last_to_regs<LOG, +1>(buf, j, a.tw, y);
+    C y[R];
+    fft_last_to_regs<LOG, +1>(buf, j, tw, y);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int w = j + r * NS;
       const long pos = out0 + w - (kEqHalf + 1);
       if (w >= kEqHalf + 1 && w < kEqHalf + 1 + kEqOut && pos < a.length) {
-        yl[pos] = y[r].x;
-        yr[pos] = y[r].y;
+        yl[pos] = static_cast<float>(y[r].x);
+        yr[pos] = static_cast<float>(y[r].y);
       }
     }
   }
@@ -376,8 +380,12 @@ void eq_setup() {
   static const bool done = [] {
     cudaFuncSetAttribute(eq_response, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqSmem);
     cudaFuncSetAttribute(eq_response_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, kBasisSmem);
-    for (auto fn : {eq_conv<13>, eq_conv<12>}) {
+    for (auto fn : {eq_conv<13, float2>, eq_conv<12, float2>}) {
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqSmem);
+      cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
+    for (auto fn : {eq_conv<13, double2>, eq_conv<12, double2>}) {
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kEqSmem);
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     }
     return true;
@@ -462,11 +470,19 @@ bool eq_uses_small_window(const StepArgs& a) {
 void launch_eq_main(const StepArgs& a, const float* resp_ws, cudaStream_t s) {
   if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
   eq_setup();
-  if (eq_uses_small_window(a)) {
-    eq_conv<12><<<eq_grid<12>(a), EqWin<12>::kThreads, EqWin<12>::kSmem, s>>>(a, resp_ws);
+  if (fft_fp64()) {
+    if (eq_uses_small_window(a)) {
+      eq_conv<12, double2><<<eq_grid<12>(a), EqWin<12>::kThreads, EqWin<12, double2>::kSmem, s>>>(a, resp_ws);
+      return;
+    }
+    eq_conv<13, double2><<<eq_grid<13>(a), 512, EqWin<13, double2>::kSmem, s>>>(a, resp_ws);
     return;
   }
-  eq_conv<13><<<eq_grid<13>(a), 512, kEqSmem, s>>>(a, resp_ws);
+  if (eq_uses_small_window(a)) {
+    eq_conv<12, float2><<<eq_grid<12>(a), EqWin<12>::kThreads, EqWin<12>::kSmem, s>>>(a, resp_ws);
+    return;
+  }
+  eq_conv<13, float2><<<eq_grid<13>(a), 512, kEqSmem, s>>>(a, resp_ws);
 }
 
 }  // namespace mgb

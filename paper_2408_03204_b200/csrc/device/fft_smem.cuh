@@ -1,32 +1,49 @@
-// Shared-memory Stockham FFT building blocks (sm_100a, fp32 complex).
+// Shared-memory Stockham FFT building blocks (sm_100a), generic over the complex element
+// type: float2 (fp32) or double2 (fp64 arithmetic for the precision-critical convolutions).
 //
 // Replaces the reference's FFTW c2c transforms (`proj/src/dsp.cpp:46-56`) on the device.
 // All sizes, radices and pass strides are compile-time so index math folds to shifts and
 // the register-resident radix-R DFTs have constant twiddles. A pass reads every butterfly
 // input into registers, barriers, then writes the outputs in place (Stockham auto-sort:
 // natural order in, natural order out, no bit reversal). Pass twiddles
-// exp(dir*2*pi*i * j*r / (Ns*R)) are read from a precomputed fp64-rounded table.
+// exp(dir*2*pi*i * j*r / (Ns*R)) are read from a precomputed table (fp32 rounded from fp64,
+// or fp64).
 #pragma once
 
 #include <cuda_runtime.h>
 
 namespace mgb {
 
-struct c2 {
-  float x, y;
+// Scalar type of a complex element and its constructor.
+template <typename C> struct Cx;
+template <> struct Cx<float2> {
+  using Real = float;
+  static __host__ __device__ __forceinline__ float2 mk(float re, float im) { return make_float2(re, im); }
 };
+template <> struct Cx<double2> {
+  using Real = double;
+  static __host__ __device__ __forceinline__ double2 mk(double re, double im) { return make_double2(re, im); }
+};
+template <typename C> using RealOf = typename Cx<C>::Real;
 
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
-__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+template <typename C>
+__device__ __forceinline__ C cadd(C a, C b) { return Cx<C>::mk(a.x + b.x, a.y + b.y); }
+template <typename C>
+__device__ __forceinline__ C csub(C a, C b) { return Cx<C>::mk(a.x - b.x, a.y - b.y); }
+template <typename C>
+__device__ __forceinline__ C cconj(C a) { return Cx<C>::mk(a.x, -a.y); }
+template <typename C>
+__device__ __forceinline__ C cscale(C a, RealOf<C> s) { return Cx<C>::mk(a.x * s, a.y * s); }
 // a * (dir * i)
-template <int DIR>
-__device__ __forceinline__ float2 cmul_i(float2 a) {
-  return DIR < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
+template <int DIR, typename C>
+__device__ __forceinline__ C cmul_i(C a) {
+  return DIR < 0 ? Cx<C>::mk(a.y, -a.x) : Cx<C>::mk(-a.y, a.x);
 }
 
 // exp(i*pi*x)
@@ -35,26 +52,36 @@ __device__ __forceinline__ float2 expi_pi(float x) {
   sincospif(x, &s, &c);
   return make_float2(c, s);
 }
+__device__ __forceinline__ double2 expi_pi(double x) {
+  double s, c;
+  sincospi(x, &s, &c);
+  return make_double2(c, s);
+}
+// Widening / narrowing between the arena's fp32 and a transform's element type.
+template <typename C>
+__device__ __forceinline__ C widen(float2 v) { return Cx<C>::mk(v.x, v.y); }
+__device__ __forceinline__ float2 narrow(float2 v) { return v; }
+__device__ __forceinline__ float2 narrow(double2 v) { return make_float2(static_cast<float>(v.x), static_cast<float>(v.y)); }
 
 // ---- register DFTs of size R (DIT split, constant twiddles) --------------------------
 
-template <int R, int DIR>
+template <int R, int DIR, typename C = float2>
 struct Dft;
 
-template <int DIR>
-struct Dft<2, DIR> {
-  static __device__ __forceinline__ void run(float2* v) {
-    const float2 a = v[0], b = v[1];
+template <int DIR, typename C>
+struct Dft<2, DIR, C> {
+  static __device__ __forceinline__ void run(C* v) {
+    const C a = v[0], b = v[1];
     v[0] = cadd(a, b);
     v[1] = csub(a, b);
   }
 };
 
-template <int DIR>
-struct Dft<4, DIR> {
-  static __device__ __forceinline__ void run(float2* v) {
-    const float2 t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
-    const float2 t2 = cadd(v[1], v[3]), t3 = cmul_i<DIR>(csub(v[1], v[3]));
+template <int DIR, typename C>
+struct Dft<4, DIR, C> {
+  static __device__ __forceinline__ void run(C* v) {
+    const C t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+    const C t2 = cadd(v[1], v[3]), t3 = cmul_i<DIR>(csub(v[1], v[3]));
     v[0] = cadd(t0, t2);
     v[2] = csub(t0, t2);
     v[1] = cadd(t1, t3);
@@ -62,18 +89,19 @@ struct Dft<4, DIR> {
   }
 };
 
-template <int DIR>
-struct Dft<8, DIR> {
-  static __device__ __forceinline__ void run(float2* v) {
-    float2 e[4] = {v[0], v[2], v[4], v[6]};
-    float2 o[4] = {v[1], v[3], v[5], v[7]};
-    Dft<4, DIR>::run(e);
-    Dft<4, DIR>::run(o);
-    constexpr float h = 0.70710678118654752440f;
+template <int DIR, typename C>
+struct Dft<8, DIR, C> {
+  static __device__ __forceinline__ void run(C* v) {
+    using T = RealOf<C>;
+    C e[4] = {v[0], v[2], v[4], v[6]};
+    C o[4] = {v[1], v[3], v[5], v[7]};
+    Dft<4, DIR, C>::run(e);
+    Dft<4, DIR, C>::run(o);
+    constexpr T h = static_cast<T>(0.70710678118654752440);
     // o[k] *= exp(dir*2*pi*i*k/8)
-    o[1] = make_float2(h * (o[1].x - DIR * o[1].y), h * (o[1].y + DIR * o[1].x));
+    o[1] = Cx<C>::mk(h * (o[1].x - DIR * o[1].y), h * (o[1].y + DIR * o[1].x));
     o[2] = cmul_i<DIR>(o[2]);
-    o[3] = make_float2(h * (-o[3].x - DIR * o[3].y), h * (-o[3].y + DIR * o[3].x));
+    o[3] = Cx<C>::mk(h * (-o[3].x - DIR * o[3].y), h * (-o[3].y + DIR * o[3].x));
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       v[k] = cadd(e[k], o[k]);
@@ -82,23 +110,25 @@ struct Dft<8, DIR> {
   }
 };
 
-template <int DIR>
-struct Dft<16, DIR> {
-  static __device__ __forceinline__ void run(float2* v) {
-    float2 e[8], o[8];
+template <int DIR, typename C>
+struct Dft<16, DIR, C> {
+  static __device__ __forceinline__ void run(C* v) {
+    using T = RealOf<C>;
+    C e[8], o[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       e[k] = v[2 * k];
       o[k] = v[2 * k + 1];
     }
-    Dft<8, DIR>::run(e);
-    Dft<8, DIR>::run(o);
+    Dft<8, DIR, C>::run(e);
+    Dft<8, DIR, C>::run(o);
     // o[k] *= exp(dir*2*pi*i*k/16)
-    constexpr float c1 = 0.92387953251128675613f, s1 = 0.38268343236508977173f, h = 0.70710678118654752440f;
-    constexpr float cs[8] = {1.f, c1, h, s1, 0.f, -s1, -h, -c1};
-    constexpr float sn[8] = {0.f, s1, h, c1, 1.f, c1, h, s1};
+    constexpr T c1 = static_cast<T>(0.92387953251128675613), s1 = static_cast<T>(0.38268343236508977173),
+                h = static_cast<T>(0.70710678118654752440);
+    constexpr T cs[8] = {T(1), c1, h, s1, T(0), -s1, -h, -c1};
+    constexpr T sn[8] = {T(0), s1, h, c1, T(1), c1, h, s1};
 #pragma unroll
-    for (int k = 1; k < 8; ++k) o[k] = cmul(o[k], make_float2(cs[k], DIR * sn[k]));
+    for (int k = 1; k < 8; ++k) o[k] = cmul(o[k], Cx<C>::mk(cs[k], DIR * sn[k]));
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       v[k] = cadd(e[k], o[k]);
@@ -107,30 +137,32 @@ struct Dft<16, DIR> {
   }
 };
 
-template <int DIR>
-struct Dft<3, DIR> {
-  static __device__ __forceinline__ void run(float2* v) {
-    constexpr float c = -0.5f;
-    constexpr float s = 0.86602540378443864676f * DIR;  // sin(dir*2*pi/3)
-    const float2 a = v[0], b = v[1], d = v[2];
-    const float2 sum = cadd(b, d), dif = csub(b, d);
+template <int DIR, typename C>
+struct Dft<3, DIR, C> {
+  static __device__ __forceinline__ void run(C* v) {
+    using T = RealOf<C>;
+    constexpr T c = T(-0.5);
+    constexpr T s = static_cast<T>(0.86602540378443864676) * DIR;  // sin(dir*2*pi/3)
+    const C a = v[0], b = v[1], d = v[2];
+    const C sum = cadd(b, d), dif = csub(b, d);
     v[0] = cadd(a, sum);
-    const float2 m = make_float2(a.x + c * sum.x, a.y + c * sum.y);
-    const float2 r = make_float2(-s * dif.y, s * dif.x);  // i*s*(b-d)
+    const C m = Cx<C>::mk(a.x + c * sum.x, a.y + c * sum.y);
+    const C r = Cx<C>::mk(-s * dif.y, s * dif.x);  // i*s*(b-d)
     v[1] = cadd(m, r);
     v[2] = csub(m, r);
   }
 };
 
 // Twiddles w[r] = exp(dir*2*pi*i * r * x / 2), r < R, for x = 2*j/(Ns*R) (so w[1] = exp(i*pi*dir*x)).
-template <int R, int DIR>
-__device__ __forceinline__ void pass_twiddles(float x, float2* w) {
-  const float s = DIR * x;
+template <int R, int DIR, typename C>
+__device__ __forceinline__ void pass_twiddles(RealOf<C> x, C* w) {
+  using T = RealOf<C>;
+  const T s = DIR * x;
   w[1] = expi_pi(s);
-  if constexpr (R >= 3) w[2] = expi_pi(2.f * s);
+  if constexpr (R >= 3) w[2] = expi_pi(T(2) * s);
   if constexpr (R >= 4) w[3] = cmul(w[1], w[2]);
   if constexpr (R >= 8) {
-    w[4] = expi_pi(4.f * s);
+    w[4] = expi_pi(T(4) * s);
     w[5] = cmul(w[1], w[4]);
     w[6] = cmul(w[2], w[4]);
     w[7] = cmul(w[3], w[4]);
@@ -154,22 +186,22 @@ __host__ __device__ constexpr int padded(int n) { return n + (n >> 4); }
 // Twiddles exp(dir*2*pi*i * jm*r / (NS*R)) come from `tw` when given (N | kTwN), else sincospif.
 // Table twiddles for one butterfly: loads w^1, w^2, w^4, w^8 (as many as R needs) from the
 // forward table at stride `step` and conjugates them for the inverse transform.
-template <int R, int DIR>
+template <int R, int DIR, typename C = float2>
 struct TwBase {
-  float2 w[4];
-  __device__ __forceinline__ void load(const float2* __restrict__ tw, int step) {
+  C w[4];
+  __device__ __forceinline__ void load(const C* __restrict__ tw, int step) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if ((1 << i) < R) {
-        float2 v = tw[step << i];
+        C v = tw[step << i];
         if (DIR > 0) v.y = -v.y;
         w[i] = v;
       }
     }
   }
   // v[r] *= w^r for r = 1..R-1 (w^3 = w w^2, w^5..w^7 via w^4, w^9..w^15 via w^8: <= 3 products)
-  __device__ __forceinline__ void apply(float2* v) const {
-    float2 p[16];
+  __device__ __forceinline__ void apply(C* v) const {
+    C p[16];
     p[1] = w[0];
     if constexpr (R > 2) p[2] = w[1];
     if constexpr (R > 3) p[3] = cmul(w[0], w[1]);
@@ -194,14 +226,15 @@ struct TwBase {
 // threads participate. Twiddles exp(dir*2*pi*i * jm*r / (NS*R)) come from the table `tw`
 // (TWN entries) when given, else sincospif; table loads are issued before the barrier-
 // separated smem reads so their latency overlaps them.
-template <int N, int R, int NS, int COUNT, int NTHR, int DIR, int TWN = kTwN, bool PAD = true>
-__device__ __forceinline__ void stockham_pass(float2* buf, int fstride, const float2* __restrict__ tw) {
+template <int N, int R, int NS, int COUNT, int NTHR, int DIR, int TWN = kTwN, bool PAD = true, typename C>
+__device__ __forceinline__ void stockham_pass(C* buf, int fstride, const C* __restrict__ tw) {
+  using T = RealOf<C>;
   constexpr int M = N / R;                 // butterflies per transform
   constexpr int TOTAL = COUNT * M;
   constexpr int PER = (TOTAL + NTHR - 1) / NTHR;
   const int tid = threadIdx.x;
-  float2 v[PER][R];
-  TwBase<R, DIR> twb[PER];
+  C v[PER][R];
+  TwBase<R, DIR, C> twb[PER];
   if constexpr (NS > 1) {
     if (tw != nullptr) {
 #pragma unroll
@@ -219,11 +252,11 @@ __device__ __forceinline__ void stockham_pass(float2* buf, int fstride, const fl
     const int b = tid + q * NTHR;
     if (TOTAL % NTHR == 0 || b < TOTAL) {
       const int f = b / M, j = b - f * M;
-      const float2* base = buf + f * fstride;
+      const C* base = buf + f * fstride;
       if constexpr (PAD && M % 16 == 0) {
         // j + r*M with M a multiple of 16: sidx(j + r*M) = sidx(j) + r*padded(M), so every
         // load is one base register plus an immediate offset (no per-element index math).
-        const float2* lb = base + sidx(j);
+        const C* lb = base + sidx(j);
 #pragma unroll
         for (int r = 0; r < R; ++r) v[q][r] = lb[r * padded(M)];
       } else {
@@ -243,21 +276,21 @@ __device__ __forceinline__ void stockham_pass(float2* buf, int fstride, const fl
         if (tw != nullptr) {
           twb[q].apply(v[q]);
         } else {
-          float2 w[R];
-          pass_twiddles<R, DIR>(2.f * static_cast<float>(jm) / static_cast<float>(NS * R), w);
+          C w[R];
+          pass_twiddles<R, DIR, C>(T(2) * static_cast<T>(jm) / static_cast<T>(NS * R), w);
 #pragma unroll
           for (int r = 1; r < R; ++r) v[q][r] = cmul(v[q][r], w[r]);
         }
       }
-      Dft<R, DIR>::run(v[q]);
-      float2* base = buf + f * fstride;
+      Dft<R, DIR, C>::run(v[q]);
+      C* base = buf + f * fstride;
       const int o0 = (j / NS) * NS * R + jm;
       if constexpr (PAD && NS % 16 == 0) {
-        float2* sb = base + sidx(o0);  // o0 + r*NS, NS a multiple of 16: immediate offsets
+        C* sb = base + sidx(o0);  // o0 + r*NS, NS a multiple of 16: immediate offsets
 #pragma unroll
         for (int r = 0; r < R; ++r) sb[r * padded(NS)] = v[q][r];
       } else if constexpr (PAD && NS == 1 && R == 16) {
-        float2* sb = base + 17 * j;    // o0 = 16 j: sidx(16 j + r) = 17 j + r
+        C* sb = base + 17 * j;    // o0 = 16 j: sidx(16 j + r) = 17 j + r
 #pragma unroll
         for (int r = 0; r < R; ++r) sb[r] = v[q][r];
       } else {
@@ -272,22 +305,22 @@ __device__ __forceinline__ void stockham_pass(float2* buf, int fstride, const fl
 // Power-of-two FFT on the padded layout: a radix-16 first pass, then radix-8 passes,
 // finishing with radix 4/2 (or 4+4 when 16 remain). Element i of transform f lives at
 // buf[f*fstride + sidx(i)].
-template <int LOG2N, int LOGNS, int COUNT, int NTHR, int DIR>
+template <int LOG2N, int LOGNS, int COUNT, int NTHR, int DIR, typename C>
 struct Pow2Fft {
-  static __device__ __forceinline__ void run(float2* buf, int fstride, const float2* tw) {
+  static __device__ __forceinline__ void run(C* buf, int fstride, const C* tw) {
     constexpr int REM = LOG2N - LOGNS;
     if constexpr (REM > 0) {
       constexpr int RL = (LOGNS == 0 && REM >= 4) ? 4 : ((REM == 4 || REM == 2) ? 2 : (REM == 1 ? 1 : 3));
       stockham_pass<(1 << LOG2N), (1 << RL), (1 << LOGNS), COUNT, NTHR, DIR>(buf, fstride, tw);
-      Pow2Fft<LOG2N, LOGNS + RL, COUNT, NTHR, DIR>::run(buf, fstride, tw);
+      Pow2Fft<LOG2N, LOGNS + RL, COUNT, NTHR, DIR, C>::run(buf, fstride, tw);
     }
   }
 };
 
-template <int LOG2N, int COUNT, int NTHR, int DIR>
-__device__ __forceinline__ void fft_pow2(float2* buf, int fstride, const float2* tw) {
+template <int LOG2N, int COUNT, int NTHR, int DIR, typename C>
+__device__ __forceinline__ void fft_pow2(C* buf, int fstride, const C* tw) {
   static_assert((1 << LOG2N) <= kTwN, "pow2 smem FFT larger than the twiddle table");
-  Pow2Fft<LOG2N, 0, COUNT, NTHR, DIR>::run(buf, fstride, tw);
+  Pow2Fft<LOG2N, 0, COUNT, NTHR, DIR, C>::run(buf, fstride, tw);
 }
 
 // ---- register-ended transforms ------------------------------------------------------------
@@ -314,64 +347,64 @@ struct Pow2Plan {
   static_assert(LOG2N >= 6 && pow2_rl(LOG2N, 0) == 4 && kLastLogNs >= 4, "register-ended plan needs 2+ passes");
 };
 
-template <int LOG2N, int LOGNS, int LOGEND, int COUNT, int NTHR, int DIR>
+template <int LOG2N, int LOGNS, int LOGEND, int COUNT, int NTHR, int DIR, typename C>
 struct Pow2FftRange {
-  static __device__ __forceinline__ void run(float2* buf, int fstride, const float2* tw) {
+  static __device__ __forceinline__ void run(C* buf, int fstride, const C* tw) {
     if constexpr (LOGNS < LOGEND) {
       constexpr int RL = pow2_rl(LOG2N, LOGNS);
       stockham_pass<(1 << LOG2N), (1 << RL), (1 << LOGNS), COUNT, NTHR, DIR>(buf, fstride, tw);
-      Pow2FftRange<LOG2N, LOGNS + RL, LOGEND, COUNT, NTHR, DIR>::run(buf, fstride, tw);
+      Pow2FftRange<LOG2N, LOGNS + RL, LOGEND, COUNT, NTHR, DIR, C>::run(buf, fstride, tw);
     }
   }
 };
 
 // First pass (radix 16, no twiddles) of butterfly j of the transform at `base`:
 // v[r] = element j + r*N/16 on entry. Writes the pass outputs; the caller barriers.
-template <int DIR>
-__device__ __forceinline__ void fft_first_from_regs(float2 (&v)[16], float2* base, int j) {
-  Dft<16, DIR>::run(v);
-  float2* sb = base + 17 * j;  // outputs 16 j + r: sidx(16 j + r) = 17 j + r
+template <int DIR, typename C>
+__device__ __forceinline__ void fft_first_from_regs(C (&v)[16], C* base, int j) {
+  Dft<16, DIR, C>::run(v);
+  C* sb = base + 17 * j;  // outputs 16 j + r: sidx(16 j + r) = 17 j + r
 #pragma unroll
   for (int r = 0; r < 16; ++r) sb[r] = v[r];
 }
 
 // Passes between the first and the last (they start and end with a barrier).
-template <int LOG2N, int COUNT, int NTHR, int DIR>
-__device__ __forceinline__ void fft_middle(float2* buf, int fstride, const float2* tw) {
-  Pow2FftRange<LOG2N, 4, Pow2Plan<LOG2N>::kLastLogNs, COUNT, NTHR, DIR>::run(buf, fstride, tw);
+template <int LOG2N, int COUNT, int NTHR, int DIR, typename C>
+__device__ __forceinline__ void fft_middle(C* buf, int fstride, const C* tw) {
+  Pow2FftRange<LOG2N, 4, Pow2Plan<LOG2N>::kLastLogNs, COUNT, NTHR, DIR, C>::run(buf, fstride, tw);
 }
 
 // Every pass after the first (the first ran from registers; starts and ends with a barrier).
-template <int LOG2N, int COUNT, int NTHR, int DIR>
-__device__ __forceinline__ void fft_after_first(float2* buf, int fstride, const float2* tw) {
-  Pow2FftRange<LOG2N, 4, LOG2N, COUNT, NTHR, DIR>::run(buf, fstride, tw);
+template <int LOG2N, int COUNT, int NTHR, int DIR, typename C>
+__device__ __forceinline__ void fft_after_first(C* buf, int fstride, const C* tw) {
+  Pow2FftRange<LOG2N, 4, LOG2N, COUNT, NTHR, DIR, C>::run(buf, fstride, tw);
 }
 
 // Every pass but the last (smem in, smem out; for a transform whose input was staged in smem).
-template <int LOG2N, int COUNT, int NTHR, int DIR>
-__device__ __forceinline__ void fft_all_but_last(float2* buf, int fstride, const float2* tw) {
-  Pow2FftRange<LOG2N, 0, Pow2Plan<LOG2N>::kLastLogNs, COUNT, NTHR, DIR>::run(buf, fstride, tw);
+template <int LOG2N, int COUNT, int NTHR, int DIR, typename C>
+__device__ __forceinline__ void fft_all_but_last(C* buf, int fstride, const C* tw) {
+  Pow2FftRange<LOG2N, 0, Pow2Plan<LOG2N>::kLastLogNs, COUNT, NTHR, DIR, C>::run(buf, fstride, tw);
 }
 
 // Last pass of butterfly j (< kLastNs) of the transform at `base`: on return v[r] = output
 // element j + r*kLastNs (reads smem after the previous pass's barrier; writes nothing).
-template <int LOG2N, int DIR>
-__device__ __forceinline__ void fft_last_to_regs(const float2* base, int j, const float2* __restrict__ tw,
-                                                 float2 (&v)[Pow2Plan<LOG2N>::kLastR]) {
+template <int LOG2N, int DIR, typename C>
+__device__ __forceinline__ void fft_last_to_regs(const C* base, int j, const C* __restrict__ tw,
+                                                 C (&v)[Pow2Plan<LOG2N>::kLastR]) {
   constexpr int NS = Pow2Plan<LOG2N>::kLastNs, R = Pow2Plan<LOG2N>::kLastR;
-  TwBase<R, DIR> twb;
+  TwBase<R, DIR, C> twb;
   twb.load(tw, j * (kTwN / (NS * R)));
-  const float2* lb = base + sidx(j);  // inputs j + r*NS, NS a multiple of 16: immediate offsets
+  const C* lb = base + sidx(j);  // inputs j + r*NS, NS a multiple of 16: immediate offsets
 #pragma unroll
   for (int r = 0; r < R; ++r) v[r] = lb[r * padded(NS)];
   twb.apply(v);
-  Dft<R, DIR>::run(v);
+  Dft<R, DIR, C>::run(v);
 }
 
 // 384 = 3 * 8 * 4 * 4 (reverb STFT frames); tw384[k] = exp(-2*pi*i*k/384), usually in smem.
 // Element i of transform f lives at buf[f*fstride + sidx(i)] (padded layout).
-template <int COUNT, int NTHR, int DIR>
-__device__ __forceinline__ void fft_384(float2* buf, int fstride, const float2* tw384) {
+template <int COUNT, int NTHR, int DIR, typename C>
+__device__ __forceinline__ void fft_384(C* buf, int fstride, const C* tw384) {
   stockham_pass<384, 3, 1, COUNT, NTHR, DIR, 384>(buf, fstride, tw384);
   stockham_pass<384, 8, 3, COUNT, NTHR, DIR, 384>(buf, fstride, tw384);
   stockham_pass<384, 4, 24, COUNT, NTHR, DIR, 384>(buf, fstride, tw384);

@@ -27,9 +27,15 @@ namespace mgb {
 
 namespace {
 
-constexpr int kColElems = 8192;  // complex elements per column tile (64 KiB)
-constexpr int kColThreads = 512;
-// Resident rows_conv threads per SM the register budget is sized for. The kernel spectrum is
+// Column tile: complex elements per CTA (64 KiB either way: 8192 fp32 or 4096 fp64 values)
+// and its threads, one per radix-16 first-pass butterfly.
+template <typename CT> struct ColCfg {
+  static constexpr int kElems = sizeof(CT) == 8 ? 8192 : 4096;
+  static constexpr int kThreads = kElems / 16;
+  static constexpr int kSmem(int n1) { return (kElems / n1) * (padded(n1) + 1) * static_cast<int>(sizeof(CT)); }
+};
+// Resident rows_conv threads per SM the register budget is sized for (half for fp64: twice the
+// registers per complex value). The kernel spectrum is
 // loaded where it is used (prefetching it into registers spilled; cp.async into shared memory
 // measured no faster).
 constexpr int kRconvThreadsPerSm = 1024;
@@ -95,13 +101,15 @@ constexpr int kMaxGridY = 65535;
 
 // ---- pass 1: column FFTs (forward) ------------------------------------------------------
 // grid (N2 / C, items); item = slot (kernel) or slot*B + b (signal).
-template <int LN1, ColSrc SRC>
-__global__ void __launch_bounds__(kColThreads, 2) cols_fwd(StepArgs a, const float2* ir, long taps, int log_n,
-                                                        float2* out, int window, SegArgs sg) {
+template <int LN1, ColSrc SRC, typename CT>
+__global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_fwd(StepArgs a, const float2* ir, long taps, int log_n,
+                                                        CT* out, int window, SegArgs sg) {
+  using T = RealOf<CT>;
   constexpr int N1 = 1 << LN1;
-  constexpr int C = kColElems / N1;
+  constexpr int C = ColCfg<CT>::kElems / N1;
   constexpr int FS = padded(N1) + 1;
-  extern __shared__ float2 tile[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CT* tile = reinterpret_cast<CT*>(smem_raw);
   const int log_n2 = log_n - LN1;
   const long N2 = 1L << log_n2;
   const long N = 1L << log_n;
@@ -123,30 +131,30 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_fwd(StepArgs a, const flo
   __shared__ float rec[SRC == ColSrc::DelayTaps ? kTaps * kTapRec : 1];
   if constexpr (SRC == ColSrc::DelayTaps) {
     const float* in = reinterpret_cast<const float*>(ir) + static_cast<long>(item) * kTaps * kTapRec;
-    for (int q = threadIdx.x; q < kTaps * kTapRec; q += kColThreads) rec[q] = __ldg(in + q);
+    for (int q = threadIdx.x; q < kTaps * kTapRec; q += ColCfg<CT>::kThreads) rec[q] = __ldg(in + q);
     __syncthreads();
   }
   // Stage all of this thread's loads in registers before any smem store (max loads in flight).
-  constexpr int EPT = kColElems / kColThreads;
-  float2 vals[EPT];
+  constexpr int EPT = ColCfg<CT>::kElems / ColCfg<CT>::kThreads;
+  CT vals[EPT];
   const float* one = nullptr;  // in-degree-1 fast path
   if constexpr (SRC == ColSrc::Signal) {
     if (e1 - e0 == 1) one = a.src + edge_row(a, e0) * a.rowstride + static_cast<long>(b) * 2 * a.length;
   }
 #pragma unroll
   for (int q = 0; q < EPT; ++q) {
-    const int idx = threadIdx.x + q * kColThreads;
+    const int idx = threadIdx.x + q * ColCfg<CT>::kThreads;
     const int c = idx % C, n1 = idx / C;
     const long n = static_cast<long>(n1) * N2 + col0 + c;
     const long m = base + n;
-    float2 v = make_float2(0.f, 0.f);
+    CT v = Cx<CT>::mk(0.f, 0.f);
     if (m >= lo && m < hi) {
       if constexpr (SRC == ColSrc::Signal) {
-        v = one ? make_float2(__ldg(one + m), __ldg(one + a.length + m)) : gather2(a, e0, e1, b, m);
+        v = one ? Cx<CT>::mk(__ldg(one + m), __ldg(one + a.length + m)) : widen<CT>(gather2(a, e0, e1, b, m));
       } else if constexpr (SRC == ColSrc::DelayTaps) {
-        v = make_float2(delay_tap_sum(rec, 0, n, window), delay_tap_sum(rec, 1, n, window));
+        v = Cx<CT>::mk(delay_tap_sum(rec, 0, n, window), delay_tap_sum(rec, 1, n, window));
       } else {
-        v = __ldg(ir + static_cast<long>(item) * taps + n);
+        v = widen<CT>(__ldg(ir + static_cast<long>(item) * taps + n));
       }
     }
     vals[q] = v;
@@ -156,26 +164,26 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_fwd(StepArgs a, const flo
   const int c = threadIdx.x % C, jt = threadIdx.x / C;
   fft_first_from_regs<-1>(vals, tile + c * FS, jt);
   __syncthreads();
-  fft_middle<LN1, C, kColThreads, -1>(tile, FS, a.tw);
+  fft_middle<LN1, C, ColCfg<CT>::kThreads, -1>(tile, FS, twiddles<CT>(a));
   // Last pass into registers, four-step twiddle exp(-2 pi i n2 k1 / N), store. Outputs of
   // butterfly j are k1 = j + r*NS: geometric in r, exact anchors (sincospif; n2 k1 < N <=
   // 2^24 is exact in fp32) every 4 outputs, <= 3 chained products in between.
   using Plan = Pow2Plan<LN1>;
-  constexpr int NS = Plan::kLastNs, R = Plan::kLastR, JSTEP = kColThreads / C;
-  float2* o = out + static_cast<long>(item) * N;
-  const float inv_n = 2.f / static_cast<float>(N);
+  constexpr int NS = Plan::kLastNs, R = Plan::kLastR, JSTEP = ColCfg<CT>::kThreads / C;
+  CT* o = out + static_cast<long>(item) * N;
+  const T inv_n = T(2) / static_cast<T>(N);
   const long n2 = col0 + c;
-  const float2 step = expi_pi(-static_cast<float>(n2 * NS) * inv_n);
+  const CT step = expi_pi(-static_cast<T>(n2 * NS) * inv_n);
 #pragma unroll
   for (int p = 0; p < NS / JSTEP; ++p) {
     const int j = jt + p * JSTEP;
-    float2 v[R];
-    fft_last_to_regs<LN1, -1>(tile + c * FS, j, a.tw, v);
-    float2 w = make_float2(1.f, 0.f);
+    CT v[R];
+    fft_last_to_regs<LN1, -1>(tile + c * FS, j, twiddles<CT>(a), v);
+    CT w = Cx<CT>::mk(1.f, 0.f);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int k1 = j + r * NS;
-      w = (r % 4 == 0) ? expi_pi(-static_cast<float>(n2 * k1) * inv_n) : cmul(w, step);
+      w = (r % 4 == 0) ? expi_pi(-static_cast<T>(n2 * k1) * inv_n) : cmul(w, step);
       o[static_cast<long>(k1) * N2 + n2] = cmul(v[r], w);
     }
   }
@@ -184,12 +192,14 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_fwd(StepArgs a, const flo
 // ---- pass 3 (last): inverse column FFTs, store into the arena --------------------------
 // BUF: the whole transform goes back into the item's own spectrum in natural order (in place:
 // a CTA owns its columns, and all its loads are consumed before its stores) for conv_ola.
-template <int LN1, bool BUF>
-__global__ void __launch_bounds__(kColThreads, 2) cols_inv(StepArgs a, int log_n, float2* X, SegArgs sg) {
+template <int LN1, bool BUF, typename CT>
+__global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_inv(StepArgs a, int log_n, CT* X, SegArgs sg) {
+  using T = RealOf<CT>;
   constexpr int N1 = 1 << LN1;
-  constexpr int C = kColElems / N1;
+  constexpr int C = ColCfg<CT>::kElems / N1;
   constexpr int FS = padded(N1) + 1;
-  extern __shared__ float2 tile[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CT* tile = reinterpret_cast<CT*>(smem_raw);
   const long N2 = 1L << (log_n - LN1);
   const long N = 1L << log_n;
   const int item = sg.item0 + blockIdx.y;
@@ -198,12 +208,12 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_inv(StepArgs a, int log_n
   const long base = seg_base(sg.seg, sg.pre, jseg);
   const long first = static_cast<long>(jseg) * sg.seg, end = min(first + sg.seg, a.length);
   const long col0 = static_cast<long>(blockIdx.x) * C;
-  const float2* x = X + static_cast<long>(item) * N;
-  constexpr int EPT = kColElems / kColThreads;
-  float2 vals[EPT];
+  const CT* x = X + static_cast<long>(item) * N;
+  constexpr int EPT = ColCfg<CT>::kElems / ColCfg<CT>::kThreads;
+  CT vals[EPT];
 #pragma unroll
   for (int q = 0; q < EPT; ++q) {
-    const int idx = threadIdx.x + q * kColThreads;
+    const int idx = threadIdx.x + q * ColCfg<CT>::kThreads;
     vals[q] = __ldg(x + static_cast<long>(idx / C) * N2 + col0 + idx % C);
   }
   // First pass from registers (vals[q] = element j + q*N1/16 of column c), last pass into
@@ -211,16 +221,16 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_inv(StepArgs a, int log_n
   const int c = threadIdx.x % C, jt = threadIdx.x / C;
   fft_first_from_regs<+1>(vals, tile + c * FS, jt);
   __syncthreads();
-  fft_middle<LN1, C, kColThreads, +1>(tile, FS, a.tw);
+  fft_middle<LN1, C, ColCfg<CT>::kThreads, +1>(tile, FS, twiddles<CT>(a));
   using Plan = Pow2Plan<LN1>;
-  constexpr int NS = Plan::kLastNs, R = Plan::kLastR, JSTEP = kColThreads / C;
+  constexpr int NS = Plan::kLastNs, R = Plan::kLastR, JSTEP = ColCfg<CT>::kThreads / C;
   float* yl = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length;
   float* yr = yl + a.length;
 #pragma unroll
   for (int p = 0; p < NS / JSTEP; ++p) {
     const int j = jt + p * JSTEP;
-    float2 v[R];
-    fft_last_to_regs<LN1, +1>(tile + c * FS, j, a.tw, v);
+    CT v[R];
+    fft_last_to_regs<LN1, +1>(tile + c * FS, j, twiddles<CT>(a), v);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const long n = static_cast<long>(j + r * NS) * N2 + col0 + c;
@@ -229,8 +239,8 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_inv(StepArgs a, int log_n
       } else {
         const long m = base + n;
         if (m >= first && m < end) {
-          yl[m] = v[r].x;
-          yr[m] = v[r].y;
+          yl[m] = static_cast<float>(v[r].x);
+          yr[m] = static_cast<float>(v[r].y);
         }
       }
     }
@@ -240,28 +250,31 @@ __global__ void __launch_bounds__(kColThreads, 2) cols_inv(StepArgs a, int log_n
 // Overlap-add of the segments' input-gradient contributions (backward, nseg > 1): segment j
 // contributes to samples [base_j, (j+1)*seg); each sample sums its segments in order j = m/seg,
 // ..., (m+pre)/seg (fixed order, deterministic). grid (ceil(L/256), slots*batch chunk).
-__global__ void __launch_bounds__(256) conv_ola(StepArgs a, SegArgs sg, long N, const float2* buf) {
+template <typename CT>
+__global__ void __launch_bounds__(256) conv_ola(StepArgs a, SegArgs sg, long N, const CT* buf) {
+  using T = RealOf<CT>;
   const long m = static_cast<long>(blockIdx.x) * 256 + threadIdx.x;
   if (m >= a.length) return;
   const int isb = sg.item0 + blockIdx.y;
   const int slot = isb / a.batch, b = isb - slot * a.batch;
   long jhi = (m + sg.pre) / sg.seg;
   if (jhi > sg.nseg - 1) jhi = sg.nseg - 1;
-  float2 acc = make_float2(0.f, 0.f);
+  CT acc = Cx<CT>::mk(0.f, 0.f);
   for (long j = m / sg.seg; j <= jhi; ++j) {
     acc = cadd(acc, __ldg(buf + (static_cast<long>(isb) * sg.nseg + j) * N + (m - seg_base(sg.seg, sg.pre, j))));
   }
   float* y = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length;
-  y[m] = acc.x;
-  y[a.length + m] = acc.y;
+  y[m] = static_cast<float>(acc.x);
+  y[a.length + m] = static_cast<float>(acc.y);
 }
 
 // ---- pass 2: row FFTs ---------------------------------------------------------------------
-__device__ __forceinline__ float2 zmix(float2 xk, float2 xm, float2 pk, float2 pm, float s) {
+template <typename CT>
+__device__ __forceinline__ CT zmix(CT xk, CT xm, CT pk, CT pm, RealOf<CT> s) {
   // xm = conj(X[N-k]), pm = conj(P[N-k]):  Z = ((xk+xm)(pk+pm) - i (xk-xm)(pk-pm)) / 4
-  const float2 s1 = cmul(cadd(xk, xm), cadd(pk, pm));
-  const float2 s2 = cmul(csub(xk, xm), csub(pk, pm));
-  return make_float2((s1.x + s2.y) * s, (s1.y - s2.x) * s);
+  const CT s1 = cmul(cadd(xk, xm), cadd(pk, pm));
+  const CT s2 = cmul(csub(xk, xm), csub(pk, pm));
+  return Cx<CT>::mk((s1.x + s2.y) * s, (s1.y - s2.x) * s);
 }
 
 // Threads = radix-16 butterflies of the first pass (COUNT rows of 2^LN2 points), so no
@@ -282,13 +295,13 @@ constexpr bool rows_reg() {
 
 // COUNT rows src[w] -> radix-16 first pass from registers into rows + w*RS, barrier, the
 // remaining forward passes (thread t owns butterfly t % (N2/16) of row t / (N2/16)).
-template <int LN2, int COUNT, int NT>
-__device__ __forceinline__ void rows_forward_from_global(float2* rows, int RS, const float2* s0, const float2* s1,
-                                                         const float2* s2, const float2* s3, const float2* tw) {
+template <int LN2, int COUNT, int NT, typename CT>
+__device__ __forceinline__ void rows_forward_from_global(CT* rows, int RS, const CT* s0, const CT* s1,
+                                                         const CT* s2, const CT* s3, const CT* tw) {
   constexpr int M1 = (1 << LN2) / 16;
   const int w = threadIdx.x / M1, j = threadIdx.x - (threadIdx.x / M1) * M1;
-  const float2* p = w == 0 ? s0 : (w == 1 ? s1 : (w == 2 ? s2 : s3));  // selects, no local array
-  float2 v[16];
+  const CT* p = w == 0 ? s0 : (w == 1 ? s1 : (w == 2 ? s2 : s3));  // selects, no local array
+  CT v[16];
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[r] = p[j + r * M1];
   fft_first_from_regs<-1>(v, rows + w * RS, j);
@@ -300,27 +313,28 @@ __device__ __forceinline__ void rows_forward_from_global(float2* rows, int RS, c
 // registers: output i of row w is scaled by the inverse four-step twiddle exp(+2 pi i r_w i / N)
 // (geometric in i = j + r*NS, exact anchors every 4) and stored to dst_w[i]; row b is skipped
 // when it is row a (self-paired rows). Half the threads per row, consecutive j per warp.
-template <int LN2, int NT>
-__device__ __forceinline__ void rows_inverse_to_global(float2* rows, int RS, int ra, int rb, bool self, float2* da,
-                                                       float2* db, float inv_n, const float2* tw) {
+template <int LN2, int NT, typename CT>
+__device__ __forceinline__ void rows_inverse_to_global(CT* rows, int RS, int ra, int rb, bool self, CT* da,
+                                                       CT* db, RealOf<CT> inv_n, const CT* tw) {
+  using T = RealOf<CT>;
   fft_all_but_last<LN2, 2, NT, +1>(rows, RS, tw);
   constexpr int NS = Pow2Plan<LN2>::kLastNs, R = Pow2Plan<LN2>::kLastR, HT = NT / 2;
   static_assert(NS % HT == 0, "rows_inverse_to_global: threads must tile the last pass");
   const int w = threadIdx.x / HT, jt = threadIdx.x - (threadIdx.x / HT) * HT;
   if (w == 1 && self) return;
   const int rw = w == 0 ? ra : rb;
-  float2* dst = w == 0 ? da : db;
-  const float2 step = expi_pi(static_cast<float>(static_cast<long>(rw) * NS) * inv_n);
+  CT* dst = w == 0 ? da : db;
+  const CT step = expi_pi(static_cast<T>(static_cast<long>(rw) * NS) * inv_n);
 #pragma unroll
   for (int p = 0; p < NS / HT; ++p) {
     const int j = jt + p * HT;
-    float2 v[R];
+    CT v[R];
     fft_last_to_regs<LN2, +1>(rows + w * RS, j, tw, v);
-    float2 wt = make_float2(1.f, 0.f);
+    CT wt = Cx<CT>::mk(1.f, 0.f);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int i = j + r * NS;
-      wt = (r % 4 == 0) ? expi_pi(static_cast<float>(static_cast<long>(rw) * i) * inv_n) : cmul(wt, step);
+      wt = (r % 4 == 0) ? expi_pi(static_cast<T>(static_cast<long>(rw) * i) * inv_n) : cmul(wt, step);
       dst[i] = cmul(v[r], wt);
     }
   }
@@ -328,20 +342,22 @@ __device__ __forceinline__ void rows_inverse_to_global(float2* rows, int RS, int
 
 // Forward row FFTs of the packed kernel, kSpecRows consecutive rows per CTA.
 // grid (N1 / kSpecRows, slots)
-template <int LN2>
-__global__ void __launch_bounds__(row_threads<LN2, kSpecRows>()) rows_spec(int log_n, float2* P, const float2* tw) {
+template <int LN2, typename CT>
+__global__ void __launch_bounds__(row_threads<LN2, kSpecRows>()) rows_spec(int log_n, CT* P, const CT* tw) {
+  using T = RealOf<CT>;
   constexpr int N2 = 1 << LN2;
   constexpr int NT = row_threads<LN2, kSpecRows>();
   constexpr int RS = padded(N2);
-  extern __shared__ float2 row[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CT* row = reinterpret_cast<CT*>(smem_raw);
   const long N = 1L << log_n;
-  float2* p = P + static_cast<long>(blockIdx.y) * N + static_cast<long>(blockIdx.x) * kSpecRows * N2;
+  CT* p = P + static_cast<long>(blockIdx.y) * N + static_cast<long>(blockIdx.x) * kSpecRows * N2;
   // All of this thread's loads are issued before any smem store (loads in flight, not a
   // load -> store dependency per element).
   if constexpr (rows_reg<LN2, kSpecRows>()) {
     constexpr int M1 = N2 / 16;
     const int w = threadIdx.x / M1, j = threadIdx.x - (threadIdx.x / M1) * M1;
-    float2 v[16];
+    CT v[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = p[w * N2 + j + r * M1];
     fft_first_from_regs<-1>(v, row + w * RS, j);
@@ -352,7 +368,7 @@ __global__ void __launch_bounds__(row_threads<LN2, kSpecRows>()) rows_spec(int l
 #pragma unroll
     for (int q = 0; q < kSpecRows * NS / NT; ++q) {
       const int bq = threadIdx.x + q * NT, f = bq / NS, jb = bq - f * NS;
-      float2 y[R];
+      CT y[R];
       fft_last_to_regs<LN2, -1>(row + f * RS, jb, tw, y);
 #pragma unroll
       for (int r = 0; r < R; ++r) p[f * N2 + jb + r * NS] = y[r];
@@ -361,7 +377,7 @@ __global__ void __launch_bounds__(row_threads<LN2, kSpecRows>()) rows_spec(int l
   }
   constexpr int PER = kSpecRows * N2 / NT;
   static_assert(PER * NT == kSpecRows * N2, "rows_spec: threads must tile the rows");
-  float2 v[PER];
+  CT v[PER];
 #pragma unroll
   for (int q = 0; q < PER; ++q) v[q] = p[threadIdx.x + q * NT];
 #pragma unroll
@@ -377,21 +393,23 @@ __global__ void __launch_bounds__(row_threads<LN2, kSpecRows>()) rows_spec(int l
 // Signal rows k1 = r and N1 - r together: forward FFTs, channel-split product with the
 // kernel spectrum, inverse FFTs, inverse four-step twiddle. grid (N1/2 + 1, slots*B)
 // `batch`: items per slot (batch * segments); item0: first item of this launch.
-template <int LN2>
-__global__ void __launch_bounds__(row_threads<LN2, 2>(), kRconvThreadsPerSm / row_threads<LN2, 2>()) rows_conv(int log_n, int batch, float2* X, const float2* P, const float2* tw, int item0) {
+template <int LN2, typename CT>
+__global__ void __launch_bounds__(row_threads<LN2, 2>(), kRconvThreadsPerSm / (sizeof(CT) / 8) / row_threads<LN2, 2>()) rows_conv(int log_n, int batch, CT* X, const CT* P, const CT* tw, int item0) {
+  using T = RealOf<CT>;
   constexpr int N2 = 1 << LN2;
   constexpr int NT = row_threads<LN2, 2>();
-  extern __shared__ float2 rows[];  // [2][N2]
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CT* rows = reinterpret_cast<CT*>(smem_raw);  // [2][N2]
   const long N = 1L << log_n;
   const int N1 = static_cast<int>(N >> LN2);
   const int item = item0 + blockIdx.y;
   const int slot = item / batch;
   const int ra = blockIdx.x, rb = (N1 - ra) & (N1 - 1);
   const bool self = ra == rb;
-  float2* xa = X + static_cast<long>(item) * N + static_cast<long>(ra) * N2;
-  float2* xb = X + static_cast<long>(item) * N + static_cast<long>(rb) * N2;
-  const float2* pa = P + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
-  const float2* pb = P + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
+  CT* xa = X + static_cast<long>(item) * N + static_cast<long>(ra) * N2;
+  CT* xb = X + static_cast<long>(item) * N + static_cast<long>(rb) * N2;
+  const CT* pa = P + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
+  const CT* pb = P + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
   constexpr int RS = padded(N2);  // second row's offset
   constexpr int KPT = N2 / NT;
   static_assert(KPT * NT == N2, "rows_conv: threads must tile a row");
@@ -403,8 +421,8 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), kRconvThreadsPerSm / ro
     // (the kernel-spectrum prefetch is issued after the first pass, registers permitting)
     constexpr int M1 = N2 / 16;
     const int w = threadIdx.x / M1, j = threadIdx.x - (threadIdx.x / M1) * M1;
-    const float2* src = w == 0 ? xa : xb;
-    float2 v[16];
+    const CT* src = w == 0 ? xa : xb;
+    CT v[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = src[j + r * M1];
     fft_first_from_regs<-1>(v, rows + w * RS, j);
@@ -413,7 +431,7 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), kRconvThreadsPerSm / ro
   } else {
     constexpr int PER = N2 / NT;
     static_assert(PER * NT == N2, "rows_conv: threads must tile a row");
-    float2 va[PER], vb[PER];  // loads in flight before any smem store
+    CT va[PER], vb[PER];  // loads in flight before any smem store
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       va[q] = xa[threadIdx.x + q * NT];
@@ -427,23 +445,23 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), kRconvThreadsPerSm / ro
     __syncthreads();
     fft_pow2<LN2, 2, NT, -1>(rows, RS, tw);
   }
-  const float s = 0.25f / static_cast<float>(N);
+  const T s = T(0.25) / static_cast<T>(N);
 #pragma unroll
   for (int q = 0; q < KPT; ++q) {
     const int k = threadIdx.x + q * NT;
     if (k >= N2) continue;
     const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
     if (self && kb < k) continue;
-    const float2 xk = rows[sidx(k)], xo = rows[RS + sidx(kb)];
-    const float2 pk = __ldg(pa + k), po = __ldg(pb + kb);
-    const float2 zk = zmix(xk, cconj(xo), pk, cconj(po), s);
-    const float2 zo = zmix(xo, cconj(xk), po, cconj(pk), s);
+    const CT xk = rows[sidx(k)], xo = rows[RS + sidx(kb)];
+    const CT pk = __ldg(pa + k), po = __ldg(pb + kb);
+    const CT zk = zmix(xk, cconj(xo), pk, cconj(po), s);
+    const CT zo = zmix(xo, cconj(xk), po, cconj(pk), s);
     rows[sidx(k)] = zk;
     rows[RS + sidx(kb)] = zo;
     if (self) rows[sidx(kb)] = zo;
   }
   __syncthreads();
-  const float inv_n = 2.f / static_cast<float>(N);
+  const T inv_n = T(2) / static_cast<T>(N);
   if constexpr (REG) {
     rows_inverse_to_global<LN2, NT>(rows, RS, ra, rb, self, xa, xb, inv_n, tw);
     return;
@@ -451,15 +469,15 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), kRconvThreadsPerSm / ro
   fft_pow2<LN2, 2, NT, +1>(rows, RS, tw);
   // Inverse four-step twiddle exp(+2 pi i k1 i / N): geometric in this thread's i (step NT),
   // exact anchors every 4 elements as in cols_fwd.
-  const float2 step_a = expi_pi(static_cast<float>(static_cast<long>(ra) * NT) * inv_n);
-  const float2 step_b = expi_pi(static_cast<float>(static_cast<long>(rb) * NT) * inv_n);
-  float2 wa = make_float2(1.f, 0.f), wb = wa;
+  const CT step_a = expi_pi(static_cast<T>(static_cast<long>(ra) * NT) * inv_n);
+  const CT step_b = expi_pi(static_cast<T>(static_cast<long>(rb) * NT) * inv_n);
+  CT wa = Cx<CT>::mk(1.f, 0.f), wb = wa;
 #pragma unroll
   for (int q = 0; q < N2 / NT; ++q) {
     const int i = threadIdx.x + q * NT;
     if (q % 4 == 0) {
-      wa = expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n);
-      wb = expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n);
+      wa = expi_pi(static_cast<T>(static_cast<long>(ra) * i) * inv_n);
+      wb = expi_pi(static_cast<T>(static_cast<long>(rb) * i) * inv_n);
     } else {
       wa = cmul(wa, step_a);
       wb = cmul(wb, step_b);
@@ -474,29 +492,31 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), kRconvThreadsPerSm / ro
 // K holds the kernel's COLUMN-stage output (cols_fwd<Kernel>, no rows_spec pass); each CTA
 // transforms the kernel rows ra / rb alongside the signal rows (4 transforms), so the kernel
 // spectrum never makes a round trip through memory. grid (N1/2 + 1, slots*B)
-template <int LN2>
-__global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_conv_fk(int log_n, int batch, float2* X, const float2* K,
-                                                                  const float2* tw, int item0) {
+template <int LN2, typename CT>
+__global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_conv_fk(int log_n, int batch, CT* X, const CT* K,
+                                                                  const CT* tw, int item0) {
+  using T = RealOf<CT>;
   constexpr int N2 = 1 << LN2;
   constexpr int NT = row_threads<LN2, 4>();
   constexpr int RS = padded(N2);
-  extern __shared__ float2 rows[];  // [4][RS]: x a, x b, k a, k b
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CT* rows = reinterpret_cast<CT*>(smem_raw);  // [4][RS]: x a, x b, k a, k b
   const long N = 1L << log_n;
   const int N1 = static_cast<int>(N >> LN2);
   const int item = item0 + blockIdx.y;
   const int slot = item / batch;
   const int ra = blockIdx.x, rb = (N1 - ra) & (N1 - 1);
   const bool self = ra == rb;
-  float2* xa = X + static_cast<long>(item) * N + static_cast<long>(ra) * N2;
-  float2* xb = X + static_cast<long>(item) * N + static_cast<long>(rb) * N2;
-  const float2* ka = K + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
-  const float2* kb_ = K + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
+  CT* xa = X + static_cast<long>(item) * N + static_cast<long>(ra) * N2;
+  CT* xb = X + static_cast<long>(item) * N + static_cast<long>(rb) * N2;
+  const CT* ka = K + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
+  const CT* kb_ = K + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
   constexpr bool REG = rows_reg<LN2, 4>();
   if constexpr (REG) {
     rows_forward_from_global<LN2, 4, NT>(rows, RS, xa, xb, ka, kb_, tw);
   } else {
     constexpr int PER = (N2 + NT - 1) / NT;
-    float2 v[4][PER];
+    CT v[4][PER];
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       const int i = threadIdx.x + q * NT;
@@ -518,16 +538,16 @@ __global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_conv_fk(int log_n,
     __syncthreads();
     fft_pow2<LN2, 4, NT, -1>(rows, RS, tw);
   }
-  const float s = 0.25f / static_cast<float>(N);
+  const T s = T(0.25) / static_cast<T>(N);
   constexpr int KPT = (N2 + NT - 1) / NT;
-  float2 zk[KPT], zo[KPT];
+  CT zk[KPT], zo[KPT];
 #pragma unroll
   for (int q = 0; q < KPT; ++q) {
     const int k = threadIdx.x + q * NT;
     if (k >= N2) continue;
     const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
-    const float2 xk = rows[sidx(k)], xo = rows[RS + sidx(kb)];
-    const float2 pk = rows[2 * RS + sidx(k)], po = rows[3 * RS + sidx(kb)];
+    const CT xk = rows[sidx(k)], xo = rows[RS + sidx(kb)];
+    const CT pk = rows[2 * RS + sidx(k)], po = rows[3 * RS + sidx(kb)];
     zk[q] = zmix(xk, cconj(xo), pk, cconj(po), s);
     zo[q] = zmix(xo, cconj(xk), po, cconj(pk), s);
   }
@@ -543,15 +563,15 @@ __global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_conv_fk(int log_n,
     else rows[RS + sidx(kb)] = zo[q];
   }
   __syncthreads();
-  const float inv_n = 2.f / static_cast<float>(N);
+  const T inv_n = T(2) / static_cast<T>(N);
   if constexpr (REG) {
     rows_inverse_to_global<LN2, NT>(rows, RS, ra, rb, self, xa, xb, inv_n, tw);
     return;
   }
   fft_pow2<LN2, 2, NT, +1>(rows, RS, tw);
   for (int i = threadIdx.x; i < N2; i += NT) {
-    xa[i] = cmul(rows[sidx(i)], expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n));
-    if (!self) xb[i] = cmul(rows[RS + sidx(i)], expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n));
+    xa[i] = cmul(rows[sidx(i)], expi_pi(static_cast<T>(static_cast<long>(ra) * i) * inv_n));
+    if (!self) xb[i] = cmul(rows[RS + sidx(i)], expi_pi(static_cast<T>(static_cast<long>(rb) * i) * inv_n));
   }
 }
 
@@ -562,119 +582,124 @@ void for_item_chunks(int items, F&& f) {
   for (int i0 = 0; i0 < items; i0 += kMaxGridY) f(i0, items - i0 < kMaxGridY ? items - i0 : kMaxGridY);
 }
 
-template <int LN1>
+template <typename CT> const CT* tw_table(const StepArgs& a);
+template <> const float2* tw_table<float2>(const StepArgs& a) { return a.tw; }
+template <> const double2* tw_table<double2>(const StepArgs& a) { return a.tw64; }
+
+template <int LN1, typename CT>
 void cols_fwd_t(ColSrc src, const StepArgs& a, const float2* ir, long taps, const ConvGeom& g, int items,
-                float2* out, int window, bool mask_out, cudaStream_t s) {
-  constexpr int C = kColElems / (1 << LN1);
-  constexpr int smem = C * (padded(1 << LN1) + 1) * 8;
+                CT* out, int window, bool mask_out, cudaStream_t s) {
+  constexpr int C = ColCfg<CT>::kElems / (1 << LN1);
+  constexpr int smem = ColCfg<CT>::kSmem(1 << LN1);
   static const bool attrs_set = [] {
-    for (const void* fn : {reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::Signal>),
-                           reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::Kernel>),
-                           reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::DelayTaps>)}) {
+    for (const void* fn : {reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::Signal, CT>),
+                           reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::Kernel, CT>),
+                           reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::DelayTaps, CT>)}) {
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     }
     return true;
   }();
   (void)attrs_set;
-  if (src == ColSrc::DelayTaps) note_prologue_kernel(reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::DelayTaps>));
-  if (src == ColSrc::Kernel) note_prologue_kernel(reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::Kernel>));
+  if (src == ColSrc::DelayTaps) note_prologue_kernel(reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::DelayTaps, CT>));
+  if (src == ColSrc::Kernel) note_prologue_kernel(reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::Kernel, CT>));
+  constexpr int nt = ColCfg<CT>::kThreads;
   for_item_chunks(items, [&](int i0, int n) {
     const dim3 grid(static_cast<unsigned>((1L << g.log_n2) / C), static_cast<unsigned>(n));
     const SegArgs sg = seg_args(g, i0, mask_out);
     if (src == ColSrc::Signal) {
-      cols_fwd<LN1, ColSrc::Signal><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out, window, sg);
+      cols_fwd<LN1, ColSrc::Signal, CT><<<grid, nt, smem, s>>>(a, ir, taps, g.log_n, out, window, sg);
     } else if (src == ColSrc::DelayTaps) {
-      cols_fwd<LN1, ColSrc::DelayTaps><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out, window, sg);
+      cols_fwd<LN1, ColSrc::DelayTaps, CT><<<grid, nt, smem, s>>>(a, ir, taps, g.log_n, out, window, sg);
     } else {
-      cols_fwd<LN1, ColSrc::Kernel><<<grid, kColThreads, smem, s>>>(a, ir, taps, g.log_n, out, window, sg);
+      cols_fwd<LN1, ColSrc::Kernel, CT><<<grid, nt, smem, s>>>(a, ir, taps, g.log_n, out, window, sg);
     }
   });
 }
 
-template <int LN1>
-void cols_inv_t(const StepArgs& a, const ConvGeom& g, float2* X, bool to_buf, cudaStream_t s) {
-  constexpr int C = kColElems / (1 << LN1);
-  constexpr int smem = C * (padded(1 << LN1) + 1) * 8;
+template <int LN1, typename CT>
+void cols_inv_t(const StepArgs& a, const ConvGeom& g, CT* X, bool to_buf, cudaStream_t s) {
+  constexpr int C = ColCfg<CT>::kElems / (1 << LN1);
+  constexpr int smem = ColCfg<CT>::kSmem(1 << LN1);
   static const bool done = [] {
-    for (const void* fn : {reinterpret_cast<const void*>(cols_inv<LN1, false>), reinterpret_cast<const void*>(cols_inv<LN1, true>)}) {
+    for (const void* fn : {reinterpret_cast<const void*>(cols_inv<LN1, false, CT>), reinterpret_cast<const void*>(cols_inv<LN1, true, CT>)}) {
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     }
     return true;
   }();
   (void)done;
+  constexpr int nt = ColCfg<CT>::kThreads;
   for_item_chunks(a.slots * a.batch * g.nseg, [&](int i0, int n) {
     const dim3 grid(static_cast<unsigned>((1L << g.log_n2) / C), static_cast<unsigned>(n));
-    if (to_buf) cols_inv<LN1, true><<<grid, kColThreads, smem, s>>>(a, g.log_n, X, seg_args(g, i0));
-    else cols_inv<LN1, false><<<grid, kColThreads, smem, s>>>(a, g.log_n, X, seg_args(g, i0));
+    if (to_buf) cols_inv<LN1, true, CT><<<grid, nt, smem, s>>>(a, g.log_n, X, seg_args(g, i0));
+    else cols_inv<LN1, false, CT><<<grid, nt, smem, s>>>(a, g.log_n, X, seg_args(g, i0));
   });
 }
 
-template <int LN2>
-void rows_spec_t(const ConvGeom& g, int slots, float2* P, const float2* tw, cudaStream_t s) {
-  constexpr int smem = kSpecRows * padded(1 << LN2) * 8;
+template <int LN2, typename CT>
+void rows_spec_t(const ConvGeom& g, int slots, CT* P, const CT* tw, cudaStream_t s) {
+  constexpr int smem = kSpecRows * padded(1 << LN2) * static_cast<int>(sizeof(CT));
   static const bool done = [] {
-    cudaFuncSetAttribute(rows_spec<LN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(rows_spec<LN2, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return true;
   }();
   (void)done;
-  note_prologue_kernel(reinterpret_cast<const void*>(rows_spec<LN2>));
+  note_prologue_kernel(reinterpret_cast<const void*>(rows_spec<LN2, CT>));
   for (int s0 = 0; s0 < slots; s0 += kMaxGridY) {
     const int n = slots - s0 < kMaxGridY ? slots - s0 : kMaxGridY;
     const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / kSpecRows), static_cast<unsigned>(n));
-    rows_spec<LN2><<<grid, row_threads<LN2, kSpecRows>(), smem, s>>>(g.log_n, P + static_cast<long>(s0) * g.n, tw);
+    rows_spec<LN2, CT><<<grid, row_threads<LN2, kSpecRows>(), smem, s>>>(g.log_n, P + static_cast<long>(s0) * g.n, tw);
   }
 }
 
-template <int LN2>
-void rows_conv_t(const ConvGeom& g, int items, int per_slot, float2* X, const float2* P, const float2* tw,
-                 cudaStream_t s) {
-  constexpr int smem = 2 * padded(1 << LN2) * 8;
+template <int LN2, typename CT>
+void rows_conv_t(const ConvGeom& g, int items, int per_slot, CT* X, const CT* P, const CT* tw, cudaStream_t s) {
+  constexpr int smem = 2 * padded(1 << LN2) * static_cast<int>(sizeof(CT));
   static const bool done = [] {
-    cudaFuncSetAttribute(rows_conv<LN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(rows_conv<LN2, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return true;
   }();
   (void)done;
   for_item_chunks(items, [&](int i0, int n) {
     const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(n));
-    rows_conv<LN2><<<grid, row_threads<LN2, 2>(), smem, s>>>(g.log_n, per_slot, X, P, tw, i0);
+    rows_conv<LN2, CT><<<grid, row_threads<LN2, 2>(), smem, s>>>(g.log_n, per_slot, X, P, tw, i0);
   });
 }
 
-template <int LN2>
-void rows_conv_fk_t(const ConvGeom& g, int items, int per_slot, float2* X, const float2* K, const float2* tw,
-                    cudaStream_t s) {
-  constexpr int smem = 4 * padded(1 << LN2) * 8;
+template <int LN2, typename CT>
+void rows_conv_fk_t(const ConvGeom& g, int items, int per_slot, CT* X, const CT* K, const CT* tw, cudaStream_t s) {
+  constexpr int smem = 4 * padded(1 << LN2) * static_cast<int>(sizeof(CT));
   static const bool done = [] {
-    cudaFuncSetAttribute(rows_conv_fk<LN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(rows_conv_fk<LN2, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return true;
   }();
   (void)done;
   for_item_chunks(items, [&](int i0, int n) {
     const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(n));
-    rows_conv_fk<LN2><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, per_slot, X, K, tw, i0);
+    rows_conv_fk<LN2, CT><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, per_slot, X, K, tw, i0);
   });
 }
 
 // log2 of the column length N1 = 2^(a/2) and row length N2 = 2^(a - a/2), a in [13, 22].
-#define MGB_DISPATCH_LN(var, FN, ...)                  \
-  switch (var) {                                       \
-    case 6: FN<6>(__VA_ARGS__); break;                 \
-    case 7: FN<7>(__VA_ARGS__); break;                 \
-    case 8: FN<8>(__VA_ARGS__); break;                 \
-    case 9: FN<9>(__VA_ARGS__); break;                 \
-    case 10: FN<10>(__VA_ARGS__); break;               \
-    case 11: FN<11>(__VA_ARGS__); break;               \
+#define MGB_DISPATCH_LN(var, FN, CT, ...)                  \
+  switch (var) {                                           \
+    case 6: FN<6, CT>(__VA_ARGS__); break;                 \
+    case 7: FN<7, CT>(__VA_ARGS__); break;                 \
+    case 8: FN<8, CT>(__VA_ARGS__); break;                 \
+    case 9: FN<9, CT>(__VA_ARGS__); break;                 \
+    case 10: FN<10, CT>(__VA_ARGS__); break;               \
+    case 11: FN<11, CT>(__VA_ARGS__); break;               \
     default: throw std::invalid_argument("fft convolution size out of range"); \
   }
 
 // Kernel spectrum P (four-step order) of the packed kernels in `ir` ([slots][taps]).
+template <typename CT>
 void kernel_spectrum(ColSrc src, const StepArgs& a, const ConvGeom& g, const float2* ir, long taps, int window,
-                     float2* P, cudaStream_t s) {
-  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, src, a, ir, taps, g, a.slots, P, window, false, s);
+                     CT* P, cudaStream_t s) {
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, CT, src, a, ir, taps, g, a.slots, P, window, false, s);
   // Large steps leave the row stage to rows_conv_fk (conv_fuse_kernel_rows).
-  if (!conv_fuse_kernel_rows(g, a.slots)) MGB_DISPATCH_LN(g.log_n2, rows_spec_t, g, a.slots, P, a.tw, s);
+  if (!conv_fuse_kernel_rows(g, a.slots)) MGB_DISPATCH_LN(g.log_n2, rows_spec_t, CT, g, a.slots, P, tw_table<CT>(a), s);
 }
 
 // ---- reverb impulse response (masked noise STFT -> ISTFT) ----------------------------------
@@ -844,39 +869,41 @@ __global__ void __launch_bounds__(256) delay_dense(const float* taps, DelayConst
 //    product with X's pair swapped; inverted into X's b = 0 item at the end.
 // `batch`: items per slot (batch * segments: the kernel gradient sums over both).
 // grid (N1/2 + 1, slots chunk from slot0)
-template <int LN2, bool KFFT>
-__global__ void __launch_bounds__(row_threads<LN2, 4>(), rbwd_min_blocks<LN2>()) rows_bwd(int log_n, int batch, float2* DY, float2* X,
-                                                                 const float2* P, const float2* tw, int slot0) {
+template <int LN2, bool KFFT, typename CT>
+__global__ void __launch_bounds__(row_threads<LN2, 4>(), rbwd_min_blocks<LN2>()) rows_bwd(int log_n, int batch, CT* DY, CT* X,
+                                                                 const CT* P, const CT* tw, int slot0) {
+  using T = RealOf<CT>;
   constexpr int N2 = 1 << LN2;
   constexpr int NT = row_threads<LN2, 4>();
   constexpr int RS = padded(N2);
-  extern __shared__ float2 rows[];  // [8][RS]: dy a, dy b, x a, x b, h a, h b, acc a, acc b
+  extern __shared__ __align__(16) unsigned char smem_raw[];  // [8][RS]: dy a, dy b, x a, x b, h a, h b, acc a, acc b
+  CT* rows = reinterpret_cast<CT*>(smem_raw);
   const long N = 1L << log_n;
   const int N1 = static_cast<int>(N >> LN2);
   const int slot = slot0 + blockIdx.y;
   const int ra = blockIdx.x, rb = (N1 - ra) & (N1 - 1);
   const bool self = ra == rb;
-  const float2* pa = P + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
-  const float2* pb = P + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
-  float2* H = rows + 4 * RS;
-  float2* A = rows + 6 * RS;
+  const CT* pa = P + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
+  const CT* pb = P + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
+  CT* H = rows + 4 * RS;
+  CT* A = rows + 6 * RS;
   for (int i = threadIdx.x; i < N2; i += NT) {
     H[sidx(i)] = __ldg(pa + i);
     H[RS + sidx(i)] = __ldg(pb + i);
-    A[sidx(i)] = A[RS + sidx(i)] = make_float2(0.f, 0.f);
+    A[sidx(i)] = A[RS + sidx(i)] = Cx<CT>::mk(0.f, 0.f);
   }
   if constexpr (KFFT) {
     __syncthreads();
     fft_pow2<LN2, 2, NT, -1>(H, RS, tw);
   }
-  const float s = 0.25f / static_cast<float>(N);
-  const float inv_n = 2.f / static_cast<float>(N);
+  const T s = T(0.25) / static_cast<T>(N);
+  const T inv_n = T(2) / static_cast<T>(N);
   for (int b = 0; b < batch; ++b) {
     const long item = static_cast<long>(slot) * batch + b;
-    float2* da = DY + item * N + static_cast<long>(ra) * N2;
-    float2* db = DY + item * N + static_cast<long>(rb) * N2;
-    const float2* xa = X + item * N + static_cast<long>(ra) * N2;
-    const float2* xb = X + item * N + static_cast<long>(rb) * N2;
+    CT* da = DY + item * N + static_cast<long>(ra) * N2;
+    CT* db = DY + item * N + static_cast<long>(rb) * N2;
+    const CT* xa = X + item * N + static_cast<long>(ra) * N2;
+    const CT* xb = X + item * N + static_cast<long>(rb) * N2;
     __syncthreads();  // previous item's rows fully consumed
     if constexpr (rows_reg<LN2, 4>()) {
       rows_forward_from_global<LN2, 4, NT>(rows, RS, da, db, xa, xb, tw);
@@ -895,9 +922,9 @@ __global__ void __launch_bounds__(row_threads<LN2, 4>(), rbwd_min_blocks<LN2>())
       const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
       if (self && kb < k) continue;
       const int ob = self ? sidx(kb) : RS + sidx(kb);
-      const float2 dk = rows[sidx(k)], dn = rows[RS + sidx(kb)];
-      const float2 xk = rows[2 * RS + sidx(k)], xn = rows[3 * RS + sidx(kb)];
-      const float2 hk = H[sidx(k)], hn = H[RS + sidx(kb)];
+      const CT dk = rows[sidx(k)], dn = rows[RS + sidx(kb)];
+      const CT xk = rows[2 * RS + sidx(k)], xn = rows[3 * RS + sidx(kb)];
+      const CT hk = H[sidx(k)], hn = H[RS + sidx(kb)];
       // kernel gradient: DY_c conj(X_c) -> X's pair swapped
       // (a self-paired bin, k == kb, has one value: written once, as rows_conv does)
       if (!(self && kb == k)) A[sidx(k)] = cadd(A[sidx(k)], zmix(dk, cconj(dn), xn, cconj(xk), s));
@@ -912,59 +939,61 @@ __global__ void __launch_bounds__(row_threads<LN2, 4>(), rbwd_min_blocks<LN2>())
     } else {
       fft_pow2<LN2, 2, NT, +1>(rows, RS, tw);
       for (int i = threadIdx.x; i < N2; i += NT) {
-        da[i] = cmul(rows[sidx(i)], expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n));
-        if (!self) db[i] = cmul(rows[RS + sidx(i)], expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n));
+        da[i] = cmul(rows[sidx(i)], expi_pi(static_cast<T>(static_cast<long>(ra) * i) * inv_n));
+        if (!self) db[i] = cmul(rows[RS + sidx(i)], expi_pi(static_cast<T>(static_cast<long>(rb) * i) * inv_n));
       }
     }
   }
   __syncthreads();
-  float2* oa = X + static_cast<long>(slot) * batch * N + static_cast<long>(ra) * N2;
-  float2* ob = X + static_cast<long>(slot) * batch * N + static_cast<long>(rb) * N2;
+  CT* oa = X + static_cast<long>(slot) * batch * N + static_cast<long>(ra) * N2;
+  CT* ob = X + static_cast<long>(slot) * batch * N + static_cast<long>(rb) * N2;
   if constexpr (rows_reg<LN2, 4>()) {
     rows_inverse_to_global<LN2, NT>(A, RS, ra, rb, self, oa, ob, inv_n, tw);
     return;
   }
   fft_pow2<LN2, 2, NT, +1>(A, RS, tw);
   for (int i = threadIdx.x; i < N2; i += NT) {
-    oa[i] = cmul(A[sidx(i)], expi_pi(static_cast<float>(static_cast<long>(ra) * i) * inv_n));
-    if (!self) ob[i] = cmul(A[RS + sidx(i)], expi_pi(static_cast<float>(static_cast<long>(rb) * i) * inv_n));
+    oa[i] = cmul(A[sidx(i)], expi_pi(static_cast<T>(static_cast<long>(ra) * i) * inv_n));
+    if (!self) ob[i] = cmul(A[RS + sidx(i)], expi_pi(static_cast<T>(static_cast<long>(rb) * i) * inv_n));
   }
 }
 
 // Inverse column FFTs of slot items (X at item slot*batch) into a packed kernel-gradient
 // buffer out[slot][taps] (x = left, y = right), first `taps` samples. grid (N2 / C, slots)
-template <int LN1>
-__global__ void __launch_bounds__(kColThreads, 2) cols_inv_buf(int log_n, int batch, const float2* X, float2* out,
-                                                            long taps, const float2* tw, int slot0) {
+template <int LN1, typename CT>
+__global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_inv_buf(int log_n, int batch, const CT* X, float2* out,
+                                                            long taps, const CT* tw, int slot0) {
+  using T = RealOf<CT>;
   constexpr int N1 = 1 << LN1;
-  constexpr int C = kColElems / N1;
+  constexpr int C = ColCfg<CT>::kElems / N1;
   constexpr int FS = padded(N1) + 1;
-  extern __shared__ float2 tile[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CT* tile = reinterpret_cast<CT*>(smem_raw);
   const long N2 = 1L << (log_n - LN1);
   const long N = 1L << log_n;
   const int slot = slot0 + blockIdx.y;
   const long col0 = static_cast<long>(blockIdx.x) * C;
-  const float2* x = X + static_cast<long>(slot) * batch * N;
+  const CT* x = X + static_cast<long>(slot) * batch * N;
   // Register-ended column transform (as cols_inv): thread (c, j) loads the 16 inputs of its
   // first-pass butterfly and stores its last-pass outputs.
-  constexpr int M1 = N1 / 16, JSTEP = kColThreads / C;
+  constexpr int M1 = N1 / 16, JSTEP = ColCfg<CT>::kThreads / C;
   const int c = threadIdx.x % C, jt = threadIdx.x / C;
-  float2 v[16];
+  CT v[16];
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[r] = __ldg(x + static_cast<long>(jt + r * M1) * N2 + col0 + c);
   fft_first_from_regs<+1>(v, tile + c * FS, jt);
   __syncthreads();
-  fft_middle<LN1, C, kColThreads, +1>(tile, FS, tw);
+  fft_middle<LN1, C, ColCfg<CT>::kThreads, +1>(tile, FS, tw);
   constexpr int NS = Pow2Plan<LN1>::kLastNs, R = Pow2Plan<LN1>::kLastR;
 #pragma unroll
   for (int p = 0; p < NS / JSTEP; ++p) {
     const int j = jt + p * JSTEP;
-    float2 y[R];
+    CT y[R];
     fft_last_to_regs<LN1, +1>(tile + c * FS, j, tw, y);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const long n = static_cast<long>(j + r * NS) * N2 + col0 + c;
-      if (n < taps) out[static_cast<long>(slot) * taps + n] = y[r];
+      if (n < taps) out[static_cast<long>(slot) * taps + n] = narrow(y[r]);
     }
   }
 }
@@ -1140,6 +1169,9 @@ unsigned grid_for(long n) {
 
 }  // namespace
 
+// Bytes per spectrum element of the current transform precision (fft_fp64()).
+std::size_t spec_elem_bytes() { return fft_fp64() ? sizeof(double2) : sizeof(float2); }
+
 static int g_conv_fuse = -1;  // -1 auto, 0 never, 1 always (mg_set_conv_fuse; tests)
 void set_conv_fuse(int mode) { g_conv_fuse = mode; }
 
@@ -1147,7 +1179,7 @@ bool conv_fuse_kernel_rows(const ConvGeom& g, int slots) {
   if (g_conv_fuse >= 0) return g_conv_fuse == 1;
   // Kernel spectra that cannot stay in L2 (> 64 MiB over the step) are not worth a separate
   // rows pass: the signal's row kernel transforms the kernel rows itself.
-  return sizeof(float2) * static_cast<std::size_t>(slots) * static_cast<std::size_t>(g.n) > (64u << 20);
+  return spec_elem_bytes() * static_cast<std::size_t>(slots) * static_cast<std::size_t>(g.n) > (64u << 20);
 }
 
 static int g_conv_log = 0;  // 0 automatic (mg_set_conv_log; tests)
@@ -1191,11 +1223,11 @@ ConvGeom conv_geom(long length, long taps) {
 }
 
 std::size_t conv_prologue_bytes(const ConvGeom& g, int slots, long taps) {
-  return ir_bytes(slots, taps) + align256(sizeof(float2) * static_cast<std::size_t>(slots) * g.n);
+  return ir_bytes(slots, taps) + align256(spec_elem_bytes() * static_cast<std::size_t>(slots) * g.n);
 }
 
 std::size_t conv_main_bytes(const ConvGeom& g, int slots, int batch) {
-  return align256(sizeof(float2) * static_cast<std::size_t>(slots) * batch * g.nseg * g.n);
+  return align256(spec_elem_bytes() * static_cast<std::size_t>(slots) * batch * g.nseg * g.n);
 }
 
 
@@ -1224,121 +1256,108 @@ void launch_delay_ir(const double* params, int slots, const DelayConst& dc, floa
   delay_dense<<<grid, 256, 0, s>>>(taps, dc, ir, ir_stride);
 }
 
-void launch_conv_prologue(bool reverb, const StepArgs& a, const ReverbConst& rc, const DelayConst& dc, void* ws,
-                          cudaStream_t s) {
-  if (a.slots == 0) return;
+namespace {
+template <typename CT>
+void conv_prologue(bool reverb, const StepArgs& a, const ReverbConst& rc, const DelayConst& dc, void* ws, cudaStream_t s) {
   const long taps = reverb ? rc.length : dc.span;
   const ConvGeom g = conv_geom(a.length, taps);
   auto* ir = static_cast<float2*>(ws);
-  auto* P = reinterpret_cast<float2*>(static_cast<char*>(ws) + ir_bytes(a.slots, taps));
+  auto* P = reinterpret_cast<CT*>(static_cast<char*>(ws) + ir_bytes(a.slots, taps));
   if (reverb) {
     launch_reverb_ir(a.params, a.slots, rc, ir, taps, s);
-    kernel_spectrum(ColSrc::Kernel, a, g, ir, taps, 0, P, s);
+    kernel_spectrum<CT>(ColSrc::Kernel, a, g, ir, taps, 0, P, s);
   } else {
     // Tap records only; the column pass synthesises the dense kernel on the fly.
     auto* rec = reinterpret_cast<float*>(ir + static_cast<long>(a.slots) * taps);
     note_prologue_kernel(reinterpret_cast<const void*>(delay_taps));
     delay_taps<<<dim3(kTaps, a.slots), 64, 0, s>>>(a.params, dc, rec);
-    kernel_spectrum(ColSrc::DelayTaps, a, g, reinterpret_cast<const float2*>(rec), taps, dc.window, P, s);
+    kernel_spectrum<CT>(ColSrc::DelayTaps, a, g, reinterpret_cast<const float2*>(rec), taps, dc.window, P, s);
   }
 }
 
-void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, void* ws, cudaStream_t s,
-                      cudaEvent_t kernel_ready) {
-  if (a.slots == 0 || a.batch == 0 || a.length == 0) {
-    if (kernel_ready) cudaStreamWaitEvent(s, kernel_ready, 0);
-    return;
-  }
+template <typename CT>
+void conv_main(const StepArgs& a, long taps, const void* prologue_ws, void* ws, cudaStream_t s, cudaEvent_t kernel_ready) {
   const ConvGeom g = conv_geom(a.length, taps);
-  const auto* P = reinterpret_cast<const float2*>(static_cast<const char*>(prologue_ws) + ir_bytes(a.slots, taps));
-  auto* X = static_cast<float2*>(ws);
+  const auto* P = reinterpret_cast<const CT*>(static_cast<const char*>(prologue_ws) + ir_bytes(a.slots, taps));
+  auto* X = static_cast<CT*>(ws);
   const int per_slot = a.batch * g.nseg;
   const int items = a.slots * per_slot;
-  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, a, nullptr, 0, g, items, X, 0, false, s);
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, CT, ColSrc::Signal, a, nullptr, 0, g, items, X, 0, false, s);
   // The signal's column pass needs no kernel spectrum: join the prologue only here.
   if (kernel_ready) cudaStreamWaitEvent(s, kernel_ready, 0);
   if (conv_fuse_kernel_rows(g, a.slots)) {
-    MGB_DISPATCH_LN(g.log_n2, rows_conv_fk_t, g, items, per_slot, X, P, a.tw, s);
+    MGB_DISPATCH_LN(g.log_n2, rows_conv_fk_t, CT, g, items, per_slot, X, P, tw_table<CT>(a), s);
   } else {
-    MGB_DISPATCH_LN(g.log_n2, rows_conv_t, g, items, per_slot, X, P, a.tw, s);
+    MGB_DISPATCH_LN(g.log_n2, rows_conv_t, CT, g, items, per_slot, X, P, tw_table<CT>(a), s);
   }
-  MGB_DISPATCH_LN(g.log_n1, cols_inv_t, a, g, X, false, s);
+  MGB_DISPATCH_LN(g.log_n1, cols_inv_t, CT, a, g, X, false, s);
 }
 
-
-namespace {
-template <int LN2>
-void rows_bwd_t(const ConvGeom& g, int slots, int per_slot, float2* DY, float2* X, const float2* P, bool kfft,
-                const float2* tw, cudaStream_t s) {
-  constexpr int smem = 8 * padded(1 << LN2) * 8;
+template <int LN2, typename CT>
+void rows_bwd_t(const ConvGeom& g, int slots, int per_slot, CT* DY, CT* X, const CT* P, bool kfft, const CT* tw,
+                cudaStream_t s) {
+  constexpr int smem = 8 * padded(1 << LN2) * static_cast<int>(sizeof(CT));
   static const bool done = [] {
-    cudaFuncSetAttribute(rows_bwd<LN2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(rows_bwd<LN2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(rows_bwd<LN2, true, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(rows_bwd<LN2, false, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return true;
   }();
   (void)done;
   for_item_chunks(slots, [&](int s0, int n) {
     const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(n));
-    if (kfft) rows_bwd<LN2, true><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, per_slot, DY, X, P, tw, s0);
-    else rows_bwd<LN2, false><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, per_slot, DY, X, P, tw, s0);
+    if (kfft) rows_bwd<LN2, true, CT><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, per_slot, DY, X, P, tw, s0);
+    else rows_bwd<LN2, false, CT><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, per_slot, DY, X, P, tw, s0);
   });
 }
 
-template <int LN1>
-void cols_inv_buf_t(const ConvGeom& g, int slots, int per_slot, const float2* X, float2* out, long taps, const float2* tw,
+template <int LN1, typename CT>
+void cols_inv_buf_t(const ConvGeom& g, int slots, int per_slot, const CT* X, float2* out, long taps, const CT* tw,
                     cudaStream_t s) {
-  constexpr int C = kColElems / (1 << LN1);
-  constexpr int smem = C * (padded(1 << LN1) + 1) * 8;
+  constexpr int C = ColCfg<CT>::kElems / (1 << LN1);
+  constexpr int smem = ColCfg<CT>::kSmem(1 << LN1);
   static const bool done = [] {
-    cudaFuncSetAttribute(cols_inv_buf<LN1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(cols_inv_buf<LN1, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return true;
   }();
   (void)done;
   for_item_chunks(slots, [&](int s0, int n) {
     const dim3 grid(static_cast<unsigned>((1L << g.log_n2) / C), static_cast<unsigned>(n));
-    cols_inv_buf<LN1><<<grid, kColThreads, smem, s>>>(g.log_n, per_slot, X, out, taps, tw, s0);
+    cols_inv_buf<LN1, CT><<<grid, ColCfg<CT>::kThreads, smem, s>>>(g.log_n, per_slot, X, out, taps, tw, s0);
   });
 }
-}  // namespace
 
-std::size_t conv_bwd_bytes(const ConvGeom& g, int slots, int batch, long taps, int rev_frames) {
-  const std::size_t spec = align256(sizeof(float2) * static_cast<std::size_t>(slots) * batch * g.nseg * g.n);
-  const std::size_t blocks = static_cast<std::size_t>((rev_frames + kRevFpc - 1) / kRevFpc);
-  return 2 * spec + align256(sizeof(float2) * static_cast<std::size_t>(slots) * taps) +
-         align256(sizeof(double) * static_cast<std::size_t>(slots) * blocks * 4 * kRevBins);
-}
-
-void launch_conv_backward(bool reverb, const StepArgs& fw, const StepArgs& bw, const ReverbConst& rc,
-                          const DelayConst& dc, const void* prologue_ws, void* ws, double* grad, cudaStream_t s) {
-  if (fw.slots == 0 || fw.batch == 0 || fw.length == 0) return;
+template <typename CT>
+void conv_backward(bool reverb, const StepArgs& fw, const StepArgs& bw, const ReverbConst& rc, const DelayConst& dc,
+                   const void* prologue_ws, void* ws, double* grad, cudaStream_t s) {
   const long taps = reverb ? rc.length : dc.span;
   const ConvGeom g = conv_geom(fw.length, taps);
-  const auto* P = reinterpret_cast<const float2*>(static_cast<const char*>(prologue_ws) + ir_bytes(fw.slots, taps));
+  const auto* P = reinterpret_cast<const CT*>(static_cast<const char*>(prologue_ws) + ir_bytes(fw.slots, taps));
   // A large step's forward left the kernel spectrum at its column stage (rows_bwd transforms it).
   const bool kfft = conv_fuse_kernel_rows(g, fw.slots);
   const int per_slot = fw.batch * g.nseg;
   const int items = fw.slots * per_slot;
-  const std::size_t spec = align256(sizeof(float2) * static_cast<std::size_t>(items) * g.n);
-  auto* DY = static_cast<float2*>(ws);
-  auto* X = reinterpret_cast<float2*>(static_cast<char*>(ws) + spec);
+  const std::size_t spec = align256(sizeof(CT) * static_cast<std::size_t>(items) * g.n);
+  auto* DY = static_cast<CT*>(ws);
+  auto* X = reinterpret_cast<CT*>(static_cast<char*>(ws) + spec);
   auto* dh = reinterpret_cast<float2*>(static_cast<char*>(ws) + 2 * spec);
   auto* part = reinterpret_cast<double*>(static_cast<char*>(ws) + 2 * spec +
                                          align256(sizeof(float2) * static_cast<std::size_t>(fw.slots) * taps));
+  const CT* tw = tw_table<CT>(fw);
   // dY masked to each segment's own outputs (kernel gradient), x laid out as in the forward.
-  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, bw, nullptr, 0, g, items, DY, 0, true, s);
-  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, ColSrc::Signal, fw, nullptr, 0, g, items, X, 0, false, s);
-  MGB_DISPATCH_LN(g.log_n2, rows_bwd_t, g, fw.slots, per_slot, DY, X, P, kfft, fw.tw, s);
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, CT, ColSrc::Signal, bw, nullptr, 0, g, items, DY, 0, true, s);
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, CT, ColSrc::Signal, fw, nullptr, 0, g, items, X, 0, false, s);
+  MGB_DISPATCH_LN(g.log_n2, rows_bwd_t, CT, g, fw.slots, per_slot, DY, X, P, kfft, tw, s);
   if (g.nseg == 1) {
-    MGB_DISPATCH_LN(g.log_n1, cols_inv_t, bw, g, DY, false, s);
+    MGB_DISPATCH_LN(g.log_n1, cols_inv_t, CT, bw, g, DY, false, s);
   } else {
     // Each segment's correlation with the kernel covers [base_j, (j+1)*seg): overlap-add.
-    MGB_DISPATCH_LN(g.log_n1, cols_inv_t, bw, g, DY, true, s);
+    MGB_DISPATCH_LN(g.log_n1, cols_inv_t, CT, bw, g, DY, true, s);
     for_item_chunks(fw.slots * fw.batch, [&](int i0, int n) {
       const dim3 grid(static_cast<unsigned>((fw.length + 255) / 256), static_cast<unsigned>(n));
-      conv_ola<<<grid, 256, 0, s>>>(bw, seg_args(g, i0), g.n, DY);
+      conv_ola<CT><<<grid, 256, 0, s>>>(bw, seg_args(g, i0), g.n, DY);
     });
   }
-  MGB_DISPATCH_LN(g.log_n1, cols_inv_buf_t, g, fw.slots, per_slot, X, dh, taps, fw.tw, s);
+  MGB_DISPATCH_LN(g.log_n1, cols_inv_buf_t, CT, g, fw.slots, per_slot, X, dh, taps, tw, s);
   if (reverb) {
     const int blocks = (rc.frames + kRevFpc - 1) / kRevFpc;
     static const bool done = [] {
@@ -1354,6 +1373,38 @@ void launch_conv_backward(bool reverb, const StepArgs& fw, const StepArgs& bw, c
     const auto* rec = reinterpret_cast<const float*>(ir + static_cast<long>(fw.slots) * taps);
     delay_taps_adjoint<<<dim3(kTaps, fw.slots), 64, 0, s>>>(fw.params, rec, dh, dc.span, grad);
   }
+}
+}  // namespace
+
+void launch_conv_prologue(bool reverb, const StepArgs& a, const ReverbConst& rc, const DelayConst& dc, void* ws,
+                          cudaStream_t s) {
+  if (a.slots == 0) return;
+  if (fft_fp64()) conv_prologue<double2>(reverb, a, rc, dc, ws, s);
+  else conv_prologue<float2>(reverb, a, rc, dc, ws, s);
+}
+
+void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, void* ws, cudaStream_t s,
+                      cudaEvent_t kernel_ready) {
+  if (a.slots == 0 || a.batch == 0 || a.length == 0) {
+    if (kernel_ready) cudaStreamWaitEvent(s, kernel_ready, 0);
+    return;
+  }
+  if (fft_fp64()) conv_main<double2>(a, taps, prologue_ws, ws, s, kernel_ready);
+  else conv_main<float2>(a, taps, prologue_ws, ws, s, kernel_ready);
+}
+
+std::size_t conv_bwd_bytes(const ConvGeom& g, int slots, int batch, long taps, int rev_frames) {
+  const std::size_t spec = align256(spec_elem_bytes() * static_cast<std::size_t>(slots) * batch * g.nseg * g.n);
+  const std::size_t blocks = static_cast<std::size_t>((rev_frames + kRevFpc - 1) / kRevFpc);
+  return 2 * spec + align256(sizeof(float2) * static_cast<std::size_t>(slots) * taps) +
+         align256(sizeof(double) * static_cast<std::size_t>(slots) * blocks * 4 * kRevBins);
+}
+
+void launch_conv_backward(bool reverb, const StepArgs& fw, const StepArgs& bw, const ReverbConst& rc,
+                          const DelayConst& dc, const void* prologue_ws, void* ws, double* grad, cudaStream_t s) {
+  if (fw.slots == 0 || fw.batch == 0 || fw.length == 0) return;
+  if (fft_fp64()) conv_backward<double2>(reverb, fw, bw, rc, dc, prologue_ws, ws, grad, s);
+  else conv_backward<float2>(reverb, fw, bw, rc, dc, prologue_ws, ws, grad, s);
 }
 
 void launch_noise_stft(const double* noise, long length, int frames, float2* out, cudaStream_t s) {

@@ -142,6 +142,12 @@ constexpr int kTw384Off = 8192 + kCosN;      // float2 offset of the 384-point t
 constexpr int kCoverOff = kTw384Off + 384;   // float2 offset of the reverb inverse covers
 constexpr int kConstFloat2s = kCoverOff + 192;
 const float2* twiddle_table(int device);
+// kTwN forward twiddles exp(-2 pi i k / kTwN) in fp64 (the fp64 transforms' table).
+const double2* twiddle_table64(int device);
+// Arithmetic precision of the FFT-based steps (EQ, reverb, delay): false fp32, true fp64 (the
+// arena stays fp32 either way). Process-wide; see DESIGN.md (precision).
+bool fft_fp64();
+void set_fft_fp64(bool on);
 __host__ __device__ inline const double* cos_table(const float2* tw) { return reinterpret_cast<const double*>(tw + 8192); }
 __host__ __device__ inline const float2* tw384_table(const float2* tw) { return tw + kTw384Off; }
 // .x = 1/(384 w(o)) for the first hop, .y = 1/(384 (w(o) + w(o+192))) afterwards

@@ -21,6 +21,7 @@ struct StepArgs {
   const int* col;        // [nnz] source rows
   const double* params;  // first parameter row of the step (row-major, width per type)
   const float2* tw;      // twiddle table (fft_smem.cuh kTwN entries)
+  const double2* tw64 = nullptr;  // the same twiddles in fp64 (fp64 transforms)
   int slots;
   int batch;
   long length;           // L
@@ -54,6 +55,11 @@ __device__ __forceinline__ float2 gather2(const StepArgs& a, int e0, int e1, int
   }
   return make_float2(l, r);
 }
+
+// The twiddle table of a transform's element type.
+template <typename C> __device__ __forceinline__ const C* twiddles(const StepArgs& a);
+template <> __device__ __forceinline__ const float2* twiddles<float2>(const StepArgs& a) { return a.tw; }
+template <> __device__ __forceinline__ const double2* twiddles<double2>(const StepArgs& a) { return a.tw64; }
 
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
 

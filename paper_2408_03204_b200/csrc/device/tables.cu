@@ -52,6 +52,35 @@ const float2* twiddle_table(int device) {
   return d;
 }
 
+const double2* twiddle_table64(int device) {
+  static std::mutex mu;
+  static std::map<int, double2*> tables;
+  std::scoped_lock lock(mu);
+  auto it = tables.find(device);
+  if (it != tables.end()) return it->second;
+  std::vector<double2> host(kTwN);
+  for (int k = 0; k < kTwN; ++k) {
+    const double a = -2.0 * 3.14159265358979323846 * static_cast<double>(k) / kTwN;
+    host[static_cast<std::size_t>(k)] = make_double2(std::cos(a), std::sin(a));
+  }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  double2* d = nullptr;
+  if (cudaMalloc(&d, sizeof(double2) * host.size()) != cudaSuccess ||
+      cudaMemcpy(d, host.data(), sizeof(double2) * host.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaSetDevice(prev);
+    throw std::runtime_error("fp64 twiddle table upload failed");
+  }
+  cudaSetDevice(prev);
+  tables.emplace(device, d);
+  return d;
+}
+
+static bool g_fft_fp64 = false;
+bool fft_fp64() { return g_fft_fp64; }
+void set_fft_fp64(bool on) { g_fft_fp64 = on; }
+
 namespace {
 std::mutex g_prologue_mu;
 std::set<const void*>& prologue_set() {
