@@ -34,6 +34,13 @@ def conv_log(mg):
     mg.set_conv_log(0)
 
 
+@pytest.fixture
+def fp64(mg):
+    mg.set_fft_precision(64)
+    yield
+    mg.set_fft_precision(32)
+
+
 def device_render(mg, t, e, params, src, fs, backward=False):
     import torch
     procs = mg.ProcessorSet(sample_rate=fs)
@@ -127,3 +134,22 @@ def test_long_param_gradients_segmented_equal_single(mg, ref, conv_log, ty):
             fd = (np.sum(w * plan.render(hi, src, sample_rate=fs)) - np.sum(w * plan.render(lo, src, sample_rate=fs))) / (2 * h)
             assert abs(grads[0].reshape(-1)[i] - fd) <= 2e-3 * max(abs(fd), scale), (i, grads[0].reshape(-1)[i], fd)
         assert flat.size == grads[0].size
+
+
+@pytest.mark.parametrize("ty", [DELAY, REVERB])
+def test_fp64_transforms_long_forward_and_gradient(mg, ref, fp64, ty):
+    # mg_set_fft_precision(64): the same segmented convolution with fp64 arithmetic (fp32 arena)
+    # matches the reference, forward and input gradient, across several segments.
+    import torch
+    fs, L = 2000.0, (1 << 20) + 3000
+    t, e = chain(mg, ty)
+    params = ref.random_legal_params(t, e, 21 + ty)
+    rng = np.random.default_rng(ty + 40)
+    src = rng.uniform(-1, 1, size=(1, 1, 2, L))
+    w = rng.uniform(-1, 1, size=(1, 1, 2, L))
+    dr, rd, out = device_render(mg, t, e, params, src, fs, backward=True)
+    plan = ref.Plan(t, e, 1)
+    assert ref.rel_linf(out.cpu().numpy(), plan.render(params, src, sample_rate=fs)) < 2e-6
+    _, gsrc = dr.backward(torch.as_tensor(w, dtype=torch.float32, device=out.device))
+    want = plan.render(params, np.ascontiguousarray(w[..., ::-1]), sample_rate=fs)[..., ::-1]
+    assert ref.rel_linf(gsrc.cpu().numpy(), want) < 2e-6

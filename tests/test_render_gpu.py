@@ -551,3 +551,21 @@ def test_pointwise_epilogue_fusion_is_bit_exact(mg, ref, tracks, L, batch):
     assert torch.equal(fused.view(torch.int32), dr.arena.view(torch.int32))
     want = ref.Plan(t, e, 1).render(params, src)
     assert rel(fused[rd.output_begin:].cpu().numpy(), want) < TOL
+
+
+def test_fp64_transforms_config2(mg, ref):
+    # The fp64-arithmetic mode of every FFT-based step (EQ, reverb, delay) on config 2 at full
+    # size; the EQ steps' own error drops ~2x (arena and the other processors stay fp32).
+    t, e, params = wl.config2()
+    L = wl.L2
+    src = wl.sources(int(np.sum(t == 0)), L)
+    rd = mg.compute_render_data_arrays(t, e)
+    procs = mg.ProcessorSet()
+    want = ref.Plan(t, e, 1).render(params, src)
+    mg.set_fft_precision(64)
+    try:
+        assert mg.fft_precision() == 64
+        y = mg.render(rd, procs, rd.reorder_params(params), src)
+    finally:
+        mg.set_fft_precision(32)
+    assert rel(y, want) < TOL
