@@ -159,12 +159,15 @@ inline const char* what_of(const std::exception& e) { return e.what(); }
 #include <cstring>
 int main(int argc, char** argv) {
   const char* filter = nullptr;
+  const char* file_filter = nullptr;  // doctest's --source-file (substring of the case's file)
   for (int i = 1; i < argc; ++i) {
     if (std::strncmp(argv[i], "--test-case=", 12) == 0) filter = argv[i] + 12;
+    if (std::strncmp(argv[i], "--source-file=", 14) == 0) file_filter = argv[i] + 14;
   }
   int cases = 0, failed_cases = 0;
   for (const auto& tc : ::doctest::detail::registry()) {
     if (filter && std::string(tc.name).find(filter) == std::string::npos) continue;
+    if (file_filter && std::string(tc.file).find(file_filter) == std::string::npos) continue;
     ++cases;
     ::doctest::detail::current_failed() = false;
     try {
