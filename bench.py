@@ -1,22 +1,32 @@
 #!/usr/bin/env python
-"""Benchmark: node-samples/s and graph renders/s of the batched render path.
+"""Benchmark: node-samples/s and graph renders/s of the batched render path (BASELINE.json).
 
-Workload (BASELINE.json configs[1], "config 2"): the paper-style mixing console
-generate_console(16, {p=0.3, seed=16}) — 121 nodes, 139 edges, 13 steps over 8 processor
-types — rendering 16 stereo sources of 2^17 samples at 44.1 kHz (B = 1). Sources are
-dsp::uniform_noise(2L, 1000+k) (`bench.cpp:33-40`), parameters testutil::random_legal_params
-(seed 2024 + rank), all generated by the product's bit-identical generators (synthetic data).
+Headline workload (the largest single-GPU BASELINE config, config 5): 512 random mixing
+consoles (generate_console(K_i in [4, 32], p = 0.3), the reference's generator, bit-identical;
+random_legal_params per graph), stereo 2^17 samples at 44.1 kHz, B = 1, sources from a 64-row
+uniform_noise bank (input k of a union takes row k % 64). The set is sharded over the ranks by
+LPT on node-sample cost (graphs are independent: no collective on the data path) and every
+rank renders its shard as unions of <= 64 consoles. A step = one render of all 512 graphs
+(every processor of every node, no skipped work).
 
-A step = one full render of the graph (every processor, no skipped work), inputs resident in
-HBM, replayed as one captured CUDA graph. One process per GPU (torchrun for N > 1): each rank renders its own console instance
-(graphs are independent, no data-path collective) -> "scaling": "weak"; value = node-samples
-of all ranks / max-over-ranks device time. L2 is flushed (512 MiB write) between timed
-iterations; each iteration is bracketed by CUDA events on the launching stream. The
-per-step roofline breakdown times each step (prologue + audio pass) repeated back to back
-between one CUDA event pair on the launching stream (profiles/ holds the ncu evidence).
+  value  — device time: each union's render captured as one CUDA graph, inputs resident in
+           HBM, all unions replayed back to back; CUDA events on the replay stream around each
+           step, max over ranks (barrier + synchronize on both sides). The working set (the
+           arenas, ~60 GB) is far larger than L2, so no flush is needed between steps.
+  e2e    — the same 512 graphs through the public API with HOST buffers (BatchRenderer /
+           mg_batch_submit: pinned fp32 sources per input node, original-order parameter
+           tables, device reorder, render, output D2H), host<->device copies inside the timed
+           region; wall clock, max over ranks. Bytes per step are counted from the copies.
+  scaling — "strong": the 512 graphs are split over N ranks.
 
---impl reference times the reference's own CPU renderer (oracle/_ref, the unmodified
-reference compiled with the FFTW-API stand-in) on the host cores, one process per core.
+--impl reference times the reference's own CPU renderer (oracle/_ref: the unmodified reference
+compiled with the FFTW-API stand-in) on the box's host cores, one process per core, each step
+a bounded sample of the same 512-graph set. Secondary lines (config 2, 3, 4, config 5's
+optimisation step) ride along under their own keys at N = 1.
+
+--backend gloo runs the N > 1 path with gloo (CPU-side timing reductions) and lets ranks share
+GPUs (rank r on cuda:(r mod devices)): for exercising multi-rank code on one GPU, not for
+scaling numbers.
 """
 import argparse
 import json
@@ -28,25 +38,28 @@ import time
 
 import numpy as np
 
-import workloads as wl
-
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-L = 1 << 17
-FS = 44100.0
-TRACKS, PRUNE, GSEED = 16, 0.3, 16
-WORKLOAD = "config2: generate_console(16, p=0.3, seed=16), 121 nodes / 139 edges, stereo 2^17 @ 44.1 kHz, B=1"
+import workloads as wl  # noqa: E402
+
+L = wl.L2
+FS = wl.FS
 METRIC = "node-samples/sec"
 UNIT = "node-samples/s"
+CHUNK = 64  # consoles per union (one plan, one arena, one CUDA graph)
+WORKLOAD = ("config5: 512 random consoles (generate_console K in [4,32], p=0.3, fixed topology), stereo 2^17 @ "
+            "44.1 kHz, B=1, LPT-sharded over ranks, unions of <= 64 consoles per rank")
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
-    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
+    p.add_argument("--no-extras", action="store_true", help="skip the secondary config lines")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
@@ -58,6 +71,9 @@ def peaks():
         return float(d["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # nominal CUDA-core FP32 at the max SM clock
 
 
 class ClockSampler:
@@ -111,112 +127,273 @@ class ClockSampler:
 
 
 def dist_setup():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def step_bytes(rd, batch, length):
-    """Algorithmic HBM bytes per step: every gathered row read once, every output row written once."""
-    return [4 * 2 * length * batch * (len(s.gather) + (s.store_end - s.store_begin)) for s in rd.steps]
+# ---- the config-5 workload -----------------------------------------------------------------
+
+def config5_shard(rank, world):
+    """(graphs, my graph indices, unions of <= CHUNK of them) for this rank."""
+    from paper_2408_03204_b200 import sharding
+    graphs = wl.config5_graphs()
+    mine = sharding.lpt_shards([sharding.graph_cost(t, L) for t, _ in graphs], world)[rank]
+    return graphs, mine, [mine[i:i + CHUNK] for i in range(0, len(mine), CHUNK)]
 
 
-def cpu_reference_sample(renders=1):
-    """Reference CPU renderer (oracle/_ref) on one core: node-samples/s over `renders` full renders."""
+def union_case(mg, graphs, idx):
+    """Union plan of graphs[idx] with the members' own parameter tables (concat_params order)."""
+    from paper_2408_03204_b200 import sharding
+    members = [graphs[i] for i in idx]
+    t, e = sharding.union_arrays(members)
+    rd = mg.compute_render_data_arrays(t, e)
+    params = wl.union_params([m[0] for m in members], [wl.config5_member_params(i, graphs[i][0]) for i in idx])
+    return t, rd, params
+
+
+def node_samples(t, length=L, batch=1):
+    return (len(t) - int(np.sum(np.asarray(t) == 0))) * length * batch
+
+
+# ---- roofline of the kernels as they run inside the render ---------------------------------
+
+def kernel_family(name):
+    for key in ("rows_conv_fk", "rows_conv", "rows_spec", "cols_fwd", "cols_inv", "eq_conv", "dyn_scan",
+                "pointwise_wide", "pointwise_chain", "pointwise", "reverb_ir", "eq_response_basis", "eq_mag_tiles",
+                "delay_taps", "eq_design", "eq_response", "eq_mags", "param_gather"):
+        if key in name:
+            return key
+    return name.split("(")[0][-40:]
+
+
+def in_render_kernel_times(replay):
+    """CUPTI (torch.profiler) trace of one replay: per kernel family, total device time (us),
+    launches and the wall span of the replay; kernels inside CUDA graphs are reported one by
+    one with their in-render (concurrent) durations."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        replay()
+        torch.cuda.synchronize()
+    fam, t0, t1 = {}, None, None
+    for ev in prof.events():
+        if ev.device_type.name != "CUDA" or "memset" in ev.name.lower() or "memcpy" in ev.name.lower():
+            continue
+        d = fam.setdefault(kernel_family(ev.name), {"us": 0.0, "launches": 0})
+        d["us"] += ev.time_range.end - ev.time_range.start
+        d["launches"] += 1
+        t0 = ev.time_range.start if t0 is None else min(t0, ev.time_range.start)
+        t1 = ev.time_range.end if t1 is None else max(t1, ev.time_range.end)
+    return fam, (t1 - t0) if t0 is not None else None
+
+
+def conv_flops(mg, procs, rd, length):
+    """FP32 flops of the implemented long-convolution passes per render of `rd`, by kernel
+    family: every segment item runs N-point four-step transforms (5 N log2 N per transform):
+    cols_fwd (signal: column half), rows_conv (row half of the forward + inverse, product),
+    cols_inv (column half of the inverse); prologue (kernel spectrum) cols_fwd + rows_spec."""
+    out = {"cols_fwd": 0.0, "rows_conv": 0.0, "cols_inv": 0.0, "rows_spec": 0.0}
+    for st in rd.steps:
+        if st.type not in (mg.NodeType.REVERB, mg.NodeType.DELAY):
+            continue
+        slots = st.store_end - st.store_begin
+        taps = procs.reverb_length if st.type == mg.NodeType.REVERB else procs.delay_span
+        g = mg.conv_geometry(length, taps)
+        n, l1, l2 = 1 << g["log_n"], g["log_n1"], g["log_n2"]
+        items = slots * g["nseg"]
+        out["cols_fwd"] += (items + slots) * 5.0 * n * l1        # signal + kernel column passes
+        out["cols_inv"] += items * 5.0 * n * l1
+        if 8.0 * slots * n > (64 << 20):  # conv_fuse_kernel_rows: kernel rows transformed per item
+            out["rows_conv_fk"] = out.get("rows_conv_fk", 0.0) + items * (3 * 5.0 * n * l2 + 16.0 * n)
+        else:
+            out["rows_spec"] += slots * 5.0 * n * l2
+            out["rows_conv"] += items * (2 * 5.0 * n * l2 + 16.0 * n)  # forward + inverse rows, product
+    return out
+
+
+# ---- reference CPU renders (cpu_baseline and --impl reference) -----------------------------
+
+def _ref_render_graphs(args):
+    idx, reps = args
+    from oracle import ref
+    graphs = wl.config5_graphs()
+    bank = wl.source_bank(64, L)
+    ns, dt = 0, 0.0
+    for _ in range(reps):
+        for i in idx:
+            t, e = graphs[i]
+            k = int(np.sum(t == 0))
+            src = bank[[j % 64 for j in range(k)]]
+            p = ref.Plan(t, e, 1)
+            t0 = time.perf_counter()
+            p.render(wl.config5_member_params(i, t), src, sample_rate=FS)
+            dt += time.perf_counter() - t0
+            ns += node_samples(t)
+    return ns, dt
+
+
+def reference_sample(procs_n, graphs_per_proc, step):
+    """One bounded step of the reference on `procs_n` processes: graphs step*P*G + ... of the
+    512-graph set (a rotating sample); returns (node-samples, wall seconds)."""
+    import multiprocessing as mp
+    start = (step * procs_n * graphs_per_proc) % 512
+    work = [([(start + p * graphs_per_proc + j) % 512 for j in range(graphs_per_proc)], 1) for p in range(procs_n)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs_n) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_ref_render_graphs, work)
+        wall = time.perf_counter() - t0
+    return sum(r[0] for r in res), wall
+
+
+def reference_arm(args):
+    rank, world, _ = dist_setup()
+    if rank != 0:
+        return
     from oracle import ref
     if not ref.available():
-        return None
-    t, e = ref.console(TRACKS, PRUNE, GSEED)
-    params = ref.random_legal_params(t, e, 2024)
-    src = np.stack([ref.uniform_noise(2 * L, 1000 + k).reshape(1, 2, L) for k in range(int(np.sum(t == 0)))])
-    plan = ref.Plan(t, e, 1)
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmixgraph_ref.so not built"}))
+        return
+    cores = os.cpu_count() or 1
+    warm = max(1, min(args.warmup, 1))
+    steps = max(1, min(args.steps, 12))
+    for s in range(warm):
+        reference_sample(cores, 1, s)
+    ns, wall = 0, 0.0
+    for s in range(steps):
+        n, w = reference_sample(cores, 1, warm + s)
+        ns, wall = ns + n, wall + w
+    value = ns / wall
+    sample = (f"{steps} steps x {cores} processes x 1 config-5 graph each (rotating through the 512-graph set; "
+              f"reference render(), oracle/_ref with the FFTW-API stand-in FFT), {wall:.1f} s wall")
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "graph_renders_per_sec": steps * cores / wall, "n_gpus": world, "steps": steps, "warmup": warm,
+        "ms_per_step": wall / steps * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (reference generators: generate_console, random_legal_params, uniform_noise)",
+        "config": {"workload": WORKLOAD, "length": L, "batch": 1, "sample_rate": FS},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+# ---- secondary configs (N = 1) ---------------------------------------------------------------
+
+def config2_lines(mg, procs, dev, steps=20, warmup=3):
+    """Config 2 (console-16, 121 nodes, 2^17): device time of the captured render (L2 flushed
+    between iterations) and e2e through RenderPipeline with double host audio."""
+    import torch
+    t, e, params = wl.config2()
+    rd = mg.compute_render_data_arrays(t, e)
+    P = rd.reorder_params(params)
+    src = wl.sources(rd.num_inputs, L)
+    dr = mg.DeviceRenderer(rd, procs, 1, L, P, device=dev)
+    dr.sources.copy_(torch.as_tensor(src, dtype=torch.float32))
+    g = dr.capture()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(warmup):
+        g.replay()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        flush.fill_(i & 0xFF)
+        ev[i][0].record(stream)
+        g.replay()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
+    ns = node_samples(t)
+    fam, span = in_render_kernel_times(g.replay)
+    pipe = mg.RenderPipeline(rd, procs, 1, L, dtype=np.float64, depth=2)
+    ps = pipe.pinned(src.shape)
+    ps[...] = src
+    outs = [pipe.pinned((rd.buffer_rows - rd.output_begin, 1, 2, L)) for _ in range(2)]
+    for i in range(3):
+        pipe.submit(P, ps, outs[i % 2])
+    pipe.sync()
     t0 = time.perf_counter()
-    for _ in range(renders):
-        plan.render(params, src, sample_rate=FS)
-    dt = time.perf_counter() - t0
-    ns = (len(t) - int(np.sum(t == 0))) * L
-    return ns * renders / dt, dt
+    for i in range(steps):
+        pipe.submit(P, ps, outs[i % 2])
+    pipe.sync()
+    e2e_s = (time.perf_counter() - t0) / steps
+    del g, dr, pipe, flush
+    torch.cuda.empty_cache()
+    return {"value": ns / (ms * 1e-3), "unit": UNIT, "ms_per_render": ms, "graph_renders_per_sec": 1e3 / ms,
+            "e2e": {"value": ns / e2e_s, "unit": UNIT, "ms_per_render": e2e_s * 1e3,
+                    "api": "RenderPipeline (mg_pipeline_submit), double host audio, pinned"},
+            "in_render_us": {k: round(v["us"], 1) for k, v in sorted(fam.items(), key=lambda kv: -kv[1]["us"])},
+            "render_span_us_traced": span, "gpu_launches_per_render": rd.kernel_count(1, L),
+            "workload": "config2: generate_console(16, p=0.3, seed=16), 121 nodes / 139 edges, stereo 2^17, B=1; "
+                        "L2 flushed between iterations",
+            "type_string": rd.schedule.type_codes()}
 
 
 def config3_rate(mg, procs, dev, steps=6, warmup=2, graphs=64):
-    """BASELINE config 3: a batch of 64 random mixing graphs per step whose topology is
-    re-drawn every step (generate_console(K_i in [4, 32], p=0.3, seed=1000*step+i), union).
-    The batches (topology arrays + random_legal_params in original row order) are prepared
-    ahead like a dataset; the timed loop does the product work per batch: the plan build
-    (compute_render_data on the union, C++ on a worker thread one batch ahead), then
-    BatchRenderer.submit — pinned staging + async upload of the step table and parameters,
-    device parameter reorder, the render, and the D2H of the 64 output rows — into pools
-    sized once. Sources: a 64-row device noise bank (uniform_noise(2L, 1000+k)) cycled over
-    the union's inputs. Wall clock over the timed steps (host plan build included)."""
+    """Config 3: 64 consoles per step with topology re-drawn every step (wl.config3_members);
+    plan build (compute_render_data, C++) on a worker thread one batch ahead, then
+    BatchRenderer.submit (async plan + original-order parameter upload, device reorder,
+    render, 64-output D2H). Wall clock over the timed steps, host plan build included."""
     import queue
-    import threading
 
     import torch
 
     from paper_2408_03204_b200 import sharding
     batches = []
     for st in range(warmup + steps):
-        rng = np.random.default_rng(st)
-        members = [wl.generate_console_arrays(int(rng.integers(4, 33)), PRUNE, 1000 * st + i) for i in range(graphs)]
+        members = wl.config3_members(st, graphs)
         t, e = sharding.union_arrays(members)
-        batches.append((t, e, wl.random_legal_params(t, 5000 + st)))
+        batches.append((t, e, wl.random_legal_params(t, wl.config3_params_seed(st))))
     cap = np.zeros(4, dtype=np.uint64)
-    for t, e, _ in batches:  # pools sized once for the dataset's largest batch
+    for t, e, _ in batches:
         cap = np.maximum(cap, mg.BatchRenderer.capacity_of(mg.compute_render_data_arrays(t, e), procs, 1, L))
     br = mg.BatchRenderer(procs, 1, L, cap, depth=2)
-    bank = torch.as_tensor(np.stack([mg.uniform_noise(2 * L, 1000 + k).reshape(1, 2, L) for k in range(64)]),
-                           dtype=torch.float32).to(dev)
+    bank = torch.as_tensor(wl.source_bank(64, L), dtype=torch.float32).to(dev)
     outs = [torch.empty((graphs, 1, 2, L), dtype=torch.float32, pin_memory=True).numpy() for _ in range(2)]
-
     q = queue.Queue(maxsize=2)
 
     def producer():
         for t, e, params in batches:
-            q.put((mg.compute_render_data_arrays(t, e), params, len(t)))
+            q.put((mg.compute_render_data_arrays(t, e), params, t))
 
     th = threading.Thread(target=producer, daemon=True)
     th.start()
-    ns, n_nodes, t0 = 0, [], None
+    ns, t0 = 0, None
     for i in range(warmup + steps):
-        rd, params, nv = q.get()
+        rd, params, t = q.get()
         if i == warmup:
             br.sync()
             t0 = time.perf_counter()
         br.submit(rd, params, bank, outs[i % 2], validate=True)
         if i >= warmup:
-            ns += (nv - rd.num_inputs) * L
-            n_nodes.append(nv)
+            ns += node_samples(t)
     br.sync()
     dt = time.perf_counter() - t0
     th.join()
+    del br, bank
+    torch.cuda.empty_cache()
     return {"value": ns / dt, "unit": UNIT, "graph_renders_per_sec": graphs * steps / dt, "steps": steps,
-            "warmup": warmup, "ms_per_step": dt / steps * 1e3, "graphs_per_step": graphs, "nodes_per_step": n_nodes,
+            "warmup": warmup, "ms_per_step": dt / steps * 1e3, "graphs_per_step": graphs,
             "workload": "config3: 64 random consoles per step (K in [4,32], p=0.3), topology re-drawn every step, "
-                        "stereo 2^17, B=1; plan build on a worker thread one batch ahead, BatchRenderer "
-                        "(async plan + original-order parameter upload, device reorder, render, 64-row D2H); "
-                        "wall clock",
+                        "stereo 2^17; plan build one batch ahead on a worker thread; BatchRenderer; wall clock",
             "data": "synthetic; sources from a 64-row device noise bank"}
 
 
 def config4_rate(mg, procs, dev, steps=3, warmup=2):
-    """BASELINE config 4: generate_large_console(64) — 966 nodes, 1093 edges — rendering 64
-    stereo sources of 10 s (L = 441,000, 2^20-point reverb/delay convolutions), forward alone
-    (captured render) and the optimisation step: forward + MSE loss + reverse-mode pass
-    (every parameter's gradient) + gradient step (training.Trainer, all types trainable).
-    Device time (CUDA events on the launching stream); the 3.4 GB arena exceeds L2."""
+    """Config 4: generate_large_console(64), 966 nodes, 10 s (L = 441,000; the reverb/delay
+    convolutions as three 2^18-point overlap-save segments): forward (captured render) and the
+    optimisation step (forward + MSE + reverse-mode pass over every parameter + update).
+    Device time (CUDA events)."""
     import torch
 
     from paper_2408_03204_b200 import training
-    L4 = 441000
+    L4 = wl.L4
     t, e = wl.generate_large_console_arrays(64)
     rd = mg.compute_render_data_arrays(t, e)
     P = rd.reorder_params(wl.random_legal_params(t, 4040))
-    trainable = [int(x) for x in P]
-    tr = training.Trainer(rd, procs, 1, L4, P, trainable=trainable, learning_rate=1e-3, device=dev)
-    src = torch.empty((rd.num_inputs, 1, 2, L4), dtype=torch.float32, device=dev)
-    for k in range(rd.num_inputs):
-        src[k].copy_(torch.as_tensor(mg.uniform_noise(2 * L4, 1000 + k).reshape(1, 2, L4), dtype=torch.float32))
+    tr = training.Trainer(rd, procs, 1, L4, P, trainable=[int(x) for x in P], learning_rate=1e-3, device=dev)
+    src = torch.as_tensor(wl.sources(rd.num_inputs, L4), dtype=torch.float32).to(dev)
     tgt = torch.zeros((rd.buffer_rows - rd.output_begin, 1, 2, L4), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     tr.dr.sources.copy_(src)
@@ -236,11 +413,10 @@ def config4_rate(mg, procs, dev, steps=3, warmup=2):
 
     fwd_ms = timed(graph.replay)
     train_ms = timed(lambda: tr.step(src, tgt))
-    ns = (len(t) - rd.num_inputs) * L4
+    ns = node_samples(t, L4)
     out = {"value": ns / (train_ms * 1e-3), "unit": UNIT, "graph_renders_per_sec": 1e3 / train_ms,
            "ms_per_step": train_ms, "forward_ms": fwd_ms, "forward_node_samples_per_sec": ns / (fwd_ms * 1e-3),
            "steps": steps, "warmup": warmup, "nodes": len(t), "edges": len(e), "type_string": rd.schedule.type_codes(),
-           "loss": float(tr.loss.item()),
            "workload": "config4: generate_large_console(64), 966 nodes / 1093 edges, stereo 10 s (L=441000) @ "
                        "44.1 kHz, B=1; step = forward + MSE + backward (all parameter gradients) + SGD update",
            "data": "synthetic (uniform_noise sources, random_legal_params, zero target)"}
@@ -249,83 +425,20 @@ def config4_rate(mg, procs, dev, steps=3, warmup=2):
     return out
 
 
-def config5_graphs(n=512, seed=5):
-    import paper_2408_03204_b200 as mg
-    rng = np.random.default_rng(seed)
-    return [wl.generate_console_arrays(int(rng.integers(4, 33)), PRUNE, 50000 + i) for i in range(n)]
-
-
-def config5_rate(mg, procs, dev, rank, world, steps=3, warmup=1, chunk=64):
-    """BASELINE config 5 (forward): 512 random consoles (K in [4,32], p=0.3, fixed topology)
-    sharded over the ranks by LPT on node-sample cost, no collective on the data path. Each
-    rank renders its shard as unions of <= 64 consoles through one BatchRenderer (plans built
-    once, outside the timed region). Strong scaling: value = node-samples of all 512 graphs /
-    max-over-ranks wall time of a step (barrier + device sync on both sides)."""
-    import torch
-    import torch.distributed as dist
-
-    from paper_2408_03204_b200 import sharding
-    graphs = config5_graphs()
-    costs = [sharding.graph_cost(t, L) for t, _ in graphs]
-    mine = sharding.lpt_shards(costs, world)[rank]
-    chunks = [mine[i:i + chunk] for i in range(0, len(mine), chunk)]
-    plans = []
-    cap = np.zeros(4, dtype=np.uint64)
-    for c in chunks:
-        t, e = sharding.union_arrays([graphs[i] for i in c])
-        rd = mg.compute_render_data_arrays(t, e)
-        plans.append((rd, wl.random_legal_params(t, 7000 + c[0])))
-        cap = np.maximum(cap, mg.BatchRenderer.capacity_of(rd, procs, 1, L))
-    br = mg.BatchRenderer(procs, 1, L, cap, depth=2)
-    bank = torch.as_tensor(np.stack([mg.uniform_noise(2 * L, 1000 + k).reshape(1, 2, L) for k in range(64)]),
-                           dtype=torch.float32).to(dev)
-
-    def step():
-        for rd, p in plans:
-            br.submit(rd, p, bank, None, validate=False)
-        br.sync()
-
-    for _ in range(warmup):
-        step()
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        step()
-    dt = (time.perf_counter() - t0) / steps
-    tt = torch.tensor([dt], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    dt = float(tt.item())
-    ns_all = sum((len(t) - int(np.sum(t == 0))) * L for t, _ in graphs)
-    del br
-    torch.cuda.empty_cache()
-    return {"value": ns_all / dt, "unit": UNIT, "graph_renders_per_sec": len(graphs) / dt, "ms_per_step": dt * 1e3,
-            "steps": steps, "warmup": warmup, "graphs": len(graphs), "graphs_on_rank0": len(mine) if rank == 0 else None,
-            "n_gpus": world, "scaling": "strong",
-            "workload": "config5 forward: 512 random consoles (K in [4,32], p=0.3), stereo 2^17, B=1, LPT-sharded "
-                        "over ranks, unions of <= 64 per BatchRenderer submit; wall clock, max over ranks",
-            "data": "synthetic; sources from a 64-row device noise bank"}
-
-
 def config5_train_rate(mg, procs, dev, rank, world, steps=4, warmup=2, batch=2):
-    """BASELINE config 5's optimisation variant: one console-16 parameter set shared by every
-    rank, each rank a batch of its own sources (data parallel); step = forward + MSE +
-    backward + ONE NCCL all-reduce of the flat fp64 gradient buffer + gradient step. Weak
-    scaling; value = node-samples of all ranks / max-over-ranks device time."""
+    """Config 5's optimisation variant: one console-16 parameter set shared by every rank,
+    each rank a batch of its own sources (data parallel); step = forward + MSE + backward +
+    ONE all-reduce of the flat fp64 gradient buffer + gradient step. Weak scaling."""
     import torch
     import torch.distributed as dist
 
     from paper_2408_03204_b200 import training
-    g = wl.generate_console(TRACKS, PRUNE, GSEED)
-    fg = mg.to_flat(g)
-    rd = mg.compute_render_data(fg)
-    P = rd.reorder_params(wl.random_legal_params(fg.node_types, 2024))
+    t, e, params = wl.config2()
+    rd = mg.compute_render_data_arrays(t, e)
+    P = rd.reorder_params(wl.random_legal_params(t, 2024))
     tr = training.Trainer(rd, procs, batch, L, P, trainable=[int(x) for x in P], learning_rate=1e-3,
                           group=dist.group.WORLD if world > 1 else None, device=dev)
-    K = rd.num_inputs
-    src = torch.as_tensor(np.stack([np.stack([mg.uniform_noise(2 * L, 1000 + 100 * rank + 10 * b + k).reshape(2, L)
-                                              for b in range(batch)]) for k in range(K)]), dtype=torch.float32).to(dev)
+    src = torch.as_tensor(wl.sources(rd.num_inputs, L, batch, base_seed=1000 + 100 * rank), dtype=torch.float32).to(dev)
     tgt = torch.zeros((rd.buffer_rows - rd.output_begin, batch, 2, L), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     for _ in range(warmup):
@@ -339,316 +452,217 @@ def config5_train_rate(mg, procs, dev, rank, world, steps=4, warmup=2, batch=2):
         tr.step(src, tgt)
     b.record(stream)
     torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / steps
-    tt = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    ms = float(tt.item())
-    ns = (fg.num_nodes() - K) * L * batch * world
+    ms = max_over_ranks(a.elapsed_time(b) / steps, dev, world)
+    ns = node_samples(t) * batch * world
     grad_bytes = int(tr.flat.numel() * 8)
     del tr
     torch.cuda.empty_cache()
     return {"value": ns / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "steps": steps, "warmup": warmup,
             "n_gpus": world, "scaling": "weak", "batch_per_rank": batch, "allreduce_bytes": grad_bytes,
-            "collective": "NCCL all-reduce (sum) of the flat fp64 gradient buffer, 1 per step" if world > 1 else "none (1 GPU)",
+            "collective": "all-reduce (sum) of the flat fp64 gradient buffer, 1 per step" if world > 1 else "none (1 GPU)",
             "workload": "config5 optimisation: console-16 (121 nodes) shared parameters, per-rank batch of 2 stereo "
                         "2^17 sources; forward + MSE + backward + all-reduce + SGD (all types trainable)",
             "data": "synthetic (uniform_noise sources, zero target)"}
 
 
+_BACKEND = "nccl"
+
+
+def max_over_ranks(x, dev, world):
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev if _BACKEND == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---- the B200 arm ---------------------------------------------------------------------------
+
 def b200_arm(args):
+    global _BACKEND
     import torch
     import torch.distributed as dist
 
     import paper_2408_03204_b200 as mg
 
     rank, world, local = dist_setup()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = max(1, torch.cuda.device_count())
+    dev_index = local % ndev
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    _BACKEND = args.backend
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
-    g = wl.generate_console(TRACKS, PRUNE, GSEED)
-    fg = mg.to_flat(g)
-    rd = mg.compute_render_data(fg, mg.Strategy.GREEDY)
-    params = wl.random_legal_params(fg.node_types, 2024 + rank)
-    P = rd.reorder_params(params)
-    K = rd.num_inputs
-    src = np.stack([mg.uniform_noise(2 * L, 1000 + k).reshape(1, 2, L) for k in range(K)])
-    procs = mg.ProcessorSet(sample_rate=FS, device=local)
-    dr = mg.DeviceRenderer(rd, procs, 1, L, P, device=dev)
-    dr.sources.copy_(torch.as_tensor(src, dtype=torch.float32))
-    node_samples = (fg.num_nodes() - K) * L
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    procs = mg.ProcessorSet(sample_rate=FS, device=dev_index)
+    graphs, mine, unions = config5_shard(rank, world)
+    ns_all = sum(node_samples(t) for t, _ in graphs)
+    ns_mine = sum(node_samples(graphs[i][0]) for i in mine)
+    bank_host = wl.source_bank(64, L)
+    bank = torch.as_tensor(bank_host, dtype=torch.float32).to(dev)
+
+    # Device-resident renders: one DeviceRenderer + captured graph per union, inputs copied in
+    # once (input k <- bank row k % 64).
+    cases, renderers, captured, kernels_per_step = [], [], [], 0
+    for idx in unions:
+        t, rd, params = union_case(mg, graphs, idx)
+        dr = mg.DeviceRenderer(rd, procs, 1, L, rd.reorder_params(params), device=dev)
+        dr.sources.copy_(bank[torch.arange(rd.num_inputs, device=dev) % 64])
+        renderers.append(dr)
+        captured.append(dr.capture())
+        cases.append((t, rd, params))
+        kernels_per_step += rd.kernel_count(1, L)
     stream = torch.cuda.current_stream(dev)
 
-    graph = dr.capture()  # whole render (13 steps, side-stream prologues) as one CUDA graph
-    for _ in range(max(args.warmup, 3)):
-        graph.replay()
-    torch.cuda.synchronize()
+    def step():
+        for g in captured:
+            g.replay()
 
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
     n = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev_index)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     sampler.start()
     wall0 = time.perf_counter()
-    step_ms_runs = []
     for i in range(n):
-        flush.fill_(i & 0xFF)  # evict the arena from L2 between timed iterations (not timed)
         ev[i][0].record(stream)
-        graph.replay()
+        step()
         ev[i][1].record(stream)
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
     clocks = sampler.stop()
-    if world > 1:
-        dist.barrier()
-    per_iter = [a.elapsed_time(b) for a, b in ev]
-    dev_ms = float(sum(per_iter))
-    # Per-step breakdown from the same timed iterations' events (re-read after the fact).
-    t_dev = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
-    dev_ms_max = float(t_dev.item())
+    dev_ms = float(sum(a.elapsed_time(b) for a, b in ev))
+    dev_ms_max = max_over_ranks(dev_ms, dev, world)
 
-    # Per-step times, isolated: each step (its parameter prologue + audio pass) re-run
-    # back to back between one CUDA event pair on this stream (mg_profile_steps).
-    from paper_2408_03204_b200.device import profile_steps
-    steps_ms = profile_steps(dr, reps=max(n, 10), stream=stream).astype(np.float64)
+    # In-render kernel timings of one step (CUPTI trace, outside the timed region).
+    fam, span_us = in_render_kernel_times(step)
+    flops = {}
+    for _, rd, _ in cases:
+        for k, v in conv_flops(mg, procs, rd, L).items():
+            flops[k] = flops.get(k, 0.0) + v
 
-    # End to end through the public host API, on every rank at once (whole-job number at N
-    # GPUs: all ranks' renders / max-over-ranks wall time, barriers on both sides). Every
-    # step: params + sources H2D from pinned host memory, the render, outputs D2H. Headline:
-    # RenderPipeline with double host audio (the reference's AudioBuffer precision),
-    # consecutive steps overlapping their copies with the previous step's kernels; also
-    # reported: float host audio, and the blocking mg_render call.
-    pbytes = int(sum(v.size for v in P.values()) * 8)
-    n_out = rd.buffer_rows - rd.output_begin
+    # End to end through the public API with host buffers: BatchRenderer (mg_batch_submit),
+    # pinned fp32 sources per input node, original-order parameters, outputs D2H.
+    cap = np.zeros(4, dtype=np.uint64)
+    for _, rd, _ in cases:
+        cap = np.maximum(cap, mg.BatchRenderer.capacity_of(rd, procs, 1, L))
+    for dr in renderers:
+        del dr
+    del captured, renderers
+    torch.cuda.empty_cache()
+    br = mg.BatchRenderer(procs, 1, L, cap, depth=2)
+    src_pin = torch.empty(bank_host.shape, dtype=torch.float32, pin_memory=True).numpy()
+    src_pin[...] = bank_host
+    outs = [torch.empty((rd.buffer_rows - rd.output_begin, 1, 2, L), dtype=torch.float32, pin_memory=True).numpy()
+            for _, rd, _ in cases]
+    row_bytes = 4 * 2 * L
+    h2d = sum(rd.num_inputs * row_bytes + int(sum(v.size for v in p.values())) * 8 for _, rd, p in cases)
+    d2h = sum(o.nbytes for o in outs)
 
-    def max_over_ranks(sec):
-        t = torch.tensor([sec], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    def e2e_step():
+        for (_, rd, params), o in zip(cases, outs):
+            br.submit(rd, params, src_pin, o, validate=False)
+        br.sync()
 
-    def pipeline_rate(dtype):
-        pipe = mg.RenderPipeline(rd, procs, 1, L, dtype=dtype, depth=2)
-        ps = pipe.pinned(src.shape)
-        ps[...] = src
-        outs = [pipe.pinned((n_out, 1, 2, L)) for _ in range(2)]
-        for i in range(3):
-            pipe.submit(P, ps, outs[i % 2])
-        pipe.sync()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for i in range(n):
-            pipe.submit(P, ps, outs[i % 2])
-        pipe.sync()
-        dt = max_over_ranks(time.perf_counter() - t0)
-        return dt, int(ps.nbytes), int(outs[0].nbytes)
-
-    e2e = {}
-    e2e_s, h2d, d2h = pipeline_rate(np.float64)
-    e2e["e2e"] = {"value": node_samples * n * world / e2e_s, "unit": UNIT,
-                  "api": "RenderPipeline (mg_pipeline_submit), double host audio, pinned, fp32 conversion on host threads",
-                  "h2d_bytes_per_step": h2d + pbytes, "d2h_bytes_per_step": d2h,
-                  "graph_renders_per_sec": n * world / e2e_s, "n_gpus": world}
-    f32_s, h2d32, d2h32 = pipeline_rate(np.float32)
-    e2e["e2e_f32"] = {"value": node_samples * n * world / f32_s, "unit": UNIT,
-                      "api": "RenderPipeline, float host audio, pinned",
-                      "h2d_bytes_per_step": h2d32 + pbytes, "d2h_bytes_per_step": d2h32, "n_gpus": world}
-    pin_src = torch.empty(src.shape, dtype=torch.float64, pin_memory=True).numpy()
-    pin_src[...] = src
-    pin_out = torch.empty((n_out, 1, 2, L), dtype=torch.float64, pin_memory=True).numpy()
     for _ in range(2):
-        mg.render(rd, procs, P, pin_src, out=pin_out)
+        e2e_step()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(n):
-        mg.render(rd, procs, P, pin_src, out=pin_out)
-    blk_s = max_over_ranks(time.perf_counter() - t0)
-    e2e["e2e_blocking"] = {"value": node_samples * n * world / blk_s, "unit": UNIT,
-                           "api": "mg_render (blocking, double host audio, pinned)", "n_gpus": world}
+        e2e_step()
+    e2e_s = max_over_ranks(time.perf_counter() - t0, dev, world)
+    del br
+    torch.cuda.empty_cache()
 
     extras = {}
-    for key, fn in (("config5", config5_rate), ("config5_train", config5_train_rate)):
+    if not args.no_extras:
         try:
-            extras[key] = fn(mg, procs, dev, rank, world)
+            extras["config5_train"] = config5_train_rate(mg, procs, dev, rank, world)
         except Exception as ex:  # report, never lose the headline line
-            extras[key] = {"error": repr(ex)[:300]}
+            extras["config5_train"] = {"error": repr(ex)[:300]}
+        if world == 1:
+            for key, fn in (("config2", config2_lines), ("config3", config3_rate), ("config4", config4_rate)):
+                try:
+                    extras[key] = fn(mg, procs, dev)
+                except Exception as ex:
+                    extras[key] = {"error": repr(ex)[:300]}
 
-    result = None
+    alg_bytes = sum(8.0 * L * (len(st.gather) + st.store_end - st.store_begin) for _, rd, _ in cases for st in rd.steps)
     if rank == 0:
-        ms_per_step = dev_ms_max / n
-        value = node_samples * world * n / (dev_ms_max / 1e3)
-        renders_ps = world * n / (dev_ms_max / 1e3)
-        peak, peak_kind = peaks()
-        sb = step_bytes(rd, 1, L)
-        by_type = {}
-        for s, ms, b in zip(rd.steps, steps_ms, sb):
-            d = by_type.setdefault(mg.type_name(s.type), {"ms": 0.0, "bytes": 0, "steps": 0})
-            d["ms"] += float(ms)
-            d["bytes"] += int(b)
-            d["steps"] += 1
-        for d in by_type.values():
-            d["achieved_gbs"] = d["bytes"] / (d["ms"] * 1e-3) / 1e9 if d["ms"] > 0 else None
-            d["hbm_frac"] = d["achieved_gbs"] / peak if d["achieved_gbs"] else None
-            d["share"] = d["ms"] / float(np.sum(steps_ms))
-        # FFT-stage flops of the implemented algorithm (complex FFTs of the L/R-packed signal):
-        # EQ: 2 x 8192-point per 6144-sample block; reverb/delay: 3 x N-point (kernel, signal,
-        # inverse) per node, N = 2^ceil(log2(L + taps - 1)); 5 N log2 N flops per FFT.
-        def fft_flops(s):
-            slots = s.store_end - s.store_begin
-            if s.type == mg.NodeType.EQ:
-                blocks = -(-L // 6144)
-                return slots * blocks * 2 * 5 * 8192 * 13
-            if s.type in (mg.NodeType.REVERB, mg.NodeType.DELAY):
-                taps = procs.reverb_length if s.type == mg.NodeType.REVERB else procs.delay_span
-                a = max(13, int(np.ceil(np.log2(L + taps - 1))))
-                return slots * 3 * 5 * (1 << a) * a
-            return 0
-        fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12  # nominal FP32 TFLOP/s at max SM clock
-        for s, ms in zip(rd.steps, steps_ms):
-            d = by_type[mg.type_name(s.type)]
-            d["fft_flops"] = d.get("fft_flops", 0) + fft_flops(s)
-        for d in by_type.values():
-            if d.get("fft_flops"):
-                d["fp32_tflops"] = d["fft_flops"] / (d["ms"] * 1e-3) / 1e12
-                d["fp32_frac_nominal"] = d["fp32_tflops"] / fp32_peak
-        dom = max(by_type.items(), key=lambda kv: kv[1]["ms"])
-        # Roofline for the dominant step's kernels: algorithmic bytes / measured duration.
-        achieved = dom[1]["achieved_gbs"]
+        hbm_peak, peak_kind = peaks()
+        value = ns_all * n / (dev_ms_max * 1e-3)
+        # Dominant kernel family in the render (in-render CUPTI time) and its roofline.
+        dom = max(fam.items(), key=lambda kv: kv[1]["us"]) if fam else (None, {"us": 0, "launches": 0})
+        dom_name, dom_t = dom
+        achieved = flops.get(dom_name, 0.0) / (dom_t["us"] * 1e-6) / 1e12 if dom_t["us"] and flops.get(dom_name) else None
         traffic = None
         try:
-            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-                tr = json.load(f)["by_step_type"]
-            key = "mix/out" if dom[0] in ("mix", "out") else dom[0]
-            traffic = tr.get(key) / dom[1]["steps"] if tr.get(key) else None
+            with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
+                traffic = json.load(f).get(dom_name)
         except Exception:
             pass
-        # Aggregation / elementwise steps (north-star target: >= 60% of HBM roofline): the
-        # multi-slot pointwise steps, algorithmic bytes over their measured step time.
-        pw = [(s, ms) for s, ms in zip(rd.steps, steps_ms)
-              if s.type in (mg.NodeType.GAIN, mg.NodeType.IMAGER, mg.NodeType.MIX) and s.store_end - s.store_begin > 1]
-        pw_bytes = sum(4 * 2 * L * (len(s.gather) + s.store_end - s.store_begin) for s, _ in pw)
-        pw_ms = float(sum(ms for _, ms in pw))
         result = {
-            "metric": METRIC,
-            "value": value,
-            "unit": UNIT,
-            "graph_renders_per_sec": renders_ps,
-            "n_gpus": world,
-            "steps": n,
-            "warmup": max(args.warmup, 3),
-            "ms_per_step": ms_per_step,
-            "higher_is_better": True,
-            "scaling": "weak",
-            "vs_baseline": None,
-            "dtype": "f32",
-            "data": "synthetic (uniform_noise sources, random_legal_params; reference generators, bit-identical)",
-            "config": {"workload": WORKLOAD, "graphs_per_gpu": 1, "length": L, "batch": 1, "sample_rate": FS,
-                       "strategy": "greedy", "type_string": rd.schedule.type_codes(), "node_samples_per_render": node_samples,
-                       "l2": "flushed (512 MiB write) between timed iterations", "parallelism": f"graph-sharded x{world}",
-                       "execution": "CUDA graph replay; parameter-only prologues on a side stream"},
-            "roofline": {"bound": "hbm", "kernel": f"{dom[0]} step", "achieved": achieved, "peak": peak,
-                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak if achieved else None,
-                         "traffic": traffic, "share_of_step": dom[1]["share"]},
-            "roofline_elementwise": {"bound": "hbm", "steps": [mg.type_code(s.type) for s, _ in pw],
-                                     "achieved": pw_bytes / (pw_ms * 1e-3) / 1e9 if pw_ms else None, "peak": peak,
-                                     "unit": "GB/s",
-                                     "frac": pw_bytes / (pw_ms * 1e-3) / 1e9 / peak if pw_ms else None},
-            "roofline_fp32": {"bound": "fp32", "kernel": f"{dom[0]} step", "achieved": dom[1].get("fp32_tflops"),
-                              "peak": fp32_peak, "peak_kind": "nominal (148 SM x 128 FMA x 2 x 1965 MHz)",
-                              "unit": "TFLOP/s", "frac": dom[1].get("fp32_frac_nominal")},
-            "roofline_by_step_type": by_type,
-            "roofline_by_step_note": ("per step: prologue + audio pass repeated in one CUDA graph (mg_profile_steps), "
-                                      "inputs L2-warm as in a render (each step reads rows its producers just wrote), "
-                                      "so small steps can exceed the HBM figure"),
-            "steps_us": [[mg.type_code(s.type), s.store_end - s.store_begin, len(s.gather), round(float(ms) * 1e3, 2)]
-                         for s, ms in zip(rd.steps, steps_ms)],
-            "wall_s_timed_region": wall,
-            "clocks": clocks,
-            "gpu_launches": rd.kernel_count(1, L) * n,
+            "metric": METRIC, "value": value, "unit": UNIT,
+            "graph_renders_per_sec": len(graphs) * n / (dev_ms_max * 1e-3),
+            "n_gpus": world, "steps": n, "warmup": max(args.warmup, 3), "ms_per_step": dev_ms_max / n,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference generators: generate_console, random_legal_params, uniform_noise bank)",
+            "config": {"workload": WORKLOAD, "graphs": len(graphs), "graphs_on_rank0": len(mine), "unions_on_rank0": len(unions),
+                       "length": L, "batch": 1, "sample_rate": FS, "node_samples_per_step": ns_all,
+                       "l2": "inputs larger than L2 (each union's arena is ~8 GB), no flush",
+                       "parallelism": f"graph-sharded x{world} ({args.backend})",
+                       "execution": "per-union CUDA graph replay; parameter-only prologues on side streams"},
+            "e2e": {"value": ns_all * n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "BatchRenderer (mg_batch_submit): pinned fp32 host sources per input node, original-order "
+                           "parameter tables, device reorder, render, output D2H; wall clock, max over ranks",
+                    "ms_per_step": e2e_s / n * 1e3, "graph_renders_per_sec": len(graphs) * n / e2e_s},
+            "roofline": {"bound": "fp32", "kernel": dom_name, "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
+                         "peak_kind": "nominal FP32 CUDA-core (148 SM x 128 FMA x 2 x 1965 MHz); no measured FP32 peak",
+                         "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS if achieved else None,
+                         "traffic": traffic, "launches_per_step": dom_t["launches"],
+                         "us_per_step_in_render": dom_t["us"], "flops_per_step": flops.get(dom_name),
+                         "share_of_kernel_time": dom_t["us"] / sum(v["us"] for v in fam.values()) if fam else None,
+                         "note": "in-render kernel time from a CUPTI trace of one replayed step (concurrent kernels "
+                                 "overlap); flops of the implemented four-step transforms, 5 N log2 N per transform"},
+            "roofline_hbm": {"bound": "hbm", "achieved": alg_bytes / (dev_ms / n * 1e-3) / 1e9,
+                             "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s", "traffic": alg_bytes,
+                             "note": "whole render of rank 0's shard: algorithmic bytes (every gathered row read once, "
+                                     "every non-input row written once, 8 B per stereo sample) over the device step "
+                                     "time; SURVEY.md 8d"},
+            "in_render_us_per_step": {k: round(v["us"], 1) for k, v in sorted(fam.items(), key=lambda kv: -kv[1]["us"])},
+            "in_render_launches_per_step": {k: v["launches"] for k, v in fam.items()},
+            "traced_span_us": span_us,
+            "wall_s_timed_region": wall, "clocks": clocks, "gpu_launches": kernels_per_step * n,
         }
-
-        result.update(e2e)
-
-        if world == 1:
-            for key, fn in (("config3", config3_rate), ("config4", config4_rate)):
-                try:
-                    result[key] = fn(mg, procs, dev)
-                except Exception as ex:  # report, never lose the headline line
-                    result[key] = {"error": repr(ex)[:300]}
+        result["roofline_hbm"]["frac"] = result["roofline_hbm"]["achieved"] / hbm_peak
         result.update(extras)
         if world == 1 and not args.no_cpu_baseline:
-            cb = cpu_reference_sample(renders=2)
-            if cb is not None:
-                result["cpu_baseline"] = {"value": cb[0], "unit": UNIT, "cores": 1, "kind": "reference",
-                                          "sample": f"2 full config-2 renders (reference render(), oracle/_ref, "
-                                                    f"FFTW-API stand-in FFT) in {cb[1]:.1f} s on 1 host core"}
+            try:
+                from oracle import ref
+                if ref.available():
+                    cores = os.cpu_count() or 1
+                    nsr, w = reference_sample(cores, 1, 0)
+                    result["cpu_baseline"] = {
+                        "value": nsr / w, "unit": UNIT, "cores": cores, "kind": "reference",
+                        "sample": f"{cores} config-5 graphs, one per host process (reference render(), oracle/_ref, "
+                                  f"FFTW-API stand-in FFT), {w:.1f} s wall"}
+            except Exception as ex:
+                result["cpu_baseline"] = {"error": repr(ex)[:200]}
         print(json.dumps(result))
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-
-
-def _ref_worker(args):
-    steps, = args
-    from oracle import ref
-    t, e = ref.console(TRACKS, PRUNE, GSEED)
-    params = ref.random_legal_params(t, e, 2024)
-    src = np.stack([ref.uniform_noise(2 * L, 1000 + k).reshape(1, 2, L) for k in range(int(np.sum(t == 0)))])
-    plan = ref.Plan(t, e, 1)
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        plan.render(params, src, sample_rate=FS)
-        times.append(time.perf_counter() - t0)
-    return times
-
-
-def reference_arm(args):
-    rank, world, _ = dist_setup()
-    if rank != 0:
-        return
-    import multiprocessing as mp
-
-    from oracle import ref
-    if not ref.available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmixgraph_ref.so not built"}))
-        return
-    cores = os.cpu_count() or 1
-    t, e = ref.console(TRACKS, PRUNE, GSEED)
-    node_samples = (len(t) - int(np.sum(t == 0))) * L
-    # Bound the run: one render is ~3.5 s on one core; keep warmup + steps within ~3 minutes.
-    warm = max(1, min(args.warmup, 1))
-    steps = max(1, min(args.steps, 40))
-    ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
-        pool.map(_ref_worker, [(warm,)] * cores)
-        t0 = time.perf_counter()
-        per = pool.map(_ref_worker, [(steps,)] * cores)
-        wall = time.perf_counter() - t0
-    value = node_samples * steps * cores / wall
-    med = statistics.median([x for p in per for x in p])
-    sample = (f"{cores} processes x {steps} full config-2 renders each (reference render(), oracle/_ref, FFTW-API "
-              f"stand-in FFT), {wall:.1f} s wall; median single render {med:.2f} s")
-    out = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "graph_renders_per_sec": steps * cores / wall,
-        "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": wall / steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (uniform_noise sources, random_legal_params)",
-        "config": {"workload": WORKLOAD, "graphs_per_process": 1, "length": L, "batch": 1, "sample_rate": FS},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(out))
 
 
 def main():

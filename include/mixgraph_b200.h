@@ -153,6 +153,10 @@ void mg_set_conv_fuse(int32_t mode);
  * points per segment. Applies to plans whose device workspace is sized after the call. */
 void mg_set_conv_log(int32_t log_n);
 
+/* Transform geometry a long convolution of `length` samples with a `taps`-tap kernel uses:
+ * out = [log2 N, log2 N1 (columns), log2 N2 (rows), segments, output samples per segment]. */
+int32_t mg_conv_geometry(int64_t length, int64_t taps, int64_t* out);
+
 /* Arithmetic precision of the FFT-based steps (EQ, reverb, delay): 32 or 64 bits; the arena
  * stays fp32. Process-wide. */
 void mg_set_fft_precision(int32_t bits);

@@ -83,6 +83,7 @@ _sig("mg_backward_workspace_bytes", _i32, _vp, _vp, _i32, _i64, _P(_u64))
 _sig("mg_render_backward_arena", _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp)
 _sig("mg_set_conv_fuse", None, _i32)
 _sig("mg_set_conv_log", None, _i32)
+_sig("mg_conv_geometry", _i32, _i64, _i64, _vp)
 _sig("mg_set_fft_precision", None, _i32)
 _sig("mg_fft_precision", _i32)
 _sig("mg_batch_capacity", _i32, _vp, _vp, _i32, _i64, _vp)
@@ -610,6 +611,13 @@ def render(rd: RenderData, procs: ProcessorSet, params: Optional[Dict[int, np.nd
 def set_conv_fuse(mode: int) -> None:
     """mg_set_conv_fuse: -1 auto (default), 0 separate kernel-spectrum rows pass, 1 fused."""
     _lib.mg_set_conv_fuse(int(mode))
+
+
+def conv_geometry(length: int, taps: int) -> Dict[str, int]:
+    """mg_conv_geometry: the segmented overlap-save transform a long convolution uses."""
+    out = np.zeros(5, dtype=np.int64)
+    _check(_lib.mg_conv_geometry(int(length), int(taps), out.ctypes.data_as(_vp)))
+    return dict(zip(("log_n", "log_n1", "log_n2", "nseg", "seg"), (int(x) for x in out)))
 
 
 def set_fft_precision(bits: int) -> None:

@@ -23,6 +23,7 @@ void launch_sgd_step(bool dynamics, double* table, const double* grad, long n, d
 void set_conv_fuse(int mode);
 void set_conv_log(int log_n);
 void set_fft_fp64(bool on);
+void conv_geometry(long length, long taps, long* out);
 bool fft_fp64();
 }  // namespace mgb
 
@@ -472,6 +473,14 @@ int32_t mg_render_backward_arena(const mg_plan* p, const mg_processors* procs, c
 void mg_set_conv_fuse(int32_t mode) { mgb::set_conv_fuse(mode); }
 
 void mg_set_conv_log(int32_t log_n) { mgb::set_conv_log(log_n); }
+
+int32_t mg_conv_geometry(int64_t length, int64_t taps, int64_t* out) {
+  return guarded([&] {
+    long g[5];
+    mgb::conv_geometry(static_cast<long>(length), static_cast<long>(taps), g);
+    for (int i = 0; i < 5; ++i) out[i] = g[i];
+  });
+}
 
 void mg_set_fft_precision(int32_t bits) { mgb::set_fft_fp64(bits == 64); }
 int32_t mg_fft_precision(void) { return mgb::fft_fp64() ? 64 : 32; }

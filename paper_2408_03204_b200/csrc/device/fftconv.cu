@@ -1222,6 +1222,15 @@ ConvGeom conv_geom(long length, long taps) {
   return g;
 }
 
+void conv_geometry(long length, long taps, long* out) {
+  const ConvGeom g = conv_geom(length, taps);
+  out[0] = g.log_n;
+  out[1] = g.log_n1;
+  out[2] = g.log_n2;
+  out[3] = g.nseg;
+  out[4] = g.seg;
+}
+
 std::size_t conv_prologue_bytes(const ConvGeom& g, int slots, long taps) {
   return ir_bytes(slots, taps) + align256(spec_elem_bytes() * static_cast<std::size_t>(slots) * g.n);
 }

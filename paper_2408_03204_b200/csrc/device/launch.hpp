@@ -72,6 +72,8 @@ constexpr int kConvMaxLog = 22;
 ConvGeom conv_geom(long length, long taps);
 // Tests: force the transform size 2^log (0 = automatic); conv_geom throws when 2^log < taps.
 void set_conv_log(int log_n);
+// [log_n, log_n1, log_n2, nseg, seg] of conv_geom (C ABI mg_conv_geometry).
+void conv_geometry(long length, long taps, long* out);
 // Large steps (kernel spectra beyond L2) fuse the kernel's row stage into the signal's row
 // pass instead of a separate prologue pass.
 bool conv_fuse_kernel_rows(const ConvGeom& g, int slots);
