@@ -234,13 +234,18 @@ __device__ __forceinline__ void stockham_pass(C* buf, int fstride, const C* __re
   constexpr int PER = (TOTAL + NTHR - 1) / NTHR;
   const int tid = threadIdx.x;
   C v[PER][R];
-  TwBase<R, DIR, C> twb[PER];
+  // When the threads cover whole transforms (NTHR a multiple of M), a thread's butterfly index
+  // j is the same for every q (one butterfly per transform): its twiddles are loaded once, not
+  // PER times (the repeated table loads were most of the L1 traffic of the row kernels).
+  constexpr bool kSharedJ = NTHR % M == 0;
+  constexpr int NTW = kSharedJ ? 1 : PER;
+  TwBase<R, DIR, C> twb[NTW];
   if constexpr (NS > 1) {
     if (tw != nullptr) {
 #pragma unroll
-      for (int q = 0; q < PER; ++q) {
+      for (int q = 0; q < NTW; ++q) {
         const int b = tid + q * NTHR;
-        if (TOTAL % NTHR == 0 || b < TOTAL) {
+        if (kSharedJ || TOTAL % NTHR == 0 || b < TOTAL) {
           const int j = b % M;
           twb[q].load(tw, (j % NS) * (TWN / (NS * R)));
         }
@@ -274,7 +279,7 @@ __device__ __forceinline__ void stockham_pass(C* buf, int fstride, const C* __re
       const int jm = j % NS;
       if constexpr (NS > 1) {
         if (tw != nullptr) {
-          twb[q].apply(v[q]);
+          twb[kSharedJ ? 0 : q].apply(v[q]);
         } else {
           C w[R];
           pass_twiddles<R, DIR, C>(T(2) * static_cast<T>(jm) / static_cast<T>(NS * R), w);
