@@ -12,6 +12,8 @@
 
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 namespace mgb {
 
 // Scalar type of a complex element and its constructor.
@@ -174,6 +176,44 @@ __device__ __forceinline__ void pass_twiddles(RealOf<C> x, C* w) {
 // pass twiddles from it (L1-resident, 64 KiB) instead of evaluating sin/cos per butterfly.
 constexpr int kTwN = 8192;
 
+// Per-pass twiddle tables, stored in the same allocation just BEFORE the kTwN table (at
+// negative offsets from the pointer the kernels receive): for every pass size M = NS*R = 2^m
+// (m = 1..13) and radix R = 2^k (k = 1..4, R <= M) a block [R-1][NS] of exp(-2 pi i j r / M),
+// j < NS, r = 1..R-1. A pass's threads (consecutive butterflies j) read consecutive entries:
+// coalesced loads and no chained products, where the strided kTwN table made every warp load
+// touch 16-32 sectors (70% of a row kernel's L1 wavefronts).
+__host__ __device__ constexpr int tw_pass_off(int m, int k) {
+  int off = 0;
+  for (int mm = 1; mm <= 13; ++mm) {
+    for (int kk = 1; kk <= 4 && kk <= mm; ++kk) {
+      if (mm == m && kk == k) return off;
+      off += ((1 << kk) - 1) << (mm - kk);
+    }
+  }
+  return off;
+}
+constexpr int kTwPassTotal = tw_pass_off(14, 1);
+__host__ __device__ constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x / 2); }
+
+// The R-1 twiddles of butterfly j of a pass (NS, R) from its per-pass table.
+template <int R, int NS, int DIR, typename C>
+struct TwPass {
+  C w[R - 1];
+  __device__ __forceinline__ void load(const C* __restrict__ tw, int j) {
+    const C* tp = tw - kTwPassTotal + tw_pass_off(ilog2c(NS * R), ilog2c(R));
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      C v = tp[(r - 1) * NS + j];
+      if (DIR > 0) v.y = -v.y;
+      w[r - 1] = v;
+    }
+  }
+  __device__ __forceinline__ void apply(C* v) const {
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], w[r - 1]);
+  }
+};
+
 // Bank-conflict-free smem layout for pow2 transforms: one float2 of padding per 16 elements.
 // With the radix-16 first pass below, every Stockham pass then reads 16-aligned runs and
 // writes either runs of >= 16 (NS >= 16) or the stride-17 pattern of the first pass — both
@@ -239,7 +279,9 @@ __device__ __forceinline__ void stockham_pass(C* buf, int fstride, const C* __re
   // PER times (the repeated table loads were most of the L1 traffic of the row kernels).
   constexpr bool kSharedJ = NTHR % M == 0;
   constexpr int NTW = kSharedJ ? 1 : PER;
-  TwBase<R, DIR, C> twb[NTW];
+  // kTwN-table transforms read the per-pass tables; others (fft_384) the strided table.
+  using TW = std::conditional_t<TWN == kTwN, TwPass<R, NS, DIR, C>, TwBase<R, DIR, C>>;
+  TW twb[NTW];
   if constexpr (NS > 1) {
     if (tw != nullptr) {
 #pragma unroll
@@ -247,7 +289,8 @@ __device__ __forceinline__ void stockham_pass(C* buf, int fstride, const C* __re
         const int b = tid + q * NTHR;
         if (kSharedJ || TOTAL % NTHR == 0 || b < TOTAL) {
           const int j = b % M;
-          twb[q].load(tw, (j % NS) * (TWN / (NS * R)));
+          if constexpr (TWN == kTwN) twb[q].load(tw, j % NS);
+          else twb[q].load(tw, (j % NS) * (TWN / (NS * R)));
         }
       }
     }
@@ -397,8 +440,8 @@ template <int LOG2N, int DIR, typename C>
 __device__ __forceinline__ void fft_last_to_regs(const C* base, int j, const C* __restrict__ tw,
                                                  C (&v)[Pow2Plan<LOG2N>::kLastR]) {
   constexpr int NS = Pow2Plan<LOG2N>::kLastNs, R = Pow2Plan<LOG2N>::kLastR;
-  TwBase<R, DIR, C> twb;
-  twb.load(tw, j * (kTwN / (NS * R)));
+  TwPass<R, NS, DIR, C> twb;
+  twb.load(tw, j);
   const C* lb = base + sidx(j);  // inputs j + r*NS, NS a multiple of 16: immediate offsets
 #pragma unroll
   for (int r = 0; r < R; ++r) v[r] = lb[r * padded(NS)];

@@ -11,14 +11,39 @@
 
 namespace mgb {
 
+namespace {
+// fft_smem.cuh per-pass tables: block (m, k) = [R-1][NS] of exp(-2 pi i j r / 2^m), fp64-exact
+// values rounded to the element type.
+template <typename C>
+std::vector<C> pass_tables() {
+  std::vector<C> t(static_cast<std::size_t>(kTwPassTotal));
+  for (int m = 1; m <= 13; ++m) {
+    for (int k = 1; k <= 4 && k <= m; ++k) {
+      const int R = 1 << k, NS = 1 << (m - k), off = tw_pass_off(m, k);
+      for (int r = 1; r < R; ++r) {
+        for (int j = 0; j < NS; ++j) {
+          const double a = -2.0 * 3.14159265358979323846 * static_cast<double>(j) * r / static_cast<double>(1 << m);
+          C& v = t[static_cast<std::size_t>(off + (r - 1) * NS + j)];
+          v.x = static_cast<decltype(v.x)>(std::cos(a));
+          v.y = static_cast<decltype(v.y)>(std::sin(a));
+        }
+      }
+    }
+  }
+  return t;
+}
+}  // namespace
+
 const float2* twiddle_table(int device) {
   static std::mutex mu;
   static std::map<int, float2*> tables;
   std::scoped_lock lock(mu);
   auto it = tables.find(device);
   if (it != tables.end()) return it->second;
-  // One allocation (float2 units): [kTwN twiddles][kCosN doubles cos(2 pi m / 2047)]
-  // [384 twiddles exp(-2 pi i k / 384)][192 float2: inverse Hann covers for the reverb OLA].
+  // One allocation (float2 units): [per-pass tables (fft_smem.cuh tw_pass_off)][kTwN twiddles]
+  // [kCosN doubles cos(2 pi m / 2047)][384 twiddles exp(-2 pi i k / 384)][192 float2: inverse
+  // Hann covers for the reverb OLA]; the returned pointer is the kTwN table.
+  std::vector<float2> pass = pass_tables<float2>();
   std::vector<float2> host(kConstFloat2s);
   for (int k = 0; k < kTwN; ++k) {
     const double a = -2.0 * 3.14159265358979323846 * static_cast<double>(k) / kTwN;
@@ -41,6 +66,7 @@ const float2* twiddle_table(int device) {
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
+  host.insert(host.begin(), pass.begin(), pass.end());
   float2* d = nullptr;
   if (cudaMalloc(&d, sizeof(float2) * host.size()) != cudaSuccess ||
       cudaMemcpy(d, host.data(), sizeof(float2) * host.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
@@ -48,8 +74,8 @@ const float2* twiddle_table(int device) {
     throw std::runtime_error("twiddle table upload failed");
   }
   cudaSetDevice(prev);
-  tables.emplace(device, d);
-  return d;
+  tables.emplace(device, d + kTwPassTotal);
+  return d + kTwPassTotal;
 }
 
 const double2* twiddle_table64(int device) {
@@ -58,10 +84,10 @@ const double2* twiddle_table64(int device) {
   std::scoped_lock lock(mu);
   auto it = tables.find(device);
   if (it != tables.end()) return it->second;
-  std::vector<double2> host(kTwN);
+  std::vector<double2> host = pass_tables<double2>();
   for (int k = 0; k < kTwN; ++k) {
     const double a = -2.0 * 3.14159265358979323846 * static_cast<double>(k) / kTwN;
-    host[static_cast<std::size_t>(k)] = make_double2(std::cos(a), std::sin(a));
+    host.push_back(make_double2(std::cos(a), std::sin(a)));
   }
   int prev = 0;
   cudaGetDevice(&prev);
@@ -73,8 +99,8 @@ const double2* twiddle_table64(int device) {
     throw std::runtime_error("fp64 twiddle table upload failed");
   }
   cudaSetDevice(prev);
-  tables.emplace(device, d);
-  return d;
+  tables.emplace(device, d + kTwPassTotal);
+  return d + kTwPassTotal;
 }
 
 static bool g_fft_fp64 = false;
