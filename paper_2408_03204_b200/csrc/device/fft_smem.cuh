@@ -178,16 +178,17 @@ constexpr int kTwN = 8192;
 
 // Per-pass twiddle tables, stored in the same allocation just BEFORE the kTwN table (at
 // negative offsets from the pointer the kernels receive): for every pass size M = NS*R = 2^m
-// (m = 1..13) and radix R = 2^k (k = 1..4, R <= M) a block [R-1][NS] of exp(-2 pi i j r / M),
-// j < NS, r = 1..R-1. A pass's threads (consecutive butterflies j) read consecutive entries:
-// coalesced loads and no chained products, where the strided kTwN table made every warp load
-// touch 16-32 sectors (70% of a row kernel's L1 wavefronts).
+// (m = 1..13) and radix R = 2^k (k = 1..4, R <= M) a block [k][NS] of the power-of-two
+// twiddles exp(-2 pi i j 2^i / M), j < NS, i < k (w, w^2, w^4, w^8; the others are <= 3
+// products, TwBase::apply). A pass's threads (consecutive butterflies j) read consecutive
+// entries — coalesced — where the strided kTwN table made every warp load touch 16-32 sectors
+// (70% of a row kernel's L1 wavefronts), and a radix-8 butterfly loads 3 values, not 7.
 __host__ __device__ constexpr int tw_pass_off(int m, int k) {
   int off = 0;
   for (int mm = 1; mm <= 13; ++mm) {
     for (int kk = 1; kk <= 4 && kk <= mm; ++kk) {
       if (mm == m && kk == k) return off;
-      off += ((1 << kk) - 1) << (mm - kk);
+      off += kk << (mm - kk);
     }
   }
   return off;
@@ -195,24 +196,6 @@ __host__ __device__ constexpr int tw_pass_off(int m, int k) {
 constexpr int kTwPassTotal = tw_pass_off(14, 1);
 __host__ __device__ constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x / 2); }
 
-// The R-1 twiddles of butterfly j of a pass (NS, R) from its per-pass table.
-template <int R, int NS, int DIR, typename C>
-struct TwPass {
-  C w[R - 1];
-  __device__ __forceinline__ void load(const C* __restrict__ tw, int j) {
-    const C* tp = tw - kTwPassTotal + tw_pass_off(ilog2c(NS * R), ilog2c(R));
-#pragma unroll
-    for (int r = 1; r < R; ++r) {
-      C v = tp[(r - 1) * NS + j];
-      if (DIR > 0) v.y = -v.y;
-      w[r - 1] = v;
-    }
-  }
-  __device__ __forceinline__ void apply(C* v) const {
-#pragma unroll
-    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], w[r - 1]);
-  }
-};
 
 // Bank-conflict-free smem layout for pow2 transforms: one float2 of padding per 16 elements.
 // With the radix-16 first pass below, every Stockham pass then reads 16-aligned runs and
@@ -258,6 +241,23 @@ struct TwBase {
     }
 #pragma unroll
     for (int r = 1; r < R; ++r) v[r] = cmul(v[r], p[r]);
+  }
+};
+
+// The twiddles of butterfly j of a pass (NS, R) from its per-pass table (w, w^2, w^4, w^8 of
+// exp(-2 pi i j / (NS R)); TwBase::apply forms the rest).
+template <int R, int NS, int DIR, typename C>
+struct TwPass : TwBase<R, DIR, C> {
+  __device__ __forceinline__ void load(const C* __restrict__ tw, int j) {
+    const C* tp = tw - kTwPassTotal + tw_pass_off(ilog2c(NS * R), ilog2c(R));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if ((1 << i) < R) {
+        C v = tp[i * NS + j];
+        if (DIR > 0) v.y = -v.y;
+        this->w[i] = v;
+      }
+    }
   }
 };
 

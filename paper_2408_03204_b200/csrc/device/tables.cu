@@ -12,18 +12,18 @@
 namespace mgb {
 
 namespace {
-// fft_smem.cuh per-pass tables: block (m, k) = [R-1][NS] of exp(-2 pi i j r / 2^m), fp64-exact
+// fft_smem.cuh per-pass tables: block (m, k) = [k][NS] of exp(-2 pi i j 2^i / 2^m), fp64-exact
 // values rounded to the element type.
 template <typename C>
 std::vector<C> pass_tables() {
   std::vector<C> t(static_cast<std::size_t>(kTwPassTotal));
   for (int m = 1; m <= 13; ++m) {
     for (int k = 1; k <= 4 && k <= m; ++k) {
-      const int R = 1 << k, NS = 1 << (m - k), off = tw_pass_off(m, k);
-      for (int r = 1; r < R; ++r) {
+      const int NS = 1 << (m - k), off = tw_pass_off(m, k);
+      for (int i = 0; i < k; ++i) {
         for (int j = 0; j < NS; ++j) {
-          const double a = -2.0 * 3.14159265358979323846 * static_cast<double>(j) * r / static_cast<double>(1 << m);
-          C& v = t[static_cast<std::size_t>(off + (r - 1) * NS + j)];
+          const double a = -2.0 * 3.14159265358979323846 * static_cast<double>(j) * (1 << i) / static_cast<double>(1 << m);
+          C& v = t[static_cast<std::size_t>(off + i * NS + j)];
           v.x = static_cast<decltype(v.x)>(std::cos(a));
           v.y = static_cast<decltype(v.y)>(std::sin(a));
         }
