@@ -46,16 +46,28 @@ struct DynBwd {
   int tiles;
 };
 
+// a^n for an integer n >= 0 by squaring (<= 2 log2 n dependent fp64 multiplies; relative error
+// ~n * 1e-16, the reference builds the same powers by repeated products). The fp64 pow() it
+// replaces held every warp of a scan tile at the barrier behind warp 0 (28 % of the gate
+// scan's stall samples).
+__device__ __forceinline__ double ipow(double a, long n) {
+  double r = 1.0;
+  while (n > 0) {
+    if (n & 1) r *= a;
+    a *= a;
+    n >>= 1;
+  }
+  return r;
+}
+
 // Slot constants, derived by warp 0 of each CTA: lanes 0-3 evaluate the four fp64 powers
-// a^Ne, a^8, a^tile, a^(32 tile) side by side (one pow latency), lane 0 assembles.
+// a^Ne, a^8, a^tile, a^(32 tile) side by side, lane 0 assembles.
 __device__ __forceinline__ void derive_params(const double* row, int env_taps, double floor_, long L, int lane,
                                               DynParams* out, long tile = kDynTile, bool gate = false) {
   const double a = row[0];
   const int Ne = static_cast<int>(env_taps < L ? env_taps : L);
-  const double e = lane == 0 ? static_cast<double>(Ne)
-                 : lane == 1 ? static_cast<double>(kDynPerThread)
-                 : lane == 2 ? static_cast<double>(tile) : 32.0 * static_cast<double>(tile);
-  const double pw = lane < 4 ? pow(a, e) : 0.0;
+  const long e = lane == 0 ? static_cast<long>(Ne) : lane == 1 ? kDynPerThread : lane == 2 ? tile : 32L * tile;
+  const double pw = lane < 4 ? ipow(a, e) : 0.0;
   const double aN = __shfl_sync(0xffffffffu, pw, 0), a16 = __shfl_sync(0xffffffffu, pw, 1);
   const double atile = __shfl_sync(0xffffffffu, pw, 2), atile32 = __shfl_sync(0xffffffffu, pw, 3);
   if (lane != 0) return;
@@ -350,7 +362,7 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
     }
     double part = 0.0;
     // weight A^d = A^lane * (A^32)^(d0/32): one pow per lane, then exact-order products
-    const double wl = tile > 0 ? pow(p.datile, static_cast<double>(lane)) : 0.0;
+    const double wl = tile > 0 ? ipow(p.datile, lane) : 0.0;
     double w32 = 1.0;  // (A^32)^(d0/32)
     for (int d0 = 0; d0 < tile; d0 += 32, w32 *= p.datile32) {
       if (w32 == 0.0) break;
@@ -768,6 +780,8 @@ void launch_dynamics_backward(bool gate, const StepArgs& fw, const StepArgs& bw,
 }
 
 constexpr int kDynSmallThreads = 128;
+// Forward tiles of 256 threads (2048 samples) for steps with many waves of tiles.
+constexpr int kDynFwdThreads = 256;
 constexpr int kDynSmallTile = kDynSmallThreads * kDynPerThread;
 
 std::size_t dyn_sync_bytes(int slots, int batch, long length) {
@@ -782,8 +796,13 @@ void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double ene
   // Few sequences (a bus compressor): 1024-sample tiles of 128 threads, so the step still
   // spreads over the SMs; otherwise 4096-sample tiles of 512 threads. (One-warp tiles measured
   // no faster on config 2 and their longer fp32 carry sums lose accuracy.)
-  const bool small = seqs * ((a.length + kDynTile - 1) / kDynTile) < 148;
-  const long tile = small ? static_cast<long>(kDynSmallThreads) * kDynPerThread : kDynTile;
+  const long big_tiles = seqs * ((a.length + kDynTile - 1) / kDynTile);
+  const bool small = big_tiles < 148;
+  // Many waves of tiles (config-5 unions): 256-thread tiles, so four CTAs per SM interleave
+  // their load / scan / carry-wait phases (98.7 vs 101.5 ms per 512-graph step). A few waves
+  // (config 2's 16 tracks): 512-thread tiles (256 measured 0.211 -> 0.216 ms per render).
+  const bool narrow = big_tiles >= 8L * 2 * 148;
+  const long tile = static_cast<long>(small ? kDynSmallThreads : (narrow ? kDynFwdThreads : kDynThreads)) * kDynPerThread;
   const int tiles = static_cast<int>((a.length + tile - 1) / tile);
   const long total = seqs * tiles;
   if (zero_sync) cudaMemsetAsync(ws, 0, dyn_sync_bytes(a.slots, a.batch, a.length), s);
@@ -798,6 +817,12 @@ void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double ene
       if (vec) MGB_DYN_LAUNCH(true, true, kDynSmallThreads); else MGB_DYN_LAUNCH(true, false, kDynSmallThreads);
     } else {
       if (vec) MGB_DYN_LAUNCH(false, true, kDynSmallThreads); else MGB_DYN_LAUNCH(false, false, kDynSmallThreads);
+    }
+  } else if (narrow) {
+    if (gate) {
+      if (vec) MGB_DYN_LAUNCH(true, true, kDynFwdThreads); else MGB_DYN_LAUNCH(true, false, kDynFwdThreads);
+    } else {
+      if (vec) MGB_DYN_LAUNCH(false, true, kDynFwdThreads); else MGB_DYN_LAUNCH(false, false, kDynFwdThreads);
     }
   } else {
     if (gate) {
