@@ -94,10 +94,12 @@ struct DeviceConstants {
   int device = 0;
   float2* stft_mid = nullptr;
   float2* stft_side = nullptr;
+  float4* stft_ms = nullptr;
   int frames = 0;
   ~DeviceConstants() {
     if (stft_mid) cudaFree(stft_mid);
     if (stft_side) cudaFree(stft_side);
+    if (stft_ms) cudaFree(stft_ms);
   }
 };
 
@@ -165,6 +167,7 @@ ProcessorSet::ProcessorSet(const ProcessorConfig& config) : config_(config) {
   const std::size_t stft_bytes = sizeof(float2) * static_cast<std::size_t>(dev_->frames) * (kReverbStftLength / 2 + 1);
   cuda_check(cudaMalloc(&dev_->stft_mid, stft_bytes > 0 ? stft_bytes : 8), "cudaMalloc");
   cuda_check(cudaMalloc(&dev_->stft_side, stft_bytes > 0 ? stft_bytes : 8), "cudaMalloc");
+  cuda_check(cudaMalloc(&dev_->stft_ms, stft_bytes > 0 ? 2 * stft_bytes : 16), "cudaMalloc");
   if (dev_->frames > 0) {
     Engine& e = engine_for(dev_->device);
     auto* d_noise = static_cast<double*>(e.aux.ensure(sizeof(double) * 2 * static_cast<std::size_t>(reverb_length_)));
@@ -172,6 +175,8 @@ ProcessorSet::ProcessorSet(const ProcessorConfig& config) : config_(config) {
     cuda_check(cudaMemcpyAsync(d_noise + reverb_length_, noise_side_.data(), sizeof(double) * reverb_length_, cudaMemcpyHostToDevice, e.stream), "H2D");
     mgb::launch_noise_stft(d_noise, reverb_length_, dev_->frames, dev_->stft_mid, e.stream);
     mgb::launch_noise_stft(d_noise + reverb_length_, reverb_length_, dev_->frames, dev_->stft_side, e.stream);
+    mgb::launch_pack_mid_side(dev_->stft_mid, dev_->stft_side, static_cast<long>(dev_->frames) * (kReverbStftLength / 2 + 1),
+                              dev_->stft_ms, e.stream);
     cuda_check(cudaStreamSynchronize(e.stream), "noise stft");
   }
 }
@@ -183,7 +188,7 @@ int ProcessorSet::device_id() const { return dev_->device; }
 namespace {
 
 mgb::ReverbConst reverb_const(const ProcessorSet& p) {
-  return {p.device().stft_mid, p.device().stft_side, p.device().frames, p.reverb_length(),
+  return {p.device().stft_mid, p.device().stft_side, p.device().stft_ms, p.device().frames, p.reverb_length(),
           mgb::twiddle_table(p.device().device)};
 }
 mgb::DelayConst delay_const(const ProcessorSet& p) { return {p.delay_span(), p.delay_window()}; }

@@ -449,14 +449,15 @@ __device__ __forceinline__ void fft_last_to_regs(const C* base, int j, const C* 
   Dft<R, DIR, C>::run(v);
 }
 
-// 384 = 3 * 8 * 4 * 4 (reverb STFT frames); tw384[k] = exp(-2*pi*i*k/384), usually in smem.
-// Element i of transform f lives at buf[f*fstride + sidx(i)] (padded layout).
+// 384 = 16 * 8 * 3 (reverb STFT frames); tw384[k] = exp(-2*pi*i*k/384), usually in smem.
+// Element i of transform f lives at buf[f*fstride + sidx(i)] (padded layout). Three passes with
+// NS = 1, 16, 128 — every store run 16-aligned (the 3*8*4*4 plan's NS = 3 and 24 passes were
+// bank-conflicted, as were its NS = 24 twiddle reads).
 template <int COUNT, int NTHR, int DIR, typename C>
 __device__ __forceinline__ void fft_384(C* buf, int fstride, const C* tw384) {
-  stockham_pass<384, 3, 1, COUNT, NTHR, DIR, 384>(buf, fstride, tw384);
-  stockham_pass<384, 8, 3, COUNT, NTHR, DIR, 384>(buf, fstride, tw384);
-  stockham_pass<384, 4, 24, COUNT, NTHR, DIR, 384>(buf, fstride, tw384);
-  stockham_pass<384, 4, 96, COUNT, NTHR, DIR, 384>(buf, fstride, tw384);
+  stockham_pass<384, 16, 1, COUNT, NTHR, DIR, 384>(buf, fstride, tw384);
+  stockham_pass<384, 8, 16, COUNT, NTHR, DIR, 384>(buf, fstride, tw384);
+  stockham_pass<384, 3, 128, COUNT, NTHR, DIR, 384>(buf, fstride, tw384);
 }
 
 }  // namespace mgb

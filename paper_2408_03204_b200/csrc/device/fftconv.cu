@@ -705,17 +705,24 @@ void kernel_spectrum(ColSrc src, const StepArgs& a, const ConvGeom& g, const flo
 // ---- reverb impulse response (masked noise STFT -> ISTFT) ----------------------------------
 constexpr int kRevBins = 193;      // kReverbStftLength / 2 + 1
 constexpr int kRevParamBins = 192;
-constexpr int kRevFpc = 16;        // output hops per CTA (frames computed: kRevFpc + 1)
-constexpr int kRevThreads = 512;
+constexpr int kRevFpc = 16;        // adjoint: hops per CTA
+constexpr int kRevThreads = 512;   // adjoint: threads per CTA
 constexpr int kRevFS = padded(384);  // frame stride in smem (padded layout)
+// Forward: 10 hops (11 frames) per CTA of 256 threads — 36 KB of frames, four CTAs per SM, so
+// config 2's 12 reverbs (46 x 12 = 552 CTAs) fit one wave of 592 slots (16 hops x 512 threads
+// made 348 CTAs for 296 slots: 1.18 waves).
+constexpr int kRevFwdFpc = 10;
+constexpr int kRevFwdThreads = 256;
 
-// grid (ceil(frames / kRevFpc), slots). Each CTA inverse-transforms frames m0-1 .. m0+15
-// (mid and side packed as one complex transform each) and overlap-adds hops m0 .. m0+15.
+// grid (ceil(frames / kRevFwdFpc), slots). Each CTA inverse-transforms frames m0-1 .. m0+9
+// (mid and side packed as one complex transform each) and overlap-adds hops m0 .. m0+9.
 // The per-bin mask exp(H0 + m Hdecay) is geometric in the frame index m: one exact expf
 // anchor per bin for the CTA's first frame and the ratio exp(Hdecay), both with fp64
-// exponents (processors.cpp:171-175), then <= 16 products.
-__global__ void __launch_bounds__(kRevThreads, 2) reverb_ir(const double* params, ReverbConst rc, float2* ir,
-                                                         long ir_stride) {
+// exponents (processors.cpp:171-175), then <= 10 products. The noise STFT is read as one
+// 16-byte (mid, side) value per (frame, bin).
+__global__ void __launch_bounds__(kRevFwdThreads, 4) reverb_ir(const double* params, ReverbConst rc, float2* ir,
+                                                            long ir_stride) {
+  constexpr int kRevThreads = kRevFwdThreads, kRevFpc = kRevFwdFpc;
   extern __shared__ float2 fr[];  // [(kRevFpc + 1)][kRevFS]
   __shared__ float base[2][kRevBins], ratio[2][kRevBins];
   __shared__ float2 tw384[384];
@@ -742,12 +749,14 @@ __global__ void __launch_bounds__(kRevThreads, 2) reverb_ir(const double* params
     const int kk = upper ? 384 - k : k;
     float gm = base[0][kk], gs = base[1][kk];
     const float rm = ratio[0][kk], rs = ratio[1][kk];
+#pragma unroll 4
     for (int f = 0; f <= kRevFpc; ++f) {
       const int m = m_first + f;
       float2 z = make_float2(0.f, 0.f);
       if (m >= 0 && m < rc.frames) {
-        float2 M = cscale(__ldg(rc.stft_mid + static_cast<long>(m) * kRevBins + kk), gm);
-        float2 S = cscale(__ldg(rc.stft_side + static_cast<long>(m) * kRevBins + kk), gs);
+        const float4 q = __ldg(rc.stft_ms + static_cast<long>(m) * kRevBins + kk);
+        float2 M = make_float2(q.x * gm, q.y * gm);
+        float2 S = make_float2(q.z * gs, q.w * gs);
         if (upper) {
           M = cconj(M);
           S = cconj(S);
@@ -1148,6 +1157,14 @@ __global__ void __launch_bounds__(256) noise_stft(const double* noise, long leng
   }
 }
 
+// (mid, side) noise STFT interleaved for reverb_ir's one-load-per-(frame, bin) fill.
+__global__ void pack_mid_side(const float2* mid, const float2* side, long n, float4* out) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n; i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const float2 a = mid[i], b = side[i];
+    out[i] = make_float4(a.x, a.y, b.x, b.y);
+  }
+}
+
 __global__ void f64_to_f32(const double* in, float* out, long n) {
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n; i += static_cast<long>(gridDim.x) * blockDim.x) {
     out[i] = static_cast<float>(in[i]);
@@ -1243,14 +1260,15 @@ std::size_t conv_main_bytes(const ConvGeom& g, int slots, int batch) {
 void launch_reverb_ir(const double* params, int slots, const ReverbConst& rc, float2* ir, long ir_stride,
                       cudaStream_t s) {
   if (slots == 0) return;
-  const dim3 grid(static_cast<unsigned>((rc.frames + kRevFpc - 1) / kRevFpc), static_cast<unsigned>(slots));
+  const dim3 grid(static_cast<unsigned>((rc.frames + kRevFwdFpc - 1) / kRevFwdFpc), static_cast<unsigned>(slots));
   note_prologue_kernel(reinterpret_cast<const void*>(reverb_ir));
+  constexpr int smem = (kRevFwdFpc + 1) * kRevFS * 8;
   static const bool done = [] {
-    cudaFuncSetAttribute(reverb_ir, cudaFuncAttributeMaxDynamicSharedMemorySize, (kRevFpc + 1) * kRevFS * 8);
+    cudaFuncSetAttribute(reverb_ir, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return true;
   }();
   (void)done;
-  reverb_ir<<<grid, kRevThreads, (kRevFpc + 1) * kRevFS * 8, s>>>(params, rc, ir, ir_stride);
+  reverb_ir<<<grid, kRevFwdThreads, smem, s>>>(params, rc, ir, ir_stride);
 }
 
 void launch_delay_ir(const double* params, int slots, const DelayConst& dc, float2* ir, long ir_stride,
@@ -1418,6 +1436,10 @@ void launch_conv_backward(bool reverb, const StepArgs& fw, const StepArgs& bw, c
 
 void launch_noise_stft(const double* noise, long length, int frames, float2* out, cudaStream_t s) {
   noise_stft<<<frames, 256, 0, s>>>(noise, length, out);
+}
+
+void launch_pack_mid_side(const float2* mid, const float2* side, long n, float4* out, cudaStream_t s) {
+  if (n > 0) pack_mid_side<<<grid_for(n), 256, 0, s>>>(mid, side, n, out);
 }
 
 void launch_f64_to_f32(const double* in, float* out, long n, cudaStream_t s) {

@@ -82,6 +82,7 @@ void set_conv_fuse(int mode);  // -1 auto (default), 0 never, 1 always
 struct ReverbConst {
   const float2* stft_mid;  // [frames][193]
   const float2* stft_side;
+  const float4* stft_ms;   // [frames][193] (mid, side) interleaved
   int frames;
   long length;  // reverb_length
   const float2* consts;  // twiddle_table(): 384-point twiddles and OLA covers
@@ -135,6 +136,7 @@ void launch_delay_ir(const double* params, int slots, const DelayConst& dc, floa
 
 // Noise STFT for the reverb (ProcessorSet construction, `processors.cpp:151-160`).
 void launch_noise_stft(const double* noise, long length, int frames, float2* out, cudaStream_t s);
+void launch_pack_mid_side(const float2* mid, const float2* side, long n, float4* out, cudaStream_t s);
 
 // Per-device constant tables, built on first use with a synchronous upload (call it before
 // any stream capture; ProcessorSet does): kTwN forward twiddles (float2), followed by
