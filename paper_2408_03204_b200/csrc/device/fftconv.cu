@@ -59,23 +59,6 @@ constexpr int kFir = 39;
 constexpr int kFirHalf = 19;
 constexpr int kTapRec = 40;
 
-// Dense multitap kernel value at sample i of channel c (processors.cpp:210-227): the FIR
-// taps of the windows whose clamped position lies within +-19 of i, summed in tap order.
-// Positions are clamped into [m w, (m+1) w) with w > 2*19, so only windows i/w - 1 .. i/w + 1
-// can reach i.
-__device__ __forceinline__ float delay_tap_sum(const float* rec, int c, long i, int window) {
-  const int m = static_cast<int>(i / window);
-  const int m0 = m > 0 ? m - 1 : 0, m1 = m < 19 ? m + 1 : 19;
-  float acc = 0.f;
-  for (int mm = m0; mm <= m1; ++mm) {
-    const float* r = rec + (c * 20 + mm) * kTapRec;
-    const int d = __float_as_int(r[0]);
-    const long j = i - d + kFirHalf;
-    if (d >= 0 && j >= 0 && j < kFir) acc += r[1 + j];
-  }
-  return acc;
-}
-
 // Column-pass input: the packed kernel from an IR buffer, the arena signal (gathered), or
 // the multitap delay kernel synthesised from its tap records (no dense IR in memory).
 enum class ColSrc { Kernel, Signal, DelayTaps };
@@ -101,6 +84,10 @@ constexpr int kMaxGridY = 65535;
 
 // ---- pass 1: column FFTs (forward) ------------------------------------------------------
 // grid (N2 / C, items); item = slot (kernel) or slot*B + b (signal).
+// Thread t owns column c = t % C and first-pass butterfly jt = t / C: elements n1 = jt + q*N1/16
+// (q < 16) of its column, i.e. n = n0 + q*N/16. Index math is 32-bit within an item (N <= 2^22)
+// on per-item base pointers: the 64-bit per-element arithmetic was a third of the instructions
+// of these issue-bound kernels.
 template <int LN1, ColSrc SRC, typename CT>
 __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_fwd(StepArgs a, const float2* ir, long taps, int log_n,
                                                         CT* out, int window, SegArgs sg) {
@@ -108,13 +95,17 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_fwd(StepArgs a, 
   constexpr int N1 = 1 << LN1;
   constexpr int C = ColCfg<CT>::kElems / N1;
   constexpr int FS = padded(N1) + 1;
+  constexpr int NT = ColCfg<CT>::kThreads;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CT* tile = reinterpret_cast<CT*>(smem_raw);
   const int log_n2 = log_n - LN1;
-  const long N2 = 1L << log_n2;
-  const long N = 1L << log_n;
+  const int N2 = 1 << log_n2;
+  const int N = 1 << log_n;
   const int item = sg.item0 + blockIdx.y;
-  const long col0 = static_cast<long>(blockIdx.x) * C;
+  const int col0 = blockIdx.x * C;
+  const int c = threadIdx.x % C, jt = threadIdx.x / C;
+  const int nstep = N >> 4;
+  const int n0 = jt * N2 + col0 + c;
   int slot = item, b = 0, e0 = 0, e1 = 0;
   long base = 0, lo = 0, hi = taps;  // sample m = base + n is loaded when lo <= m < hi
   if constexpr (SRC == ColSrc::Signal) {
@@ -128,51 +119,82 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_fwd(StepArgs a, 
     lo = sg.mask_out ? first : base;
     hi = min(first + sg.seg, a.length);
   }
-  __shared__ float rec[SRC == ColSrc::DelayTaps ? kTaps * kTapRec : 1];
-  if constexpr (SRC == ColSrc::DelayTaps) {
-    const float* in = reinterpret_cast<const float*>(ir) + static_cast<long>(item) * kTaps * kTapRec;
-    for (int q = threadIdx.x; q < kTaps * kTapRec; q += ColCfg<CT>::kThreads) rec[q] = __ldg(in + q);
-    __syncthreads();
-  }
-  // Stage all of this thread's loads in registers before any smem store (max loads in flight).
-  constexpr int EPT = ColCfg<CT>::kElems / ColCfg<CT>::kThreads;
+  // Valid n of this item: [nlo, nhi).
+  const int nlo = static_cast<int>(min(max(lo - base, 0L), static_cast<long>(N)));
+  const int nhi = static_cast<int>(min(max(hi - base, 0L), static_cast<long>(N)));
+  constexpr int EPT = ColCfg<CT>::kElems / NT;
+  static_assert(EPT == 16, "cols_fwd: one radix-16 first-pass butterfly per thread");
   CT vals[EPT];
-  const float* one = nullptr;  // in-degree-1 fast path
-  if constexpr (SRC == ColSrc::Signal) {
-    if (e1 - e0 == 1) one = a.src + edge_row(a, e0) * a.rowstride + static_cast<long>(b) * 2 * a.length;
-  }
+  if constexpr (SRC == ColSrc::DelayTaps) {
+    // The dense multitap kernel (processors.cpp:210-227) has <= 40 x 39 nonzeros: zero the
+    // tile, scatter the tap FIRs into it, read the butterfly inputs back. Windows of one parity
+    // never overlap (w > 2*19), so the even taps then the odd taps add without races; an
+    // element reached by two taps gets 0 + f_a + f_b in either order — the same float as the
+    // dense synthesis's tap-order sum.
+    __shared__ float rec[kTaps * kTapRec];
+    const float* in = reinterpret_cast<const float*>(ir) + static_cast<long>(item) * kTaps * kTapRec;
+    for (int q = threadIdx.x; q < kTaps * kTapRec; q += NT) rec[q] = __ldg(in + q);
+    T* zt = reinterpret_cast<T*>(tile);
+    for (int q = threadIdx.x; q < 2 * C * FS; q += NT) zt[q] = T(0);
+    __syncthreads();
+    constexpr int kPhase = 20 * kFir;  // (channel, tap of one parity, FIR index)
+    for (int ph = 0; ph < 2; ++ph) {
+      for (int q = threadIdx.x; q < kPhase; q += NT) {
+        const int ch = q / (10 * kFir), rem = q - ch * (10 * kFir);
+        const int m = 2 * (rem / kFir) + ph, jj = rem % kFir;
+        const float* r = rec + (ch * 20 + m) * kTapRec;
+        const int d = __float_as_int(r[0]);
+        const int i = d - kFirHalf + jj;
+        if (d < 0 || i < nlo || i >= nhi) continue;
+        const int cc = (i & (N2 - 1)) - col0;
+        if (cc < 0 || cc >= C) continue;
+        T* e = zt + 2 * (cc * FS + sidx(i >> log_n2)) + ch;
+        *e = *e + static_cast<T>(r[1 + jj]);
+      }
+      __syncthreads();
+    }
 #pragma unroll
-  for (int q = 0; q < EPT; ++q) {
-    const int idx = threadIdx.x + q * ColCfg<CT>::kThreads;
-    const int c = idx % C, n1 = idx / C;
-    const long n = static_cast<long>(n1) * N2 + col0 + c;
-    const long m = base + n;
-    CT v = Cx<CT>::mk(0.f, 0.f);
-    if (m >= lo && m < hi) {
-      if constexpr (SRC == ColSrc::Signal) {
-        v = one ? Cx<CT>::mk(__ldg(one + m), __ldg(one + a.length + m)) : widen<CT>(gather2(a, e0, e1, b, m));
-      } else if constexpr (SRC == ColSrc::DelayTaps) {
-        v = Cx<CT>::mk(delay_tap_sum(rec, 0, n, window), delay_tap_sum(rec, 1, n, window));
-      } else {
-        v = widen<CT>(__ldg(ir + static_cast<long>(item) * taps + n));
+    for (int q = 0; q < EPT; ++q) vals[q] = tile[c * FS + sidx(jt + q * (N1 / 16))];
+    __syncthreads();
+  } else {
+    // All of this thread's loads are in flight before any smem store.
+    const float* one = nullptr;  // in-degree-1 fast path
+    if constexpr (SRC == ColSrc::Signal) {
+      if (e1 - e0 == 1) one = a.src + edge_row(a, e0) * a.rowstride + static_cast<long>(b) * 2 * a.length + base;
+    }
+    const float2* irp = ir + static_cast<long>(item) * taps;
+    if (SRC != ColSrc::Signal || one) {
+#pragma unroll
+      for (int q = 0; q < EPT; ++q) {
+        const int n = n0 + q * nstep;
+        CT v = Cx<CT>::mk(0.f, 0.f);
+        if (n >= nlo && n < nhi) {
+          if constexpr (SRC == ColSrc::Signal) v = Cx<CT>::mk(__ldg(one + n), __ldg(one + a.length + n));
+          else v = widen<CT>(__ldg(irp + n));
+        }
+        vals[q] = v;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < EPT; ++q) {
+        const int n = n0 + q * nstep;
+        vals[q] = (n >= nlo && n < nhi) ? widen<CT>(gather2(a, e0, e1, b, base + n)) : Cx<CT>::mk(0.f, 0.f);
       }
     }
-    vals[q] = v;
   }
-  // vals[q] = element j + q*N1/16 of column c (j = threadIdx.x / C): exactly the inputs of
-  // radix-16 first-pass butterfly j, so the first pass runs from registers.
-  const int c = threadIdx.x % C, jt = threadIdx.x / C;
+  // vals[q] = element jt + q*N1/16 of column c: exactly the inputs of radix-16 first-pass
+  // butterfly jt, so the first pass runs from registers.
   fft_first_from_regs<-1>(vals, tile + c * FS, jt);
   __syncthreads();
-  fft_middle<LN1, C, ColCfg<CT>::kThreads, -1>(tile, FS, twiddles<CT>(a));
+  fft_middle<LN1, C, NT, -1>(tile, FS, twiddles<CT>(a));
   // Last pass into registers, four-step twiddle exp(-2 pi i n2 k1 / N), store. Outputs of
   // butterfly j are k1 = j + r*NS: geometric in r, exact anchors (sincospif; n2 k1 < N <=
   // 2^24 is exact in fp32) every 4 outputs, <= 3 chained products in between.
   using Plan = Pow2Plan<LN1>;
-  constexpr int NS = Plan::kLastNs, R = Plan::kLastR, JSTEP = ColCfg<CT>::kThreads / C;
-  CT* o = out + static_cast<long>(item) * N;
+  constexpr int NS = Plan::kLastNs, R = Plan::kLastR, JSTEP = NT / C;
+  const int n2 = col0 + c;
+  CT* o = out + static_cast<long>(item) * N + n2;
   const T inv_n = T(2) / static_cast<T>(N);
-  const long n2 = col0 + c;
   const CT step = expi_pi(-static_cast<T>(n2 * NS) * inv_n);
 #pragma unroll
   for (int p = 0; p < NS / JSTEP; ++p) {
@@ -184,7 +206,7 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_fwd(StepArgs a, 
     for (int r = 0; r < R; ++r) {
       const int k1 = j + r * NS;
       w = (r % 4 == 0) ? expi_pi(-static_cast<T>(n2 * k1) * inv_n) : cmul(w, step);
-      o[static_cast<long>(k1) * N2 + n2] = cmul(v[r], w);
+      o[k1 * N2] = cmul(v[r], w);
     }
   }
 }
@@ -194,37 +216,52 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_fwd(StepArgs a, 
 // a CTA owns its columns, and all its loads are consumed before its stores) for conv_ola.
 template <int LN1, bool BUF, typename CT>
 __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_inv(StepArgs a, int log_n, CT* X, SegArgs sg) {
-  using T = RealOf<CT>;
   constexpr int N1 = 1 << LN1;
   constexpr int C = ColCfg<CT>::kElems / N1;
   constexpr int FS = padded(N1) + 1;
+  constexpr int NT = ColCfg<CT>::kThreads;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CT* tile = reinterpret_cast<CT*>(smem_raw);
-  const long N2 = 1L << (log_n - LN1);
-  const long N = 1L << log_n;
+  const int N2 = 1 << (log_n - LN1);
+  const int N = 1 << log_n;
   const int item = sg.item0 + blockIdx.y;
+  const int c = threadIdx.x % C, jt = threadIdx.x / C;
+  const int n2 = blockIdx.x * C + c;
+  {
+    const CT* xc = X + static_cast<long>(item) * N + n2;  // column n2: element n1 at xc[n1 * N2]
+    constexpr int EPT = ColCfg<CT>::kElems / NT;
+    CT vals[EPT];
+#pragma unroll
+    for (int q = 0; q < EPT; ++q) vals[q] = __ldg(xc + (jt + q * (N1 / 16)) * N2);
+    // First pass from registers (vals[q] = element jt + q*N1/16 of column c), last pass into
+    // registers and straight to the arena (outputs n1 = j + r*NS of column c).
+    fft_first_from_regs<+1>(vals, tile + c * FS, jt);
+  }
+  __syncthreads();
+  fft_middle<LN1, C, NT, +1>(tile, FS, twiddles<CT>(a));
+  // (segment bookkeeping after the transform: nothing 64-bit stays live across it)
   const int isb = item / sg.nseg, jseg = item - isb * sg.nseg;
   const int slot = isb / a.batch, b = isb - slot * a.batch;
   const long base = seg_base(sg.seg, sg.pre, jseg);
   const long first = static_cast<long>(jseg) * sg.seg, end = min(first + sg.seg, a.length);
-  const long col0 = static_cast<long>(blockIdx.x) * C;
-  const CT* x = X + static_cast<long>(item) * N;
-  constexpr int EPT = ColCfg<CT>::kElems / ColCfg<CT>::kThreads;
-  CT vals[EPT];
-#pragma unroll
-  for (int q = 0; q < EPT; ++q) {
-    const int idx = threadIdx.x + q * ColCfg<CT>::kThreads;
-    vals[q] = __ldg(x + static_cast<long>(idx / C) * N2 + col0 + idx % C);
-  }
-  // First pass from registers (vals[q] = element j + q*N1/16 of column c), last pass into
-  // registers and straight to the arena (outputs n1 = j + r*NS of column c).
-  const int c = threadIdx.x % C, jt = threadIdx.x / C;
-  fft_first_from_regs<+1>(vals, tile + c * FS, jt);
-  __syncthreads();
-  fft_middle<LN1, C, ColCfg<CT>::kThreads, +1>(tile, FS, twiddles<CT>(a));
+  CT* xc = X + static_cast<long>(item) * N + n2;
   using Plan = Pow2Plan<LN1>;
-  constexpr int NS = Plan::kLastNs, R = Plan::kLastR, JSTEP = ColCfg<CT>::kThreads / C;
-  float* yl = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length;
+  constexpr int NS = Plan::kLastNs, R = Plan::kLastR, JSTEP = NT / C;
+  // Output n = n1*N2 + n2 is sample base + n, stored when first <= base + n < end.
+  if constexpr (BUF) {
+#pragma unroll 1
+    for (int p = 0; p < NS / JSTEP; ++p) {
+      const int j = jt + p * JSTEP;
+      CT v[R];
+      fft_last_to_regs<LN1, +1>(tile + c * FS, j, twiddles<CT>(a), v);
+#pragma unroll
+      for (int r = 0; r < R; ++r) xc[(j + r * NS) * N2] = v[r];
+    }
+    return;
+  }
+  const int nlo = static_cast<int>(min(max(first - base, 0L), static_cast<long>(N))) - n2;
+  const int nhi = static_cast<int>(min(max(end - base, 0L), static_cast<long>(N))) - n2;
+  float* yl = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length + base + n2;
   float* yr = yl + a.length;
 #pragma unroll
   for (int p = 0; p < NS / JSTEP; ++p) {
@@ -233,15 +270,10 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_inv(StepArgs a, 
     fft_last_to_regs<LN1, +1>(tile + c * FS, j, twiddles<CT>(a), v);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const long n = static_cast<long>(j + r * NS) * N2 + col0 + c;
-      if constexpr (BUF) {
-        X[static_cast<long>(item) * N + n] = v[r];
-      } else {
-        const long m = base + n;
-        if (m >= first && m < end) {
-          yl[m] = static_cast<float>(v[r].x);
-          yr[m] = static_cast<float>(v[r].y);
-        }
+      const int k = (j + r * NS) * N2;
+      if (k >= nlo && k < nhi) {
+        yl[k] = static_cast<float>(v[r].x);
+        yr[k] = static_cast<float>(v[r].y);
       }
     }
   }
