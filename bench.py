@@ -188,28 +188,84 @@ def in_render_kernel_times(replay):
     return fam, (t1 - t0) if t0 is not None else None
 
 
-def conv_flops(mg, procs, rd, length):
-    """FP32 flops of the implemented long-convolution passes per render of `rd`, by kernel
-    family: every segment item runs N-point four-step transforms (5 N log2 N per transform):
-    cols_fwd (signal: column half), rows_conv (row half of the forward + inverse, product),
-    cols_inv (column half of the inverse); prologue (kernel spectrum) cols_fwd + rows_spec."""
-    out = {"cols_fwd": 0.0, "rows_conv": 0.0, "cols_inv": 0.0, "rows_spec": 0.0}
-    for st in rd.steps:
-        if st.type not in (mg.NodeType.REVERB, mg.NodeType.DELAY):
-            continue
+def family_work(mg, procs, rd, length, batch=1):
+    """Algorithmic work per render of `rd` by kernel family:
+    FFT families -> ("fp32", flops of the implemented transforms, 5 N log2 N per N-point
+    complex transform plus 8 flops per point of every spectral product); gather / scan /
+    pointwise families -> ("hbm", bytes: every gathered row read once, every stored row written
+    once, 8 B per stereo sample; a scan step's fused pointwise followers are counted with the
+    pointwise family).
+      reverb / delay, per (slot, batch, segment) item of the N = N1 N2 segmented transform:
+        cols_fwd  column halves of the signal forward and of the kernel spectrum (per slot)
+        rows_conv row halves of the forward and inverse + product (rows_conv_fk: + the kernel's
+                  row half per item; otherwise rows_spec does it once per slot)
+        cols_inv  column half of the inverse
+      eq_conv: per overlap-save window a forward and an inverse 8192-point (4096 when the step
+        is too small to fill the GPU) transform + product.
+    Steps computed in another step's launch (rd.step_owners: fused pointwise runs, scan
+    epilogues) are counted with that launch's family, followers as writes only."""
+    out = {}
+
+    def add(k, bound, v):
+        b, w = out.get(k, (bound, 0.0))
+        out[k] = (bound, w + v)
+
+    nsm = 148
+    owner = rd.step_owners(batch, length)
+    fam_of = {mg.NodeType.COMPRESSOR: "dyn_scan", mg.NodeType.NOISEGATE: "dyn_scan"}
+    for k, st in enumerate(rd.steps):
         slots = st.store_end - st.store_begin
-        taps = procs.reverb_length if st.type == mg.NodeType.REVERB else procs.delay_span
-        g = mg.conv_geometry(length, taps)
-        n, l1, l2 = 1 << g["log_n"], g["log_n1"], g["log_n2"]
-        items = slots * g["nseg"]
-        out["cols_fwd"] += (items + slots) * 5.0 * n * l1        # signal + kernel column passes
-        out["cols_inv"] += items * 5.0 * n * l1
-        if 8.0 * slots * n > (64 << 20):  # conv_fuse_kernel_rows: kernel rows transformed per item
-            out["rows_conv_fk"] = out.get("rows_conv_fk", 0.0) + items * (3 * 5.0 * n * l2 + 16.0 * n)
-        else:
-            out["rows_spec"] += slots * 5.0 * n * l2
-            out["rows_conv"] += items * (2 * 5.0 * n * l2 + 16.0 * n)  # forward + inverse rows, product
+        t = st.type
+        hbm = 8.0 * length * batch * (len(st.gather) + slots)
+        if owner[k] != k and rd.steps[owner[k]].type in fam_of:
+            # pointwise follower computed in a scan's epilogue: it only writes its rows
+            add("dyn_scan", "hbm", 8.0 * length * batch * slots)
+        elif owner[k] != k:
+            add("pointwise", "hbm", 8.0 * length * batch * slots)
+        elif t in (mg.NodeType.REVERB, mg.NodeType.DELAY):
+            taps = procs.reverb_length if t == mg.NodeType.REVERB else procs.delay_span
+            g = mg.conv_geometry(length, taps)
+            n, l1, l2 = 1 << g["log_n"], g["log_n1"], g["log_n2"]
+            items = slots * batch * g["nseg"]
+            add("cols_fwd", "fp32", (items + slots) * 5.0 * n * l1)
+            add("cols_inv", "fp32", items * 5.0 * n * l1)
+            if 8.0 * slots * n > (64 << 20):  # conv_fuse: kernel rows transformed per item
+                add("rows_conv_fk", "fp32", items * (3 * 5.0 * n * l2 + 16.0 * n))
+            else:
+                add("rows_spec", "fp32", slots * 5.0 * n * l2)
+                add("rows_conv", "fp32", items * (2 * 5.0 * n * l2 + 16.0 * n))
+        elif t == mg.NodeType.EQ:
+            big = slots * batch * -(-length // 6144) >= nsm  # eq.cu eq_uses_small_window
+            nw, hop = (8192, 6144) if big else (4096, 2048)
+            wins = slots * batch * -(-length // hop)
+            add("eq_conv", "fp32", wins * (2 * 5.0 * nw * (13 if big else 12) + 8.0 * nw))
+        elif t in fam_of:
+            add("dyn_scan", "hbm", hbm)
+        elif t != mg.NodeType.IN:
+            add("pointwise", "hbm", hbm)
     return out
+
+
+def roofline_table(fam_serial, work, hbm_peak):
+    """Per kernel family: serialized in-render time, algorithmic work, achieved and fraction of
+    its bound's peak (nominal FP32 for FFT families, measured HBM for the others)."""
+    tab, merged = {}, {}
+    for k, d in fam_serial.items():  # pointwise / pointwise_wide / pointwise_chain: one family
+        m = merged.setdefault("pointwise" if k.startswith("pointwise") else k, {"us": 0.0, "launches": 0})
+        m["us"] += d["us"]
+        m["launches"] += d["launches"]
+    for k, d in merged.items():
+        row = {"us": round(d["us"], 1), "launches": d["launches"]}
+        if k in work and d["us"] > 0:
+            bound, w = work[k]
+            if bound == "fp32":
+                a = w / (d["us"] * 1e-6) / 1e12
+                row.update(bound="fp32", flops=w, achieved_tflops=round(a, 3), frac=round(a / FP32_PEAK_TFLOPS, 4))
+            else:
+                a = w / (d["us"] * 1e-6) / 1e9
+                row.update(bound="hbm", bytes=w, achieved_gbs=round(a, 1), frac=round(a / hbm_peak, 4))
+        tab[k] = row
+    return dict(sorted(tab.items(), key=lambda kv: -kv[1]["us"]))
 
 
 # ---- reference CPU renders (cpu_baseline and --impl reference) -----------------------------
@@ -306,6 +362,9 @@ def config2_lines(mg, procs, dev, steps=20, warmup=3):
     ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
     ns = node_samples(t)
     fam, span = in_render_kernel_times(g.replay)
+    dr.render_profiled(hoist=False)
+    fam_s, span_s = in_render_kernel_times(lambda: dr.render_profiled(hoist=False))
+    serial = roofline_table(fam_s, family_work(mg, procs, rd, L), peaks()[0])
     pipe = mg.RenderPipeline(rd, procs, 1, L, dtype=np.float64, depth=2)
     ps = pipe.pinned(src.shape)
     ps[...] = src
@@ -324,7 +383,8 @@ def config2_lines(mg, procs, dev, steps=20, warmup=3):
             "e2e": {"value": ns / e2e_s, "unit": UNIT, "ms_per_render": e2e_s * 1e3,
                     "api": "RenderPipeline (mg_pipeline_submit), double host audio, pinned"},
             "in_render_us": {k: round(v["us"], 1) for k, v in sorted(fam.items(), key=lambda kv: -kv[1]["us"])},
-            "render_span_us_traced": span, "gpu_launches_per_render": rd.kernel_count(1, L),
+            "render_span_us_traced": span, "roofline_families_serialized": serial,
+            "serialized_span_us": span_s, "gpu_launches_per_render": rd.kernel_count(1, L),
             "workload": "config2: generate_console(16, p=0.3, seed=16), 121 nodes / 139 edges, stereo 2^17, B=1; "
                         "L2 flushed between iterations",
             "type_string": rd.schedule.type_codes()}
@@ -544,12 +604,22 @@ def b200_arm(args):
     dev_ms = float(sum(a.elapsed_time(b) for a, b in ev))
     dev_ms_max = max_over_ranks(dev_ms, dev, world)
 
-    # In-render kernel timings of one step (CUPTI trace, outside the timed region).
+    # In-render kernel timings of one step (CUPTI traces, outside the timed region): the
+    # replayed step as timed (concurrent kernels overlap, low-priority prologues include time
+    # waiting for SMs) and the same renders serialised on one stream (each kernel's own cost,
+    # with the render's cache state) for the roofline.
     fam, span_us = in_render_kernel_times(step)
-    flops = {}
+
+    def serial_step():
+        for dr in renderers:
+            dr.render_profiled(hoist=False)
+
+    serial_step()
+    fam_serial, serial_span_us = in_render_kernel_times(serial_step)
+    work = {}
     for _, rd, _ in cases:
-        for k, v in conv_flops(mg, procs, rd, L).items():
-            flops[k] = flops.get(k, 0.0) + v
+        for k, (bound, w) in family_work(mg, procs, rd, L).items():
+            work[k] = (bound, work.get(k, (bound, 0.0))[1] + w)
 
     # End to end through the public API with host buffers: BatchRenderer (mg_batch_submit),
     # pinned fp32 sources per input node, original-order parameters, outputs D2H.
@@ -602,14 +672,14 @@ def b200_arm(args):
     if rank == 0:
         hbm_peak, peak_kind = peaks()
         value = ns_all * n / (dev_ms_max * 1e-3)
-        # Dominant kernel family in the render (in-render CUPTI time) and its roofline.
-        dom = max(fam.items(), key=lambda kv: kv[1]["us"]) if fam else (None, {"us": 0, "launches": 0})
-        dom_name, dom_t = dom
-        achieved = flops.get(dom_name, 0.0) / (dom_t["us"] * 1e-6) / 1e12 if dom_t["us"] and flops.get(dom_name) else None
+        # Dominant kernel family by its serialised in-render time, and its roofline.
+        table = roofline_table(fam_serial, work, hbm_peak)
+        dom_name = next(iter(table)) if table else None
+        dom = table.get(dom_name, {})
         traffic = None
         try:
-            with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
-                traffic = json.load(f).get(dom_name)
+            with open(os.path.join(ROOT, "profiles", "r02s_traffic.json")) as f:
+                traffic = (json.load(f).get(dom_name) or {}).get("dram_bytes_per_launch")
         except Exception:
             pass
         result = {
@@ -627,20 +697,31 @@ def b200_arm(args):
                     "api": "BatchRenderer (mg_batch_submit): pinned fp32 host sources per input node, original-order "
                            "parameter tables, device reorder, render, output D2H; wall clock, max over ranks",
                     "ms_per_step": e2e_s / n * 1e3, "graph_renders_per_sec": len(graphs) * n / e2e_s},
-            "roofline": {"bound": "fp32", "kernel": dom_name, "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
-                         "peak_kind": "nominal FP32 CUDA-core (148 SM x 128 FMA x 2 x 1965 MHz); no measured FP32 peak",
-                         "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS if achieved else None,
-                         "traffic": traffic, "launches_per_step": dom_t["launches"],
-                         "us_per_step_in_render": dom_t["us"], "flops_per_step": flops.get(dom_name),
-                         "share_of_kernel_time": dom_t["us"] / sum(v["us"] for v in fam.values()) if fam else None,
-                         "note": "in-render kernel time from a CUPTI trace of one replayed step (concurrent kernels "
-                                 "overlap); flops of the implemented four-step transforms, 5 N log2 N per transform"},
+            "roofline": {"bound": dom.get("bound"), "kernel": dom_name,
+                         "achieved": dom.get("achieved_tflops", dom.get("achieved_gbs")),
+                         "peak": FP32_PEAK_TFLOPS if dom.get("bound") == "fp32" else hbm_peak,
+                         "peak_kind": ("nominal FP32 CUDA-core (148 SM x 128 FMA x 2 x 1965 MHz); no measured FP32 "
+                                       "peak" if dom.get("bound") == "fp32" else peak_kind),
+                         "unit": "TFLOP/s" if dom.get("bound") == "fp32" else "GB/s", "frac": dom.get("frac"),
+                         "traffic": traffic, "launches_per_step": dom.get("launches"),
+                         "us_per_step_serialized": dom.get("us"),
+                         "work_per_step": dom.get("flops", dom.get("bytes")),
+                         "share_of_serialized_kernel_time": (dom.get("us", 0.0) / sum(v["us"] for v in table.values())
+                                                             if table else None),
+                         "note": "dominant kernel family by in-render time with the step's renders serialised on one "
+                                 "stream (CUPTI trace, prologues inline, no side streams: each kernel's own cost "
+                                 "with the render's cache state); work = algorithmic flops of the implemented "
+                                 "transforms (5 N log2 N per complex N-point transform + 8 per spectral product) "
+                                 "or algorithmic bytes; traffic = ncu dram bytes per launch of that family from "
+                                 "the committed capture (profiles/r02s_traffic.json)"},
+            "roofline_families": table,
             "roofline_hbm": {"bound": "hbm", "achieved": alg_bytes / (dev_ms / n * 1e-3) / 1e9,
                              "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s", "traffic": alg_bytes,
                              "note": "whole render of rank 0's shard: algorithmic bytes (every gathered row read once, "
                                      "every non-input row written once, 8 B per stereo sample) over the device step "
                                      "time; SURVEY.md 8d"},
             "in_render_us_per_step": {k: round(v["us"], 1) for k, v in sorted(fam.items(), key=lambda kv: -kv[1]["us"])},
+            "serialized_span_us": serial_span_us,
             "in_render_launches_per_step": {k: v["launches"] for k, v in fam.items()},
             "traced_span_us": span_us,
             "wall_s_timed_region": wall, "clocks": clocks, "gpu_launches": kernels_per_step * n,

@@ -96,12 +96,18 @@ int32_t mg_render(const mg_plan* plan, const mg_processors* procs, const double*
 int32_t mg_plan_workspace_bytes(const mg_plan* plan, const mg_processors* procs, int32_t batch, int64_t length,
                                 uint64_t* bytes);
 int32_t mg_plan_kernel_count(const mg_plan* plan, int32_t batch, int64_t length, int32_t* count);
+/* owner[k] (num_steps entries) = the step whose kernel launch computes step k in a render:
+ * k itself, the first step of a fused run of small pointwise steps, or the scan / pointwise
+ * step whose epilogue computes it (measurement: per-kernel attribution of the render's work).
+ * No reference counterpart (the reference runs one step at a time, render.cpp:40-80). */
+int32_t mg_plan_step_owners(const mg_plan* plan, int32_t batch, int64_t length, int32_t* owner);
 int32_t mg_render_arena(const mg_plan* plan, const mg_processors* procs, const double* const* d_tables, float* d_arena,
                         int32_t batch, int64_t length, void* d_workspace, uint64_t workspace_bytes, void* stream);
 
-/* Same as mg_render_arena with a device event pair recorded around every step; when step_ms
- * is non-NULL the call synchronises `stream` and writes each step's duration (ms). hoist = 0
- * runs each step's parameter prologue inline (isolated per-step costs). */
+/* Same as mg_render_arena with, when step_ms is non-NULL, a device event pair recorded around
+ * every step (each step then launches on its own): the call synchronises `stream` and writes
+ * each step's duration (ms). hoist = 0 runs every parameter prologue inline and nothing on
+ * side streams: the render's kernels serialised on `stream` (per-kernel costs in a trace). */
 int32_t mg_render_arena_profiled(const mg_plan* plan, const mg_processors* procs, const double* const* d_tables,
                                  float* d_arena, int32_t batch, int64_t length, void* d_workspace,
                                  uint64_t workspace_bytes, void* stream, float* step_ms, int32_t hoist);
@@ -146,6 +152,12 @@ int32_t mg_render_backward_arena(const mg_plan* plan, const mg_processors* procs
  * pass), 0 always runs the separate kernel-spectrum row pass, 1 always fuses. Process-wide;
  * results agree either way. */
 void mg_set_conv_fuse(int32_t mode);
+
+/* Execution-strategy switch for the compressor / noisegate scans (diagnostics and tests): -1
+ * chooses per step (default: steps with a full wave of dense sequences stream one sequence per
+ * CTA, others run the chained look-back scan), 0 always chained, 1 streaming wherever legal
+ * (dense steps, L % 4 == 0). Process-wide; results agree to fp64 rounding of the envelope. */
+void mg_set_dyn_stream(int32_t mode);
 
 /* Transform-size switch for the long convolutions (tests): 0 (default) picks per step the
  * cheapest segmented overlap-save size (one next_pow2(L + taps - 1) transform, as the

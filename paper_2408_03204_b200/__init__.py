@@ -69,6 +69,7 @@ _sig("mg_processors_info", _i32, _vp, _vp)
 _sig("mg_render", _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i64, _dbl, _vp, _vp)
 _sig("mg_plan_workspace_bytes", _i32, _vp, _vp, _i32, _i64, _P(_u64))
 _sig("mg_plan_kernel_count", _i32, _vp, _i32, _i64, _P(_i32))
+_sig("mg_plan_step_owners", _i32, _vp, _i32, _i64, _vp)
 _sig("mg_render_arena", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp)
 _sig("mg_render_arena_profiled", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp, _vp, _i32)
 _sig("mg_profile_steps", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp, _i32, _vp)
@@ -82,6 +83,7 @@ _sig("mg_pipeline_destroy", None, _vp)
 _sig("mg_backward_workspace_bytes", _i32, _vp, _vp, _i32, _i64, _P(_u64))
 _sig("mg_render_backward_arena", _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp)
 _sig("mg_set_conv_fuse", None, _i32)
+_sig("mg_set_dyn_stream", None, _i32)
 _sig("mg_set_conv_log", None, _i32)
 _sig("mg_conv_geometry", _i32, _i64, _i64, _vp)
 _sig("mg_set_fft_precision", None, _i32)
@@ -442,6 +444,13 @@ class RenderData:
         _check(_lib.mg_plan_kernel_count(self._h, batch, length, ctypes.byref(c)))
         return int(c.value)
 
+    def step_owners(self, batch: int, length: int) -> np.ndarray:
+        """owner[k] = the step whose kernel launch computes step k (itself, the head of a fused
+        pointwise run, or the producer whose epilogue computes it); mg_plan_step_owners."""
+        out = np.zeros(self.num_steps, dtype=np.int32)
+        _check(_lib.mg_plan_step_owners(self._h, batch, length, out.ctypes.data_as(_vp)))
+        return out
+
     def __del__(self, _destroy=_lib.mg_plan_destroy):
         h, self._h = getattr(self, "_h", None), None
         if h:
@@ -611,6 +620,12 @@ def render(rd: RenderData, procs: ProcessorSet, params: Optional[Dict[int, np.nd
 def set_conv_fuse(mode: int) -> None:
     """mg_set_conv_fuse: -1 auto (default), 0 separate kernel-spectrum rows pass, 1 fused."""
     _lib.mg_set_conv_fuse(int(mode))
+
+
+def set_dyn_stream(mode: int) -> None:
+    """mg_set_dyn_stream: -1 auto (default), 0 chained look-back scan, 1 streaming scan
+    (one CTA per sequence) wherever legal."""
+    _lib.mg_set_dyn_stream(int(mode))
 
 
 def conv_geometry(length: int, taps: int) -> Dict[str, int]:

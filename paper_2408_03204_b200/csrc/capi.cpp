@@ -21,6 +21,7 @@ void launch_mse_loss_grad(const float* y, const float* target, long n, float* gr
                           cudaStream_t s);
 void launch_sgd_step(bool dynamics, double* table, const double* grad, long n, double lr, cudaStream_t s);
 void set_conv_fuse(int mode);
+void set_dyn_stream(int mode);
 void set_conv_log(int log_n);
 void set_fft_fp64(bool on);
 void conv_geometry(long length, long taps, long* out);
@@ -355,6 +356,10 @@ int32_t mg_plan_kernel_count(const mg_plan* p, int32_t batch, int64_t length, in
   return guarded([&] { *count = device_plan(p, nullptr).kernels_per_render(batch, static_cast<long>(length)); });
 }
 
+int32_t mg_plan_step_owners(const mg_plan* p, int32_t batch, int64_t length, int32_t* owner) {
+  return guarded([&] { device_plan(p, nullptr).step_owners(batch, static_cast<long>(length), owner); });
+}
+
 int32_t mg_render_arena(const mg_plan* p, const mg_processors* procs, const double* const* d_tables, float* d_arena,
                         int32_t batch, int64_t length, void* d_ws, uint64_t ws_bytes, void* stream) {
   return guarded([&] {
@@ -381,7 +386,8 @@ int32_t mg_render_arena_profiled(const mg_plan* cp, const mg_processors* procs, 
     }
     auto s = static_cast<cudaStream_t>(stream);
     std::scoped_lock rlock(p->render_mu);
-    render_arena(dp, *procs->ps, d_tables, d_arena, batch, static_cast<long>(length), d_ws, ws_bytes, s, p->events.data(), hoist != 0);
+    render_arena(dp, *procs->ps, d_tables, d_arena, batch, static_cast<long>(length), d_ws, ws_bytes, s,
+                 step_ms ? p->events.data() : nullptr, hoist != 0);
     if (step_ms) {
       if (cudaStreamSynchronize(s) != cudaSuccess) throw std::runtime_error("render failed");
       for (std::size_t k = 0; k < p->rd.steps.size(); ++k) {
@@ -471,6 +477,7 @@ int32_t mg_render_backward_arena(const mg_plan* p, const mg_processors* procs, c
 }
 
 void mg_set_conv_fuse(int32_t mode) { mgb::set_conv_fuse(mode); }
+void mg_set_dyn_stream(int32_t mode) { mgb::set_dyn_stream(mode); }
 
 void mg_set_conv_log(int32_t log_n) { mgb::set_conv_log(log_n); }
 

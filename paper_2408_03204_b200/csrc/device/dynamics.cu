@@ -427,6 +427,194 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
   }
 }
 
+// ---- streaming scan: one CTA per sequence (steps with many sequences) ----------------------
+//
+// When a step has at least a full wave of sequences (a config-5 union's 1,124 track
+// compressors), each CTA owns one (slot, batch) sequence and walks its tiles in order: the
+// carry into tile t is the CTA's own running state (carry = a^tile * carry + B_tile, fp64), so
+// there is no look-back, no status words and no cross-CTA waiting. The input rows are streamed
+// into a 3-stage shared-memory ring by the bulk-copy engine (cp.async.bulk, one elected thread,
+// mbarrier completion), two tiles ahead of the scan, so every CTA keeps 32 KB of loads in
+// flight while it scans and stores. One block barrier per tile: the stage a tile was read from
+// is refilled after the next tile's barrier, and the per-warp aggregates alternate between two
+// buffers. Arithmetic per sample is dyn_scan's (fp64 recurrence, correctly rounded gain).
+// Needs a dense step (slot s reads row dense + s) and L % 4 == 0 (16-byte bulk copies).
+constexpr int kStreamThreads = 256;
+constexpr int kStreamDepth = 3;
+constexpr int kStreamTile = kStreamThreads * kDynPerThread;
+constexpr int kStreamSmem = kStreamDepth * 2 * kStreamTile * static_cast<int>(sizeof(float));
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+
+template <bool GATE, bool VEC>
+__global__ void __launch_bounds__(kStreamThreads, 4) dyn_stream(StepArgs a, int env_taps, double floor_, PwEpi epi) {
+  constexpr int NT = kStreamThreads, TS = kStreamTile, NW = NT / 32;
+  extern __shared__ __align__(128) unsigned char stream_smem[];
+  float* ring = reinterpret_cast<float*>(stream_smem);  // [stage][channel][TS]
+  __shared__ __align__(8) unsigned long long bar[kStreamDepth];
+  __shared__ double wA[2][NW], wB[2][NW];
+  __shared__ DynParams s_p;
+  __shared__ PwEpiSlots s_epi;
+  const int seq = blockIdx.x;
+  const int slot = seq / a.batch, b = seq - slot * a.batch;
+  const long L = a.length;
+  const long boff = static_cast<long>(b) * 2 * L;
+  const float* in = a.src + (static_cast<long>(a.dense) + slot) * a.rowstride + boff;
+  const int tiles = static_cast<int>((L + TS - 1) / TS);
+  auto issue = [&](int t) {
+    const int st = t % kStreamDepth;
+    const long n0 = static_cast<long>(t) * TS;
+    const uint32_t bytes = static_cast<uint32_t>(min(static_cast<long>(TS), L - n0)) * 4u;
+    float* dst = ring + st * 2 * TS;
+    mbar_expect_tx(&bar[st], 2 * bytes);
+    bulk_g2s(dst, in + n0, bytes, &bar[st]);
+    bulk_g2s(dst + TS, in + L + n0, bytes, &bar[st]);
+  };
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int d = 0; d < kStreamDepth; ++d) mbar_init(&bar[d], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int t = 0; t < kStreamDepth && t < tiles; ++t) issue(t);
+  }
+  if (threadIdx.x < 32) {
+    derive_params(a.params + 4L * slot, env_taps, floor_, L, threadIdx.x, &s_p, TS, GATE);
+    if (epi.n > 0 && threadIdx.x == 1) pw_epi_slots(epi, slot, s_epi);
+  }
+  __syncthreads();
+  const DynParams& p = s_p;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e0 = slot_e0(a, slot), e1 = slot_e1(a, slot);
+  float* ol0 = a.dst + static_cast<long>(slot) * a.rowstride + boff;
+  double carry = 0.0;
+  for (int t = 0; t < tiles; ++t) {
+    const int st = t % kStreamDepth;
+    const long n0 = static_cast<long>(t) * TS + static_cast<long>(threadIdx.x) * kDynPerThread;
+    const bool live = n0 < L;  // L % 4 == 0: a live thread has 4 or 8 valid samples
+    const bool full = n0 + kDynPerThread <= L;
+    mbar_wait(&bar[st], static_cast<uint32_t>((t / kStreamDepth) & 1));
+    const float* sl = ring + st * 2 * TS + threadIdx.x * kDynPerThread;
+    double drive[kDynPerThread];
+    {
+      float mid[kDynPerThread];
+#pragma unroll
+      for (int q = 0; q < kDynPerThread / 4; ++q) {
+        float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
+        if (live && (q == 0 || full)) {
+          l = *reinterpret_cast<const float4*>(sl + 4 * q);
+          r = *reinterpret_cast<const float4*>(sl + TS + 4 * q);
+        }
+        // the gather of one row is 0 + x (dyn_scan's edge-order sum)
+        mid[4 * q] = (0.f + l.x) + (0.f + r.x);
+        mid[4 * q + 1] = (0.f + l.y) + (0.f + r.y);
+        mid[4 * q + 2] = (0.f + l.z) + (0.f + r.z);
+        mid[4 * q + 3] = (0.f + l.w) + (0.f + r.w);
+      }
+      if (p.daN != 0.0) {
+        float mo[kDynPerThread];
+        load_mid<VEC>(a, e0, e1, b, live ? n0 - p.Ne : L, mo);
+#pragma unroll
+        for (int k = 0; k < kDynPerThread; ++k) {
+          const double m = mid[k], o = mo[k];
+          drive[k] = p.doma * (m * m - p.daN * (o * o));
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < kDynPerThread; ++k) {
+          const double m = mid[k];
+          drive[k] = p.doma * (m * m);
+        }
+      }
+    }
+    double B = 0.0;
+#pragma unroll
+    for (int k = 0; k < kDynPerThread; ++k) B = fma(p.da, B, drive[k]);
+    double A = p.da16;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const double Ap = __shfl_up_sync(0xffffffffu, A, off);
+      const double Bp = __shfl_up_sync(0xffffffffu, B, off);
+      if (lane >= off) compose(A, B, Ap, Bp);
+    }
+    if (lane == 31) {
+      wA[t & 1][warp] = A;
+      wB[t & 1][warp] = B;
+    }
+    double xA = __shfl_up_sync(0xffffffffu, A, 1), xB = __shfl_up_sync(0xffffffffu, B, 1);
+    if (lane == 0) {
+      xA = 1.0;
+      xB = 0.0;
+    }
+    __syncthreads();
+    // Every thread of tile t - 1 is past its output pass: refill its stage two tiles ahead.
+    if (threadIdx.x == 0 && t >= 1 && t - 1 + kStreamDepth < tiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(t - 1 + kStreamDepth);
+    }
+    // Prefix of the earlier warps (in order) and the tile's aggregate, the same values in every thread.
+    double pA = 1.0, pB = 0.0, tB = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const double Aw = wA[t & 1][w], Bw = wB[t & 1][w];
+      if (w < warp) {
+        pB = fma(Aw, pB, Bw);
+        pA = Aw * pA;
+      }
+      tB = fma(Aw, tB, Bw);
+    }
+    compose(xA, xB, pA, pB);
+    double g = fma(xA, carry, xB);
+    carry = fma(p.datile, carry, tB);
+    if (!live) continue;
+    float* ol = ol0 + n0;
+    float* orr = ol + L;
+#pragma unroll
+    for (int q = 0; q < kDynPerThread / 4; ++q) {
+      if (q > 0 && !full) break;
+      const float4 l4 = *reinterpret_cast<const float4*>(sl + 4 * q);
+      const float4 r4 = *reinterpret_cast<const float4*>(sl + TS + 4 * q);
+      const float ul[4] = {0.f + l4.x, 0.f + l4.y, 0.f + l4.z, 0.f + l4.w};
+      const float ur[4] = {0.f + r4.x, 0.f + r4.y, 0.f + r4.z, 0.f + r4.w};
+      float yl[4], yr[4];
+#pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4) {
+        g = fma(p.da, g, drive[4 * q + k4]);
+        const float gn = gain_of<GATE>(static_cast<float>(g), p);
+        yl[k4] = gn * ul[k4];
+        yr[k4] = gn * ur[k4];
+      }
+      reinterpret_cast<float4*>(ol)[q] = make_float4(yl[0], yl[1], yl[2], yl[3]);
+      reinterpret_cast<float4*>(orr)[q] = make_float4(yr[0], yr[1], yr[2], yr[3]);
+      if (epi.n > 0) {
+        pw_epi_apply(epi, s_epi, a.rowstride, L, boff + n0 + 4 * q, yl, yr, true, 4);
+      }
+    }
+  }
+}
+
 // ---- backward (parameter gradients; no reference counterpart, see backward.cu) -------------
 //
 // Given dy (gathered over the consumers' input gradients) and the forward quantities
@@ -789,6 +977,24 @@ std::size_t dyn_sync_bytes(int slots, int batch, long length) {
   return 256 + sizeof(unsigned long long) * static_cast<std::size_t>(slots) * batch * tiles;
 }
 
+// The streaming scan (one CTA per sequence) when the step has a full wave of sequences at four
+// CTAs per SM, its slots read consecutive rows and the rows are 16-byte aligned (L % 4 == 0).
+// (mg_set_dyn_stream: 0 forces the chained scan, for tests.)
+static int g_dyn_stream = -1;
+void set_dyn_stream(int mode) { g_dyn_stream = mode; }
+static int sm_count_dyn() {
+  static const int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+bool dyn_stream_ok(const StepArgs& a) {
+  if (g_dyn_stream == 0 || a.dense < 0 || a.length % 4 != 0) return false;
+  return g_dyn_stream == 1 || static_cast<long>(a.slots) * a.batch >= 4L * sm_count_dyn();
+}
+
 void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double energy_floor, void* ws,
                      bool zero_sync, cudaStream_t s, const PwEpi& epi) {
   if (a.slots == 0 || a.batch == 0 || a.length == 0) return;
@@ -809,6 +1015,24 @@ void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double ene
   auto* status = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 256);
   const long ne = envelope_taps < a.length ? envelope_taps : a.length;
   const bool vec = (a.length % 4 == 0) && (ne % 4 == 0);
+  if (dyn_stream_ok(a)) {
+    static const bool attr = [] {
+      for (auto fn : {dyn_stream<false, false>, dyn_stream<false, true>, dyn_stream<true, false>, dyn_stream<true, true>}) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamSmem);
+      }
+      return true;
+    }();
+    (void)attr;
+    const dim3 sgrid(static_cast<unsigned>(seqs));
+    if (gate) {
+      if (vec) dyn_stream<true, true><<<sgrid, kStreamThreads, kStreamSmem, s>>>(a, envelope_taps, energy_floor, epi);
+      else dyn_stream<true, false><<<sgrid, kStreamThreads, kStreamSmem, s>>>(a, envelope_taps, energy_floor, epi);
+    } else {
+      if (vec) dyn_stream<false, true><<<sgrid, kStreamThreads, kStreamSmem, s>>>(a, envelope_taps, energy_floor, epi);
+      else dyn_stream<false, false><<<sgrid, kStreamThreads, kStreamSmem, s>>>(a, envelope_taps, energy_floor, epi);
+    }
+    return;
+  }
   const dim3 grid(static_cast<unsigned>(total));
 #define MGB_DYN_LAUNCH(G, V, T) \
   dyn_scan<G, V, false, T><<<grid, T, 0, s>>>(a, envelope_taps, energy_floor, tiles, status, nullptr, nullptr, epi)

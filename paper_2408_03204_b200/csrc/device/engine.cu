@@ -552,6 +552,15 @@ int DevicePlan::kernels_per_render(int batch, long length) const {
   return k;
 }
 
+void DevicePlan::step_owners(int batch, long length, int* owner) const {
+  for (std::size_t i = 0; i < rd_.steps.size();) {
+    const int n = chain_length(rd_, i, batch, length);
+    const std::size_t span = static_cast<std::size_t>(n > 1 ? n : 1 + epi_followers(*this, i, batch, length));
+    for (std::size_t j = i; j < i + span; ++j) owner[j] = static_cast<int>(i);
+    i += span;
+  }
+}
+
 void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const double* const* param_tables, float* arena,
                   int batch, long length, void* workspace, std::size_t workspace_bytes, cudaStream_t stream,
                   cudaEvent_t* step_events, bool hoist) {
@@ -629,9 +638,11 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
       continue;
     }
     // Pointwise followers ride in this step's epilogue (not with per-step events, nor for a
-    // step that runs on the side lane).
+    // step that runs on the side lane). Without hoisting everything is serialised on `stream`
+    // (no side lane either): the product's kernels one after another, for per-kernel costs.
     mgb::PwEpi epi{};
-    if (!step_events && !lay.paired[k]) {
+    const bool paired = hoist && !step_events && lay.paired[k];
+    if (!step_events && !paired) {
       epi.n = epi_followers(plan, k, batch, length);
       for (int f = 0; f < epi.n; ++f) {
         const std::size_t j = k + 1 + static_cast<std::size_t>(f);
@@ -641,7 +652,7 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
         epi.params[f] = args[j].params;
       }
     }
-    if (!step_events && lay.paired[k]) {
+    if (paired) {
       // Steps k and k+1 side by side: k on the lane, k+1 on the main stream, then join.
       const cudaEvent_t* le = plan.lane_events();
       cudaStream_t lane = plan.lane();
@@ -1481,6 +1492,8 @@ void ProcessorSet::process_device(NodeType type, const float* in, float* out, in
   a.tw = mgb::twiddle_table(dev_->device);
   a.tw64 = mgb::twiddle_table64(dev_->device);
   a.rowstride = static_cast<long>(batch) * 2 * length;
+  a.nnz = slots;
+  a.dense = 0;  // the identity CSR is dense: slot s reads row 0 + s
   run_step(type, a, *this, aux + align256(sizeof(int) * idx.size()), stream);
   cuda_check(cudaGetLastError(), "process launch");
   // The CSR lives in a reused staging buffer: finish before it can be overwritten.

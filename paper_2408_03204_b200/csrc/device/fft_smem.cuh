@@ -28,8 +28,39 @@ template <> struct Cx<double2> {
 };
 template <typename C> using RealOf = typename Cx<C>::Real;
 
+// fp32 complex arithmetic on Blackwell's packed f32x2 pipe (FADD2 / FMUL2 / FFMA2: both
+// lanes of a float2 in one instruction, IEEE round-to-nearest per lane, so every value equals
+// the scalar operation's). ptxas folds lane swaps, broadcasts and per-lane negations into the
+// operands (R.F32x2.LO_HI, R.F32, -R.NP), so a*i +- b is one FADD2 and a complex product two
+// instructions, where the scalar forms took two and four: the FFT passes are issue-bound.
+__device__ __forceinline__ float2 f2_add(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 x, y, z;\n\tmov.b64 x, {%2,%3};\n\tmov.b64 y, {%4,%5};\n\tadd.rn.f32x2 z, x, y;\n\t"
+      "mov.b64 {%0,%1}, z;}" : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 f2_sub(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 x, y, z;\n\tmov.b64 x, {%2,%3};\n\tmov.b64 y, {%4,%5};\n\tsub.rn.f32x2 z, x, y;\n\t"
+      "mov.b64 {%0,%1}, z;}" : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 f2_mul(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 x, y, z;\n\tmov.b64 x, {%2,%3};\n\tmov.b64 y, {%4,%5};\n\tmul.rn.f32x2 z, x, y;\n\t"
+      "mov.b64 {%0,%1}, z;}" : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{.reg .b64 x, y, z, w;\n\tmov.b64 x, {%2,%3};\n\tmov.b64 y, {%4,%5};\n\tmov.b64 z, {%6,%7};\n\t"
+      "fma.rn.f32x2 w, x, y, z;\n\tmov.b64 {%0,%1}, w;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+// a*b = a*b.x + (-a.y, a.x)*b.y: re = fma(-a.y, b.y, a.x b.x), im = fma(a.x, b.y, a.y b.x).
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+  return f2_fma(make_float2(-a.y, a.x), make_float2(b.y, b.y), f2_mul(a, make_float2(b.x, b.x)));
 }
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -38,10 +69,17 @@ template <typename C>
 __device__ __forceinline__ C cadd(C a, C b) { return Cx<C>::mk(a.x + b.x, a.y + b.y); }
 template <typename C>
 __device__ __forceinline__ C csub(C a, C b) { return Cx<C>::mk(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return f2_add(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return f2_sub(a, b); }
 template <typename C>
 __device__ __forceinline__ C cconj(C a) { return Cx<C>::mk(a.x, -a.y); }
 template <typename C>
 __device__ __forceinline__ C cscale(C a, RealOf<C> s) { return Cx<C>::mk(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return f2_mul(a, make_float2(s, s)); }
+// a * s + b (one rounding per component)
+template <typename C>
+__device__ __forceinline__ C caxpy(C a, RealOf<C> s, C b) { return Cx<C>::mk(fma(a.x, s, b.x), fma(a.y, s, b.y)); }
+__device__ __forceinline__ float2 caxpy(float2 a, float s, float2 b) { return f2_fma(a, make_float2(s, s), b); }
 // a * (dir * i)
 template <int DIR, typename C>
 __device__ __forceinline__ C cmul_i(C a) {
@@ -101,9 +139,9 @@ struct Dft<8, DIR, C> {
     Dft<4, DIR, C>::run(o);
     constexpr T h = static_cast<T>(0.70710678118654752440);
     // o[k] *= exp(dir*2*pi*i*k/8)
-    o[1] = Cx<C>::mk(h * (o[1].x - DIR * o[1].y), h * (o[1].y + DIR * o[1].x));
+    o[1] = cmul(o[1], Cx<C>::mk(h, DIR * h));
     o[2] = cmul_i<DIR>(o[2]);
-    o[3] = Cx<C>::mk(h * (-o[3].x - DIR * o[3].y), h * (-o[3].y + DIR * o[3].x));
+    o[3] = cmul(o[3], Cx<C>::mk(-h, DIR * h));
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       v[k] = cadd(e[k], o[k]);
@@ -148,8 +186,8 @@ struct Dft<3, DIR, C> {
     const C a = v[0], b = v[1], d = v[2];
     const C sum = cadd(b, d), dif = csub(b, d);
     v[0] = cadd(a, sum);
-    const C m = Cx<C>::mk(a.x + c * sum.x, a.y + c * sum.y);
-    const C r = Cx<C>::mk(-s * dif.y, s * dif.x);  // i*s*(b-d)
+    const C m = caxpy(sum, c, a);
+    const C r = cscale(Cx<C>::mk(-dif.y, dif.x), s);  // i*s*(b-d)
     v[1] = cadd(m, r);
     v[2] = csub(m, r);
   }

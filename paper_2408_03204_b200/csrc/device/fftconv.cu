@@ -306,7 +306,7 @@ __device__ __forceinline__ CT zmix(CT xk, CT xm, CT pk, CT pm, RealOf<CT> s) {
   // xm = conj(X[N-k]), pm = conj(P[N-k]):  Z = ((xk+xm)(pk+pm) - i (xk-xm)(pk-pm)) / 4
   const CT s1 = cmul(cadd(xk, xm), cadd(pk, pm));
   const CT s2 = cmul(csub(xk, xm), csub(pk, pm));
-  return Cx<CT>::mk((s1.x + s2.y) * s, (s1.y - s2.x) * s);
+  return cscale(cadd(s1, Cx<CT>::mk(s2.y, -s2.x)), s);
 }
 
 // Threads = radix-16 butterflies of the first pass (COUNT rows of 2^LN2 points), so no

@@ -46,6 +46,11 @@ constexpr int kDynTile = kDynThreads * kDynPerThread;
 std::size_t dyn_sync_bytes(int slots, int batch, long length);
 void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double energy_floor, void* sync,
                      bool zero_sync, cudaStream_t s, const PwEpi& epi = {});
+// Steps with a full wave of dense sequences run the streaming scan (one CTA per sequence, no
+// look-back); set_dyn_stream(0) forces the chained scan, 1 the streaming one where legal
+// (dense, L % 4 == 0), -1 automatic (tests).
+bool dyn_stream_ok(const StepArgs& a);
+void set_dyn_stream(int mode);
 
 // Backward of a compressor / noisegate step: `bw` gathers dy over the consumers' input
 // gradients (transposed CSR) and stores du into bw.dst; parameter gradients [slots][4] fp64

@@ -140,6 +140,9 @@ class DevicePlan {
   // Workspace for a forward render followed by backward_arena (forward layout + scratch).
   std::size_t backward_workspace_bytes(int batch, long length, const ProcessorSet& procs) const;
   int kernels_per_render(int batch, long length) const;
+  // owner[k] = the step whose launch computes step k: k itself, the head of its pointwise
+  // chain, or the producer whose epilogue computes it (render_arena without per-step events).
+  void step_owners(int batch, long length, int* owner) const;
 
   // Workspace: one persistent region per step for its parameter-only prologue, the steps'
   // synchronisation words, then one transient region shared by every step's audio pass.

@@ -569,3 +569,64 @@ def test_fp64_transforms_config2(mg, ref):
     finally:
         mg.set_fft_precision(32)
     assert rel(y, want) < TOL
+
+
+def test_step_owners_and_serialized_render(mg, ref):
+    # step_owners: which launch computes each step (measurement attribution). A serialised
+    # render (render_profiled(hoist=False) without step times: prologues inline, no side
+    # streams) runs the same kernels, so its arena equals the overlapped render's bit for bit.
+    import torch
+    from paper_2408_03204_b200.device import DeviceRenderer
+    t, e = ref.console(6, 0.3, 5)
+    params = ref.random_legal_params(t, e, 9)
+    rd = mg.compute_render_data(make(mg, t, e))
+    L = 20000
+    own = rd.step_owners(1, L)
+    assert len(own) == rd.num_steps
+    for k, o in enumerate(own):
+        assert 0 <= o <= k and own[o] == o
+        if o != k:  # followers are pointwise types
+            assert int(rd.steps[k].type) in (1, 2, 3, 7)
+    types = [int(st.type) for st in rd.steps]
+    gate = types.index(6)
+    assert own[gate + 1] == gate  # the per-track imager rides in the noisegate scan's epilogue
+    procs = mg.ProcessorSet()
+    src = np.random.default_rng(4).uniform(-1, 1, size=(rd.num_inputs, 1, 2, L))
+    dr = DeviceRenderer(rd, procs, 1, L, rd.reorder_params(params))
+    dr.sources.copy_(torch.as_tensor(src, dtype=torch.float32))
+    dr.render()
+    a = dr.arena.clone()
+    dr.arena[rd.num_inputs:].fill_(float("nan"))
+    dr.render_profiled(hoist=False)
+    torch.cuda.synchronize()
+    assert torch.equal(a.view(torch.int32), dr.arena.view(torch.int32))
+
+
+@pytest.mark.parametrize("taps,L", [(None, 70000), (4096, 20000), (4097, 20000), (4096, 12)])
+def test_streaming_scan_matches_reference(mg, ref, taps, L):
+    # The compressor / noisegate scan forced onto the streaming kernel (one CTA per sequence,
+    # bulk-copy ring, running carry) and onto the chained look-back scan: both match the
+    # reference, and each other to fp64 rounding of the envelope. envelope_taps < L exercises
+    # the a^Ne correction (4097: its unaligned re-gather); L = 12: one partial tile.
+    rng = np.random.default_rng(L + (taps or 0))
+    slots, batch = 5, 2
+    x = rng.uniform(-1, 1, size=(slots, batch, 2, L)) * np.linspace(0.01, 1, L)
+    cfg = {} if taps is None else {"envelope_taps": taps}
+    for t in (5, 6):
+        g = mg.Graph()
+        for _ in range(slots):
+            g.add_node(t)
+        gt, ge = g.arrays()
+        params = ref.random_legal_params(gt, ge, 77 + t)[t]
+        params[:, 0] = np.linspace(0.9, 0.9999, slots)
+        procs = mg.ProcessorSet(sample_rate=44100.0, **cfg)
+        want = ref.process(t, x, slots, batch, L, params, 0, **cfg)
+        got = {}
+        for mode in (1, 0):
+            mg.set_dyn_stream(mode)
+            try:
+                got[mode] = procs.process(t, x, slots, batch, L, params, 0)
+            finally:
+                mg.set_dyn_stream(-1)
+            assert rel(got[mode], want) < TOL, (t, mode)
+        assert rel(got[1], got[0]) < 1e-5
