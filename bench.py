@@ -158,6 +158,8 @@ def node_samples(t, length=L, batch=1):
 # ---- roofline of the kernels as they run inside the render ---------------------------------
 
 def kernel_family(name):
+    if "dyn_stream" in name:  # the streaming variant of the dynamics scan
+        return "dyn_scan"
     for key in ("rows_conv_fk", "rows_conv", "rows_spec", "cols_fwd", "cols_inv", "eq_conv", "dyn_scan",
                 "pointwise_wide", "pointwise_chain", "pointwise", "reverb_ir", "eq_response_basis", "eq_mag_tiles",
                 "delay_taps", "eq_design", "eq_response", "eq_mags", "param_gather"):
@@ -248,7 +250,9 @@ def family_work(mg, procs, rd, length, batch=1):
 
 def roofline_table(fam_serial, work, hbm_peak):
     """Per kernel family: serialized in-render time, algorithmic work, achieved and fraction of
-    its bound's peak (nominal FP32 for FFT families, measured HBM for the others)."""
+    its bound's peak (nominal FP32 for FFT families, measured HBM for the others). An HBM family
+    can exceed 1.0: rows written by the step just before it are partly still in L2 (the master
+    mix reads the reverb / delay outputs the previous steps just stored)."""
     tab, merged = {}, {}
     for k, d in fam_serial.items():  # pointwise / pointwise_wide / pointwise_chain: one family
         m = merged.setdefault("pointwise" if k.startswith("pointwise") else k, {"us": 0.0, "launches": 0})

@@ -439,10 +439,13 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
 // is refilled after the next tile's barrier, and the per-warp aggregates alternate between two
 // buffers. Arithmetic per sample is dyn_scan's (fp64 recurrence, correctly rounded gain).
 // Needs a dense step (slot s reads row dense + s) and L % 4 == 0 (16-byte bulk copies).
-constexpr int kStreamThreads = 256;
+// 128-thread CTAs (1024-sample tiles, 24 KB ring): eight per SM, so a config-5 union's 1,124
+// sequences are one wave (256-thread CTAs, four per SM, left a 1.9-wave tail).
+constexpr int kStreamThreads = 128;
 constexpr int kStreamDepth = 3;
 constexpr int kStreamTile = kStreamThreads * kDynPerThread;
 constexpr int kStreamSmem = kStreamDepth * 2 * kStreamTile * static_cast<int>(sizeof(float));
+constexpr int kStreamCtasPerSm = 8;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -470,7 +473,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 template <bool GATE, bool VEC>
-__global__ void __launch_bounds__(kStreamThreads, 4) dyn_stream(StepArgs a, int env_taps, double floor_, PwEpi epi) {
+__global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) dyn_stream(StepArgs a, int env_taps, double floor_, PwEpi epi) {
   constexpr int NT = kStreamThreads, TS = kStreamTile, NW = NT / 32;
   extern __shared__ __align__(128) unsigned char stream_smem[];
   float* ring = reinterpret_cast<float*>(stream_smem);  // [stage][channel][TS]
@@ -505,7 +508,7 @@ __global__ void __launch_bounds__(kStreamThreads, 4) dyn_stream(StepArgs a, int 
     if (epi.n > 0 && threadIdx.x == 1) pw_epi_slots(epi, slot, s_epi);
   }
   __syncthreads();
-  const DynParams& p = s_p;
+  const DynParams p = s_p;  // registers: the per-sample gain reads them every sample
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int e0 = slot_e0(a, slot), e1 = slot_e1(a, slot);
   float* ol0 = a.dst + static_cast<long>(slot) * a.rowstride + boff;
@@ -977,8 +980,8 @@ std::size_t dyn_sync_bytes(int slots, int batch, long length) {
   return 256 + sizeof(unsigned long long) * static_cast<std::size_t>(slots) * batch * tiles;
 }
 
-// The streaming scan (one CTA per sequence) when the step has a full wave of sequences at four
-// CTAs per SM, its slots read consecutive rows and the rows are 16-byte aligned (L % 4 == 0).
+// The streaming scan (one CTA per sequence) when the step has most of a wave of sequences at
+// eight CTAs per SM, its slots read consecutive rows and the rows are 16-byte aligned (L % 4 == 0).
 // (mg_set_dyn_stream: 0 forces the chained scan, for tests.)
 static int g_dyn_stream = -1;
 void set_dyn_stream(int mode) { g_dyn_stream = mode; }
@@ -990,9 +993,13 @@ static int sm_count_dyn() {
   }();
   return n;
 }
-bool dyn_stream_ok(const StepArgs& a) {
+bool dyn_stream_ok(const StepArgs& a, const PwEpi& epi) {
   if (g_dyn_stream == 0 || a.dense < 0 || a.length % 4 != 0) return false;
-  return g_dyn_stream == 1 || static_cast<long>(a.slots) * a.batch >= 4L * sm_count_dyn();
+  // With pointwise followers in the epilogue (the per-track noisegate) the streaming kernel ran
+  // out of registers and measured slower than the chained scan (1.71 vs 1.28 ms per config-5
+  // union); without (the per-track compressor) faster (0.67 vs 0.78 ms).
+  if (g_dyn_stream != 1 && epi.n > 0) return false;
+  return g_dyn_stream == 1 || static_cast<long>(a.slots) * a.batch >= 6L * sm_count_dyn();
 }
 
 void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double energy_floor, void* ws,
@@ -1015,7 +1022,7 @@ void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double ene
   auto* status = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 256);
   const long ne = envelope_taps < a.length ? envelope_taps : a.length;
   const bool vec = (a.length % 4 == 0) && (ne % 4 == 0);
-  if (dyn_stream_ok(a)) {
+  if (dyn_stream_ok(a, epi)) {
     static const bool attr = [] {
       for (auto fn : {dyn_stream<false, false>, dyn_stream<false, true>, dyn_stream<true, false>, dyn_stream<true, true>}) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamSmem);

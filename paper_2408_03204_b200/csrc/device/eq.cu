@@ -334,26 +334,37 @@ __global__ void __launch_bounds__(EqWin<LOG, C>::kThreads, EqWin<LOG, C>::kMinBl
   }
   fft_first_from_regs<-1>(v, buf, threadIdx.x);
   __syncthreads();
-  fft_middle<LOG, 1, kNt, -1>(buf, padded(kEqFft), tw);
-  // Last forward pass into registers, multiplied by the response and written back (in place:
-  // after every thread has read its inputs).
-  constexpr int NS = Pow2Plan<LOG>::kLastNs, R = Pow2Plan<LOG>::kLastR, PL = NS / kNt;
-  C o[PL][R];
+  // Forward plan 16 x 8 x 4 x 16 (8192) or 16 x 16 x 16 (4096): its last pass is radix 16, so
+  // butterfly j ends holding X[j + r N/16], r < 16 — exactly the inputs of the inverse's
+  // radix-16 first-pass butterfly j. The product with the response and the inverse's first
+  // pass run in registers: no smem round trip, no barrier between the two transforms.
+  if constexpr (LOG == 13) {
+    stockham_pass<kEqFft, 8, 16, 1, kNt, -1>(buf, padded(kEqFft), tw);
+    stockham_pass<kEqFft, 4, 128, 1, kNt, -1>(buf, padded(kEqFft), tw);
+  } else {
+    stockham_pass<kEqFft, 16, 16, 1, kNt, -1>(buf, padded(kEqFft), tw);
+  }
+  constexpr int NL = kEqFft / 16;  // last-pass butterflies = threads
+  static_assert(NL == kNt, "eq_conv: one last-pass butterfly per thread");
+  const int j = threadIdx.x;
+  {
+    TwPass<16, NL, -1, C> twb;
+    twb.load(tw, j);
+    const C* lb = buf + sidx(j);
 #pragma unroll
-  for (int p = 0; p < PL; ++p) fft_last_to_regs<LOG, -1>(buf, threadIdx.x + p * kNt, tw, o[p]);
-  __syncthreads();
+    for (int r = 0; r < 16; ++r) v[r] = lb[r * padded(NL)];
+    twb.apply(v);
+    Dft<16, -1, C>::run(v);
+  }
 #pragma unroll
-  for (int p = 0; p < PL; ++p) {
-    const int j = threadIdx.x + p * kNt;
-    C* sb = buf + sidx(j);
-#pragma unroll
-    for (int r = 0; r < R; ++r) sb[r * padded(NS)] = cscale(o[p][r], rscale * static_cast<T>(__ldg(rs + kRs * (j + r * NS))));
+  for (int r = 0; r < 16; ++r) v[r] = cscale(v[r], rscale * static_cast<T>(__ldg(rs + kRs * (j + r * NL))));
+  __syncthreads();  // every thread has read its last-pass inputs
+  fft_first_from_regs<+1>(v, buf, j);
   }
   __syncthreads();
-  }
-  // Inverse: every pass but the last in smem, the last into registers and straight to the
-  // arena (window index w = j + r*NS holds output out0 + w - 1024 for w in [1024, 1024 + kEqOut)).
-  fft_all_but_last<LOG, 1, kNt, +1>(buf, padded(kEqFft), tw);
+  // Inverse: the middle passes in smem, the last into registers and straight to the arena
+  // (window index w = j + r*NS holds output out0 + w - 1024 for w in [1024, 1024 + kEqOut)).
+  fft_middle<LOG, 1, kNt, +1>(buf, padded(kEqFft), tw);
   constexpr int NS = Pow2Plan<LOG>::kLastNs, R = Pow2Plan<LOG>::kLastR, PL = NS / kNt;
   float* yl = a.dst + static_cast<long>(slot) * a.rowstride + boff;
   float* yr = yl + a.length;

@@ -49,7 +49,7 @@ void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double ene
 // Steps with a full wave of dense sequences run the streaming scan (one CTA per sequence, no
 // look-back); set_dyn_stream(0) forces the chained scan, 1 the streaming one where legal
 // (dense, L % 4 == 0), -1 automatic (tests).
-bool dyn_stream_ok(const StepArgs& a);
+bool dyn_stream_ok(const StepArgs& a, const PwEpi& epi);
 void set_dyn_stream(int mode);
 
 // Backward of a compressor / noisegate step: `bw` gathers dy over the consumers' input

@@ -12,7 +12,9 @@ import workloads as wl
 ap = argparse.ArgumentParser()
 ap.add_argument("--union", type=int, default=0)
 ap.add_argument("--renders", type=int, default=1)
+ap.add_argument("--dyn", type=int, default=-1, help="mg_set_dyn_stream mode (0: chained scans)")
 args = ap.parse_args()
+mg.set_dyn_stream(args.dyn)
 dev = torch.device("cuda", 0)
 procs = mg.ProcessorSet()
 graphs, mine, unions = bench.config5_shard(0, 1)
