@@ -13,6 +13,7 @@
 #include <deque>
 #include <functional>
 #include <thread>
+#include <unordered_map>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -411,6 +412,60 @@ void DevicePlan::build_index() {
     follow_off_[k] = static_cast<long>(host.size());
     host.insert(host.end(), map.begin(), map.end());
   }
+  // Shared signal spectra of adjacent long-convolution steps: slots with exactly one input edge
+  // reading the same row (and step k reading none of step k-1's outputs).
+  share_off_.assign(rd_.steps.size(), -1);
+  share_own_n_.assign(rd_.steps.size(), 0);
+  auto conv = [](NodeType t) { return t == NodeType::Reverb || t == NodeType::Delay; };
+  auto single_sources = [](const StepIndex& st) {
+    const int slots = st.store_end - st.store_begin;
+    std::vector<int> cnt(static_cast<std::size_t>(slots), 0), src(static_cast<std::size_t>(slots), -1);
+    for (std::size_t e = 0; e < st.gather.size(); ++e) {
+      ++cnt[static_cast<std::size_t>(st.aggregate[e])];
+      src[static_cast<std::size_t>(st.aggregate[e])] = st.gather[e];
+    }
+    for (int q = 0; q < slots; ++q) {
+      if (cnt[static_cast<std::size_t>(q)] != 1) src[static_cast<std::size_t>(q)] = -1;
+    }
+    return src;
+  };
+  for (std::size_t k = 1; k < rd_.steps.size(); ++k) {
+    const StepIndex& a = rd_.steps[k - 1];
+    const StepIndex& b = rd_.steps[k];
+    if (!conv(a.type) || !conv(b.type)) continue;
+    bool reads_a = false;
+    for (int g : b.gather) reads_a = reads_a || (g >= a.store_begin && g < a.store_end);
+    if (reads_a) continue;
+    std::unordered_map<int, int> slot_of;
+    const std::vector<int> sa = single_sources(a);
+    for (int q = 0; q < static_cast<int>(sa.size()); ++q) {
+      if (sa[static_cast<std::size_t>(q)] >= 0) slot_of.emplace(sa[static_cast<std::size_t>(q)], q);
+    }
+    const std::vector<int> sb = single_sources(b);
+    std::vector<int> map(sb.size(), -1), own;
+    for (int q = 0; q < static_cast<int>(sb.size()); ++q) {
+      const auto it = sb[static_cast<std::size_t>(q)] >= 0 ? slot_of.find(sb[static_cast<std::size_t>(q)]) : slot_of.end();
+      if (it != slot_of.end()) map[static_cast<std::size_t>(q)] = it->second;
+      else own.push_back(q);
+    }
+    if (own.size() == sb.size()) continue;
+    share_off_[k] = static_cast<long>(host.size());
+    share_own_n_[k] = static_cast<int>(own.size());
+    host.insert(host.end(), map.begin(), map.end());
+    host.insert(host.end(), own.begin(), own.end());
+  }
+}
+
+const int* DevicePlan::share_map(int step) const {
+  const long off = share_off_[static_cast<std::size_t>(step)];
+  return off < 0 ? nullptr : d_index_ + off;
+}
+
+const int* DevicePlan::share_own(int step) const {
+  const long off = share_off_[static_cast<std::size_t>(step)];
+  if (off < 0) return nullptr;
+  const StepIndex& st = rd_.steps[static_cast<std::size_t>(step)];
+  return d_index_ + off + (st.store_end - st.store_begin);
 }
 
 const int* DevicePlan::follow_map(int step) const {
@@ -479,6 +534,22 @@ bool pairable(const RenderData& rd, std::size_t k, long length, const ProcessorS
   }
   return true;
 }
+
+// Step k reuses step k-1's signal spectra (launch_conv_shared) when the plan found shared
+// sources and both steps use the same transform with the kernel rows fused into the row pass
+// (large steps: the rows kernel reads the other step's spectra).
+bool shareable(const DevicePlan& plan, std::size_t k, long length, const ProcessorSet& p) {
+  if (k == 0 || !plan.shares(static_cast<int>(k))) return false;
+  const RenderData& rd = plan.data();
+  long taps[2];
+  for (int i = 0; i < 2; ++i) {
+    const StepIndex& st = rd.steps[k - 1 + static_cast<std::size_t>(i)];
+    taps[i] = st.type == NodeType::Reverb ? p.reverb_length() : p.delay_span();
+    if (!mgb::conv_fuse_kernel_rows(mgb::conv_geom(length, taps[i]), st.store_end - st.store_begin)) return false;
+  }
+  const mgb::ConvGeom ga = mgb::conv_geom(length, taps[0]), gb = mgb::conv_geom(length, taps[1]);
+  return ga.log_n == gb.log_n && ga.log_n1 == gb.log_n1 && ga.seg == gb.seg && ga.nseg == gb.nseg && taps[0] == taps[1];
+}
 }  // namespace
 
 DevicePlan::Layout DevicePlan::layout(int batch, long length, const ProcessorSet& procs) const {
@@ -495,6 +566,17 @@ DevicePlan::Layout DevicePlan::layout(int batch, long length, const ProcessorSet
       }
     }
   }
+  l.shared.assign(rd_.steps.size(), 0);
+  for (std::size_t k = 1; k < rd_.steps.size(); ++k) {
+    if (shareable(*this, k, length, procs) && !l.paired[k - 1]) {
+      l.shared[k] = 1;
+      const StepIndex& a = rd_.steps[k - 1];
+      const StepIndex& b = rd_.steps[k];
+      const std::size_t ma = align256(main_bytes(a.type, a.store_end - a.store_begin, batch, length, procs));
+      l.share_off = std::max(l.share_off, ma);
+      main = std::max(main, ma + main_bytes(b.type, b.store_end - b.store_begin, batch, length, procs));
+    }
+  }
   for (const StepIndex& st : rd_.steps) {
     const int slots = st.store_end - st.store_begin;
     l.prologue_off.push_back(off);
@@ -508,6 +590,7 @@ DevicePlan::Layout DevicePlan::layout(int batch, long length, const ProcessorSet
   }
   l.sync_bytes = off - l.sync_begin;
   l.main_off = off;
+  l.share_off += off;
   l.main2_off = off + align256(main);
   l.total = l.main2_off + align256(main2);
   return l;
@@ -667,6 +750,21 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
       }
       cuda_check(cudaEventRecord(le[2 * k + 1], lane), "event");
       cuda_check(cudaStreamWaitEvent(stream, le[2 * k + 1], 0), "wait");
+      ++k;
+      continue;
+    }
+    if (!step_events && k + 1 < rd.steps.size() && lay.shared[k + 1]) {
+      // Steps k and k+1: long convolutions sharing the transforms of common source rows.
+      const std::size_t j = k + 1;
+      const long taps = t == NodeType::Reverb ? procs.reverb_length() : procs.delay_span();
+      if (!hoist) {
+        run_prologue(t, args[k], procs, ws + lay.prologue_off[k], stream);
+        run_prologue(rd.steps[j].type, args[j], procs, ws + lay.prologue_off[j], stream);
+      }
+      mgb::launch_conv_shared(args[k], args[j], taps, ws + lay.prologue_off[k], ws + lay.prologue_off[j],
+                              ws + lay.main_off, ws + lay.share_off, plan.share_map(static_cast<int>(j)),
+                              plan.share_own(static_cast<int>(j)), plan.share_own_count(static_cast<int>(j)), stream,
+                              hoist ? ev[k + 1] : nullptr, hoist ? ev[j + 1] : nullptr);
       ++k;
       continue;
     }

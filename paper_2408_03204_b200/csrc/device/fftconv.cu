@@ -72,9 +72,10 @@ struct SegArgs {
   int nseg;
   int item0;
   int mask_out;  // gather only the segment's own output samples (dY of the kernel gradient)
+  const int* slot_map = nullptr;  // signal column pass over a subset of slots: launch slot -> step slot
 };
-SegArgs seg_args(const ConvGeom& g, int item0 = 0, bool mask_out = false) {
-  return SegArgs{g.seg, g.pre, g.nseg, item0, mask_out ? 1 : 0};
+SegArgs seg_args(const ConvGeom& g, int item0 = 0, bool mask_out = false, const int* slot_map = nullptr) {
+  return SegArgs{g.seg, g.pre, g.nseg, item0, mask_out ? 1 : 0, slot_map};
 }
 __host__ __device__ __forceinline__ long seg_base(long seg, long pre, long j) {
   const long b = j * seg - pre;
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_fwd(StepArgs a, 
   const int log_n2 = log_n - LN1;
   const int N2 = 1 << log_n2;
   const int N = 1 << log_n;
-  const int item = sg.item0 + blockIdx.y;
+  int item = sg.item0 + blockIdx.y;
   const int col0 = blockIdx.x * C;
   const int c = threadIdx.x % C, jt = threadIdx.x / C;
   const int nstep = N >> 4;
@@ -112,6 +113,10 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_fwd(StepArgs a, 
     const int isb = item / sg.nseg, j = item - isb * sg.nseg;
     slot = isb / a.batch;
     b = isb - slot * a.batch;
+    if (sg.slot_map != nullptr) {  // a subset of the step's slots: store at the step's own item
+      slot = __ldg(sg.slot_map + slot);
+      item = (slot * a.batch + b) * sg.nseg + j;
+    }
     e0 = slot_e0(a, slot);
     e1 = slot_e1(a, slot);
     base = seg_base(sg.seg, sg.pre, j);
@@ -524,9 +529,12 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), kRconvThreadsPerSm / (s
 // K holds the kernel's COLUMN-stage output (cols_fwd<Kernel>, no rows_spec pass); each CTA
 // transforms the kernel rows ra / rb alongside the signal rows (4 transforms), so the kernel
 // spectrum never makes a round trip through memory. grid (N1/2 + 1, slots*B)
+// share (optional): per slot, the slot of Xalt's step whose signal spectrum this slot reuses
+// (same source row, same transform; -1: its own, in X). The output always goes to X.
 template <int LN2, typename CT>
 __global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_conv_fk(int log_n, int batch, CT* X, const CT* K,
-                                                                  const CT* tw, int item0) {
+                                                                  const CT* tw, int item0, const CT* Xalt,
+                                                                  const int* share) {
   using T = RealOf<CT>;
   constexpr int N2 = 1 << LN2;
   constexpr int NT = row_threads<LN2, 4>();
@@ -541,11 +549,21 @@ __global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_conv_fk(int log_n,
   const bool self = ra == rb;
   CT* xa = X + static_cast<long>(item) * N + static_cast<long>(ra) * N2;
   CT* xb = X + static_cast<long>(item) * N + static_cast<long>(rb) * N2;
+  const CT* xa_in = xa;
+  const CT* xb_in = xb;
+  if (share != nullptr) {
+    const int from = __ldg(share + slot);
+    if (from >= 0) {
+      const long alt = static_cast<long>(from) * batch + (item - slot * batch);
+      xa_in = Xalt + alt * N + static_cast<long>(ra) * N2;
+      xb_in = Xalt + alt * N + static_cast<long>(rb) * N2;
+    }
+  }
   const CT* ka = K + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
   const CT* kb_ = K + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
   constexpr bool REG = rows_reg<LN2, 4>();
   if constexpr (REG) {
-    rows_forward_from_global<LN2, 4, NT>(rows, RS, xa, xb, ka, kb_, tw);
+    rows_forward_from_global<LN2, 4, NT>(rows, RS, xa_in, xb_in, ka, kb_, tw);
   } else {
     constexpr int PER = (N2 + NT - 1) / NT;
     CT v[4][PER];
@@ -553,8 +571,8 @@ __global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_conv_fk(int log_n,
     for (int q = 0; q < PER; ++q) {
       const int i = threadIdx.x + q * NT;
       if (N2 % NT == 0 || i < N2) {
-        v[0][q] = xa[i];
-        v[1][q] = xb[i];
+        v[0][q] = xa_in[i];
+        v[1][q] = xb_in[i];
         v[2][q] = __ldg(ka + i);
         v[3][q] = __ldg(kb_ + i);
       }
@@ -620,7 +638,7 @@ template <> const double2* tw_table<double2>(const StepArgs& a) { return a.tw64;
 
 template <int LN1, typename CT>
 void cols_fwd_t(ColSrc src, const StepArgs& a, const float2* ir, long taps, const ConvGeom& g, int items,
-                CT* out, int window, bool mask_out, cudaStream_t s) {
+                CT* out, int window, bool mask_out, cudaStream_t s, const int* slot_map = nullptr) {
   constexpr int C = ColCfg<CT>::kElems / (1 << LN1);
   constexpr int smem = ColCfg<CT>::kSmem(1 << LN1);
   static const bool attrs_set = [] {
@@ -638,7 +656,7 @@ void cols_fwd_t(ColSrc src, const StepArgs& a, const float2* ir, long taps, cons
   constexpr int nt = ColCfg<CT>::kThreads;
   for_item_chunks(items, [&](int i0, int n) {
     const dim3 grid(static_cast<unsigned>((1L << g.log_n2) / C), static_cast<unsigned>(n));
-    const SegArgs sg = seg_args(g, i0, mask_out);
+    const SegArgs sg = seg_args(g, i0, mask_out, slot_map);
     if (src == ColSrc::Signal) {
       cols_fwd<LN1, ColSrc::Signal, CT><<<grid, nt, smem, s>>>(a, ir, taps, g.log_n, out, window, sg);
     } else if (src == ColSrc::DelayTaps) {
@@ -700,7 +718,8 @@ void rows_conv_t(const ConvGeom& g, int items, int per_slot, CT* X, const CT* P,
 }
 
 template <int LN2, typename CT>
-void rows_conv_fk_t(const ConvGeom& g, int items, int per_slot, CT* X, const CT* K, const CT* tw, cudaStream_t s) {
+void rows_conv_fk_t(const ConvGeom& g, int items, int per_slot, CT* X, const CT* K, const CT* tw, cudaStream_t s,
+                    const CT* Xalt = nullptr, const int* share = nullptr) {
   constexpr int smem = 4 * padded(1 << LN2) * static_cast<int>(sizeof(CT));
   static const bool done = [] {
     cudaFuncSetAttribute(rows_conv_fk<LN2, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -709,7 +728,7 @@ void rows_conv_fk_t(const ConvGeom& g, int items, int per_slot, CT* X, const CT*
   (void)done;
   for_item_chunks(items, [&](int i0, int n) {
     const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(n));
-    rows_conv_fk<LN2, CT><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, per_slot, X, K, tw, i0);
+    rows_conv_fk<LN2, CT><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, per_slot, X, K, tw, i0, Xalt, share);
   });
 }
 
@@ -1352,6 +1371,33 @@ void conv_main(const StepArgs& a, long taps, const void* prologue_ws, void* ws, 
   MGB_DISPATCH_LN(g.log_n1, cols_inv_t, CT, a, g, X, false, s);
 }
 
+// Adjacent long-convolution steps A, B whose slots read the same source rows (a console
+// track's gain feeds both its delay and its reverb send): B's slots listed in `share` reuse A's
+// signal spectrum instead of transforming the same row again. A's column pass, B's column pass
+// over its own slots only, B's rows (reading A's spectra where shared, writing its own buffer),
+// then A's rows in place (after B has read them), then both inverse column passes.
+template <typename CT>
+void conv_shared(const StepArgs& a, const StepArgs& b, long taps, const void* pws_a, const void* pws_b, void* ws_a,
+                 void* ws_b, const int* share, const int* own, int n_own, cudaStream_t s, cudaEvent_t ready_a,
+                 cudaEvent_t ready_b) {
+  const ConvGeom g = conv_geom(a.length, taps);
+  const auto* Pa = reinterpret_cast<const CT*>(static_cast<const char*>(pws_a) + ir_bytes(a.slots, taps));
+  const auto* Pb = reinterpret_cast<const CT*>(static_cast<const char*>(pws_b) + ir_bytes(b.slots, taps));
+  auto* Xa = static_cast<CT*>(ws_a);
+  auto* Xb = static_cast<CT*>(ws_b);
+  const int per_slot = a.batch * g.nseg;
+  MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, CT, ColSrc::Signal, a, nullptr, 0, g, a.slots * per_slot, Xa, 0, false, s);
+  if (n_own > 0) {
+    MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, CT, ColSrc::Signal, b, nullptr, 0, g, n_own * per_slot, Xb, 0, false, s, own);
+  }
+  if (ready_b) cudaStreamWaitEvent(s, ready_b, 0);
+  MGB_DISPATCH_LN(g.log_n2, rows_conv_fk_t, CT, g, b.slots * per_slot, per_slot, Xb, Pb, tw_table<CT>(b), s, Xa, share);
+  if (ready_a) cudaStreamWaitEvent(s, ready_a, 0);
+  MGB_DISPATCH_LN(g.log_n2, rows_conv_fk_t, CT, g, a.slots * per_slot, per_slot, Xa, Pa, tw_table<CT>(a), s);
+  MGB_DISPATCH_LN(g.log_n1, cols_inv_t, CT, a, g, Xa, false, s);
+  MGB_DISPATCH_LN(g.log_n1, cols_inv_t, CT, b, g, Xb, false, s);
+}
+
 template <int LN2, typename CT>
 void rows_bwd_t(const ConvGeom& g, int slots, int per_slot, CT* DY, CT* X, const CT* P, bool kfft, const CT* tw,
                 cudaStream_t s) {
@@ -1440,6 +1486,16 @@ void launch_conv_prologue(bool reverb, const StepArgs& a, const ReverbConst& rc,
   if (a.slots == 0) return;
   if (fft_fp64()) conv_prologue<double2>(reverb, a, rc, dc, ws, s);
   else conv_prologue<float2>(reverb, a, rc, dc, ws, s);
+}
+
+void launch_conv_shared(const StepArgs& a, const StepArgs& b, long taps, const void* pws_a, const void* pws_b,
+                        void* ws_a, void* ws_b, const int* share, const int* own, int n_own, cudaStream_t s,
+                        cudaEvent_t ready_a, cudaEvent_t ready_b) {
+  if (fft_fp64()) {
+    conv_shared<double2>(a, b, taps, pws_a, pws_b, ws_a, ws_b, share, own, n_own, s, ready_a, ready_b);
+  } else {
+    conv_shared<float2>(a, b, taps, pws_a, pws_b, ws_a, ws_b, share, own, n_own, s, ready_a, ready_b);
+  }
 }
 
 void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, void* ws, cudaStream_t s,

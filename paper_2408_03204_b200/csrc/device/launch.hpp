@@ -108,6 +108,14 @@ void launch_conv_prologue(bool reverb, const StepArgs& a, const ReverbConst& rc,
 void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, void* ws, cudaStream_t s,
                       cudaEvent_t kernel_ready = nullptr);
 
+// Two adjacent conv steps with the same transform (conv_fuse_kernel_rows for both) where B's
+// slots listed in `share` (per B slot: the A slot reading the same single source row, or -1)
+// reuse A's signal spectrum; `own` lists the n_own B slots that transform their own input.
+// ws_a / ws_b: conv_main_bytes each, both live until the call's kernels finish.
+void launch_conv_shared(const StepArgs& a, const StepArgs& b, long taps, const void* pws_a, const void* pws_b,
+                        void* ws_a, void* ws_b, const int* share, const int* own, int n_own, cudaStream_t s,
+                        cudaEvent_t ready_a, cudaEvent_t ready_b);
+
 // Backward of a reverb / delay step: dX = correlation with the kernel (stored into bw.dst),
 // kernel gradient = correlation of dY with X, then through the IR build / tap FIRs into
 // `grad` ([slots][768] / [slots][880] fp64). prologue_ws: the forward's prologue region.

@@ -136,6 +136,14 @@ class DevicePlan {
   // slots to step k's slots (device); nullptr otherwise.
   bool follows(int step) const { return follow_off_[static_cast<std::size_t>(step)] >= 0; }
   const int* follow_map(int step) const;
+  // Step k (k >= 1) and step k-1 are long convolutions and some of step k's slots read the same
+  // single source row as a slot of step k-1 (a console track's delay and reverb sends):
+  // share_map(k)[s] = that slot of step k-1 or -1 (device), share_own(k) = the n_own(k) slots
+  // of step k with no such partner (device). shares(k) is false when no slot matches.
+  bool shares(int step) const { return share_off_[static_cast<std::size_t>(step)] >= 0; }
+  const int* share_map(int step) const;
+  const int* share_own(int step) const;
+  int share_own_count(int step) const { return share_own_n_[static_cast<std::size_t>(step)]; }
   std::size_t workspace_bytes(int batch, long length, const ProcessorSet& procs) const;
   // Workspace for a forward render followed by backward_arena (forward layout + scratch).
   std::size_t backward_workspace_bytes(int batch, long length, const ProcessorSet& procs) const;
@@ -153,6 +161,8 @@ class DevicePlan {
     std::size_t main_off = 0;
     std::size_t main2_off = 0;  // second transient region (a step run concurrently with its predecessor)
     std::vector<char> paired;   // paired[k]: step k runs on the lane beside step k + 1
+    std::vector<char> shared;   // shared[k]: step k reuses step k-1's signal spectra (launch_conv_shared)
+    std::size_t share_off = 0;  // step k's transient region when shared[k] (after step k-1's)
     std::size_t total = 0;
   };
   Layout layout(int batch, long length, const ProcessorSet& procs) const;
@@ -173,7 +183,8 @@ class DevicePlan {
   const cudaEvent_t* borrowed_events_ = nullptr;
   const int* d_index_ = nullptr;
   std::vector<int> host_;
-  std::vector<long> rp_off_, col_off_, trp_off_, tcol_off_, follow_off_;
+  std::vector<long> rp_off_, col_off_, trp_off_, tcol_off_, follow_off_, share_off_;
+  std::vector<int> share_own_n_;
   std::vector<int> zero_rows_;
   std::vector<int> dense_;
 };

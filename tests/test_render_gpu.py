@@ -630,3 +630,40 @@ def test_streaming_scan_matches_reference(mg, ref, taps, L):
                 mg.set_dyn_stream(-1)
             assert rel(got[mode], want) < TOL, (t, mode)
         assert rel(got[1], got[0]) < 1e-5
+
+
+@pytest.mark.parametrize("prune,L,batch", [(0.0, 20000, 1), (0.4, 9000, 2)])
+def test_shared_signal_spectra_bit_exact(mg, ref, prune, L, batch):
+    # A console track's gain feeds its delay and its reverb: with the kernel rows fused into the
+    # row pass (forced here; automatic for config-5-sized steps), the second conv step reuses
+    # the first one's signal spectra for those tracks (launch_conv_shared). render_profiled()
+    # runs every step on its own (no sharing): the arenas must be bit-identical.
+    import torch
+    from paper_2408_03204_b200.device import DeviceRenderer
+    t, e = ref.console(6, prune, 11)
+    params = ref.random_legal_params(t, e, 12)
+    rd = mg.compute_render_data(make(mg, t, e))
+    types = [int(st.type) for st in rd.steps]
+    k = next(i for i in range(1, len(types)) if {types[i - 1], types[i]} == {8, 9})
+    assert k > 0
+    procs = mg.ProcessorSet()
+    src = np.random.default_rng(5).uniform(-1, 1, size=(rd.num_inputs, batch, 2, L))
+    mg.set_conv_fuse(1)
+    try:
+        dr = DeviceRenderer(rd, procs, batch, L, rd.reorder_params(params))
+        dr.sources.copy_(torch.as_tensor(src, dtype=torch.float32))
+        dr.render()
+        shared = dr.arena.clone()
+        dr.arena[rd.num_inputs:].fill_(float("nan"))
+        dr.render_profiled(sync=True)
+        torch.cuda.synchronize()
+        assert torch.equal(shared.view(torch.int32), dr.arena.view(torch.int32))
+        g = dr.capture()
+        dr.arena[rd.num_inputs:].fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(shared.view(torch.int32), dr.arena.view(torch.int32))
+    finally:
+        mg.set_conv_fuse(-1)
+    want = ref.Plan(t, e, 1).render(params, src)
+    assert rel(shared[rd.output_begin:].cpu().numpy(), want) < TOL
