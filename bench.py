@@ -160,6 +160,8 @@ def node_samples(t, length=L, batch=1):
 def kernel_family(name):
     if "dyn_stream" in name:  # the streaming variant of the dynamics scan
         return "dyn_scan"
+    if "rows_conv_pair" in name:  # row passes of delay / reverb items sharing a signal spectrum
+        return "rows_conv_fk"
     for key in ("rows_conv_fk", "rows_conv", "rows_spec", "cols_fwd", "cols_inv", "eq_conv", "dyn_scan",
                 "pointwise_wide", "pointwise_chain", "pointwise", "reverb_ir", "eq_response_basis", "eq_mag_tiles",
                 "delay_taps", "eq_design", "eq_response", "eq_mags", "param_gather"):
@@ -198,7 +200,8 @@ def family_work(mg, procs, rd, length, batch=1):
     once, 8 B per stereo sample; a scan step's fused pointwise followers are counted with the
     pointwise family).
       reverb / delay, per (slot, batch, segment) item of the N = N1 N2 segmented transform:
-        cols_fwd  column halves of the signal forward and of the kernel spectrum (per slot)
+        cols_fwd  column halves of the signal forward (not for items reusing the previous
+                  step's spectrum, rd.shared_pairs) and of the kernel spectrum (per slot)
         rows_conv row halves of the forward and inverse + product (rows_conv_fk: + the kernel's
                   row half per item; otherwise rows_spec does it once per slot)
         cols_inv  column half of the inverse
@@ -214,6 +217,7 @@ def family_work(mg, procs, rd, length, batch=1):
 
     nsm = 148
     owner = rd.step_owners(batch, length)
+    pairs = rd.shared_pairs(procs, batch, length)
     fam_of = {mg.NodeType.COMPRESSOR: "dyn_scan", mg.NodeType.NOISEGATE: "dyn_scan"}
     for k, st in enumerate(rd.steps):
         slots = st.store_end - st.store_begin
@@ -228,11 +232,14 @@ def family_work(mg, procs, rd, length, batch=1):
             taps = procs.reverb_length if t == mg.NodeType.REVERB else procs.delay_span
             g = mg.conv_geometry(length, taps)
             n, l1, l2 = 1 << g["log_n"], g["log_n1"], g["log_n2"]
-            items = slots * batch * g["nseg"]
-            add("cols_fwd", "fp32", (items + slots) * 5.0 * n * l1)
+            per = batch * g["nseg"]
+            items = slots * per
+            shared = int(pairs[k]) * per  # items reusing step k-1's signal spectra
+            add("cols_fwd", "fp32", (items - shared + slots) * 5.0 * n * l1)
             add("cols_inv", "fp32", items * 5.0 * n * l1)
             if 8.0 * slots * n > (64 << 20):  # conv_fuse: kernel rows transformed per item
-                add("rows_conv_fk", "fp32", items * (3 * 5.0 * n * l2 + 16.0 * n))
+                # a shared pair (this item + its partner in step k-1) runs 5 row transforms, not 6
+                add("rows_conv_fk", "fp32", items * (3 * 5.0 * n * l2 + 16.0 * n) - shared * 5.0 * n * l2)
             else:
                 add("rows_spec", "fp32", slots * 5.0 * n * l2)
                 add("rows_conv", "fp32", items * (2 * 5.0 * n * l2 + 16.0 * n))

@@ -101,6 +101,12 @@ int32_t mg_plan_kernel_count(const mg_plan* plan, int32_t batch, int64_t length,
  * step whose epilogue computes it (measurement: per-kernel attribution of the render's work).
  * No reference counterpart (the reference runs one step at a time, render.cpp:40-80). */
 int32_t mg_plan_step_owners(const mg_plan* plan, int32_t batch, int64_t length, int32_t* owner);
+/* pairs[k] (num_steps entries) = the number of step k's slots that reuse the signal spectrum of a
+ * slot of step k-1 in a render with these processors / batch / length (adjacent delay and
+ * reverb steps on common source rows; 0 = step k transforms all its inputs). Measurement and
+ * tests; no reference counterpart (the reference transforms every input, dsp.cpp:64-86). */
+int32_t mg_plan_shared_pairs(const mg_plan* plan, const mg_processors* procs, int32_t batch, int64_t length,
+                             int32_t* pairs);
 int32_t mg_render_arena(const mg_plan* plan, const mg_processors* procs, const double* const* d_tables, float* d_arena,
                         int32_t batch, int64_t length, void* d_workspace, uint64_t workspace_bytes, void* stream);
 

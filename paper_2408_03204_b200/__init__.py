@@ -70,6 +70,7 @@ _sig("mg_render", _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i64, _dbl, _vp, _v
 _sig("mg_plan_workspace_bytes", _i32, _vp, _vp, _i32, _i64, _P(_u64))
 _sig("mg_plan_kernel_count", _i32, _vp, _i32, _i64, _P(_i32))
 _sig("mg_plan_step_owners", _i32, _vp, _i32, _i64, _vp)
+_sig("mg_plan_shared_pairs", _i32, _vp, _vp, _i32, _i64, _vp)
 _sig("mg_render_arena", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp)
 _sig("mg_render_arena_profiled", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp, _vp, _i32)
 _sig("mg_profile_steps", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp, _i32, _vp)
@@ -443,6 +444,14 @@ class RenderData:
         c = _i32()
         _check(_lib.mg_plan_kernel_count(self._h, batch, length, ctypes.byref(c)))
         return int(c.value)
+
+    def shared_pairs(self, procs: "ProcessorSet", batch: int, length: int) -> np.ndarray:
+        """pairs[k] = slots of step k reusing a signal spectrum of step k-1 in a render with
+        these processors / batch / length (adjacent delay / reverb sends of the same tracks);
+        mg_plan_shared_pairs."""
+        out = np.zeros(self.num_steps, dtype=np.int32)
+        _check(_lib.mg_plan_shared_pairs(self._h, procs.handle, batch, length, out.ctypes.data_as(_vp)))
+        return out
 
     def step_owners(self, batch: int, length: int) -> np.ndarray:
         """owner[k] = the step whose kernel launch computes step k (itself, the head of a fused

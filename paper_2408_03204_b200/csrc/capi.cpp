@@ -356,6 +356,17 @@ int32_t mg_plan_kernel_count(const mg_plan* p, int32_t batch, int64_t length, in
   return guarded([&] { *count = device_plan(p, nullptr).kernels_per_render(batch, static_cast<long>(length)); });
 }
 
+int32_t mg_plan_shared_pairs(const mg_plan* p, const mg_processors* procs, int32_t batch, int64_t length,
+                             int32_t* pairs) {
+  return guarded([&] {
+    const DevicePlan& dp = device_plan(p, procs);
+    const DevicePlan::Layout lay = dp.layout(batch, static_cast<long>(length), *procs->ps);
+    for (std::size_t k = 0; k < p->rd.steps.size(); ++k) {
+      pairs[k] = lay.shared[k] ? dp.share_info(static_cast<int>(k)).pairs : 0;
+    }
+  });
+}
+
 int32_t mg_plan_step_owners(const mg_plan* p, int32_t batch, int64_t length, int32_t* owner) {
   return guarded([&] { device_plan(p, nullptr).step_owners(batch, static_cast<long>(length), owner); });
 }

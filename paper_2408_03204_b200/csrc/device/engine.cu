@@ -414,8 +414,7 @@ void DevicePlan::build_index() {
   }
   // Shared signal spectra of adjacent long-convolution steps: slots with exactly one input edge
   // reading the same row (and step k reading none of step k-1's outputs).
-  share_off_.assign(rd_.steps.size(), -1);
-  share_own_n_.assign(rd_.steps.size(), 0);
+  share_.assign(rd_.steps.size(), Share{});
   auto conv = [](NodeType t) { return t == NodeType::Reverb || t == NodeType::Delay; };
   auto single_sources = [](const StepIndex& st) {
     const int slots = st.store_end - st.store_begin;
@@ -436,36 +435,42 @@ void DevicePlan::build_index() {
     bool reads_a = false;
     for (int g : b.gather) reads_a = reads_a || (g >= a.store_begin && g < a.store_end);
     if (reads_a) continue;
-    std::unordered_map<int, int> slot_of;
+    std::unordered_map<int, int> slot_of;  // source row -> unpaired slot of step k-1
     const std::vector<int> sa = single_sources(a);
     for (int q = 0; q < static_cast<int>(sa.size()); ++q) {
       if (sa[static_cast<std::size_t>(q)] >= 0) slot_of.emplace(sa[static_cast<std::size_t>(q)], q);
     }
     const std::vector<int> sb = single_sources(b);
-    std::vector<int> map(sb.size(), -1), own;
+    std::vector<int> pa, pb, own_b;
+    std::vector<char> paired_a(sa.size(), 0);
     for (int q = 0; q < static_cast<int>(sb.size()); ++q) {
       const auto it = sb[static_cast<std::size_t>(q)] >= 0 ? slot_of.find(sb[static_cast<std::size_t>(q)]) : slot_of.end();
-      if (it != slot_of.end()) map[static_cast<std::size_t>(q)] = it->second;
-      else own.push_back(q);
+      if (it != slot_of.end()) {
+        pa.push_back(it->second);
+        pb.push_back(q);
+        paired_a[static_cast<std::size_t>(it->second)] = 1;
+        slot_of.erase(it);
+      } else {
+        own_b.push_back(q);
+      }
     }
-    if (own.size() == sb.size()) continue;
-    share_off_[k] = static_cast<long>(host.size());
-    share_own_n_[k] = static_cast<int>(own.size());
-    host.insert(host.end(), map.begin(), map.end());
-    host.insert(host.end(), own.begin(), own.end());
+    if (pa.empty()) continue;
+    std::vector<int> own_a;
+    for (int q = 0; q < static_cast<int>(sa.size()); ++q) {
+      if (!paired_a[static_cast<std::size_t>(q)]) own_a.push_back(q);
+    }
+    Share& sh = share_[k];
+    sh.off = static_cast<long>(host.size());
+    sh.pairs = static_cast<int>(pa.size());
+    sh.own_prev = static_cast<int>(own_a.size());
+    sh.own = static_cast<int>(own_b.size());
+    for (const std::vector<int>* v : {&pa, &pb, &own_a, &own_b}) host.insert(host.end(), v->begin(), v->end());
   }
 }
 
-const int* DevicePlan::share_map(int step) const {
-  const long off = share_off_[static_cast<std::size_t>(step)];
+const int* DevicePlan::share_ints(int step) const {
+  const long off = share_[static_cast<std::size_t>(step)].off;
   return off < 0 ? nullptr : d_index_ + off;
-}
-
-const int* DevicePlan::share_own(int step) const {
-  const long off = share_off_[static_cast<std::size_t>(step)];
-  if (off < 0) return nullptr;
-  const StepIndex& st = rd_.steps[static_cast<std::size_t>(step)];
-  return d_index_ + off + (st.store_end - st.store_begin);
 }
 
 const int* DevicePlan::follow_map(int step) const {
@@ -761,10 +766,19 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
         run_prologue(t, args[k], procs, ws + lay.prologue_off[k], stream);
         run_prologue(rd.steps[j].type, args[j], procs, ws + lay.prologue_off[j], stream);
       }
+      const DevicePlan::Share& si = plan.share_info(static_cast<int>(j));
+      const int* ints = plan.share_ints(static_cast<int>(j));
+      mgb::ConvShare sh;
+      sh.pair_a = ints;
+      sh.pair_b = ints + si.pairs;
+      sh.own_a = ints + 2 * si.pairs;
+      sh.own_b = ints + 2 * si.pairs + si.own_prev;
+      sh.n_pairs = si.pairs;
+      sh.n_own_a = si.own_prev;
+      sh.n_own_b = si.own;
       mgb::launch_conv_shared(args[k], args[j], taps, ws + lay.prologue_off[k], ws + lay.prologue_off[j],
-                              ws + lay.main_off, ws + lay.share_off, plan.share_map(static_cast<int>(j)),
-                              plan.share_own(static_cast<int>(j)), plan.share_own_count(static_cast<int>(j)), stream,
-                              hoist ? ev[k + 1] : nullptr, hoist ? ev[j + 1] : nullptr);
+                              ws + lay.main_off, ws + lay.share_off, sh, stream, hoist ? ev[k + 1] : nullptr,
+                              hoist ? ev[j + 1] : nullptr);
       ++k;
       continue;
     }

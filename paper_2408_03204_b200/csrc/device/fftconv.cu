@@ -350,17 +350,19 @@ __device__ __forceinline__ void rows_forward_from_global(CT* rows, int RS, const
 // registers: output i of row w is scaled by the inverse four-step twiddle exp(+2 pi i r_w i / N)
 // (geometric in i = j + r*NS, exact anchors every 4) and stored to dst_w[i]; row b is skipped
 // when it is row a (self-paired rows). Half the threads per row, consecutive j per warp.
-template <int LN2, int NT, typename CT>
+// ROWS = 4: two such pairs (rows 2, 3 -> dc, dd at row indices ra, rb), a quarter of the threads each.
+template <int LN2, int NT, typename CT, int ROWS = 2>
 __device__ __forceinline__ void rows_inverse_to_global(CT* rows, int RS, int ra, int rb, bool self, CT* da,
-                                                       CT* db, RealOf<CT> inv_n, const CT* tw) {
+                                                       CT* db, RealOf<CT> inv_n, const CT* tw, CT* dc = nullptr,
+                                                       CT* dd = nullptr) {
   using T = RealOf<CT>;
-  fft_all_but_last<LN2, 2, NT, +1>(rows, RS, tw);
-  constexpr int NS = Pow2Plan<LN2>::kLastNs, R = Pow2Plan<LN2>::kLastR, HT = NT / 2;
+  fft_all_but_last<LN2, ROWS, NT, +1>(rows, RS, tw);
+  constexpr int NS = Pow2Plan<LN2>::kLastNs, R = Pow2Plan<LN2>::kLastR, HT = NT / ROWS;
   static_assert(NS % HT == 0, "rows_inverse_to_global: threads must tile the last pass");
   const int w = threadIdx.x / HT, jt = threadIdx.x - (threadIdx.x / HT) * HT;
-  if (w == 1 && self) return;
-  const int rw = w == 0 ? ra : rb;
-  CT* dst = w == 0 ? da : db;
+  if ((w & 1) && self) return;
+  const int rw = (w & 1) ? rb : ra;
+  CT* dst = w == 0 ? da : (w == 1 ? db : (w == 2 ? dc : dd));
   const CT step = expi_pi(static_cast<T>(static_cast<long>(rw) * NS) * inv_n);
 #pragma unroll
   for (int p = 0; p < NS / HT; ++p) {
@@ -529,12 +531,10 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), kRconvThreadsPerSm / (s
 // K holds the kernel's COLUMN-stage output (cols_fwd<Kernel>, no rows_spec pass); each CTA
 // transforms the kernel rows ra / rb alongside the signal rows (4 transforms), so the kernel
 // spectrum never makes a round trip through memory. grid (N1/2 + 1, slots*B)
-// share (optional): per slot, the slot of Xalt's step whose signal spectrum this slot reuses
-// (same source row, same transform; -1: its own, in X). The output always goes to X.
+// slot_map (optional): the launch covers a subset of the step's slots (launch slot -> slot).
 template <int LN2, typename CT>
 __global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_conv_fk(int log_n, int batch, CT* X, const CT* K,
-                                                                  const CT* tw, int item0, const CT* Xalt,
-                                                                  const int* share) {
+                                                                  const CT* tw, int item0, const int* slot_map) {
   using T = RealOf<CT>;
   constexpr int N2 = 1 << LN2;
   constexpr int NT = row_threads<LN2, 4>();
@@ -543,22 +543,19 @@ __global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_conv_fk(int log_n,
   CT* rows = reinterpret_cast<CT*>(smem_raw);  // [4][RS]: x a, x b, k a, k b
   const long N = 1L << log_n;
   const int N1 = static_cast<int>(N >> LN2);
-  const int item = item0 + blockIdx.y;
-  const int slot = item / batch;
+  int item = item0 + blockIdx.y;
+  int slot = item / batch;
+  if (slot_map != nullptr) {
+    const int sub = item - slot * batch;
+    slot = __ldg(slot_map + slot);
+    item = slot * batch + sub;
+  }
   const int ra = blockIdx.x, rb = (N1 - ra) & (N1 - 1);
   const bool self = ra == rb;
   CT* xa = X + static_cast<long>(item) * N + static_cast<long>(ra) * N2;
   CT* xb = X + static_cast<long>(item) * N + static_cast<long>(rb) * N2;
   const CT* xa_in = xa;
   const CT* xb_in = xb;
-  if (share != nullptr) {
-    const int from = __ldg(share + slot);
-    if (from >= 0) {
-      const long alt = static_cast<long>(from) * batch + (item - slot * batch);
-      xa_in = Xalt + alt * N + static_cast<long>(ra) * N2;
-      xb_in = Xalt + alt * N + static_cast<long>(rb) * N2;
-    }
-  }
   const CT* ka = K + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
   const CT* kb_ = K + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
   constexpr bool REG = rows_reg<LN2, 4>();
@@ -623,6 +620,91 @@ __global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_conv_fk(int log_n,
     xa[i] = cmul(rows[sidx(i)], expi_pi(static_cast<T>(static_cast<long>(ra) * i) * inv_n));
     if (!self) xb[i] = cmul(rows[RS + sidx(i)], expi_pi(static_cast<T>(static_cast<long>(rb) * i) * inv_n));
   }
+}
+
+// Two conv steps sharing a signal spectrum (launch_conv_shared): for pair p, step A's item
+// (slot pa[p]) and step B's item (slot pb[p]) convolve the same X (in Xa). One CTA per row pair
+// and item pair transforms the two X rows once and both kernels' rows (6 forward row FFTs
+// instead of 8), forms both channel-split products, inverts the 4 rows and stores A's result in
+// place into Xa (only this CTA reads these rows) and B's into Xb.
+template <int LN2>
+constexpr int pair_threads() {
+  constexpr int t = 6 * (1 << LN2) / 16;
+  return t <= 32 ? 32 : (t <= 64 ? 64 : (t <= 128 ? 128 : (t <= 256 ? 256 : (t <= 512 ? 512 : 1024))));
+}
+template <int LN2, typename CT>
+__global__ void __launch_bounds__(pair_threads<LN2>()) rows_conv_pair(int log_n, int batch, CT* Xa, CT* Xb,
+                                                                   const CT* Ka, const CT* Kb, const int* pa,
+                                                                   const int* pb, const CT* tw, int item0) {
+  using T = RealOf<CT>;
+  constexpr int N2 = 1 << LN2;
+  constexpr int NT = pair_threads<LN2>();
+  constexpr int RS = padded(N2);
+  constexpr int M1 = N2 / 16;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CT* rows = reinterpret_cast<CT*>(smem_raw);  // [6][RS]: x a, x b, kA a, kA b, kB a, kB b
+  const long N = 1L << log_n;
+  const int N1 = static_cast<int>(N >> LN2);
+  const int pi = item0 + blockIdx.y;
+  const int p = pi / batch, sub = pi - p * batch;
+  const int sa = __ldg(pa + p), sb = __ldg(pb + p);
+  const long ia = static_cast<long>(sa) * batch + sub, ib = static_cast<long>(sb) * batch + sub;
+  const int ra = blockIdx.x, rb = (N1 - ra) & (N1 - 1);
+  const bool self = ra == rb;
+  CT* xa = Xa + ia * N + static_cast<long>(ra) * N2;
+  CT* xb = Xa + ia * N + static_cast<long>(rb) * N2;
+  {
+    const int w = threadIdx.x / M1, j = threadIdx.x - (threadIdx.x / M1) * M1;
+    if (w < 6) {
+      const long r = (w & 1) ? rb : ra;
+      const CT* src = w < 2 ? Xa + ia * N : (w < 4 ? Ka + static_cast<long>(sa) * N : Kb + static_cast<long>(sb) * N);
+      src += r * N2;
+      CT v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = src[j + q * M1];
+      fft_first_from_regs<-1>(v, rows + w * RS, j);
+    }
+  }
+  __syncthreads();
+  fft_after_first<LN2, 6, NT, -1>(rows, RS, tw);
+  const T s = T(0.25) / static_cast<T>(N);
+  constexpr int KPT = (N2 + NT - 1) / NT;
+  CT zak[KPT], zao[KPT], zbk[KPT], zbo[KPT];
+#pragma unroll
+  for (int q = 0; q < KPT; ++q) {
+    const int k = threadIdx.x + q * NT;
+    if (k >= N2) continue;
+    const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
+    const CT xk = rows[sidx(k)], xo = rows[RS + sidx(kb)];
+    const CT ak = rows[2 * RS + sidx(k)], ao = rows[3 * RS + sidx(kb)];
+    const CT bk = rows[4 * RS + sidx(k)], bo = rows[5 * RS + sidx(kb)];
+    zak[q] = zmix(xk, cconj(xo), ak, cconj(ao), s);
+    zao[q] = zmix(xo, cconj(xk), ao, cconj(ak), s);
+    zbk[q] = zmix(xk, cconj(xo), bk, cconj(bo), s);
+    zbo[q] = zmix(xo, cconj(xk), bo, cconj(bk), s);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < KPT; ++q) {
+    const int k = threadIdx.x + q * NT;
+    if (k >= N2) continue;
+    const int kb = ra == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k);
+    if (self && kb < k) continue;
+    // Z_A into rows 0, 1 (the X rows' slots), Z_B into rows 2, 3: the inverse runs on rows 0..3
+    rows[sidx(k)] = zak[q];
+    rows[2 * RS + sidx(k)] = zbk[q];
+    if (self) {
+      rows[sidx(kb)] = zao[q];
+      rows[2 * RS + sidx(kb)] = zbo[q];
+    } else {
+      rows[RS + sidx(kb)] = zao[q];
+      rows[3 * RS + sidx(kb)] = zbo[q];
+    }
+  }
+  __syncthreads();
+  CT* ya = Xb + ib * N + static_cast<long>(ra) * N2;
+  CT* yb = Xb + ib * N + static_cast<long>(rb) * N2;
+  rows_inverse_to_global<LN2, NT, CT, 4>(rows, RS, ra, rb, self, xa, xb, T(2) / static_cast<T>(N), tw, ya, yb);
 }
 
 // ---- dispatch -----------------------------------------------------------------------------
@@ -719,7 +801,7 @@ void rows_conv_t(const ConvGeom& g, int items, int per_slot, CT* X, const CT* P,
 
 template <int LN2, typename CT>
 void rows_conv_fk_t(const ConvGeom& g, int items, int per_slot, CT* X, const CT* K, const CT* tw, cudaStream_t s,
-                    const CT* Xalt = nullptr, const int* share = nullptr) {
+                    const int* slot_map = nullptr) {
   constexpr int smem = 4 * padded(1 << LN2) * static_cast<int>(sizeof(CT));
   static const bool done = [] {
     cudaFuncSetAttribute(rows_conv_fk<LN2, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -728,7 +810,22 @@ void rows_conv_fk_t(const ConvGeom& g, int items, int per_slot, CT* X, const CT*
   (void)done;
   for_item_chunks(items, [&](int i0, int n) {
     const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(n));
-    rows_conv_fk<LN2, CT><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, per_slot, X, K, tw, i0, Xalt, share);
+    rows_conv_fk<LN2, CT><<<grid, row_threads<LN2, 4>(), smem, s>>>(g.log_n, per_slot, X, K, tw, i0, slot_map);
+  });
+}
+
+template <int LN2, typename CT>
+void rows_conv_pair_t(const ConvGeom& g, int items, int per_slot, CT* Xa, CT* Xb, const CT* Ka, const CT* Kb,
+                      const int* pa, const int* pb, const CT* tw, cudaStream_t s) {
+  constexpr int smem = 6 * padded(1 << LN2) * static_cast<int>(sizeof(CT));
+  static const bool done = [] {
+    cudaFuncSetAttribute(rows_conv_pair<LN2, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    return true;
+  }();
+  (void)done;
+  for_item_chunks(items, [&](int i0, int n) {
+    const dim3 grid(static_cast<unsigned>((1L << g.log_n1) / 2 + 1), static_cast<unsigned>(n));
+    rows_conv_pair<LN2, CT><<<grid, pair_threads<LN2>(), smem, s>>>(g.log_n, per_slot, Xa, Xb, Ka, Kb, pa, pb, tw, i0);
   });
 }
 
@@ -1378,8 +1475,7 @@ void conv_main(const StepArgs& a, long taps, const void* prologue_ws, void* ws, 
 // then A's rows in place (after B has read them), then both inverse column passes.
 template <typename CT>
 void conv_shared(const StepArgs& a, const StepArgs& b, long taps, const void* pws_a, const void* pws_b, void* ws_a,
-                 void* ws_b, const int* share, const int* own, int n_own, cudaStream_t s, cudaEvent_t ready_a,
-                 cudaEvent_t ready_b) {
+                 void* ws_b, const ConvShare& sh, cudaStream_t s, cudaEvent_t ready_a, cudaEvent_t ready_b) {
   const ConvGeom g = conv_geom(a.length, taps);
   const auto* Pa = reinterpret_cast<const CT*>(static_cast<const char*>(pws_a) + ir_bytes(a.slots, taps));
   const auto* Pb = reinterpret_cast<const CT*>(static_cast<const char*>(pws_b) + ir_bytes(b.slots, taps));
@@ -1387,13 +1483,22 @@ void conv_shared(const StepArgs& a, const StepArgs& b, long taps, const void* pw
   auto* Xb = static_cast<CT*>(ws_b);
   const int per_slot = a.batch * g.nseg;
   MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, CT, ColSrc::Signal, a, nullptr, 0, g, a.slots * per_slot, Xa, 0, false, s);
-  if (n_own > 0) {
-    MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, CT, ColSrc::Signal, b, nullptr, 0, g, n_own * per_slot, Xb, 0, false, s, own);
+  if (sh.n_own_b > 0) {
+    MGB_DISPATCH_LN(g.log_n1, cols_fwd_t, CT, ColSrc::Signal, b, nullptr, 0, g, sh.n_own_b * per_slot, Xb, 0, false, s,
+                    sh.own_b);
   }
-  if (ready_b) cudaStreamWaitEvent(s, ready_b, 0);
-  MGB_DISPATCH_LN(g.log_n2, rows_conv_fk_t, CT, g, b.slots * per_slot, per_slot, Xb, Pb, tw_table<CT>(b), s, Xa, share);
   if (ready_a) cudaStreamWaitEvent(s, ready_a, 0);
-  MGB_DISPATCH_LN(g.log_n2, rows_conv_fk_t, CT, g, a.slots * per_slot, per_slot, Xa, Pa, tw_table<CT>(a), s);
+  if (ready_b) cudaStreamWaitEvent(s, ready_b, 0);
+  MGB_DISPATCH_LN(g.log_n2, rows_conv_pair_t, CT, g, sh.n_pairs * per_slot, per_slot, Xa, Xb, Pa, Pb, sh.pair_a,
+                  sh.pair_b, tw_table<CT>(a), s);
+  if (sh.n_own_a > 0) {
+    MGB_DISPATCH_LN(g.log_n2, rows_conv_fk_t, CT, g, sh.n_own_a * per_slot, per_slot, Xa, Pa, tw_table<CT>(a), s,
+                    sh.own_a);
+  }
+  if (sh.n_own_b > 0) {
+    MGB_DISPATCH_LN(g.log_n2, rows_conv_fk_t, CT, g, sh.n_own_b * per_slot, per_slot, Xb, Pb, tw_table<CT>(b), s,
+                    sh.own_b);
+  }
   MGB_DISPATCH_LN(g.log_n1, cols_inv_t, CT, a, g, Xa, false, s);
   MGB_DISPATCH_LN(g.log_n1, cols_inv_t, CT, b, g, Xb, false, s);
 }
@@ -1489,12 +1594,12 @@ void launch_conv_prologue(bool reverb, const StepArgs& a, const ReverbConst& rc,
 }
 
 void launch_conv_shared(const StepArgs& a, const StepArgs& b, long taps, const void* pws_a, const void* pws_b,
-                        void* ws_a, void* ws_b, const int* share, const int* own, int n_own, cudaStream_t s,
-                        cudaEvent_t ready_a, cudaEvent_t ready_b) {
+                        void* ws_a, void* ws_b, const ConvShare& sh, cudaStream_t s, cudaEvent_t ready_a,
+                        cudaEvent_t ready_b) {
   if (fft_fp64()) {
-    conv_shared<double2>(a, b, taps, pws_a, pws_b, ws_a, ws_b, share, own, n_own, s, ready_a, ready_b);
+    conv_shared<double2>(a, b, taps, pws_a, pws_b, ws_a, ws_b, sh, s, ready_a, ready_b);
   } else {
-    conv_shared<float2>(a, b, taps, pws_a, pws_b, ws_a, ws_b, share, own, n_own, s, ready_a, ready_b);
+    conv_shared<float2>(a, b, taps, pws_a, pws_b, ws_a, ws_b, sh, s, ready_a, ready_b);
   }
 }
 

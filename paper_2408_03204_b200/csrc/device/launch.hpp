@@ -108,13 +108,21 @@ void launch_conv_prologue(bool reverb, const StepArgs& a, const ReverbConst& rc,
 void launch_conv_main(const StepArgs& a, long taps, const void* prologue_ws, void* ws, cudaStream_t s,
                       cudaEvent_t kernel_ready = nullptr);
 
-// Two adjacent conv steps with the same transform (conv_fuse_kernel_rows for both) where B's
-// slots listed in `share` (per B slot: the A slot reading the same single source row, or -1)
-// reuse A's signal spectrum; `own` lists the n_own B slots that transform their own input.
-// ws_a / ws_b: conv_main_bytes each, both live until the call's kernels finish.
+// Two adjacent conv steps A, B with the same transform (conv_fuse_kernel_rows for both) whose
+// slots pair up on a common single source row (a console track's delay and reverb sends):
+// pairs (pair_a[p], pair_b[p]) share A's signal spectrum (each A slot in at most one pair);
+// own_a / own_b list the remaining slots of each step. ws_a / ws_b: conv_main_bytes each, both
+// live until the call's kernels finish.
+struct ConvShare {
+  const int* pair_a = nullptr;
+  const int* pair_b = nullptr;
+  const int* own_a = nullptr;
+  const int* own_b = nullptr;
+  int n_pairs = 0, n_own_a = 0, n_own_b = 0;
+};
 void launch_conv_shared(const StepArgs& a, const StepArgs& b, long taps, const void* pws_a, const void* pws_b,
-                        void* ws_a, void* ws_b, const int* share, const int* own, int n_own, cudaStream_t s,
-                        cudaEvent_t ready_a, cudaEvent_t ready_b);
+                        void* ws_a, void* ws_b, const ConvShare& sh, cudaStream_t s, cudaEvent_t ready_a,
+                        cudaEvent_t ready_b);
 
 // Backward of a reverb / delay step: dX = correlation with the kernel (stored into bw.dst),
 // kernel gradient = correlation of dY with X, then through the IR build / tap FIRs into

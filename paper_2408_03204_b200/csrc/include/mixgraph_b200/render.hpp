@@ -137,13 +137,16 @@ class DevicePlan {
   bool follows(int step) const { return follow_off_[static_cast<std::size_t>(step)] >= 0; }
   const int* follow_map(int step) const;
   // Step k (k >= 1) and step k-1 are long convolutions and some of step k's slots read the same
-  // single source row as a slot of step k-1 (a console track's delay and reverb sends):
-  // share_map(k)[s] = that slot of step k-1 or -1 (device), share_own(k) = the n_own(k) slots
-  // of step k with no such partner (device). shares(k) is false when no slot matches.
-  bool shares(int step) const { return share_off_[static_cast<std::size_t>(step)] >= 0; }
-  const int* share_map(int step) const;
-  const int* share_own(int step) const;
-  int share_own_count(int step) const { return share_own_n_[static_cast<std::size_t>(step)]; }
+  // single source row as a slot of step k-1 (a console track's delay and reverb sends; each
+  // slot of step k-1 pairs at most once). share(k): device lists of the pairs (slot of k-1,
+  // slot of k) and of each step's unpaired slots; shares(k) is false when nothing pairs.
+  struct Share {
+    int pairs = 0, own_prev = 0, own = 0;
+    long off = -1;  // host_index offset: [pair_prev][pair][own_prev][own]
+  };
+  bool shares(int step) const { return share_[static_cast<std::size_t>(step)].off >= 0; }
+  const Share& share_info(int step) const { return share_[static_cast<std::size_t>(step)]; }
+  const int* share_ints(int step) const;  // device pointer to the step's lists
   std::size_t workspace_bytes(int batch, long length, const ProcessorSet& procs) const;
   // Workspace for a forward render followed by backward_arena (forward layout + scratch).
   std::size_t backward_workspace_bytes(int batch, long length, const ProcessorSet& procs) const;
@@ -183,8 +186,8 @@ class DevicePlan {
   const cudaEvent_t* borrowed_events_ = nullptr;
   const int* d_index_ = nullptr;
   std::vector<int> host_;
-  std::vector<long> rp_off_, col_off_, trp_off_, tcol_off_, follow_off_, share_off_;
-  std::vector<int> share_own_n_;
+  std::vector<long> rp_off_, col_off_, trp_off_, tcol_off_, follow_off_;
+  std::vector<Share> share_;
   std::vector<int> zero_rows_;
   std::vector<int> dense_;
 };

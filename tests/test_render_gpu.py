@@ -648,8 +648,11 @@ def test_shared_signal_spectra_bit_exact(mg, ref, prune, L, batch):
     assert k > 0
     procs = mg.ProcessorSet()
     src = np.random.default_rng(5).uniform(-1, 1, size=(rd.num_inputs, batch, 2, L))
+    assert rd.shared_pairs(procs, batch, L)[k] == 0  # small steps: separate (side-by-side) passes
     mg.set_conv_fuse(1)
     try:
+        pairs = rd.shared_pairs(procs, batch, L)
+        assert pairs[k] > 0 and pairs.sum() == pairs[k]
         dr = DeviceRenderer(rd, procs, batch, L, rd.reorder_params(params))
         dr.sources.copy_(torch.as_tensor(src, dtype=torch.float32))
         dr.render()

@@ -10,7 +10,7 @@ hdr = rows[h]
 ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
 data = rows[h + 1:]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else len(data)
-KEYS = ("rows_conv_fk", "rows_conv", "rows_spec", "cols_fwd<9, 2", "cols_fwd<9, 0",
+KEYS = ("rows_conv_fk", "rows_conv_pair", "rows_conv", "rows_spec", "cols_fwd<9, 2", "cols_fwd<9, 0",
         "cols_fwd<9, 1", "cols_inv", "eq_conv", "dyn_scan<0", "dyn_scan<1", "pointwise", "reverb_ir",
         "eq_response_basis", "eq_mag_tiles", "delay_taps", "eq_design", "eq_response", "eq_mags", "param_gather")
 ALIAS = {"cols_fwd<9, 2": "cols_fwd<delay taps>", "cols_fwd<9, 0": "cols_fwd<kernel>",
