@@ -156,49 +156,101 @@ constexpr int kCorrOut = 6144;  // outputs per block (as the forward's 8192 wind
 constexpr int kCorrThreads = 512;
 constexpr int kCorrFS = padded(kCorrFft);
 
-// count samples of (gathered) signal from position `start` into buf[sidx(i)] (channels as
-// re/im), zeros outside [0, L) and for i >= count.
-__device__ __forceinline__ void load_window(const StepArgs& a, int e0, int e1, int b, long start, int count,
-                                            float2* buf) {
-  for (int i = threadIdx.x; i < kCorrFft; i += kCorrThreads) {
-    const long n = start + i;
-    float2 v = make_float2(0.f, 0.f);
-    if (i < count && n >= 0 && n < a.length) v = gather2(a, e0, e1, b, n);
-    buf[sidx(i)] = v;
-  }
-}
-
 // dh[j] over `per` consecutive output blocks: with W = x[out0 - 1024 + u] (u < 8192) and
 // D = dy[out0 + v] (v < 6144, zero-padded), sum_v D[v] W[v + s] = IFFT(conj(D^) W^)[s]; tap
 // j = 2047 - s. The product spectra of the CTA's blocks are summed (fixed order) before ONE
 // inverse transform. Channels packed as re/im: the real part of the product sums both
 // channels' correlations. grid (ceil(blocks / per), slots*B); out[(sb * gridDim.x + cta) * 2048 + j].
+// Register-ended transforms (as eq_conv): thread j loads the 16 inputs j + r*512 of its
+// radix-16 first-pass butterfly straight from memory, and the forward plan 16 x 8 x 4 x 16 ends
+// with a radix-16 pass whose butterfly j holds bins j + r*512 — the same bins every block, so
+// the product spectrum accumulates in registers, and they are exactly the inputs of the
+// inverse's radix-16 first-pass butterfly j. One smem buffer (the old kernel staged both
+// windows and the accumulator in smem: 3x the smem traffic).
+__device__ __forceinline__ void corr_load(const StepArgs& a, int e0, int e1, int b, long start, int count,
+                                          float2 (&v)[16]) {
+  constexpr int M1 = kCorrFft / 16;
+  if (e1 - e0 == 1) {  // one input row (the common case): its base address once, not per sample
+    const float* p = a.src + edge_row(a, e0) * a.rowstride + static_cast<long>(b) * 2 * a.length;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int i = threadIdx.x + r * M1;
+      const long n = start + i;
+      v[r] = (i < count && n >= 0 && n < a.length) ? make_float2(0.f + __ldg(p + n), 0.f + __ldg(p + a.length + n))
+                                                   : make_float2(0.f, 0.f);
+    }
+    return;
+  }
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int i = threadIdx.x + r * M1;
+    const long n = start + i;
+    v[r] = (i < count && n >= 0 && n < a.length) ? gather2(a, e0, e1, b, n) : make_float2(0.f, 0.f);
+  }
+}
+// Forward transform of v (first-pass inputs) through `buf`; on return v = bins j + r*512.
+__device__ __forceinline__ void corr_forward(float2 (&v)[16], float2* buf, const float2* tw) {
+  constexpr int NL = kCorrFft / 16;
+  const int j = threadIdx.x;
+  fft_first_from_regs<-1>(v, buf, j);
+  __syncthreads();
+  stockham_pass<kCorrFft, 8, 16, 1, kCorrThreads, -1>(buf, kCorrFS, tw);
+  stockham_pass<kCorrFft, 4, 128, 1, kCorrThreads, -1>(buf, kCorrFS, tw);
+  TwPass<16, NL, -1, float2> twb;
+  twb.load(tw, j);
+  const float2* lb = buf + sidx(j);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = lb[r * padded(NL)];
+  twb.apply(v);
+  Dft<16, -1, float2>::run(v);
+  __syncthreads();  // buf is free again
+}
+
 __global__ void __launch_bounds__(kCorrThreads, 1) eq_corr(StepArgs fw, StepArgs bw, int per, float* out) {
-  extern __shared__ float2 buf[];  // [3][kCorrFS]: window, dy block, accumulated product
+  static_assert(kCorrFft / 16 == kCorrThreads, "eq_corr: one first-pass butterfly per thread");
+  extern __shared__ float2 buf[];  // [kCorrFS] transforms, then [16][512] this thread's accumulated bins
+  float2* acc = buf + kCorrFS;
   const int sb = blockIdx.y;
   const int slot = sb / fw.batch, b = sb - slot * fw.batch;
-  float2* acc = buf + 2 * kCorrFS;
-  for (int k = threadIdx.x; k < kCorrFft; k += kCorrThreads) acc[sidx(k)] = make_float2(0.f, 0.f);
   const long nblk = (fw.length + kCorrOut - 1) / kCorrOut;
   const int fe0 = __ldg(fw.row_ptr + slot), fe1 = __ldg(fw.row_ptr + slot + 1);
   const int be0 = __ldg(bw.row_ptr + slot), be1 = __ldg(bw.row_ptr + slot + 1);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) acc[r * kCorrThreads + threadIdx.x] = make_float2(0.f, 0.f);
   for (long blk = static_cast<long>(blockIdx.x) * per; blk < nblk && blk < static_cast<long>(blockIdx.x + 1) * per; ++blk) {
     const long out0 = blk * kCorrOut;
-    __syncthreads();  // previous block's buffers consumed
-    load_window(fw, fe0, fe1, b, out0 - (kEqHalf + 1), kCorrFft, buf);
-    load_window(bw, be0, be1, b, out0, kCorrOut, buf + kCorrFS);
-    __syncthreads();
-    fft_pow2<kCorrLog, 2, kCorrThreads, -1>(buf, kCorrFS, fw.tw);
-    for (int k = threadIdx.x; k < kCorrFft; k += kCorrThreads) {
-      const float2 w = buf[sidx(k)], d = buf[kCorrFS + sidx(k)];
-      acc[sidx(k)] = cadd(acc[sidx(k)], cmul(cconj(d), w));
+    float2 w[16], d[16];
+    corr_load(fw, fe0, fe1, b, out0 - (kEqHalf + 1), kCorrFft, w);
+    corr_forward(w, buf, fw.tw);
+    corr_load(bw, be0, be1, b, out0, kCorrOut, d);
+    corr_forward(d, buf, fw.tw);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {  // this thread's own entries: no barrier
+      float2& a = acc[r * kCorrThreads + threadIdx.x];
+      a = cadd(a, cmul(cconj(d[r]), w[r]));
     }
   }
+  {
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = acc[r * kCorrThreads + threadIdx.x];
+    fft_first_from_regs<+1>(v, buf, threadIdx.x);
+  }
   __syncthreads();
-  fft_pow2<kCorrLog, 1, kCorrThreads, +1>(acc, kCorrFS, fw.tw);
+  fft_middle<kCorrLog, 1, kCorrThreads, +1>(buf, kCorrFS, fw.tw);
+  // Last inverse pass into registers: outputs k = jj + r*NS; tap 2047 - k for k in [1, 2047].
+  constexpr int NS = Pow2Plan<kCorrLog>::kLastNs, R = Pow2Plan<kCorrLog>::kLastR;
   float* o = out + (static_cast<long>(sb) * gridDim.x + blockIdx.x) * 2048;
-  for (int j = threadIdx.x; j < 2 * kEqHalf + 1; j += kCorrThreads) {
-    o[j] = acc[sidx(2 * kEqHalf + 1 - j)].x * (1.f / kCorrFft);
+#pragma unroll
+  for (int p = 0; p < NS / kCorrThreads; ++p) {
+    const int jj = threadIdx.x + p * kCorrThreads;
+    float2 y[R];
+    fft_last_to_regs<kCorrLog, +1>(buf, jj, fw.tw, y);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int k = jj + r * NS;
+      if (k >= 1 && k <= 2 * kEqHalf + 1) o[2 * kEqHalf + 1 - k] = y[r].x * (1.f / kCorrFft);
+    }
   }
 }
 
@@ -209,7 +261,9 @@ __global__ void __launch_bounds__(1024) eq_grad(const float* partial, int rows_p
                                                 const double* __restrict__ cos_tab, double* grad) {
   constexpr int N = 2 * kEqHalf + 1, C = kEqHalf;
   __shared__ double sym[kEqHalf + 1];  // S_j = (dh w)[c + j] + (dh w)[c - j], S_0 = (dh w)[c]
+  __shared__ double cs[N];             // cos(2 pi i / N): the loop below gathers it at q t mod N
   const int slot = blockIdx.x;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) cs[i] = __ldg(cos_tab + i);
   const float* p = partial + static_cast<long>(slot) * rows_per_slot * 2048;
   const int j = threadIdx.x;  // 0..1023
   double hi = 0.0, lo = 0.0;
@@ -226,7 +280,7 @@ __global__ void __launch_bounds__(1024) eq_grad(const float* partial, int rows_p
   double acc = 0.0;
   int idx = 0;
   for (int t = 0; t <= kEqHalf; ++t) {
-    acc = fma(sym[t], __ldg(cos_tab + idx), acc);
+    acc = fma(sym[t], cs[idx], acc);  // (from L1 each warp's 32 scattered entries were ~32 wavefronts)
     idx += q;
     if (idx >= N) idx -= N;
   }
@@ -340,7 +394,7 @@ std::size_t eq_grad_bytes(int slots, int batch, long length) {
 void launch_eq_param_grad(const StepArgs& fw, const StepArgs& bw, void* ws, double* grad, cudaStream_t s) {
   if (fw.slots == 0) return;
   static const bool done = [] {
-    cudaFuncSetAttribute(eq_corr, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * kCorrFS * 8);
+    cudaFuncSetAttribute(eq_corr, cudaFuncAttributeMaxDynamicSharedMemorySize, (kCorrFS + kCorrFft) * 8);
     return true;
   }();
   (void)done;
@@ -351,7 +405,7 @@ void launch_eq_param_grad(const StepArgs& fw, const StepArgs& bw, void* ws, doub
   per = std::min(per, blocks);
   const long ctas = (blocks + per - 1) / per;
   auto* part = static_cast<float*>(ws);
-  eq_corr<<<dim3(static_cast<unsigned>(ctas), static_cast<unsigned>(items)), kCorrThreads, 3 * kCorrFS * 8, s>>>(
+  eq_corr<<<dim3(static_cast<unsigned>(ctas), static_cast<unsigned>(items)), kCorrThreads, (kCorrFS + kCorrFft) * 8, s>>>(
       fw, bw, static_cast<int>(per), part);
   eq_grad<<<fw.slots, 1024, 0, s>>>(part, static_cast<int>(ctas) * fw.batch, fw.params, cos_table(fw.tw), grad);
 }
