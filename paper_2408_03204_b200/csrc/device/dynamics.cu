@@ -678,19 +678,49 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_bwd_dg(DynBwd d) {
   float dgg = 0.f;
   float* env = d.env + static_cast<long>(seq) * L;
   float* dgo = d.dg + static_cast<long>(seq) * L;
+  // The thread's envelope samples in, its gains and dg out, four at a time as float4 when all
+  // four are in range (scalar accesses at an 8-sample stride made every warp access touch 32
+  // sectors).
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const long n = n0 + k;
-    if (n >= L) break;
-    const float g = env[n];
-    float gu;
-    const float gain = gain_of<GATE>(g, p, &gu);  // the forward's own arithmetic
-    const float dD = (dyl[k] * ul[k] + dyr[k] * ur[k]) * gain;
-    const float slope = knee_grad<GATE>(gu, p, dD, acc);
-    const float dg = g > p.floor_ ? dD * (slope - 1.f) / g : 0.f;
-    dgg += dg * g;
-    env[n] = gain;
-    dgo[n] = dg;
+  for (int q = 0; q < K / 4; ++q) {
+    const long nq = n0 + 4 * q;
+    const bool full = VEC && nq + 4 <= L;
+    float gv[4], go[4], dv[4];
+    if (full) {
+      const float4 a4 = *reinterpret_cast<const float4*>(env + nq);
+      gv[0] = a4.x; gv[1] = a4.y; gv[2] = a4.z; gv[3] = a4.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) gv[k] = nq + k < L ? env[nq + k] : 1.f;
+    }
+#pragma unroll
+    for (int k4 = 0; k4 < 4; ++k4) {
+      const int k = 4 * q + k4;
+      go[k4] = 0.f;
+      dv[k4] = 0.f;
+      if (nq + k4 >= L) continue;
+      const float g = gv[k4];
+      float gu;
+      const float gain = gain_of<GATE>(g, p, &gu);  // the forward's own arithmetic
+      const float dD = (dyl[k] * ul[k] + dyr[k] * ur[k]) * gain;
+      const float slope = knee_grad<GATE>(gu, p, dD, acc);
+      const float dg = g > p.floor_ ? dD * (slope - 1.f) / g : 0.f;
+      dgg += dg * g;
+      go[k4] = gain;
+      dv[k4] = dg;
+    }
+    if (full) {
+      *reinterpret_cast<float4*>(env + nq) = make_float4(go[0], go[1], go[2], go[3]);
+      *reinterpret_cast<float4*>(dgo + nq) = make_float4(dv[0], dv[1], dv[2], dv[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (nq + k < L) {
+          env[nq + k] = go[k];
+          dgo[nq + k] = dv[k];
+        }
+      }
+    }
   }
   double vals[4] = {acc[0], acc[1], acc[2], dgg};
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -711,8 +741,17 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_bwd_dg(DynBwd d) {
   }
 }
 
-// dg at kDynPerThread samples from n0 (0 outside [0, L)).
+// dg at kDynPerThread samples from n0 (0 outside [0, L)); VEC: n0 is a multiple of 4.
+template <bool VEC>
 __device__ __forceinline__ void load_dg(const float* dg, long L, long n0, float* v) {
+  if (VEC && n0 >= 0 && n0 + kDynPerThread <= L) {
+#pragma unroll
+    for (int q = 0; q < kDynPerThread / 4; ++q) {
+      const float4 f = __ldg(reinterpret_cast<const float4*>(dg + n0) + q);
+      v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
+    }
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < kDynPerThread; ++k) {
     const long n = n0 + k;
@@ -740,10 +779,10 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_bwd(DynBwd d) {
   const float* dgs = d.dg + static_cast<long>(seq) * L;
   // a_k = dg[n] - a^Ne dg[n+Ne], b_k = -Ne a^(Ne-1) dg[n+Ne] (skipped when a^Ne < 1e-30).
   float av[K], bv[K];
-  load_dg(dgs, L, n0, av);
+  load_dg<VEC>(dgs, L, n0, av);
   if (p.aN != 0.f) {
     float t2[K];
-    load_dg(dgs, L, n0 + p.Ne, t2);
+    load_dg<VEC>(dgs, L, n0 + p.Ne, t2);
     const float nb = static_cast<float>(p.Ne) * p.aN / p.a;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -822,15 +861,40 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_bwd(DynBwd d) {
     float* dr = dl + L;
     double ev = 0.0;
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const long n = n0 + k;
-      if (n >= L) break;
-      const float mid = ul[k] + ur[k];
-      const float dmid = 2.f * mid * (p.oma * wv[k]);
-      const float gn = __ldg(gain + n);
-      dl[n] = fmaf(gn, dyl[k], dmid);
-      dr[n] = fmaf(gn, dyr[k], dmid);
-      ev += static_cast<double>(mid * mid) * vv[k];
+    for (int q = 0; q < K / 4; ++q) {
+      const long nq = n0 + 4 * q;
+      const bool full = VEC && nq + 4 <= L;
+      float gn[4], ol[4], orr[4];
+      if (full) {
+        const float4 g4 = __ldg(reinterpret_cast<const float4*>(gain + nq));  // the gains pass A stored
+        gn[0] = g4.x; gn[1] = g4.y; gn[2] = g4.z; gn[3] = g4.w;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) gn[k] = nq + k < L ? __ldg(gain + nq + k) : 0.f;
+      }
+#pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4) {
+        const int k = 4 * q + k4;
+        ol[k4] = orr[k4] = 0.f;
+        if (nq + k4 >= L) continue;
+        const float mid = ul[k] + ur[k];
+        const float dmid = 2.f * mid * (p.oma * wv[k]);
+        ol[k4] = fmaf(gn[k4], dyl[k], dmid);
+        orr[k4] = fmaf(gn[k4], dyr[k], dmid);
+        ev += static_cast<double>(mid * mid) * vv[k];
+      }
+      if (full) {
+        *reinterpret_cast<float4*>(dl + nq) = make_float4(ol[0], ol[1], ol[2], ol[3]);
+        *reinterpret_cast<float4*>(dr + nq) = make_float4(orr[0], orr[1], orr[2], orr[3]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (nq + k < L) {
+            dl[nq + k] = ol[k];
+            dr[nq + k] = orr[k];
+          }
+        }
+      }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, off);
