@@ -393,18 +393,27 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
     // this thread's own stashed input, four samples at a time (no barrier: written by itself)
     const float4 l4 = s_in[0][q][threadIdx.x], r4 = s_in[1][q][threadIdx.x];
     const float ul[4] = {l4.x, l4.y, l4.z, l4.w}, ur[4] = {r4.x, r4.y, r4.z, r4.w};
-    float yl[4], yr[4];
+    float yl[4], yr[4], ev[4];
 #pragma unroll
     for (int k4 = 0; k4 < 4; ++k4) {
       const int k = 4 * q + k4;
       g = fma(p.da, g, drive[k]);
       const float gf = static_cast<float>(g);
-      if constexpr (ENV) {
-        if (n0 + k < a.length) env[static_cast<long>(seq) * a.length + n0 + k] = gf;
-      }
+      ev[k4] = gf;
       const float gn = gain_of<GATE>(gf, p);
       yl[k4] = gn * ul[k4];
       yr[k4] = gn * ur[k4];
+    }
+    if constexpr (ENV) {  // the envelope for the backward pass, four samples per store
+      float* e = env + static_cast<long>(seq) * a.length + n0 + 4 * q;
+      if (full) {
+        *reinterpret_cast<float4*>(e) = make_float4(ev[0], ev[1], ev[2], ev[3]);
+      } else {
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+          if (n0 + 4 * q + k4 < a.length) e[k4] = ev[k4];
+        }
+      }
     }
     if (full) {
       reinterpret_cast<float4*>(ol)[q] = make_float4(yl[0], yl[1], yl[2], yl[3]);

@@ -290,15 +290,18 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_inv(StepArgs a, 
 template <typename CT>
 __global__ void __launch_bounds__(256) conv_ola(StepArgs a, SegArgs sg, long N, const CT* buf) {
   using T = RealOf<CT>;
-  const long m = static_cast<long>(blockIdx.x) * 256 + threadIdx.x;
+  // 32-bit index math (L, seg, pre < 2^31; the 64-bit divisions dominated this kernel)
+  const int m = static_cast<int>(blockIdx.x) * 256 + static_cast<int>(threadIdx.x);
   if (m >= a.length) return;
   const int isb = sg.item0 + blockIdx.y;
   const int slot = isb / a.batch, b = isb - slot * a.batch;
-  long jhi = (m + sg.pre) / sg.seg;
-  if (jhi > sg.nseg - 1) jhi = sg.nseg - 1;
+  const int seg = static_cast<int>(sg.seg), pre = static_cast<int>(sg.pre);
+  const int jhi = min((m + pre) / seg, sg.nseg - 1);
   CT acc = Cx<CT>::mk(0.f, 0.f);
-  for (long j = m / sg.seg; j <= jhi; ++j) {
-    acc = cadd(acc, __ldg(buf + (static_cast<long>(isb) * sg.nseg + j) * N + (m - seg_base(sg.seg, sg.pre, j))));
+  const CT* bi = buf + static_cast<long>(isb) * sg.nseg * N;
+  for (int j = m / seg; j <= jhi; ++j) {
+    const int base = max(j * seg - pre, 0);
+    acc = cadd(acc, __ldg(bi + static_cast<long>(j) * N + (m - base)));
   }
   float* y = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length;
   y[m] = static_cast<float>(acc.x);
