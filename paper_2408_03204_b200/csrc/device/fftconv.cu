@@ -216,6 +216,107 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_fwd(StepArgs a, 
   }
 }
 
+// ---- delay kernel: column stage as a sparse DFT -------------------------------------------
+// The multitap delay kernel (processors.cpp:210-227) has <= 40 taps x 39 FIR coefficients in
+// a 2 s span: a column n2 of the four-step layout (samples n1*N2 + n2, N2 >= 64 > 39) meets
+// each tap's FIR window at most once, ~3 times in all. Its N1-point DFT is therefore the sum
+// of those few terms, f * w_N1^(n1 k1), evaluated directly: no zero fill, no scatter, no smem
+// FFT passes — the kernel is bound by writing the 2 MiB column-stage spectrum per slot.
+// Per CTA (C columns, as cols_fwd): warp w builds the hit lists of columns w, w + 16, ... in
+// tap order (ballot + popc: deterministic), then thread (column c, group g) sums the hits of
+// its column for k1 = g + G r (G = 512 / C, r < 16) and applies the four-step twiddle
+// exp(-2 pi i n2 k1 / N). Twiddles from the table (exact anchors every 4 outputs, <= 3
+// chained products in between). Same values as the transform of the synthesised kernel up to
+// fp32 rounding (a direct sum of <= 40 terms).
+constexpr int kDelayColThreads = 512;
+constexpr int kDelayColBlocks = 4;  // column blocks per CTA (the records are loaded once)
+template <int LN1>
+__global__ void __launch_bounds__(kDelayColThreads) delay_cols(const float* taps_rec, long taps, int log_n, float2* out,
+                                                           const float2* tw) {
+  constexpr int N1 = 1 << LN1;
+  constexpr int C = 8192 / N1;                  // columns per CTA (cols_fwd's tiling)
+  constexpr int G = kDelayColThreads / C;       // k1 groups
+  constexpr int R = N1 / G;                     // outputs per thread (16)
+  constexpr int NW = kDelayColThreads / 32;
+  static_assert(R == 16, "delay_cols: 16 outputs per thread");
+  __shared__ float rec[kTaps * kTapRec];
+  __shared__ int hn1[C][kTaps];
+  __shared__ float2 hv[C][kTaps];
+  __shared__ int hcnt[C];
+  const int slot = blockIdx.y;
+  const int log_n2 = log_n - LN1;
+  const int N2 = 1 << log_n2;
+  const int N = 1 << log_n;
+  const float* in = taps_rec + static_cast<long>(slot) * kTaps * kTapRec;
+  for (int q = threadIdx.x; q < kTaps * kTapRec; q += kDelayColThreads) rec[q] = __ldg(in + q);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nhi = static_cast<int>(min(taps, static_cast<long>(N)));
+  const int c = threadIdx.x % C, g = threadIdx.x / C;
+  constexpr int TS = 8192 / N1;  // table stride: w_N1^x = tw[x * TS]
+  const float inv_n = 2.f / static_cast<float>(N);
+  // Column blocks blockIdx.x, + gridDim.x, ...: the tap records are loaded once per CTA.
+  for (int col0 = blockIdx.x * C; col0 < N2; col0 += gridDim.x * C) {
+    __syncthreads();  // records loaded / previous block's hit lists consumed
+    for (int cc = warp; cc < C; cc += NW) {
+      const int n2 = col0 + cc;
+      int base = 0;
+      for (int m0 = 0; m0 < kTaps; m0 += 32) {
+        const int m = m0 + lane;
+        bool hit = false;
+        int n1 = 0;
+        float f = 0.f;
+        if (m < kTaps) {
+          const float* r = rec + m * kTapRec;
+          const int d = __float_as_int(r[0]);
+          if (d >= 0) {
+            const int i0 = d - kFirHalf;
+            const int i = i0 + (((n2 - i0) % N2) + N2) % N2;  // first sample of column n2 at or after i0
+            if (i <= d + kFirHalf && i >= 0 && i < nhi) {
+              hit = true;
+              n1 = i >> log_n2;
+              f = r[1 + (i - i0)];
+            }
+          }
+        }
+        const unsigned mask = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const int pos = base + __popc(mask & ((1u << lane) - 1u));
+          hn1[cc][pos] = n1;
+          hv[cc][pos] = m < kTaps / 2 ? make_float2(f, 0.f) : make_float2(0.f, f);  // left taps 0-19, right 20-39
+        }
+        base += __popc(mask);
+      }
+      if (lane == 0) hcnt[cc] = base;
+    }
+    __syncthreads();
+    const int n2 = col0 + c;
+    float2 acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = make_float2(0.f, 0.f);
+    const int nh = hcnt[c];
+    for (int h = 0; h < nh; ++h) {
+      const int n1 = hn1[c][h];
+      const float2 v = hv[c][h];
+      const float2 ws = __ldg(tw + ((n1 * G) & (N1 - 1)) * TS);
+      float2 w = make_float2(1.f, 0.f);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        w = (r % 4 == 0) ? __ldg(tw + ((n1 * (g + G * r)) & (N1 - 1)) * TS) : cmul(w, ws);
+        acc[r] = cadd(acc[r], cmul(v, w));
+      }
+    }
+    float2* o = out + static_cast<long>(slot) * N + n2;
+    const float2 st = expi_pi(-static_cast<float>(n2 * G) * inv_n);
+    float2 w = make_float2(1.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int k1 = g + G * r;
+      w = (r % 4 == 0) ? expi_pi(-static_cast<float>(n2 * k1) * inv_n) : cmul(w, st);
+      o[static_cast<long>(k1) * N2] = cmul(acc[r], w);
+    }
+  }
+}
+
 // ---- pass 3 (last): inverse column FFTs, store into the arena --------------------------
 // BUF: the whole transform goes back into the item's own spectrum in natural order (in place:
 // a CTA owns its columns, and all its loads are consumed before its stores) for conv_ola.
@@ -736,7 +837,10 @@ void cols_fwd_t(ColSrc src, const StepArgs& a, const float2* ir, long taps, cons
     return true;
   }();
   (void)attrs_set;
-  if (src == ColSrc::DelayTaps) note_prologue_kernel(reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::DelayTaps, CT>));
+  if (src == ColSrc::DelayTaps) {
+    if constexpr (sizeof(CT) == 8 && LN1 >= 8) note_prologue_kernel(reinterpret_cast<const void*>(delay_cols<LN1>));
+    else note_prologue_kernel(reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::DelayTaps, CT>));
+  }
   if (src == ColSrc::Kernel) note_prologue_kernel(reinterpret_cast<const void*>(cols_fwd<LN1, ColSrc::Kernel, CT>));
   constexpr int nt = ColCfg<CT>::kThreads;
   for_item_chunks(items, [&](int i0, int n) {
@@ -745,7 +849,13 @@ void cols_fwd_t(ColSrc src, const StepArgs& a, const float2* ir, long taps, cons
     if (src == ColSrc::Signal) {
       cols_fwd<LN1, ColSrc::Signal, CT><<<grid, nt, smem, s>>>(a, ir, taps, g.log_n, out, window, sg);
     } else if (src == ColSrc::DelayTaps) {
-      cols_fwd<LN1, ColSrc::DelayTaps, CT><<<grid, nt, smem, s>>>(a, ir, taps, g.log_n, out, window, sg);
+      if constexpr (sizeof(CT) == 8 && LN1 >= 8) {  // fp32, <= 32 columns per CTA: the sparse direct DFT
+        const dim3 dgrid(static_cast<unsigned>(std::max<long>(1, ((1L << g.log_n2) / C) / kDelayColBlocks)), static_cast<unsigned>(n));
+        delay_cols<LN1><<<dgrid, kDelayColThreads, 0, s>>>(reinterpret_cast<const float*>(ir) + static_cast<long>(i0) * kTaps * kTapRec,
+                                                          taps, g.log_n, out + static_cast<long>(i0) * (1L << g.log_n), a.tw);
+      } else {
+        cols_fwd<LN1, ColSrc::DelayTaps, CT><<<grid, nt, smem, s>>>(a, ir, taps, g.log_n, out, window, sg);
+      }
     } else {
       cols_fwd<LN1, ColSrc::Kernel, CT><<<grid, nt, smem, s>>>(a, ir, taps, g.log_n, out, window, sg);
     }
