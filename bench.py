@@ -162,6 +162,8 @@ def kernel_family(name):
         return "dyn_scan"
     if "rows_conv_pair" in name:  # row passes of delay / reverb items sharing a signal spectrum
         return "rows_conv_fk"
+    if "delay_cols" in name:  # the delay kernel's column stage as a sparse direct DFT
+        return "delay_cols"
     for key in ("rows_conv_fk", "rows_conv", "rows_spec", "cols_fwd", "cols_inv", "eq_conv", "dyn_scan",
                 "pointwise_wide", "pointwise_chain", "pointwise", "reverb_ir", "eq_response_basis", "eq_mag_tiles",
                 "delay_taps", "eq_design", "eq_response", "eq_mags", "param_gather"):
@@ -201,7 +203,8 @@ def family_work(mg, procs, rd, length, batch=1):
     pointwise family).
       reverb / delay, per (slot, batch, segment) item of the N = N1 N2 segmented transform:
         cols_fwd  column halves of the signal forward (not for items reusing the previous
-                  step's spectrum, rd.shared_pairs) and of the kernel spectrum (per slot)
+                  step's spectrum, rd.shared_pairs) and of the reverb kernel spectrum (per slot)
+        delay_cols the delay kernel's column stage (sparse direct DFT): HBM, its 8 N B write
         rows_conv row halves of the forward and inverse + product (rows_conv_fk: + the kernel's
                   row half per item; otherwise rows_spec does it once per slot)
         cols_inv  column half of the inverse
@@ -235,7 +238,10 @@ def family_work(mg, procs, rd, length, batch=1):
             per = batch * g["nseg"]
             items = slots * per
             shared = int(pairs[k]) * per  # items reusing step k-1's signal spectra
-            add("cols_fwd", "fp32", (items - shared + slots) * 5.0 * n * l1)
+            sparse = t == mg.NodeType.DELAY and l1 >= 8 and mg.fft_precision() == 32
+            if sparse:  # delay_cols: writes the column-stage spectrum, a few terms per output
+                add("delay_cols", "hbm", slots * n * 8.0)
+            add("cols_fwd", "fp32", (items - shared + (0 if sparse else slots)) * 5.0 * n * l1)
             add("cols_inv", "fp32", items * 5.0 * n * l1)
             if 8.0 * slots * n > (64 << 20):  # conv_fuse: kernel rows transformed per item
                 # a shared pair (this item + its partner in step k-1) runs 5 row transforms, not 6
