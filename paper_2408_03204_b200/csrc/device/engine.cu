@@ -163,7 +163,8 @@ ProcessorSet::ProcessorSet(const ProcessorConfig& config) : config_(config) {
   cuda_check(cudaGetDevice(&dev_->device), "cudaGetDevice");
   mgb::twiddle_table(dev_->device);
   mgb::twiddle_table64(dev_->device);
-  mgb::eq_basis(dev_->device);
+  mgb::eq_basis(dev_->device, true);
+  mgb::eq_basis(dev_->device, false);
   dev_->frames = static_cast<int>((reverb_length_ + kReverbStftHop - 1) / kReverbStftHop);
   const std::size_t stft_bytes = sizeof(float2) * static_cast<std::size_t>(dev_->frames) * (kReverbStftLength / 2 + 1);
   cuda_check(cudaMalloc(&dev_->stft_mid, stft_bytes > 0 ? stft_bytes : 8), "cudaMalloc");

@@ -16,6 +16,7 @@
 //     that did not wrap. Arena in -> arena out in one kernel.
 #include <cstdlib>
 #include <map>
+#include <utility>
 #include <mutex>
 #include <stdexcept>
 #include <vector>
@@ -113,23 +114,30 @@ __global__ void __launch_bounds__(512) eq_response(const float* taps, float* res
   for (int i = threadIdx.x; i < kEqFft; i += blockDim.x) r[i] = buf[sidx(i)].x * (1.f / kEqFft);
 }
 
-// ---- response as a product with a fixed basis ---------------------------------------------
-// The 8192-bin response is LINEAR in the magnitudes m_q = exp(lm_q): R = A m with
-// A[k][q] = the response of eq_design/eq_response to the unit spectrum e_q (the cosine sum,
-// the symmetric Hann and the 8192-point DFT are all linear). The basis A^T [1024][kBasisK] is
-// built once per device by running exactly those two kernels on the 1024 unit spectra
-// (eq_basis), so every render's prologue is one small fp32 product (eq_response_basis)
-// instead of the fp64 design + one serial 8192-point FFT per slot. R is real and even:
-// bins k <= 4096 are computed and mirrored.
+// ---- FIR design as a product with a fixed basis -------------------------------------------
+// The zero-phase FIR (dsp.cpp:106-136) is LINEAR in the magnitudes m_q = exp(lm_q): its taps
+// are h[c + t] = h[c - t] = sum_q m_q D[q][t] with D[q][t] = w(c + t) c_q cos(2 pi q t / 2047)
+// / 2047 (c = 1023, c_0 = 1, c_q = 2, w the symmetric Hann) — eq_design's cosine sum as a
+// matrix. D (1024 x 1024, fp32 rounded from fp64 with exact-integer angle reduction) is built
+// once per device; a step with many slots computes every slot's 1024 distinct taps as one fp32
+// product (eq_basis_product<true>), then the 8192-point FFT per slot (eq_response): 0.45 ->
+// 0.19 ms per config-5 union. The 8192-bin response is linear in m too, R = A m, A[k][q] = the
+// response to the unit spectrum e_q in closed form (a sum of Dirichlet kernels, below): steps
+// with few slots (config 2's 16 tracks) take the product with A directly (4x the multiply-adds
+// of the taps product, but no per-slot FFT on the critical path).
 constexpr int kBasisTileK = 32;                                          // bins per CTA (one per lane)
-constexpr int kBasisK = ((kEqFft / 2 + 1 + kBasisTileK - 1) / kBasisTileK) * kBasisTileK;  // 4128
+constexpr int kTapsK = kEqHalf + 1;                                      // design basis: 1024 distinct taps t
+constexpr int kRespK = ((kEqFft / 2 + 1 + kBasisTileK - 1) / kBasisTileK) * kBasisTileK;  // response basis: 4128 bins
 constexpr int kBasisSlots = 16;                                          // slots per CTA
 constexpr int kBasisWarps = 16;                                          // q split over warps
 constexpr int kBasisQ = (kEqHalf + 1) / kBasisWarps;                     // 64 q per warp
 constexpr int kBasisTileBytes = (kEqHalf + 1) * kBasisTileK * 4;         // 128 KiB column block
 constexpr int kBasisMBytes = (kEqHalf + 1) * kBasisSlots * 4;            // magnitude tile, 64 KiB
 constexpr int kBasisSmem = kBasisTileBytes + kBasisMBytes;
-constexpr int kBasisMinSlots = 4;  // fewer slots: the 16.9 MB basis read costs more than the FFT design
+constexpr int kBasisMinSlots = 4;    // fewer slots: the fp64 cosine-sum design (eq_design) is as fast
+constexpr int kTapsMinSlots = 128;  // from here the design basis (4x fewer multiply-adds, then one FFT per
+                                    // slot); below, the response basis (the per-slot FFT's latency
+                                    // sat on config 2's critical path: 0.1945 -> 0.1986 ms)
 
 // m[group][q][16 slots] = exp(lm) in fp32 (0 past the last slot): the basis kernel's
 // magnitude tiles, built once per step instead of once per basis CTA (129 CTAs each
@@ -163,12 +171,16 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 // grid (kBasisK / 32, ceil(slots / 16)) x 512. The basis is stored tiled, [kBasisK / 32][1024 q]
-// [32 bins], so a CTA's column block is one contiguous 128 KiB run, copied into smem with the
-// slot group's magnitude tile (eq_mag_tiles). Lane l of warp w then sums bin k0 + l over q in
+// [32 taps], so a CTA's column block is one contiguous 128 KiB run, copied into smem with the
+// slot group's magnitude tile (eq_mag_tiles). Lane l of warp w then sums tap t0 + l over q in
 // [64 w, 64 w + 64) for 16 slots (conflict-free basis reads, broadcast float4 magnitude reads,
-// slot pairs in FFMA2); the 16 warp partials are added in warp order.
-__global__ void __launch_bounds__(512, 1) eq_response_basis(const float4* __restrict__ mtiles, int slots,
-                                                            const float* __restrict__ basis, float* resp) {
+// slot pairs in FFMA2); the 16 warp partials are added in warp order. Output: taps[slot][2048]
+// (h[c + t] and its mirror h[c - t]), eq_design's layout.
+// TAPS = false: the response basis [kRespK / 32][1024 q][32 bins], output resp[slot][8192]
+// (bins k <= 4096 and their mirrors 8192 - k).
+template <bool TAPS>
+__global__ void __launch_bounds__(512, 1) eq_basis_product(const float4* __restrict__ mtiles, int slots,
+                                                           const float* __restrict__ basis, float* out) {
   extern __shared__ __align__(128) unsigned char bsm[];
   float* tile = reinterpret_cast<float*>(bsm);                                    // [1024][32]
   float4* msm = reinterpret_cast<float4*>(bsm + kBasisTileBytes);                 // [1024][4] float4
@@ -229,12 +241,35 @@ __global__ void __launch_bounds__(512, 1) eq_response_basis(const float4* __rest
 #pragma unroll
     for (int ww = 1; ww < kBasisWarps; ++ww) v += part[(ww * kBasisSlots + s) * 32 + l];
     const int kk = blockIdx.x * kBasisTileK + l;
-    if (s < ns && kk <= kEqFft / 2) {
-      float* r = resp + static_cast<long>(s0 + s) * kEqFft;
+    if constexpr (TAPS) {
+      if (s < ns) {
+        float* h = out + static_cast<long>(s0 + s) * 2048;
+        h[kEqHalf + kk] = v;
+        if (kk > 0) h[kEqHalf - kk] = v;
+      }
+    } else if (s < ns && kk <= kEqFft / 2) {
+      float* r = out + static_cast<long>(s0 + s) * kEqFft;
       r[kk] = v;
       if (kk > 0 && kk < kEqFft / 2) r[kEqFft - kk] = v;
     }
   }
+}
+
+// Design-basis entries (fp64, rounded to fp32): tiled[(t / 32) * 1024 + q][t % 32] =
+// w(c + t) c_q cos(2 pi ((q t) mod 2047) / 2047) / 2047, the exact-integer angle reduction of
+// eq_design's cosine table, w(c + t) = 0.5 - 0.5 cos(2 pi (c + t) / 2046) as eq_design.
+__global__ void eq_taps_basis_build(float* tiled) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<long>(kTapsK) * (kEqHalf + 1)) return;
+  const int tl = static_cast<int>(i % kBasisTileK);
+  const int q = static_cast<int>((i / kBasisTileK) % (kEqHalf + 1));
+  const int t = static_cast<int>(i / (static_cast<long>(kBasisTileK) * (kEqHalf + 1))) * kBasisTileK + tl;
+  const long qt = (static_cast<long>(q) * t) % kN;
+  double sw, cw;
+  sincospi(2.0 * (kEqHalf + t) / (kN - 1), &sw, &cw);
+  const double w = 0.5 - 0.5 * cw;
+  const double cq = q == 0 ? 1.0 : 2.0;
+  tiled[i] = static_cast<float>(w * cq * cospi(2.0 * static_cast<double>(qt) / kN) / kN);
 }
 
 // Basis entries in closed form (fp64). With c = 1023, theta_q = 2 pi q / 2047 and
@@ -260,9 +295,9 @@ __device__ double eq_window_transform(long long n, long long d) {  // F(2 pi n /
   return 0.5 * eq_dirichlet(n, d) + 0.25 * eq_dirichlet(n + s, d) + 0.25 * eq_dirichlet(n - s, d);
 }
 // tiled[(k / 32) * 1024 + q][k % 32] = R_q[k] / 8192 (the response prescale), 0 for k > 4096.
-__global__ void eq_basis_build(float* tiled) {
+__global__ void eq_resp_basis_build(float* tiled) {
   const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= static_cast<long>(kBasisK) * (kEqHalf + 1)) return;
+  if (i >= static_cast<long>(kRespK) * (kEqHalf + 1)) return;
   const int kl = static_cast<int>(i % kBasisTileK);
   const int q = static_cast<int>((i / kBasisTileK) % (kEqHalf + 1));
   const int k = static_cast<int>(i / (static_cast<long>(kBasisTileK) * (kEqHalf + 1))) * kBasisTileK + kl;
@@ -390,7 +425,8 @@ __global__ void __launch_bounds__(EqWin<LOG, C>::kThreads, EqWin<LOG, C>::kMinBl
 void eq_setup() {
   static const bool done = [] {
     cudaFuncSetAttribute(eq_response, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqSmem);
-    cudaFuncSetAttribute(eq_response_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, kBasisSmem);
+    cudaFuncSetAttribute(eq_basis_product<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBasisSmem);
+    cudaFuncSetAttribute(eq_basis_product<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBasisSmem);
     for (auto fn : {eq_conv<13, float2>, eq_conv<12, float2>}) {
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqSmem);
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -404,31 +440,33 @@ void eq_setup() {
   (void)done;
 }
 
-// Per-device basis A^T [1024][kBasisK] (see eq_response_basis), built synchronously on first
-// use (ProcessorSet's constructor calls it, before any stream capture).
-const float* eq_basis(int device) {
+// Per-device bases (the design basis D [1024 q][1024 t] and the response basis A^T
+// [1024 q][4128 bins], both tiled by 32 columns), built synchronously on first use
+// (ProcessorSet's constructor calls it, before any stream capture).
+const float* eq_basis(int device, bool taps) {
   static std::mutex mu;
-  static std::map<int, float*> bases;
+  static std::map<std::pair<int, bool>, float*> bases;
   std::scoped_lock lock(mu);
-  auto it = bases.find(device);
+  auto it = bases.find({device, taps});
   if (it != bases.end()) return it->second;
   eq_setup();
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   float* basis = nullptr;
-  const long n = static_cast<long>(kBasisK) * (kEqHalf + 1);
+  const long n = static_cast<long>(taps ? kTapsK : kRespK) * (kEqHalf + 1);
   bool ok = cudaMalloc(&basis, sizeof(float) * n) == cudaSuccess;
   if (ok) {
-    eq_basis_build<<<static_cast<unsigned>((n + 255) / 256), 256>>>(basis);
+    if (taps) eq_taps_basis_build<<<static_cast<unsigned>((n + 255) / 256), 256>>>(basis);
+    else eq_resp_basis_build<<<static_cast<unsigned>((n + 255) / 256), 256>>>(basis);
     ok = cudaDeviceSynchronize() == cudaSuccess;
   }
   cudaSetDevice(prev);
   if (!ok) {
     cudaFree(basis);
-    throw std::runtime_error("EQ response basis build failed");
+    throw std::runtime_error("EQ basis build failed");
   }
-  bases.emplace(device, basis);
+  bases.emplace(std::make_pair(device, taps), basis);
   return basis;
 }
 
@@ -438,12 +476,25 @@ void launch_eq_prologue(const StepArgs& a, float* taps_ws, float* resp_ws, cudaS
   if (a.slots >= kBasisMinSlots) {
     int dev = 0;
     cudaGetDevice(&dev);
-    note_prologue_kernel(reinterpret_cast<const void*>(eq_mag_tiles));
-    note_prologue_kernel(reinterpret_cast<const void*>(eq_response_basis));
     const int groups = (a.slots + kBasisSlots - 1) / kBasisSlots;
+    note_prologue_kernel(reinterpret_cast<const void*>(eq_mag_tiles));
+    if (a.slots >= kTapsMinSlots) {
+      note_prologue_kernel(reinterpret_cast<const void*>(eq_basis_product<true>));
+      note_prologue_kernel(reinterpret_cast<const void*>(eq_response));
+      // the magnitude tiles (64 KiB per 16 slots) borrow the response region (32 KiB per slot),
+      // which eq_response overwrites only after the product has read them
+      auto* mt = reinterpret_cast<float4*>(resp_ws);
+      eq_mag_tiles<<<dim3(groups, (kEqHalf + 1) / 128), 128, 0, s>>>(a.params, a.slots, mt);
+      eq_basis_product<true><<<dim3(kTapsK / kBasisTileK, groups), 512, kBasisSmem, s>>>(mt, a.slots, eq_basis(dev, true),
+                                                                                        taps_ws);
+      eq_response<<<a.slots, 512, kEqSmem, s>>>(taps_ws, resp_ws, a.tw);
+      return;
+    }
+    note_prologue_kernel(reinterpret_cast<const void*>(eq_basis_product<false>));
     auto* mt = reinterpret_cast<float4*>(taps_ws);  // the taps region is unused on this path
     eq_mag_tiles<<<dim3(groups, (kEqHalf + 1) / 128), 128, 0, s>>>(a.params, a.slots, mt);
-    eq_response_basis<<<dim3(kBasisK / kBasisTileK, groups), 512, kBasisSmem, s>>>(mt, a.slots, eq_basis(dev), resp_ws);
+    eq_basis_product<false><<<dim3(kRespK / kBasisTileK, groups), 512, kBasisSmem, s>>>(mt, a.slots, eq_basis(dev, false),
+                                                                                       resp_ws);
     return;
   }
   // taps_ws holds [slots][2048] floats followed by [slots][1024] doubles of magnitudes.

@@ -33,8 +33,9 @@ constexpr int kEqHalf = 1023;
 constexpr int kEqValid = kEqFft - 2 * kEqHalf;
 void launch_eq_prologue(const StepArgs& a, float* taps_ws /*slots*2048*/, float* resp_ws /*slots*8192*/, cudaStream_t s);
 void launch_eq_main(const StepArgs& a, const float* resp_ws, cudaStream_t s);
-// Per-device response basis (1024 x 4128 fp32), built synchronously on first use.
-const float* eq_basis(int device);
+// Per-device EQ bases (taps: the FIR design basis 1024 x 1024; else the response basis
+// 1024 x 4128; fp32), built synchronously on first use.
+const float* eq_basis(int device, bool taps);
 
 // Compressor / noisegate: chained (decoupled look-back) scan of the energy envelope.
 constexpr int kDynThreads = 512;
