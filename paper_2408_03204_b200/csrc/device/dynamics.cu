@@ -456,8 +456,10 @@ constexpr int kStreamTile = kStreamThreads * kDynPerThread;
 constexpr int kStreamSmem = kStreamDepth * 2 * kStreamTile * static_cast<int>(sizeof(float));
 constexpr int kStreamCtasPerSm = 8;
 
-template <bool GATE, bool VEC>
-__global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) dyn_stream(StepArgs a, int env_taps, double floor_, PwEpi epi) {
+// NF: pointwise followers in the epilogue (compile time: their row pointers and coefficients
+// are per-CTA constants in registers; six CTAs per SM leave room for them).
+template <bool GATE, bool VEC, int NF>
+__global__ void __launch_bounds__(kStreamThreads, NF == 0 ? kStreamCtasPerSm : 6) dyn_stream(StepArgs a, int env_taps, double floor_, PwEpi epi) {
   constexpr int NT = kStreamThreads, TS = kStreamTile, NW = NT / 32;
   extern __shared__ __align__(128) unsigned char stream_smem[];
   float* ring = reinterpret_cast<float*>(stream_smem);  // [stage][channel][TS]
@@ -493,6 +495,14 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) dyn_stream(S
   }
   __syncthreads();
   const DynParams p = s_p;  // registers: the per-sample gain reads them every sample
+  float* fdst[NF > 0 ? NF : 1];
+  float fg0[NF > 0 ? NF : 1], fg1[NF > 0 ? NF : 1];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    fdst[f] = epi.dst[f] + static_cast<long>(s_epi.slot[f]) * a.rowstride + boff;
+    fg0[f] = s_epi.g0[f];
+    fg1[f] = s_epi.g1[f];
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int e0 = slot_e0(a, slot), e1 = slot_e1(a, slot);
   float* ol0 = a.dst + static_cast<long>(slot) * a.rowstride + boff;
@@ -595,8 +605,16 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) dyn_stream(S
       }
       reinterpret_cast<float4*>(ol)[q] = make_float4(yl[0], yl[1], yl[2], yl[3]);
       reinterpret_cast<float4*>(orr)[q] = make_float4(yr[0], yr[1], yr[2], yr[3]);
-      if (epi.n > 0) {
-        pw_epi_apply(epi, s_epi, a.rowstride, L, boff + n0 + 4 * q, yl, yr, true, 4);
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {  // the followers' arithmetic of pw_epi_apply
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          yl[k] = 0.f + yl[k];
+          yr[k] = 0.f + yr[k];
+          pw_op(epi.op[f], yl[k], yr[k], fg0[f], fg1[f]);
+        }
+        reinterpret_cast<float4*>(fdst[f] + n0)[q] = make_float4(yl[0], yl[1], yl[2], yl[3]);
+        reinterpret_cast<float4*>(fdst[f] + L + n0)[q] = make_float4(yr[0], yr[1], yr[2], yr[3]);
       }
     }
   }
@@ -1029,7 +1047,7 @@ std::size_t dyn_sync_bytes(int slots, int batch, long length) {
 }
 
 // The streaming scan (one CTA per sequence) when the step has most of a wave of sequences at
-// eight CTAs per SM, its slots read consecutive rows and the rows are 16-byte aligned (L % 4 == 0).
+// eight (six with epilogue followers) CTAs per SM, its slots read consecutive rows and the rows are 16-byte aligned (L % 4 == 0).
 // (mg_set_dyn_stream: 0 forces the chained scan, for tests.)
 static int g_dyn_stream = -1;
 void set_dyn_stream(int mode) { g_dyn_stream = mode; }
@@ -1043,10 +1061,6 @@ static int sm_count_dyn() {
 }
 bool dyn_stream_ok(const StepArgs& a, const PwEpi& epi) {
   if (g_dyn_stream == 0 || a.dense < 0 || a.length % 4 != 0) return false;
-  // With pointwise followers in the epilogue (the per-track noisegate) the streaming kernel ran
-  // out of registers and measured slower than the chained scan (1.71 vs 1.28 ms per config-5
-  // union); without (the per-track compressor) faster (0.67 vs 0.78 ms).
-  if (g_dyn_stream != 1 && epi.n > 0) return false;
   return g_dyn_stream == 1 || static_cast<long>(a.slots) * a.batch >= 6L * sm_count_dyn();
 }
 
@@ -1071,21 +1085,33 @@ void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double ene
   const long ne = envelope_taps < a.length ? envelope_taps : a.length;
   const bool vec = (a.length % 4 == 0) && (ne % 4 == 0);
   if (dyn_stream_ok(a, epi)) {
+    const dim3 sgrid(static_cast<unsigned>(seqs));
     static const bool attr = [] {
-      for (auto fn : {dyn_stream<false, false>, dyn_stream<false, true>, dyn_stream<true, false>, dyn_stream<true, true>}) {
+      for (auto fn : {dyn_stream<false, false, 0>, dyn_stream<false, false, 1>, dyn_stream<false, false, 2>,
+                      dyn_stream<false, false, 3>, dyn_stream<false, true, 0>, dyn_stream<false, true, 1>,
+                      dyn_stream<false, true, 2>, dyn_stream<false, true, 3>, dyn_stream<true, false, 0>,
+                      dyn_stream<true, false, 1>, dyn_stream<true, false, 2>, dyn_stream<true, false, 3>,
+                      dyn_stream<true, true, 0>, dyn_stream<true, true, 1>, dyn_stream<true, true, 2>,
+                      dyn_stream<true, true, 3>}) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamSmem);
       }
       return true;
     }();
     (void)attr;
-    const dim3 sgrid(static_cast<unsigned>(seqs));
+    auto go = [&](auto fn) { fn<<<sgrid, kStreamThreads, kStreamSmem, s>>>(a, envelope_taps, energy_floor, epi); };
+#define MGB_DYN_STREAM(G, V)                          \
+  switch (epi.n) {                                    \
+    case 0: go(dyn_stream<G, V, 0>); break;           \
+    case 1: go(dyn_stream<G, V, 1>); break;           \
+    case 2: go(dyn_stream<G, V, 2>); break;           \
+    default: go(dyn_stream<G, V, 3>); break;          \
+  }
     if (gate) {
-      if (vec) dyn_stream<true, true><<<sgrid, kStreamThreads, kStreamSmem, s>>>(a, envelope_taps, energy_floor, epi);
-      else dyn_stream<true, false><<<sgrid, kStreamThreads, kStreamSmem, s>>>(a, envelope_taps, energy_floor, epi);
+      if (vec) { MGB_DYN_STREAM(true, true) } else { MGB_DYN_STREAM(true, false) }
     } else {
-      if (vec) dyn_stream<false, true><<<sgrid, kStreamThreads, kStreamSmem, s>>>(a, envelope_taps, energy_floor, epi);
-      else dyn_stream<false, false><<<sgrid, kStreamThreads, kStreamSmem, s>>>(a, envelope_taps, energy_floor, epi);
+      if (vec) { MGB_DYN_STREAM(false, true) } else { MGB_DYN_STREAM(false, false) }
     }
+#undef MGB_DYN_STREAM
     return;
   }
   const dim3 grid(static_cast<unsigned>(total));
