@@ -164,6 +164,10 @@ void mg_set_conv_fuse(int32_t mode);
  * CTA, others run the chained look-back scan), 0 always chained, 1 streaming wherever legal
  * (dense steps, L % 4 == 0). Process-wide; results agree to fp64 rounding of the envelope. */
 void mg_set_dyn_stream(int32_t mode);
+/* A compressor / noisegate step followed by one reading exactly its rows (a console track's
+ * compressor -> noisegate), both on the streaming scan, runs as ONE kernel (-1 / 1, default);
+ * 0 runs them as two launches (tests). Process-wide. */
+void mg_set_dyn_pair(int32_t mode);
 
 /* Transform-size switch for the long convolutions (tests): 0 (default) picks per step the
  * cheapest segmented overlap-save size (one next_pow2(L + taps - 1) transform, as the

@@ -85,6 +85,7 @@ _sig("mg_backward_workspace_bytes", _i32, _vp, _vp, _i32, _i64, _P(_u64))
 _sig("mg_render_backward_arena", _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp)
 _sig("mg_set_conv_fuse", None, _i32)
 _sig("mg_set_dyn_stream", None, _i32)
+_sig("mg_set_dyn_pair", None, _i32)
 _sig("mg_set_conv_log", None, _i32)
 _sig("mg_conv_geometry", _i32, _i64, _i64, _vp)
 _sig("mg_set_fft_precision", None, _i32)
@@ -635,6 +636,12 @@ def set_dyn_stream(mode: int) -> None:
     """mg_set_dyn_stream: -1 auto (default), 0 chained look-back scan, 1 streaming scan
     (one CTA per sequence) wherever legal."""
     _lib.mg_set_dyn_stream(int(mode))
+
+
+def set_dyn_pair(mode: int) -> None:
+    """mg_set_dyn_pair: a compressor / noisegate step followed by one reading exactly its rows
+    runs as one streaming kernel (-1 / 1, default) or two (0)."""
+    _lib.mg_set_dyn_pair(int(mode))
 
 
 def conv_geometry(length: int, taps: int) -> Dict[str, int]:

@@ -22,6 +22,7 @@ void launch_mse_loss_grad(const float* y, const float* target, long n, float* gr
 void launch_sgd_step(bool dynamics, double* table, const double* grad, long n, double lr, cudaStream_t s);
 void set_conv_fuse(int mode);
 void set_dyn_stream(int mode);
+void set_dyn_pair(int mode);
 void set_conv_log(int log_n);
 void set_fft_fp64(bool on);
 void conv_geometry(long length, long taps, long* out);
@@ -489,6 +490,7 @@ int32_t mg_render_backward_arena(const mg_plan* p, const mg_processors* procs, c
 
 void mg_set_conv_fuse(int32_t mode) { mgb::set_conv_fuse(mode); }
 void mg_set_dyn_stream(int32_t mode) { mgb::set_dyn_stream(mode); }
+void mg_set_dyn_pair(int32_t mode) { mgb::set_dyn_pair(mode); }
 
 void mg_set_conv_log(int32_t log_n) { mgb::set_conv_log(log_n); }
 

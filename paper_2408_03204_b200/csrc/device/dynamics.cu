@@ -620,6 +620,227 @@ __global__ void __launch_bounds__(kStreamThreads, NF == 0 ? kStreamCtasPerSm : 6
   }
 }
 
+// Two streaming scans in one CTA: step A (compressor or noisegate) and step B reading exactly
+// A's output rows (slot s of B reads row A.store_begin + s: a console track's compressor ->
+// noisegate). Per tile the CTA scans A on its streamed input, stores A's output and keeps it
+// in registers, then scans B on that output (its own running carry) and stores B's output and
+// B's epilogue followers: A's rows are never read back (one read of the track signal for
+// both), and one launch instead of two. Arithmetic per sample as dyn_scan / dyn_stream
+// (B's gather of one row is 0 + y, kept). The block scan of one tile, shared by both stages:
+// returns this thread's start state and advances the CTA's carry (one barrier).
+template <int NW>
+__device__ __forceinline__ double stream_block_scan(const double (&drive)[kDynPerThread], const DynParams& p,
+                                                    double& carry, double (*wA)[NW], double (*wB)[NW], int t,
+                                                    int lane, int warp) {
+  double B = 0.0;
+#pragma unroll
+  for (int k = 0; k < kDynPerThread; ++k) B = fma(p.da, B, drive[k]);
+  double A = p.da16;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const double Ap = __shfl_up_sync(0xffffffffu, A, off);
+    const double Bp = __shfl_up_sync(0xffffffffu, B, off);
+    if (lane >= off) compose(A, B, Ap, Bp);
+  }
+  if (lane == 31) {
+    wA[t & 1][warp] = A;
+    wB[t & 1][warp] = B;
+  }
+  double xA = __shfl_up_sync(0xffffffffu, A, 1), xB = __shfl_up_sync(0xffffffffu, B, 1);
+  if (lane == 0) {
+    xA = 1.0;
+    xB = 0.0;
+  }
+  __syncthreads();
+  double pA = 1.0, pB = 0.0, tB = 0.0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const double Aw = wA[t & 1][w], Bw = wB[t & 1][w];
+    if (w < warp) {
+      pB = fma(Aw, pB, Bw);
+      pA = Aw * pA;
+    }
+    tB = fma(Aw, tB, Bw);
+  }
+  compose(xA, xB, pA, pB);
+  const double g = fma(xA, carry, xB);
+  carry = fma(p.datile, carry, tB);
+  return g;
+}
+
+// drive[k] = (1-a) (mid^2 - a^Ne mo^2) for this thread's samples (mo: mid at n - Ne).
+__device__ __forceinline__ void stream_drive(const float (&mid)[kDynPerThread], const float (&mo)[kDynPerThread],
+                                             const DynParams& p, double (&drive)[kDynPerThread]) {
+#pragma unroll
+  for (int k = 0; k < kDynPerThread; ++k) {
+    const double m = mid[k], o = mo[k];
+    drive[k] = p.daN != 0.0 ? p.doma * (m * m - p.daN * (o * o)) : p.doma * (m * m);
+  }
+}
+
+template <bool GATE1, bool GATE2, int NF>
+__global__ void __launch_bounds__(kStreamThreads, 6) dyn_stream_pair(StepArgs a1, StepArgs a2, int env_taps,
+                                                                     double floor_, PwEpi epi) {
+  constexpr int NT = kStreamThreads, TS = kStreamTile, NW = NT / 32, K = kDynPerThread;
+  extern __shared__ __align__(128) unsigned char stream_smem[];
+  float* ring = reinterpret_cast<float*>(stream_smem);  // [stage][channel][TS]
+  __shared__ __align__(8) unsigned long long bar[kStreamDepth];
+  __shared__ double wA1[2][NW], wB1[2][NW], wA2[2][NW], wB2[2][NW];
+  __shared__ DynParams s_p1, s_p2;
+  __shared__ PwEpiSlots s_epi;
+  const int seq = blockIdx.x;
+  const int slot = seq / a1.batch, b = seq - slot * a1.batch;
+  const long L = a1.length;
+  const long boff = static_cast<long>(b) * 2 * L;
+  const float* in = a1.src + (static_cast<long>(a1.dense) + slot) * a1.rowstride + boff;
+  float* y1 = a1.dst + static_cast<long>(slot) * a1.rowstride + boff;  // A's output row (B's input)
+  float* y2 = a2.dst + static_cast<long>(slot) * a2.rowstride + boff;
+  const int tiles = static_cast<int>((L + TS - 1) / TS);
+  auto issue = [&](int t) {
+    const int st = t % kStreamDepth;
+    const long n0 = static_cast<long>(t) * TS;
+    const uint32_t bytes = static_cast<uint32_t>(min(static_cast<long>(TS), L - n0)) * 4u;
+    float* dst = ring + st * 2 * TS;
+    mbar_expect_tx(&bar[st], 2 * bytes);
+    bulk_g2s(dst, in + n0, bytes, &bar[st]);
+    bulk_g2s(dst + TS, in + L + n0, bytes, &bar[st]);
+  };
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int d = 0; d < kStreamDepth; ++d) mbar_init(&bar[d], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int t = 0; t < kStreamDepth && t < tiles; ++t) issue(t);
+  }
+  if (threadIdx.x < 32) {
+    derive_params(a1.params + 4L * slot, env_taps, floor_, L, threadIdx.x, &s_p1, TS, GATE1);
+  } else if (threadIdx.x < 64) {
+    derive_params(a2.params + 4L * slot, env_taps, floor_, L, threadIdx.x - 32, &s_p2, TS, GATE2);
+    if (epi.n > 0 && threadIdx.x == 33) pw_epi_slots(epi, slot, s_epi);
+  }
+  __syncthreads();
+  float* fdst[NF > 0 ? NF : 1];
+  float fg0[NF > 0 ? NF : 1], fg1[NF > 0 ? NF : 1];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    fdst[f] = epi.dst[f] + static_cast<long>(s_epi.slot[f]) * a2.rowstride + boff;
+    fg0[f] = s_epi.g0[f];
+    fg1[f] = s_epi.g1[f];
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double carry1 = 0.0, carry2 = 0.0;
+  for (int t = 0; t < tiles; ++t) {
+    const int st = t % kStreamDepth;
+    const long n0 = static_cast<long>(t) * TS + static_cast<long>(threadIdx.x) * K;
+    const bool live = n0 < L;  // L % 4 == 0: a live thread has 4 or 8 valid samples
+    const bool full = n0 + K <= L;
+    mbar_wait(&bar[st], static_cast<uint32_t>((t / kStreamDepth) & 1));
+    const float* sl = ring + st * 2 * TS + threadIdx.x * K;
+    float ul[K], ur[K];
+    double drive[K];
+    {
+      float mid[K], mo[K];
+#pragma unroll
+      for (int q = 0; q < K / 4; ++q) {
+        float4 l = make_float4(0.f, 0.f, 0.f, 0.f), r = l;
+        if (live && (q == 0 || full)) {
+          l = *reinterpret_cast<const float4*>(sl + 4 * q);
+          r = *reinterpret_cast<const float4*>(sl + TS + 4 * q);
+        }
+        const float lv[4] = {0.f + l.x, 0.f + l.y, 0.f + l.z, 0.f + l.w}, rv[4] = {0.f + r.x, 0.f + r.y, 0.f + r.z, 0.f + r.w};
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+          ul[4 * q + k4] = lv[k4];
+          ur[4 * q + k4] = rv[k4];
+          mid[4 * q + k4] = lv[k4] + rv[k4];
+        }
+      }
+      const DynParams& p1 = s_p1;
+#pragma unroll
+      for (int k = 0; k < K; ++k) mo[k] = 0.f;
+      if (p1.daN != 0.0) {
+        if ((p1.Ne & 3) == 0) load_mid<true>(a1, slot, slot + 1, b, live ? n0 - p1.Ne : L, mo);
+        else load_mid<false>(a1, slot, slot + 1, b, live ? n0 - p1.Ne : L, mo);
+      }
+      stream_drive(mid, mo, p1, drive);
+    }
+    double g = stream_block_scan<NW>(drive, s_p1, carry1, wA1, wB1, t, lane, warp);
+    // Every thread of tile t - 1 is past its output pass: refill its stage two tiles ahead.
+    if (threadIdx.x == 0 && t >= 1 && t - 1 + kStreamDepth < tiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(t - 1 + kStreamDepth);
+    }
+    // Stage A: gains, A's output (kept in ul / ur), stored.
+    {
+      const DynParams& p1 = s_p1;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        g = fma(p1.da, g, drive[k]);
+        const float gn = gain_of<GATE1>(static_cast<float>(g), p1);
+        ul[k] *= gn;
+        ur[k] *= gn;
+      }
+    }
+    if (live) {
+#pragma unroll
+      for (int q = 0; q < K / 4; ++q) {
+        if (q > 0 && !full) break;
+        reinterpret_cast<float4*>(y1 + n0)[q] = make_float4(ul[4 * q], ul[4 * q + 1], ul[4 * q + 2], ul[4 * q + 3]);
+        reinterpret_cast<float4*>(y1 + L + n0)[q] = make_float4(ur[4 * q], ur[4 * q + 1], ur[4 * q + 2], ur[4 * q + 3]);
+      }
+    }
+    // Stage B on A's output: B's gather of one row is 0 + y.
+    {
+      const DynParams& p2 = s_p2;
+      float mid[K], mo[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        ul[k] = 0.f + ul[k];
+        ur[k] = 0.f + ur[k];
+        mid[k] = live && (k < 4 || full) ? ul[k] + ur[k] : 0.f;
+        mo[k] = 0.f;
+      }
+      if (p2.daN != 0.0) {  // A's output at n - Ne: this CTA stored it (at least Ne samples back)
+        __syncthreads();
+        if ((p2.Ne & 3) == 0) load_mid<true>(a2, slot, slot + 1, b, live ? n0 - p2.Ne : L, mo);
+        else load_mid<false>(a2, slot, slot + 1, b, live ? n0 - p2.Ne : L, mo);
+      }
+      stream_drive(mid, mo, p2, drive);
+    }
+    g = stream_block_scan<NW>(drive, s_p2, carry2, wA2, wB2, t, lane, warp);
+    if (!live) continue;
+    {
+      const DynParams& p2 = s_p2;
+#pragma unroll
+      for (int q = 0; q < K / 4; ++q) {
+        if (q > 0 && !full) break;
+        float yl[4], yr[4];
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+          const int k = 4 * q + k4;
+          g = fma(p2.da, g, drive[k]);
+          const float gn = gain_of<GATE2>(static_cast<float>(g), p2);
+          yl[k4] = gn * ul[k];
+          yr[k4] = gn * ur[k];
+        }
+        reinterpret_cast<float4*>(y2 + n0)[q] = make_float4(yl[0], yl[1], yl[2], yl[3]);
+        reinterpret_cast<float4*>(y2 + L + n0)[q] = make_float4(yr[0], yr[1], yr[2], yr[3]);
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            yl[k4] = 0.f + yl[k4];
+            yr[k4] = 0.f + yr[k4];
+            pw_op(epi.op[f], yl[k4], yr[k4], fg0[f], fg1[f]);
+          }
+          reinterpret_cast<float4*>(fdst[f] + n0)[q] = make_float4(yl[0], yl[1], yl[2], yl[3]);
+          reinterpret_cast<float4*>(fdst[f] + L + n0)[q] = make_float4(yr[0], yr[1], yr[2], yr[3]);
+        }
+      }
+    }
+  }
+}
+
 // ---- backward (parameter gradients; no reference counterpart, see backward.cu) -------------
 //
 // Given dy (gathered over the consumers' input gradients) and the forward quantities
@@ -1050,7 +1271,9 @@ std::size_t dyn_sync_bytes(int slots, int batch, long length) {
 // eight (six with epilogue followers) CTAs per SM, its slots read consecutive rows and the rows are 16-byte aligned (L % 4 == 0).
 // (mg_set_dyn_stream: 0 forces the chained scan, for tests.)
 static int g_dyn_stream = -1;
+static int g_dyn_pair = -1;
 void set_dyn_stream(int mode) { g_dyn_stream = mode; }
+void set_dyn_pair(int mode) { g_dyn_pair = mode; }
 static int sm_count_dyn() {
   static const int n = [] {
     int dev = 0, v = 148;
@@ -1062,6 +1285,51 @@ static int sm_count_dyn() {
 bool dyn_stream_ok(const StepArgs& a, const PwEpi& epi) {
   if (g_dyn_stream == 0 || a.dense < 0 || a.length % 4 != 0) return false;
   return g_dyn_stream == 1 || static_cast<long>(a.slots) * a.batch >= 6L * sm_count_dyn();
+}
+
+bool dyn_pair_shape(int slots, int batch, long length) {
+  return g_dyn_stream != 0 && g_dyn_pair != 0 && length % 4 == 0 &&
+         (g_dyn_stream == 1 || static_cast<long>(slots) * batch >= 6L * sm_count_dyn());
+}
+
+bool dyn_pair_ok(const StepArgs& a1, const StepArgs& a2) {
+  if (g_dyn_stream == 0 || g_dyn_pair == 0 || !dyn_stream_ok(a1, PwEpi{}) || !dyn_stream_ok(a2, PwEpi{})) return false;
+  // B reads exactly A's rows slot by slot
+  return a1.slots == a2.slots && a1.batch == a2.batch && a1.length == a2.length &&
+         a2.src + static_cast<long>(a2.dense) * a2.rowstride == a1.dst;
+}
+
+void launch_dynamics_pair(bool gate1, bool gate2, const StepArgs& a1, const StepArgs& a2, int envelope_taps,
+                          double energy_floor, cudaStream_t s, const PwEpi& epi) {
+  const long seqs = static_cast<long>(a1.slots) * a1.batch;
+  if (seqs == 0 || a1.length == 0) return;
+  static const bool attr = [] {
+    for (auto fn : {dyn_stream_pair<false, false, 0>, dyn_stream_pair<false, false, 1>, dyn_stream_pair<false, false, 2>,
+                    dyn_stream_pair<false, false, 3>, dyn_stream_pair<false, true, 0>, dyn_stream_pair<false, true, 1>,
+                    dyn_stream_pair<false, true, 2>, dyn_stream_pair<false, true, 3>, dyn_stream_pair<true, false, 0>,
+                    dyn_stream_pair<true, false, 1>, dyn_stream_pair<true, false, 2>, dyn_stream_pair<true, false, 3>,
+                    dyn_stream_pair<true, true, 0>, dyn_stream_pair<true, true, 1>, dyn_stream_pair<true, true, 2>,
+                    dyn_stream_pair<true, true, 3>}) {
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamSmem);
+    }
+    return true;
+  }();
+  (void)attr;
+  const dim3 grid(static_cast<unsigned>(seqs));
+  auto go = [&](auto fn) { fn<<<grid, kStreamThreads, kStreamSmem, s>>>(a1, a2, envelope_taps, energy_floor, epi); };
+#define MGB_DYN_PAIR(G1, G2)                         \
+  switch (epi.n) {                                   \
+    case 0: go(dyn_stream_pair<G1, G2, 0>); break;   \
+    case 1: go(dyn_stream_pair<G1, G2, 1>); break;   \
+    case 2: go(dyn_stream_pair<G1, G2, 2>); break;   \
+    default: go(dyn_stream_pair<G1, G2, 3>); break;  \
+  }
+  if (gate1) {
+    if (gate2) { MGB_DYN_PAIR(true, true) } else { MGB_DYN_PAIR(true, false) }
+  } else {
+    if (gate2) { MGB_DYN_PAIR(false, true) } else { MGB_DYN_PAIR(false, false) }
+  }
+#undef MGB_DYN_PAIR
 }
 
 void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double energy_floor, void* ws,

@@ -319,6 +319,20 @@ int epi_followers(const DevicePlan& plan, std::size_t k, int batch, long length)
   return n;
 }
 
+// Steps k, k+1 run as one fused streaming scan (launch_dynamics_pair): both compressor /
+// noisegate, dense, step k+1 reading step k's rows slot by slot (a console track's compressor
+// -> noisegate).
+bool dyn_pair(const DevicePlan& plan, std::size_t k, int batch, long length) {
+  const RenderData& rd = plan.data();
+  if (k + 1 >= rd.steps.size()) return false;
+  auto dyn = [](NodeType t) { return t == NodeType::Compressor || t == NodeType::Noisegate; };
+  const StepIndex& a = rd.steps[k];
+  const StepIndex& b = rd.steps[k + 1];
+  const int slots = a.store_end - a.store_begin;
+  return dyn(a.type) && dyn(b.type) && slots == b.store_end - b.store_begin && plan.dense_src(static_cast<int>(k)) >= 0 &&
+         plan.dense_src(static_cast<int>(k + 1)) == a.store_begin && mgb::dyn_pair_shape(slots, batch, length);
+}
+
 std::size_t step_ws_bytes(NodeType t, int slots, int batch, long length, const ProcessorSet& p) {
   return align256(prologue_bytes(t, slots, length, p)) + align256(sync_bytes(t, slots, batch, length)) +
          main_bytes(t, slots, batch, length, p);
@@ -634,6 +648,11 @@ std::size_t DevicePlan::backward_workspace_bytes(int batch, long length, const P
 int DevicePlan::kernels_per_render(int batch, long length) const {
   int k = 0;
   for (std::size_t i = 0; i < rd_.steps.size();) {
+    if (dyn_pair(*this, i, batch, length)) {
+      k += 1;
+      i += 2 + static_cast<std::size_t>(epi_followers(*this, i + 1, batch, length));
+      continue;
+    }
     const int n = chain_length(rd_, i, batch, length);
     k += n > 1 ? 1 : step_kernels(rd_.steps[i].type);
     i += static_cast<std::size_t>(n > 1 ? n : 1 + epi_followers(*this, i, batch, length));
@@ -644,7 +663,8 @@ int DevicePlan::kernels_per_render(int batch, long length) const {
 void DevicePlan::step_owners(int batch, long length, int* owner) const {
   for (std::size_t i = 0; i < rd_.steps.size();) {
     const int n = chain_length(rd_, i, batch, length);
-    const std::size_t span = static_cast<std::size_t>(n > 1 ? n : 1 + epi_followers(*this, i, batch, length));
+    std::size_t span = static_cast<std::size_t>(n > 1 ? n : 1 + epi_followers(*this, i, batch, length));
+    if (dyn_pair(*this, i, batch, length)) span = 2 + static_cast<std::size_t>(epi_followers(*this, i + 1, batch, length));
     for (std::size_t j = i; j < i + span; ++j) owner[j] = static_cast<int>(i);
     i += span;
   }
@@ -757,6 +777,24 @@ void render_arena(const DevicePlan& plan, const ProcessorSet& procs, const doubl
       cuda_check(cudaEventRecord(le[2 * k + 1], lane), "event");
       cuda_check(cudaStreamWaitEvent(stream, le[2 * k + 1], 0), "wait");
       ++k;
+      continue;
+    }
+    if (!step_events && dyn_pair(plan, k, batch, length) && mgb::dyn_pair_ok(args[k], args[k + 1])) {
+      // Steps k, k+1: one streaming kernel scans both (the second reads the first's rows);
+      // the second step's pointwise followers ride in its epilogue.
+      const std::size_t j = k + 1;
+      mgb::PwEpi e2{};
+      e2.n = epi_followers(plan, j, batch, length);
+      for (int f = 0; f < e2.n; ++f) {
+        const std::size_t q = j + 1 + static_cast<std::size_t>(f);
+        e2.op[f] = point_op(rd.steps[q].type);
+        e2.dst[f] = args[q].dst;
+        e2.map[f] = plan.follow_map(static_cast<int>(q));
+        e2.params[f] = args[q].params;
+      }
+      mgb::launch_dynamics_pair(t == NodeType::Noisegate, rd.steps[j].type == NodeType::Noisegate, args[k], args[j],
+                                procs.config().envelope_taps, procs.config().energy_floor, stream, e2);
+      k = j + static_cast<std::size_t>(e2.n);
       continue;
     }
     if (!step_events && k + 1 < rd.steps.size() && lay.shared[k + 1]) {

@@ -52,6 +52,15 @@ void launch_dynamics(bool gate, const StepArgs& a, int envelope_taps, double ene
 // (dense, L % 4 == 0), -1 automatic (tests).
 bool dyn_stream_ok(const StepArgs& a, const PwEpi& epi);
 void set_dyn_stream(int mode);
+// A compressor / noisegate step A followed by one (B) reading exactly A's rows slot by slot,
+// both streaming-eligible: one kernel scans both (A's rows are written, never read back);
+// `epi` = B's epilogue followers. set_dyn_pair(0) runs them as two launches (tests).
+bool dyn_pair_ok(const StepArgs& a1, const StepArgs& a2);
+// The shape part of dyn_pair_ok (plans decide their launch structure with it).
+bool dyn_pair_shape(int slots, int batch, long length);
+void launch_dynamics_pair(bool gate1, bool gate2, const StepArgs& a1, const StepArgs& a2, int envelope_taps,
+                          double energy_floor, cudaStream_t s, const PwEpi& epi);
+void set_dyn_pair(int mode);
 
 // Backward of a compressor / noisegate step: `bw` gathers dy over the consumers' input
 // gradients (transposed CSR) and stores du into bw.dst; parameter gradients [slots][4] fp64

@@ -670,3 +670,39 @@ def test_shared_signal_spectra_bit_exact(mg, ref, prune, L, batch):
         mg.set_conv_fuse(-1)
     want = ref.Plan(t, e, 1).render(params, src)
     assert rel(shared[rd.output_begin:].cpu().numpy(), want) < TOL
+
+
+@pytest.mark.parametrize("taps,L", [(None, 20000), (4096, 20000), (4097, 12000), (600, 9000)])
+def test_fused_compressor_gate_scan(mg, ref, taps, L):
+    # A console track's compressor -> noisegate (-> imager -> gain) as ONE streaming kernel
+    # (forced onto the streaming path; automatic for config-5-sized steps): matches the
+    # reference, the two-launch streaming path and the chained scans; envelope_taps < L
+    # exercises both stages' a^Ne re-gathers (600: within the same tile).
+    import torch
+    from paper_2408_03204_b200.device import DeviceRenderer
+    t, e = ref.console(5, 0.3, 21)
+    params = ref.random_legal_params(t, e, 22)
+    for ty in (5, 6):
+        params[ty][:, 0] = np.linspace(0.99, 0.9999, len(params[ty]))
+    rd = mg.compute_render_data(make(mg, t, e))
+    cfg = {} if taps is None else {"envelope_taps": taps}
+    procs = mg.ProcessorSet(**cfg)
+    src = np.random.default_rng(23).uniform(-1, 1, size=(rd.num_inputs, 1, 2, L)) * np.linspace(0.01, 1, L)
+    dr = DeviceRenderer(rd, procs, 1, L, rd.reorder_params(params))
+    dr.sources.copy_(torch.as_tensor(src, dtype=torch.float32))
+    arenas = {}
+    try:
+        for mode in ((1, 1), (1, 0), (0, 0)):
+            mg.set_dyn_stream(mode[0])
+            mg.set_dyn_pair(mode[1])
+            dr.arena[rd.num_inputs:].fill_(float("nan"))
+            dr.render()
+            torch.cuda.synchronize()
+            arenas[mode] = dr.arena.clone()
+    finally:
+        mg.set_dyn_stream(-1)
+        mg.set_dyn_pair(-1)
+    assert torch.equal(arenas[(1, 1)].view(torch.int32), arenas[(1, 0)].view(torch.int32))
+    want = ref.Plan(t, e, 1).render(params, src, **cfg)
+    for mode, a in arenas.items():
+        assert rel(a[rd.output_begin:].cpu().numpy(), want) < TOL, mode

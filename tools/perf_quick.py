@@ -1,6 +1,6 @@
 """Quick device-time check of the two headline workloads (A/B between builds):
 config 2 (captured render, L2 flushed between iterations) and config 5 (512 graphs as 8
-captured unions). Usage: PYTHONPATH=. python tools/perf_quick.py [c2] [c5] [dyn=0|1]"""
+captured unions). Usage: PYTHONPATH=. python tools/perf_quick.py [c2] [c5] [dyn=0|1] [pair=0|1]"""
 import json
 import sys
 
@@ -11,10 +11,12 @@ import bench
 import paper_2408_03204_b200 as mg
 import workloads as wl
 
-what = [w for w in sys.argv[1:] if not w.startswith("dyn=")] or ["c2", "c5"]
+what = [w for w in sys.argv[1:] if "=" not in w] or ["c2", "c5"]
 for w in sys.argv[1:]:
     if w.startswith("dyn="):  # dyn=0: chained look-back scans only (A/B of the streaming scan)
         mg.set_dyn_stream(int(w[4:]))
+    if w.startswith("pair="):  # pair=0: compressor -> noisegate as two streaming launches
+        mg.set_dyn_pair(int(w[5:]))
 dev = torch.device("cuda", 0)
 procs = mg.ProcessorSet()
 res = {}
