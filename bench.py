@@ -165,7 +165,7 @@ def kernel_family(name):
     if "delay_cols" in name:  # the delay kernel's column stage as a sparse direct DFT
         return "delay_cols"
     for key in ("rows_conv_fk", "rows_conv", "rows_spec", "cols_fwd", "cols_inv", "eq_conv", "dyn_scan",
-                "pointwise_wide", "pointwise_chain", "pointwise", "reverb_ir", "eq_response_basis", "eq_mag_tiles",
+                "pointwise_wide", "pointwise_chain", "pointwise", "reverb_ir", "eq_basis_product", "eq_mag_tiles",
                 "delay_taps", "eq_design", "eq_response", "eq_mags", "param_gather"):
         if key in name:
             return key
