@@ -23,7 +23,6 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmgb200.so")
 # Diagnostics only (same-box A/B timing of two builds): load another build of the library.
-LIB_PATH = os.environ.get("MGB_LIB_OVERRIDE") or LIB_PATH
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
