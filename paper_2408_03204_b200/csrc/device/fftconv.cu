@@ -39,10 +39,12 @@ template <typename CT> struct ColCfg {
 // loaded where it is used (prefetching it into registers spilled; cp.async into shared memory
 // measured no faster).
 constexpr int kRconvThreadsPerSm = 1024;
-// Resident CTAs per SM rows_bwd is compiled for: 2 up to 256-point rows (3 spills, measured
-// slower); 1 from 1024 points, whose 256/512 threads need more than 128/64 registers.
+// Resident CTAs per SM rows_bwd is compiled for: 4 up to 512-point rows (at 2 the 512-point
+// kernel took 178 registers, 2 CTAs of 128 threads per SM: 0.76 -> 0.53 ms per config-4 launch
+// at 4 with 44 B of spills; 6 spilled 700 B and was slower); 1 from 1024 points, whose 256/512
+// threads need more than 128/64 registers.
 template <int LN2>
-constexpr int rbwd_min_blocks() { return LN2 >= 10 ? 1 : 2; }
+constexpr int rbwd_min_blocks() { return LN2 >= 10 ? 1 : 4; }
 
 inline std::size_t align256(std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255); }
 
