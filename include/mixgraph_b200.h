@@ -107,6 +107,12 @@ int32_t mg_plan_step_owners(const mg_plan* plan, int32_t batch, int64_t length, 
  * tests; no reference counterpart (the reference transforms every input, dsp.cpp:64-86). */
 int32_t mg_plan_shared_pairs(const mg_plan* plan, const mg_processors* procs, int32_t batch, int64_t length,
                              int32_t* pairs);
+/* Host-side plan analysis (no device needed), num_steps entries each: share_pairs[k] = slots
+ * of step k that pair with a slot of step k-1 on a common single source row (both long
+ * convolutions; used when the transforms match, mg_plan_shared_pairs), reads_prev_rows[k] = 1
+ * when step k reads exactly step k-1's rows slot by slot (a compressor -> noisegate pair runs
+ * as one kernel then). */
+int32_t mg_plan_fusion_candidates(const mg_plan* plan, int32_t* share_pairs, int32_t* reads_prev_rows);
 int32_t mg_render_arena(const mg_plan* plan, const mg_processors* procs, const double* const* d_tables, float* d_arena,
                         int32_t batch, int64_t length, void* d_workspace, uint64_t workspace_bytes, void* stream);
 

@@ -70,6 +70,7 @@ _sig("mg_plan_workspace_bytes", _i32, _vp, _vp, _i32, _i64, _P(_u64))
 _sig("mg_plan_kernel_count", _i32, _vp, _i32, _i64, _P(_i32))
 _sig("mg_plan_step_owners", _i32, _vp, _i32, _i64, _vp)
 _sig("mg_plan_shared_pairs", _i32, _vp, _vp, _i32, _i64, _vp)
+_sig("mg_plan_fusion_candidates", _i32, _vp, _vp, _vp)
 _sig("mg_render_arena", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp)
 _sig("mg_render_arena_profiled", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp, _vp, _i32)
 _sig("mg_profile_steps", _i32, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _u64, _vp, _i32, _vp)
@@ -452,6 +453,15 @@ class RenderData:
         out = np.zeros(self.num_steps, dtype=np.int32)
         _check(_lib.mg_plan_shared_pairs(self._h, procs.handle, batch, length, out.ctypes.data_as(_vp)))
         return out
+
+    def fusion_candidates(self):
+        """Host-side plan analysis (mg_plan_fusion_candidates): (share_pairs, reads_prev_rows),
+        per step — slots pairing with the previous conv step on a common source row, and
+        whether the step reads exactly the previous step's rows slot by slot."""
+        a = np.zeros(self.num_steps, dtype=np.int32)
+        b = np.zeros(self.num_steps, dtype=np.int32)
+        _check(_lib.mg_plan_fusion_candidates(self._h, a.ctypes.data_as(_vp), b.ctypes.data_as(_vp)))
+        return a, b.astype(bool)
 
     def step_owners(self, batch: int, length: int) -> np.ndarray:
         """owner[k] = the step whose kernel launch computes step k (itself, the head of a fused

@@ -357,6 +357,21 @@ int32_t mg_plan_kernel_count(const mg_plan* p, int32_t batch, int64_t length, in
   return guarded([&] { *count = device_plan(p, nullptr).kernels_per_render(batch, static_cast<long>(length)); });
 }
 
+int32_t mg_plan_fusion_candidates(const mg_plan* p, int32_t* share_pairs, int32_t* reads_prev_rows) {
+  return guarded([&] {
+    const DevicePlan plan(p->rd, DevicePlan::Deferred{});  // host-side analysis only, no device
+    for (std::size_t k = 0; k < p->rd.steps.size(); ++k) {
+      const int ks = static_cast<int>(k);
+      share_pairs[k] = plan.shares(ks) ? plan.share_info(ks).pairs : 0;
+      reads_prev_rows[k] = k > 0 && plan.dense_src(ks) >= 0 && plan.dense_src(ks) == p->rd.steps[k - 1].store_begin &&
+                                   p->rd.steps[k].store_end - p->rd.steps[k].store_begin ==
+                                       p->rd.steps[k - 1].store_end - p->rd.steps[k - 1].store_begin
+                               ? 1
+                               : 0;
+    }
+  });
+}
+
 int32_t mg_plan_shared_pairs(const mg_plan* p, const mg_processors* procs, int32_t batch, int64_t length,
                              int32_t* pairs) {
   return guarded([&] {
