@@ -201,6 +201,31 @@ __device__ __forceinline__ void load_tile(const StepArgs& a, int e0, int e1, int
     return;
   }
   const long boff = static_cast<long>(b) * 2 * a.length;
+  if (VEC && n0 + kDynPerThread <= a.length && (a.length & 7) == 0) {
+    // 256-bit loads (a warp reads 1 KiB contiguous per row and edge), summed in edge order
+    float l[kDynPerThread], r[kDynPerThread];
+#pragma unroll
+    for (int k = 0; k < kDynPerThread; ++k) l[k] = r[k] = 0.f;
+    for (int e = e0; e < e1; ++e) {
+      const float* p = a.src + edge_row(a, e) * a.rowstride + boff + n0;
+      float vl[kDynPerThread], vr[kDynPerThread];
+      ld8(p, vl);
+      ld8(p + a.length, vr);
+#pragma unroll
+      for (int k = 0; k < kDynPerThread; ++k) {
+        l[k] += vl[k];
+        r[k] += vr[k];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kDynPerThread / 4; ++q) {
+      sl[q * NT + t] = make_float4(l[4 * q], l[4 * q + 1], l[4 * q + 2], l[4 * q + 3]);
+      sr[q * NT + t] = make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+    }
+#pragma unroll
+    for (int k = 0; k < kDynPerThread; ++k) mid[k] = l[k] + r[k];
+    return;
+  }
   if (VEC && n0 + kDynPerThread <= a.length) {
 #pragma unroll
     for (int q = 0; q < kDynPerThread / 4; ++q) {
@@ -388,6 +413,37 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
   float* ol = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length + n0;
   float* orr = ol + a.length;
   const bool full = VEC && n0 + kDynPerThread <= a.length;
+  if (!ENV && full && (a.length & 7) == 0) {
+    // 256-bit stores (a warp writes 1 KiB contiguous per row), followers included
+    float yl[kDynPerThread], yr[kDynPerThread];
+#pragma unroll
+    for (int q = 0; q < kDynPerThread / 4; ++q) {
+      const float4 l4 = s_in[0][q][threadIdx.x], r4 = s_in[1][q][threadIdx.x];
+      const float ul[4] = {l4.x, l4.y, l4.z, l4.w}, ur[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4) {
+        g = fma(p.da, g, drive[4 * q + k4]);
+        const float gn = gain_of<GATE>(static_cast<float>(g), p);
+        yl[4 * q + k4] = gn * ul[k4];
+        yr[4 * q + k4] = gn * ur[k4];
+      }
+    }
+    st8(ol, yl);
+    st8(orr, yr);
+    for (int f = 0; f < epi.n; ++f) {
+      const float g0 = s_epi.g0[f], g1 = s_epi.g1[f];
+#pragma unroll
+      for (int k = 0; k < kDynPerThread; ++k) {
+        yl[k] = 0.f + yl[k];
+        yr[k] = 0.f + yr[k];
+        pw_op(epi.op[f], yl[k], yr[k], g0, g1);
+      }
+      float* fo = epi.dst[f] + static_cast<long>(s_epi.slot[f]) * a.rowstride + static_cast<long>(b) * 2 * a.length + n0;
+      st8(fo, yl);
+      st8(fo + a.length, yr);
+    }
+    return;
+  }
 #pragma unroll
   for (int q = 0; q < kDynPerThread / 4; ++q) {
     // this thread's own stashed input, four samples at a time (no barrier: written by itself)
@@ -588,6 +644,30 @@ __global__ void __launch_bounds__(kStreamThreads, NF == 0 ? kStreamCtasPerSm : 6
     if (!live) continue;
     float* ol = ol0 + n0;
     float* orr = ol + L;
+    if (full && (L & 7) == 0) {  // 256-bit stores: a warp writes 1 KiB contiguous per row
+      float yl[kDynPerThread], yr[kDynPerThread];
+#pragma unroll
+      for (int k = 0; k < kDynPerThread; ++k) {
+        g = fma(p.da, g, drive[k]);
+        const float gn = gain_of<GATE>(static_cast<float>(g), p);
+        yl[k] = gn * (0.f + sl[k]);
+        yr[k] = gn * (0.f + sl[TS + k]);
+      }
+      st8(ol, yl);
+      st8(orr, yr);
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+#pragma unroll
+        for (int k = 0; k < kDynPerThread; ++k) {
+          yl[k] = 0.f + yl[k];
+          yr[k] = 0.f + yr[k];
+          pw_op(epi.op[f], yl[k], yr[k], fg0[f], fg1[f]);
+        }
+        st8(fdst[f] + n0, yl);
+        st8(fdst[f] + L + n0, yr);
+      }
+      continue;
+    }
 #pragma unroll
     for (int q = 0; q < kDynPerThread / 4; ++q) {
       if (q > 0 && !full) break;
@@ -728,6 +808,7 @@ __global__ void __launch_bounds__(kStreamThreads, 6) dyn_stream_pair(StepArgs a1
     fg1[f] = s_epi.g1[f];
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool wide = (L & 7) == 0;  // 32-byte aligned rows: 256-bit stores
   double carry1 = 0.0, carry2 = 0.0;
   for (int t = 0; t < tiles; ++t) {
     const int st = t % kStreamDepth;
@@ -781,7 +862,10 @@ __global__ void __launch_bounds__(kStreamThreads, 6) dyn_stream_pair(StepArgs a1
         ur[k] *= gn;
       }
     }
-    if (live) {
+    if (live && full && wide) {  // one 256-bit store per channel: a warp writes 1 KiB contiguous
+      st8(y1 + n0, ul);
+      st8(y1 + L + n0, ur);
+    } else if (live) {
 #pragma unroll
       for (int q = 0; q < K / 4; ++q) {
         if (q > 0 && !full) break;
@@ -809,6 +893,30 @@ __global__ void __launch_bounds__(kStreamThreads, 6) dyn_stream_pair(StepArgs a1
     }
     g = stream_block_scan<NW>(drive, s_p2, carry2, wA2, wB2, t, lane, warp);
     if (!live) continue;
+    if (full && wide) {
+      const DynParams& p2 = s_p2;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        g = fma(p2.da, g, drive[k]);
+        const float gn = gain_of<GATE2>(static_cast<float>(g), p2);
+        ul[k] *= gn;
+        ur[k] *= gn;
+      }
+      st8(y2 + n0, ul);
+      st8(y2 + L + n0, ur);
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          ul[k] = 0.f + ul[k];
+          ur[k] = 0.f + ur[k];
+          pw_op(epi.op[f], ul[k], ur[k], fg0[f], fg1[f]);
+        }
+        st8(fdst[f] + n0, ul);
+        st8(fdst[f] + L + n0, ur);
+      }
+      continue;
+    }
     {
       const DynParams& p2 = s_p2;
 #pragma unroll

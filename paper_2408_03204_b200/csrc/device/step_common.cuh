@@ -148,6 +148,20 @@ __device__ __forceinline__ void pw_epi_apply(const PwEpi& e, const PwEpiSlots& c
   }
 }
 
+// 256-bit global accesses (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256): a thread's 8 consecutive
+// floats in one instruction, so a warp's access is 1 KiB contiguous. p must be 32-byte aligned.
+__device__ __forceinline__ void st8(float* p, const float (&v)[8]) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]),
+               "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void ld8(const float* p, float (&v)[8]) {
+  asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p)
+               : "memory");
+}
+
 // Bulk asynchronous copies global -> shared (cp.async.bulk, the TMA engine's 1-D form) with
 // mbarrier completion: one elected thread arms the barrier with the byte count and issues the
 // copies; consumers wait on the barrier's phase parity.
