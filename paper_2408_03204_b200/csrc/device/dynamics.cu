@@ -132,6 +132,20 @@ __device__ __forceinline__ void load16(const StepArgs& a, int e0, int e1, int b,
   for (int k = 0; k < kDynPerThread; ++k) ul[k] = ur[k] = 0.f;
   if (n0 >= a.length || n0 < 0) return;
   const long boff = static_cast<long>(b) * 2 * a.length;
+  if (VEC && n0 + kDynPerThread <= a.length && (a.length & 7) == 0) {  // 256-bit loads
+    for (int e = e0; e < e1; ++e) {
+      const float* p = a.src + edge_row(a, e) * a.rowstride + boff + n0;
+      float vl[kDynPerThread], vr[kDynPerThread];
+      ld8(p, vl);
+      ld8(p + a.length, vr);
+#pragma unroll
+      for (int k = 0; k < kDynPerThread; ++k) {
+        ul[k] += vl[k];
+        ur[k] += vr[k];
+      }
+    }
+    return;
+  }
   if (VEC && n0 + kDynPerThread <= a.length) {
     for (int e = e0; e < e1; ++e) {
       const float* p = a.src + edge_row(a, e) * a.rowstride + boff + n0;
@@ -1100,6 +1114,13 @@ __global__ void __launch_bounds__(kDynThreads, 2) dyn_bwd_dg(DynBwd d) {
 // dg at kDynPerThread samples from n0 (0 outside [0, L)); VEC: n0 is a multiple of 4.
 template <bool VEC>
 __device__ __forceinline__ void load_dg(const float* dg, long L, long n0, float* v) {
+  if (VEC && n0 >= 0 && n0 + kDynPerThread <= L && ((L | n0) & 7) == 0) {  // 256-bit load
+    float t[kDynPerThread];
+    ld8(dg + n0, t);
+#pragma unroll
+    for (int k = 0; k < kDynPerThread; ++k) v[k] = t[k];
+    return;
+  }
   if (VEC && n0 >= 0 && n0 + kDynPerThread <= L) {
 #pragma unroll
     for (int q = 0; q < kDynPerThread / 4; ++q) {
