@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
   float* ol = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length + n0;
   float* orr = ol + a.length;
   const bool full = VEC && n0 + kDynPerThread <= a.length;
-  if (!ENV && full && (a.length & 7) == 0) {
+  if (full && (a.length & 7) == 0) {
     // 256-bit stores (a warp writes 1 KiB contiguous per row), followers included
     float yl[kDynPerThread], yr[kDynPerThread];
 #pragma unroll
@@ -437,10 +437,18 @@ __global__ void __launch_bounds__(NT, 2 * kDynThreads / NT) dyn_scan(StepArgs a,
 #pragma unroll
       for (int k4 = 0; k4 < 4; ++k4) {
         g = fma(p.da, g, drive[4 * q + k4]);
-        const float gn = gain_of<GATE>(static_cast<float>(g), p);
+        const float gf = static_cast<float>(g);
+        const float gn = gain_of<GATE>(gf, p);
+        if constexpr (ENV) drive[4 * q + k4] = gf;  // drive[k] is consumed: reuse it for the envelope
         yl[4 * q + k4] = gn * ul[k4];
         yr[4 * q + k4] = gn * ur[k4];
       }
+    }
+    if constexpr (ENV) {
+      float ev[kDynPerThread];
+#pragma unroll
+      for (int k = 0; k < kDynPerThread; ++k) ev[k] = static_cast<float>(drive[k]);
+      st8(env + static_cast<long>(seq) * a.length + n0, ev);
     }
     st8(ol, yl);
     st8(orr, yr);

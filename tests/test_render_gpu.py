@@ -602,7 +602,7 @@ def test_step_owners_and_serialized_render(mg, ref):
     assert torch.equal(a.view(torch.int32), dr.arena.view(torch.int32))
 
 
-@pytest.mark.parametrize("taps,L", [(None, 70000), (4096, 20000), (4097, 20000), (4096, 12)])
+@pytest.mark.parametrize("taps,L", [(None, 70000), (4096, 20000), (4097, 20000), (4096, 12), (4096, 20004)])
 def test_streaming_scan_matches_reference(mg, ref, taps, L):
     # The compressor / noisegate scan forced onto the streaming kernel (one CTA per sequence,
     # bulk-copy ring, running carry) and onto the chained look-back scan: both match the
@@ -672,7 +672,7 @@ def test_shared_signal_spectra_bit_exact(mg, ref, prune, L, batch):
     assert rel(shared[rd.output_begin:].cpu().numpy(), want) < TOL
 
 
-@pytest.mark.parametrize("taps,L", [(None, 20000), (4096, 20000), (4097, 12000), (600, 9000)])
+@pytest.mark.parametrize("taps,L", [(None, 20000), (4096, 20000), (4097, 12000), (600, 9000), (4096, 9004)])
 def test_fused_compressor_gate_scan(mg, ref, taps, L):
     # A console track's compressor -> noisegate (-> imager -> gain) as ONE streaming kernel
     # (forced onto the streaming path; automatic for config-5-sized steps): matches the
