@@ -485,6 +485,41 @@ __device__ __forceinline__ void rows_inverse_to_global(CT* rows, int RS, int ra,
   }
 }
 
+// The channel-split product in registers at the forward transforms' last pass. Thread j runs
+// the last-pass butterflies j of rows xa / ka and jb of rows xb / kb, where jb's outputs are
+// the conjugate partners of j's (k -> N2 - 1 - k, or N2 - k for row pair 0): the product needs
+// no smem round trip of the four spectra. Z_a / Z_b are stored in place into rows ka / kb (the
+// positions this thread just read), ready for the inverse. Requires NS last-pass butterflies =
+// the threads of one row group.
+template <int LN2, typename CT>
+__device__ __forceinline__ void rows_last_zmix(CT* rows, int RS, int xra, int xrb, int kra, int krb, int ra, int j,
+                                               RealOf<CT> s, const CT* tw) {
+  constexpr int NS = Pow2Plan<LN2>::kLastNs, R = Pow2Plan<LN2>::kLastR;
+  const int jb = ra == 0 ? (NS - j) & (NS - 1) : NS - 1 - j;
+  CT xa[R], xb[R], ka[R], kb[R];
+  fft_last_to_regs<LN2, -1>(rows + xra * RS, j, tw, xa);
+  fft_last_to_regs<LN2, -1>(rows + xrb * RS, jb, tw, xb);
+  fft_last_to_regs<LN2, -1>(rows + kra * RS, j, tw, ka);
+  fft_last_to_regs<LN2, -1>(rows + krb * RS, jb, tw, kb);
+  CT* za = rows + kra * RS + sidx(j);
+  CT* zb = rows + krb * RS + sidx(jb);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    // output k = j + r NS of row a pairs with output jb + rp NS of row b
+    const int rp = (ra == 0 && j == 0) ? (R - r) & (R - 1) : R - 1 - r;
+    CT xo = xb[0], po = kb[0];
+#pragma unroll
+    for (int q = 1; q < R; ++q) {  // select without dynamic register indexing
+      if (q == rp) {
+        xo = xb[q];
+        po = kb[q];
+      }
+    }
+    za[r * padded(NS)] = zmix(xa[r], cconj(xo), ka[r], cconj(po), s);
+    zb[rp * padded(NS)] = zmix(xo, cconj(xa[r]), po, cconj(ka[r]), s);
+  }
+}
+
 // Forward row FFTs of the packed kernel, kSpecRows consecutive rows per CTA.
 // grid (N1 / kSpecRows, slots)
 template <int LN2, typename CT>
@@ -665,7 +700,24 @@ __global__ void __launch_bounds__(row_threads<LN2, 4>()) rows_conv_fk(int log_n,
   const CT* ka = K + static_cast<long>(slot) * N + static_cast<long>(ra) * N2;
   const CT* kb_ = K + static_cast<long>(slot) * N + static_cast<long>(rb) * N2;
   constexpr bool REG = rows_reg<LN2, 4>();
-  if constexpr (REG) {
+  if constexpr (REG && NT == Pow2Plan<LN2>::kLastNs) {
+    // first pass from global, middle passes in smem, the last pass + product in registers
+    constexpr int M1 = N2 / 16;
+    {
+      const int w = threadIdx.x / M1, j = threadIdx.x - (threadIdx.x / M1) * M1;
+      const CT* p = w == 0 ? xa_in : (w == 1 ? xb_in : (w == 2 ? ka : kb_));
+      CT v[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[r] = p[j + r * M1];
+      fft_first_from_regs<-1>(v, rows + w * RS, j);
+    }
+    __syncthreads();
+    fft_middle<LN2, 4, NT, -1>(rows, RS, tw);
+    rows_last_zmix<LN2>(rows, RS, 0, 1, 2, 3, ra, threadIdx.x, T(0.25) / static_cast<T>(N), tw);
+    __syncthreads();
+    rows_inverse_to_global<LN2, NT>(rows + 2 * RS, RS, ra, rb, self, xa, xb, T(2) / static_cast<T>(N), tw);
+    return;
+  } else if constexpr (REG) {
     rows_forward_from_global<LN2, 4, NT>(rows, RS, xa_in, xb_in, ka, kb_, tw);
   } else {
     constexpr int PER = (N2 + NT - 1) / NT;
