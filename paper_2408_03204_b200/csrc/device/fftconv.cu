@@ -491,18 +491,29 @@ __device__ __forceinline__ void rows_inverse_to_global(CT* rows, int RS, int ra,
 // no smem round trip of the four spectra. Z_a / Z_b are stored in place into rows ka / kb (the
 // positions this thread just read), ready for the inverse. Requires NS last-pass butterflies =
 // the threads of one row group.
+// pa / pb non-null: the kernel spectrum rows come from global memory (rows_conv: P already
+// row-transformed) and Z goes in place into the X rows instead.
 template <int LN2, typename CT>
 __device__ __forceinline__ void rows_last_zmix(CT* rows, int RS, int xra, int xrb, int kra, int krb, int ra, int j,
-                                               RealOf<CT> s, const CT* tw) {
+                                               RealOf<CT> s, const CT* tw, const CT* pa = nullptr,
+                                               const CT* pb = nullptr) {
   constexpr int NS = Pow2Plan<LN2>::kLastNs, R = Pow2Plan<LN2>::kLastR;
   const int jb = ra == 0 ? (NS - j) & (NS - 1) : NS - 1 - j;
   CT xa[R], xb[R], ka[R], kb[R];
   fft_last_to_regs<LN2, -1>(rows + xra * RS, j, tw, xa);
   fft_last_to_regs<LN2, -1>(rows + xrb * RS, jb, tw, xb);
-  fft_last_to_regs<LN2, -1>(rows + kra * RS, j, tw, ka);
-  fft_last_to_regs<LN2, -1>(rows + krb * RS, jb, tw, kb);
-  CT* za = rows + kra * RS + sidx(j);
-  CT* zb = rows + krb * RS + sidx(jb);
+  if (pa != nullptr) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      ka[r] = __ldg(pa + j + r * NS);
+      kb[r] = __ldg(pb + jb + r * NS);
+    }
+  } else {
+    fft_last_to_regs<LN2, -1>(rows + kra * RS, j, tw, ka);
+    fft_last_to_regs<LN2, -1>(rows + krb * RS, jb, tw, kb);
+  }
+  CT* za = rows + (pa != nullptr ? xra : kra) * RS + sidx(j);
+  CT* zb = rows + (pa != nullptr ? xrb : krb) * RS + sidx(jb);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     // output k = j + r NS of row a pairs with output jb + rp NS of row b
@@ -607,6 +618,17 @@ __global__ void __launch_bounds__(row_threads<LN2, 2>(), kRconvThreadsPerSm / (s
     for (int r = 0; r < 16; ++r) v[r] = src[j + r * M1];
     fft_first_from_regs<-1>(v, rows + w * RS, j);
     __syncthreads();
+    if constexpr (2 * NT == Pow2Plan<LN2>::kLastNs) {
+      // middle passes in smem; the last pass and the product in registers (rows_conv_fk's
+      // scheme, two butterfly pairs per thread), Z in place in the X rows, then the inverse
+      fft_middle<LN2, 2, NT, -1>(rows, RS, tw);
+      const T sc = T(0.25) / static_cast<T>(N);
+      rows_last_zmix<LN2>(rows, RS, 0, 1, -1, -1, ra, threadIdx.x, sc, tw, pa, pb);
+      rows_last_zmix<LN2>(rows, RS, 0, 1, -1, -1, ra, threadIdx.x + NT, sc, tw, pa, pb);
+      __syncthreads();
+      rows_inverse_to_global<LN2, NT>(rows, RS, ra, rb, self, xa, xb, T(2) / static_cast<T>(N), tw);
+      return;
+    }
     fft_after_first<LN2, 2, NT, -1>(rows, RS, tw);
   } else {
     constexpr int PER = N2 / NT;
