@@ -706,3 +706,39 @@ def test_fused_compressor_gate_scan(mg, ref, taps, L):
     want = ref.Plan(t, e, 1).render(params, src, **cfg)
     for mode, a in arenas.items():
         assert rel(a[rd.output_begin:].cpu().numpy(), want) < TOL, mode
+
+
+def test_serialized_render_equals_fused_render_all_paths(mg, ref):
+    # bench.py's per-kernel roofline trace renders with hoist=False (everything on one stream):
+    # with the shared delay/reverb spectra, the fused compressor -> noisegate scan and the
+    # epilogue followers all active (forced here), its arena must equal the overlapped render's.
+    import torch
+    from paper_2408_03204_b200.device import DeviceRenderer
+    t, e = ref.console(7, 0.2, 31)
+    params = ref.random_legal_params(t, e, 32)
+    rd = mg.compute_render_data(make(mg, t, e))
+    L = 24000
+    procs = mg.ProcessorSet()
+    src = np.random.default_rng(33).uniform(-1, 1, size=(rd.num_inputs, 1, 2, L))
+    mg.set_conv_fuse(1)
+    mg.set_dyn_stream(1)
+    try:
+        assert rd.shared_pairs(procs, 1, L).sum() > 0
+        own = rd.step_owners(1, L)
+        types = [int(st.type) for st in rd.steps]
+        assert own[types.index(6)] == types.index(5)  # the noisegate runs in the compressor's launch
+        dr = DeviceRenderer(rd, procs, 1, L, rd.reorder_params(params))
+        dr.sources.copy_(torch.as_tensor(src, dtype=torch.float32))
+        g = dr.capture()
+        g.replay()
+        torch.cuda.synchronize()
+        a = dr.arena.clone()
+        dr.arena[rd.num_inputs:].fill_(float("nan"))
+        dr.render_profiled(hoist=False)
+        torch.cuda.synchronize()
+        assert torch.equal(a.view(torch.int32), dr.arena.view(torch.int32))
+    finally:
+        mg.set_conv_fuse(-1)
+        mg.set_dyn_stream(-1)
+    want = ref.Plan(t, e, 1).render(params, src)
+    assert rel(a[rd.output_begin:].cpu().numpy(), want) < TOL
