@@ -346,6 +346,19 @@ __global__ void __launch_bounds__(EqWin<LOG, C>::kThreads, EqWin<LOG, C>::kMinBl
   const long s0 = out0 - (kEqHalf + 1);
   const long boff = static_cast<long>(b) * 2 * a.length;
   const float* rs = resp + static_cast<long>(slot) * 8192;
+  // fp32 8192-point windows: the slot's response (32 KiB, L2-resident) is requested into shared
+  // memory with cp.async now and read after the forward transform, instead of 16 L2 round
+  // trips per thread in the middle of the kernel
+  constexpr bool kStageResp = LOG == 13 && sizeof(C) == 8;
+  float* rsm = reinterpret_cast<float*>(eq_smem + W::kSmem);
+  if constexpr (kStageResp) {
+#pragma unroll
+    for (int i = 0; i < 8192 / 4 / kNt; ++i) {
+      const int off = (i * kNt + threadIdx.x) * 4;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(rsm + off)), "l"(rs + off) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   {
   // Gather-sum of the window straight into the radix-16 first-pass butterfly this thread
   // owns (elements t + r*N/16: consecutive threads read consecutive samples), edges
@@ -391,9 +404,18 @@ __global__ void __launch_bounds__(EqWin<LOG, C>::kThreads, EqWin<LOG, C>::kMinBl
     twb.apply(v);
     Dft<16, -1, C>::run(v);
   }
+  if constexpr (kStageResp) {
+    asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's own copies (the bins it
+                                                      // reads are other threads': barrier below)
+  }
+  __syncthreads();  // every thread has read its last-pass inputs (and the response is staged)
+  if constexpr (kStageResp) {
 #pragma unroll
-  for (int r = 0; r < 16; ++r) v[r] = cscale(v[r], rscale * static_cast<T>(__ldg(rs + kRs * (j + r * NL))));
-  __syncthreads();  // every thread has read its last-pass inputs
+    for (int r = 0; r < 16; ++r) v[r] = cscale(v[r], rscale * rsm[j + r * NL]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = cscale(v[r], rscale * static_cast<T>(__ldg(rs + kRs * (j + r * NL))));
+  }
   fft_first_from_regs<+1>(v, buf, j);
   }
   __syncthreads();
@@ -428,7 +450,7 @@ void eq_setup() {
     cudaFuncSetAttribute(eq_basis_product<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBasisSmem);
     cudaFuncSetAttribute(eq_basis_product<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBasisSmem);
     for (auto fn : {eq_conv<13, float2>, eq_conv<12, float2>}) {
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqSmem);
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kEqSmem + 8192 * 4);
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     }
     for (auto fn : {eq_conv<13, double2>, eq_conv<12, double2>}) {
@@ -544,7 +566,7 @@ void launch_eq_main(const StepArgs& a, const float* resp_ws, cudaStream_t s) {
     eq_conv<12, float2><<<eq_grid<12>(a), EqWin<12>::kThreads, EqWin<12>::kSmem, s>>>(a, resp_ws);
     return;
   }
-  eq_conv<13, float2><<<eq_grid<13>(a), 512, kEqSmem, s>>>(a, resp_ws);
+  eq_conv<13, float2><<<eq_grid<13>(a), 512, kEqSmem + 8192 * 4, s>>>(a, resp_ws);
 }
 
 }  // namespace mgb
