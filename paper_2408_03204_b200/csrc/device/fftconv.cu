@@ -176,8 +176,9 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_fwd(StepArgs a, 
         const int n = n0 + q * nstep;
         CT v = Cx<CT>::mk(0.f, 0.f);
         if (n >= nlo && n < nhi) {
-          if constexpr (SRC == ColSrc::Signal) v = Cx<CT>::mk(__ldg(one + n), __ldg(one + a.length + n));
-          else v = widen<CT>(__ldg(irp + n));
+          const unsigned un = static_cast<unsigned>(n);
+          if constexpr (SRC == ColSrc::Signal) v = Cx<CT>::mk(__ldg(one + un), __ldg(one + a.length + un));
+          else v = widen<CT>(__ldg(irp + un));
         }
         vals[q] = v;
       }
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_fwd(StepArgs a, 
     for (int r = 0; r < R; ++r) {
       const int k1 = j + r * NS;
       w = (r % 4 == 0) ? expi_pi(-static_cast<T>(n2 * k1) * inv_n) : cmul(w, step);
-      o[k1 * N2] = cmul(v[r], w);
+      o[static_cast<unsigned>(k1 * N2)] = cmul(v[r], w);
     }
   }
 }
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(kDelayColThreads) delay_cols(const float* taps
           const int d = __float_as_int(r[0]);
           if (d >= 0) {
             const int i0 = d - kFirHalf;
-            const int i = i0 + (((n2 - i0) % N2) + N2) % N2;  // first sample of column n2 at or after i0
+            const int i = i0 + ((n2 - i0) & (N2 - 1));  // first sample of column n2 at or after i0
             if (i <= d + kFirHalf && i >= 0 && i < nhi) {
               hit = true;
               n1 = i >> log_n2;
@@ -299,12 +300,14 @@ __global__ void __launch_bounds__(kDelayColThreads) delay_cols(const float* taps
     for (int h = 0; h < nh; ++h) {
       const int n1 = hn1[c][h];
       const float2 v = hv[c][h];
+      // u = v w_N1^(n1 k1) chained on the product itself (v is real or imaginary: the anchor
+      // product is exact up to one rounding), exact table anchors every 4 outputs.
       const float2 ws = __ldg(tw + ((n1 * G) & (N1 - 1)) * TS);
-      float2 w = make_float2(1.f, 0.f);
+      float2 u = v;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        w = (r % 4 == 0) ? __ldg(tw + ((n1 * (g + G * r)) & (N1 - 1)) * TS) : cmul(w, ws);
-        acc[r] = cadd(acc[r], cmul(v, w));
+        u = (r % 4 == 0) ? cmul(v, __ldg(tw + ((n1 * (g + G * r)) & (N1 - 1)) * TS)) : cmul(u, ws);
+        acc[r] = cadd(acc[r], u);
       }
     }
     float2* o = out + static_cast<long>(slot) * N + n2;
@@ -340,7 +343,7 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_inv(StepArgs a, 
     constexpr int EPT = ColCfg<CT>::kElems / NT;
     CT vals[EPT];
 #pragma unroll
-    for (int q = 0; q < EPT; ++q) vals[q] = __ldg(xc + (jt + q * (N1 / 16)) * N2);
+    for (int q = 0; q < EPT; ++q) vals[q] = __ldg(xc + static_cast<unsigned>((jt + q * (N1 / 16)) * N2));
     // First pass from registers (vals[q] = element jt + q*N1/16 of column c), last pass into
     // registers and straight to the arena (outputs n1 = j + r*NS of column c).
     fft_first_from_regs<+1>(vals, tile + c * FS, jt);
@@ -363,14 +366,17 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_inv(StepArgs a, 
       CT v[R];
       fft_last_to_regs<LN1, +1>(tile + c * FS, j, twiddles<CT>(a), v);
 #pragma unroll
-      for (int r = 0; r < R; ++r) xc[(j + r * NS) * N2] = v[r];
+      for (int r = 0; r < R; ++r) xc[static_cast<unsigned>((j + r * NS) * N2)] = v[r];
     }
     return;
   }
+  // Offsets k >= 0 as unsigned: one IMAD.WIDE.U32 per store address, one compare per bound.
   const int nlo = static_cast<int>(min(max(first - base, 0L), static_cast<long>(N))) - n2;
   const int nhi = static_cast<int>(min(max(end - base, 0L), static_cast<long>(N))) - n2;
-  float* yl = a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length + base + n2;
-  float* yr = yl + a.length;
+  const unsigned span = static_cast<unsigned>(max(nhi - nlo, 0));
+  // Opaque row pointers: otherwise the compiler re-derives each store's address from a.dst.
+  float* yl = opaque_ptr(a.dst + static_cast<long>(slot) * a.rowstride + static_cast<long>(b) * 2 * a.length + base + n2);
+  float* yr = opaque_ptr(yl + a.length);
 #pragma unroll
   for (int p = 0; p < NS / JSTEP; ++p) {
     const int j = jt + p * JSTEP;
@@ -379,9 +385,9 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_inv(StepArgs a, 
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int k = (j + r * NS) * N2;
-      if (k >= nlo && k < nhi) {
-        yl[k] = static_cast<float>(v[r].x);
-        yr[k] = static_cast<float>(v[r].y);
+      if (static_cast<unsigned>(k - nlo) < span) {
+        st_global(yl + static_cast<unsigned>(k), static_cast<float>(v[r].x));
+        st_global(yr + static_cast<unsigned>(k), static_cast<float>(v[r].y));
       }
     }
   }

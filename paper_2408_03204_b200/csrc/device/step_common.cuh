@@ -30,6 +30,18 @@ struct StepArgs {
   int dense = -1;        // >= 0: slot s reads exactly row dense + s (no CSR loads needed)
 };
 
+// A pointer the compiler cannot re-associate with the index math of its uses (so a loop of
+// stores at p[k] costs one IMAD.WIDE per address instead of re-deriving p from the kernel
+// parameters each time).
+template <typename T>
+__device__ __forceinline__ T* opaque_ptr(T* p) {
+  asm volatile("" : "+l"(p));
+  return p;
+}
+
+// Plain global store through a pointer the compiler no longer knows the space of.
+__device__ __forceinline__ void st_global(float* p, float v) { asm("st.global.f32 [%0], %1;" ::"l"(p), "f"(v)); }
+
 // CSR access. Dense steps (a track chain's steps read the previous step's rows in order)
 // skip the row_ptr -> col -> sample chain of dependent L2 round trips: only sample loads.
 __device__ __forceinline__ int slot_e0(const StepArgs& a, int slot) { return a.dense >= 0 ? slot : __ldg(a.row_ptr + slot); }
