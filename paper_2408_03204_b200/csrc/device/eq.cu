@@ -369,14 +369,19 @@ __global__ void __launch_bounds__(EqWin<LOG, C>::kThreads, EqWin<LOG, C>::kMinBl
   C v[16];
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[r] = Cx<C>::mk(T(0), T(0));
+  // 32-bit sample positions (L < 2^31), one unsigned compare for both bounds, addresses from
+  // opaque row pointers (the 64-bit re-derivation per element was a fifth of the instructions)
+  const int pos0 = static_cast<int>(s0) + static_cast<int>(threadIdx.x);
+  const unsigned len = static_cast<unsigned>(a.length);
   for (int e = e0; e < e1; ++e) {
-    const float* p = a.src + edge_row(a, e) * a.rowstride + boff;
+    const float* pl = opaque_ptr(a.src + edge_row(a, e) * a.rowstride + boff);
+    const float* pr = opaque_ptr(pl + a.length);
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      const long pos = s0 + threadIdx.x + r * M1;
-      if (pos >= 0 && pos < a.length) {
-        v[r].x += static_cast<T>(__ldg(p + pos));
-        v[r].y += static_cast<T>(__ldg(p + a.length + pos));
+      const unsigned pos = static_cast<unsigned>(pos0 + r * M1);
+      if (pos < len) {
+        v[r].x += static_cast<T>(__ldg(pl + pos));
+        v[r].y += static_cast<T>(__ldg(pr + pos));
       }
     }
   }
@@ -423,8 +428,9 @@ __global__ void __launch_bounds__(EqWin<LOG, C>::kThreads, EqWin<LOG, C>::kMinBl
   // (window index w = j + r*NS holds output out0 + w - 1024 for w in [1024, 1024 + kEqOut)).
   fft_middle<LOG, 1, kNt, +1>(buf, padded(kEqFft), tw);
   constexpr int NS = Pow2Plan<LOG>::kLastNs, R = Pow2Plan<LOG>::kLastR, PL = NS / kNt;
-  float* yl = a.dst + static_cast<long>(slot) * a.rowstride + boff;
-  float* yr = yl + a.length;
+  float* yl = opaque_ptr(a.dst + static_cast<long>(slot) * a.rowstride + boff + out0);
+  float* yr = opaque_ptr(yl + a.length);
+  const int pend = static_cast<int>(min(a.length - out0, static_cast<long>(kEqOut)));  // outputs of this block
 #pragma unroll
   for (int p = 0; p < PL; ++p) {
     const int j = threadIdx.x + p * kNt;
@@ -432,11 +438,10 @@ __global__ void __launch_bounds__(EqWin<LOG, C>::kThreads, EqWin<LOG, C>::kMinBl
     fft_last_to_regs<LOG, +1>(buf, j, tw, y);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const int w = j + r * NS;
-      const long pos = out0 + w - (kEqHalf + 1);
-      if (w >= kEqHalf + 1 && w < kEqHalf + 1 + kEqOut && pos < a.length) {
-        yl[pos] = static_cast<float>(y[r].x);
-        yr[pos] = static_cast<float>(y[r].y);
+      const int w = j + r * NS - (kEqHalf + 1);  // output out0 + w, stored for 0 <= w < pend
+      if (static_cast<unsigned>(w) < static_cast<unsigned>(pend)) {
+        st_global(yl + static_cast<unsigned>(w), static_cast<float>(y[r].x));
+        st_global(yr + static_cast<unsigned>(w), static_cast<float>(y[r].y));
       }
     }
   }
