@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_fwd(StepArgs a, 
   // Valid n of this item: [nlo, nhi).
   const int nlo = static_cast<int>(min(max(lo - base, 0L), static_cast<long>(N)));
   const int nhi = static_cast<int>(min(max(hi - base, 0L), static_cast<long>(N)));
+  const unsigned span = static_cast<unsigned>(max(nhi - nlo, 0));  // n valid: unsigned(n - nlo) < span
   constexpr int EPT = ColCfg<CT>::kElems / NT;
   static_assert(EPT == 16, "cols_fwd: one radix-16 first-pass butterfly per thread");
   CT vals[EPT];
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_fwd(StepArgs a, 
     // All of this thread's loads are in flight before any smem store.
     const float* one = nullptr;  // in-degree-1 fast path
     if constexpr (SRC == ColSrc::Signal) {
-      if (e1 - e0 == 1) one = a.src + edge_row(a, e0) * a.rowstride + static_cast<long>(b) * 2 * a.length + base;
+      if (e1 - e0 == 1) one = opaque_ptr(a.src + edge_row(a, e0) * a.rowstride + static_cast<long>(b) * 2 * a.length + base);
     }
     const float2* irp = ir + static_cast<long>(item) * taps;
     if (SRC != ColSrc::Signal || one) {
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_fwd(StepArgs a, 
       for (int q = 0; q < EPT; ++q) {
         const int n = n0 + q * nstep;
         CT v = Cx<CT>::mk(0.f, 0.f);
-        if (n >= nlo && n < nhi) {
+        if (static_cast<unsigned>(n - nlo) < span) {
           const unsigned un = static_cast<unsigned>(n);
           if constexpr (SRC == ColSrc::Signal) v = Cx<CT>::mk(__ldg(one + un), __ldg(one + a.length + un));
           else v = widen<CT>(__ldg(irp + un));
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(ColCfg<CT>::kThreads, 2) cols_fwd(StepArgs a, 
 #pragma unroll
       for (int q = 0; q < EPT; ++q) {
         const int n = n0 + q * nstep;
-        vals[q] = (n >= nlo && n < nhi) ? widen<CT>(gather2(a, e0, e1, b, base + n)) : Cx<CT>::mk(0.f, 0.f);
+        vals[q] = (static_cast<unsigned>(n - nlo) < span) ? widen<CT>(gather2(a, e0, e1, b, base + n)) : Cx<CT>::mk(0.f, 0.f);
       }
     }
   }
